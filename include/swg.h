@@ -1,0 +1,222 @@
+/*
+ * swg.h — C-ABI of the B200-native SWIH hot path (libswg.so).
+ *
+ * Plain C: opaque handles, POD structs, pointers + sizes, int status codes.
+ * No exceptions, no torch types.  Every entry point below replaces one body
+ * of the reference C++ library (paths relative to /root/reference/proj):
+ *
+ *   swg_tables_build        IntegralTableSet::build      src/integral_tables.cpp:72-115
+ *                           (+ quantize_image            src/image.cpp:34-40, fused)
+ *   swg_tables_export_i64   IntegralTableSet::cell/plane include/swih/integral_tables.hpp:69-101
+ *                           and ::save                   src/integral_tables.cpp:167-183
+ *   swg_tables_upload_i64   IntegralTableSet::load       src/integral_tables.cpp:185-206
+ *   swg_query_terms         accumulate_term / swih_query_into / quadrant_histogram /
+ *                           plain_local_histogram_into   src/engine.cpp:39-165
+ *   swg_likelihood_map      likelihood_map               src/matching.cpp:108-209
+ *                           (score_counts/score_weights  src/matching.cpp:20-52,
+ *                            WeddingCakePlan::histogram_into src/baselines.cpp:133-149,
+ *                            BruteForcePlan             src/baselines.cpp:24-69)
+ *                           and peak                     src/matching.cpp:211-223
+ *
+ * Error behaviour: one status code per reference exception class
+ * (include/swih/errors.hpp:10-79); the message is kept per thread
+ * (swg_last_error) together with CapacityError::required_bytes
+ * (swg_last_required_bytes).  The C++ drop-in layer (include/swih/*.hpp)
+ * rethrows the matching class.
+ *
+ * Threading: a context owns one CUDA stream on one device; calls on one
+ * context are serialised by the caller (the C++ layer holds a mutex).
+ * Tables are immutable after build and may be queried from any thread.
+ */
+#ifndef SWG_H
+#define SWG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWG_ABI_VERSION 1
+#define SWG_MAX_BINS 1024  /* model / bin count limit of one map request   */
+#define SWG_MAX_RINGS 512  /* wedding-cake ring limit of one map request   */
+
+typedef enum swg_status {
+  SWG_OK = 0,
+  SWG_ERR = 1,                   /* swih::Error                  */
+  SWG_ERR_IO = 2,                /* swih::IoError                */
+  SWG_ERR_ZERO_MASS = 3,         /* swih::ZeroMassError          */
+  SWG_ERR_INVALID_KERNEL = 4,    /* swih::InvalidKernelError     */
+  SWG_ERR_OUT_OF_RANGE = 5,      /* swih::OutOfRangeError        */
+  SWG_ERR_UNSUPPORTED_KERNEL = 6,/* swih::UnsupportedKernelError */
+  SWG_ERR_WINDOW_OOB = 7,        /* swih::WindowOutOfBoundsError */
+  SWG_ERR_CAPACITY = 8,          /* swih::CapacityError          */
+  SWG_ERR_CONFIG = 9,            /* swih::ConfigError            */
+  SWG_ERR_MODEL = 10,            /* swih::ModelError             */
+  SWG_ERR_SIZE = 11,             /* swih::SizeError              */
+  SWG_ERR_CUDA = 64,             /* device / runtime failure     */
+  SWG_ERR_NO_DEVICE = 65,        /* no usable sm_100 device      */
+  SWG_ERR_ARG = 66               /* NULL handle / bad enum value */
+} swg_status;
+
+/* Input pixel formats.  GRAY8 + bins is the reference Quantizer
+ * (image.hpp:43-45).  BINS16 is a pre-quantised FeatureImage
+ * (image.hpp:52-76).  GRAY16 / RGB8 are declared extensions. */
+typedef enum swg_format {
+  SWG_FMT_GRAY8 = 0,  /* uint8,  bin = v*bins/256                       */
+  SWG_FMT_GRAY16 = 1, /* uint16, bin = v*bins/65536                     */
+  SWG_FMT_RGB8 = 2,   /* 3 x uint8, bins = levels^3                     */
+  SWG_FMT_BINS16 = 3  /* uint16 bin index per pixel, < bins             */
+} swg_format;
+
+/* Weight-plane sets.  PLAIN = {1}; AFFINE = {1, x, y}, the reference's
+ * plain / xramp / yramp tables (integral_tables.hpp:53-58). */
+typedef enum swg_planes { SWG_PLANES_PLAIN = 1, SWG_PLANES_AFFINE = 3 } swg_planes;
+
+typedef enum swg_table_kind { SWG_TABLE_PLAIN = 0, SWG_TABLE_XRAMP = 1, SWG_TABLE_YRAMP = 2 } swg_table_kind;
+typedef enum swg_kernel_kind {      /* kernel.hpp:9-14 */
+  SWG_KERNEL_UNIFORM = 0,
+  SWG_KERNEL_MANHATTAN = 1,
+  SWG_KERNEL_CHEBYSHEV = 2,
+  SWG_KERNEL_GAUSS_CHEBYSHEV = 3
+} swg_kernel_kind;
+typedef enum swg_method { SWG_METHOD_SWIH = 0, SWG_METHOD_BRUTE = 1, SWG_METHOD_CAKE = 2, SWG_METHOD_PLAIN = 3 } swg_method;
+typedef enum swg_similarity { SWG_SIM_BHATTACHARYYA = 0, SWG_SIM_INTERSECTION = 1 } swg_similarity;
+typedef enum swg_border { SWG_BORDER_STRICT = 0, SWG_BORDER_CLIPPED = 1 } swg_border;
+typedef enum swg_ring_rule { SWG_RING_MEAN = 0, SWG_RING_LEVEL = 1 } swg_ring_rule;
+
+typedef struct swg_ctx swg_ctx;
+typedef struct swg_tables swg_tables;
+
+typedef struct swg_kernel {   /* KernelSpec, kernel.hpp:18-36 */
+  int kind;
+  int kw;
+  int kh;
+  double sigma;
+} swg_kernel;
+
+typedef struct swg_peak {     /* Peak, matching.hpp:41-47 */
+  int map_x;
+  int map_y;
+  int center_x;
+  int center_y;
+  double score;
+} swg_peak;
+
+/* One likelihood-map request (likelihood_map arguments + MatchOptions,
+ * matching.hpp:49-54,72-75).  Map rows [row_begin, row_end) only; 0,0 means
+ * the whole strict map.  `model` holds `bins` normalised doubles. */
+typedef struct swg_map_request {
+  swg_kernel kernel;
+  int method;      /* swg_method                         */
+  int sim;         /* swg_similarity                     */
+  int rings;       /* WeddingCakeConfig::rings (CAKE)     */
+  int ring_rule;   /* WeddingCakeConfig::rule  (CAKE)     */
+  int row_begin;
+  int row_end;
+  const double* model;
+} swg_map_request;
+
+/* One quadrant term of a window query (QuadrantTerm, engine.hpp:27-32). */
+typedef struct swg_term {
+  int valid;       /* 0 = empty quadrant (std::nullopt) */
+  int x0, y0, x1, y1;
+  int64_t sx, sy, beta;
+} swg_term;
+
+/* ---- library / errors ---------------------------------------------- */
+int swg_abi_version(void);
+const char* swg_last_error(void);
+size_t swg_last_required_bytes(void);
+swg_status swg_device_count(int* n);
+
+/* ---- context --------------------------------------------------------- */
+swg_status swg_ctx_create(int device, swg_ctx** out);
+swg_status swg_ctx_destroy(swg_ctx* ctx);
+swg_status swg_ctx_synchronize(swg_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
+ * the context's own stream. */
+swg_status swg_ctx_set_stream(swg_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context launched so far (bench evidence). */
+swg_status swg_ctx_launch_count(swg_ctx* ctx, uint64_t* n);
+
+/* ---- integral tables ------------------------------------------------- */
+/* Quantise + build one plane set.  `pixels` is host memory
+ * (is_device = 0) or device memory (1), rows `pitch_bytes` apart (0 = tight).
+ * `bins` is the bin count (GRAY8 / GRAY16 / BINS16) or the levels per
+ * channel (RGB8, bins = levels^3).  memory_budget = 0: no limit.
+ * CapacityError semantics: SWG_ERR_CAPACITY + swg_last_required_bytes(). */
+swg_status swg_tables_build(swg_ctx* ctx, const void* pixels, int is_device,
+                            size_t pitch_bytes, int width, int height,
+                            int format, int bins, int planes,
+                            size_t memory_budget, swg_tables** out);
+/* Re-run quantise + build for a new frame of the same geometry into the
+ * same device buffers (no allocation; stream ordered, asynchronous). */
+swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
+                              size_t pitch_bytes);
+/* Create tables from exact int64 host planes (SWIH1 load path); each array
+ * holds bins*(w+1)*(h+1) entries, bin-major, row stride w+1. */
+swg_status swg_tables_upload_i64(swg_ctx* ctx, int width, int height, int bins,
+                                 const int64_t* plain, const int64_t* xramp,
+                                 const int64_t* yramp, swg_tables** out);
+swg_status swg_tables_destroy(swg_tables* t);
+swg_status swg_tables_info(const swg_tables* t, int* width, int* height,
+                           int* bins, int* planes, size_t* device_bytes);
+/* Exact int64 planes for bins [bin_begin, bin_end), reference layout. */
+swg_status swg_tables_export_i64(swg_tables* t, int kind, int bin_begin,
+                                 int bin_end, int64_t* host_out);
+/* The stored 32-bit words (exact value mod 2^32), reference layout. */
+swg_status swg_tables_export_u32(swg_tables* t, int kind, int bin_begin,
+                                 int bin_end, uint32_t* host_out);
+/* The quantised feature image (uint16 bins, w*h). */
+swg_status swg_tables_feature_image(swg_tables* t, uint16_t* host_out);
+/* Device pointer + geometry of the 32-bit planes (for tests / bench):
+ * element (x, y) of plane (bin*planes + kind) sits at
+ * base[(bin*planes + kind)*plane_stride + y*pitch + x + xoff]. */
+swg_status swg_tables_device_layout(const swg_tables* t, const void** base,
+                                    size_t* plane_stride, size_t* pitch,
+                                    int* xoff);
+
+/* ---- window queries (engine API) ----------------------------------- */
+/* n windows, each `terms_per_window` consecutive terms (already clipped by
+ * the caller per the border policy).  out[n][bins] = sum over the window's
+ * terms of sx*X + sy*Y + beta*P per bin, exact int64. */
+swg_status swg_query_terms(swg_tables* t, int n, int terms_per_window,
+                           const swg_term* terms, int64_t* host_out);
+
+/* Window queries at centres (cx[i], cy[i]) with the reference semantics of
+ * swih_query_into (method SWIH, engine.cpp:140-147) or
+ * plain_local_histogram_into (method PLAIN, engine.cpp:156-165), border
+ * policy per engine.cpp:7-35.  out[n][bins] exact int64. */
+swg_status swg_query_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                             const swg_kernel* kernel, int method, int border,
+                             int64_t* host_out);
+/* Wedding-cake histograms (WeddingCakePlan, baselines.cpp:84-149) at n
+ * centres; out[n][bins] doubles, bit-identical to the reference. */
+swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                            const swg_kernel* kernel, int rings, int ring_rule,
+                            int border, double* host_out);
+/* Ring plan of a wedding-cake configuration: per ring the box half extents
+ * and the ring weight (WeddingCakePlan::shrink_x/shrink_y/ring_weight). */
+swg_status swg_cake_plan(const swg_kernel* kernel, int rings, int ring_rule,
+                         int* shrink_x, int* shrink_y, double* ring_weight);
+
+/* ---- likelihood maps ------------------------------------------------- */
+/* Full strict likelihood map(s) + peak(s).  For request i:
+ *   scores_host[i]   host array of rows x map_width doubles, or NULL
+ *   scores_dev[i]    device array (same size), or NULL
+ *   peaks_host[i]    filled when peaks_host != NULL
+ *   peaks_dev        device array of n swg_peak, or NULL
+ * With only device outputs the call is asynchronous on the context stream.
+ * Any of the per-request pointer arrays may itself be NULL. */
+swg_status swg_likelihood_maps(swg_tables* t, int n,
+                               const swg_map_request* reqs,
+                               double* const* scores_host,
+                               double* const* scores_dev,
+                               swg_peak* peaks_host, swg_peak* peaks_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWG_H */

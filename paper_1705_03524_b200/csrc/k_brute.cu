@@ -1,0 +1,123 @@
+// k_brute.cu — direct per-pixel weighted histogram sweep (MapMethod::Brute).
+//
+// Replaces BruteForcePlan::counts_into / weights_into
+// (proj/src/baselines.cpp:24-69) + score_counts / score_weights
+// (proj/src/matching.cpp:20-52) for kernels without an O(1) decomposition
+// (ChebyshevLinear, GaussianChebyshev).  One thread owns one window; bins are
+// processed in chunks of kChunk with per-thread shared-memory accumulators,
+// and within a chunk the window pixels are visited in the reference's
+// row-major order, so every per-bin fp64 sum has the reference's rounding
+// sequence.  Integer kernels accumulate exact integers in fp64 (< 2^53).
+#include "swg_internal.cuh"
+
+namespace swg {
+
+namespace {
+
+constexpr int kChunk = 32;
+
+__device__ __forceinline__ double clamp01b(double v) {
+  return (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+}
+
+__device__ __forceinline__ bool better_b(double s, long long i, double s2, long long i2) {
+  return s > s2 || (s == s2 && i < i2);
+}
+
+__device__ void block_peak_b(double s, long long idx, PeakPart* out) {
+  __shared__ double ss[32];
+  __shared__ long long si[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int off = 16; off > 0; off >>= 1) {
+    const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
+    const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
+    if (better_b(s2, i2, s, idx)) { s = s2; idx = i2; }
+  }
+  if (lane == 0) { ss[warp] = s; si[warp] = idx; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? ss[lane] : -2.0;
+    idx = lane < nw ? si[lane] : 0x7FFFFFFFFFFFFFFFLL;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
+      const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
+      if (better_b(s2, i2, s, idx)) { s = s2; idx = i2; }
+    }
+    if (lane == 0) *out = PeakPart{s, idx};
+  }
+}
+
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a,
+                                                               const BruteArgs g) {
+  __shared__ double acc[kChunk * kSweepThreads];
+  const int tid = threadIdx.x;
+  const int u0 = blockIdx.x * blockDim.x + tid;
+  const int v = a.row0 + blockIdx.y;
+  const bool active = u0 < a.mw;
+  const int u = active ? u0 : a.mw - 1;
+  const int cx = u + a.hx, cy = v + a.hy;
+  const uint16_t* win = g.fi + (size_t)(cy - a.hy) * g.fi_pitch + (cx - a.hx);
+
+  // Accumulate bins [b0, b0 + kChunk) of this window into acc[j*T + tid].
+  auto chunk = [&](int b0) {
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) acc[j * kSweepThreads + tid] = 0.0;
+    for (int dy = 0; dy < g.kh; ++dy) {
+      const uint16_t* row = win + (size_t)dy * g.fi_pitch;
+      const double* wrow = g.grid + (size_t)dy * g.kw;
+      for (int dx = 0; dx < g.kw; ++dx) {
+        const int j = (int)row[dx] - b0;
+        if ((unsigned)j < (unsigned)kChunk) {
+          double& slot = acc[j * kSweepThreads + tid];
+          slot = __dadd_rn(slot, __ldg(wrow + dx));
+        }
+      }
+    }
+  };
+
+  double s = 0.0, mass = 0.0;
+  if (a.sim == SWG_SIM_BHATTACHARYYA) {
+    for (int b0 = 0; b0 < a.bins; b0 += kChunk) {
+      chunk(b0);
+      const int nb = min(kChunk, a.bins - b0);
+      for (int j = 0; j < nb; ++j) {
+        const double raw = acc[j * kSweepThreads + tid];
+        mass = __dadd_rn(mass, raw);
+        if (raw != 0.0) s = __dadd_rn(s, __dsqrt_rn(__dmul_rn(a.model[b0 + j], raw)));
+      }
+    }
+    s = __ddiv_rn(s, __dsqrt_rn(mass));
+  } else {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int b0 = 0; b0 < a.bins; b0 += kChunk) {
+        chunk(b0);
+        const int nb = min(kChunk, a.bins - b0);
+        for (int j = 0; j < nb; ++j) {
+          const double raw = acc[j * kSweepThreads + tid];
+          if (pass == 0) {
+            mass = __dadd_rn(mass, raw);
+          } else {
+            const double q = __ddiv_rn(raw, mass);
+            const double m = a.model[b0 + j];
+            s = __dadd_rn(s, (q < m) ? q : m);
+          }
+        }
+      }
+  }
+  s = clamp01b(s);
+  if (active) a.scores[(size_t)blockIdx.y * a.mw + u] = s;
+  block_peak_b(active ? s : -2.0, (long long)v * a.mw + u,
+               a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+}  // namespace
+
+cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
+                               cudaStream_t s) {
+  dim3 grid((unsigned)blocks_x, (unsigned)a.rows);
+  k_sweep_brute<<<grid, kSweepThreads, 0, s>>>(a, b);
+  return cudaGetLastError();
+}
+
+}  // namespace swg

@@ -1,0 +1,943 @@
+// swg_abi.cu — host side of the C-ABI (include/swg.h): contexts, device
+// memory, validation with the reference's error classes, plan set-up
+// (exact host restatement of the reference kernel formulas the GPU needs as
+// constants) and kernel launches.  No compute on the data path runs here:
+// every table, histogram, score and peak is produced by the sm_100a kernels
+// in k_build.cu / k_sweep.cu / k_brute.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "swg.h"
+#include "swg_internal.cuh"
+
+using namespace swg;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local size_t g_required = 0;
+
+swg_status fail(swg_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (expr);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? SWG_ERR_CAPACITY          \
+                                                  : SWG_ERR_CUDA,             \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                  \
+  } while (0)
+
+#define ST_TRY(expr)                 \
+  do {                               \
+    swg_status s_ = (expr);          \
+    if (s_ != SWG_OK) return s_;     \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  swg_status ensure(size_t bytes) {
+    if (bytes <= n) return SWG_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    bytes = round_up(bytes, 1 << 16);
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    n = bytes;
+    return SWG_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// ---- exact host restatement of kernel.cpp (plan constants only) --------
+int k_hx(const swg_kernel& k) { return (k.kw - 1) / 2; }
+int k_hy(const swg_kernel& k) { return (k.kh - 1) / 2; }
+bool k_affine(const swg_kernel& k) {
+  return k.kind == SWG_KERNEL_UNIFORM || k.kind == SWG_KERNEL_MANHATTAN;
+}
+bool k_integer(const swg_kernel& k) { return k.kind != SWG_KERNEL_GAUSS_CHEBYSHEV; }
+
+swg_status validate_kernel(const swg_kernel& k) {  // kernel.cpp:10-19
+  if (k.kind < 0 || k.kind > 3) return fail(SWG_ERR_INVALID_KERNEL, "kernel: unknown kind");
+  if (k.kw < 1 || k.kh < 1) return fail(SWG_ERR_INVALID_KERNEL, "kernel: dimensions must be >= 1");
+  if (k.kw % 2 == 0 || k.kh % 2 == 0)
+    return fail(SWG_ERR_INVALID_KERNEL, "kernel: dimensions must be odd, got %dx%d", k.kw, k.kh);
+  if (k.kind == SWG_KERNEL_GAUSS_CHEBYSHEV && !(k.sigma > 0.0))
+    return fail(SWG_ERR_INVALID_KERNEL, "kernel: sigma must be positive");
+  return SWG_OK;
+}
+
+double weight_at(const swg_kernel& k, int dx, int dy) {  // kernel.cpp:25-59
+  const int hx = k_hx(k), hy = k_hy(k);
+  switch (k.kind) {
+    case SWG_KERNEL_UNIFORM:
+      return 1.0;
+    case SWG_KERNEL_MANHATTAN:
+      return static_cast<double>((hx + hy + 1) - (std::abs(dx) + std::abs(dy)));
+    case SWG_KERNEL_CHEBYSHEV: {
+      const int hmax = std::max(hx, hy);
+      const double sx = static_cast<double>(std::abs(dx)) * hmax / std::max(hx, 1);
+      const double sy = static_cast<double>(std::abs(dy)) * hmax / std::max(hy, 1);
+      const long level = std::lround(std::max(sx, sy));
+      return static_cast<double>(hmax + 1 - level);
+    }
+    default: {
+      const double nx = static_cast<double>(std::abs(dx)) / std::max(hx, 1);
+      const double ny = static_cast<double>(std::abs(dy)) / std::max(hy, 1);
+      const double r = std::max(nx, ny);
+      return std::exp(-(r * r) / (2.0 * k.sigma * k.sigma));
+    }
+  }
+}
+
+// Exact strict-window mass of an integer affine kernel (kernel.cpp:61-75).
+int64_t affine_mass(const swg_kernel& k) {
+  const int64_t hx = k_hx(k), hy = k_hy(k);
+  const int64_t area = (int64_t)k.kw * k.kh;
+  if (k.kind == SWG_KERNEL_UNIFORM) return area;
+  return area * (hx + hy + 1) - k.kh * (hx * (hx + 1)) - k.kw * (hy * (hy + 1));
+}
+
+// WeddingCakePlan constructor (baselines.cpp:84-131), same arithmetic order.
+swg_status cake_plan(const swg_kernel& k, int m, int rule, CakeRings& out,
+                     std::vector<double>* weights = nullptr) {
+  const int hx = k_hx(k), hy = k_hy(k);
+  const int max_rings = std::min(hx, hy) + 1;
+  if (m < 1 || m > max_rings)
+    return fail(SWG_ERR_CONFIG, "wedding cake: ring count %d outside [1, %d] for %dx%d", m,
+                max_rings, k.kw, k.kh);
+  if (m > kMaxRings) return fail(SWG_ERR_CONFIG, "wedding cake: more than %d rings", kMaxRings);
+  std::vector<int> sx(m), sy(m);
+  std::vector<double> rw(m, 0.0);
+  for (int i = 0; i < m; ++i) {
+    sx[i] = static_cast<int>((int64_t(i) * hx + m - 1) / m);
+    sy[i] = static_cast<int>((int64_t(i) * hy + m - 1) / m);
+  }
+  if (rule == SWG_RING_LEVEL) {
+    for (int i = 0; i < m; ++i) rw[i] = weight_at(k, hx - sx[i], 0);
+  } else {
+    std::vector<double> sum(m, 0.0);
+    std::vector<int64_t> cnt(m, 0);
+    for (int dy = -hy; dy <= hy; ++dy)
+      for (int dx = -hx; dx <= hx; ++dx) {
+        int ring = 0;
+        for (int i = m - 1; i > 0; --i)
+          if (std::abs(dx) <= hx - sx[i] && std::abs(dy) <= hy - sy[i]) {
+            ring = i;
+            break;
+          }
+        sum[ring] += weight_at(k, dx, dy);
+        cnt[ring] += 1;
+      }
+    for (int i = 0; i < m; ++i) rw[i] = sum[i] / cnt[i];
+  }
+  for (int i = 0; i < m; ++i) {
+    out.a[i] = hx - sx[i];
+    out.c[i] = hy - sy[i];
+    out.coeff[i] = rw[i] - (i > 0 ? rw[i - 1] : 0.0);  // baselines.cpp:141
+  }
+  if (weights) *weights = rw;
+  return SWG_OK;
+}
+
+}  // namespace
+
+struct swg_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::atomic<uint64_t> launches{0};
+  DevBuf parts, scores, peaks, terms, qout, grid;
+};
+
+struct swg_tables {
+  swg_ctx* ctx = nullptr;
+  int w = 0, h = 0, bins = 0, planes = 0, format = 0, levels = 0;
+  bool has_fi = false;
+  uint16_t* fi = nullptr;
+  size_t fip = 0;
+  uint8_t* in = nullptr;  // staging for host input
+  size_t in_pitch = 0, in_row = 0;
+  uint32_t* t32 = nullptr;
+  size_t p32 = 0, ps32 = 0;
+  uint64_t* t64 = nullptr;
+  size_t p64 = 0, ps64 = 0;
+  uint32_t* lb = nullptr;  // look-back scratch: agg + pref
+  int* flags = nullptr;    // nbands*bins flags + ticket
+  int band_h = 0, nbands = 0;
+  size_t wa = 0;
+  size_t bytes = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t pixel_bytes(int format) {
+  switch (format) {
+    case SWG_FMT_GRAY8: return 1;
+    case SWG_FMT_RGB8: return 3;
+    default: return 2;
+  }
+}
+
+void choose_bands(swg_tables* t) {
+  const int target = 148 * 8;
+  int nb = (target + t->bins - 1) / t->bins;
+  nb = std::max(1, std::min(nb, (t->h + 7) / 8));
+  t->band_h = (t->h + nb - 1) / nb;
+  t->nbands = (t->h + t->band_h - 1) / t->band_h;
+  t->wa = round_up((size_t)t->w, 16);
+}
+
+template <typename T>
+swg_status run_build(swg_tables* t, T* out, size_t pitch, size_t ps) {
+  swg_ctx* c = t->ctx;
+  const size_t nflags = (size_t)t->nbands * t->bins;
+  CUDA_TRY(cudaMemsetAsync(t->flags, 0, (nflags + 1) * sizeof(int), c->stream));
+  BuildArgs a{};
+  a.fi = t->fi;
+  a.fi_pitch = t->fip;
+  a.out = out;
+  a.pitch = pitch;
+  a.plane_stride = ps;
+  a.w = t->w;
+  a.h = t->h;
+  a.bins = t->bins;
+  a.planes = t->planes;
+  a.band_h = t->band_h;
+  a.nbands = t->nbands;
+  a.wa = t->wa;
+  const size_t slots = nflags * 2 * t->wa;
+  a.agg = t->lb;
+  a.pref = t->lb + slots;
+  a.flags = t->flags;
+  a.ticket = reinterpret_cast<unsigned*>(t->flags + nflags);
+  CUDA_TRY(launch_build<T>(a, c->stream));
+  c->launches += 2;  // memset + build
+  return SWG_OK;
+}
+
+swg_status upload_and_quantize(swg_tables* t, const void* pixels, int is_device,
+                               size_t pitch_bytes) {
+  swg_ctx* c = t->ctx;
+  const size_t row = (size_t)t->w * pixel_bytes(t->format);
+  if (!pitch_bytes) pitch_bytes = row;
+  if (pitch_bytes < row) return fail(SWG_ERR_ARG, "pitch %zu smaller than a row (%zu)", pitch_bytes, row);
+  const uint8_t* src = static_cast<const uint8_t*>(pixels);
+  size_t src_pitch = pitch_bytes;
+  if (!is_device) {
+    if (!t->in) {
+      t->in_row = row;
+      CUDA_TRY(cudaMallocPitch(reinterpret_cast<void**>(&t->in), &t->in_pitch, row, t->h));
+      t->bytes += t->in_pitch * t->h;
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(t->in, t->in_pitch, pixels, pitch_bytes, row, t->h,
+                               cudaMemcpyHostToDevice, c->stream));
+    src = t->in;
+    src_pitch = t->in_pitch;
+  }
+  QuantArgs q{src, src_pitch, t->w, t->h, t->format,
+              t->format == SWG_FMT_RGB8 ? t->levels : t->bins, t->fi, t->fip};
+  CUDA_TRY(launch_quantize(q, c->stream));
+  c->launches += 1;
+  t->has_fi = true;
+  return SWG_OK;
+}
+
+swg_status ensure_t64(swg_tables* t) {
+  if (t->t64) return SWG_OK;
+  if (!t->has_fi) return fail(SWG_ERR, "tables: no 64-bit planes and no feature image");
+  t->p64 = plane_pitch(t->w, 8);
+  t->ps64 = t->p64 * (size_t)(t->h + 1);
+  const size_t bytes = t->ps64 * t->planes * t->bins * 8;
+  cudaError_t e = cudaMalloc(&t->t64, bytes);
+  if (e != cudaSuccess) {
+    t->t64 = nullptr;
+    g_required = bytes;
+    return fail(SWG_ERR_CAPACITY, "tables: 64-bit export planes need %zu bytes: %s", bytes,
+                cudaGetErrorString(e));
+  }
+  t->bytes += bytes;
+  return run_build<uint64_t>(t, t->t64, t->p64, t->ps64);
+}
+
+swg_status check_tables(const swg_tables* t) {
+  if (!t || !t->ctx) return fail(SWG_ERR_ARG, "NULL tables");
+  return SWG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int swg_abi_version(void) { return SWG_ABI_VERSION; }
+const char* swg_last_error(void) { return g_err.c_str(); }
+size_t swg_last_required_bytes(void) { return g_required; }
+
+swg_status swg_device_count(int* n) {
+  if (!n) return fail(SWG_ERR_ARG, "NULL");
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return fail(SWG_ERR_NO_DEVICE, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  return SWG_OK;
+}
+
+swg_status swg_ctx_create(int device, swg_ctx** out) {
+  if (!out) return fail(SWG_ERR_ARG, "NULL out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(SWG_ERR_NO_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(SWG_ERR_NO_DEVICE, "device %d of %d", device, n);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(SWG_ERR_NO_DEVICE, "device %d is sm_%d%d; libswg is built for sm_100a only",
+                device, prop.major, prop.minor);
+  DeviceGuard g(device);
+  swg_ctx* c = new swg_ctx;
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(SWG_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
+  }
+  c->stream = c->own;
+  *out = c;
+  return SWG_OK;
+}
+
+swg_status swg_ctx_destroy(swg_ctx* c) {
+  if (!c) return SWG_OK;
+  {
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->parts.release();
+    c->scores.release();
+    c->peaks.release();
+    c->terms.release();
+    c->qout.release();
+    c->grid.release();
+    cudaStreamDestroy(c->own);
+  }
+  delete c;
+  return SWG_OK;
+}
+
+swg_status swg_ctx_synchronize(swg_ctx* c) {
+  if (!c) return fail(SWG_ERR_ARG, "NULL ctx");
+  DeviceGuard g(c->device);
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_ctx_set_stream(swg_ctx* c, void* s) {
+  if (!c) return fail(SWG_ERR_ARG, "NULL ctx");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  return SWG_OK;
+}
+
+swg_status swg_ctx_launch_count(swg_ctx* c, uint64_t* n) {
+  if (!c || !n) return fail(SWG_ERR_ARG, "NULL");
+  *n = c->launches.load();
+  return SWG_OK;
+}
+
+swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
+                            size_t pitch_bytes, int width, int height,
+                            int format, int bins, int planes,
+                            size_t memory_budget, swg_tables** out) {
+  if (!c || !pixels || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  if (width < 1 || height < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
+  if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
+  if (planes != SWG_PLANES_PLAIN && planes != SWG_PLANES_AFFINE)
+    return fail(SWG_ERR_ARG, "planes %d", planes);
+  int nb = bins;
+  if (format == SWG_FMT_RGB8) {
+    if (bins < 1 || bins > 40) return fail(SWG_ERR, "RGB levels must be in [1, 40]");
+    nb = bins * bins * bins;
+  }
+  if (nb < 1) return fail(SWG_ERR, "bin count must be >= 1");
+  if (nb > 65535) return fail(SWG_ERR, "bin count must be <= 65535");
+  if (width > 8192) return fail(SWG_ERR_SIZE, "width %d > 8192", width);
+
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  swg_tables* t = new swg_tables;
+  t->ctx = c;
+  t->w = width;
+  t->h = height;
+  t->bins = nb;
+  t->levels = bins;
+  t->planes = planes;
+  t->format = format;
+  t->fip = fi_pitch(width);
+  t->p32 = plane_pitch(width, 4);
+  t->ps32 = t->p32 * (size_t)(height + 1);
+  choose_bands(t);
+  const size_t tab_bytes = t->ps32 * planes * (size_t)nb * 4;
+  const size_t nflags = (size_t)t->nbands * nb;
+  const size_t lb_bytes = nflags * 2 * t->wa * 4 * 2;
+  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2 + (nflags + 1) * 4;
+  if (memory_budget && need > memory_budget) {
+    delete t;
+    g_required = need;
+    return fail(SWG_ERR_CAPACITY, "integral tables need %zu bytes, budget is %zu", need,
+                memory_budget);
+  }
+  auto cleanup = [&](swg_status st) {
+    swg_tables_destroy(t);
+    return st;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
+      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&t->flags, (nflags + 1) * 4)) != cudaSuccess) {
+    g_required = need;
+    cudaGetLastError();
+    return cleanup(fail(SWG_ERR_CAPACITY, "integral tables need %zu device bytes: %s", need,
+                        cudaGetErrorString(e)));
+  }
+  t->bytes = need;
+  swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
+  if (st == SWG_OK) st = run_build<uint32_t>(t, t->t32, t->p32, t->ps32);
+  if (st != SWG_OK) return cleanup(st);
+  *out = t;
+  return SWG_OK;
+}
+
+swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
+                              size_t pitch_bytes) {
+  ST_TRY(check_tables(t));
+  if (!pixels) return fail(SWG_ERR_ARG, "NULL pixels");
+  if (!t->fi) return fail(SWG_ERR, "tables were loaded, not built: cannot rebuild");
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
+  ST_TRY(run_build<uint32_t>(t, t->t32, t->p32, t->ps32));
+  if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64, t->p64, t->ps64));
+  return SWG_OK;
+}
+
+swg_status swg_tables_upload_i64(swg_ctx* c, int w, int h, int bins,
+                                 const int64_t* plain, const int64_t* xramp,
+                                 const int64_t* yramp, swg_tables** out) {
+  if (!c || !plain || !xramp || !yramp || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  if (w < 1 || h < 1 || bins < 1) return fail(SWG_ERR_IO, "table dump: bad dimensions");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  swg_tables* t = new swg_tables;
+  t->ctx = c;
+  t->w = w;
+  t->h = h;
+  t->bins = bins;
+  t->planes = 3;
+  t->format = SWG_FMT_BINS16;
+  t->p32 = plane_pitch(w, 4);
+  t->ps32 = t->p32 * (size_t)(h + 1);
+  t->p64 = plane_pitch(w, 8);
+  t->ps64 = t->p64 * (size_t)(h + 1);
+  const size_t b32 = t->ps32 * 3 * (size_t)bins * 4, b64 = t->ps64 * 3 * (size_t)bins * 8;
+  cudaError_t e;
+  if ((e = cudaMalloc(&t->t32, b32)) != cudaSuccess || (e = cudaMalloc(&t->t64, b64)) != cudaSuccess) {
+    cudaGetLastError();
+    swg_tables_destroy(t);
+    g_required = b32 + b64;
+    return fail(SWG_ERR_CAPACITY, "loaded tables need %zu device bytes", b32 + b64);
+  }
+  t->bytes = b32 + b64;
+  const size_t n = (size_t)(w + 1) * (h + 1);
+  const int64_t* src[3] = {plain, xramp, yramp};
+  for (int b = 0; b < bins; ++b)
+    for (int k = 0; k < 3; ++k) {
+      uint64_t* dst = t->t64 + (size_t)(b * 3 + k) * t->ps64 + Layout<uint64_t>::xoff;
+      e = cudaMemcpy2DAsync(dst, t->p64 * 8, src[k] + (size_t)b * n, (size_t)(w + 1) * 8,
+                            (size_t)(w + 1) * 8, h + 1, cudaMemcpyHostToDevice, c->stream);
+      if (e != cudaSuccess) {
+        swg_tables_destroy(t);
+        return fail(SWG_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
+      }
+    }
+  e = launch_narrow(t->t64, t->p64, t->ps64, t->t32, t->p32, t->ps32, w, h, 3 * bins, c->stream);
+  c->launches += 1;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    swg_tables_destroy(t);
+    return fail(SWG_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  *out = t;
+  return SWG_OK;
+}
+
+swg_status swg_tables_destroy(swg_tables* t) {
+  if (!t) return SWG_OK;
+  if (t->ctx) {
+    DeviceGuard g(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    cudaFree(t->t32);
+    cudaFree(t->t64);
+    cudaFree(t->fi);
+    cudaFree(t->in);
+    cudaFree(t->lb);
+    cudaFree(t->flags);
+  }
+  delete t;
+  return SWG_OK;
+}
+
+swg_status swg_tables_info(const swg_tables* t, int* w, int* h, int* bins, int* planes,
+                           size_t* bytes) {
+  ST_TRY(check_tables(t));
+  if (w) *w = t->w;
+  if (h) *h = t->h;
+  if (bins) *bins = t->bins;
+  if (planes) *planes = t->planes;
+  if (bytes) *bytes = t->bytes;
+  return SWG_OK;
+}
+
+swg_status swg_tables_device_layout(const swg_tables* t, const void** base, size_t* ps,
+                                    size_t* pitch, int* xoff) {
+  ST_TRY(check_tables(t));
+  if (base) *base = t->t32;
+  if (ps) *ps = t->ps32;
+  if (pitch) *pitch = t->p32;
+  if (xoff) *xoff = Layout<uint32_t>::xoff;
+  return SWG_OK;
+}
+
+static swg_status check_export(swg_tables* t, int kind, int b0, int b1, const void* out) {
+  ST_TRY(check_tables(t));
+  if (!out) return fail(SWG_ERR_ARG, "NULL out");
+  if (kind < 0 || kind >= t->planes)
+    return fail(SWG_ERR_OUT_OF_RANGE, "table kind %d not built (planes=%d)", kind, t->planes);
+  if (b0 < 0 || b1 > t->bins || b0 > b1)
+    return fail(SWG_ERR_OUT_OF_RANGE, "bins [%d, %d) outside [0, %d)", b0, b1, t->bins);
+  return SWG_OK;
+}
+
+swg_status swg_tables_export_i64(swg_tables* t, int kind, int b0, int b1, int64_t* out) {
+  ST_TRY(check_export(t, kind, b0, b1, out));
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  ST_TRY(ensure_t64(t));
+  const size_t n = (size_t)(t->w + 1) * (t->h + 1);
+  for (int b = b0; b < b1; ++b)
+    CUDA_TRY(cudaMemcpy2DAsync(out + (size_t)(b - b0) * n, (size_t)(t->w + 1) * 8,
+                               t->t64 + (size_t)(b * t->planes + kind) * t->ps64 +
+                                   Layout<uint64_t>::xoff,
+                               t->p64 * 8, (size_t)(t->w + 1) * 8, t->h + 1,
+                               cudaMemcpyDeviceToHost, t->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  return SWG_OK;
+}
+
+swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32_t* out) {
+  ST_TRY(check_export(t, kind, b0, b1, out));
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  const size_t n = (size_t)(t->w + 1) * (t->h + 1);
+  for (int b = b0; b < b1; ++b)
+    CUDA_TRY(cudaMemcpy2DAsync(out + (size_t)(b - b0) * n, (size_t)(t->w + 1) * 4,
+                               t->t32 + (size_t)(b * t->planes + kind) * t->ps32 +
+                                   Layout<uint32_t>::xoff,
+                               t->p32 * 4, (size_t)(t->w + 1) * 4, t->h + 1,
+                               cudaMemcpyDeviceToHost, t->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  return SWG_OK;
+}
+
+swg_status swg_tables_feature_image(swg_tables* t, uint16_t* out) {
+  ST_TRY(check_tables(t));
+  if (!out) return fail(SWG_ERR_ARG, "NULL out");
+  if (!t->has_fi) return fail(SWG_ERR, "tables were loaded from int64 planes: no feature image");
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  CUDA_TRY(cudaMemcpy2DAsync(out, (size_t)t->w * 2, t->fi, t->fip * 2, (size_t)t->w * 2, t->h,
+                             cudaMemcpyDeviceToHost, t->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  return SWG_OK;
+}
+
+swg_status swg_query_terms(swg_tables* t, int n, int tpw, const swg_term* terms,
+                           int64_t* out) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || tpw < 1 || (n && (!terms || !out))) return fail(SWG_ERR_ARG, "bad query arguments");
+  if (n == 0) return SWG_OK;
+  // Validate rectangles against the table (rect_sum bounds, integral_tables.cpp:127-138)
+  // and bound the magnitude to pick 32-bit (sign-extended) or 64-bit planes.
+  bool need64 = false;
+  for (int w = 0; w < n; ++w) {
+    double bound = 0.0;
+    for (int k = 0; k < tpw; ++k) {
+      const swg_term& q = terms[(size_t)w * tpw + k];
+      if (!q.valid) continue;
+      if (q.x0 < 0 || q.y0 < 0 || q.x0 > q.x1 || q.y0 > q.y1 || q.x1 >= t->w || q.y1 >= t->h)
+        return fail(SWG_ERR_OUT_OF_RANGE,
+                    "rect_sum: rectangle (%d,%d)-(%d,%d) out of bounds for %dx%d", q.x0, q.y0,
+                    q.x1, q.y1, t->w, t->h);
+      if ((q.sx || q.sy) && t->planes < 3)
+        return fail(SWG_ERR_ARG, "query needs ramp planes; tables have plain only");
+      const double area = double(q.x1 - q.x0 + 1) * double(q.y1 - q.y0 + 1);
+      bound += area * (std::fabs(double(q.sx)) * t->w + std::fabs(double(q.sy)) * t->h +
+                       std::fabs(double(q.beta)));
+    }
+    if (bound >= 2147483647.0) need64 = true;
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  swg_ctx* c = t->ctx;
+  if (need64) ST_TRY(ensure_t64(t));
+  const size_t tb = (size_t)n * tpw * sizeof(swg_term), ob = (size_t)n * t->bins * 8;
+  ST_TRY(c->terms.ensure(tb));
+  ST_TRY(c->qout.ensure(ob));
+  CUDA_TRY(cudaMemcpyAsync(c->terms.p, terms, tb, cudaMemcpyHostToDevice, c->stream));
+  QueryArgs a{};
+  a.planes = t->planes;
+  a.bins = t->bins;
+  a.n = n;
+  a.tpw = tpw;
+  a.terms = static_cast<const swg_term*>(c->terms.p);
+  a.out = static_cast<long long*>(c->qout.p);
+  if (need64) {
+    a.tab = t->t64;
+    a.plane_stride = t->ps64;
+    a.pitch = t->p64;
+    CUDA_TRY(launch_query<uint64_t>(a, c->stream));
+  } else {
+    a.tab = t->t32;
+    a.plane_stride = t->ps32;
+    a.pitch = t->p32;
+    CUDA_TRY(launch_query<uint32_t>(a, c->stream));
+  }
+  c->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(out, c->qout.p, ob, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (!need64)  // 32-bit planes: |value| < 2^31, sign-extend the low word
+    for (size_t i = 0; i < (size_t)n * t->bins; ++i) out[i] = (int64_t)(int32_t)(uint32_t)out[i];
+  return SWG_OK;
+}
+
+namespace {
+
+// validate_window (engine.cpp:7-25)
+swg_status validate_window(int w, int h, int cx, int cy, const swg_kernel& k, int border) {
+  ST_TRY(validate_kernel(k));
+  const int hx = k_hx(k), hy = k_hy(k);
+  if (border == SWG_BORDER_STRICT) {
+    if (cx - hx < 0 || cx + hx >= w || cy - hy < 0 || cy + hy >= h)
+      return fail(SWG_ERR_WINDOW_OOB, "strict window %dx%d at (%d,%d) does not fit inside %dx%d",
+                  k.kw, k.kh, cx, cy, w, h);
+  } else if (border == SWG_BORDER_CLIPPED) {
+    if (cx < 0 || cx >= w || cy < 0 || cy >= h)
+      return fail(SWG_ERR_WINDOW_OOB, "clipped window center (%d,%d) outside image", cx, cy);
+  } else {
+    return fail(SWG_ERR_ARG, "border policy %d", border);
+  }
+  return SWG_OK;
+}
+
+// clip_rect (engine.cpp:29-35); an empty intersection invalidates the term.
+void clip_term(swg_term& t, int w, int h) {
+  if (!t.valid) return;
+  t.x0 = std::max(t.x0, 0);
+  t.y0 = std::max(t.y0, 0);
+  t.x1 = std::min(t.x1, w - 1);
+  t.y1 = std::min(t.y1, h - 1);
+  if (t.x0 > t.x1 || t.y0 > t.y1) t.valid = 0;
+}
+
+}  // namespace
+
+swg_status swg_cake_plan(const swg_kernel* k, int rings, int rule, int* sx, int* sy,
+                         double* rw) {
+  if (!k) return fail(SWG_ERR_ARG, "NULL kernel");
+  ST_TRY(validate_kernel(*k));
+  static thread_local CakeRings rg;
+  std::vector<double> w;
+  ST_TRY(cake_plan(*k, rings, rule, rg, &w));
+  for (int i = 0; i < rings; ++i) {
+    if (sx) sx[i] = k_hx(*k) - rg.a[i];
+    if (sy) sy[i] = k_hy(*k) - rg.c[i];
+    if (rw) rw[i] = w[i];
+  }
+  return SWG_OK;
+}
+
+swg_status swg_query_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                             const swg_kernel* k, int method, int border, int64_t* out) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || !k || (n && (!cx || !cy || !out))) return fail(SWG_ERR_ARG, "bad query arguments");
+  if (method != SWG_METHOD_SWIH && method != SWG_METHOD_PLAIN)
+    return fail(SWG_ERR_ARG, "query method %d", method);
+  const int tpw = method == SWG_METHOD_SWIH ? 4 : 1;
+  std::vector<swg_term> terms((size_t)n * tpw);
+  for (int i = 0; i < n; ++i) {
+    ST_TRY(validate_window(t->w, t->h, cx[i], cy[i], *k, border));
+    const int hx = k_hx(*k), hy = k_hy(*k), x = cx[i], y = cy[i];
+    swg_term* d = &terms[(size_t)i * tpw];
+    if (method == SWG_METHOD_PLAIN) {
+      d[0] = swg_term{1, x - hx, y - hy, x + hx, y + hy, 0, 0, 1};
+    } else {
+      // decompose (engine.cpp:83-122): TL owns the centre row and column
+      if (!k_affine(*k))
+        return fail(SWG_ERR_UNSUPPORTED_KERNEL,
+                    "decompose: kernel kind is not quadrant-affine; use the wedding-cake or "
+                    "brute-force baseline");
+      d[0] = swg_term{1, x - hx, y - hy, x, y, 0, 0, 0};
+      d[1] = swg_term{hx > 0, x + 1, y - hy, x + hx, y, 0, 0, 0};
+      d[2] = swg_term{hy > 0, x - hx, y + 1, x, y + hy, 0, 0, 0};
+      d[3] = swg_term{hx > 0 && hy > 0, x + 1, y + 1, x + hx, y + hy, 0, 0, 0};
+      if (k->kind == SWG_KERNEL_UNIFORM) {
+        for (int q = 0; q < 4; ++q) d[q].beta = 1;
+      } else {
+        const int64_t m = hx + hy + 1;
+        d[0].sx = +1; d[0].sy = +1; d[0].beta = m - x - y;
+        d[1].sx = -1; d[1].sy = +1; d[1].beta = m + x - y;
+        d[2].sx = +1; d[2].sy = -1; d[2].beta = m - x + y;
+        d[3].sx = -1; d[3].sy = -1; d[3].beta = m + x + y;
+      }
+    }
+    if (border == SWG_BORDER_CLIPPED)
+      for (int q = 0; q < tpw; ++q) clip_term(d[q], t->w, t->h);
+  }
+  return swg_query_terms(t, n, tpw, terms.data(), out);
+}
+
+swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                            const swg_kernel* k, int rings, int rule, int border, double* out) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || !k || (n && (!cx || !cy || !out))) return fail(SWG_ERR_ARG, "bad query arguments");
+  ST_TRY(validate_kernel(*k));
+  static thread_local CakeRings rg;
+  ST_TRY(cake_plan(*k, rings, rule, rg));
+  if (n == 0) return SWG_OK;
+  std::vector<swg_term> terms((size_t)n * rings);
+  std::vector<double> coeff((size_t)n * rings);
+  for (int i = 0; i < n; ++i) {
+    ST_TRY(validate_window(t->w, t->h, cx[i], cy[i], *k, border));
+    for (int r = 0; r < rings; ++r) {
+      swg_term& q = terms[(size_t)i * rings + r];
+      q = swg_term{1, cx[i] - rg.a[r], cy[i] - rg.c[r], cx[i] + rg.a[r], cy[i] + rg.c[r], 0, 0, 1};
+      if (border == SWG_BORDER_CLIPPED) clip_term(q, t->w, t->h);
+      coeff[(size_t)i * rings + r] = rg.coeff[r];
+    }
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  swg_ctx* c = t->ctx;
+  const size_t tb = terms.size() * sizeof(swg_term), cb = coeff.size() * 8;
+  const size_t ob = (size_t)n * t->bins * 8;
+  ST_TRY(c->terms.ensure(tb + cb));
+  ST_TRY(c->qout.ensure(ob));
+  CUDA_TRY(cudaMemcpyAsync(c->terms.p, terms.data(), tb, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->terms.p) + tb, coeff.data(), cb,
+                           cudaMemcpyHostToDevice, c->stream));
+  QueryArgs a{};
+  a.tab = t->t32;
+  a.plane_stride = t->ps32;
+  a.pitch = t->p32;
+  a.planes = t->planes;
+  a.bins = t->bins;
+  a.n = n;
+  a.tpw = rings;
+  a.terms = static_cast<const swg_term*>(c->terms.p);
+  a.coeff = reinterpret_cast<const double*>(static_cast<char*>(c->terms.p) + tb);
+  a.outd = static_cast<double*>(c->qout.p);
+  CUDA_TRY(launch_cake_query(a, c->stream));
+  c->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(out, c->qout.p, ob, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs,
+                               double* const* scores_host, double* const* scores_dev,
+                               swg_peak* peaks_host, swg_peak* peaks_dev) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || (n && !reqs)) return fail(SWG_ERR_ARG, "bad request list");
+  if (n == 0) return SWG_OK;
+  // ---- validation in the reference order (matching.cpp:112-124)
+  std::vector<int> v0(n), v1(n), mws(n);
+  for (int i = 0; i < n; ++i) {
+    const swg_map_request& r = reqs[i];
+    ST_TRY(validate_kernel(r.kernel));
+    if (t->w < r.kernel.kw || t->h < r.kernel.kh)
+      return fail(SWG_ERR_SIZE, "likelihood map: kernel %dx%d larger than search image %dx%d",
+                  r.kernel.kw, r.kernel.kh, t->w, t->h);
+    if (!r.model) return fail(SWG_ERR_MODEL, "likelihood map: model must be normalized with %d bins", t->bins);
+    if (r.method < 0 || r.method > 3) return fail(SWG_ERR_ARG, "method %d", r.method);
+    if (r.sim < 0 || r.sim > 1) return fail(SWG_ERR_ARG, "similarity %d", r.sim);
+    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel))
+      return fail(SWG_ERR_UNSUPPORTED_KERNEL,
+                  "likelihood map: method swih requires a quadrant-affine kernel");
+    if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
+    const bool needs_ramps = (r.method == SWG_METHOD_SWIH || r.method == SWG_METHOD_BRUTE) &&
+                             r.kernel.kind == SWG_KERNEL_MANHATTAN;
+    if (needs_ramps && t->planes < 3 && !(r.method == SWG_METHOD_BRUTE && t->has_fi))
+      return fail(SWG_ERR_CONFIG, "likelihood map: Manhattan swih needs the ramp planes");
+    if (r.method == SWG_METHOD_BRUTE && !k_affine(r.kernel) && !t->has_fi)
+      return fail(SWG_ERR_CONFIG, "likelihood map: brute force needs the feature image");
+    const int mw = t->w - r.kernel.kw + 1, mh = t->h - r.kernel.kh + 1;
+    int a = r.row_begin, b = r.row_end;
+    if (a == 0 && b == 0) b = mh;
+    if (a < 0 || b > mh || a > b) return fail(SWG_ERR_OUT_OF_RANGE, "map rows [%d, %d) of %d", a, b, mh);
+    if (r.kernel.kind == SWG_KERNEL_MANHATTAN && affine_mass(r.kernel) >= (int64_t(1) << 32))
+      return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the 32-bit exact range", r.kernel.kw,
+                  r.kernel.kh);
+    v0[i] = a;
+    v1[i] = b;
+    mws[i] = mw;
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  swg_ctx* c = t->ctx;
+  // ---- scratch: per-request score buffers (when the caller gave no device
+  // output), CTA peak candidates, device peaks
+  std::vector<size_t> soff(n, 0), poff(n, 0);
+  size_t stot = 0, ptot = 0;
+  std::vector<int> bx(n);
+  for (int i = 0; i < n; ++i) {
+    const size_t cells = (size_t)(v1[i] - v0[i]) * mws[i];
+    if (!(scores_dev && scores_dev[i])) {
+      soff[i] = stot;
+      stot += round_up(cells, 32);
+    }
+    bx[i] = (mws[i] + kSweepThreads - 1) / kSweepThreads;
+    poff[i] = ptot;
+    ptot += (size_t)bx[i] * std::max(v1[i] - v0[i], 1);
+  }
+  ST_TRY(c->scores.ensure(std::max<size_t>(stot, 1) * 8));
+  ST_TRY(c->parts.ensure(ptot * sizeof(PeakPart)));
+  ST_TRY(c->peaks.ensure((size_t)n * sizeof(swg_peak)));
+  swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(c->peaks.p);
+
+  for (int i = 0; i < n; ++i) {
+    const swg_map_request& r = reqs[i];
+    const int rows = v1[i] - v0[i];
+    double* dscores = (scores_dev && scores_dev[i])
+                          ? scores_dev[i]
+                          : static_cast<double*>(c->scores.p) + soff[i];
+    PeakPart* parts = static_cast<PeakPart*>(c->parts.p) + poff[i];
+    if (rows > 0) {
+      static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
+      a.tab = t->t32;
+      a.plane_stride = t->ps32;
+      a.pitch = t->p32;
+      a.planes = t->planes;
+      a.bins = t->bins;
+      a.hx = k_hx(r.kernel);
+      a.hy = k_hy(r.kernel);
+      a.mw = mws[i];
+      a.row0 = v0[i];
+      a.rows = rows;
+      a.sim = r.sim;
+      a.scores = dscores;
+      a.parts = parts;
+      std::memcpy(a.model, r.model, sizeof(double) * t->bins);
+      int method = r.method;
+      swg_kernel k = r.kernel;
+      if (method == SWG_METHOD_PLAIN) {
+        k.kind = SWG_KERNEL_UNIFORM;
+        method = SWG_METHOD_SWIH;
+      }
+      // Brute force on an integer affine kernel yields the same exact counts
+      // as the quadrant path (engine.hpp:62-66; test_matching.cpp:115-141),
+      // so it shares that kernel; other kernels run the direct sum.
+      if (method == SWG_METHOD_BRUTE && k_affine(k) && t->planes == 3) method = SWG_METHOD_SWIH;
+      if (method == SWG_METHOD_BRUTE && k.kind == SWG_KERNEL_UNIFORM) method = SWG_METHOD_SWIH;
+      if (method == SWG_METHOD_SWIH) {
+        a.mass = (double)affine_mass(k);
+        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, bx[i], c->stream));
+      } else if (method == SWG_METHOD_CAKE) {
+        static thread_local CakeRings rg;
+        ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
+        a.rings = r.rings;
+        CUDA_TRY(launch_sweep_cake(a, rg, bx[i], c->stream));
+      } else {
+        // direct per-pixel weighted histogram (baselines.cpp:24-69)
+        const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);
+        std::vector<double> grid((size_t)kw * kh);
+        for (int dy = -hy; dy <= hy; ++dy)
+          for (int dx = -hx; dx <= hx; ++dx)
+            grid[(size_t)(dy + hy) * kw + dx + hx] = weight_at(k, dx, dy);
+        if (k_integer(k))
+          for (auto& w : grid) w = (double)std::llround(w);
+        ST_TRY(c->grid.ensure(grid.size() * 8));
+        CUDA_TRY(cudaMemcpyAsync(c->grid.p, grid.data(), grid.size() * 8,
+                                 cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));  // grid is reused per request
+        BruteArgs ba{};
+        ba.fi = t->fi;
+        ba.fi_pitch = t->fip;
+        ba.grid = static_cast<const double*>(c->grid.p);
+        ba.kw = kw;
+        ba.kh = kh;
+        ba.integer = k_integer(k);
+        CUDA_TRY(launch_sweep_brute(a, ba, bx[i], c->stream));
+      }
+      c->launches += 1;
+      CUDA_TRY(launch_peak_reduce(parts, bx[i] * rows, mws[i], a.hx, a.hy, dpeaks + i, c->stream));
+      c->launches += 1;
+    }
+    if (scores_host && scores_host[i] && rows > 0)
+      CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)rows * mws[i] * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+  }
+  bool sync = false;
+  if (scores_host)
+    for (int i = 0; i < n; ++i) sync |= scores_host[i] != nullptr;
+  if (peaks_host) {
+    CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
+                             cudaMemcpyDeviceToHost, c->stream));
+    sync = true;
+  }
+  if (sync) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,356 @@
+"""GPU parity: the sm_100a path through the C-ABI against the reference's
+golden vectors (tests/golden) and the oracle restatement on seeded inputs.
+
+Bar (BASELINE.json north_star): integral tables bit-exact (uint32 words ==
+reference int64 mod 2^32; int64 export == reference), every likelihood-map
+value bit-exact (the GPU repeats the reference's fp64 operation sequence),
+peak locations and tie resolution identical.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import oracle as O
+from paper_1705_03524_b200 import swg
+
+pytestmark = pytest.mark.gpu
+
+K = swg.Kernel
+
+
+def build(ctx, img, bins, planes=swg.PLANES_AFFINE, fmt=swg.FMT_GRAY8):
+    return ctx.build(np.ascontiguousarray(img), fmt, bins, planes)
+
+
+# ------------------------------------------------------------------ tables
+@pytest.mark.parametrize("name,bins", [("cross3", 2), ("tables_32x32_s99_b8", 8)])
+def test_tables_golden(ctx, name, bins):
+    g = golden(name)
+    t = build(ctx, g["image"], bins)
+    for kind, key in ((0, "plain"), (1, "xramp"), (2, "yramp")):
+        assert (t.export_i64(kind) == g[key]).all()
+        assert (t.export_u32(kind) == (g[key] & 0xFFFFFFFF).astype(np.uint32)).all()
+
+
+@pytest.mark.parametrize("w,h,bins", [(1, 1, 4), (3, 2, 2), (17, 13, 8), (64, 64, 16),
+                                      (255, 37, 5), (1000, 23, 3), (1025, 40, 4),
+                                      (1031, 61, 2), (4100, 9, 2), (33, 700, 3)])
+def test_tables_vs_oracle_shapes(ctx, oracle, w, h, bins):
+    """Widths around the CPT / thread-count / band boundaries, tall images
+    (many look-back bands), degenerate 1x1."""
+    img = oracle.random_gray(w, h, w * 1000 + h)
+    fi = oracle.quantize_gray8(img, bins)
+    p, x, y = oracle.build_tables(fi, bins)
+    t = build(ctx, img, bins)
+    assert (t.feature_image() == fi).all()
+    for kind, ref in ((0, p), (1, x), (2, y)):
+        assert (t.export_u32(kind) == (ref & 0xFFFFFFFF).astype(np.uint32)).all(), kind
+        assert (t.export_i64(kind) == ref).all(), kind
+    tp = build(ctx, img, bins, swg.PLANES_PLAIN)
+    assert (tp.export_u32(0) == p.astype(np.uint32)).all()
+
+
+def test_tables_wrap_exact_large(ctx, oracle):
+    """Ramp values beyond 2^32: the uint32 words are the low
+    32 bits and the int64 export is exact."""
+    w, h, bins = 2048, 2100, 1
+    img = np.zeros((h, w), np.uint8)
+    fi = oracle.quantize_gray8(img, bins)
+    t = build(ctx, img, bins)
+    xr = t.export_i64(1)
+    yy, xx = np.meshgrid(np.arange(h + 1, dtype=np.int64), np.arange(w + 1, dtype=np.int64),
+                         indexing="ij")
+    expect = yy * (xx * (xx - 1) // 2)
+    assert expect.max() > 2**32
+    assert (xr[0] == expect).all()
+    assert (t.export_u32(1)[0] == (expect & 0xFFFFFFFF).astype(np.uint32)).all()
+
+
+@pytest.mark.parametrize("fmt", [swg.FMT_GRAY16, swg.FMT_RGB8, swg.FMT_BINS16])
+def test_tables_other_formats(ctx, oracle, fmt):
+    rng = np.random.default_rng(fmt)
+    h, w = 45, 77
+    if fmt == swg.FMT_GRAY16:
+        img = rng.integers(0, 65536, (h, w), dtype=np.uint16)
+        bins = 64
+        fi = oracle.quantize_gray16(img, bins)
+    elif fmt == swg.FMT_RGB8:
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        bins = 4
+        fi = oracle.quantize_rgb8(img, bins)
+    else:
+        bins = 11
+        img = rng.integers(0, bins, (h, w), dtype=np.uint16)
+        fi = img
+    nb = bins ** 3 if fmt == swg.FMT_RGB8 else bins
+    p, x, y = oracle.build_tables(fi, nb)
+    t = ctx.build(img, fmt, bins, swg.PLANES_AFFINE)
+    assert t.bins == nb
+    assert (t.feature_image() == fi).all()
+    assert (t.export_i64(0) == p).all() and (t.export_i64(1) == x).all()
+    assert (t.export_i64(2) == y).all()
+
+
+def test_rebuild_same_buffers(ctx, oracle):
+    a, b = oracle.random_gray(300, 200, 1), oracle.random_gray(300, 200, 2)
+    t = build(ctx, a, 8)
+    t.rebuild(b)
+    assert (t.export_i64(1) == oracle.build_tables(oracle.quantize_gray8(b, 8), 8)[1]).all()
+
+
+def test_upload_i64_round_trip(ctx):
+    g = golden("tables_32x32_s99_b8")
+    t = ctx.upload_i64(g["plain"], g["xramp"], g["yramp"])
+    for kind, key in ((0, "plain"), (1, "xramp"), (2, "yramp")):
+        assert (t.export_i64(kind) == g[key]).all()
+    k = K(swg.MANHATTAN, 9, 9)
+    b = build(ctx, g["image"], 8)
+    assert (t.query_windows([10, 20], [10, 15], k) == b.query_windows([10, 20], [10, 15], k)).all()
+
+
+# ------------------------------------------------------------------ queries
+def test_cross3_queries(ctx):
+    g = golden("cross3")
+    t = build(ctx, g["image"], 2)
+    assert t.query_windows(1, 1, K(swg.MANHATTAN, 3))[0].tolist() == [7, 8]
+    assert t.query_windows(1, 1, K(swg.UNIFORM, 3))[0].tolist() == [5, 4]
+    assert t.query_windows(1, 1, K(swg.UNIFORM, 3), swg.PLAIN)[0].tolist() == [5, 4]
+    assert t.query_terms([[(1, 0, 0, 1, 1, 1, 1, 1)]])[0].tolist() == [4, 4]
+    assert t.query_terms([[(0, 0, 0, 0, 0, 1, 1, 0)]])[0].tolist() == [0, 0]
+    assert (t.cake_windows(1, 1, K(swg.CHEBYSHEV, 3), 2)[0] == g["cake_cheb3_r2"]).all()
+    assert (t.cake_windows(1, 1, K(swg.MANHATTAN, 3), 2)[0] == g["cake_man3_r2"]).all()
+    assert (t.cake_windows(1, 1, K(swg.MANHATTAN, 3), 2, swg.RING_LEVEL)[0]
+            == g["cake_man3_level"]).all()
+
+
+def test_clipped_queries_golden(ctx):
+    g = golden("clipped_15x11_s8_b4")
+    t = build(ctx, g["image"], 4)
+    cy, cx = np.mgrid[0:11, 0:15]
+    got = t.query_windows(cx.ravel(), cy.ravel(), K(swg.MANHATTAN, 7, 5), swg.SWIH, swg.CLIPPED)
+    assert (got.reshape(11, 15, 4) == g["counts"]).all()
+
+
+@pytest.mark.parametrize("seed", [4242, 55])
+def test_exactness_gate(ctx, oracle, seed):
+    """acceptance_main.cpp:44-85: swih == brute force at every strict centre,
+    b in {2, 8, 16}, Manhattan kernels 1x1 .. 31x31."""
+    rng = np.random.default_rng(seed)
+    for i in range(6):
+        w, h = int(rng.integers(33, 65)), int(rng.integers(33, 65))
+        img = oracle.random_gray(w, h, int(rng.integers(1 << 30)))
+        for bins in (2, 8, 16):
+            fi = oracle.quantize_gray8(img, bins)
+            t = build(ctx, img, bins)
+            for kw, kh in ((1, 1), (3, 3), (5, 9), (7, 7), (11, 11), (31, 31)):
+                k = K(swg.MANHATTAN, kw, kh)
+                cy, cx = np.mgrid[k.hy:h - k.hy, k.hx:w - k.hx]
+                got = t.query_windows(cx.ravel(), cy.ravel(), k)
+                ok = oracle.kernel(O.MANHATTAN, kw, kh)
+                want = np.array([oracle.brute_counts(fi, bins, int(a), int(b), ok)
+                                 for a, b in zip(cx.ravel(), cy.ravel())])
+                assert (got == want).all(), (w, h, bins, kw, kh)
+
+
+def test_cake_windows_vs_oracle(ctx, oracle):
+    img = oracle.random_gray(40, 40, 60)
+    fi = oracle.quantize_gray8(img, 8)
+    tabs = oracle.build_tables(fi, 8)
+    t = build(ctx, img, 8, swg.PLANES_PLAIN)
+    for kind, k, sig in ((swg.GAUSS_CHEB, 9, .6), (swg.CHEBYSHEV, 5, .5), (swg.MANHATTAN, 11, .5)):
+        h = k // 2
+        for rings, rule in ((h + 1, swg.RING_MEAN), (2, swg.RING_LEVEL)):
+            for border, pts in ((swg.STRICT, [(h, h), (20, 20), (39 - h, 39 - h)]),
+                                (swg.CLIPPED, [(0, 0), (3, 39), (39, 5)])):
+                cxs, cys = [p[0] for p in pts], [p[1] for p in pts]
+                got = t.cake_windows(cxs, cys, K(kind, k, k, sig), rings, rule, border)
+                for i, (cx, cy) in enumerate(pts):
+                    want = oracle.cake_histogram(tabs, oracle.kernel(kind, k, k, sig), rings,
+                                                 rule, cx, cy, border)
+                    assert (got[i] == want).all(), (kind, rings, rule, border, cx, cy)
+
+
+def test_query_errors(ctx):
+    t = build(ctx, np.zeros((9, 9), np.uint8), 2)
+    with pytest.raises(swg.WindowOutOfBoundsError):
+        t.query_windows(1, 4, K(swg.MANHATTAN, 5))
+    with pytest.raises(swg.WindowOutOfBoundsError):
+        t.query_windows(4, 9, K(swg.MANHATTAN, 3), swg.SWIH, swg.CLIPPED)
+    with pytest.raises(swg.InvalidKernelError):
+        t.query_windows(4, 4, K(swg.MANHATTAN, 4, 3))
+    with pytest.raises(swg.UnsupportedKernelError):
+        t.query_windows(4, 4, K(swg.GAUSS_CHEB, 3))
+    with pytest.raises(swg.ConfigError):
+        t.cake_windows(4, 4, K(swg.CHEBYSHEV, 3), 3)
+    with pytest.raises(swg.OutOfRangeError):
+        t.query_terms([[(1, 0, 0, 9, 3, 0, 0, 1)]])
+    with pytest.raises(swg.OutOfRangeError):
+        t.export_i64(0, 0, 3)
+    with pytest.raises(swg.CapacityError) as e:
+        ctx.build(np.zeros((8, 8), np.uint8), swg.FMT_GRAY8, 4, swg.PLANES_AFFINE, budget=64)
+    assert e.value.required_bytes > 64
+
+
+# ------------------------------------------------------------------ maps
+@pytest.mark.parametrize("key,method,sim", [("map_bhatt", swg.SWIH, swg.BHATTACHARYYA),
+                                            ("map_inter", swg.SWIH, swg.INTERSECTION),
+                                            ("map_brute", swg.BRUTE, swg.BHATTACHARYYA)])
+def test_map_golden(ctx, key, method, sim):
+    g = golden("map_40x33_s2024_b8_man9x7")
+    t = build(ctx, g["image"], 8)
+    m, pk = t.likelihood_map(K(swg.MANHATTAN, 9, 7), g["model"], method, sim)
+    assert (m == g[key]).all()
+    if key != "map_brute":
+        assert pk == tuple(g["peak_" + key[4:]].tolist())
+        assert (pk[2], pk[3]) == (16, 12)
+
+
+def test_map_plain_golden(ctx):
+    g = golden("map_40x33_s2024_b8_man9x7")
+    t = build(ctx, g["image"], 8, swg.PLANES_PLAIN)
+    templ = np.ascontiguousarray(g["image"][9:16, 12:21])
+    from paper_1705_03524_b200 import api
+    mdl = api.target_model(ctx, templ, K(swg.MANHATTAN, 9, 7), bins=8, method=swg.PLAIN)
+    m, pk = t.likelihood_map(K(swg.MANHATTAN, 9, 7), mdl, swg.PLAIN)
+    assert (m == g["map_plain"]).all() and pk == tuple(g["peak_plain"].tolist())
+
+
+def test_tiled_golden_all_methods(ctx):
+    g = golden("tiled_9x6")
+    t = build(ctx, g["image"], 2)
+    for name, meth in (("swih", swg.SWIH), ("brute", swg.BRUTE), ("cake", swg.CAKE),
+                       ("plain", swg.PLAIN)):
+        m, pk = t.likelihood_map(K(swg.MANHATTAN, 3), g["model_" + name], meth, rings=2)
+        assert (m == g["map_" + name]).all(), name
+
+
+def test_gaussian_golden(ctx):
+    g = golden("gauss_48x40_s60_b8_k9")
+    t = build(ctx, g["image"], 8, swg.PLANES_PLAIN)
+    kg = K(swg.GAUSS_CHEB, 9, 9, 0.6)
+    assert (t.likelihood_map(kg, g["model_cake"], swg.CAKE, rings=5)[0] == g["map_cake"]).all()
+    assert (t.likelihood_map(kg, g["model_cake"], swg.CAKE, swg.INTERSECTION, rings=5)[0]
+            == g["map_cake_inter"]).all()
+    assert (t.likelihood_map(kg, g["model_brute"], swg.BRUTE)[0] == g["map_brute"]).all()
+    assert (t.likelihood_map(kg, g["model_brute"], swg.BRUTE, swg.INTERSECTION)[0]
+            == g["map_brute_inter"]).all()
+
+
+def test_chebyshev_golden(ctx):
+    g = golden("cheb_40x36_s5_b8_k7x5")
+    t = build(ctx, g["image"], 8, swg.PLANES_PLAIN)
+    kc = K(swg.CHEBYSHEV, 7, 5)
+    assert (t.likelihood_map(kc, g["model"], swg.BRUTE)[0] == g["map_brute"]).all()
+    assert (t.likelihood_map(kc, g["model"], swg.CAKE, rings=2, ring_rule=swg.RING_LEVEL)[0]
+            == g["map_cake_level"]).all()
+
+
+@pytest.mark.parametrize("name,k", [("scene_96x80_man21_b16", 21), ("config1_s3", 33)])
+def test_scene_golden(ctx, name, k):
+    g = golden(name)
+    t = build(ctx, g["image"], 16)
+    m, pk = t.likelihood_map(K(swg.MANHATTAN, k), g["model"])
+    assert (m == g["map"]).all()
+    assert pk == tuple(g["peak"].tolist())
+
+
+def test_peak_tie_rule(ctx):
+    """A constant image: every window scores the same; the first cell wins
+    (matching.cpp:211-223).  Ties across CTA boundaries and rows."""
+    img = np.full((40, 300), 77, np.uint8)
+    t = build(ctx, img, 4)
+    mdl = np.array([0.25, 0.25, 0.25, 0.25])
+    for k in (K(swg.MANHATTAN, 5), K(swg.UNIFORM, 3, 7)):
+        m, pk = t.likelihood_map(k, mdl)
+        assert (m == m[0, 0]).all()
+        assert pk[:2] == (0, 0)
+    # equal maxima placed late in row-major order: first one must win
+    img = np.zeros((50, 400), np.uint8)
+    img[30:33, 350:353] = 255
+    img[40:43, 10:13] = 255
+    img[30:33, 200:203] = 255
+    t = build(ctx, img, 2)
+    mdl = np.array([0.0, 1.0])
+    m, pk = t.likelihood_map(K(swg.UNIFORM, 3), mdl)
+    assert pk[:2] == (200, 30) and pk[4] == 1.0
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_maps_vs_oracle_random(ctx, oracle, seed):
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(60, 200)), int(rng.integers(40, 120))
+    img = oracle.random_gray(w, h, seed)
+    for bins in (2, 16, 32):
+        fi = oracle.quantize_gray8(img, bins)
+        t = build(ctx, img, bins)
+        for kind, kw, kh, sig in ((swg.MANHATTAN, 1, 1, .5), (swg.MANHATTAN, 13, 7, .5),
+                                  (swg.UNIFORM, 9, 15, .5), (swg.MANHATTAN, 31, 31, .5),
+                                  (swg.GAUSS_CHEB, 11, 11, .5), (swg.CHEBYSHEV, 7, 9, .5)):
+            ok = oracle.kernel(kind, kw, kh, sig)
+            methods = [swg.SWIH, swg.PLAIN] if kind in (swg.MANHATTAN, swg.UNIFORM) else []
+            methods += [swg.CAKE, swg.BRUTE]
+            for method in methods:
+                rings = min(kw, kh) // 2 + 1 if method == swg.CAKE else 1
+                mdl = oracle.target_model(fi[:kh, :kw].copy(), bins, ok, method, rings)
+                for sim in (swg.BHATTACHARYYA, swg.INTERSECTION):
+                    want = oracle.likelihood_map(fi, bins, mdl, ok, method, sim, rings=rings)
+                    got, pk = t.likelihood_map(K(kind, kw, kh, sig), mdl, method, sim, rings)
+                    assert (got == want).all(), (bins, kind, kw, kh, method, sim)
+                    assert pk == oracle.peak(want, kw // 2, kh // 2)
+
+
+def test_map_row_ranges_and_device_outputs(ctx, oracle):
+    torch = pytest.importorskip("torch")
+    img = oracle.random_gray(128, 96, 9)
+    fi = oracle.quantize_gray8(img, 16)
+    t = build(ctx, img, 16)
+    k = K(swg.MANHATTAN, 17, 17)
+    ok = oracle.kernel(O.MANHATTAN, 17, 17)
+    mdl = oracle.target_model(fi[:17, :17].copy(), 16, ok)
+    full = oracle.likelihood_map(fi, 16, mdl, ok)
+    got, pk = t.likelihood_map(k, mdl, rows=(10, 33))
+    assert (got == full[10:33]).all()
+    mx, my, _, _, sc = oracle.peak(full[10:33], 8, 8)
+    assert pk == (mx, my + 10, mx + 8, my + 18, sc)
+    dev = torch.empty(full.shape, dtype=torch.float64, device="cuda")
+    peaks = torch.zeros(1, 3, dtype=torch.float64, device="cuda")  # 24 B >= sizeof(swg_peak)
+    t.likelihood_maps([swg.MapRequest(k, mdl)], scores="none", scores_dev=[dev], peaks_dev=peaks)
+    ctx.synchronize()
+    assert (dev.cpu().numpy() == full).all()
+
+
+def test_map_errors(ctx):
+    t = build(ctx, np.full((5, 5), 10, np.uint8), 4)
+    mdl = np.full(4, .25)
+    with pytest.raises(swg.SizeError):
+        t.likelihood_map(K(swg.MANHATTAN, 7), mdl)
+    with pytest.raises(swg.UnsupportedKernelError):
+        t.likelihood_map(K(swg.GAUSS_CHEB, 3), mdl, swg.SWIH)
+    with pytest.raises(swg.InvalidKernelError):
+        t.likelihood_map(K(swg.MANHATTAN, 2, 3), mdl)
+    with pytest.raises(swg.ModelError):
+        t.likelihood_map(K(swg.MANHATTAN, 3), np.full(3, 1 / 3))
+    with pytest.raises(swg.ConfigError):
+        t.likelihood_map(K(swg.MANHATTAN, 3), mdl, swg.CAKE, rings=3)
+
+
+# ------------------------------------------------------------------ full-size properties
+def test_config2_full_size_properties(ctx):
+    """BASELINE config 2 geometry (1024^2, b=32): plain-table checksums
+    (T(W,H) per bin = bin population; all bins sum to W*H) and the Gaussian
+    maps' peaks on the planted targets."""
+    from paper_1705_03524_b200 import api, synth
+    sc = synth.config2(1)
+    t = ctx.build(sc.image, swg.FMT_GRAY8, 32, swg.PLANES_PLAIN)
+    corner = t.export_u32(0)[:, -1, -1].astype(np.int64)
+    fi = (sc.image.astype(np.int64) * 32) >> 8
+    assert (corner == np.bincount(fi.ravel(), minlength=32)).all()
+    assert corner.sum() == 1024 * 1024
+    for (cx, cy, tw, th), s in zip(sc.targets[:3], (32, 64, 96)):
+        kw = synth.odd_window(s)
+        k = K(swg.GAUSS_CHEB, kw, kw, 0.5)
+        mdl = api.target_model(ctx, synth.crop(sc.image, cx, cy, kw, kw), k, bins=32,
+                               method=swg.CAKE, rings=kw // 2 + 1)
+        m, pk = t.likelihood_map(k, mdl, swg.CAKE, rings=kw // 2 + 1)
+        assert m.min() >= 0.0 and m.max() <= 1.0
+        assert abs(pk[2] - cx) <= 1 and abs(pk[3] - cy) <= 1 and pk[4] > 0.999
