@@ -50,6 +50,13 @@ def workload(name):
                     gen=synth.config1, bins=16, planes=swg.PLANES_AFFINE,
                     scales=[(swg.Kernel(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)],
                     P=3)
+    if name == "c5m":
+        ks = (17, 25, 37, 53, 79, 117, 173, 257)
+        return dict(name="config5 (Manhattan subset): 2048x2048 u16, 64 bins, Manhattan, windows "
+                         + "/".join(map(str, ks)),
+                    gen=synth.config5, bins=64, planes=swg.PLANES_AFFINE, fmt=swg.FMT_GRAY16,
+                    scales=[(swg.Kernel(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks],
+                    P=3)
     scales = []
     for i, s in enumerate((32, 64, 96)):
         kw = synth.odd_window(s)
@@ -59,13 +66,21 @@ def workload(name):
                 gen=synth.config2, bins=32, planes=swg.PLANES_PLAIN, scales=scales, P=1)
 
 
+def target_center(scene, ti):
+    if ti is None:  # no planted target: template from a fixed interior point
+        h, w = scene.image.shape[:2]
+        return w // 3, h // 2
+    return scene.targets[ti][:2]
+
+
 def make_requests(ctx, wl, scene):
     from paper_1705_03524_b200 import api, swg, synth
     reqs = []
     for k, method, rings, ti in wl["scales"]:
-        cx, cy, _, _ = scene.targets[ti]
+        cx, cy = target_center(scene, ti)
         templ = synth.crop(scene.image, cx, cy, k.kw, k.kh)
-        model = api.target_model(ctx, templ, k, bins=wl["bins"], method=method, rings=rings)
+        model = api.target_model(ctx, templ, k, fmt=wl.get("fmt", swg.FMT_GRAY8),
+                                 bins=wl["bins"], method=method, rings=rings)
         reqs.append(swg.MapRequest(k, model, method, swg.BHATTACHARYYA, rings))
     return reqs
 
@@ -128,7 +143,10 @@ def cpu_reference(wl, scene, models, budget_s=12.0, threads=None):
     img = scene.image
     bins = wl["bins"]
     t0 = time.perf_counter()
-    fi = R.quantize(img, bins)
+    if img.dtype == np.uint16:  # declared uint16 quantiser (no reference counterpart)
+        fi = O.Oracle().quantize_gray16(img, bins)
+    else:
+        fi = R.quantize(img, bins)
     tabs = R.tables(fi, bins, budget=1 << 40)
     t_build = time.perf_counter() - t0
     per_scale = []
@@ -172,7 +190,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -196,11 +214,14 @@ def main():
     scene = wl["gen"](1 + rank)
     H, W = scene.image.shape
     ctx = swg.Context(local)
-    stream = torch.cuda.current_stream()
+    # a non-default torch stream: our launches and the CUDA events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     reqs = make_requests(ctx, wl, scene)
     frame_dev = torch.from_numpy(scene.image).cuda()
-    tables = ctx.build(frame_dev, swg.FMT_GRAY8, wl["bins"], wl["planes"])
+    fmt = wl.get("fmt", swg.FMT_GRAY8)
+    tables = ctx.build(frame_dev, fmt, wl["bins"], wl["planes"])
     maps_dev = [torch.empty(tables.map_shape(r.kernel), dtype=torch.float64, device="cuda")
                 for r in reqs]
     peaks_dev = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
@@ -256,23 +277,24 @@ def main():
     for i, (k, _, _, ti) in enumerate(wl["scales"]):
         ints = pk[i, :2].view(np.int32)
         cxp, cyp = int(ints[2]), int(ints[3])
-        tx, ty = scene.targets[ti][:2]
+        tx, ty = target_center(scene, ti)
         ok_peaks &= abs(cxp - tx) <= 1 and abs(cyp - ty) <= 1
 
     # ---- e2e through the C-ABI with host buffers (pinned), same frame
-    frame_host = torch.from_numpy(scene.image).pin_memory()
-    maps_host = [torch.empty(m.shape, dtype=torch.float64).pin_memory() for m in maps_dev]
+    frame_pin = swg.PinnedBuffer(scene.image.shape, scene.image.dtype)
+    frame_pin.array[...] = scene.image
+    maps_pin = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in maps_dev]
     import ctypes as C
     from paper_1705_03524_b200.swg import Peak, _Req, _check, lib
     creqs = (_Req * len(reqs))()
     for i, r in enumerate(reqs):
         creqs[i] = _Req(r.kernel, r.method, r.sim, r.rings, r.ring_rule, 0, 0,
                         r.model.ctypes.data_as(C.POINTER(C.c_double)))
-    host_ptrs = (C.c_void_p * len(reqs))(*[m.data_ptr() for m in maps_host])
+    host_ptrs = (C.c_void_p * len(reqs))(*[m.array.ctypes.data for m in maps_pin])
     peaks_host = (Peak * len(reqs))()
 
     def e2e_step():
-        _check(lib().swg_tables_rebuild(tables._h, frame_host.data_ptr(), 0, 0))
+        _check(lib().swg_tables_rebuild(tables._h, frame_pin.array.ctypes.data, 0, 0))
         _check(lib().swg_likelihood_maps(tables._h, len(reqs), C.addressof(creqs),
                                          C.addressof(host_ptrs), None, C.addressof(peaks_host),
                                          None))
@@ -296,7 +318,7 @@ def main():
         e2e_total = float(t.item())
     e2e_value = world * n_win * args.steps / e2e_total
     for i in range(len(reqs)):
-        assert (maps_host[i].numpy() == maps_dev[i].cpu().numpy()).all()
+        assert (maps_pin[i].array == maps_dev[i].cpu().numpy()).all()
 
     if rank != 0:
         if dist:
@@ -310,7 +332,7 @@ def main():
     sweep_bytes = sum(ih_bytes + 8 * m.numel() for m in maps_dev)
     sweep_ms = sum(sum(x) for x in scale_ms) / args.steps
     build_avg = sum(build_ms) / args.steps
-    build_bytes = W * H + ih_bytes
+    build_bytes = scene.image.nbytes + ih_bytes
     roofline = {"bound": "hbm", "achieved": sweep_bytes / (sweep_ms / 1e3) / 1e9, "peak": hbm,
                 "unit": "GB/s", "traffic": None, "peak_source": src,
                 "kernel": "k_sweep_cake (3 launches/step, bytes = IH read once + 8 B/window "
@@ -344,7 +366,7 @@ def main():
         "ih_build": {"ms": build_avg, "gbps": build_roof["achieved"], "frac": build_roof["frac"]},
         "per_scale_ms": [sum(x) / args.steps for x in scale_ms],
         "roofline": roofline, "build_roofline": build_roof,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": W * H,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": scene.image.nbytes,
                 "d2h_bytes_per_step": 8 * n_win + 24 * len(reqs),
                 "ms_per_step": e2e_total / args.steps * 1e3},
         "gpu_launches": launches, "peaks_on_targets": bool(ok_peaks),
@@ -366,10 +388,15 @@ def run_reference(args, wl, rank, world):
     R = O.Ref()
     models = []
     for k, method, rings, ti in wl["scales"]:
-        cx, cy, _, _ = scene.targets[ti]
+        cx, cy = target_center(scene, ti)
         templ = synth.crop(scene.image, cx, cy, k.kw, k.kh)
-        models.append(R.target_model(templ, wl["bins"], O.kernel(k.kind, k.kw, k.kh, k.sigma),
-                                     method, rings))
+        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+        if templ.dtype == np.uint16:
+            orc = O.Oracle()
+            models.append(orc.target_model(orc.quantize_gray16(templ, wl["bins"]), wl["bins"], ok,
+                                           method, rings))
+        else:
+            models.append(R.target_model(templ, wl["bins"], ok, method, rings))
     vals = []
     for s in range(args.warmup + args.steps):
         c = cpu_reference(wl, scene, models, budget_s=max(60.0 / (args.warmup + args.steps), 1.5))

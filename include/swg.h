@@ -131,7 +131,13 @@ const char* swg_last_error(void);
 size_t swg_last_required_bytes(void);
 swg_status swg_device_count(int* n);
 
+/* Page-locked host memory for asynchronous host<->device copies. */
+swg_status swg_host_alloc(size_t bytes, void** out);
+swg_status swg_host_free(void* p);
+
 /* ---- context --------------------------------------------------------- */
+/* Contexts are reference counted by the tables built on them: destroying a
+ * context with live tables defers the release to the last table. */
 swg_status swg_ctx_create(int device, swg_ctx** out);
 swg_status swg_ctx_destroy(swg_ctx* ctx);
 swg_status swg_ctx_synchronize(swg_ctx* ctx);
@@ -171,12 +177,14 @@ swg_status swg_tables_export_u32(swg_tables* t, int kind, int bin_begin,
                                  int bin_end, uint32_t* host_out);
 /* The quantised feature image (uint16 bins, w*h). */
 swg_status swg_tables_feature_image(swg_tables* t, uint16_t* host_out);
-/* Device pointer + geometry of the 32-bit planes (for tests / bench):
- * element (x, y) of plane (bin*planes + kind) sits at
- * base[(bin*planes + kind)*plane_stride + y*pitch + x + xoff]. */
+/* Device pointer + geometry of the 32-bit planes (for tests / bench).
+ * Bins are tiled in records of 8 ("bin octets"): element (x, y) of bin b,
+ * table kind k sits at
+ *   base[(((b/8)*planes + k)*plane_stride + y*pitch + x)*8 + b%8]
+ * with plane_stride and pitch counted in records. */
 swg_status swg_tables_device_layout(const swg_tables* t, const void** base,
                                     size_t* plane_stride, size_t* pitch,
-                                    int* xoff);
+                                    int* bins_per_record);
 
 /* ---- window queries (engine API) ----------------------------------- */
 /* n windows, each `terms_per_window` consecutive terms (already clipped by

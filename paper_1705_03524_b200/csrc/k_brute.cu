@@ -48,9 +48,9 @@ __device__ void block_peak_b(double s, long long idx, PeakPart* out) {
   }
 }
 
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a,
+__global__ void __launch_bounds__(kBruteThreads) k_sweep_brute(const SweepArgs a,
                                                                const BruteArgs g) {
-  __shared__ double acc[kChunk * kSweepThreads];
+  __shared__ double acc[kChunk * kBruteThreads];
   const int tid = threadIdx.x;
   const int u0 = blockIdx.x * blockDim.x + tid;
   const int v = a.row0 + blockIdx.y;
@@ -62,14 +62,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a
   // Accumulate bins [b0, b0 + kChunk) of this window into acc[j*T + tid].
   auto chunk = [&](int b0) {
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) acc[j * kSweepThreads + tid] = 0.0;
+    for (int j = 0; j < kChunk; ++j) acc[j * kBruteThreads + tid] = 0.0;
     for (int dy = 0; dy < g.kh; ++dy) {
       const uint16_t* row = win + (size_t)dy * g.fi_pitch;
       const double* wrow = g.grid + (size_t)dy * g.kw;
       for (int dx = 0; dx < g.kw; ++dx) {
         const int j = (int)row[dx] - b0;
         if ((unsigned)j < (unsigned)kChunk) {
-          double& slot = acc[j * kSweepThreads + tid];
+          double& slot = acc[j * kBruteThreads + tid];
           slot = __dadd_rn(slot, __ldg(wrow + dx));
         }
       }
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a
       chunk(b0);
       const int nb = min(kChunk, a.bins - b0);
       for (int j = 0; j < nb; ++j) {
-        const double raw = acc[j * kSweepThreads + tid];
+        const double raw = acc[j * kBruteThreads + tid];
         mass = __dadd_rn(mass, raw);
         if (raw != 0.0) s = __dadd_rn(s, __dsqrt_rn(__dmul_rn(a.model[b0 + j], raw)));
       }
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a
         chunk(b0);
         const int nb = min(kChunk, a.bins - b0);
         for (int j = 0; j < nb; ++j) {
-          const double raw = acc[j * kSweepThreads + tid];
+          const double raw = acc[j * kBruteThreads + tid];
           if (pass == 0) {
             mass = __dadd_rn(mass, raw);
           } else {
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_brute(const SweepArgs a
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
                                cudaStream_t s) {
   dim3 grid((unsigned)blocks_x, (unsigned)a.rows);
-  k_sweep_brute<<<grid, kSweepThreads, 0, s>>>(a, b);
+  k_sweep_brute<<<grid, kBruteThreads, 0, s>>>(a, b);
   return cudaGetLastError();
 }
 

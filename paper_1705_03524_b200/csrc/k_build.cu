@@ -1,21 +1,23 @@
 // k_build.cu — K0 quantise and K1 weighted integral-histogram build (sm_100a).
 //
-// K1 replaces IntegralTableSet::build (proj/src/integral_tables.cpp:72-115).
-// The reference walks bin -> row -> column with running row sums plus the row
-// above.  Here one CTA owns (row band, bin) and the FULL row width:
-//   phase 1  column aggregates of its band (count, y-sum per column),
-//            published for later bands;
-//   phase 2  decoupled look-back over earlier bands of the same bin (flags +
-//            aggregates / inclusive prefixes in global memory) gives the
-//            column sums of all rows above the band; one block scan turns
-//            them into the band's carry row T(x, y0);
-//   phase 3  per row: bin compare, block-wide scan of (count, x-sum) row
-//            prefixes, T(x+1, y+1) = T(x+1, y) + R(x, y) for the three
-//            planes {1, x, y}, written once with 16-byte vector stores
-//            (a warp writes 512 B - 2 KB contiguous per plane and row).
+// K1 replaces IntegralTableSet::build (proj/src/integral_tables.cpp:72-115),
+// which walks bin -> row -> column with running row sums plus the row above.
+// Here one CTA owns (row band, bin octet) of ONE table kind (plain / xramp /
+// yramp; one launch per kind) and the FULL row width, CPT columns per thread:
+//   phase 1  column aggregates of the band for the octet's 8 bins (count, or
+//            y-sum for the yramp kind), published for later bands;
+//   phase 2  decoupled look-back over earlier bands of the same octet
+//            (flags + aggregates / inclusive prefixes in global memory)
+//            gives the column sums of all rows above the band; one block
+//            scan turns them into the band's carry row T(x, y0);
+//   phase 3  per row: bin compare, one block-wide scan of the row prefixes
+//            (counts packed two bins per 32-bit word, or per-bin x sums),
+//            T(x+1, y+1) = T(x+1, y) + R(x, y), and one 32-byte record per
+//            column written with 16-byte stores (a warp writes 4-8 KB of
+//            contiguous records per row).
 // Arithmetic is modulo 2^(8*sizeof(T)); for T = uint32_t every window
-// histogram the sweep forms is < 2^32, so the wrapped tables are exact for
-// it.
+// histogram the sweeps form is < 2^32, so the wrapped tables are exact for
+// them; T = uint64_t reproduces the reference's int64 tables.
 #include "swg_internal.cuh"
 
 namespace swg {
@@ -38,41 +40,40 @@ __device__ __forceinline__ void load_bins(const uint16_t* p, uint16_t (&v)[CPT])
     const uint2 q = *reinterpret_cast<const uint2*>(p);
     v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
   } else {
-#pragma unroll
-    for (int j = 0; j < CPT / 8; ++j) {
-      const uint4 q = *reinterpret_cast<const uint4*>(p + 8 * j);
-      v[8 * j + 0] = q.x & 0xFFFF; v[8 * j + 1] = q.x >> 16;
-      v[8 * j + 2] = q.y & 0xFFFF; v[8 * j + 3] = q.y >> 16;
-      v[8 * j + 4] = q.z & 0xFFFF; v[8 * j + 5] = q.z >> 16;
-      v[8 * j + 6] = q.w & 0xFFFF; v[8 * j + 7] = q.w >> 16;
-    }
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+    v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
   }
 }
 
-// Stores CPT consecutive elements (16-byte aligned) with 16-byte stores.
-template <typename T, int CPT>
-__device__ __forceinline__ void store_run(T* dst, const T (&v)[CPT]) {
-  static_assert((CPT * sizeof(T)) % 16 == 0, "vector store");
+// One 8-element record with 16-byte stores.
+template <typename T>
+__device__ __forceinline__ void store_record(T* dst, const T (&v)[kOct]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  if constexpr (sizeof(T) == 4) {
+    d[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    d[1] = make_uint4(v[4], v[5], v[6], v[7]);
+  } else {
 #pragma unroll
-  for (int j = 0; j < (int)(CPT * sizeof(T) / 16); ++j) {
-    uint4 q;
-    if constexpr (sizeof(T) == 4) {
-      q = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    } else {
-      q = make_uint4((uint32_t)v[2 * j], (uint32_t)(v[2 * j] >> 32),
-                     (uint32_t)v[2 * j + 1], (uint32_t)(v[2 * j + 1] >> 32));
-    }
-    reinterpret_cast<uint4*>(dst)[j] = q;
+    for (int j = 0; j < 4; ++j)
+      d[j] = make_uint4((uint32_t)v[2 * j], (uint32_t)(v[2 * j] >> 32),
+                        (uint32_t)v[2 * j + 1], (uint32_t)(v[2 * j + 1] >> 32));
   }
 }
 
-// Exclusive block scan of N components; one __syncthreads.  `buf` must not
-// be reused by the next call before every thread passed this call's sync
-// (callers alternate two buffers).
+template <typename T>
+__device__ __forceinline__ void store_zero_record(T* dst) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < (int)(kOct * sizeof(T) / 16); ++j) d[j] = make_uint4(0, 0, 0, 0);
+}
+
+// Exclusive block scan of N components with one __syncthreads.  `buf`
+// ([N][32]) must not be rewritten before every thread passed this call's
+// barrier; callers alternate two buffers.
 template <int N, typename V>
-__device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N],
-                                             V* buf, int lane, int warp,
-                                             int nwarps) {
+__device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V* buf,
+                                             int lane, int warp, int nwarps) {
   V inc[N];
 #pragma unroll
   for (int c = 0; c < N; ++c) inc[c] = val[c];
@@ -102,21 +103,21 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N],
   }
 }
 
-template <typename T, int P, int CPT>
+// KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}.
+template <typename T, int KIND, int CPT>
 __global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs g) {
-  constexpr int XOFF = Layout<T>::xoff;
   __shared__ unsigned s_ticket;
   __shared__ int s_flag;
-  __shared__ uint32_t s_row[2][2 * 32];
-  __shared__ T s_carry[3 * 32];
+  __shared__ uint32_t s_row[2][kOct * 32];
+  __shared__ T s_carry[kOct * 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
   if (tid == 0) s_ticket = atomicAdd(g.ticket, 1u);
   __syncthreads();
   const unsigned ticket = s_ticket;
-  const int bin = (int)(ticket % (unsigned)g.bins);
-  const int band = (int)(ticket / (unsigned)g.bins);
+  const int grp = (int)(ticket % (unsigned)g.groups);
+  const int band = (int)(ticket / (unsigned)g.groups);
   const int y0 = band * g.band_h;
   const int y1 = min(y0 + g.band_h, g.h);
   const int xb = tid * CPT;
@@ -125,105 +126,113 @@ __global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs 
   // memory; the last live thread may straddle the edge (padding = kNoBin).
   const bool live = xb < g.w;
   const uint16_t* fi = g.fi + (live ? xb : 0);
+  const uint32_t gb = (uint32_t)grp * kOct;
 
   // ---- phase 1: this band's column aggregates (only later bands need them)
-  uint32_t ac[CPT], ay[CPT];
+  uint32_t ac[CPT][kOct];
 #pragma unroll
-  for (int i = 0; i < CPT; ++i) ac[i] = ay[i] = 0;
-  const size_t slot = ((size_t)band * g.bins + bin) * 2 * g.wa;
+  for (int i = 0; i < CPT; ++i)
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) ac[i][j] = 0;
+  const size_t slot = ((size_t)band * g.groups + grp) * g.wa * kOct;
   if (!last_band) {
     if (live) {
       for (int y = y0; y < y1; ++y) {
         uint16_t v[CPT];
         load_bins<CPT>(fi + (size_t)y * g.fi_pitch, v);
+        const uint32_t inc = KIND == 2 ? (uint32_t)y : 1u;
 #pragma unroll
-        for (int i = 0; i < CPT; ++i)
-          if (v[i] == bin) {
-            ac[i] += 1;
-            ay[i] += (uint32_t)y;
-          }
+        for (int i = 0; i < CPT; ++i) {
+          const uint32_t d = (uint32_t)v[i] - gb;
+#pragma unroll
+          for (int j = 0; j < kOct; ++j) ac[i][j] += (d == (uint32_t)j) ? inc : 0u;
+        }
       }
-      store_run<uint32_t, CPT>(g.agg + slot + xb, ac);
-      store_run<uint32_t, CPT>(g.agg + slot + g.wa + xb, ay);
+      uint4* dst = reinterpret_cast<uint4*>(g.agg + slot + (size_t)xb * kOct);
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        dst[2 * i] = make_uint4(ac[i][0], ac[i][1], ac[i][2], ac[i][3]);
+        dst[2 * i + 1] = make_uint4(ac[i][4], ac[i][5], ac[i][6], ac[i][7]);
+      }
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) st_release(&g.flags[band * g.bins + bin], 1);
+    if (tid == 0) st_release(&g.flags[band * g.groups + grp], 1);
   }
 
-  // ---- phase 2: decoupled look-back along bands of the same bin
-  uint32_t cc[CPT], cy[CPT];
+  // ---- phase 2: decoupled look-back along bands of the same octet
+  uint32_t cc[CPT][kOct];
 #pragma unroll
-  for (int i = 0; i < CPT; ++i) cc[i] = cy[i] = 0;
+  for (int i = 0; i < CPT; ++i)
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) cc[i][j] = 0;
   for (int k = band - 1; k >= 0; --k) {
     if (tid == 0) {
       int f;
-      const int* fp = &g.flags[k * g.bins + bin];
-      while ((f = ld_acquire(fp)) == 0) __nanosleep(64);
+      const int* fp = &g.flags[k * g.groups + grp];
+      while ((f = ld_acquire(fp)) == 0) __nanosleep(32);
       s_flag = f;
     }
     __syncthreads();
     const int f = s_flag;
-    const uint32_t* src = (f == 2 ? g.pref : g.agg) + ((size_t)k * g.bins + bin) * 2 * g.wa;
     if (live) {
+      const uint4* src = reinterpret_cast<const uint4*>(
+          (f == 2 ? g.pref : g.agg) + ((size_t)k * g.groups + grp) * g.wa * kOct +
+          (size_t)xb * kOct);
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        cc[i] += __ldcg(src + xb + i);
-        cy[i] += __ldcg(src + g.wa + xb + i);
+        const uint4 a = __ldcg(src + 2 * i), b = __ldcg(src + 2 * i + 1);
+        cc[i][0] += a.x; cc[i][1] += a.y; cc[i][2] += a.z; cc[i][3] += a.w;
+        cc[i][4] += b.x; cc[i][5] += b.y; cc[i][6] += b.z; cc[i][7] += b.w;
       }
     }
     __syncthreads();  // s_flag is rewritten next iteration
     if (f == 2) break;
   }
   if (!last_band) {
-    uint32_t pc[CPT], py[CPT];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      pc[i] = cc[i] + ac[i];
-      py[i] = cy[i] + ay[i];
-    }
     if (live) {
-      store_run<uint32_t, CPT>(g.pref + slot + xb, pc);
-      store_run<uint32_t, CPT>(g.pref + slot + g.wa + xb, py);
+      uint4* dst = reinterpret_cast<uint4*>(g.pref + slot + (size_t)xb * kOct);
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        dst[2 * i] = make_uint4(cc[i][0] + ac[i][0], cc[i][1] + ac[i][1], cc[i][2] + ac[i][2],
+                                cc[i][3] + ac[i][3]);
+        dst[2 * i + 1] = make_uint4(cc[i][4] + ac[i][4], cc[i][5] + ac[i][5],
+                                    cc[i][6] + ac[i][6], cc[i][7] + ac[i][7]);
+      }
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) st_release(&g.flags[band * g.bins + bin], 2);
+    if (tid == 0) st_release(&g.flags[band * g.groups + grp], 2);
   }
 
-  // ---- carry row T(x+1, y0) = prefix over x of the column sums above y0
-  T tp[CPT], tx[CPT], ty[CPT];
+  // ---- carry row T(x+1, y0): prefix over x of the column sums above y0
+  T t[CPT][kOct];
   {
-    T lp[CPT], lx[CPT], lyv[CPT];
-    T rp = 0, rx = 0, ry = 0;
+    T tot[kOct], ex[kOct];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      rp += (T)cc[i];
-      rx += (T)cc[i] * (T)(xb + i);
-      ry += (T)cy[i];
-      lp[i] = rp;
-      lx[i] = rx;
-      lyv[i] = ry;
-    }
-    T tot[3] = {rp, rx, ry}, ex[3];
-    block_exscan<3, T>(tot, ex, s_carry, lane, warp, nwarps);
+    for (int j = 0; j < kOct; ++j) {
+      T run = 0;
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      tp[i] = ex[0] + lp[i];
-      tx[i] = ex[1] + lx[i];
-      ty[i] = ex[2] + lyv[i];
+      for (int i = 0; i < CPT; ++i) {
+        run += KIND == 1 ? (T)cc[i][j] * (T)(xb + i) : (T)cc[i][j];
+        t[i][j] = run;
+      }
+      tot[j] = run;
     }
+    block_exscan<kOct, T>(tot, ex, s_carry, lane, warp, nwarps);
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) t[i][j] += ex[j];
   }
 
-  T* out = reinterpret_cast<T*>(g.out);
-  T* plane0 = out + (size_t)bin * P * g.plane_stride;
-  if (band == 0) {  // zero row 0 of every plane of this bin
-    const T z[CPT] = {};
+  T* plane = reinterpret_cast<T*>(g.out) +
+             ((size_t)grp * g.planes + KIND) * g.plane_stride * kOct;
+  if (band == 0) {  // zero row 0
+    if (live)
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      if (live) store_run<T, CPT>(plane0 + (size_t)k * g.plane_stride + XOFF + 1 + xb, z);
-      if (tid == 0) plane0[(size_t)k * g.plane_stride + XOFF] = 0;
-    }
+      for (int i = 0; i < CPT; ++i) store_zero_record<T>(plane + (size_t)(xb + 1 + i) * kOct);
+    if (tid == 0) store_zero_record<T>(plane);
   }
 
   // ---- phase 3: rows of the band
@@ -235,40 +244,57 @@ __global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs 
 #pragma unroll
       for (int i = 0; i < CPT; ++i) v[i] = kNoBin;
     }
-    uint32_t lp[CPT], lx[CPT];
-    uint32_t rp = 0, rx = 0;
+    uint32_t d[CPT];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      if (v[i] == bin) {
-        rp += 1;
-        rx += (uint32_t)(xb + i);
-      }
-      lp[i] = rp;
-      lx[i] = rx;
-    }
-    uint32_t tot[2] = {rp, rx}, ex[2];
-    block_exscan<2, uint32_t>(tot, ex, s_row[y & 1], lane, warp, nwarps);
-    const size_t row = (size_t)(y + 1) * g.pitch + XOFF;
+    for (int i = 0; i < CPT; ++i) d[i] = (uint32_t)v[i] - gb;
+    uint32_t* buf = s_row[y & 1];
+    if constexpr (KIND == 1) {
+      // per-bin x sums of this thread's columns, then the block prefix
+      uint32_t tot[kOct], ex[kOct];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const uint32_t r = ex[0] + lp[i];
-      tp[i] += (T)r;
-      if constexpr (P == 3) {
-        tx[i] += (T)(ex[1] + lx[i]);
-        ty[i] += (T)y * (T)r;
-      }
-    }
-    if (live) {
-      store_run<T, CPT>(plane0 + row + 1 + xb, tp);
-      if constexpr (P == 3) {
-        store_run<T, CPT>(plane0 + g.plane_stride + row + 1 + xb, tx);
-        store_run<T, CPT>(plane0 + 2 * g.plane_stride + row + 1 + xb, ty);
-      }
-    }
-    if (tid == 0) {
+      for (int j = 0; j < kOct; ++j) {
+        uint32_t s = 0;
 #pragma unroll
-      for (int k = 0; k < P; ++k) plane0[(size_t)k * g.plane_stride + row] = 0;
+        for (int i = 0; i < CPT; ++i) s += (d[i] == (uint32_t)j) ? (uint32_t)(xb + i) : 0u;
+        tot[j] = s;
+      }
+      block_exscan<kOct, uint32_t>(tot, ex, buf, lane, warp, nwarps);
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+#pragma unroll
+        for (int j = 0; j < kOct; ++j) {
+          ex[j] += (d[i] == (uint32_t)j) ? (uint32_t)(xb + i) : 0u;
+          t[i][j] += (T)ex[j];
+        }
+    } else {
+      // counts, two bins per 32-bit word (16-bit fields; row prefix <= W < 2^16)
+      uint32_t tot[4], ex[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i)
+          s += ((d[i] >> 1) == (uint32_t)q) ? (1u << ((d[i] & 1u) << 4)) : 0u;
+        tot[q] = s;
+      }
+      block_exscan<4, uint32_t>(tot, ex, buf, lane, warp, nwarps);
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ex[q] += ((d[i] >> 1) == (uint32_t)q) ? (1u << ((d[i] & 1u) << 4)) : 0u;
+#pragma unroll
+        for (int j = 0; j < kOct; ++j) {
+          const uint32_t r = (ex[j >> 1] >> ((j & 1) << 4)) & 0xFFFFu;
+          t[i][j] += KIND == 2 ? (T)y * (T)r : (T)r;
+        }
+      }
     }
+    T* row = plane + (size_t)(y + 1) * g.pitch * kOct;
+    if (live)
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+    if (tid == 0) store_zero_record<T>(row);
   }
 }
 
@@ -291,9 +317,9 @@ __global__ void k_quantize(const QuantArgs a) {
           break;
         case SWG_FMT_RGB8: {
           const uint32_t n = (uint32_t)a.bins;  // levels per channel
-          const uint32_t r = (row[3 * x] * n) >> 8, g = (row[3 * x + 1] * n) >> 8,
+          const uint32_t r = (row[3 * x] * n) >> 8, gg = (row[3 * x + 1] * n) >> 8,
                          b = (row[3 * x + 2] * n) >> 8;
-          bin = (uint16_t)((r * n + g) * n + b);
+          bin = (uint16_t)((r * n + gg) * n + b);
           break;
         }
         default:
@@ -304,15 +330,31 @@ __global__ void k_quantize(const QuantArgs a) {
   }
 }
 
-__global__ void k_narrow(const uint64_t* src, size_t pitch64, size_t ps64,
-                         uint32_t* dst, size_t pitch32, size_t ps32, int w,
-                         int h) {
-  const int plane = blockIdx.z;
+// Octet layout -> reference bin-major layout [bin][y][x] (export).
+template <typename T, typename O>
+__global__ void k_export(const T* tab, size_t ps, size_t pitch, int planes, int w, int h,
+                         int kind, int b0, O* out) {
+  const int b = b0 + blockIdx.z;
   const int y = blockIdx.y;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x <= w;
-       x += gridDim.x * blockDim.x)
-    dst[plane * ps32 + (size_t)y * pitch32 + x + Layout<uint32_t>::xoff] =
-        (uint32_t)src[plane * ps64 + (size_t)y * pitch64 + x + Layout<uint64_t>::xoff];
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x <= w; x += gridDim.x * blockDim.x)
+    out[((size_t)blockIdx.z * (h + 1) + y) * (w + 1) + x] =
+        (O)tab[elem_index(ps, pitch, planes, x, y, b, kind)];
+}
+
+// Reference layout int64 (bin-major) -> octet uint64 planes (SWIH1 load).
+__global__ void k_import(const int64_t* src, int w, int h, int kind, uint64_t* tab,
+                         size_t ps, size_t pitch, int planes) {
+  const int b = blockIdx.z;
+  const int y = blockIdx.y;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x <= w; x += gridDim.x * blockDim.x)
+    tab[elem_index(ps, pitch, planes, x, y, b, kind)] =
+        (uint64_t)src[((size_t)b * (h + 1) + y) * (w + 1) + x];
+}
+
+__global__ void k_narrow(const uint64_t* src, uint32_t* dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = (uint32_t)src[i];
 }
 
 }  // namespace
@@ -325,34 +367,47 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
 }
 
 template <typename T>
-cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
+cudaError_t launch_build(const BuildArgs& a, int kind, cudaStream_t s) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
-  const unsigned grid = (unsigned)(a.nbands * a.bins);
-  if (a.planes == 3) {
-    switch (cpt) {
-      case 4: k_build<T, 3, 4><<<grid, threads, 0, s>>>(a); break;
-      case 8: k_build<T, 3, 8><<<grid, threads, 0, s>>>(a); break;
-      default: k_build<T, 3, 16><<<grid, threads, 0, s>>>(a);
-    }
+  const unsigned grid = (unsigned)(a.nbands * a.groups);
+#define SWG_BUILD(K, C) k_build<T, K, C><<<grid, threads, 0, s>>>(a)
+  if (cpt == 4) {
+    if (kind == 0) SWG_BUILD(0, 4); else if (kind == 1) SWG_BUILD(1, 4); else SWG_BUILD(2, 4);
   } else {
-    switch (cpt) {
-      case 4: k_build<T, 1, 4><<<grid, threads, 0, s>>>(a); break;
-      case 8: k_build<T, 1, 8><<<grid, threads, 0, s>>>(a); break;
-      default: k_build<T, 1, 16><<<grid, threads, 0, s>>>(a);
-    }
+    if (kind == 0) SWG_BUILD(0, 8); else if (kind == 1) SWG_BUILD(1, 8); else SWG_BUILD(2, 8);
   }
+#undef SWG_BUILD
   return cudaGetLastError();
 }
 
-template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t);
-template cudaError_t launch_build<uint64_t>(const BuildArgs&, cudaStream_t);
+template cudaError_t launch_build<uint32_t>(const BuildArgs&, int, cudaStream_t);
+template cudaError_t launch_build<uint64_t>(const BuildArgs&, int, cudaStream_t);
 
-cudaError_t launch_narrow(const uint64_t* src, size_t pitch64, size_t ps64,
-                          uint32_t* dst, size_t pitch32, size_t ps32, int w,
-                          int h, int nplanes, cudaStream_t s) {
-  dim3 grid((unsigned)((w + 1 + 255) / 256), (unsigned)(h + 1), (unsigned)nplanes);
-  k_narrow<<<grid, 256, 0, s>>>(src, pitch64, ps64, dst, pitch32, ps32, w, h);
+template <typename T, typename O>
+cudaError_t launch_export(const T* tab, size_t ps, size_t pitch, int planes, int w, int h,
+                          int kind, int b0, int b1, O* out, cudaStream_t s) {
+  dim3 grid((unsigned)((w + 1 + 255) / 256), (unsigned)(h + 1), (unsigned)(b1 - b0));
+  k_export<T, O><<<grid, 256, 0, s>>>(tab, ps, pitch, planes, w, h, kind, b0, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_export<uint32_t, uint32_t>(const uint32_t*, size_t, size_t, int,
+                                                       int, int, int, int, int, uint32_t*,
+                                                       cudaStream_t);
+template cudaError_t launch_export<uint64_t, int64_t>(const uint64_t*, size_t, size_t, int,
+                                                      int, int, int, int, int, int64_t*,
+                                                      cudaStream_t);
+
+cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int kind,
+                              uint64_t* tab, size_t ps, size_t pitch, int planes,
+                              cudaStream_t s) {
+  dim3 grid((unsigned)((w + 1 + 255) / 256), (unsigned)(h + 1), (unsigned)bins);
+  k_import<<<grid, 256, 0, s>>>(src, w, h, kind, tab, ps, pitch, planes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_narrow(const uint64_t* src, uint32_t* dst, size_t n, cudaStream_t s) {
+  k_narrow<<<148 * 8, 256, 0, s>>>(src, dst, n);
   return cudaGetLastError();
 }
 

@@ -1,4 +1,4 @@
-// k_sweep.cu — K2 likelihood-map sweeps, K3 peak reduction, query kernel.
+// k_sweep.cu — K2 likelihood-map sweeps, K3 peak reduction, window queries.
 //
 // K2a (affine) replaces, per strict window, swih_query_into
 // (proj/src/engine.cpp:140-147: decompose 83-122 + 4 x accumulate_term
@@ -9,20 +9,24 @@
 // absolute-offset terms:
 //   H = M*N + X_L - X_R + cx*(N_R - N_L) + Y_T - Y_B + cy*(N_B - N_T)
 // (L/R = columns [cx-hx, cx] / [cx+1, cx+hx], T/B = rows [cy-hy, cy] /
-// [cy+1, cy+hy]), which needs 8 plain + 6 xramp + 6 yramp = 20 cells per bin.
-// All of it is exact integer arithmetic modulo 2^32; the true value lies in
-// [0, mass] with mass < 2^32, so the wrapped result IS the reference count.
+// [cy+1, cy+hy]): 8 plain + 6 xramp + 6 yramp = 20 cells per bin.  Exact
+// integer arithmetic modulo 2^32; the true value lies in [0, mass] with
+// mass < 2^32, so the wrapped result IS the reference count.
 //
 // K2c (cake) replaces WeddingCakePlan::histogram_into
 // (proj/src/baselines.cpp:133-149) + score_weights (matching.cpp:37-52):
-// out[b] = sum_i coeff_i * box_i[b] in ring order, in fp64.
+// out[b] = sum_i coeff_i * box_i[b] in ring order (outer -> inner), fp64.
+// Boxes are nested, so once a bin's box count is 0 every inner term is
+// coeff * 0 and the ring loop stops early (bit-identical: x + (+-0) == x).
 //
-// Scores: one thread owns one window and walks the bins in order with
-// separately rounded IEEE ops (__dmul_rn/__dadd_rn/__dsqrt_rn/__ddiv_rn, no
-// FMA contraction), the reference's exact operation sequence, so every map
-// value is bit-identical to the reference's.  The peak uses
-// the reference tie rule (matching.cpp:211-223): larger score, then smaller
-// row-major index.
+// Thread mapping (both): a warp covers 16 consecutive windows of one map
+// row; lanes 2u / 2u+1 own bins 0-3 / 4-7 of every octet of window u and
+// read 16-byte half records, so each corner load of the warp is 512
+// contiguous bytes.  Scores: the two lanes swap their per-bin terms and both
+// add the octet's 8 terms in bin order with separately rounded IEEE ops
+// (__dmul_rn/__dadd_rn/__dsqrt_rn/__ddiv_rn) — the reference's exact fp64
+// sequence, so every map value is bit-identical.  The peak
+// uses the reference tie rule (matching.cpp:211-223).
 #include "swg_internal.cuh"
 
 namespace swg {
@@ -73,72 +77,114 @@ __device__ __forceinline__ void block_peak(double s, long long idx, PeakPart* ou
   }
 }
 
-template <int SIM>
-__device__ __forceinline__ double add_count_score(double s, double model,
-                                                  uint32_t raw, double mass) {
-  if (raw == 0u) return s;  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
-  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
-    return __dadd_rn(s, __dsqrt_rn(__dmul_rn(model, (double)raw)));
-  } else {
-    const double q = __ddiv_rn((double)raw, mass);
-    return __dadd_rn(s, (q < model) ? q : model);
+__device__ __forceinline__ uint4 ldq(const uint32_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ uint4 box4(uint4 br, uint4 bl, uint4 tr, uint4 tl) {
+  return make_uint4(br.x - bl.x - tr.x + tl.x, br.y - bl.y - tr.y + tl.y,
+                    br.z - bl.z - tr.z + tl.z, br.w - bl.w - tr.w + tl.w);
+}
+__device__ __forceinline__ uint32_t comp(const uint4& v, int k) {
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+
+// Ordered accumulation of one octet: lanes hold bins 0-3 (even) / 4-7 (odd).
+// mass += value_b and s += term_b for b = 0..7 in order, in both lanes.
+__device__ __forceinline__ void add_octet(const double (&val)[4], const double (&term)[4],
+                                          int half, double& mass, double& s, bool with_mass) {
+  double pv[4], pt[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    pv[k] = __shfl_xor_sync(0xFFFFFFFFu, val[k], 1);
+    pt[k] = __shfl_xor_sync(0xFFFFFFFFu, term[k], 1);
+  }
+#pragma unroll
+  for (int j = 0; j < kOct; ++j) {
+    const int k = j & 3;
+    const bool own = (j >> 2) == half;
+    const double v = own ? val[k] : pv[k];
+    const double t = own ? term[k] : pt[k];
+    if (with_mass) mass = __dadd_rn(mass, v);
+    if (v != 0.0) s = __dadd_rn(s, t);
   }
 }
 
-// K2a: Uniform (N only, 4 cells/bin) or Manhattan (20 cells/bin).
+// K2a: Uniform (4 cells per bin) or Manhattan (20 cells per bin).
 template <int SIM, bool UNIFORM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs a) {
-  const int u0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
+  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
+  const int r0 = blockIdx.y * kSweepTileY + warp;
+  const bool active = u0 < a.mw && r0 < a.rows;
+  const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
-  const bool active = u0 < a.mw;
-  const int u = active ? u0 : a.mw - 1;
   const int cx = u + a.hx, cy = v + a.hy;
-  // padded-table corner coordinates
-  const int x0 = cx - a.hx, x1 = cx + 1, x2 = cx + a.hx + 1;
   const size_t pitch = a.pitch;
-  const size_t r0 = (size_t)(cy - a.hy) * pitch + Layout<uint32_t>::xoff;
-  const size_t r1 = (size_t)(cy + 1) * pitch + Layout<uint32_t>::xoff;
-  const size_t r2 = (size_t)(cy + a.hy + 1) * pitch + Layout<uint32_t>::xoff;
+  // record offsets (in uint32 elements) of the corner lattice
+  const size_t x0 = (size_t)(cx - a.hx) * kOct + half * 4;
+  const size_t x1 = (size_t)(cx + 1) * kOct + half * 4;
+  const size_t x2 = (size_t)(cx + a.hx + 1) * kOct + half * 4;
+  const size_t y0 = (size_t)(cy - a.hy) * pitch * kOct;
+  const size_t y1 = (size_t)(cy + 1) * pitch * kOct;
+  const size_t y2 = (size_t)(cy + a.hy + 1) * pitch * kOct;
   const uint32_t* base = reinterpret_cast<const uint32_t*>(a.tab);
-  const size_t ps = a.plane_stride;
+  const size_t ps8 = a.plane_stride * kOct;
   const uint32_t M = (uint32_t)(a.hx + a.hy + 1);
   const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
 
-  double s = 0.0;
-  for (int b = 0; b < a.bins; ++b) {
-    const uint32_t* P = base + (size_t)b * a.planes * ps;
-    uint32_t hist;
+  double s = 0.0, mass_unused = 0.0;
+  for (int g = 0; g < a.groups; ++g) {
+    const uint32_t* P = base + (size_t)g * a.planes * ps8;
+    uint4 hist;
     if constexpr (UNIFORM) {
-      hist = __ldg(P + r2 + x2) - __ldg(P + r2 + x0) - __ldg(P + r0 + x2) + __ldg(P + r0 + x0);
+      hist = box4(ldq(P + y2 + x2), ldq(P + y2 + x0), ldq(P + y0 + x2), ldq(P + y0 + x0));
     } else {
-      const uint32_t* X = P + ps;
-      const uint32_t* Y = P + 2 * ps;
-      const uint32_t p00 = __ldg(P + r0 + x0), p10 = __ldg(P + r0 + x1), p20 = __ldg(P + r0 + x2);
-      const uint32_t p01 = __ldg(P + r1 + x0), p21 = __ldg(P + r1 + x2);
-      const uint32_t p02 = __ldg(P + r2 + x0), p12 = __ldg(P + r2 + x1), p22 = __ldg(P + r2 + x2);
-      const uint32_t q00 = __ldg(X + r0 + x0), q10 = __ldg(X + r0 + x1), q20 = __ldg(X + r0 + x2);
-      const uint32_t q02 = __ldg(X + r2 + x0), q12 = __ldg(X + r2 + x1), q22 = __ldg(X + r2 + x2);
-      const uint32_t w00 = __ldg(Y + r0 + x0), w20 = __ldg(Y + r0 + x2);
-      const uint32_t w01 = __ldg(Y + r1 + x0), w21 = __ldg(Y + r1 + x2);
-      const uint32_t w02 = __ldg(Y + r2 + x0), w22 = __ldg(Y + r2 + x2);
-      const uint32_t n = p22 - p02 - p20 + p00;       // whole window
-      const uint32_t nl = p12 - p02 - p10 + p00;      // columns [x0, x1)
-      const uint32_t nt = p21 - p01 - p20 + p00;      // rows    [y0, y1)
-      const uint32_t xl = q12 - q02 - q10 + q00;
-      const uint32_t xall = q22 - q02 - q20 + q00;
-      const uint32_t yt = w21 - w01 - w20 + w00;
-      const uint32_t yall = w22 - w02 - w20 + w00;
-      const uint32_t nr = n - nl, nb = n - nt;
-      const uint32_t xr = xall - xl, yb = yall - yt;
-      hist = M * n + xl - xr + ucx * (nr - nl) + yt - yb + ucy * (nb - nt);
+      const uint32_t* X = P + ps8;
+      const uint32_t* Y = P + 2 * ps8;
+      const uint4 p00 = ldq(P + y0 + x0), p10 = ldq(P + y0 + x1), p20 = ldq(P + y0 + x2);
+      const uint4 p01 = ldq(P + y1 + x0), p21 = ldq(P + y1 + x2);
+      const uint4 p02 = ldq(P + y2 + x0), p12 = ldq(P + y2 + x1), p22 = ldq(P + y2 + x2);
+      const uint4 n = box4(p22, p02, p20, p00);   // whole window
+      const uint4 nl = box4(p12, p02, p10, p00);  // columns [x0, x1)
+      const uint4 nt = box4(p21, p01, p20, p00);  // rows    [y0, y1)
+      const uint4 q00 = ldq(X + y0 + x0), q10 = ldq(X + y0 + x1), q20 = ldq(X + y0 + x2);
+      const uint4 q02 = ldq(X + y2 + x0), q12 = ldq(X + y2 + x1), q22 = ldq(X + y2 + x2);
+      const uint4 xl = box4(q12, q02, q10, q00), xall = box4(q22, q02, q20, q00);
+      const uint4 w00 = ldq(Y + y0 + x0), w20 = ldq(Y + y0 + x2);
+      const uint4 w01 = ldq(Y + y1 + x0), w21 = ldq(Y + y1 + x2);
+      const uint4 w02 = ldq(Y + y2 + x0), w22 = ldq(Y + y2 + x2);
+      const uint4 yt = box4(w21, w01, w20, w00), yall = box4(w22, w02, w20, w00);
+      auto lin = [&](uint32_t n_, uint32_t nl_, uint32_t nt_, uint32_t xl_, uint32_t xa_,
+                     uint32_t yt_, uint32_t ya_) {
+        const uint32_t nr = n_ - nl_, nb = n_ - nt_, xr = xa_ - xl_, yb = ya_ - yt_;
+        return M * n_ + xl_ - xr + ucx * (nr - nl_) + yt_ - yb + ucy * (nb - nt_);
+      };
+      hist.x = lin(n.x, nl.x, nt.x, xl.x, xall.x, yt.x, yall.x);
+      hist.y = lin(n.y, nl.y, nt.y, xl.y, xall.y, yt.y, yall.y);
+      hist.z = lin(n.z, nl.z, nt.z, xl.z, xall.z, yt.z, yall.z);
+      hist.w = lin(n.w, nl.w, nt.w, xl.w, xall.w, yt.w, yall.w);
     }
-    s = add_count_score<SIM>(s, a.model[b], hist, a.mass);
+    double val[4], term[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t raw = comp(hist, k);
+      const double model = a.model[g * kOct + half * 4 + k];
+      val[k] = (double)raw;
+      if (raw == 0u) {
+        term[k] = 0.0;  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
+      } else if (SIM == SWG_SIM_BHATTACHARYYA) {
+        term[k] = __dsqrt_rn(__dmul_rn(model, (double)raw));
+      } else {
+        const double q = __ddiv_rn((double)raw, a.mass);
+        term[k] = (q < model) ? q : model;
+      }
+    }
+    add_octet(val, term, half, mass_unused, s, false);
   }
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
   s = clamp01(s);
-  if (active) a.scores[(size_t)r * a.mw + u] = s;
-  block_peak(active ? s : -2.0, (long long)v * a.mw + u,
+  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
@@ -146,57 +192,77 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
                                                               const CakeRings rg) {
-  const int u0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
+  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
+  const int r0 = blockIdx.y * kSweepTileY + warp;
+  const bool active = u0 < a.mw && r0 < a.rows;
+  const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
-  const bool active = u0 < a.mw;
-  const int u = active ? u0 : a.mw - 1;
   const int cx = u + a.hx, cy = v + a.hy;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(a.tab);
-  const size_t pitch = a.pitch, ps = a.plane_stride;
-  const int xo = Layout<uint32_t>::xoff;
+  const uint32_t* base = reinterpret_cast<const uint32_t*>(a.tab) + half * 4;
+  const size_t pitch8 = a.pitch * kOct, ps8 = a.plane_stride * kOct;
 
-  auto weighted = [&](const uint32_t* P) {
-    double out = 0.0;
+  // out[k] for bins 4*half + k of octet g: ring order, early exit on empty.
+  auto octet = [&](int g, double (&out)[4]) {
+    const uint32_t* P = base + (size_t)g * a.planes * ps8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = 0.0;
     for (int i = 0; i < a.rings; ++i) {
       const int ax = rg.a[i], cyv = rg.c[i];
-      const size_t ra = (size_t)(cy - cyv) * pitch + xo;
-      const size_t rb = (size_t)(cy + cyv + 1) * pitch + xo;
-      const int xa = cx - ax, xe = cx + ax + 1;
-      const uint32_t cnt = __ldg(P + rb + xe) - __ldg(P + rb + xa) - __ldg(P + ra + xe) +
-                           __ldg(P + ra + xa);
-      if (cnt) out = __dadd_rn(out, __dmul_rn(rg.coeff[i], (double)cnt));
+      const uint32_t* ra = P + (size_t)(cy - cyv) * pitch8;
+      const uint32_t* rb = P + (size_t)(cy + cyv + 1) * pitch8;
+      const size_t xa = (size_t)(cx - ax) * kOct, xe = (size_t)(cx + ax + 1) * kOct;
+      const uint4 cnt = box4(ldq(rb + xe), ldq(rb + xa), ldq(ra + xe), ldq(ra + xa));
+      if ((cnt.x | cnt.y | cnt.z | cnt.w) == 0u) break;  // nested boxes: all inner 0
+      const double c = rg.coeff[i];
+      if (cnt.x) out[0] = __dadd_rn(out[0], __dmul_rn(c, (double)cnt.x));
+      if (cnt.y) out[1] = __dadd_rn(out[1], __dmul_rn(c, (double)cnt.y));
+      if (cnt.z) out[2] = __dadd_rn(out[2], __dmul_rn(c, (double)cnt.z));
+      if (cnt.w) out[3] = __dadd_rn(out[3], __dmul_rn(c, (double)cnt.w));
     }
-    return out;
   };
 
   double s = 0.0, mass = 0.0;
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
-    for (int b = 0; b < a.bins; ++b) {
-      const double out = weighted(base + (size_t)b * a.planes * ps);
-      mass = __dadd_rn(mass, out);
-      if (out != 0.0) s = __dadd_rn(s, __dsqrt_rn(__dmul_rn(a.model[b], out)));
+    for (int g = 0; g < a.groups; ++g) {
+      double out[4], term[4];
+      octet(g, out);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        term[k] = out[k] != 0.0
+                      ? __dsqrt_rn(__dmul_rn(a.model[g * kOct + half * 4 + k], out[k]))
+                      : 0.0;
+      add_octet(out, term, half, mass, s, true);
     }
     s = __ddiv_rn(s, __dsqrt_rn(mass));
   } else {
-    for (int b = 0; b < a.bins; ++b)
-      mass = __dadd_rn(mass, weighted(base + (size_t)b * a.planes * ps));
-    for (int b = 0; b < a.bins; ++b) {
-      const double out = weighted(base + (size_t)b * a.planes * ps);
-      const double q = __ddiv_rn(out, mass);
-      s = __dadd_rn(s, (q < a.model[b]) ? q : a.model[b]);
+    double unused = 0.0;
+    for (int g = 0; g < a.groups; ++g) {
+      double out[4];
+      octet(g, out);
+      add_octet(out, out, half, mass, unused, true);
+    }
+    for (int g = 0; g < a.groups; ++g) {
+      double out[4], term[4];
+      octet(g, out);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double q = __ddiv_rn(out[k], mass);
+        const double m = a.model[g * kOct + half * 4 + k];
+        term[k] = (q < m) ? q : m;
+      }
+      add_octet(out, term, half, unused, s, false);
     }
   }
   s = clamp01(s);
-  if (active) a.scores[(size_t)r * a.mw + u] = s;
-  block_peak(active ? s : -2.0, (long long)v * a.mw + u,
+  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
 // K3: reduce CTA candidates to the map peak (one CTA).
-__global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int n,
-                                                      int mw, int hx, int hy,
-                                                      swg_peak* out) {
+__global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int n, int mw,
+                                                      int hx, int hy, swg_peak* out) {
   double s = -2.0;
   long long idx = 0x7FFFFFFFFFFFFFFFLL;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -226,27 +292,24 @@ __global__ void k_query(const QueryArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const int w = blockIdx.y;
   if (b >= a.bins) return;
-  const T* base = reinterpret_cast<const T*>(a.tab) + (size_t)b * a.planes * a.plane_stride;
-  const int xo = Layout<T>::xoff;
+  const T* tab = reinterpret_cast<const T*>(a.tab);
+  auto at = [&](int x, int y, int k) {
+    return tab[elem_index(a.plane_stride, a.pitch, a.planes, x, y, b, k)];
+  };
   T acc = 0;
   for (int k = 0; k < a.tpw; ++k) {
     const swg_term t = a.terms[(size_t)w * a.tpw + k];
     if (!t.valid) continue;
-    const size_t i00 = (size_t)t.y0 * a.pitch + t.x0 + xo;
-    const size_t i10 = (size_t)t.y0 * a.pitch + t.x1 + 1 + xo;
-    const size_t i01 = (size_t)(t.y1 + 1) * a.pitch + t.x0 + xo;
-    const size_t i11 = (size_t)(t.y1 + 1) * a.pitch + t.x1 + 1 + xo;
-    const T* P = base;
-    const T cnt = P[i11] - P[i01] - P[i10] + P[i00];
+    auto rect = [&](int kind) {
+      return at(t.x1 + 1, t.y1 + 1, kind) - at(t.x0, t.y1 + 1, kind) -
+             at(t.x1 + 1, t.y0, kind) + at(t.x0, t.y0, kind);
+    };
+    const T cnt = rect(0);
     if (t.sx == 0 && t.sy == 0) {
       acc += (T)t.beta * cnt;
       continue;
     }
-    const T* X = base + a.plane_stride;
-    const T* Y = base + 2 * a.plane_stride;
-    const T xs = X[i11] - X[i01] - X[i10] + X[i00];
-    const T ys = Y[i11] - Y[i01] - Y[i10] + Y[i00];
-    acc += (T)t.sx * xs + (T)t.sy * ys + (T)t.beta * cnt;
+    acc += (T)t.sx * rect(1) + (T)t.sy * rect(2) + (T)t.beta * cnt;
   }
   a.out[(size_t)w * a.bins + b] = sizeof(T) == 8 ? (long long)acc : (long long)(uint32_t)acc;
 }
@@ -257,17 +320,16 @@ __global__ void k_cake_query(const QueryArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const int w = blockIdx.y;
   if (b >= a.bins) return;
-  const uint32_t* P = reinterpret_cast<const uint32_t*>(a.tab) + (size_t)b * a.planes * a.plane_stride;
-  const int xo = Layout<uint32_t>::xoff;
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(a.tab);
+  auto at = [&](int x, int y) {
+    return tab[elem_index(a.plane_stride, a.pitch, a.planes, x, y, b, 0)];
+  };
   double out = 0.0;
   for (int k = 0; k < a.tpw; ++k) {
     const swg_term t = a.terms[(size_t)w * a.tpw + k];
     if (!t.valid) continue;
-    const size_t i00 = (size_t)t.y0 * a.pitch + t.x0 + xo;
-    const size_t i10 = (size_t)t.y0 * a.pitch + t.x1 + 1 + xo;
-    const size_t i01 = (size_t)(t.y1 + 1) * a.pitch + t.x0 + xo;
-    const size_t i11 = (size_t)(t.y1 + 1) * a.pitch + t.x1 + 1 + xo;
-    const uint32_t cnt = P[i11] - P[i01] - P[i10] + P[i00];
+    const uint32_t cnt = at(t.x1 + 1, t.y1 + 1) - at(t.x0, t.y1 + 1) - at(t.x1 + 1, t.y0) +
+                         at(t.x0, t.y0);
     out = __dadd_rn(out, __dmul_rn(a.coeff[(size_t)w * a.tpw + k], (double)cnt));
   }
   a.outd[(size_t)w * a.bins + b] = out;
@@ -275,15 +337,7 @@ __global__ void k_cake_query(const QueryArgs a) {
 
 }  // namespace
 
-cudaError_t launch_cake_query(const QueryArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)((a.bins + 127) / 128), (unsigned)a.n);
-  k_cake_query<<<grid, 128, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, int blocks_x,
-                                cudaStream_t s) {
-  dim3 grid((unsigned)blocks_x, (unsigned)a.rows);
+cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) {
     if (uniform) k_sweep_affine<0, true><<<grid, kSweepThreads, 0, s>>>(a);
     else k_sweep_affine<0, false><<<grid, kSweepThreads, 0, s>>>(a);
@@ -294,16 +348,15 @@ cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, int blocks_x,
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, int blocks_x,
+cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, dim3 grid,
                               cudaStream_t s) {
-  dim3 grid((unsigned)blocks_x, (unsigned)a.rows);
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake<0><<<grid, kSweepThreads, 0, s>>>(a, r);
   else k_sweep_cake<1><<<grid, kSweepThreads, 0, s>>>(a, r);
   return cudaGetLastError();
 }
 
-cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw, int hx,
-                               int hy, swg_peak* out, cudaStream_t s) {
+cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw, int hx, int hy,
+                               swg_peak* out, cudaStream_t s) {
   k_peak_reduce<<<1, 1024, 0, s>>>(parts, nparts, mw, hx, hy, out);
   return cudaGetLastError();
 }
@@ -316,5 +369,11 @@ cudaError_t launch_query(const QueryArgs& a, cudaStream_t s) {
 }
 template cudaError_t launch_query<uint32_t>(const QueryArgs&, cudaStream_t);
 template cudaError_t launch_query<uint64_t>(const QueryArgs&, cudaStream_t);
+
+cudaError_t launch_cake_query(const QueryArgs& a, cudaStream_t s) {
+  dim3 grid((unsigned)((a.bins + 127) / 128), (unsigned)a.n);
+  k_cake_query<<<grid, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 }  // namespace swg

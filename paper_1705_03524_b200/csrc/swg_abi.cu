@@ -167,6 +167,7 @@ swg_status cake_plan(const swg_kernel& k, int m, int rule, CakeRings& out,
 }  // namespace
 
 struct swg_ctx {
+  std::atomic<int> refs{1};  // 1 for the handle + 1 per live table
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
@@ -183,12 +184,12 @@ struct swg_tables {
   size_t fip = 0;
   uint8_t* in = nullptr;  // staging for host input
   size_t in_pitch = 0, in_row = 0;
+  int groups = 0;          // bin octets
+  size_t pitch = 0, ps = 0;  // records (shared by the 32- and 64-bit planes)
   uint32_t* t32 = nullptr;
-  size_t p32 = 0, ps32 = 0;
   uint64_t* t64 = nullptr;
-  size_t p64 = 0, ps64 = 0;
   uint32_t* lb = nullptr;  // look-back scratch: agg + pref
-  int* flags = nullptr;    // nbands*bins flags + ticket
+  int* flags = nullptr;    // per kind: nbands*groups flags + ticket
   int band_h = 0, nbands = 0;
   size_t wa = 0;
   size_t bytes = 0;
@@ -218,39 +219,45 @@ size_t pixel_bytes(int format) {
 }
 
 void choose_bands(swg_tables* t) {
-  const int target = 148 * 8;
-  int nb = (target + t->bins - 1) / t->bins;
+  // ~2 waves of row-wide CTAs per table kind on 148 SMs
+  const int target = 148 * 2;
+  int nb = (target + t->groups - 1) / t->groups;
   nb = std::max(1, std::min(nb, (t->h + 7) / 8));
   t->band_h = (t->h + nb - 1) / nb;
   t->nbands = (t->h + t->band_h - 1) / t->band_h;
   t->wa = round_up((size_t)t->w, 16);
 }
 
+size_t flag_words(const swg_tables* t) { return (size_t)t->nbands * t->groups + 1; }
+
 template <typename T>
-swg_status run_build(swg_tables* t, T* out, size_t pitch, size_t ps) {
+swg_status run_build(swg_tables* t, T* out) {
   swg_ctx* c = t->ctx;
-  const size_t nflags = (size_t)t->nbands * t->bins;
-  CUDA_TRY(cudaMemsetAsync(t->flags, 0, (nflags + 1) * sizeof(int), c->stream));
+  const size_t nf = flag_words(t);
+  CUDA_TRY(cudaMemsetAsync(t->flags, 0, nf * t->planes * sizeof(int), c->stream));
   BuildArgs a{};
   a.fi = t->fi;
   a.fi_pitch = t->fip;
   a.out = out;
-  a.pitch = pitch;
-  a.plane_stride = ps;
+  a.pitch = t->pitch;
+  a.plane_stride = t->ps;
   a.w = t->w;
   a.h = t->h;
   a.bins = t->bins;
+  a.groups = t->groups;
   a.planes = t->planes;
   a.band_h = t->band_h;
   a.nbands = t->nbands;
   a.wa = t->wa;
-  const size_t slots = nflags * 2 * t->wa;
+  const size_t slots = (size_t)t->nbands * t->groups * t->wa * kOct;
   a.agg = t->lb;
   a.pref = t->lb + slots;
-  a.flags = t->flags;
-  a.ticket = reinterpret_cast<unsigned*>(t->flags + nflags);
-  CUDA_TRY(launch_build<T>(a, c->stream));
-  c->launches += 2;  // memset + build
+  for (int kind = 0; kind < t->planes; ++kind) {  // kinds run back to back: scratch reuse
+    a.flags = t->flags + kind * nf;
+    a.ticket = reinterpret_cast<unsigned*>(a.flags + nf - 1);
+    CUDA_TRY(launch_build<T>(a, kind, c->stream));
+    c->launches += 1;
+  }
   return SWG_OK;
 }
 
@@ -284,9 +291,7 @@ swg_status upload_and_quantize(swg_tables* t, const void* pixels, int is_device,
 swg_status ensure_t64(swg_tables* t) {
   if (t->t64) return SWG_OK;
   if (!t->has_fi) return fail(SWG_ERR, "tables: no 64-bit planes and no feature image");
-  t->p64 = plane_pitch(t->w, 8);
-  t->ps64 = t->p64 * (size_t)(t->h + 1);
-  const size_t bytes = t->ps64 * t->planes * t->bins * 8;
+  const size_t bytes = t->ps * t->planes * t->groups * kOct * 8;
   cudaError_t e = cudaMalloc(&t->t64, bytes);
   if (e != cudaSuccess) {
     t->t64 = nullptr;
@@ -295,7 +300,7 @@ swg_status ensure_t64(swg_tables* t) {
                 cudaGetErrorString(e));
   }
   t->bytes += bytes;
-  return run_build<uint64_t>(t, t->t64, t->p64, t->ps64);
+  return run_build<uint64_t>(t, t->t64);
 }
 
 swg_status check_tables(const swg_tables* t) {
@@ -347,8 +352,8 @@ swg_status swg_ctx_create(int device, swg_ctx** out) {
   return SWG_OK;
 }
 
-swg_status swg_ctx_destroy(swg_ctx* c) {
-  if (!c) return SWG_OK;
+static void ctx_release(swg_ctx* c) {
+  if (c->refs.fetch_sub(1) != 1) return;
   {
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
@@ -361,6 +366,22 @@ swg_status swg_ctx_destroy(swg_ctx* c) {
     cudaStreamDestroy(c->own);
   }
   delete c;
+}
+
+swg_status swg_ctx_destroy(swg_ctx* c) {
+  if (!c) return SWG_OK;
+  ctx_release(c);
+  return SWG_OK;
+}
+
+swg_status swg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(SWG_ERR_ARG, "NULL out");
+  CUDA_TRY(cudaMallocHost(out, bytes));
+  return SWG_OK;
+}
+
+swg_status swg_host_free(void* p) {
+  if (p) CUDA_TRY(cudaFreeHost(p));
   return SWG_OK;
 }
 
@@ -401,12 +422,13 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   }
   if (nb < 1) return fail(SWG_ERR, "bin count must be >= 1");
   if (nb > 65535) return fail(SWG_ERR, "bin count must be <= 65535");
-  if (width > 8192) return fail(SWG_ERR_SIZE, "width %d > 8192", width);
+  if (width > kMaxWidth) return fail(SWG_ERR_SIZE, "width %d > %d", width, kMaxWidth);
 
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   swg_tables* t = new swg_tables;
   t->ctx = c;
+  c->refs++;
   t->w = width;
   t->h = height;
   t->bins = nb;
@@ -414,15 +436,16 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   t->planes = planes;
   t->format = format;
   t->fip = fi_pitch(width);
-  t->p32 = plane_pitch(width, 4);
-  t->ps32 = t->p32 * (size_t)(height + 1);
+  t->groups = (nb + kOct - 1) / kOct;
+  t->pitch = record_pitch(width);
+  t->ps = t->pitch * (size_t)(height + 1);
   choose_bands(t);
-  const size_t tab_bytes = t->ps32 * planes * (size_t)nb * 4;
-  const size_t nflags = (size_t)t->nbands * nb;
-  const size_t lb_bytes = nflags * 2 * t->wa * 4 * 2;
-  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2 + (nflags + 1) * 4;
+  const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * 4;
+  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct * 4 * 2;
+  const size_t flag_bytes = flag_words(t) * planes * 4;
+  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2 + flag_bytes;
   if (memory_budget && need > memory_budget) {
-    delete t;
+    swg_tables_destroy(t);
     g_required = need;
     return fail(SWG_ERR_CAPACITY, "integral tables need %zu bytes, budget is %zu", need,
                 memory_budget);
@@ -435,7 +458,7 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   if ((e = cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
       (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&t->flags, (nflags + 1) * 4)) != cudaSuccess) {
+      (e = cudaMalloc(&t->flags, flag_bytes)) != cudaSuccess) {
     g_required = need;
     cudaGetLastError();
     return cleanup(fail(SWG_ERR_CAPACITY, "integral tables need %zu device bytes: %s", need,
@@ -443,7 +466,7 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   }
   t->bytes = need;
   swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
-  if (st == SWG_OK) st = run_build<uint32_t>(t, t->t32, t->p32, t->ps32);
+  if (st == SWG_OK) st = run_build<uint32_t>(t, t->t32);
   if (st != SWG_OK) return cleanup(st);
   *out = t;
   return SWG_OK;
@@ -457,8 +480,8 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
-  ST_TRY(run_build<uint32_t>(t, t->t32, t->p32, t->ps32));
-  if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64, t->p64, t->ps64));
+  ST_TRY(run_build<uint32_t>(t, t->t32));
+  if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   return SWG_OK;
 }
 
@@ -468,43 +491,47 @@ swg_status swg_tables_upload_i64(swg_ctx* c, int w, int h, int bins,
   if (!c || !plain || !xramp || !yramp || !out) return fail(SWG_ERR_ARG, "NULL argument");
   *out = nullptr;
   if (w < 1 || h < 1 || bins < 1) return fail(SWG_ERR_IO, "table dump: bad dimensions");
+  if (bins > 65535) return fail(SWG_ERR_IO, "table dump: bad dimensions");
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   swg_tables* t = new swg_tables;
   t->ctx = c;
+  c->refs++;
   t->w = w;
   t->h = h;
   t->bins = bins;
   t->planes = 3;
   t->format = SWG_FMT_BINS16;
-  t->p32 = plane_pitch(w, 4);
-  t->ps32 = t->p32 * (size_t)(h + 1);
-  t->p64 = plane_pitch(w, 8);
-  t->ps64 = t->p64 * (size_t)(h + 1);
-  const size_t b32 = t->ps32 * 3 * (size_t)bins * 4, b64 = t->ps64 * 3 * (size_t)bins * 8;
+  t->groups = (bins + kOct - 1) / kOct;
+  t->pitch = record_pitch(w);
+  t->ps = t->pitch * (size_t)(h + 1);
+  const size_t nel = t->ps * 3 * t->groups * kOct;
+  const size_t n = (size_t)(w + 1) * (h + 1) * bins;
+  int64_t* staging = nullptr;
   cudaError_t e;
-  if ((e = cudaMalloc(&t->t32, b32)) != cudaSuccess || (e = cudaMalloc(&t->t64, b64)) != cudaSuccess) {
+  if ((e = cudaMalloc(&t->t32, nel * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&t->t64, nel * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&staging, n * 8)) != cudaSuccess) {
     cudaGetLastError();
+    cudaFree(staging);
     swg_tables_destroy(t);
-    g_required = b32 + b64;
-    return fail(SWG_ERR_CAPACITY, "loaded tables need %zu device bytes", b32 + b64);
+    g_required = nel * 12 + n * 8;
+    return fail(SWG_ERR_CAPACITY, "loaded tables need %zu device bytes", g_required);
   }
-  t->bytes = b32 + b64;
-  const size_t n = (size_t)(w + 1) * (h + 1);
+  t->bytes = nel * 12;
+  // padding bins / columns of the octet records stay zero
+  e = cudaMemsetAsync(t->t64, 0, nel * 8, c->stream);
   const int64_t* src[3] = {plain, xramp, yramp};
-  for (int b = 0; b < bins; ++b)
-    for (int k = 0; k < 3; ++k) {
-      uint64_t* dst = t->t64 + (size_t)(b * 3 + k) * t->ps64 + Layout<uint64_t>::xoff;
-      e = cudaMemcpy2DAsync(dst, t->p64 * 8, src[k] + (size_t)b * n, (size_t)(w + 1) * 8,
-                            (size_t)(w + 1) * 8, h + 1, cudaMemcpyHostToDevice, c->stream);
-      if (e != cudaSuccess) {
-        swg_tables_destroy(t);
-        return fail(SWG_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
-      }
-    }
-  e = launch_narrow(t->t64, t->p64, t->ps64, t->t32, t->p32, t->ps32, w, h, 3 * bins, c->stream);
+  for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
+    e = cudaMemcpyAsync(staging, src[k], n * 8, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      e = launch_import_i64(staging, w, h, bins, k, t->t64, t->ps, t->pitch, 3, c->stream);
+    c->launches += 1;
+  }
+  if (e == cudaSuccess) e = launch_narrow(t->t64, t->t32, nel, c->stream);
   c->launches += 1;
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(staging);
   if (e != cudaSuccess) {
     swg_tables_destroy(t);
     return fail(SWG_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
@@ -524,6 +551,7 @@ swg_status swg_tables_destroy(swg_tables* t) {
     cudaFree(t->in);
     cudaFree(t->lb);
     cudaFree(t->flags);
+    ctx_release(t->ctx);
   }
   delete t;
   return SWG_OK;
@@ -541,12 +569,12 @@ swg_status swg_tables_info(const swg_tables* t, int* w, int* h, int* bins, int* 
 }
 
 swg_status swg_tables_device_layout(const swg_tables* t, const void** base, size_t* ps,
-                                    size_t* pitch, int* xoff) {
+                                    size_t* pitch, int* bins_per_record) {
   ST_TRY(check_tables(t));
   if (base) *base = t->t32;
-  if (ps) *ps = t->ps32;
-  if (pitch) *pitch = t->p32;
-  if (xoff) *xoff = Layout<uint32_t>::xoff;
+  if (ps) *ps = t->ps;
+  if (pitch) *pitch = t->pitch;
+  if (bins_per_record) *bins_per_record = kOct;
   return SWG_OK;
 }
 
@@ -560,35 +588,46 @@ static swg_status check_export(swg_tables* t, int kind, int b0, int b1, const vo
   return SWG_OK;
 }
 
+}  // extern "C"
+
+template <typename T, typename O>
+static swg_status export_planes(swg_tables* t, const T* tab, int kind, int b0, int b1, O* out) {
+  swg_ctx* c = t->ctx;
+  const size_t per_bin = (size_t)(t->w + 1) * (t->h + 1);
+  // bounded staging: chunks of bins up to ~256 MB
+  const int chunk = (int)std::max<size_t>(1, (256u << 20) / (per_bin * sizeof(O)));
+  ST_TRY(c->qout.ensure((size_t)std::min(chunk, b1 - b0) * per_bin * sizeof(O)));
+  for (int b = b0; b < b1; b += chunk) {
+    const int e = std::min(b1, b + chunk);
+    O* dev = static_cast<O*>(c->qout.p);
+    CUDA_TRY((launch_export<T, O>(tab, t->ps, t->pitch, t->planes, t->w, t->h, kind, b, e,
+                                  dev, c->stream)));
+    c->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(out + (size_t)(b - b0) * per_bin, dev,
+                             (size_t)(e - b) * per_bin * sizeof(O), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return SWG_OK;
+}
+
+extern "C" {
+
 swg_status swg_tables_export_i64(swg_tables* t, int kind, int b0, int b1, int64_t* out) {
   ST_TRY(check_export(t, kind, b0, b1, out));
+  if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(ensure_t64(t));
-  const size_t n = (size_t)(t->w + 1) * (t->h + 1);
-  for (int b = b0; b < b1; ++b)
-    CUDA_TRY(cudaMemcpy2DAsync(out + (size_t)(b - b0) * n, (size_t)(t->w + 1) * 8,
-                               t->t64 + (size_t)(b * t->planes + kind) * t->ps64 +
-                                   Layout<uint64_t>::xoff,
-                               t->p64 * 8, (size_t)(t->w + 1) * 8, t->h + 1,
-                               cudaMemcpyDeviceToHost, t->ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
-  return SWG_OK;
+  return export_planes<uint64_t, int64_t>(t, t->t64, kind, b0, b1, out);
 }
 
 swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32_t* out) {
   ST_TRY(check_export(t, kind, b0, b1, out));
+  if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
-  const size_t n = (size_t)(t->w + 1) * (t->h + 1);
-  for (int b = b0; b < b1; ++b)
-    CUDA_TRY(cudaMemcpy2DAsync(out + (size_t)(b - b0) * n, (size_t)(t->w + 1) * 4,
-                               t->t32 + (size_t)(b * t->planes + kind) * t->ps32 +
-                                   Layout<uint32_t>::xoff,
-                               t->p32 * 4, (size_t)(t->w + 1) * 4, t->h + 1,
-                               cudaMemcpyDeviceToHost, t->ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
-  return SWG_OK;
+  return export_planes<uint32_t, uint32_t>(t, t->t32, kind, b0, b1, out);
 }
 
 swg_status swg_tables_feature_image(swg_tables* t, uint16_t* out) {
@@ -643,15 +682,13 @@ swg_status swg_query_terms(swg_tables* t, int n, int tpw, const swg_term* terms,
   a.tpw = tpw;
   a.terms = static_cast<const swg_term*>(c->terms.p);
   a.out = static_cast<long long*>(c->qout.p);
+  a.plane_stride = t->ps;
+  a.pitch = t->pitch;
   if (need64) {
     a.tab = t->t64;
-    a.plane_stride = t->ps64;
-    a.pitch = t->p64;
     CUDA_TRY(launch_query<uint64_t>(a, c->stream));
   } else {
     a.tab = t->t32;
-    a.plane_stride = t->ps32;
-    a.pitch = t->p32;
     CUDA_TRY(launch_query<uint32_t>(a, c->stream));
   }
   c->launches += 1;
@@ -779,8 +816,8 @@ swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
                            cudaMemcpyHostToDevice, c->stream));
   QueryArgs a{};
   a.tab = t->t32;
-  a.plane_stride = t->ps32;
-  a.pitch = t->p32;
+  a.plane_stride = t->ps;
+  a.pitch = t->pitch;
   a.planes = t->planes;
   a.bins = t->bins;
   a.n = n;
@@ -840,16 +877,26 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // output), CTA peak candidates, device peaks
   std::vector<size_t> soff(n, 0), poff(n, 0);
   size_t stot = 0, ptot = 0;
-  std::vector<int> bx(n);
+  std::vector<dim3> grid(n);
+  std::vector<int> brute(n, 0);
   for (int i = 0; i < n; ++i) {
-    const size_t cells = (size_t)(v1[i] - v0[i]) * mws[i];
+    const swg_map_request& r = reqs[i];
+    const int rows = v1[i] - v0[i];
+    const size_t cells = (size_t)rows * mws[i];
     if (!(scores_dev && scores_dev[i])) {
       soff[i] = stot;
       stot += round_up(cells, 32);
     }
-    bx[i] = (mws[i] + kSweepThreads - 1) / kSweepThreads;
+    brute[i] = r.method == SWG_METHOD_BRUTE && r.kernel.kind != SWG_KERNEL_UNIFORM &&
+               !(r.kernel.kind == SWG_KERNEL_MANHATTAN && t->planes == 3);
+    if (brute[i])
+      grid[i] = dim3((unsigned)((mws[i] + kBruteThreads - 1) / kBruteThreads),
+                     (unsigned)std::max(rows, 1));
+    else
+      grid[i] = dim3((unsigned)((mws[i] + kSweepTileX - 1) / kSweepTileX),
+                     (unsigned)std::max((rows + kSweepTileY - 1) / kSweepTileY, 1));
     poff[i] = ptot;
-    ptot += (size_t)bx[i] * std::max(v1[i] - v0[i], 1);
+    ptot += (size_t)grid[i].x * grid[i].y;
   }
   ST_TRY(c->scores.ensure(std::max<size_t>(stot, 1) * 8));
   ST_TRY(c->parts.ensure(ptot * sizeof(PeakPart)));
@@ -866,10 +913,11 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     if (rows > 0) {
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
       a.tab = t->t32;
-      a.plane_stride = t->ps32;
-      a.pitch = t->p32;
+      a.plane_stride = t->ps;
+      a.pitch = t->pitch;
       a.planes = t->planes;
       a.bins = t->bins;
+      a.groups = t->groups;
       a.hx = k_hx(r.kernel);
       a.hy = k_hy(r.kernel);
       a.mw = mws[i];
@@ -878,6 +926,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       a.sim = r.sim;
       a.scores = dscores;
       a.parts = parts;
+      std::memset(a.model, 0, sizeof(a.model));
       std::memcpy(a.model, r.model, sizeof(double) * t->bins);
       int method = r.method;
       swg_kernel k = r.kernel;
@@ -888,27 +937,26 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       // Brute force on an integer affine kernel yields the same exact counts
       // as the quadrant path (engine.hpp:62-66; test_matching.cpp:115-141),
       // so it shares that kernel; other kernels run the direct sum.
-      if (method == SWG_METHOD_BRUTE && k_affine(k) && t->planes == 3) method = SWG_METHOD_SWIH;
-      if (method == SWG_METHOD_BRUTE && k.kind == SWG_KERNEL_UNIFORM) method = SWG_METHOD_SWIH;
+      if (method == SWG_METHOD_BRUTE && !brute[i]) method = SWG_METHOD_SWIH;
       if (method == SWG_METHOD_SWIH) {
         a.mass = (double)affine_mass(k);
-        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, bx[i], c->stream));
+        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], c->stream));
       } else if (method == SWG_METHOD_CAKE) {
         static thread_local CakeRings rg;
         ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
         a.rings = r.rings;
-        CUDA_TRY(launch_sweep_cake(a, rg, bx[i], c->stream));
+        CUDA_TRY(launch_sweep_cake(a, rg, grid[i], c->stream));
       } else {
         // direct per-pixel weighted histogram (baselines.cpp:24-69)
         const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);
-        std::vector<double> grid((size_t)kw * kh);
+        std::vector<double> wgrid((size_t)kw * kh);
         for (int dy = -hy; dy <= hy; ++dy)
           for (int dx = -hx; dx <= hx; ++dx)
-            grid[(size_t)(dy + hy) * kw + dx + hx] = weight_at(k, dx, dy);
+            wgrid[(size_t)(dy + hy) * kw + dx + hx] = weight_at(k, dx, dy);
         if (k_integer(k))
-          for (auto& w : grid) w = (double)std::llround(w);
-        ST_TRY(c->grid.ensure(grid.size() * 8));
-        CUDA_TRY(cudaMemcpyAsync(c->grid.p, grid.data(), grid.size() * 8,
+          for (auto& w : wgrid) w = (double)std::llround(w);
+        ST_TRY(c->grid.ensure(wgrid.size() * 8));
+        CUDA_TRY(cudaMemcpyAsync(c->grid.p, wgrid.data(), wgrid.size() * 8,
                                  cudaMemcpyHostToDevice, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));  // grid is reused per request
         BruteArgs ba{};
@@ -918,10 +966,11 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ba.kw = kw;
         ba.kh = kh;
         ba.integer = k_integer(k);
-        CUDA_TRY(launch_sweep_brute(a, ba, bx[i], c->stream));
+        CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, c->stream));
       }
       c->launches += 1;
-      CUDA_TRY(launch_peak_reduce(parts, bx[i] * rows, mws[i], a.hx, a.hy, dpeaks + i, c->stream));
+      CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
+                                  dpeaks + i, c->stream));
       c->launches += 1;
     }
     if (scores_host && scores_host[i] && rows > 0)

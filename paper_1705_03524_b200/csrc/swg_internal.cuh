@@ -1,15 +1,21 @@
-// swg_internal.cuh — shared structs, device-layout rules and helpers for the
-// sm_100a kernels behind include/swg.h.
+// swg_internal.cuh — shared structs, the device layout and kernel launchers
+// behind include/swg.h.
 //
-// Device layout of one plane set:
-//   plane (bin, kind) = base + (bin * P + kind) * plane_stride
-//   element (x, y), x in [0, W], y in [0, H] (zero row 0 / column 0, the
-//   reference's padded (W+1)x(H+1) plane, integral_tables.hpp:53-58)
-//   sits at  y * pitch + x + XOFF,  XOFF = 16/sizeof(T) - 1
-// so that the data columns x = 1 .. W start on a 16-byte boundary and every
-// row starts on a 128-byte boundary (pitch is a multiple of 32 elements).
+// Device layout of one plane set: "bin octets".
+// The reference stores one (W+1)x(H+1) int64 plane per bin and table kind,
+// bin-major (integral_tables.hpp:53-58,116-118).  Here bins are tiled in
+// groups of 8: a RECORD holds the 8 bins of one group at one padded cell,
+//   record (x, y) of plane (group g, kind k)
+//       = base + ((g*P + k) * plane_stride + y * pitch + x) * 8 elements,
+//   element of bin b = record[b % 8],  g = b / 8,
+// x in [0, W], y in [0, H] with the reference's zero row 0 / column 0.
+// A record is 32 B (uint32) or 64 B (uint64); `pitch` (records) is a multiple
+// of 4, so rows start on 128-byte boundaries.  A sweep thread reads one
+// 16-byte half record per corner (4 bins), two adjacent lanes cover one
+// window's octet, and a warp's load is 512 contiguous bytes.
 // T = uint32_t (default: exact mod 2^32, every strict window histogram fits)
-// or uint64_t (exact export / wide kernels).
+// or uint64_t (exact export / large-magnitude queries); both share pitch
+// and plane_stride (in records).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -21,44 +27,39 @@ namespace swg {
 
 constexpr int kMaxBins = SWG_MAX_BINS;
 constexpr int kMaxRings = SWG_MAX_RINGS;
+constexpr int kOct = 8;              // bins per record
 constexpr uint16_t kNoBin = 0xFFFF;  // feature-image padding sentinel
-
-template <typename T>
-struct Layout {
-  static constexpr int xoff = 16 / (int)sizeof(T) - 1;
-};
+constexpr int kMaxWidth = 4096;      // build CTA spans a full row (CPT <= 8)
 
 inline size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
-// Columns per build thread, chosen from the width (see choose_cpt).
-inline int choose_cpt(int w) {
-  if (w <= 1024) return 4;
-  if (w <= 4096) return 8;
-  return 16;
-}
+// Columns per build thread.
+inline int choose_cpt(int w) { return w <= 1024 ? 4 : 8; }
 
-// Row pitch (elements) of a plane with element type of `elem` bytes.
-inline size_t plane_pitch(int w, int elem) {
-  const int xoff = 16 / elem - 1;
-  return round_up((size_t)xoff + 1 + round_up((size_t)w, 16), 32);
-}
+// Row pitch in records (room for the straddling last build thread).
+inline size_t record_pitch(int w) { return round_up((size_t)w + 1 + 8, 4); }
 
 // Feature-image pitch (uint16 elements); rows padded with kNoBin.
 inline size_t fi_pitch(int w) { return round_up((size_t)w, 64); }
+
+__host__ __device__ inline size_t elem_index(size_t ps, size_t pitch, int planes, int x,
+                                             int y, int b, int k) {
+  return ((((size_t)(b >> 3) * planes + k) * ps + (size_t)y * pitch + x) << 3) + (b & 7);
+}
 
 // ---------------------------------------------------------------- build
 struct BuildArgs {
   const uint16_t* fi;  // quantised image, fi_pitch elements per row
   size_t fi_pitch;
   void* out;           // planes (T)
-  size_t pitch;        // elements
-  size_t plane_stride; // elements
-  int w, h, bins, planes;
+  size_t pitch;        // records
+  size_t plane_stride; // records
+  int w, h, bins, groups, planes;
   int band_h, nbands;
-  size_t wa;           // padded width of the look-back arrays
-  uint32_t* agg;       // [nbands][bins][2][wa]: band column count / y-sum
-  uint32_t* pref;      // [nbands][bins][2][wa]: inclusive prefix over bands
-  int* flags;          // [nbands * bins]: 0 none, 1 aggregate, 2 prefix
+  size_t wa;           // padded width (columns) of the look-back arrays
+  uint32_t* agg;       // [nbands][groups][wa][8]: band column count / y-sum
+  uint32_t* pref;      // [nbands][groups][wa][8]: inclusive prefix over bands
+  int* flags;          // [nbands * groups]: 0 none, 1 aggregate, 2 prefix
   unsigned* ticket;    // dynamic CTA ordering for the look-back
 };
 
@@ -77,11 +78,12 @@ struct PeakPart {
 };
 
 struct SweepArgs {
-  const void* tab;     // planes
-  size_t plane_stride; // elements
-  size_t pitch;        // elements
+  const void* tab;     // planes (uint32 records)
+  size_t plane_stride; // records
+  size_t pitch;        // records
   int planes;
   int bins;
+  int groups;
   int hx, hy;
   int mw;              // map width
   int row0;            // first map row of this launch
@@ -91,13 +93,13 @@ struct SweepArgs {
   double mass;         // exact strict-window mass (affine kernels)
   double* scores;      // rows x mw, row r = map row row0 + r
   PeakPart* parts;     // one per CTA
-  double model[kMaxBins];
+  double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
 struct CakeRings {
-  int a[kMaxRings];       // ring i box half-extent in x: hx - shrink_x[i]
-  int c[kMaxRings];       // ring i box half-extent in y: hy - shrink_y[i]
-  double coeff[kMaxRings];// w_i - w_{i-1} (baselines.cpp:141)
+  int a[kMaxRings];        // ring i box half-extent in x: hx - shrink_x[i]
+  int c[kMaxRings];        // ring i box half-extent in y: hy - shrink_y[i]
+  double coeff[kMaxRings]; // w_i - w_{i-1} (baselines.cpp:141)
 };
 
 struct BruteArgs {
@@ -110,7 +112,7 @@ struct BruteArgs {
 
 struct QueryArgs {
   const void* tab;
-  size_t plane_stride, pitch;
+  size_t plane_stride, pitch;  // records
   int planes, bins;
   int n, tpw;
   const swg_term* terms;  // device
@@ -119,25 +121,34 @@ struct QueryArgs {
   double* outd;           // cake: device n x bins
 };
 
+// Sweep CTA geometry: 8 warps; a warp = 16 windows of one map row, two lanes
+// per window (lane parity = which half of each bin octet).
+constexpr int kSweepThreads = 256;
+constexpr int kSweepTileX = 16;
+constexpr int kSweepTileY = 8;
+// Brute-force sweep: one thread per window.
+constexpr int kBruteThreads = 128;
+
 // Kernel launchers (defined in the .cu files).
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
 template <typename T>
-cudaError_t launch_build(const BuildArgs& a, cudaStream_t s);
-cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, int blocks_x,
-                                cudaStream_t s);
-cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r,
-                              int blocks_x, cudaStream_t s);
-cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b,
-                               int blocks_x, cudaStream_t s);
-cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw,
-                               int hx, int hy, swg_peak* out, cudaStream_t s);
+cudaError_t launch_build(const BuildArgs& a, int kind, cudaStream_t s);
+cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
+cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, dim3 grid,
+                              cudaStream_t s);
+cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
+                               cudaStream_t s);
+cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw, int hx, int hy,
+                               swg_peak* out, cudaStream_t s);
 template <typename T>
 cudaError_t launch_query(const QueryArgs& a, cudaStream_t s);
 cudaError_t launch_cake_query(const QueryArgs& a, cudaStream_t s);
-cudaError_t launch_narrow(const uint64_t* src, size_t pitch64, size_t ps64,
-                          uint32_t* dst, size_t pitch32, size_t ps32, int w,
-                          int h, int nplanes, cudaStream_t s);
-
-constexpr int kSweepThreads = 128;
+template <typename T, typename O>
+cudaError_t launch_export(const T* tab, size_t ps, size_t pitch, int planes, int w, int h,
+                          int kind, int b0, int b1, O* out, cudaStream_t s);
+cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int kind,
+                              uint64_t* tab, size_t ps, size_t pitch, int planes,
+                              cudaStream_t s);
+cudaError_t launch_narrow(const uint64_t* src, uint32_t* dst, size_t n, cudaStream_t s);
 
 }  // namespace swg

@@ -162,6 +162,8 @@ def lib():
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
         "swg_likelihood_maps": [vp, C.c_int, vp, vp, vp, vp, vp],
+        "swg_host_alloc": [C.c_size_t, C.POINTER(vp)],
+        "swg_host_free": [vp],
     }.items():
         f = getattr(L, name)
         f.argtypes = args
@@ -371,6 +373,8 @@ class Tables:
                             m.ctypes.data_as(C.POINTER(C.c_double)))
         maps = [None] * n
         host_ptrs = None
+        if any(min(self.map_shape(r.kernel, r.rows)) <= 0 for r in reqs):
+            scores = "none"  # invalid geometry: let the library raise SizeError
         if scores == "host":
             host_ptrs = (C.c_void_p * n)()
             for i, r in enumerate(reqs):
@@ -393,6 +397,25 @@ class Tables:
         maps, peaks = self.likelihood_maps([MapRequest(kernel, model, method, sim, rings,
                                                        ring_rule, rows)])
         return maps[0], peaks[0]
+
+
+class PinnedBuffer:
+    """Page-locked host memory from libswg's own CUDA runtime
+    (swg_host_alloc); exposed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self._p = C.c_void_p()
+        _check(lib().swg_host_alloc(max(self.nbytes, 1), C.byref(self._p)))
+        buf = (C.c_char * max(self.nbytes, 1)).from_address(self._p.value)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self._p:
+                lib().swg_host_free(self._p)
+        except Exception:
+            pass
 
 
 def cake_plan(kernel: Kernel, rings: int, rule=RING_MEAN):

@@ -146,7 +146,7 @@ def test_exactness_gate(ctx, oracle, seed):
                 k = K(swg.MANHATTAN, kw, kh)
                 cy, cx = np.mgrid[k.hy:h - k.hy, k.hx:w - k.hx]
                 got = t.query_windows(cx.ravel(), cy.ravel(), k)
-                ok = oracle.kernel(O.MANHATTAN, kw, kh)
+                ok = O.kernel(O.MANHATTAN, kw, kh)
                 want = np.array([oracle.brute_counts(fi, bins, int(a), int(b), ok)
                                  for a, b in zip(cx.ravel(), cy.ravel())])
                 assert (got == want).all(), (w, h, bins, kw, kh)
@@ -165,7 +165,7 @@ def test_cake_windows_vs_oracle(ctx, oracle):
                 cxs, cys = [p[0] for p in pts], [p[1] for p in pts]
                 got = t.cake_windows(cxs, cys, K(kind, k, k, sig), rings, rule, border)
                 for i, (cx, cy) in enumerate(pts):
-                    want = oracle.cake_histogram(tabs, oracle.kernel(kind, k, k, sig), rings,
+                    want = oracle.cake_histogram(tabs, O.kernel(kind, k, k, sig), rings,
                                                  rule, cx, cy, border)
                     assert (got[i] == want).all(), (kind, rings, rule, border, cx, cy)
 
@@ -286,7 +286,7 @@ def test_maps_vs_oracle_random(ctx, oracle, seed):
         for kind, kw, kh, sig in ((swg.MANHATTAN, 1, 1, .5), (swg.MANHATTAN, 13, 7, .5),
                                   (swg.UNIFORM, 9, 15, .5), (swg.MANHATTAN, 31, 31, .5),
                                   (swg.GAUSS_CHEB, 11, 11, .5), (swg.CHEBYSHEV, 7, 9, .5)):
-            ok = oracle.kernel(kind, kw, kh, sig)
+            ok = O.kernel(kind, kw, kh, sig)
             methods = [swg.SWIH, swg.PLAIN] if kind in (swg.MANHATTAN, swg.UNIFORM) else []
             methods += [swg.CAKE, swg.BRUTE]
             for method in methods:
@@ -305,7 +305,7 @@ def test_map_row_ranges_and_device_outputs(ctx, oracle):
     fi = oracle.quantize_gray8(img, 16)
     t = build(ctx, img, 16)
     k = K(swg.MANHATTAN, 17, 17)
-    ok = oracle.kernel(O.MANHATTAN, 17, 17)
+    ok = O.kernel(O.MANHATTAN, 17, 17)
     mdl = oracle.target_model(fi[:17, :17].copy(), 16, ok)
     full = oracle.likelihood_map(fi, 16, mdl, ok)
     got, pk = t.likelihood_map(k, mdl, rows=(10, 33))
