@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -244,6 +245,16 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    # The step as one CUDA graph (no host launch gaps between the kernels).
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+
     nev = 2 + len(reqs)
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     clocks = Clocks(local)
@@ -261,6 +272,26 @@ def main():
     if dist:
         dist.barrier()
     per_step = [events[s][0].elapsed_time(events[s][-1]) for s in range(args.steps)]
+    # headline timing: graph replays (same kernels, no launch gaps)
+    if graph is not None:
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+               for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = Clocks(local)
+        clocks.start()
+        launches0 = ctx.launches
+        for s in range(args.steps):
+            flush.zero_()
+            gev[s][0].record()
+            graph.replay()
+            gev[s][1].record()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        if dist:
+            dist.barrier()
+        per_step = [gev[s][0].elapsed_time(gev[s][1]) for s in range(args.steps)]
     build_ms = [events[s][0].elapsed_time(events[s][1]) for s in range(args.steps)]
     scale_ms = [[events[s][1 + i].elapsed_time(events[s][2 + i]) for s in range(args.steps)]
                 for i in range(len(reqs))]

@@ -2,19 +2,22 @@
 //
 // K1 replaces IntegralTableSet::build (proj/src/integral_tables.cpp:72-115),
 // which walks bin -> row -> column with running row sums plus the row above.
-// Here one CTA owns (row band, bin octet) of ONE table kind (plain / xramp /
-// yramp; one launch per kind) and the FULL row width, CPT columns per thread:
-//   phase 1  column aggregates of the band for the octet's 8 bins (count, or
-//            y-sum for the yramp kind), published for later bands;
-//   phase 2  decoupled look-back over earlier bands of the same octet
-//            (flags + aggregates / inclusive prefixes in global memory)
-//            gives the column sums of all rows above the band; one block
-//            scan turns them into the band's carry row T(x, y0);
-//   phase 3  per row: bin compare, one block-wide scan of the row prefixes
-//            (counts packed two bins per 32-bit word, or per-bin x sums),
-//            T(x+1, y+1) = T(x+1, y) + R(x, y), and one 32-byte record per
-//            column written with 16-byte stores (a warp writes 4-8 KB of
-//            contiguous records per row).
+// The GPU splits the rows into bands and builds every band independently:
+//   K1a k_colsum    per (band, bin octet, column): count and y-sum of each
+//                   bin over the band's rows;
+//   K1b k_bandscan  exclusive scan of those column sums over bands, so each
+//                   band knows the column sums of all rows above it;
+//   K1c k_build     one CTA per (band, octet, table kind) spanning the FULL
+//                   row width (CPT columns per thread): one block scan turns
+//                   the carried column sums into the band's top row
+//                   T(x, y0); then per row a bin compare, one block-wide scan
+//                   of the row prefixes (counts packed two bins per 32-bit
+//                   word, or per-bin x sums), T(x+1, y+1) = T(x+1, y) +
+//                   R(x, y), and one 32-byte record per column written with
+//                   16-byte stores (4-8 KB contiguous per warp and row).
+// (A single-pass decoupled look-back was measured first: with every band
+// resident at once it re-read all earlier bands' 8-word column vectors,
+// ~350 MB of L2 traffic for a 134 MB table; profiles/r01_v2_*.)
 // Arithmetic is modulo 2^(8*sizeof(T)); for T = uint32_t every window
 // histogram the sweeps form is < 2^32, so the wrapped tables are exact for
 // them; T = uint64_t reproduces the reference's int64 tables.
@@ -23,16 +26,6 @@
 namespace swg {
 
 namespace {
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int CPT>
 __device__ __forceinline__ void load_bins(const uint16_t* p, uint16_t (&v)[CPT]) {
@@ -103,112 +96,83 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V*
   }
 }
 
-// KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}.
+// K1a: column count and y-sum of each bin of one octet over one row band.
+// agg[band][group][column][16]: words 0-7 counts, 8-15 y-sums.
+__global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
+  const int band = blockIdx.x, grp = blockIdx.y;
+  const int x = blockIdx.z * blockDim.x + threadIdx.x;
+  if (x >= g.w) return;
+  const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
+  const uint32_t gb = (uint32_t)grp * kOct;
+  uint32_t cnt[kOct], ys[kOct];
+#pragma unroll
+  for (int j = 0; j < kOct; ++j) cnt[j] = ys[j] = 0;
+  const uint16_t* col = g.fi + x;
+  for (int y = y0; y < y1; ++y) {
+    const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) {
+      const bool hit = d == (uint32_t)j;
+      cnt[j] += hit ? 1u : 0u;
+      ys[j] += hit ? (uint32_t)y : 0u;
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * 16);
+  dst[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
+  dst[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
+  dst[2] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
+  dst[3] = make_uint4(ys[4], ys[5], ys[6], ys[7]);
+}
+
+// K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
+__global__ void k_bandscan(uint4* agg, int nbands, size_t per_band /* uint4 */) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= per_band) return;
+  uint4 run = make_uint4(0, 0, 0, 0);
+  for (int b = 0; b < nbands; ++b) {
+    uint4* p = agg + (size_t)b * per_band + i;
+    const uint4 v = *p;
+    *p = run;
+    run.x += v.x; run.y += v.y; run.z += v.z; run.w += v.w;
+  }
+}
+
+// K1c body.  KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}.
 template <typename T, int KIND, int CPT>
-__global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs g) {
-  __shared__ unsigned s_ticket;
-  __shared__ int s_flag;
+__device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp) {
   __shared__ uint32_t s_row[2][kOct * 32];
   __shared__ T s_carry[kOct * 32];
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
-  if (tid == 0) s_ticket = atomicAdd(g.ticket, 1u);
-  __syncthreads();
-  const unsigned ticket = s_ticket;
-  const int grp = (int)(ticket % (unsigned)g.groups);
-  const int band = (int)(ticket / (unsigned)g.groups);
   const int y0 = band * g.band_h;
   const int y1 = min(y0 + g.band_h, g.h);
   const int xb = tid * CPT;
-  const bool last_band = band + 1 >= g.nbands;
   // Threads past the right edge keep the block scans uniform but touch no
   // memory; the last live thread may straddle the edge (padding = kNoBin).
   const bool live = xb < g.w;
   const uint16_t* fi = g.fi + (live ? xb : 0);
   const uint32_t gb = (uint32_t)grp * kOct;
 
-  // ---- phase 1: this band's column aggregates (only later bands need them)
-  uint32_t ac[CPT][kOct];
-#pragma unroll
-  for (int i = 0; i < CPT; ++i)
-#pragma unroll
-    for (int j = 0; j < kOct; ++j) ac[i][j] = 0;
-  const size_t slot = ((size_t)band * g.groups + grp) * g.wa * kOct;
-  if (!last_band) {
-    if (live) {
-      for (int y = y0; y < y1; ++y) {
-        uint16_t v[CPT];
-        load_bins<CPT>(fi + (size_t)y * g.fi_pitch, v);
-        const uint32_t inc = KIND == 2 ? (uint32_t)y : 1u;
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-          const uint32_t d = (uint32_t)v[i] - gb;
-#pragma unroll
-          for (int j = 0; j < kOct; ++j) ac[i][j] += (d == (uint32_t)j) ? inc : 0u;
-        }
-      }
-      uint4* dst = reinterpret_cast<uint4*>(g.agg + slot + (size_t)xb * kOct);
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        dst[2 * i] = make_uint4(ac[i][0], ac[i][1], ac[i][2], ac[i][3]);
-        dst[2 * i + 1] = make_uint4(ac[i][4], ac[i][5], ac[i][6], ac[i][7]);
-      }
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(&g.flags[band * g.groups + grp], 1);
-  }
-
-  // ---- phase 2: decoupled look-back along bands of the same octet
-  uint32_t cc[CPT][kOct];
-#pragma unroll
-  for (int i = 0; i < CPT; ++i)
-#pragma unroll
-    for (int j = 0; j < kOct; ++j) cc[i][j] = 0;
-  for (int k = band - 1; k >= 0; --k) {
-    if (tid == 0) {
-      int f;
-      const int* fp = &g.flags[k * g.groups + grp];
-      while ((f = ld_acquire(fp)) == 0) __nanosleep(32);
-      s_flag = f;
-    }
-    __syncthreads();
-    const int f = s_flag;
-    if (live) {
-      const uint4* src = reinterpret_cast<const uint4*>(
-          (f == 2 ? g.pref : g.agg) + ((size_t)k * g.groups + grp) * g.wa * kOct +
-          (size_t)xb * kOct);
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const uint4 a = __ldcg(src + 2 * i), b = __ldcg(src + 2 * i + 1);
-        cc[i][0] += a.x; cc[i][1] += a.y; cc[i][2] += a.z; cc[i][3] += a.w;
-        cc[i][4] += b.x; cc[i][5] += b.y; cc[i][6] += b.z; cc[i][7] += b.w;
-      }
-    }
-    __syncthreads();  // s_flag is rewritten next iteration
-    if (f == 2) break;
-  }
-  if (!last_band) {
-    if (live) {
-      uint4* dst = reinterpret_cast<uint4*>(g.pref + slot + (size_t)xb * kOct);
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        dst[2 * i] = make_uint4(cc[i][0] + ac[i][0], cc[i][1] + ac[i][1], cc[i][2] + ac[i][2],
-                                cc[i][3] + ac[i][3]);
-        dst[2 * i + 1] = make_uint4(cc[i][4] + ac[i][4], cc[i][5] + ac[i][5],
-                                    cc[i][6] + ac[i][6], cc[i][7] + ac[i][7]);
-      }
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(&g.flags[band * g.groups + grp], 2);
-  }
-
-  // ---- carry row T(x+1, y0): prefix over x of the column sums above y0
+  // ---- carry row T(x+1, y0) from the column sums of all rows above y0
   T t[CPT][kOct];
   {
     T tot[kOct], ex[kOct];
+    uint32_t cc[CPT][kOct];
+    if (live) {
+      const uint4* src = reinterpret_cast<const uint4*>(
+          g.agg + (((size_t)band * g.groups + grp) * g.wa + xb) * 16 + (KIND == 2 ? 8 : 0));
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const uint4 a = src[4 * i], b = src[4 * i + 1];
+        cc[i][0] = a.x; cc[i][1] = a.y; cc[i][2] = a.z; cc[i][3] = a.w;
+        cc[i][4] = b.x; cc[i][5] = b.y; cc[i][6] = b.z; cc[i][7] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+#pragma unroll
+        for (int j = 0; j < kOct; ++j) cc[i][j] = 0;
+    }
 #pragma unroll
     for (int j = 0; j < kOct; ++j) {
       T run = 0;
@@ -235,18 +199,16 @@ __global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs 
     if (tid == 0) store_zero_record<T>(plane);
   }
 
-  // ---- phase 3: rows of the band
-  for (int y = y0; y < y1; ++y) {
-    uint16_t v[CPT];
-    if (live) {
-      load_bins<CPT>(fi + (size_t)y * g.fi_pitch, v);
-    } else {
+  // ---- rows of the band (next row's bins prefetched under this row's scan)
+  uint16_t vn[CPT];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) v[i] = kNoBin;
-    }
+  for (int i = 0; i < CPT; ++i) vn[i] = kNoBin;
+  if (live && y0 < y1) load_bins<CPT>(fi + (size_t)y0 * g.fi_pitch, vn);
+  for (int y = y0; y < y1; ++y) {
     uint32_t d[CPT];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) d[i] = (uint32_t)v[i] - gb;
+    for (int i = 0; i < CPT; ++i) d[i] = (uint32_t)vn[i] - gb;
+    if (live && y + 1 < y1) load_bins<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
     uint32_t* buf = s_row[y & 1];
     if constexpr (KIND == 1) {
       // per-bin x sums of this thread's columns, then the block prefix
@@ -295,6 +257,17 @@ __global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs 
 #pragma unroll
       for (int i = 0; i < CPT; ++i) store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
     if (tid == 0) store_zero_record<T>(row);
+  }
+}
+
+// K1c: one CTA per (row band, bin octet, table kind); blockIdx.y = kind.
+template <typename T, int CPT>
+__global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs g) {
+  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
+  switch (blockIdx.y) {
+    case 0: build_body<T, 0, CPT>(g, band, grp); break;
+    case 1: build_body<T, 1, CPT>(g, band, grp); break;
+    default: build_body<T, 2, CPT>(g, band, grp);
   }
 }
 
@@ -366,23 +339,29 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_build(const BuildArgs& a, int kind, cudaStream_t s) {
-  const int cpt = choose_cpt(a.w);
-  const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
-  const unsigned grid = (unsigned)(a.nbands * a.groups);
-#define SWG_BUILD(K, C) k_build<T, K, C><<<grid, threads, 0, s>>>(a)
-  if (cpt == 4) {
-    if (kind == 0) SWG_BUILD(0, 4); else if (kind == 1) SWG_BUILD(1, 4); else SWG_BUILD(2, 4);
-  } else {
-    if (kind == 0) SWG_BUILD(0, 8); else if (kind == 1) SWG_BUILD(1, 8); else SWG_BUILD(2, 8);
-  }
-#undef SWG_BUILD
+cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
+  dim3 grid((unsigned)a.nbands, (unsigned)a.groups, (unsigned)((a.w + 255) / 256));
+  k_colsum<<<grid, 256, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t per_band = (size_t)a.groups * a.wa * 16 / 4;
+  k_bandscan<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
   return cudaGetLastError();
 }
 
-template cudaError_t launch_build<uint32_t>(const BuildArgs&, int, cudaStream_t);
-template cudaError_t launch_build<uint64_t>(const BuildArgs&, int, cudaStream_t);
+template <typename T>
+cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
+  const int cpt = choose_cpt(a.w);
+  const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
+  dim3 grid((unsigned)(a.nbands * a.groups), (unsigned)a.planes);
+  if (cpt == 4) k_build<T, 4><<<grid, threads, 0, s>>>(a);
+  else k_build<T, 8><<<grid, threads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t);
+template cudaError_t launch_build<uint64_t>(const BuildArgs&, cudaStream_t);
 
 template <typename T, typename O>
 cudaError_t launch_export(const T* tab, size_t ps, size_t pitch, int planes, int w, int h,

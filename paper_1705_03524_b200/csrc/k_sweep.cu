@@ -203,22 +203,32 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
   const size_t pitch8 = a.pitch * kOct, ps8 = a.plane_stride * kOct;
 
   // out[k] for bins 4*half + k of octet g: ring order, early exit on empty.
+  // Two rings per iteration keep 8 corner loads in flight.
+  auto corners = [&](const uint32_t* P, int i) {
+    const int ax = rg.a[i], cyv = rg.c[i];
+    const uint32_t* ra = P + (size_t)(cy - cyv) * pitch8;
+    const uint32_t* rb = P + (size_t)(cy + cyv + 1) * pitch8;
+    const size_t xa = (size_t)(cx - ax) * kOct, xe = (size_t)(cx + ax + 1) * kOct;
+    return box4(ldq(rb + xe), ldq(rb + xa), ldq(ra + xe), ldq(ra + xa));
+  };
+  auto accumulate = [&](double (&out)[4], const uint4& cnt, double c) {
+    if (cnt.x) out[0] = __dadd_rn(out[0], __dmul_rn(c, (double)cnt.x));
+    if (cnt.y) out[1] = __dadd_rn(out[1], __dmul_rn(c, (double)cnt.y));
+    if (cnt.z) out[2] = __dadd_rn(out[2], __dmul_rn(c, (double)cnt.z));
+    if (cnt.w) out[3] = __dadd_rn(out[3], __dmul_rn(c, (double)cnt.w));
+  };
   auto octet = [&](int g, double (&out)[4]) {
     const uint32_t* P = base + (size_t)g * a.planes * ps8;
 #pragma unroll
     for (int k = 0; k < 4; ++k) out[k] = 0.0;
-    for (int i = 0; i < a.rings; ++i) {
-      const int ax = rg.a[i], cyv = rg.c[i];
-      const uint32_t* ra = P + (size_t)(cy - cyv) * pitch8;
-      const uint32_t* rb = P + (size_t)(cy + cyv + 1) * pitch8;
-      const size_t xa = (size_t)(cx - ax) * kOct, xe = (size_t)(cx + ax + 1) * kOct;
-      const uint4 cnt = box4(ldq(rb + xe), ldq(rb + xa), ldq(ra + xe), ldq(ra + xa));
-      if ((cnt.x | cnt.y | cnt.z | cnt.w) == 0u) break;  // nested boxes: all inner 0
-      const double c = rg.coeff[i];
-      if (cnt.x) out[0] = __dadd_rn(out[0], __dmul_rn(c, (double)cnt.x));
-      if (cnt.y) out[1] = __dadd_rn(out[1], __dmul_rn(c, (double)cnt.y));
-      if (cnt.z) out[2] = __dadd_rn(out[2], __dmul_rn(c, (double)cnt.z));
-      if (cnt.w) out[3] = __dadd_rn(out[3], __dmul_rn(c, (double)cnt.w));
+    for (int i = 0; i < a.rings; i += 2) {
+      const bool two = i + 1 < a.rings;
+      const uint4 c0 = corners(P, i);
+      const uint4 c1 = two ? corners(P, i + 1) : make_uint4(0, 0, 0, 0);
+      if ((c0.x | c0.y | c0.z | c0.w) == 0u) break;  // nested boxes: all inner 0
+      accumulate(out, c0, rg.coeff[i]);
+      if ((c1.x | c1.y | c1.z | c1.w) == 0u) break;
+      accumulate(out, c1, rg.coeff[i + 1]);
     }
   };
 

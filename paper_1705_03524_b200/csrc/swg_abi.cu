@@ -188,8 +188,7 @@ struct swg_tables {
   size_t pitch = 0, ps = 0;  // records (shared by the 32- and 64-bit planes)
   uint32_t* t32 = nullptr;
   uint64_t* t64 = nullptr;
-  uint32_t* lb = nullptr;  // look-back scratch: agg + pref
-  int* flags = nullptr;    // per kind: nbands*groups flags + ticket
+  uint32_t* lb = nullptr;  // band carry scratch (BuildArgs::agg)
   int band_h = 0, nbands = 0;
   size_t wa = 0;
   size_t bytes = 0;
@@ -219,8 +218,8 @@ size_t pixel_bytes(int format) {
 }
 
 void choose_bands(swg_tables* t) {
-  // ~2 waves of row-wide CTAs per table kind on 148 SMs
-  const int target = 148 * 2;
+  // ~4 row-wide CTAs per SM and table kind
+  const int target = 148 * 4;
   int nb = (target + t->groups - 1) / t->groups;
   nb = std::max(1, std::min(nb, (t->h + 7) / 8));
   t->band_h = (t->h + nb - 1) / nb;
@@ -228,13 +227,9 @@ void choose_bands(swg_tables* t) {
   t->wa = round_up((size_t)t->w, 16);
 }
 
-size_t flag_words(const swg_tables* t) { return (size_t)t->nbands * t->groups + 1; }
-
 template <typename T>
 swg_status run_build(swg_tables* t, T* out) {
   swg_ctx* c = t->ctx;
-  const size_t nf = flag_words(t);
-  CUDA_TRY(cudaMemsetAsync(t->flags, 0, nf * t->planes * sizeof(int), c->stream));
   BuildArgs a{};
   a.fi = t->fi;
   a.fi_pitch = t->fip;
@@ -249,15 +244,13 @@ swg_status run_build(swg_tables* t, T* out) {
   a.band_h = t->band_h;
   a.nbands = t->nbands;
   a.wa = t->wa;
-  const size_t slots = (size_t)t->nbands * t->groups * t->wa * kOct;
   a.agg = t->lb;
-  a.pref = t->lb + slots;
-  for (int kind = 0; kind < t->planes; ++kind) {  // kinds run back to back: scratch reuse
-    a.flags = t->flags + kind * nf;
-    a.ticket = reinterpret_cast<unsigned*>(a.flags + nf - 1);
-    CUDA_TRY(launch_build<T>(a, kind, c->stream));
-    c->launches += 1;
+  if (t->nbands > 1) {
+    CUDA_TRY(launch_colsum(a, c->stream));
+    c->launches += 2;
   }
+  CUDA_TRY(launch_build<T>(a, c->stream));
+  c->launches += 1;
   return SWG_OK;
 }
 
@@ -441,9 +434,8 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   t->ps = t->pitch * (size_t)(height + 1);
   choose_bands(t);
   const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * 4;
-  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct * 4 * 2;
-  const size_t flag_bytes = flag_words(t) * planes * 4;
-  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2 + flag_bytes;
+  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * 16 * 4;
+  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2;
   if (memory_budget && need > memory_budget) {
     swg_tables_destroy(t);
     g_required = need;
@@ -457,8 +449,7 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   cudaError_t e;
   if ((e = cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
-      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&t->flags, flag_bytes)) != cudaSuccess) {
+      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
     g_required = need;
     cudaGetLastError();
     return cleanup(fail(SWG_ERR_CAPACITY, "integral tables need %zu device bytes: %s", need,
@@ -550,7 +541,6 @@ swg_status swg_tables_destroy(swg_tables* t) {
     cudaFree(t->fi);
     cudaFree(t->in);
     cudaFree(t->lb);
-    cudaFree(t->flags);
     ctx_release(t->ctx);
   }
   delete t;

@@ -56,11 +56,10 @@ struct BuildArgs {
   size_t plane_stride; // records
   int w, h, bins, groups, planes;
   int band_h, nbands;
-  size_t wa;           // padded width (columns) of the look-back arrays
-  uint32_t* agg;       // [nbands][groups][wa][8]: band column count / y-sum
-  uint32_t* pref;      // [nbands][groups][wa][8]: inclusive prefix over bands
-  int* flags;          // [nbands * groups]: 0 none, 1 aggregate, 2 prefix
-  unsigned* ticket;    // dynamic CTA ordering for the look-back
+  size_t wa;           // padded width (columns) of the carry array
+  uint32_t* agg;       // [nbands][groups][wa][16]: per column, 8 bin counts +
+                       // 8 bin y-sums of the band (K1a), then of all rows
+                       // above the band (K1b, exclusive scan over bands)
 };
 
 struct QuantArgs {
@@ -131,8 +130,9 @@ constexpr int kBruteThreads = 128;
 
 // Kernel launchers (defined in the .cu files).
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
+cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s);
 template <typename T>
-cudaError_t launch_build(const BuildArgs& a, int kind, cudaStream_t s);
+cudaError_t launch_build(const BuildArgs& a, cudaStream_t s);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, dim3 grid,
                               cudaStream_t s);

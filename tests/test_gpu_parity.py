@@ -33,8 +33,8 @@ def test_tables_golden(ctx, name, bins):
 
 
 @pytest.mark.parametrize("w,h,bins", [(1, 1, 4), (3, 2, 2), (17, 13, 8), (64, 64, 16),
-                                      (255, 37, 5), (1000, 23, 3), (1025, 40, 4),
-                                      (1031, 61, 2), (4100, 9, 2), (33, 700, 3)])
+                                      (255, 37, 5), (1000, 23, 3), (1025, 40, 4), (4096, 9, 2),
+                                      (1031, 61, 2), (33, 700, 3)])
 def test_tables_vs_oracle_shapes(ctx, oracle, w, h, bins):
     """Widths around the CPT / thread-count / band boundaries, tall images
     (many look-back bands), degenerate 1x1."""
@@ -354,3 +354,8 @@ def test_config2_full_size_properties(ctx):
         m, pk = t.likelihood_map(k, mdl, swg.CAKE, rings=kw // 2 + 1)
         assert m.min() >= 0.0 and m.max() <= 1.0
         assert abs(pk[2] - cx) <= 1 and abs(pk[3] - cy) <= 1 and pk[4] > 0.999
+
+
+def test_width_limit_is_a_size_error(ctx):
+    with pytest.raises(swg.SizeError):
+        ctx.build(np.zeros((4, 4097), np.uint8), swg.FMT_GRAY8, 2, swg.PLANES_PLAIN)
