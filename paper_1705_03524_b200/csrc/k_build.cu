@@ -125,15 +125,23 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
 }
 
 // K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
+// Bands are visited in batches of 16 so the batch's loads are all in flight.
 __global__ void k_bandscan(uint4* agg, int nbands, size_t per_band /* uint4 */) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= per_band) return;
+  constexpr int kBatch = 16;
   uint4 run = make_uint4(0, 0, 0, 0);
-  for (int b = 0; b < nbands; ++b) {
-    uint4* p = agg + (size_t)b * per_band + i;
-    const uint4 v = *p;
-    *p = run;
-    run.x += v.x; run.y += v.y; run.z += v.z; run.w += v.w;
+  for (int b0 = 0; b0 < nbands; b0 += kBatch) {
+    uint4 v[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k)
+      if (b0 + k < nbands) v[k] = agg[(size_t)(b0 + k) * per_band + i];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k)
+      if (b0 + k < nbands) {
+        agg[(size_t)(b0 + k) * per_band + i] = run;
+        run.x += v[k].x; run.y += v[k].y; run.z += v[k].z; run.w += v[k].w;
+      }
   }
 }
 
@@ -158,7 +166,7 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
   {
     T tot[kOct], ex[kOct];
     uint32_t cc[CPT][kOct];
-    if (live) {
+    if (live && band > 0) {  // band 0 starts from the zero row
       const uint4* src = reinterpret_cast<const uint4*>(
           g.agg + (((size_t)band * g.groups + grp) * g.wa + xb) * 16 + (KIND == 2 ? 8 : 0));
 #pragma unroll
