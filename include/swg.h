@@ -21,7 +21,7 @@
  * Error behaviour: one status code per reference exception class
  * (include/swih/errors.hpp:10-79); the message is kept per thread
  * (swg_last_error) together with CapacityError::required_bytes
- * (swg_last_required_bytes).  The C++ drop-in layer (include/swih/*.hpp)
+ * (swg_last_required_bytes).  The C++ drop-in layer (include/swih/ headers)
  * rethrows the matching class.
  *
  * Threading: a context owns one CUDA stream on one device; calls on one
@@ -209,6 +209,22 @@ swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
  * and the ring weight (WeddingCakePlan::shrink_x/shrink_y/ring_weight). */
 swg_status swg_cake_plan(const swg_kernel* kernel, int rings, int ring_rule,
                          int* shrink_x, int* shrink_y, double* ring_weight);
+
+/* Quantise an image on the device (quantize_image, image.cpp:34-40, and
+ * the declared uint16 / RGB forms); out: w*h uint16 bins. */
+swg_status swg_quantize(swg_ctx* ctx, const void* pixels, int width, int height,
+                        int format, int bins, uint16_t* host_out);
+/* Brute-force weighted histograms of a host feature image at n centres
+ * (BruteForcePlan::counts_into / weights_into, baselines.cpp:24-69):
+ * integer kernels -> exact int64 counts in out_i64 (out_f64 may be NULL);
+ * any kernel -> fp64 sums in row-major pixel order in out_f64. */
+swg_status swg_brute_windows(swg_ctx* ctx, const uint16_t* fi, int width, int height,
+                             int bins, int n, const int* cx, const int* cy,
+                             const swg_kernel* kernel, int border, int64_t* out_i64,
+                             double* out_f64);
+/* Peak of a host likelihood map (peak, matching.cpp:211-223). */
+swg_status swg_map_peak(swg_ctx* ctx, const double* scores, int map_width,
+                        int map_height, int hx, int hy, swg_peak* out);
 
 /* ---- likelihood maps ------------------------------------------------- */
 /* Full strict likelihood map(s) + peak(s).  For request i:

@@ -39,6 +39,45 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+CPP_DIR = os.path.join(PKG, "cpp")
+CPP_SOURCES = ["core.cpp", "tables.cpp", "engine.cpp", "matching.cpp"]
+CPP_LIB = os.path.join(LIBDIR, "libswih_b200.so")
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra",
+             "-I" + os.path.join(ROOT, "include"), "-I" + CPP_DIR]
+
+
+def build_cpp(verbose: bool = False, force: bool = False) -> str:
+    """The reference-compatible C++ API (include/swih/*.hpp) over libswg."""
+    build(verbose, force)
+    hdrs = [os.path.join(ROOT, "include", "swih", h)
+            for h in os.listdir(os.path.join(ROOT, "include", "swih"))]
+    srcs = [os.path.join(CPP_DIR, s) for s in CPP_SOURCES] + [os.path.join(CPP_DIR, "runtime.hpp")]
+    if force or _stale(CPP_LIB, srcs + hdrs + [LIB]):
+        cmd = [CXX, *CXX_FLAGS, "-shared", *[os.path.join(CPP_DIR, s) for s in CPP_SOURCES],
+               "-o", CPP_LIB, "-L" + LIBDIR, "-lswg", "-Wl,-rpath,$ORIGIN"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return CPP_LIB
+
+
+def build_cpp_tests(verbose: bool = False) -> str:
+    """tests/cpp/test_api.cpp against libswih_b200.so (binary in tests/cpp/build)."""
+    build_cpp(verbose)
+    tdir = os.path.join(ROOT, "tests", "cpp")
+    out = os.path.join(tdir, "build", "test_api")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    deps = [os.path.join(tdir, "test_api.cpp"), os.path.join(tdir, "minitest.hpp"), CPP_LIB]
+    if _stale(out, deps):
+        cmd = [CXX, *CXX_FLAGS, os.path.join(tdir, "test_api.cpp"), "-o", out,
+               "-L" + LIBDIR, "-lswih_b200", "-lswg", "-Wl,-rpath," + LIBDIR, "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     objdir = os.path.join(PKG, "build")
@@ -65,5 +104,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
+    build_cpp(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
+    if "--tests" in sys.argv:
+        print(build_cpp_tests(verbose="--verbose" in sys.argv))
     print(LIB)
+    print(CPP_LIB)

@@ -111,7 +111,42 @@ __global__ void __launch_bounds__(kBruteThreads) k_sweep_brute(const SweepArgs a
                a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+// Brute-force histograms of explicit windows: one thread per window walks
+// the window's pixels in row-major order (baselines.cpp:24-69), skipping
+// pixels outside the image (Clipped) and accumulating into its own row of
+// the output (int64 counts for integer kernels, fp64 sums otherwise).
+__global__ void k_brute_query(const BruteQueryArgs a) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= a.n) return;
+  const int hx = (a.kw - 1) / 2, hy = (a.kh - 1) / 2;
+  const int cx = a.cx[w], cy = a.cy[w];
+  long long* oi = a.out_i64 ? a.out_i64 + (size_t)w * a.bins : nullptr;
+  double* od = a.out_f64 ? a.out_f64 + (size_t)w * a.bins : nullptr;
+  for (int b = 0; b < a.bins; ++b) {
+    if (oi) oi[b] = 0;
+    if (od) od[b] = 0.0;
+  }
+  for (int dy = -hy; dy <= hy; ++dy) {
+    const int y = cy + dy;
+    if (y < 0 || y >= a.h) continue;
+    for (int dx = -hx; dx <= hx; ++dx) {
+      const int x = cx + dx;
+      if (x < 0 || x >= a.w) continue;
+      const int bin = a.fi[(size_t)y * a.w + x];
+      if (bin >= a.bins) continue;
+      const double wt = a.grid[(size_t)(dy + hy) * a.kw + (dx + hx)];
+      if (oi) oi[bin] += (long long)wt;
+      if (od) od[bin] = __dadd_rn(od[bin], wt);
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_brute_query(const BruteQueryArgs& a, cudaStream_t s) {
+  k_brute_query<<<(a.n + 127) / 128, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
                                cudaStream_t s) {

@@ -111,7 +111,7 @@ __device__ __forceinline__ void add_octet(const double (&val)[4], const double (
 
 // K2a: Uniform (4 cells per bin) or Manhattan (20 cells per bin).
 template <int SIM, bool UNIFORM>
-__global__ void __launch_bounds__(kSweepThreads, 3) k_sweep_affine(const SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
   const int r0 = blockIdx.y * kSweepTileY + warp;
@@ -296,6 +296,21 @@ __global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int
   }
 }
 
+// Argmax of a map held in device memory: CTA candidates (tie rule).
+__global__ void __launch_bounds__(256) k_map_peak(const double* sc, size_t n, PeakPart* parts) {
+  double best = -2.0;
+  long long bi = 0x7FFFFFFFFFFFFFFFLL;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double v = sc[i];
+    if (better(v, (long long)i, best, bi)) {
+      best = v;
+      bi = (long long)i;
+    }
+  }
+  block_peak(best, bi, parts + blockIdx.x);
+}
+
 // Window queries from explicit quadrant terms (engine.cpp:39-79 semantics).
 template <typename T>
 __global__ void k_query(const QueryArgs a) {
@@ -346,6 +361,14 @@ __global__ void k_cake_query(const QueryArgs a) {
 }
 
 }  // namespace
+
+cudaError_t launch_map_peak(const double* scores, size_t n, int mw, int hx, int hy,
+                            PeakPart* parts, int nparts, swg_peak* out, cudaStream_t s) {
+  k_map_peak<<<nparts, 256, 0, s>>>(scores, n, parts);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_peak_reduce(parts, nparts, mw, hx, hy, out, s);
+}
 
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) {

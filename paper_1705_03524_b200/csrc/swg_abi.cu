@@ -173,7 +173,7 @@ struct swg_ctx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
-  DevBuf parts, scores, peaks, terms, qout, grid;
+  DevBuf parts, scores, peaks, terms, qout, grid, io;
 };
 
 struct swg_tables {
@@ -356,6 +356,7 @@ static void ctx_release(swg_ctx* c) {
     c->terms.release();
     c->qout.release();
     c->grid.release();
+    c->io.release();
     cudaStreamDestroy(c->own);
   }
   delete c;
@@ -818,6 +819,94 @@ swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
   CUDA_TRY(launch_cake_query(a, c->stream));
   c->launches += 1;
   CUDA_TRY(cudaMemcpyAsync(out, c->qout.p, ob, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_quantize(swg_ctx* c, const void* pixels, int w, int h, int format, int bins,
+                        uint16_t* out) {
+  if (!c || !pixels || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  if (w < 1 || h < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
+  if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
+  if (bins < 1) return fail(SWG_ERR, "Quantizer: bin count must be >= 1");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  const size_t in_bytes = (size_t)w * h * pixel_bytes(format);
+  const size_t in_pad = round_up(in_bytes, 256);
+  ST_TRY(c->io.ensure(in_pad + (size_t)w * h * 2));
+  uint8_t* din = static_cast<uint8_t*>(c->io.p);
+  uint16_t* dout = reinterpret_cast<uint16_t*>(din + in_pad);
+  CUDA_TRY(cudaMemcpyAsync(din, pixels, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  QuantArgs q{din, (size_t)w * pixel_bytes(format), w, h, format, bins, dout, (size_t)w};
+  CUDA_TRY(launch_quantize(q, c->stream));
+  c->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)w * h * 2, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_brute_windows(swg_ctx* c, const uint16_t* fi, int w, int h, int bins, int n,
+                             const int* cx, const int* cy, const swg_kernel* k, int border,
+                             int64_t* out_i64, double* out_f64) {
+  if (!c || !fi || !k || (n && (!cx || !cy))) return fail(SWG_ERR_ARG, "NULL argument");
+  if (!out_i64 && !out_f64) return fail(SWG_ERR_ARG, "no output");
+  ST_TRY(validate_kernel(*k));
+  if (out_i64 && !k_integer(*k))
+    return fail(SWG_ERR_INVALID_KERNEL, "brute force counts: kernel weights are not integers");
+  for (int i = 0; i < n; ++i) ST_TRY(validate_window(w, h, cx[i], cy[i], *k, border));
+  if (n == 0) return SWG_OK;
+  std::vector<double> wgrid((size_t)k->kw * k->kh);
+  const int hx = k_hx(*k), hy = k_hy(*k);
+  for (int dy = -hy; dy <= hy; ++dy)
+    for (int dx = -hx; dx <= hx; ++dx) {
+      double v = weight_at(*k, dx, dy);
+      if (out_i64) v = (double)std::llround(v);  // BruteForcePlan grid_i (baselines.cpp:18-20)
+      wgrid[(size_t)(dy + hy) * k->kw + dx + hx] = v;
+    }
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  const size_t fb = round_up((size_t)w * h * 2, 256), cb = round_up((size_t)n * 4, 256);
+  const size_t gb = round_up(wgrid.size() * 8, 256), ob = (size_t)n * bins * 8;
+  ST_TRY(c->io.ensure(fb + 2 * cb + gb + 2 * ob));
+  char* base = static_cast<char*>(c->io.p);
+  uint16_t* dfi = reinterpret_cast<uint16_t*>(base);
+  int* dcx = reinterpret_cast<int*>(base + fb);
+  int* dcy = reinterpret_cast<int*>(base + fb + cb);
+  double* dgrid = reinterpret_cast<double*>(base + fb + 2 * cb);
+  long long* di = reinterpret_cast<long long*>(base + fb + 2 * cb + gb);
+  double* dd = reinterpret_cast<double*>(base + fb + 2 * cb + gb + ob);
+  CUDA_TRY(cudaMemcpyAsync(dfi, fi, (size_t)w * h * 2, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dcx, cx, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dcy, cy, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dgrid, wgrid.data(), wgrid.size() * 8, cudaMemcpyHostToDevice,
+                           c->stream));
+  BruteQueryArgs a{dfi, w, h, bins, n, dcx, dcy, dgrid, k->kw, k->kh, border,
+                   out_i64 != nullptr, out_i64 ? di : nullptr, out_f64 ? dd : nullptr};
+  CUDA_TRY(launch_brute_query(a, c->stream));
+  c->launches += 1;
+  if (out_i64) CUDA_TRY(cudaMemcpyAsync(out_i64, di, ob, cudaMemcpyDeviceToHost, c->stream));
+  if (out_f64) CUDA_TRY(cudaMemcpyAsync(out_f64, dd, ob, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_map_peak(swg_ctx* c, const double* scores, int mw, int mh, int hx, int hy,
+                        swg_peak* out) {
+  if (!c || !scores || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  if (mw < 1 || mh < 1) return fail(SWG_ERR, "peak: empty likelihood map");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  const size_t n = (size_t)mw * mh;
+  const int nparts = (int)std::min<size_t>((n + 255) / 256, 148 * 4);
+  ST_TRY(c->io.ensure(round_up(n * 8, 256)));
+  ST_TRY(c->parts.ensure((size_t)nparts * sizeof(PeakPart)));
+  ST_TRY(c->peaks.ensure(sizeof(swg_peak)));
+  CUDA_TRY(cudaMemcpyAsync(c->io.p, scores, n * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_map_peak(static_cast<const double*>(c->io.p), n, mw, hx, hy,
+                           static_cast<PeakPart*>(c->parts.p), nparts,
+                           static_cast<swg_peak*>(c->peaks.p), c->stream));
+  c->launches += 2;
+  CUDA_TRY(cudaMemcpyAsync(out, c->peaks.p, sizeof(swg_peak), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return SWG_OK;
 }

@@ -150,5 +150,19 @@ cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int ki
                               uint64_t* tab, size_t ps, size_t pitch, int planes,
                               cudaStream_t s);
 cudaError_t launch_narrow(const uint64_t* src, uint32_t* dst, size_t n, cudaStream_t s);
+// Brute-force histograms of explicit windows (API queries).
+struct BruteQueryArgs {
+  const uint16_t* fi;  // w*h, tight rows
+  int w, h, bins, n;
+  const int* cx;
+  const int* cy;
+  const double* grid;  // kh x kw weights
+  int kw, kh, border, integer;
+  long long* out_i64;  // n x bins (integer kernels)
+  double* out_f64;     // n x bins
+};
+cudaError_t launch_brute_query(const BruteQueryArgs& a, cudaStream_t s);
+cudaError_t launch_map_peak(const double* scores, size_t n, int mw, int hx, int hy,
+                            PeakPart* parts, int nparts, swg_peak* out, cudaStream_t s);
 
 }  // namespace swg

@@ -1,0 +1,127 @@
+"""Multi-GPU partitioning of the SWIH hot path.
+
+One process per GPU; torch.distributed (NCCL on the box, gloo in the CPU
+tests) carries the few small exchanges.  The path partitions without a
+data-path collective:
+
+* frames       — `frame_shards`: frames of a batch round-robin over ranks.
+* row bands    — `row_bands`: rank r owns map rows [v0, v1) and receives
+                 pixel rows [v0, v1 + kh - 1) (an input halo).  Window
+                 histograms do not depend on the crop, so its local tables
+                 give bit-identical map rows with no table exchange.
+* global IH    — `band_carry` / `globalize_band_tables`: to export the GLOBAL
+                 integral tables from row bands, every rank all-gathers its
+                 band's last prefix row ((W+1)*b*3 values) and adds the sum of
+                 the earlier bands' rows — the boundary prefix-row exchange.
+                 y-ramps also shift by y0 * plain (local y = global y - y0).
+* peak         — `gather_peak`: all-gather of each rank's (score, global
+                 row-major index) and the reference tie rule
+                 (matching.cpp:211-223): max score, then smallest index.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Band:
+    rank: int
+    map_rows: Tuple[int, int]    # [v0, v1) of the strict map
+    pixel_rows: Tuple[int, int]  # [y0, y1) of the image this rank needs
+
+
+def frame_shards(n_frames: int, world: int, rank: int) -> List[int]:
+    return list(range(rank, n_frames, world))
+
+
+def row_bands(height: int, kh: int, world: int) -> List[Band]:
+    """Split the strict map of an image of `height` rows (kernel height kh)
+    into `world` contiguous, near-equal row bands."""
+    mh = height - kh + 1
+    if mh < 1:
+        raise ValueError("kernel taller than the image")
+    out = []
+    for r in range(world):
+        v0 = r * mh // world
+        v1 = (r + 1) * mh // world
+        out.append(Band(r, (v0, v1), (v0, v1 + kh - 1 if v1 > v0 else v0)))
+    return out
+
+
+def table_bands(height: int, world: int) -> List[Tuple[int, int]]:
+    """Pixel-row bands [y0, y1) covering the image, for a banded IH build."""
+    return [(r * height // world, (r + 1) * height // world) for r in range(world)]
+
+
+def band_carry(last_rows: Sequence[np.ndarray], rank: int) -> np.ndarray:
+    """Exclusive sum of the earlier bands' last prefix rows."""
+    carry = np.zeros_like(last_rows[0])
+    for r in range(rank):
+        carry = carry + last_rows[r]
+    return carry
+
+
+def globalize_band_tables(local: Tuple[np.ndarray, np.ndarray, np.ndarray], y0: int,
+                          carry: np.ndarray) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Local int64 tables of pixel rows [y0, y0+h) (bins, h+1, W+1), zero at
+    their own row 0 -> global tables rows y0 .. y0+h.  carry: (3, bins, W+1),
+    the global prefix row at y0 of (plain, xramp, yramp)."""
+    p, x, y = local
+    gp = p + carry[0][:, None, :]
+    gx = x + carry[1][:, None, :]
+    gy = y + np.int64(y0) * p + carry[2][:, None, :]
+    return gp, gx, gy
+
+
+def last_rows(local: Tuple[np.ndarray, np.ndarray, np.ndarray], y0: int) -> np.ndarray:
+    """This band's contribution to the prefix row below it: (3, bins, W+1)."""
+    p, x, y = local
+    return np.stack([p[:, -1, :], x[:, -1, :], y[:, -1, :] + np.int64(y0) * p[:, -1, :]])
+
+
+def exchange_last_rows(mine: np.ndarray, group=None) -> List[np.ndarray]:
+    """all_gather of every band's last prefix row (the boundary exchange)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(mine))
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    return [q.cpu().numpy() for q in parts]
+
+
+def better(a: Tuple[float, int], b: Tuple[float, int]) -> bool:
+    """Reference tie rule: higher score, then smaller row-major index."""
+    return a[0] > b[0] or (a[0] == b[0] and a[1] < b[1])
+
+
+def reduce_peaks(cands: Sequence[Tuple[float, int]]) -> Tuple[float, int]:
+    best = (-2.0, 1 << 62)
+    for c in cands:
+        if better(c, best):
+            best = c
+    return best
+
+
+def gather_peak(score: float, index: int, map_width: int, hx: int, hy: int,
+                group=None) -> Optional[tuple]:
+    """Global peak over ranks: (map_x, map_y, center_x, center_y, score)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    # the score travels as its IEEE bits so the comparison stays exact
+    bits = np.array([score], np.float64).view(np.int64)[0]
+    mine = torch.tensor([int(bits), int(index)], dtype=torch.int64, device=dev)
+    parts = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, mine, group=group)
+    cands = []
+    for p in parts:
+        b, i = p.cpu().tolist()
+        cands.append((float(np.array([b], np.int64).view(np.float64)[0]), int(i)))
+    s, i = reduce_peaks(cands)
+    u, v = i % map_width, i // map_width
+    return (u, v, u + hx, v + hy, s)

@@ -1,0 +1,88 @@
+"""Multi-GPU host logic on CPU with gloo, world_size 2:
+row-band maps == full map, boundary prefix-row exchange rebuilds the global
+integral tables exactly, and the peak gather applies the reference tie rule.
+The oracle stands in for each rank's GPU work here; on the box the same
+functions run with NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1705_03524_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        orc = O.Oracle()
+        img = orc.random_gray(57, 83, 4)
+        bins = 8
+        fi = orc.quantize_gray8(img, bins)
+        # --- banded IH build + boundary prefix-row exchange
+        y0, y1 = D.table_bands(83, world)[rank]
+        local = orc.build_tables(np.ascontiguousarray(fi[y0:y1]), bins)
+        rows = D.exchange_last_rows(D.last_rows(local, y0))
+        glob = D.globalize_band_tables(local, y0, D.band_carry(rows, rank))
+        full = orc.build_tables(fi, bins)
+        ok_tables = all((g == f[:, y0:y1 + 1, :]).all() for g, f in zip(glob, full))
+        # --- row-band map + global peak
+        k = O.kernel(O.MANHATTAN, 9, 7)
+        model = orc.target_model(np.ascontiguousarray(fi[20:27, 30:39]), bins, k)
+        band = D.row_bands(83, 7, world)[rank]
+        (v0, v1), (p0, p1) = band.map_rows, band.pixel_rows
+        part = orc.likelihood_map(np.ascontiguousarray(fi[p0:p1]), bins, model, k)
+        mw = part.shape[1]
+        u, v, _, _, s = orc.peak(part, 4, 3)
+        pk = D.gather_peak(s, (v + v0) * mw + u, mw, 4, 3)
+        fullmap = orc.likelihood_map(fi, bins, model, k)
+        q.put((rank, ok_tables, bool((part == fullmap[v0:v1]).all()),
+               pk == orc.peak(fullmap, 4, 3)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_bands_exchange_and_peak():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, ok_t, ok_map, ok_peak in res:
+        assert ok_t and ok_map and ok_peak, (rank, ok_t, ok_map, ok_peak)
+
+
+def test_tie_rule_across_ranks():
+    assert D.reduce_peaks([(0.5, 10), (0.9, 40), (0.9, 12), (0.1, 0)]) == (0.9, 12)
+    assert D.reduce_peaks([(0.7, 3)]) == (0.7, 3)
+
+
+def test_band_geometry_covers_the_map():
+    for h, kh, world in ((83, 7, 2), (1024, 97, 8), (40, 39, 4)):
+        bands = D.row_bands(h, kh, world)
+        assert bands[0].map_rows[0] == 0 and bands[-1].map_rows[1] == h - kh + 1
+        for a, b in zip(bands, bands[1:]):
+            assert a.map_rows[1] == b.map_rows[0]
+        for bd in bands:
+            assert bd.pixel_rows[1] - bd.pixel_rows[0] == (bd.map_rows[1] - bd.map_rows[0]) + \
+                (kh - 1 if bd.map_rows[1] > bd.map_rows[0] else 0)
+    assert D.frame_shards(64, 8, 3) == list(range(3, 64, 8))

@@ -359,3 +359,37 @@ def test_config2_full_size_properties(ctx):
 def test_width_limit_is_a_size_error(ctx):
     with pytest.raises(swg.SizeError):
         ctx.build(np.zeros((4, 4097), np.uint8), swg.FMT_GRAY8, 2, swg.PLANES_PLAIN)
+
+
+def test_row_band_tables_and_maps_on_gpu(ctx, oracle):
+    """Row-band split on the device: per-band GPU tables +
+    boundary prefix rows rebuild the global tables exactly; per-band GPU maps
+    are the full map's rows; the band peaks reduce to the full-map peak."""
+    from paper_1705_03524_b200 import dist as D
+    img = oracle.random_gray(301, 203, 77)
+    bins, world = 16, 4
+    full = build(ctx, img, bins)
+    glob_ref = [full.export_i64(k) for k in range(3)]
+    locs, rows = [], []
+    for y0, y1 in D.table_bands(203, world):
+        t = build(ctx, np.ascontiguousarray(img[y0:y1]), bins)
+        loc = tuple(t.export_i64(k) for k in range(3))
+        locs.append((y0, y1, loc))
+        rows.append(D.last_rows(loc, y0))
+    for r, (y0, y1, loc) in enumerate(locs):
+        g = D.globalize_band_tables(loc, y0, D.band_carry(rows, r))
+        for k in range(3):
+            assert (g[k] == glob_ref[k][:, y0:y1 + 1]).all()
+    k = K(swg.MANHATTAN, 25, 17)
+    fi = oracle.quantize_gray8(img, bins)
+    mdl = oracle.target_model(fi[40:57, 100:125].copy(), bins, O.kernel(O.MANHATTAN, 25, 17))
+    fmap, fpk = full.likelihood_map(k, mdl)
+    cands = []
+    for bd in D.row_bands(203, 17, world):
+        (v0, v1), (p0, p1) = bd.map_rows, bd.pixel_rows
+        tb = build(ctx, np.ascontiguousarray(img[p0:p1]), bins)
+        m, pk = tb.likelihood_map(k, mdl)
+        assert (m == fmap[v0:v1]).all()
+        cands.append((pk[4], (pk[1] + v0) * fmap.shape[1] + pk[0]))
+    s, i = D.reduce_peaks(cands)
+    assert (i % fmap.shape[1], i // fmap.shape[1], s) == (fpk[0], fpk[1], fpk[4])
