@@ -80,9 +80,17 @@ __device__ __forceinline__ void block_peak(double s, long long idx, PeakPart* ou
 __device__ __forceinline__ uint4 ldq(const uint32_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
+__device__ __forceinline__ uint4 ldqb(const char* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
 __device__ __forceinline__ uint4 box4(uint4 br, uint4 bl, uint4 tr, uint4 tl) {
   return make_uint4(br.x - bl.x - tr.x + tl.x, br.y - bl.y - tr.y + tl.y,
                     br.z - bl.z - tr.z + tl.z, br.w - bl.w - tr.w + tl.w);
+}
+// Exact uint32 -> double: (2^52 + n) - 2^52 on the fp64 pipe instead of an
+// I2F.F64 on the narrower conversion pipe.
+__device__ __forceinline__ double u2d(uint32_t n) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)n), 4503599627370496.0);
 }
 __device__ __forceinline__ uint32_t comp(const uint4& v, int k) {
   return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
@@ -119,40 +127,31 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
   const int cx = u + a.hx, cy = v + a.hy;
-  const size_t pitch = a.pitch;
-  // record offsets (in uint32 elements) of the corner lattice
-  const size_t x0 = (size_t)(cx - a.hx) * kOct + half * 4;
-  const size_t x1 = (size_t)(cx + 1) * kOct + half * 4;
-  const size_t x2 = (size_t)(cx + a.hx + 1) * kOct + half * 4;
-  const size_t y0 = (size_t)(cy - a.hy) * pitch * kOct;
-  const size_t y1 = (size_t)(cy + 1) * pitch * kOct;
-  const size_t y2 = (size_t)(cy + a.hy + 1) * pitch * kOct;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(a.tab);
+  const uint32_t centre = ((uint32_t)cy * (uint32_t)a.pitch + (uint32_t)cx) * kOct + half * 4;
   const size_t ps8 = a.plane_stride * kOct;
   const uint32_t M = (uint32_t)(a.hx + a.hy + 1);
   const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
 
   double s = 0.0, mass_unused = 0.0;
   for (int g = 0; g < a.groups; ++g) {
-    const uint32_t* P = base + (size_t)g * a.planes * ps8;
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
+                                                  (size_t)g * a.planes * ps8 + centre);
     uint4 hist;
     if constexpr (UNIFORM) {
-      hist = box4(ldq(P + y2 + x2), ldq(P + y2 + x0), ldq(P + y0 + x2), ldq(P + y0 + x0));
+      hist = box4(ldqb(w + a.lat[7]), ldqb(w + a.lat[5]), ldqb(w + a.lat[2]), ldqb(w + a.lat[0]));
     } else {
-      const uint32_t* X = P + ps8;
-      const uint32_t* Y = P + 2 * ps8;
-      const uint4 p00 = ldq(P + y0 + x0), p10 = ldq(P + y0 + x1), p20 = ldq(P + y0 + x2);
-      const uint4 p01 = ldq(P + y1 + x0), p21 = ldq(P + y1 + x2);
-      const uint4 p02 = ldq(P + y2 + x0), p12 = ldq(P + y2 + x1), p22 = ldq(P + y2 + x2);
+      const uint4 p00 = ldqb(w + a.lat[0]), p10 = ldqb(w + a.lat[1]), p20 = ldqb(w + a.lat[2]);
+      const uint4 p01 = ldqb(w + a.lat[3]), p21 = ldqb(w + a.lat[4]);
+      const uint4 p02 = ldqb(w + a.lat[5]), p12 = ldqb(w + a.lat[6]), p22 = ldqb(w + a.lat[7]);
       const uint4 n = box4(p22, p02, p20, p00);   // whole window
       const uint4 nl = box4(p12, p02, p10, p00);  // columns [x0, x1)
       const uint4 nt = box4(p21, p01, p20, p00);  // rows    [y0, y1)
-      const uint4 q00 = ldq(X + y0 + x0), q10 = ldq(X + y0 + x1), q20 = ldq(X + y0 + x2);
-      const uint4 q02 = ldq(X + y2 + x0), q12 = ldq(X + y2 + x1), q22 = ldq(X + y2 + x2);
+      const uint4 q00 = ldqb(w + a.lat[8]), q10 = ldqb(w + a.lat[9]), q20 = ldqb(w + a.lat[10]);
+      const uint4 q02 = ldqb(w + a.lat[11]), q12 = ldqb(w + a.lat[12]), q22 = ldqb(w + a.lat[13]);
       const uint4 xl = box4(q12, q02, q10, q00), xall = box4(q22, q02, q20, q00);
-      const uint4 w00 = ldq(Y + y0 + x0), w20 = ldq(Y + y0 + x2);
-      const uint4 w01 = ldq(Y + y1 + x0), w21 = ldq(Y + y1 + x2);
-      const uint4 w02 = ldq(Y + y2 + x0), w22 = ldq(Y + y2 + x2);
+      const uint4 w00 = ldqb(w + a.lat[14]), w20 = ldqb(w + a.lat[15]);
+      const uint4 w01 = ldqb(w + a.lat[16]), w21 = ldqb(w + a.lat[17]);
+      const uint4 w02 = ldqb(w + a.lat[18]), w22 = ldqb(w + a.lat[19]);
       const uint4 yt = box4(w21, w01, w20, w00), yall = box4(w22, w02, w20, w00);
       auto lin = [&](uint32_t n_, uint32_t nl_, uint32_t nt_, uint32_t xl_, uint32_t xa_,
                      uint32_t yt_, uint32_t ya_) {
@@ -169,13 +168,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
     for (int k = 0; k < 4; ++k) {
       const uint32_t raw = comp(hist, k);
       const double model = a.model[g * kOct + half * 4 + k];
-      val[k] = (double)raw;
+      val[k] = u2d(raw);
       if (raw == 0u) {
         term[k] = 0.0;  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
       } else if (SIM == SWG_SIM_BHATTACHARYYA) {
-        term[k] = __dsqrt_rn(__dmul_rn(model, (double)raw));
+        term[k] = __dsqrt_rn(__dmul_rn(model, val[k]));
       } else {
-        const double q = __ddiv_rn((double)raw, a.mass);
+        const double q = __ddiv_rn(val[k], a.mass);
         term[k] = (q < model) ? q : model;
       }
     }
@@ -191,7 +190,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 // K2c: wedding-cake telescoping over nested boxes of the plain table.
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
-                                                              const CakeRings rg) {
+                                                              const CakeSweep rg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
   const int r0 = blockIdx.y * kSweepTileY + warp;
@@ -199,36 +198,29 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
   const int cx = u + a.hx, cy = v + a.hy;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(a.tab) + half * 4;
-  const size_t pitch8 = a.pitch * kOct, ps8 = a.plane_stride * kOct;
+  // element offset of this window's centre record in its plane (+ the half
+  // of each octet this lane reads)
+  const uint32_t centre = ((uint32_t)cy * (uint32_t)a.pitch + (uint32_t)cx) * kOct + half * 4;
+  const size_t ps8 = a.plane_stride * kOct;
 
-  // out[k] for bins 4*half + k of octet g: ring order, early exit on empty.
-  // Two rings per iteration keep 8 corner loads in flight.
-  auto corners = [&](const uint32_t* P, int i) {
-    const int ax = rg.a[i], cyv = rg.c[i];
-    const uint32_t* ra = P + (size_t)(cy - cyv) * pitch8;
-    const uint32_t* rb = P + (size_t)(cy + cyv + 1) * pitch8;
-    const size_t xa = (size_t)(cx - ax) * kOct, xe = (size_t)(cx + ax + 1) * kOct;
-    return box4(ldq(rb + xe), ldq(rb + xa), ldq(ra + xe), ldq(ra + xa));
-  };
-  auto accumulate = [&](double (&out)[4], const uint4& cnt, double c) {
-    if (cnt.x) out[0] = __dadd_rn(out[0], __dmul_rn(c, (double)cnt.x));
-    if (cnt.y) out[1] = __dadd_rn(out[1], __dmul_rn(c, (double)cnt.y));
-    if (cnt.z) out[2] = __dadd_rn(out[2], __dmul_rn(c, (double)cnt.z));
-    if (cnt.w) out[3] = __dadd_rn(out[3], __dmul_rn(c, (double)cnt.w));
-  };
+  // out[k] for bins 4*half + k of octet g, rings in order (outer -> inner).
+  // out + coeff*0 == out bit for bit (out is never -0), so zero counts need
+  // no guard; nested boxes: once all four counts are 0 every inner ring is.
   auto octet = [&](int g, double (&out)[4]) {
-    const uint32_t* P = base + (size_t)g * a.planes * ps8;
+    // per-thread byte pointer to the centre record; ring offsets are bytes
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
+                                                  (size_t)g * a.planes * ps8 + centre);
 #pragma unroll
     for (int k = 0; k < 4; ++k) out[k] = 0.0;
-    for (int i = 0; i < a.rings; i += 2) {
-      const bool two = i + 1 < a.rings;
-      const uint4 c0 = corners(P, i);
-      const uint4 c1 = two ? corners(P, i + 1) : make_uint4(0, 0, 0, 0);
-      if ((c0.x | c0.y | c0.z | c0.w) == 0u) break;  // nested boxes: all inner 0
-      accumulate(out, c0, rg.coeff[i]);
-      if ((c1.x | c1.y | c1.z | c1.w) == 0u) break;
-      accumulate(out, c1, rg.coeff[i + 1]);
+    for (int i = 0; i < a.rings; ++i) {
+      const int4 o = rg.off[i];
+      const uint4 cnt = box4(ldqb(w + o.w), ldqb(w + o.z), ldqb(w + o.y), ldqb(w + o.x));
+      if ((cnt.x | cnt.y | cnt.z | cnt.w) == 0u) break;
+      const double c = rg.coeff[i];
+      out[0] = __dadd_rn(out[0], __dmul_rn(c, u2d(cnt.x)));
+      out[1] = __dadd_rn(out[1], __dmul_rn(c, u2d(cnt.y)));
+      out[2] = __dadd_rn(out[2], __dmul_rn(c, u2d(cnt.z)));
+      out[3] = __dadd_rn(out[3], __dmul_rn(c, u2d(cnt.w)));
     }
   };
 
@@ -275,12 +267,20 @@ __global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int
                                                       int hx, int hy, swg_peak* out) {
   double s = -2.0;
   long long idx = 0x7FFFFFFFFFFFFFFFLL;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const PeakPart p = parts[i];
-    if (better(p.score, p.idx, s, idx)) {
-      s = p.score;
-      idx = p.idx;
+  constexpr int kBatch = 8;  // independent loads in flight per thread
+  for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x * kBatch) {
+    PeakPart p[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const int i = i0 + k * blockDim.x;
+      p[k] = i < n ? parts[i] : PeakPart{-2.0, 0x7FFFFFFFFFFFFFFFLL};
     }
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k)
+      if (better(p[k].score, p[k].idx, s, idx)) {
+        s = p[k].score;
+        idx = p[k].idx;
+      }
   }
   __shared__ PeakPart res;
   block_peak(s, idx, &res);
@@ -381,7 +381,7 @@ cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cud
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, dim3 grid,
+cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake<0><<<grid, kSweepThreads, 0, s>>>(a, r);
   else k_sweep_cake<1><<<grid, kSweepThreads, 0, s>>>(a, r);

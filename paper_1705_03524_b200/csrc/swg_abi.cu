@@ -1019,12 +1019,35 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       if (method == SWG_METHOD_BRUTE && !brute[i]) method = SWG_METHOD_SWIH;
       if (method == SWG_METHOD_SWIH) {
         a.mass = (double)affine_mass(k);
+        {  // corner byte offsets from the centre record (SweepArgs::lat order)
+          const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
+          const long long xs[3] = {-a.hx, 1, a.hx + 1}, ys[3] = {-a.hy, 1, a.hy + 1};
+          auto off = [&](int plane, int xi, int yi) {
+            return (int)(4 * (plane * ps8 + ys[yi] * p8 + xs[xi] * kOct));
+          };
+          const int pts[20][3] = {{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, 1}, {0, 2, 1},
+                                  {0, 0, 2}, {0, 1, 2}, {0, 2, 2}, {1, 0, 0}, {1, 1, 0},
+                                  {1, 2, 0}, {1, 0, 2}, {1, 1, 2}, {1, 2, 2}, {2, 0, 0},
+                                  {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
+          for (int q = 0; q < 20; ++q)
+            a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
+        }
         CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], c->stream));
       } else if (method == SWG_METHOD_CAKE) {
         static thread_local CakeRings rg;
+        static thread_local CakeSweep cs;
         ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
+        const long long p8 = (long long)t->pitch * kOct;
+        for (int q = 0; q < r.rings; ++q) {  // corner byte offsets from the centre record
+          const long long ax = rg.a[q], cy_ = rg.c[q];
+          cs.off[q] = make_int4((int)(4 * (-cy_ * p8 - ax * kOct)),
+                                (int)(4 * (-cy_ * p8 + (ax + 1) * kOct)),
+                                (int)(4 * ((cy_ + 1) * p8 - ax * kOct)),
+                                (int)(4 * ((cy_ + 1) * p8 + (ax + 1) * kOct)));
+          cs.coeff[q] = rg.coeff[q];
+        }
         a.rings = r.rings;
-        CUDA_TRY(launch_sweep_cake(a, rg, grid[i], c->stream));
+        CUDA_TRY(launch_sweep_cake(a, cs, grid[i], c->stream));
       } else {
         // direct per-pixel weighted histogram (baselines.cpp:24-69)
         const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);

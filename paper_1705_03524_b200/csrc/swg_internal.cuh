@@ -90,15 +90,31 @@ struct SweepArgs {
   int sim;
   int rings;
   double mass;         // exact strict-window mass (affine kernels)
+  // affine: byte offsets of the corner cells from the window's centre record
+  // (window independent): plain (x0,y0) (x1,y0) (x2,y0) (x0,y1) (x2,y1)
+  // (x0,y2) (x1,y2) (x2,y2); xramp (x0,y0) (x1,y0) (x2,y0) (x0,y2) (x1,y2)
+  // (x2,y2); yramp (x0,y0) (x2,y0) (x0,y1) (x2,y1) (x0,y2) (x2,y2), with
+  // x0 = -hx, x1 = +1, x2 = hx+1 (y likewise) in padded coordinates.
+  int lat[20];
   double* scores;      // rows x mw, row r = map row row0 + r
   PeakPart* parts;     // one per CTA
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
+// Host-side ring plan of a wedding-cake configuration.
 struct CakeRings {
   int a[kMaxRings];        // ring i box half-extent in x: hx - shrink_x[i]
   int c[kMaxRings];        // ring i box half-extent in y: hy - shrink_y[i]
   double coeff[kMaxRings]; // w_i - w_{i-1} (baselines.cpp:141)
+};
+
+// Kernel-side ring constants: the four box-corner offsets of ring i relative
+// to the window centre's record, in BYTES and window independent --
+// (TL, TR, BL, BR) = 32 * (-c*p - a, -c*p + a+1, (c+1)*p - a, (c+1)*p + a+1)
+// with p = pitch in records -- and the ring coefficient.
+struct CakeSweep {
+  int4 off[kMaxRings];
+  double coeff[kMaxRings];
 };
 
 struct BruteArgs {
@@ -134,7 +150,7 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s);
 template <typename T>
 cudaError_t launch_build(const BuildArgs& a, cudaStream_t s);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
-cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeRings& r, dim3 grid,
+cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
                                cudaStream_t s);
