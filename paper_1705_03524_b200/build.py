@@ -78,9 +78,11 @@ def build_cpp_tests(verbose: bool = False) -> str:
     return out
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str = "",
+          defines=()) -> str:
+    """variant/defines: an A/B build (lib/libswg_<variant>.so, -D flags)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" + ("_" + variant if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     deps_common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "swg.h")]
     objs = []
@@ -89,18 +91,19 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + deps_common):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *NVCC_FLAGS, *["-D" + d for d in defines], "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
+    lib = LIB if not variant else os.path.join(LIBDIR, f"libswg_{variant}.so")
+    if force or _stale(lib, objs):
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib,
                "-Xcompiler", "-fPIC"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

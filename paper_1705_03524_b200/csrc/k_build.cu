@@ -268,15 +268,11 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
   }
 }
 
-// K1c: one CTA per (row band, bin octet, table kind); blockIdx.y = kind.
-template <typename T, int CPT>
-__global__ void __launch_bounds__(CPT == 4 ? 256 : 512) k_build(const BuildArgs g) {
-  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
-  switch (blockIdx.y) {
-    case 0: build_body<T, 0, CPT>(g, band, grp); break;
-    case 1: build_body<T, 1, CPT>(g, band, grp); break;
-    default: build_body<T, 2, CPT>(g, band, grp);
-  }
+// K1c: one CTA per (row band, bin octet); one launch per table kind so each
+// kind gets its own register allocation.
+template <typename T, int KIND, int CPT>
+__global__ void __launch_bounds__(512) k_build(const BuildArgs g) {
+  build_body<T, KIND, CPT>(g, blockIdx.x / g.groups, blockIdx.x % g.groups);
 }
 
 // K0: any input format -> uint16 bin image (pitched, padded with kNoBin).
@@ -362,10 +358,21 @@ template <typename T>
 cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
-  dim3 grid((unsigned)(a.nbands * a.groups), (unsigned)a.planes);
-  if (cpt == 4) k_build<T, 4><<<grid, threads, 0, s>>>(a);
-  else k_build<T, 8><<<grid, threads, 0, s>>>(a);
-  return cudaGetLastError();
+  const unsigned grid = (unsigned)(a.nbands * a.groups);
+  for (int kind = 0; kind < a.planes; ++kind) {
+    if (cpt == 4) {
+      if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
+      else if (kind == 1) k_build<T, 1, 4><<<grid, threads, 0, s>>>(a);
+      else k_build<T, 2, 4><<<grid, threads, 0, s>>>(a);
+    } else {
+      if (kind == 0) k_build<T, 0, 8><<<grid, threads, 0, s>>>(a);
+      else if (kind == 1) k_build<T, 1, 8><<<grid, threads, 0, s>>>(a);
+      else k_build<T, 2, 8><<<grid, threads, 0, s>>>(a);
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t);

@@ -29,6 +29,10 @@
 // uses the reference tie rule (matching.cpp:211-223).
 #include "swg_internal.cuh"
 
+#ifndef SWG_CAKE_UNROLL
+#define SWG_CAKE_UNROLL 2
+#endif
+
 namespace swg {
 
 namespace {
@@ -77,9 +81,6 @@ __device__ __forceinline__ void block_peak(double s, long long idx, PeakPart* ou
   }
 }
 
-__device__ __forceinline__ uint4 ldq(const uint32_t* p) {
-  return __ldg(reinterpret_cast<const uint4*>(p));
-}
 __device__ __forceinline__ uint4 ldqb(const char* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
@@ -212,15 +213,31 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
                                                   (size_t)g * a.planes * ps8 + centre);
 #pragma unroll
     for (int k = 0; k < 4; ++k) out[k] = 0.0;
-    for (int i = 0; i < a.rings; ++i) {
+    auto ring = [&](int i) {
       const int4 o = rg.off[i];
-      const uint4 cnt = box4(ldqb(w + o.w), ldqb(w + o.z), ldqb(w + o.y), ldqb(w + o.x));
-      if ((cnt.x | cnt.y | cnt.z | cnt.w) == 0u) break;
-      const double c = rg.coeff[i];
+      return box4(ldqb(w + o.w), ldqb(w + o.z), ldqb(w + o.y), ldqb(w + o.x));
+    };
+    auto add = [&](const uint4& cnt, double c) {
       out[0] = __dadd_rn(out[0], __dmul_rn(c, u2d(cnt.x)));
       out[1] = __dadd_rn(out[1], __dmul_rn(c, u2d(cnt.y)));
       out[2] = __dadd_rn(out[2], __dmul_rn(c, u2d(cnt.z)));
       out[3] = __dadd_rn(out[3], __dmul_rn(c, u2d(cnt.w)));
+    };
+    // two rings per iteration: 8 independent 16-byte loads in flight
+    int i = 0;
+#if SWG_CAKE_UNROLL >= 2
+    for (; i + 1 < a.rings; i += 2) {
+      const uint4 c0 = ring(i), c1 = ring(i + 1);
+      if ((c0.x | c0.y | c0.z | c0.w) == 0u) return;
+      add(c0, rg.coeff[i]);
+      if ((c1.x | c1.y | c1.z | c1.w) == 0u) return;
+      add(c1, rg.coeff[i + 1]);
+    }
+#endif
+    for (; i < a.rings; ++i) {
+      const uint4 c0 = ring(i);
+      if ((c0.x | c0.y | c0.z | c0.w) == 0u) return;
+      add(c0, rg.coeff[i]);
     }
   };
 

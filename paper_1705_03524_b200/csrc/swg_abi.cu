@@ -250,7 +250,7 @@ swg_status run_build(swg_tables* t, T* out) {
     c->launches += 2;
   }
   CUDA_TRY(launch_build<T>(a, c->stream));
-  c->launches += 1;
+  c->launches += (uint64_t)t->planes;
   return SWG_OK;
 }
 

@@ -34,7 +34,7 @@ constexpr int kMaxWidth = 4096;      // build CTA spans a full row (CPT <= 8)
 inline size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
 // Columns per build thread.
-inline int choose_cpt(int w) { return w <= 1024 ? 4 : 8; }
+inline int choose_cpt(int w) { return w <= 2048 ? 4 : 8; }
 
 // Row pitch in records (room for the straddling last build thread).
 inline size_t record_pitch(int w) { return round_up((size_t)w + 1 + 8, 4); }

@@ -20,7 +20,8 @@ import numpy as np
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+# SWG_LIB selects an A/B variant build of the same library (tuning only)
+LIB_PATH = os.environ.get("SWG_LIB", _build.LIB)
 
 # enums (include/swg.h)
 FMT_GRAY8, FMT_GRAY16, FMT_RGB8, FMT_BINS16 = 0, 1, 2, 3
