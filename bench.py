@@ -49,21 +49,22 @@ def workload(name):
         return dict(name="config1: 256x256 u8, 16 bins, Manhattan, window 33x33",
                     gen=synth.config1, bins=16, planes=swg.PLANES_AFFINE,
                     scales=[(swg.Kernel(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)],
-                    P=3)
+                    P=3, elem=4)
     if name == "c5m":
         ks = (17, 25, 37, 53, 79, 117, 173, 257)
         return dict(name="config5 (Manhattan subset): 2048x2048 u16, 64 bins, Manhattan, windows "
                          + "/".join(map(str, ks)),
                     gen=synth.config5, bins=64, planes=swg.PLANES_AFFINE, fmt=swg.FMT_GRAY16,
                     scales=[(swg.Kernel(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks],
-                    P=3)
+                    P=3, elem=4)
     scales = []
     for i, s in enumerate((32, 64, 96)):
         kw = synth.odd_window(s)
         scales.append((swg.Kernel(swg.GAUSS_CHEB, kw, kw, 0.5), swg.CAKE, kw // 2 + 1, i))
     return dict(name="config2: 1024x1024 u8, 32 bins, Gaussian (GaussianChebyshev sigma=0.5, "
                      "exact full-ring cake), windows 33/65/97",
-                gen=synth.config2, bins=32, planes=swg.PLANES_PLAIN, scales=scales, P=1)
+                gen=synth.config2, bins=32, planes=swg.PLANES_PLAIN, scales=scales, P=1,
+                elem=2)
 
 
 def target_center(scene, ti):
@@ -358,7 +359,7 @@ def main():
 
     # ---- roofline of the dominant kernel (the sweep) and of the IH build
     hbm, src = peaks_json()
-    b, P, e = wl["bins"], wl["P"], 4
+    b, P, e = wl["bins"], wl["P"], wl["elem"]  # e: bytes per table entry
     ih_bytes = (W + 1) * (H + 1) * b * P * e
     sweep_bytes = sum(ih_bytes + 8 * m.numel() for m in maps_dev)
     sweep_ms = sum(sum(x) for x in scale_ms) / args.steps

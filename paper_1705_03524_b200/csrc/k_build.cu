@@ -43,7 +43,10 @@ __device__ __forceinline__ void load_bins(const uint16_t* p, uint16_t (&v)[CPT])
 template <typename T>
 __device__ __forceinline__ void store_record(T* dst, const T (&v)[kOct]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (sizeof(T) == 2) {
+    d[0] = make_uint4(uint32_t(v[0]) | uint32_t(v[1]) << 16, uint32_t(v[2]) | uint32_t(v[3]) << 16,
+                      uint32_t(v[4]) | uint32_t(v[5]) << 16, uint32_t(v[6]) | uint32_t(v[7]) << 16);
+  } else if constexpr (sizeof(T) == 4) {
     d[0] = make_uint4(v[0], v[1], v[2], v[3]);
     d[1] = make_uint4(v[4], v[5], v[6], v[7]);
   } else {
@@ -359,7 +362,8 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const unsigned grid = (unsigned)(a.nbands * a.groups);
-  for (int kind = 0; kind < a.planes; ++kind) {
+  const int kinds = sizeof(T) == 2 ? 1 : a.planes;  // narrow tables: plain only
+  for (int kind = 0; kind < kinds; ++kind) {
     if (cpt == 4) {
       if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
       else if (kind == 1) k_build<T, 1, 4><<<grid, threads, 0, s>>>(a);
@@ -375,6 +379,7 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
   return cudaSuccess;
 }
 
+template cudaError_t launch_build<uint16_t>(const BuildArgs&, cudaStream_t);
 template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t);
 template cudaError_t launch_build<uint64_t>(const BuildArgs&, cudaStream_t);
 

@@ -279,6 +279,83 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+// K2c16: the cake sweep over NARROW (uint16) plain planes.  Every box of a
+// window with area < 2^16 has a count < 2^16, so box sums of the wrapped
+// 16-bit prefix tables are exact.  One lane owns one window and reads whole
+// 16-byte records (8 bins) per corner: half the bytes of the 32-bit path,
+// box arithmetic on packed 16-bit pairs (vsub2/vadd2).
+template <int SIM>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs a,
+                                                                const CakeSweep rg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u0 = blockIdx.x * 32 + lane;
+  const int r0 = blockIdx.y * kSweepTileY + warp;
+  const bool active = u0 < a.mw && r0 < a.rows;
+  const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
+  const int v = a.row0 + r;
+  const int cx = u + a.hx, cy = v + a.hy;
+  const uint32_t centre = ((uint32_t)cy * (uint32_t)a.pitch + (uint32_t)cx) * kOct;
+  const size_t ps8 = a.plane_stride * kOct;
+
+  auto octet = [&](int g, double (&out)[kOct]) {
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint16_t*>(a.tab) +
+                                                  (size_t)g * a.planes * ps8 + centre);
+#pragma unroll
+    for (int k = 0; k < kOct; ++k) out[k] = 0.0;
+    for (int i = 0; i < a.rings; ++i) {
+      const int4 o = rg.off[i];
+      const uint4 br = ldqb(w + o.w), bl = ldqb(w + o.z), tr = ldqb(w + o.y), tl = ldqb(w + o.x);
+      const uint32_t c0 = __vadd2(__vsub2(__vsub2(br.x, bl.x), tr.x), tl.x);
+      const uint32_t c1 = __vadd2(__vsub2(__vsub2(br.y, bl.y), tr.y), tl.y);
+      const uint32_t c2 = __vadd2(__vsub2(__vsub2(br.z, bl.z), tr.z), tl.z);
+      const uint32_t c3 = __vadd2(__vsub2(__vsub2(br.w, bl.w), tr.w), tl.w);
+      if ((c0 | c1 | c2 | c3) == 0u) break;  // nested boxes: all inner counts 0
+      const double c = rg.coeff[i];
+      const uint32_t cw[4] = {c0, c1, c2, c3};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        out[2 * q] = __dadd_rn(out[2 * q], __dmul_rn(c, u2d(cw[q] & 0xFFFFu)));
+        out[2 * q + 1] = __dadd_rn(out[2 * q + 1], __dmul_rn(c, u2d(cw[q] >> 16)));
+      }
+    }
+  };
+
+  double s = 0.0, mass = 0.0;
+  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
+    for (int g = 0; g < a.groups; ++g) {
+      double out[kOct];
+      octet(g, out);
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) {
+        mass = __dadd_rn(mass, out[j]);
+        if (out[j] != 0.0) s = __dadd_rn(s, __dsqrt_rn(__dmul_rn(a.model[g * kOct + j], out[j])));
+      }
+    }
+    s = __ddiv_rn(s, __dsqrt_rn(mass));
+  } else {
+    for (int g = 0; g < a.groups; ++g) {
+      double out[kOct];
+      octet(g, out);
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) mass = __dadd_rn(mass, out[j]);
+    }
+    for (int g = 0; g < a.groups; ++g) {
+      double out[kOct];
+      octet(g, out);
+#pragma unroll
+      for (int j = 0; j < kOct; ++j)
+        if (out[j] != 0.0) {
+          const double q = __ddiv_rn(out[j], mass), m = a.model[g * kOct + j];
+          s = __dadd_rn(s, (q < m) ? q : m);
+        }
+    }
+  }
+  s = clamp01(s);
+  if (active) a.scores[(size_t)r * a.mw + u] = s;
+  block_peak(active ? s : -2.0, (long long)v * a.mw + u,
+             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
 // K3: reduce CTA candidates to the map peak (one CTA).
 __global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int n, int mw,
                                                       int hx, int hy, swg_peak* out) {
@@ -402,6 +479,13 @@ cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake<0><<<grid, kSweepThreads, 0, s>>>(a, r);
   else k_sweep_cake<1><<<grid, kSweepThreads, 0, s>>>(a, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
+                                cudaStream_t s) {
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake16<0><<<grid, kSweepThreads, 0, s>>>(a, r);
+  else k_sweep_cake16<1><<<grid, kSweepThreads, 0, s>>>(a, r);
   return cudaGetLastError();
 }
 

@@ -186,7 +186,9 @@ struct swg_tables {
   size_t in_pitch = 0, in_row = 0;
   int groups = 0;          // bin octets
   size_t pitch = 0, ps = 0;  // records (shared by the 32- and 64-bit planes)
-  uint32_t* t32 = nullptr;
+  uint16_t* t16 = nullptr;  // narrow plain planes (P = 1 tables): exact box
+                            // counts for boxes of area < 2^16
+  uint32_t* t32 = nullptr;  // primary for P = 3; on demand for P = 1
   uint64_t* t64 = nullptr;
   uint32_t* lb = nullptr;  // band carry scratch (BuildArgs::agg)
   int band_h = 0, nbands = 0;
@@ -279,6 +281,22 @@ swg_status upload_and_quantize(swg_tables* t, const void* pixels, int is_device,
   c->launches += 1;
   t->has_fi = true;
   return SWG_OK;
+}
+
+swg_status ensure_t32(swg_tables* t) {
+  if (t->t32) return SWG_OK;
+  if (!t->has_fi) return fail(SWG_ERR, "tables: no 32-bit planes and no feature image");
+  const size_t bytes = t->ps * t->planes * t->groups * kOct * 4;
+  cudaError_t e = cudaMalloc(&t->t32, bytes);
+  if (e != cudaSuccess) {
+    t->t32 = nullptr;
+    cudaGetLastError();
+    g_required = bytes;
+    return fail(SWG_ERR_CAPACITY, "tables: 32-bit planes need %zu bytes: %s", bytes,
+                cudaGetErrorString(e));
+  }
+  t->bytes += bytes;
+  return run_build<uint32_t>(t, t->t32);
 }
 
 swg_status ensure_t64(swg_tables* t) {
@@ -434,7 +452,10 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   t->pitch = record_pitch(width);
   t->ps = t->pitch * (size_t)(height + 1);
   choose_bands(t);
-  const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * 4;
+  // plain-only tables keep narrow uint16 planes (32-bit ones are built on
+  // demand); affine tables keep uint32 planes
+  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : 4;
+  const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * elem;
   const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * 16 * 4;
   const size_t need = tab_bytes + lb_bytes + t->fip * height * 2;
   if (memory_budget && need > memory_budget) {
@@ -448,7 +469,8 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
     return st;
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
+  if ((e = elem == 2 ? cudaMalloc(&t->t16, tab_bytes) : cudaMalloc(&t->t32, tab_bytes)) !=
+          cudaSuccess ||
       (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
       (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
     g_required = need;
@@ -458,7 +480,7 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   }
   t->bytes = need;
   swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
-  if (st == SWG_OK) st = run_build<uint32_t>(t, t->t32);
+  if (st == SWG_OK) st = t->t16 ? run_build<uint16_t>(t, t->t16) : run_build<uint32_t>(t, t->t32);
   if (st != SWG_OK) return cleanup(st);
   *out = t;
   return SWG_OK;
@@ -472,7 +494,8 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
-  ST_TRY(run_build<uint32_t>(t, t->t32));
+  if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
+  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   return SWG_OK;
 }
@@ -537,6 +560,7 @@ swg_status swg_tables_destroy(swg_tables* t) {
   if (t->ctx) {
     DeviceGuard g(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
+    cudaFree(t->t16);
     cudaFree(t->t32);
     cudaFree(t->t64);
     cudaFree(t->fi);
@@ -618,6 +642,7 @@ swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
+  ST_TRY(ensure_t32(t));
   return export_planes<uint32_t, uint32_t>(t, t->t32, kind, b0, b1, out);
 }
 
@@ -662,6 +687,7 @@ swg_status swg_query_terms(swg_tables* t, int n, int tpw, const swg_term* terms,
   DeviceGuard g(t->ctx->device);
   swg_ctx* c = t->ctx;
   if (need64) ST_TRY(ensure_t64(t));
+  else ST_TRY(ensure_t32(t));
   const size_t tb = (size_t)n * tpw * sizeof(swg_term), ob = (size_t)n * t->bins * 8;
   ST_TRY(c->terms.ensure(tb));
   ST_TRY(c->qout.ensure(ob));
@@ -798,6 +824,7 @@ swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   swg_ctx* c = t->ctx;
+  ST_TRY(ensure_t32(t));
   const size_t tb = terms.size() * sizeof(swg_term), cb = coeff.size() * 8;
   const size_t ob = (size_t)n * t->bins * 8;
   ST_TRY(c->terms.ensure(tb + cb));
@@ -956,8 +983,16 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // output), CTA peak candidates, device peaks
   std::vector<size_t> soff(n, 0), poff(n, 0);
   size_t stot = 0, ptot = 0;
+  // Engine per request.  The kernel-independent choices: Plain maps are
+  // Uniform-kernel maps; brute force on an integer affine kernel gives the
+  // quadrant path's exact counts (engine.hpp:62-66, test_matching.cpp:115-141)
+  // and shares its kernel; a Uniform box is a one-ring cake with coefficient
+  // 1.0 (exact integer weights, same scores: score_counts == score_weights on
+  // integers), so on narrow tables it runs the 16-bit cake sweep.
+  enum Engine { kAffine32, kCake16, kCake32, kBrute };
   std::vector<dim3> grid(n);
-  std::vector<int> brute(n, 0);
+  std::vector<int> engine(n);
+  std::vector<swg_kernel> kern(n);
   for (int i = 0; i < n; ++i) {
     const swg_map_request& r = reqs[i];
     const int rows = v1[i] - v0[i];
@@ -966,13 +1001,27 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       soff[i] = stot;
       stot += round_up(cells, 32);
     }
-    brute[i] = r.method == SWG_METHOD_BRUTE && r.kernel.kind != SWG_KERNEL_UNIFORM &&
-               !(r.kernel.kind == SWG_KERNEL_MANHATTAN && t->planes == 3);
-    if (brute[i])
+    swg_kernel k = r.kernel;
+    int method = r.method;
+    if (method == SWG_METHOD_PLAIN) {
+      k.kind = SWG_KERNEL_UNIFORM;
+      method = SWG_METHOD_SWIH;
+    }
+    if (method == SWG_METHOD_BRUTE && (k.kind == SWG_KERNEL_UNIFORM ||
+                                       (k.kind == SWG_KERNEL_MANHATTAN && t->planes == 3)))
+      method = SWG_METHOD_SWIH;
+    const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
+    if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
+    else if (method == SWG_METHOD_CAKE) engine[i] = (t->t16 && small) ? kCake16 : kCake32;
+    else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
+    else engine[i] = kAffine32;
+    kern[i] = k;
+    if (engine[i] == kBrute)
       grid[i] = dim3((unsigned)((mws[i] + kBruteThreads - 1) / kBruteThreads),
                      (unsigned)std::max(rows, 1));
     else
-      grid[i] = dim3((unsigned)((mws[i] + kSweepTileX - 1) / kSweepTileX),
+      grid[i] = dim3((unsigned)((mws[i] + (engine[i] == kCake16 ? 32 : kSweepTileX) - 1) /
+                                (engine[i] == kCake16 ? 32 : kSweepTileX)),
                      (unsigned)std::max((rows + kSweepTileY - 1) / kSweepTileY, 1));
     poff[i] = ptot;
     ptot += (size_t)grid[i].x * grid[i].y;
@@ -990,15 +1039,17 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
                           : static_cast<double*>(c->scores.p) + soff[i];
     PeakPart* parts = static_cast<PeakPart*>(c->parts.p) + poff[i];
     if (rows > 0) {
+      if (engine[i] == kAffine32 || engine[i] == kCake32) ST_TRY(ensure_t32(t));
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
-      a.tab = t->t32;
+      const swg_kernel k = kern[i];
+      a.tab = engine[i] == kCake16 ? (const void*)t->t16 : (const void*)t->t32;
       a.plane_stride = t->ps;
       a.pitch = t->pitch;
       a.planes = t->planes;
       a.bins = t->bins;
       a.groups = t->groups;
-      a.hx = k_hx(r.kernel);
-      a.hy = k_hy(r.kernel);
+      a.hx = k_hx(k);
+      a.hy = k_hy(k);
       a.mw = mws[i];
       a.row0 = v0[i];
       a.rows = rows;
@@ -1007,17 +1058,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       a.parts = parts;
       std::memset(a.model, 0, sizeof(a.model));
       std::memcpy(a.model, r.model, sizeof(double) * t->bins);
-      int method = r.method;
-      swg_kernel k = r.kernel;
-      if (method == SWG_METHOD_PLAIN) {
-        k.kind = SWG_KERNEL_UNIFORM;
-        method = SWG_METHOD_SWIH;
-      }
-      // Brute force on an integer affine kernel yields the same exact counts
-      // as the quadrant path (engine.hpp:62-66; test_matching.cpp:115-141),
-      // so it shares that kernel; other kernels run the direct sum.
-      if (method == SWG_METHOD_BRUTE && !brute[i]) method = SWG_METHOD_SWIH;
-      if (method == SWG_METHOD_SWIH) {
+      if (engine[i] == kAffine32) {
         a.mass = (double)affine_mass(k);
         {  // corner byte offsets from the centre record (SweepArgs::lat order)
           const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
@@ -1033,21 +1074,31 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
             a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
         }
         CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], c->stream));
-      } else if (method == SWG_METHOD_CAKE) {
+      } else if (engine[i] == kCake16 || engine[i] == kCake32) {
         static thread_local CakeRings rg;
         static thread_local CakeSweep cs;
-        ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
+        int rings = 1;
+        if (r.method == SWG_METHOD_CAKE) {
+          ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
+          rings = r.rings;
+        } else {  // Uniform box: one ring, coefficient 1
+          rg.a[0] = a.hx;
+          rg.c[0] = a.hy;
+          rg.coeff[0] = 1.0;
+        }
         const long long p8 = (long long)t->pitch * kOct;
-        for (int q = 0; q < r.rings; ++q) {  // corner byte offsets from the centre record
+        const long long eb = engine[i] == kCake16 ? 2 : 4;  // element bytes
+        for (int q = 0; q < rings; ++q) {  // corner byte offsets from the centre record
           const long long ax = rg.a[q], cy_ = rg.c[q];
-          cs.off[q] = make_int4((int)(4 * (-cy_ * p8 - ax * kOct)),
-                                (int)(4 * (-cy_ * p8 + (ax + 1) * kOct)),
-                                (int)(4 * ((cy_ + 1) * p8 - ax * kOct)),
-                                (int)(4 * ((cy_ + 1) * p8 + (ax + 1) * kOct)));
+          cs.off[q] = make_int4((int)(eb * (-cy_ * p8 - ax * kOct)),
+                                (int)(eb * (-cy_ * p8 + (ax + 1) * kOct)),
+                                (int)(eb * ((cy_ + 1) * p8 - ax * kOct)),
+                                (int)(eb * ((cy_ + 1) * p8 + (ax + 1) * kOct)));
           cs.coeff[q] = rg.coeff[q];
         }
-        a.rings = r.rings;
-        CUDA_TRY(launch_sweep_cake(a, cs, grid[i], c->stream));
+        a.rings = rings;
+        if (engine[i] == kCake16) CUDA_TRY(launch_sweep_cake16(a, cs, grid[i], c->stream));
+        else CUDA_TRY(launch_sweep_cake(a, cs, grid[i], c->stream));
       } else {
         // direct per-pixel weighted histogram (baselines.cpp:24-69)
         const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);

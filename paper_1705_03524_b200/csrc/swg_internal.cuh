@@ -152,6 +152,8 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
+cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
+                                cudaStream_t s);
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
                                cudaStream_t s);
 cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw, int hx, int hy,

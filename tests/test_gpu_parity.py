@@ -393,3 +393,20 @@ def test_row_band_tables_and_maps_on_gpu(ctx, oracle):
         cands.append((pk[4], (pk[1] + v0) * fmap.shape[1] + pk[0]))
     s, i = D.reduce_peaks(cands)
     assert (i % fmap.shape[1], i // fmap.shape[1], s) == (fpk[0], fpk[1], fpk[4])
+
+
+def test_narrow_and_wide_plain_paths(ctx, oracle):
+    """Plain-only tables sweep with 16-bit planes while every box has area
+    < 2^16 and switch to 32-bit planes beyond (257x257 = 66049 px)."""
+    img = oracle.random_gray(300, 280, 31)
+    bins = 4
+    fi = oracle.quantize_gray8(img, bins)
+    t = build(ctx, img, bins, swg.PLANES_PLAIN)
+    for kw, kh in ((255, 255), (257, 257), (255, 259)):
+        for kind, method, rings in ((swg.UNIFORM, swg.PLAIN, 1), (swg.GAUSS_CHEB, swg.CAKE, 3)):
+            ok = O.kernel(kind, kw, kh, 0.5)
+            mdl = oracle.target_model(fi[:kh, :kw].copy(), bins, ok, method, rings)
+            want = oracle.likelihood_map(fi, bins, mdl, ok, method, O.BHATTACHARYYA, rings=rings)
+            got, pk = t.likelihood_map(K(kind, kw, kh, 0.5), mdl, method, rings=rings)
+            assert (got == want).all(), (kw, kh, kind)
+            assert pk == oracle.peak(want, kw // 2, kh // 2)
