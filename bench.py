@@ -265,6 +265,9 @@ def main():
     launches0 = ctx.launches
     clocks.start()
     for s in range(args.steps):
+        # a ~1 ms spin lets the host enqueue the whole step before the GPU
+        # reaches it, so the per-kernel events carry no host launch gaps
+        torch.cuda._sleep(2_000_000)
         flush.zero_()  # evict L2 (256 MiB > 126 MB) between timed steps; not timed
         step(events[s])
     torch.cuda.synchronize()
