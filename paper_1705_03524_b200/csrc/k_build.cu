@@ -278,6 +278,18 @@ __global__ void __launch_bounds__(512) k_build(const BuildArgs g) {
   build_body<T, KIND, CPT>(g, blockIdx.x / g.groups, blockIdx.x % g.groups);
 }
 
+// Small tables: all kinds in ONE launch (blockIdx.y = kind) -- fewer
+// serialized launches where a launch is latency, not bandwidth.
+template <typename T, int CPT>
+__global__ void __launch_bounds__(512) k_build_fused(const BuildArgs g) {
+  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
+  switch (blockIdx.y) {
+    case 0: build_body<T, 0, CPT>(g, band, grp); break;
+    case 1: build_body<T, 1, CPT>(g, band, grp); break;
+    default: build_body<T, 2, CPT>(g, band, grp);
+  }
+}
+
 // K0: any input format -> uint16 bin image (pitched, padded with kNoBin).
 __global__ void k_quantize(const QuantArgs a) {
   const int y = blockIdx.y;
@@ -363,6 +375,12 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const unsigned grid = (unsigned)(a.nbands * a.groups);
   const int kinds = sizeof(T) == 2 ? 1 : a.planes;  // narrow tables: plain only
+  if (kinds > 1 && grid < 2u * 148u) {
+    dim3 g3(grid, (unsigned)kinds);
+    if (cpt == 4) k_build_fused<T, 4><<<g3, threads, 0, s>>>(a);
+    else k_build_fused<T, 8><<<g3, threads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   for (int kind = 0; kind < kinds; ++kind) {
     if (cpt == 4) {
       if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);

@@ -305,17 +305,20 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
     for (int i = 0; i < a.rings; ++i) {
       const int4 o = rg.off[i];
       const uint4 br = ldqb(w + o.w), bl = ldqb(w + o.z), tr = ldqb(w + o.y), tl = ldqb(w + o.x);
-      const uint32_t c0 = __vadd2(__vsub2(__vsub2(br.x, bl.x), tr.x), tl.x);
-      const uint32_t c1 = __vadd2(__vsub2(__vsub2(br.y, bl.y), tr.y), tl.y);
-      const uint32_t c2 = __vadd2(__vsub2(__vsub2(br.z, bl.z), tr.z), tl.z);
-      const uint32_t c3 = __vadd2(__vsub2(__vsub2(br.w, bl.w), tr.w), tl.w);
+      // (br + tl) - (bl + tr) on packed 16-bit pairs
+      const uint32_t c0 = __vsub2(__vadd2(br.x, tl.x), __vadd2(bl.x, tr.x));
+      const uint32_t c1 = __vsub2(__vadd2(br.y, tl.y), __vadd2(bl.y, tr.y));
+      const uint32_t c2 = __vsub2(__vadd2(br.z, tl.z), __vadd2(bl.z, tr.z));
+      const uint32_t c3 = __vsub2(__vadd2(br.w, tl.w), __vadd2(bl.w, tr.w));
       if ((c0 | c1 | c2 | c3) == 0u) break;  // nested boxes: all inner counts 0
       const double c = rg.coeff[i];
       const uint32_t cw[4] = {c0, c1, c2, c3};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        // exact conversions, split between the fp64 pipe (magic number) and
+        // the conversion pipe (I2F) so neither saturates
         out[2 * q] = __dadd_rn(out[2 * q], __dmul_rn(c, u2d(cw[q] & 0xFFFFu)));
-        out[2 * q + 1] = __dadd_rn(out[2 * q + 1], __dmul_rn(c, u2d(cw[q] >> 16)));
+        out[2 * q + 1] = __dadd_rn(out[2 * q + 1], __dmul_rn(c, __uint2double_rn(cw[q] >> 16)));
       }
     }
   };
