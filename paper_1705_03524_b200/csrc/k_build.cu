@@ -370,7 +370,7 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
 }
 
 template <typename T>
-cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
+cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const unsigned grid = (unsigned)(a.nbands * a.groups);
@@ -379,8 +379,10 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
     dim3 g3(grid, (unsigned)kinds);
     if (cpt == 4) k_build_fused<T, 4><<<g3, threads, 0, s>>>(a);
     else k_build_fused<T, 8><<<g3, threads, 0, s>>>(a);
+    *launches = 1;
     return cudaGetLastError();
   }
+  *launches = kinds;
   for (int kind = 0; kind < kinds; ++kind) {
     if (cpt == 4) {
       if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
@@ -397,9 +399,9 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s) {
   return cudaSuccess;
 }
 
-template cudaError_t launch_build<uint16_t>(const BuildArgs&, cudaStream_t);
-template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t);
-template cudaError_t launch_build<uint64_t>(const BuildArgs&, cudaStream_t);
+template cudaError_t launch_build<uint16_t>(const BuildArgs&, cudaStream_t, int*);
+template cudaError_t launch_build<uint32_t>(const BuildArgs&, cudaStream_t, int*);
+template cudaError_t launch_build<uint64_t>(const BuildArgs&, cudaStream_t, int*);
 
 template <typename T, typename O>
 cudaError_t launch_export(const T* tab, size_t ps, size_t pitch, int planes, int w, int h,

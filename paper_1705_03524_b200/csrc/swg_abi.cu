@@ -251,8 +251,9 @@ swg_status run_build(swg_tables* t, T* out) {
     CUDA_TRY(launch_colsum(a, c->stream));
     c->launches += 2;
   }
-  CUDA_TRY(launch_build<T>(a, c->stream));
-  c->launches += (uint64_t)t->planes;
+  int nl = 0;
+  CUDA_TRY(launch_build<T>(a, c->stream, &nl));
+  c->launches += (uint64_t)nl;
   return SWG_OK;
 }
 

@@ -148,7 +148,7 @@ constexpr int kBruteThreads = 128;
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
 cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s);
 template <typename T>
-cudaError_t launch_build(const BuildArgs& a, cudaStream_t s);
+cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
