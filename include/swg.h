@@ -72,14 +72,22 @@ typedef enum swg_format {
 
 /* Weight-plane sets.  PLAIN = {1}; AFFINE = {1, x, y}, the reference's
  * plain / xramp / yramp tables (integral_tables.hpp:53-58). */
-typedef enum swg_planes { SWG_PLANES_PLAIN = 1, SWG_PLANES_AFFINE = 3 } swg_planes;
+typedef enum swg_planes {
+  SWG_PLANES_PLAIN = 1,
+  SWG_PLANES_AFFINE = 3,
+  SWG_PLANES_QUADRATIC = 5  /* {1, x, y, x^2, y^2}, uint64 (EUCLID_QUAD maps) */
+} swg_planes;
 
 typedef enum swg_table_kind { SWG_TABLE_PLAIN = 0, SWG_TABLE_XRAMP = 1, SWG_TABLE_YRAMP = 2 } swg_table_kind;
-typedef enum swg_kernel_kind {      /* kernel.hpp:9-14 */
+typedef enum swg_kernel_kind {      /* kernel.hpp:9-14, then declared extensions */
   SWG_KERNEL_UNIFORM = 0,
   SWG_KERNEL_MANHATTAN = 1,
   SWG_KERNEL_CHEBYSHEV = 2,
-  SWG_KERNEL_GAUSS_CHEBYSHEV = 3
+  SWG_KERNEL_GAUSS_CHEBYSHEV = 3,
+  /* Declared extensions (no reference implementation):       */
+  SWG_KERNEL_EUCLID_QUAD = 4, /* w = 2(hx+1)^2(hy+1)^2 - dx^2(hy+1)^2 - dy^2(hx+1)^2,
+                                 exact on SWG_PLANES_QUADRATIC tables   */
+  SWG_KERNEL_EXP_L1 = 5       /* w = exp(-sigma*(|dx|+|dy|)), sigma = decay per pixel */
 } swg_kernel_kind;
 typedef enum swg_method { SWG_METHOD_SWIH = 0, SWG_METHOD_BRUTE = 1, SWG_METHOD_CAKE = 2, SWG_METHOD_PLAIN = 3 } swg_method;
 typedef enum swg_similarity { SWG_SIM_BHATTACHARYYA = 0, SWG_SIM_INTERSECTION = 1 } swg_similarity;

@@ -20,6 +20,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libswihref.so")
 
 UNIFORM, MANHATTAN, CHEBYSHEV, GAUSS_CHEB = 0, 1, 2, 3
+EUCLID_QUAD, EXP_L1 = 4, 5  # declared extensions (parity unpinned)
 SWIH, BRUTE, CAKE, PLAIN = 0, 1, 2, 3
 BHATTACHARYYA, INTERSECTION = 0, 1
 STRICT, CLIPPED = 0, 1

@@ -98,15 +98,16 @@ static inline int k_affine(const orc_kernel* k) {
   return k->kind == ORC_UNIFORM || k->kind == ORC_MANHATTAN;
 }
 static inline int k_integer(const orc_kernel* k) {
-  return k->kind != ORC_GAUSS_CHEB;
+  return k->kind != ORC_GAUSS_CHEB && k->kind != ORC_EXP_L1;
 }
 
 /* kernel.cpp:10-19 */
 int orc_validate_kernel(const orc_kernel* k) {
   if (k->kw < 1 || k->kh < 1) return ORC_INVALID_KERNEL;
   if (k->kw % 2 == 0 || k->kh % 2 == 0) return ORC_INVALID_KERNEL;
-  if (k->kind == ORC_GAUSS_CHEB && !(k->sigma > 0.0)) return ORC_INVALID_KERNEL;
-  if (k->kind < 0 || k->kind > 3) return ORC_INVALID_KERNEL;
+  if ((k->kind == ORC_GAUSS_CHEB || k->kind == ORC_EXP_L1) && !(k->sigma > 0.0))
+    return ORC_INVALID_KERNEL;
+  if (k->kind < 0 || k->kind > 5) return ORC_INVALID_KERNEL;
   return ORC_OK;
 }
 
@@ -138,6 +139,14 @@ int orc_weight_at(const orc_kernel* k, int dx, int dy, double* w) {
       *w = exp(-(r * r) / (2.0 * k->sigma * k->sigma));
       return ORC_OK;
     }
+    case ORC_EUCLID_QUAD: { /* declared extension, exact integer */
+      const int64_t kx = (int64_t)(hx + 1) * (hx + 1), ky = (int64_t)(hy + 1) * (hy + 1);
+      *w = (double)(2 * kx * ky - (int64_t)dx * dx * ky - (int64_t)dy * dy * kx);
+      return ORC_OK;
+    }
+    case ORC_EXP_L1: /* declared extension */
+      *w = exp(-k->sigma * (double)(iabs(dx) + iabs(dy)));
+      return ORC_OK;
   }
   return ORC_INVALID_KERNEL;
 }

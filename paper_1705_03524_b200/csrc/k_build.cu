@@ -99,17 +99,18 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V*
   }
 }
 
-// K1a: column count and y-sum of each bin of one octet over one row band.
-// agg[band][group][column][16]: words 0-7 counts, 8-15 y-sums.
+// K1a: column count, y-sum (and y^2-sum for quadratic planes) of each bin of
+// one octet over one row band.  agg[band][group][column][aw]: words 0-7
+// counts, 8-15 y-sums, 16-23 y^2-sums (aw = 24 only).
 __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
   const int band = blockIdx.x, grp = blockIdx.y;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
   const uint32_t gb = (uint32_t)grp * kOct;
-  uint32_t cnt[kOct], ys[kOct];
+  uint32_t cnt[kOct], ys[kOct], y2[kOct];
 #pragma unroll
-  for (int j = 0; j < kOct; ++j) cnt[j] = ys[j] = 0;
+  for (int j = 0; j < kOct; ++j) cnt[j] = ys[j] = y2[j] = 0;
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
     const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
@@ -118,40 +119,58 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
       const bool hit = d == (uint32_t)j;
       cnt[j] += hit ? 1u : 0u;
       ys[j] += hit ? (uint32_t)y : 0u;
+      y2[j] += hit ? (uint32_t)y * (uint32_t)y : 0u;
     }
   }
-  uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * 16);
+  uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * g.aw);
   dst[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
   dst[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
   dst[2] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
   dst[3] = make_uint4(ys[4], ys[5], ys[6], ys[7]);
-}
-
-// K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
-// Bands are visited in batches of 16 so the batch's loads are all in flight.
-__global__ void k_bandscan(uint4* agg, int nbands, size_t per_band /* uint4 */) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= per_band) return;
-  constexpr int kBatch = 16;
-  uint4 run = make_uint4(0, 0, 0, 0);
-  for (int b0 = 0; b0 < nbands; b0 += kBatch) {
-    uint4 v[kBatch];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k)
-      if (b0 + k < nbands) v[k] = agg[(size_t)(b0 + k) * per_band + i];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k)
-      if (b0 + k < nbands) {
-        agg[(size_t)(b0 + k) * per_band + i] = run;
-        run.x += v[k].x; run.y += v[k].y; run.z += v[k].z; run.w += v[k].w;
-      }
+  if (g.aw == 24) {
+    dst[4] = make_uint4(y2[0], y2[1], y2[2], y2[3]);
+    dst[5] = make_uint4(y2[4], y2[5], y2[6], y2[7]);
   }
 }
 
-// K1c body.  KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}.
+// K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
+// One warp per uint4 column of the carry array: the lanes hold 32 bands at a
+// time and a shuffle scan combines them (all loads of a batch in flight).
+__global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t per_band) {
+  const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (col >= per_band) return;
+  uint4 run = make_uint4(0, 0, 0, 0);
+  for (int b0 = 0; b0 < nbands; b0 += 32) {
+    const int b = b0 + lane;
+    uint4 v = b < nbands ? agg[(size_t)b * per_band + col] : make_uint4(0, 0, 0, 0);
+    uint4 inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc.x, off);
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc.y, off);
+      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, inc.z, off);
+      const uint32_t w = __shfl_up_sync(0xFFFFFFFFu, inc.w, off);
+      if (lane >= off) {
+        inc.x += x; inc.y += y; inc.z += z; inc.w += w;
+      }
+    }
+    if (b < nbands)
+      agg[(size_t)b * per_band + col] = make_uint4(run.x + inc.x - v.x, run.y + inc.y - v.y,
+                                                   run.z + inc.z - v.z, run.w + inc.w - v.w);
+    run.x += __shfl_sync(0xFFFFFFFFu, inc.x, 31);
+    run.y += __shfl_sync(0xFFFFFFFFu, inc.y, 31);
+    run.z += __shfl_sync(0xFFFFFFFFu, inc.z, 31);
+    run.w += __shfl_sync(0xFFFFFFFFu, inc.w, 31);
+  }
+}
+
+// K1c body.  KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}, and for the
+// quadratic planes 3 = {x^2}, 4 = {y^2} (64-bit tables only).
 template <typename T, int KIND, int CPT>
 __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp) {
   __shared__ uint32_t s_row[2][kOct * 32];
+  __shared__ T s_rowT[KIND == 3 ? 2 : 1][KIND == 3 ? kOct * 32 : 1];
   __shared__ T s_carry[kOct * 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -170,11 +189,14 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
     T tot[kOct], ex[kOct];
     uint32_t cc[CPT][kOct];
     if (live && band > 0) {  // band 0 starts from the zero row
+      // counts for kinds 0/1/3, y-sums for kind 2, y^2-sums for kind 4
       const uint4* src = reinterpret_cast<const uint4*>(
-          g.agg + (((size_t)band * g.groups + grp) * g.wa + xb) * 16 + (KIND == 2 ? 8 : 0));
+          g.agg + (((size_t)band * g.groups + grp) * g.wa + xb) * g.aw +
+          (KIND == 2 ? 8 : KIND == 4 ? 16 : 0));
+      const int st = g.aw / 4;  // uint4 per column
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        const uint4 a = src[4 * i], b = src[4 * i + 1];
+        const uint4 a = src[st * i], b = src[st * i + 1];
         cc[i][0] = a.x; cc[i][1] = a.y; cc[i][2] = a.z; cc[i][3] = a.w;
         cc[i][4] = b.x; cc[i][5] = b.y; cc[i][6] = b.z; cc[i][7] = b.w;
       }
@@ -189,7 +211,8 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
       T run = 0;
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        run += KIND == 1 ? (T)cc[i][j] * (T)(xb + i) : (T)cc[i][j];
+        const T x = (T)(xb + i);
+        run += KIND == 1 ? (T)cc[i][j] * x : KIND == 3 ? (T)cc[i][j] * x * x : (T)cc[i][j];
         t[i][j] = run;
       }
       tot[j] = run;
@@ -221,7 +244,26 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
     for (int i = 0; i < CPT; ++i) d[i] = (uint32_t)vn[i] - gb;
     if (live && y + 1 < y1) load_bins<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
     uint32_t* buf = s_row[y & 1];
-    if constexpr (KIND == 1) {
+    if constexpr (KIND == 3) {
+      // per-bin x^2 sums (64-bit: a row prefix reaches W^3/3)
+      T tot[kOct], ex[kOct];
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) {
+        T s = 0;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i)
+          s += (d[i] == (uint32_t)j) ? (T)(xb + i) * (T)(xb + i) : (T)0;
+        tot[j] = s;
+      }
+      block_exscan<kOct, T>(tot, ex, s_rowT[y & 1], lane, warp, nwarps);
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+#pragma unroll
+        for (int j = 0; j < kOct; ++j) {
+          ex[j] += (d[i] == (uint32_t)j) ? (T)(xb + i) * (T)(xb + i) : (T)0;
+          t[i][j] += ex[j];
+        }
+    } else if constexpr (KIND == 1) {
       // per-bin x sums of this thread's columns, then the block prefix
       uint32_t tot[kOct], ex[kOct];
 #pragma unroll
@@ -259,7 +301,7 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
 #pragma unroll
         for (int j = 0; j < kOct; ++j) {
           const uint32_t r = (ex[j >> 1] >> ((j & 1) << 4)) & 0xFFFFu;
-          t[i][j] += KIND == 2 ? (T)y * (T)r : (T)r;
+          t[i][j] += KIND == 2 ? (T)y * (T)r : KIND == 4 ? (T)y * (T)y * (T)r : (T)r;
         }
       }
     }
@@ -286,7 +328,12 @@ __global__ void __launch_bounds__(512) k_build_fused(const BuildArgs g) {
   switch (blockIdx.y) {
     case 0: build_body<T, 0, CPT>(g, band, grp); break;
     case 1: build_body<T, 1, CPT>(g, band, grp); break;
-    default: build_body<T, 2, CPT>(g, band, grp);
+    case 2: build_body<T, 2, CPT>(g, band, grp); break;
+    default:
+      if constexpr (sizeof(T) == 8) {
+        if (blockIdx.y == 3) build_body<T, 3, CPT>(g, band, grp);
+        else build_body<T, 4, CPT>(g, band, grp);
+      }
   }
 }
 
@@ -363,8 +410,8 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
   k_colsum<<<grid, 256, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t per_band = (size_t)a.groups * a.wa * 16 / 4;
-  k_bandscan<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
+  const size_t per_band = (size_t)a.groups * a.wa * a.aw / 4;
+  k_bandscan<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
       reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
   return cudaGetLastError();
 }
@@ -387,11 +434,19 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
     if (cpt == 4) {
       if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
       else if (kind == 1) k_build<T, 1, 4><<<grid, threads, 0, s>>>(a);
-      else k_build<T, 2, 4><<<grid, threads, 0, s>>>(a);
+      else if (kind == 2) k_build<T, 2, 4><<<grid, threads, 0, s>>>(a);
+      else if constexpr (sizeof(T) == 8) {
+        if (kind == 3) k_build<T, 3, 4><<<grid, threads, 0, s>>>(a);
+        else k_build<T, 4, 4><<<grid, threads, 0, s>>>(a);
+      }
     } else {
       if (kind == 0) k_build<T, 0, 8><<<grid, threads, 0, s>>>(a);
       else if (kind == 1) k_build<T, 1, 8><<<grid, threads, 0, s>>>(a);
-      else k_build<T, 2, 8><<<grid, threads, 0, s>>>(a);
+      else if (kind == 2) k_build<T, 2, 8><<<grid, threads, 0, s>>>(a);
+      else if constexpr (sizeof(T) == 8) {
+        if (kind == 3) k_build<T, 3, 8><<<grid, threads, 0, s>>>(a);
+        else k_build<T, 4, 8><<<grid, threads, 0, s>>>(a);
+      }
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -188,6 +188,69 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+// K2q: declared Euclidean extension, w = A - ky*dx^2 - kx*dy^2 with
+// kx = (hx+1)^2, ky = (hy+1)^2, A = 2*kx*ky.  Over the whole window box,
+//   H = A*N - ky*(Sxx - 2cx*Sx + cx^2*N) - kx*(Syy - 2cy*Sy + cy^2*N)
+// from the five planes {1, x, y, x^2, y^2}; exact modulo 2^64, and the true
+// value is < 2^53 (checked on the host), so the double conversion is exact.
+// Tables are uint64: a lane reads 32 bytes (4 bins) per corner.
+template <int SIM>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
+  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
+  const int r0 = blockIdx.y * kSweepTileY + warp;
+  const bool active = u0 < a.mw && r0 < a.rows;
+  const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
+  const int v = a.row0 + r;
+  const int cx = u + a.hx, cy = v + a.hy;
+  const size_t centre = ((size_t)cy * a.pitch + (size_t)cx) * kOct + half * 4;
+  const size_t ps8 = a.plane_stride * kOct;
+  const uint64_t kx = (uint64_t)(a.hx + 1) * (a.hx + 1), ky = (uint64_t)(a.hy + 1) * (a.hy + 1);
+  const uint64_t A = 2 * kx * ky, ucx = (uint64_t)cx, ucy = (uint64_t)cy;
+
+  double s = 0.0, unused = 0.0;
+  for (int g = 0; g < a.groups; ++g) {
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint64_t*>(a.tab) +
+                                                  (size_t)g * a.planes * ps8 + centre);
+    uint64_t box[5][4];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      uint64_t c4[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const ulonglong2 lo = __ldg(reinterpret_cast<const ulonglong2*>(w + a.lat[4 * p + q]));
+        const ulonglong2 hi = __ldg(reinterpret_cast<const ulonglong2*>(w + a.lat[4 * p + q] + 16));
+        c4[q][0] = lo.x; c4[q][1] = lo.y; c4[q][2] = hi.x; c4[q][3] = hi.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) box[p][k] = c4[3][k] - c4[2][k] - c4[1][k] + c4[0][k];
+    }
+    double val[4], term[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t n = box[0][k];
+      const uint64_t h = A * n - ky * (box[3][k] - 2 * ucx * box[1][k] + ucx * ucx * n) -
+                         kx * (box[4][k] - 2 * ucy * box[2][k] + ucy * ucy * n);
+      val[k] = (double)h;
+      const double model = a.model[g * kOct + half * 4 + k];
+      if (h == 0) {
+        term[k] = 0.0;
+      } else if (SIM == SWG_SIM_BHATTACHARYYA) {
+        term[k] = __dsqrt_rn(__dmul_rn(model, val[k]));
+      } else {
+        const double q = __ddiv_rn(val[k], a.mass);
+        term[k] = (q < model) ? q : model;
+      }
+    }
+    add_octet(val, term, half, unused, s, false);
+  }
+  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
+  s = clamp01(s);
+  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
+             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
 // K2c: wedding-cake telescoping over nested boxes of the plain table.
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
@@ -482,6 +545,12 @@ cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake<0><<<grid, kSweepThreads, 0, s>>>(a, r);
   else k_sweep_cake<1><<<grid, kSweepThreads, 0, s>>>(a, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad<0><<<grid, kSweepThreads, 0, s>>>(a);
+  else k_sweep_quad<1><<<grid, kSweepThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -79,14 +79,16 @@ int k_hy(const swg_kernel& k) { return (k.kh - 1) / 2; }
 bool k_affine(const swg_kernel& k) {
   return k.kind == SWG_KERNEL_UNIFORM || k.kind == SWG_KERNEL_MANHATTAN;
 }
-bool k_integer(const swg_kernel& k) { return k.kind != SWG_KERNEL_GAUSS_CHEBYSHEV; }
+bool k_integer(const swg_kernel& k) {
+  return k.kind != SWG_KERNEL_GAUSS_CHEBYSHEV && k.kind != SWG_KERNEL_EXP_L1;
+}
 
 swg_status validate_kernel(const swg_kernel& k) {  // kernel.cpp:10-19
-  if (k.kind < 0 || k.kind > 3) return fail(SWG_ERR_INVALID_KERNEL, "kernel: unknown kind");
+  if (k.kind < 0 || k.kind > 5) return fail(SWG_ERR_INVALID_KERNEL, "kernel: unknown kind");
   if (k.kw < 1 || k.kh < 1) return fail(SWG_ERR_INVALID_KERNEL, "kernel: dimensions must be >= 1");
   if (k.kw % 2 == 0 || k.kh % 2 == 0)
     return fail(SWG_ERR_INVALID_KERNEL, "kernel: dimensions must be odd, got %dx%d", k.kw, k.kh);
-  if (k.kind == SWG_KERNEL_GAUSS_CHEBYSHEV && !(k.sigma > 0.0))
+  if ((k.kind == SWG_KERNEL_GAUSS_CHEBYSHEV || k.kind == SWG_KERNEL_EXP_L1) && !(k.sigma > 0.0))
     return fail(SWG_ERR_INVALID_KERNEL, "kernel: sigma must be positive");
   return SWG_OK;
 }
@@ -105,6 +107,12 @@ double weight_at(const swg_kernel& k, int dx, int dy) {  // kernel.cpp:25-59
       const long level = std::lround(std::max(sx, sy));
       return static_cast<double>(hmax + 1 - level);
     }
+    case SWG_KERNEL_EUCLID_QUAD: {  // declared extension
+      const int64_t kx = int64_t(hx + 1) * (hx + 1), ky = int64_t(hy + 1) * (hy + 1);
+      return static_cast<double>(2 * kx * ky - int64_t(dx) * dx * ky - int64_t(dy) * dy * kx);
+    }
+    case SWG_KERNEL_EXP_L1:  // declared extension
+      return std::exp(-k.sigma * static_cast<double>(std::abs(dx) + std::abs(dy)));
     default: {
       const double nx = static_cast<double>(std::abs(dx)) / std::max(hx, 1);
       const double ny = static_cast<double>(std::abs(dy)) / std::max(hy, 1);
@@ -112,6 +120,15 @@ double weight_at(const swg_kernel& k, int dx, int dy) {  // kernel.cpp:25-59
       return std::exp(-(r * r) / (2.0 * k.sigma * k.sigma));
     }
   }
+}
+
+// Exact strict-window mass of the quadratic (Euclidean) extension:
+// sum of A - ky*dx^2 - kx*dy^2 over the window.
+int64_t quad_mass(const swg_kernel& k) {
+  const int64_t hx = k_hx(k), hy = k_hy(k);
+  const int64_t kx = (hx + 1) * (hx + 1), ky = (hy + 1) * (hy + 1);
+  const int64_t sdx = hx * (hx + 1) * (2 * hx + 1) / 3, sdy = hy * (hy + 1) * (2 * hy + 1) / 3;
+  return 2 * kx * ky * k.kw * k.kh - ky * k.kh * sdx - kx * k.kw * sdy;
 }
 
 // Exact strict-window mass of an integer affine kernel (kernel.cpp:61-75).
@@ -246,6 +263,7 @@ swg_status run_build(swg_tables* t, T* out) {
   a.band_h = t->band_h;
   a.nbands = t->nbands;
   a.wa = t->wa;
+  a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : 16;
   a.agg = t->lb;
   if (t->nbands > 1) {
     CUDA_TRY(launch_colsum(a, c->stream));
@@ -426,8 +444,11 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   *out = nullptr;
   if (width < 1 || height < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
   if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
-  if (planes != SWG_PLANES_PLAIN && planes != SWG_PLANES_AFFINE)
+  if (planes != SWG_PLANES_PLAIN && planes != SWG_PLANES_AFFINE &&
+      planes != SWG_PLANES_QUADRATIC)
     return fail(SWG_ERR_ARG, "planes %d", planes);
+  if (planes == SWG_PLANES_QUADRATIC && height > 2340)  // column y^2-sums stay < 2^32
+    return fail(SWG_ERR_SIZE, "quadratic planes: height %d > 2340", height);
   int nb = bins;
   if (format == SWG_FMT_RGB8) {
     if (bins < 1 || bins > 40) return fail(SWG_ERR, "RGB levels must be in [1, 40]");
@@ -455,9 +476,10 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   choose_bands(t);
   // plain-only tables keep narrow uint16 planes (32-bit ones are built on
   // demand); affine tables keep uint32 planes
-  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : 4;
+  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_QUADRATIC ? 8 : 4;
   const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * elem;
-  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * 16 * 4;
+  const size_t lb_bytes =
+      (size_t)t->nbands * t->groups * t->wa * (planes == SWG_PLANES_QUADRATIC ? 24 : 16) * 4;
   const size_t need = tab_bytes + lb_bytes + t->fip * height * 2;
   if (memory_budget && need > memory_budget) {
     swg_tables_destroy(t);
@@ -470,8 +492,9 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
     return st;
   };
   cudaError_t e;
-  if ((e = elem == 2 ? cudaMalloc(&t->t16, tab_bytes) : cudaMalloc(&t->t32, tab_bytes)) !=
-          cudaSuccess ||
+  if ((e = elem == 2   ? cudaMalloc(&t->t16, tab_bytes)
+           : elem == 8 ? cudaMalloc(&t->t64, tab_bytes)
+                       : cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
       (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
     g_required = need;
@@ -481,7 +504,10 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   }
   t->bytes = need;
   swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
-  if (st == SWG_OK) st = t->t16 ? run_build<uint16_t>(t, t->t16) : run_build<uint32_t>(t, t->t32);
+  if (st == SWG_OK)
+    st = t->t16   ? run_build<uint16_t>(t, t->t16)
+         : t->t64 ? run_build<uint64_t>(t, t->t64)
+                  : run_build<uint32_t>(t, t->t32);
   if (st != SWG_OK) return cleanup(st);
   *out = t;
   return SWG_OK;
@@ -643,6 +669,7 @@ swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
+  if (kind >= 3) return fail(SWG_ERR_OUT_OF_RANGE, "quadratic planes are 64-bit only");
   ST_TRY(ensure_t32(t));
   return export_planes<uint32_t, uint32_t>(t, t->t32, kind, b0, b1, out);
 }
@@ -956,9 +983,17 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     if (!r.model) return fail(SWG_ERR_MODEL, "likelihood map: model must be normalized with %d bins", t->bins);
     if (r.method < 0 || r.method > 3) return fail(SWG_ERR_ARG, "method %d", r.method);
     if (r.sim < 0 || r.sim > 1) return fail(SWG_ERR_ARG, "similarity %d", r.sim);
-    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel))
+    const bool quad = r.kernel.kind == SWG_KERNEL_EUCLID_QUAD;
+    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel) && !quad)
       return fail(SWG_ERR_UNSUPPORTED_KERNEL,
                   "likelihood map: method swih requires a quadrant-affine kernel");
+    if (r.method == SWG_METHOD_SWIH && quad) {
+      if (t->planes != SWG_PLANES_QUADRATIC)
+        return fail(SWG_ERR_CONFIG, "likelihood map: Euclidean swih needs quadratic planes");
+      if (quad_mass(r.kernel) >= (int64_t(1) << 53))
+        return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the exact fp64 range",
+                    r.kernel.kw, r.kernel.kh);
+    }
     if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
     const bool needs_ramps = (r.method == SWG_METHOD_SWIH || r.method == SWG_METHOD_BRUTE) &&
                              r.kernel.kind == SWG_KERNEL_MANHATTAN;
@@ -990,7 +1025,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // and shares its kernel; a Uniform box is a one-ring cake with coefficient
   // 1.0 (exact integer weights, same scores: score_counts == score_weights on
   // integers), so on narrow tables it runs the 16-bit cake sweep.
-  enum Engine { kAffine32, kCake16, kCake32, kBrute };
+  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad64 };
   std::vector<dim3> grid(n);
   std::vector<int> engine(n);
   std::vector<swg_kernel> kern(n);
@@ -1013,6 +1048,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       method = SWG_METHOD_SWIH;
     const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
     if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
+    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad64;
     else if (method == SWG_METHOD_CAKE) engine[i] = (t->t16 && small) ? kCake16 : kCake32;
     else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
     else engine[i] = kAffine32;
@@ -1043,7 +1079,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       if (engine[i] == kAffine32 || engine[i] == kCake32) ST_TRY(ensure_t32(t));
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
       const swg_kernel k = kern[i];
-      a.tab = engine[i] == kCake16 ? (const void*)t->t16 : (const void*)t->t32;
+      a.tab = engine[i] == kCake16   ? (const void*)t->t16
+              : engine[i] == kQuad64 ? (const void*)t->t64
+                                     : (const void*)t->t32;
       a.plane_stride = t->ps;
       a.pitch = t->pitch;
       a.planes = t->planes;
@@ -1059,7 +1097,17 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       a.parts = parts;
       std::memset(a.model, 0, sizeof(a.model));
       std::memcpy(a.model, r.model, sizeof(double) * t->bins);
-      if (engine[i] == kAffine32) {
+      if (engine[i] == kQuad64) {
+        a.mass = (double)quad_mass(k);
+        // box corners (TL, TR, BL, BR) of the whole window, per plane, as byte
+        // offsets from the centre record of the 64-bit tables
+        const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
+        const long long xs[2] = {-a.hx, a.hx + 1}, ys[2] = {-a.hy, a.hy + 1};
+        for (int pl = 0; pl < 5; ++pl)
+          for (int q = 0; q < 4; ++q)
+            a.lat[4 * pl + q] = (int)(8 * (pl * ps8 + ys[q >> 1] * p8 + xs[q & 1] * kOct));
+        CUDA_TRY(launch_sweep_quad(a, grid[i], c->stream));
+      } else if (engine[i] == kAffine32) {
         a.mass = (double)affine_mass(k);
         {  // corner byte offsets from the centre record (SweepArgs::lat order)
           const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;

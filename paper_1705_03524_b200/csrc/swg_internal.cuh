@@ -57,9 +57,10 @@ struct BuildArgs {
   int w, h, bins, groups, planes;
   int band_h, nbands;
   size_t wa;           // padded width (columns) of the carry array
-  uint32_t* agg;       // [nbands][groups][wa][16]: per column, 8 bin counts +
-                       // 8 bin y-sums of the band (K1a), then of all rows
-                       // above the band (K1b, exclusive scan over bands)
+  int aw;              // carry words per column: 16, or 24 with quadratic planes
+  uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
+                       // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
+                       // then of all rows above the band (K1b, exclusive scan)
 };
 
 struct QuantArgs {
@@ -152,6 +153,7 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
+cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                                 cudaStream_t s);
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,

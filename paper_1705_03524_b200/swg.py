@@ -25,9 +25,10 @@ LIB_PATH = os.environ.get("SWG_LIB", _build.LIB)
 
 # enums (include/swg.h)
 FMT_GRAY8, FMT_GRAY16, FMT_RGB8, FMT_BINS16 = 0, 1, 2, 3
-PLANES_PLAIN, PLANES_AFFINE = 1, 3
+PLANES_PLAIN, PLANES_AFFINE, PLANES_QUADRATIC = 1, 3, 5
 TABLE_PLAIN, TABLE_XRAMP, TABLE_YRAMP = 0, 1, 2
 UNIFORM, MANHATTAN, CHEBYSHEV, GAUSS_CHEB = 0, 1, 2, 3
+EUCLID_QUAD, EXP_L1 = 4, 5  # declared extensions
 SWIH, BRUTE, CAKE, PLAIN = 0, 1, 2, 3
 BHATTACHARYYA, INTERSECTION = 0, 1
 STRICT, CLIPPED = 0, 1

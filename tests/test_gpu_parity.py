@@ -410,3 +410,66 @@ def test_narrow_and_wide_plain_paths(ctx, oracle):
             got, pk = t.likelihood_map(K(kind, kw, kh, 0.5), mdl, method, rings=rings)
             assert (got == want).all(), (kw, kh, kind)
             assert pk == oracle.peak(want, kw // 2, kh // 2)
+
+
+# ------------------------------------------------------------------ declared extensions
+def test_quadratic_planes_exact(ctx, oracle):
+    """x^2 / y^2 planes of the quadratic table set, exact int64."""
+    img = oracle.random_gray(77, 61, 3)
+    bins = 5
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC)
+    p, x, y = oracle.build_tables(fi, bins)
+    assert (t.export_i64(0) == p).all() and (t.export_i64(1) == x).all()
+    assert (t.export_i64(2) == y).all()
+    yy, xx = np.mgrid[0:61, 0:77].astype(np.int64)
+    for kind, wgt in ((3, xx * xx), (4, yy * yy)):
+        got = t.export_i64(kind)
+        for b in range(bins):
+            want = np.zeros((62, 78), np.int64)
+            want[1:, 1:] = np.cumsum(np.cumsum((fi == b) * wgt, 0), 1)
+            assert (got[b] == want).all(), (kind, b)
+
+
+@pytest.mark.parametrize("bins", [8, 16])
+def test_euclid_quadratic_maps_exact(ctx, oracle, bins):
+    """Declared Euclidean kernel on quadratic planes (O(1)) == the oracle's
+    brute-force map bit for bit; the GPU brute force agrees too."""
+    img = oracle.random_gray(150, 120, bins)
+    fi = oracle.quantize_gray8(img, bins)
+    tq = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC)
+    tp = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    for kw, kh in ((1, 1), (5, 5), (9, 7), (31, 31), (45, 59)):
+        ok = O.kernel(O.EUCLID_QUAD, kw, kh)
+        mdl = oracle.target_model(fi[10:10 + kh, 20:20 + kw].copy(), bins, ok, O.BRUTE)
+        for sim in (swg.BHATTACHARYYA, swg.INTERSECTION):
+            want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE, sim)
+            got, pk = tq.likelihood_map(K(swg.EUCLID_QUAD, kw, kh), mdl, swg.SWIH, sim)
+            assert (got == want).all(), (kw, kh, sim)
+            assert pk == oracle.peak(want, kw // 2, kh // 2)
+        got_b, _ = tp.likelihood_map(K(swg.EUCLID_QUAD, kw, kh), mdl, swg.BRUTE)
+        assert (got_b == oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)).all()
+    with pytest.raises(swg.ConfigError):
+        tp.likelihood_map(K(swg.EUCLID_QUAD, 5, 5), np.full(bins, 1 / bins), swg.SWIH)
+
+
+def test_exponential_brute_and_cake(ctx, oracle):
+    """Declared exponential kernel: GPU brute force == oracle brute force
+    (same fp64 pixel order); exact ring telescope is not applicable (not
+    ring-constant), the cake path is checked as an approximation route."""
+    img = oracle.random_gray(96, 80, 5)
+    bins = 8
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    for kw, lam in ((9, 0.25), (21, 0.1)):
+        ok = O.kernel(O.EXP_L1, kw, kw, lam)
+        mdl = oracle.target_model(fi[:kw, :kw].copy(), bins, ok, O.BRUTE)
+        want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)
+        got, pk = t.likelihood_map(K(swg.EXP_L1, kw, kw, lam), mdl, swg.BRUTE)
+        assert (got == want).all()
+        assert pk == oracle.peak(want, kw // 2, kw // 2)
+        r = kw // 2 + 1
+        mc = oracle.target_model(fi[:kw, :kw].copy(), bins, ok, O.CAKE, r)
+        want_c = oracle.likelihood_map(fi, bins, mc, ok, O.CAKE, rings=r)
+        got_c, _ = t.likelihood_map(K(swg.EXP_L1, kw, kw, lam), mc, swg.CAKE, rings=r)
+        assert (got_c == want_c).all()
