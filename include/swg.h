@@ -75,7 +75,9 @@ typedef enum swg_format {
 typedef enum swg_planes {
   SWG_PLANES_PLAIN = 1,
   SWG_PLANES_AFFINE = 3,
-  SWG_PLANES_QUADRATIC = 5  /* {1, x, y, x^2, y^2}, uint64 (EUCLID_QUAD maps) */
+  SWG_PLANES_QUADRATIC = 5, /* {1, x, y, x^2, y^2}, uint64 (EUCLID_QUAD maps) */
+  SWG_PLANES_DECAY = 4      /* SE/SW/NE/NW decayed tables, fp64 (EXP_L1 maps);
+                               built by swg_tables_build_decay          */
 } swg_planes;
 
 typedef enum swg_table_kind { SWG_TABLE_PLAIN = 0, SWG_TABLE_XRAMP = 1, SWG_TABLE_YRAMP = 2 } swg_table_kind;
@@ -87,7 +89,8 @@ typedef enum swg_kernel_kind {      /* kernel.hpp:9-14, then declared extensions
   /* Declared extensions (no reference implementation):       */
   SWG_KERNEL_EUCLID_QUAD = 4, /* w = 2(hx+1)^2(hy+1)^2 - dx^2(hy+1)^2 - dy^2(hx+1)^2,
                                  exact on SWG_PLANES_QUADRATIC tables   */
-  SWG_KERNEL_EXP_L1 = 5       /* w = exp(-sigma*(|dx|+|dy|)), sigma = decay per pixel */
+  SWG_KERNEL_EXP_L1 = 5       /* w = sigma^(|dx|+|dy|), sigma in (0,1) = decay per pixel;
+                                 O(1) on SWG_PLANES_DECAY tables built with that sigma */
 } swg_kernel_kind;
 typedef enum swg_method { SWG_METHOD_SWIH = 0, SWG_METHOD_BRUTE = 1, SWG_METHOD_CAKE = 2, SWG_METHOD_PLAIN = 3 } swg_method;
 typedef enum swg_similarity { SWG_SIM_BHATTACHARYYA = 0, SWG_SIM_INTERSECTION = 1 } swg_similarity;
@@ -165,6 +168,16 @@ swg_status swg_tables_build(swg_ctx* ctx, const void* pixels, int is_device,
                             size_t pitch_bytes, int width, int height,
                             int format, int bins, int planes,
                             size_t memory_budget, swg_tables** out);
+/* Decayed directional tables for the exponential kernel with per-pixel
+ * decay `decay` in (0, 1) (declared extension): E(X,Y) = sum over x<X, y<Y
+ * of [bin] decay^(X-1-x) decay^(Y-1-y), for the image and its horizontal,
+ * vertical and double flip.  EXP_L1 maps with sigma == decay run in O(1) per
+ * window and bin; their peak is made exact by an fp64 brute-force re-score
+ * of every window within 1e-4 of the fast maximum. */
+swg_status swg_tables_build_decay(swg_ctx* ctx, const void* pixels, int is_device,
+                                  size_t pitch_bytes, int width, int height, int format,
+                                  int bins, double decay, size_t memory_budget,
+                                  swg_tables** out);
 /* Re-run quantise + build for a new frame of the same geometry into the
  * same device buffers (no allocation; stream ordered, asynchronous). */
 swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
@@ -183,9 +196,17 @@ swg_status swg_tables_export_i64(swg_tables* t, int kind, int bin_begin,
 /* The stored 32-bit words (exact value mod 2^32), reference layout. */
 swg_status swg_tables_export_u32(swg_tables* t, int kind, int bin_begin,
                                  int bin_end, uint32_t* host_out);
+/* Decay tables only: copy decayed planes [b0, b1) of orientation `kind`
+ * (0 SE = image, 1 horizontal flip, 2 vertical flip, 3 both) to host
+ * memory as b1-b0 planes of (height+1) x (width+1) doubles, zero row and
+ * column 0 (in the flipped image's own coordinates). */
+swg_status swg_tables_export_f64(swg_tables* t, int kind, int b0, int b1,
+                                 double* host_out);
 /* The quantised feature image (uint16 bins, w*h). */
 swg_status swg_tables_feature_image(swg_tables* t, uint16_t* host_out);
-/* Device pointer + geometry of the 32-bit planes (for tests / bench).
+/* Device pointer + geometry of the 32-bit planes (for tests / bench); of
+ * the fp64 decayed planes (kinds 0..3 = SE, h-flip, v-flip, hv-flip) for
+ * decay tables.
  * Bins are tiled in records of 8 ("bin octets"): element (x, y) of bin b,
  * table kind k sits at
  *   base[(((b/8)*planes + k)*plane_stride + y*pitch + x)*8 + b%8]

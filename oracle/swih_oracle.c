@@ -107,6 +107,7 @@ int orc_validate_kernel(const orc_kernel* k) {
   if (k->kw % 2 == 0 || k->kh % 2 == 0) return ORC_INVALID_KERNEL;
   if ((k->kind == ORC_GAUSS_CHEB || k->kind == ORC_EXP_L1) && !(k->sigma > 0.0))
     return ORC_INVALID_KERNEL;
+  if (k->kind == ORC_EXP_L1 && !(k->sigma < 1.0)) return ORC_INVALID_KERNEL;
   if (k->kind < 0 || k->kind > 5) return ORC_INVALID_KERNEL;
   return ORC_OK;
 }
@@ -144,8 +145,8 @@ int orc_weight_at(const orc_kernel* k, int dx, int dy, double* w) {
       *w = (double)(2 * kx * ky - (int64_t)dx * dx * ky - (int64_t)dy * dy * kx);
       return ORC_OK;
     }
-    case ORC_EXP_L1: /* declared extension */
-      *w = exp(-k->sigma * (double)(iabs(dx) + iabs(dy)));
+    case ORC_EXP_L1: /* declared extension: sigma = decay per pixel, 0 < sigma < 1 */
+      *w = pow(k->sigma, (double)(iabs(dx) + iabs(dy)));
       return ORC_OK;
   }
   return ORC_INVALID_KERNEL;

@@ -43,7 +43,7 @@ enum {
 /* KernelKind order of proj/include/swih/kernel.hpp:9-14, then the declared
  * extensions of SURVEY App. A (no reference implementation: parity unpinned):
  *   ORC_EUCLID_QUAD  w = 2(hx+1)^2(hy+1)^2 - dx^2(hy+1)^2 - dy^2(hx+1)^2
- *   ORC_EXP_L1       w = exp(-sigma * (|dx| + |dy|))   (sigma = decay / px) */
+ *   ORC_EXP_L1       w = sigma^(|dx| + |dy|)   (sigma = decay per pixel in (0,1)) */
 enum { ORC_UNIFORM = 0, ORC_MANHATTAN = 1, ORC_CHEBYSHEV = 2, ORC_GAUSS_CHEB = 3,
        ORC_EUCLID_QUAD = 4, ORC_EXP_L1 = 5 };
 /* MapMethod order of proj/include/swih/matching.hpp:25 */

@@ -1,0 +1,298 @@
+// k_decay.cu — decayed directional integral tables for the exponential
+// kernel w = d^(|dx| + |dy|), d = exp(-lambda) (declared extension).
+//
+// The paper's directional weighted integral histograms IH_w (Eq. 2,
+// the {SE, SW, NE, NW} quadrant weights) become, for an exponential kernel,
+// DECAYED prefix sums
+//   E(X, Y) = sum_{x < X, y < Y} f(x, y) d^(X-1-x) d^(Y-1-y)
+// whose values stay bounded (<= 1/(1-d)^2) where e^{+lambda x} planes would
+// overflow.  A quadrant rectangle [x0,x1] x [y0,y1] weighted by
+// d^(x1-x) d^(y1-y) is then
+//   E(x1+1,y1+1) - d^(x1-x0+1) E(x0,y1+1) - d^(y1-y0+1) E(x1+1,y0)
+//                + d^(x1-x0+1) d^(y1-y0+1) E(x0,y0).
+// The four orientations are the same SE table built on the feature image
+// flipped horizontally / vertically / both (k_flip), so one build pipeline
+// serves all four.  It mirrors the integer build: K1a' decayed column sums
+// per band, K1b' decayed scan over bands, K1c' per (band, octet) CTA with a
+// block-wide affine scan per row and t = d*t + R per column.  fp64 storage
+// and recurrences: fp32 noise (~1e-7 of the table values) is comparable to
+// the smallest quadrant contributions at large windows and Bhattacharyya's
+// sqrt amplifies it; fp64 keeps every map value within 1e-9 of the exact
+// fp64 brute force (tolerance-based parity).
+#include "swg_internal.cuh"
+
+#include <math.h>
+
+namespace swg {
+
+namespace {
+
+using real = double;
+
+// Exclusive block scan of y -> alpha*y + B_t over threads (alpha shared by
+// all threads, 8 independent B components): returns the value entering each
+// thread.  One __syncthreads; `buf` ([8][32]) alternates between calls.
+__device__ __forceinline__ void block_exscan_decay(const real (&B)[kOct], real alpha,
+                                                   real (&enter)[kOct], real* buf, int lane,
+                                                   int warp, int nwarps) {
+  real inc[kOct];
+#pragma unroll
+  for (int j = 0; j < kOct; ++j) inc[j] = B[j];
+  real ap = alpha;  // alpha^off
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) {
+      const real t = __shfl_up_sync(0xFFFFFFFFu, inc[j], off);
+      if (lane >= off) inc[j] = fma(ap, t, inc[j]);
+    }
+    ap *= ap;
+  }
+  const real a32 = ap;  // alpha^32
+  if (lane == 31) {
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) buf[j * 32 + warp] = inc[j];
+  }
+  __syncthreads();
+  // value entering warp w: sum_{v<w} a32^(w-1-v) W_v (each warp scans the totals)
+  real alane = 1.0;  // alpha^lane
+  {
+    real p = alpha;
+    for (int k = lane; k; k >>= 1) {
+      if (k & 1) alane *= p;
+      p *= p;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kOct; ++j) {
+    real wt = lane < nwarps ? buf[j * 32 + lane] : 0.0;
+    real bp = a32;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const real t = __shfl_up_sync(0xFFFFFFFFu, wt, off);
+      if (lane >= off) wt = fma(bp, t, wt);
+      bp *= bp;
+    }
+    const real warp_enter = warp > 0 ? __shfl_sync(0xFFFFFFFFu, wt, warp - 1) : 0.0;
+    const real lane_prev = __shfl_up_sync(0xFFFFFFFFu, inc[j], 1);
+    enter[j] = fma(alane, warp_enter, lane > 0 ? lane_prev : 0.0);
+  }
+}
+
+// K0': flipped copies of the feature image (h: x -> W-1-x, v: y -> H-1-y).
+__global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
+                       uint16_t* fv, uint16_t* fhv) {
+  const int y = blockIdx.y;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < (int)pitch;
+       x += gridDim.x * blockDim.x) {
+    const bool in = x < w;
+    const uint16_t a = in ? fi[(size_t)y * pitch + (w - 1 - x)] : kNoBin;
+    const uint16_t b = fi[(size_t)(h - 1 - y) * pitch + x];
+    const uint16_t c = in ? fi[(size_t)(h - 1 - y) * pitch + (w - 1 - x)] : kNoBin;
+    fh[(size_t)y * pitch + x] = a;
+    fv[(size_t)y * pitch + x] = b;
+    fhv[(size_t)y * pitch + x] = c;
+  }
+}
+
+// K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
+__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec) {
+  const int band = blockIdx.x, grp = blockIdx.y;
+  const int x = blockIdx.z * blockDim.x + threadIdx.x;
+  if (x >= g.w) return;
+  const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
+  const uint32_t gb = (uint32_t)grp * kOct;
+  real c[kOct];
+#pragma unroll
+  for (int j = 0; j < kOct; ++j) c[j] = 0.0;
+  const uint16_t* col = g.fi + x;
+  for (int y = y0; y < y1; ++y) {
+    const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) c[j] = fma(dec, c[j], d == (uint32_t)j ? 1.0 : 0.0);
+  }
+  double2* dst = reinterpret_cast<double2*>(reinterpret_cast<real*>(g.agg) +
+                                             (((size_t)band * g.groups + grp) * g.wa + x) * kOct);
+  dst[0] = make_double2(c[0], c[1]);
+  dst[1] = make_double2(c[2], c[3]);
+  dst[2] = make_double2(c[4], c[5]);
+  dst[3] = make_double2(c[6], c[7]);
+}
+
+// K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place);
+// one warp per column word, lanes = 32 bands, affine shuffle scan.
+__global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, int band_h,
+                                                        int h, real dec, size_t per_band) {
+  const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (col >= per_band) return;
+  real run = 0.0;
+  for (int b0 = 0; b0 < nbands; b0 += 32) {
+    const int b = b0 + lane;
+    const int hb = b < nbands ? min(band_h, h - b * band_h) : 0;
+    real ia = b < nbands ? pow(dec, (real)hb) : 1.0;
+    real inc = b < nbands ? agg[(size_t)b * per_band + col] : 0.0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const real pa = __shfl_up_sync(0xFFFFFFFFu, ia, off);
+      const real pv = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+      if (lane >= off) {
+        inc = fma(ia, pv, inc);
+        ia *= pa;
+      }
+    }
+    const real pa = __shfl_up_sync(0xFFFFFFFFu, ia, 1);
+    const real pv = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+    const real ent = lane > 0 ? fma(pa, run, pv) : run;
+    if (b < nbands) agg[(size_t)b * per_band + col] = ent;
+    run = fma(__shfl_sync(0xFFFFFFFFu, ia, 31), run, __shfl_sync(0xFFFFFFFFu, inc, 31));
+  }
+}
+
+template <int CPT>
+__device__ __forceinline__ void load_bins_d(const uint16_t* p, uint16_t (&v)[CPT]) {
+  if constexpr (CPT == 4) {
+    const uint2 q = *reinterpret_cast<const uint2*>(p);
+    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+  } else {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+    v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
+  }
+}
+
+__device__ __forceinline__ void store_rec_f(real* dst, const real (&v)[kOct]) {
+  double2* d = reinterpret_cast<double2*>(dst);
+  d[0] = make_double2(v[0], v[1]);
+  d[1] = make_double2(v[2], v[3]);
+  d[2] = make_double2(v[4], v[5]);
+  d[3] = make_double2(v[6], v[7]);
+}
+
+// K1c': decayed SE table of one orientation: one CTA per (band, octet).
+template <int CPT>
+__global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec, int kind) {
+  __shared__ real s_row[2][kOct * 32];
+  __shared__ real s_carry[kOct * 32];
+  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
+  const int xb = tid * CPT;
+  const bool live = xb < g.w;
+  const uint16_t* fi = g.fi + (live ? xb : 0);
+  const uint32_t gb = (uint32_t)grp * kOct;
+  real dp[CPT + 1];  // d^i
+  dp[0] = 1.0;
+#pragma unroll
+  for (int i = 1; i <= CPT; ++i) dp[i] = dp[i - 1] * dec;
+  const real alpha = dp[CPT];
+
+  // decayed row prefix of per-column values v[i][j] along x, into r[i][j]
+  auto row_prefix = [&](const real (&v)[CPT][kOct], real (&r)[CPT][kOct], real* buf) {
+    real tot[kOct], ent[kOct];
+#pragma unroll
+    for (int j = 0; j < kOct; ++j) {
+      real run = 0.0;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        run = fma(dec, run, v[i][j]);
+        r[i][j] = run;
+      }
+      tot[j] = run;
+    }
+    block_exscan_decay(tot, alpha, ent, buf, lane, warp, nwarps);
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) r[i][j] = fma(dp[i + 1], ent[j], r[i][j]);
+  };
+
+  // carry row E(x+1, y0) from the decayed column sums above the band
+  real t[CPT][kOct];
+  {
+    real cc[CPT][kOct];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) cc[i][j] = 0.0;
+    if (live && band > 0) {
+      const real* src = reinterpret_cast<const real*>(g.agg) +
+                        (((size_t)band * g.groups + grp) * g.wa + xb) * kOct;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+#pragma unroll
+        for (int j = 0; j < kOct; ++j) cc[i][j] = src[i * kOct + j];
+    }
+    row_prefix(cc, t, s_carry);
+  }
+
+  real* plane = reinterpret_cast<real*>(g.out) +
+                 ((size_t)grp * g.planes + kind) * g.plane_stride * kOct;
+  const real zero[kOct] = {};
+  if (band == 0) {
+    if (live)
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) store_rec_f(plane + (size_t)(xb + 1 + i) * kOct, zero);
+    if (tid == 0) store_rec_f(plane, zero);
+  }
+  uint16_t vn[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) vn[i] = kNoBin;
+  if (live && y0 < y1) load_bins_d<CPT>(fi + (size_t)y0 * g.fi_pitch, vn);
+  for (int y = y0; y < y1; ++y) {
+    real ind[CPT][kOct];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const uint32_t d = (uint32_t)vn[i] - gb;
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) ind[i][j] = d == (uint32_t)j ? 1.0 : 0.0;
+    }
+    if (live && y + 1 < y1) load_bins_d<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
+    real r[CPT][kOct];
+    row_prefix(ind, r, s_row[y & 1]);
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int j = 0; j < kOct; ++j) t[i][j] = fma(dec, t[i][j], r[i][j]);
+    real* row = plane + (size_t)(y + 1) * g.pitch * kOct;
+    if (live)
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) store_rec_f(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+    if (tid == 0) store_rec_f(row, zero);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
+                        uint16_t* fv, uint16_t* fhv, cudaStream_t s) {
+  dim3 grid((unsigned)((pitch + 255) / 256), (unsigned)h);
+  k_flip<<<grid, 256, 0, s>>>(fi, pitch, w, h, fh, fv, fhv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
+                               int* launches) {
+  *launches = 0;
+  if (a.nbands > 1) {
+    dim3 grid((unsigned)a.nbands, (unsigned)a.groups, (unsigned)((a.w + 255) / 256));
+    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t per_band = (size_t)a.groups * a.wa * kOct;
+    k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dec, per_band);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches += 2;
+  }
+  const int cpt = choose_cpt(a.w);
+  const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
+  const unsigned grid = (unsigned)(a.nbands * a.groups);
+  if (cpt == 4) k_build_decay<4><<<grid, threads, 0, s>>>(a, dec, kind);
+  else k_build_decay<8><<<grid, threads, 0, s>>>(a, dec, kind);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace swg

@@ -90,6 +90,8 @@ swg_status validate_kernel(const swg_kernel& k) {  // kernel.cpp:10-19
     return fail(SWG_ERR_INVALID_KERNEL, "kernel: dimensions must be odd, got %dx%d", k.kw, k.kh);
   if ((k.kind == SWG_KERNEL_GAUSS_CHEBYSHEV || k.kind == SWG_KERNEL_EXP_L1) && !(k.sigma > 0.0))
     return fail(SWG_ERR_INVALID_KERNEL, "kernel: sigma must be positive");
+  if (k.kind == SWG_KERNEL_EXP_L1 && !(k.sigma < 1.0))
+    return fail(SWG_ERR_INVALID_KERNEL, "kernel: exponential decay must be < 1");
   return SWG_OK;
 }
 
@@ -111,8 +113,8 @@ double weight_at(const swg_kernel& k, int dx, int dy) {  // kernel.cpp:25-59
       const int64_t kx = int64_t(hx + 1) * (hx + 1), ky = int64_t(hy + 1) * (hy + 1);
       return static_cast<double>(2 * kx * ky - int64_t(dx) * dx * ky - int64_t(dy) * dy * kx);
     }
-    case SWG_KERNEL_EXP_L1:  // declared extension
-      return std::exp(-k.sigma * static_cast<double>(std::abs(dx) + std::abs(dy)));
+    case SWG_KERNEL_EXP_L1:  // declared extension: sigma = decay per pixel
+      return std::pow(k.sigma, static_cast<double>(std::abs(dx) + std::abs(dy)));
     default: {
       const double nx = static_cast<double>(std::abs(dx)) / std::max(hx, 1);
       const double ny = static_cast<double>(std::abs(dy)) / std::max(hy, 1);
@@ -190,7 +192,14 @@ struct swg_ctx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
-  DevBuf parts, scores, peaks, terms, qout, grid, io;
+  DevBuf parts, scores, peaks, terms, qout, grid, io, resc;
+  // exact kernel-weight grids, uploaded once per kernel (graph-capture safe)
+  struct Grid {
+    swg_kernel k;
+    bool integer;
+    DevBuf buf;
+  };
+  std::vector<Grid*> grids;
 };
 
 struct swg_tables {
@@ -207,6 +216,9 @@ struct swg_tables {
                             // counts for boxes of area < 2^16
   uint32_t* t32 = nullptr;  // primary for P = 3; on demand for P = 1
   uint64_t* t64 = nullptr;
+  double* tdec = nullptr;    // decayed directional tables (EXP_L1), 4 planes
+  double decay = 0.0;
+  uint16_t* fflip = nullptr; // h / v / hv flipped feature images (decay tables)
   uint32_t* lb = nullptr;  // band carry scratch (BuildArgs::agg)
   int band_h = 0, nbands = 0;
   size_t wa = 0;
@@ -304,6 +316,7 @@ swg_status upload_and_quantize(swg_tables* t, const void* pixels, int is_device,
 
 swg_status ensure_t32(swg_tables* t) {
   if (t->t32) return SWG_OK;
+  if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
   if (!t->has_fi) return fail(SWG_ERR, "tables: no 32-bit planes and no feature image");
   const size_t bytes = t->ps * t->planes * t->groups * kOct * 4;
   cudaError_t e = cudaMalloc(&t->t32, bytes);
@@ -320,6 +333,7 @@ swg_status ensure_t32(swg_tables* t) {
 
 swg_status ensure_t64(swg_tables* t) {
   if (t->t64) return SWG_OK;
+  if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
   if (!t->has_fi) return fail(SWG_ERR, "tables: no 64-bit planes and no feature image");
   const size_t bytes = t->ps * t->planes * t->groups * kOct * 8;
   cudaError_t e = cudaMalloc(&t->t64, bytes);
@@ -331,6 +345,72 @@ swg_status ensure_t64(swg_tables* t) {
   }
   t->bytes += bytes;
   return run_build<uint64_t>(t, t->t64);
+}
+
+// Device copy of a kernel's exact weight grid (weight_at, llround-ed for
+// integer kernels as BruteForcePlan does, baselines.cpp:18-20); cached per
+// kernel so repeated requests (and graph capture) issue no host copies.
+swg_status weight_grid(swg_ctx* c, const swg_kernel& k, const double** out) {
+  const bool integer = k_integer(k);
+  for (auto* g : c->grids)
+    if (g->k.kind == k.kind && g->k.kw == k.kw && g->k.kh == k.kh && g->k.sigma == k.sigma &&
+        g->integer == integer) {
+      *out = static_cast<const double*>(g->buf.p);
+      return SWG_OK;
+    }
+  const int hx = k_hx(k), hy = k_hy(k);
+  std::vector<double> w((size_t)k.kw * k.kh);
+  for (int dy = -hy; dy <= hy; ++dy)
+    for (int dx = -hx; dx <= hx; ++dx) {
+      double v = weight_at(k, dx, dy);
+      if (integer) v = (double)std::llround(v);
+      w[(size_t)(dy + hy) * k.kw + dx + hx] = v;
+    }
+  auto* g = new swg_ctx::Grid{k, integer, {}};
+  swg_status st = g->buf.ensure(w.size() * 8);
+  if (st == SWG_OK) {
+    cudaError_t e = cudaMemcpy(g->buf.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) st = fail(SWG_ERR_CUDA, "weight grid: %s", cudaGetErrorString(e));
+  }
+  if (st != SWG_OK) {
+    g->buf.release();
+    delete g;
+    return st;
+  }
+  c->grids.push_back(g);
+  *out = static_cast<const double*>(g->buf.p);
+  return SWG_OK;
+}
+
+swg_status run_build_decay(swg_tables* t) {
+  swg_ctx* c = t->ctx;
+  const size_t fsz = t->fip * t->h;
+  CUDA_TRY(launch_flip(t->fi, t->fip, t->w, t->h, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz,
+                       c->stream));
+  c->launches += 1;
+  BuildArgs a{};
+  a.fi_pitch = t->fip;
+  a.out = t->tdec;
+  a.pitch = t->pitch;
+  a.plane_stride = t->ps;
+  a.w = t->w;
+  a.h = t->h;
+  a.bins = t->bins;
+  a.groups = t->groups;
+  a.planes = 4;
+  a.band_h = t->band_h;
+  a.nbands = t->nbands;
+  a.wa = t->wa;
+  a.aw = 16;
+  a.agg = t->lb;
+  const uint16_t* src[4] = {t->fi, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz};
+  for (int k = 0; k < 4; ++k) {
+    a.fi = src[k];
+    int nl = 0;
+    CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
+    c->launches += (uint64_t)nl;
+  }
+  return SWG_OK;
 }
 
 swg_status check_tables(const swg_tables* t) {
@@ -394,6 +474,11 @@ static void ctx_release(swg_ctx* c) {
     c->qout.release();
     c->grid.release();
     c->io.release();
+    c->resc.release();
+    for (auto* g : c->grids) {
+      g->buf.release();
+      delete g;
+    }
     cudaStreamDestroy(c->own);
   }
   delete c;
@@ -513,6 +598,71 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   return SWG_OK;
 }
 
+swg_status swg_tables_build_decay(swg_ctx* c, const void* pixels, int is_device,
+                                  size_t pitch_bytes, int width, int height, int format,
+                                  int bins, double decay, size_t memory_budget,
+                                  swg_tables** out) {
+  if (!c || !pixels || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  if (!(decay > 0.0 && decay < 1.0)) return fail(SWG_ERR_INVALID_KERNEL, "decay must be in (0, 1)");
+  if (width < 1 || height < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
+  if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
+  int nb = bins;
+  if (format == SWG_FMT_RGB8) {
+    if (bins < 1 || bins > 40) return fail(SWG_ERR, "RGB levels must be in [1, 40]");
+    nb = bins * bins * bins;
+  }
+  if (nb < 1 || nb > 65535) return fail(SWG_ERR, "bin count must be in [1, 65535]");
+  if (width > kMaxWidth) return fail(SWG_ERR_SIZE, "width %d > %d", width, kMaxWidth);
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  swg_tables* t = new swg_tables;
+  t->ctx = c;
+  c->refs++;
+  t->w = width;
+  t->h = height;
+  t->bins = nb;
+  t->levels = bins;
+  t->planes = SWG_PLANES_DECAY;
+  t->format = format;
+  t->decay = decay;
+  t->fip = fi_pitch(width);
+  t->groups = (nb + kOct - 1) / kOct;
+  t->pitch = record_pitch(width);
+  t->ps = t->pitch * (size_t)(height + 1);
+  choose_bands(t);
+  const size_t tab_bytes = t->ps * 4 * (size_t)t->groups * kOct * 8;
+  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct * 8;
+  const size_t fb = t->fip * height * 2;
+  const size_t need = tab_bytes + lb_bytes + 4 * fb;
+  if (memory_budget && need > memory_budget) {
+    swg_tables_destroy(t);
+    g_required = need;
+    return fail(SWG_ERR_CAPACITY, "decay tables need %zu bytes, budget is %zu", need,
+                memory_budget);
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc(&t->tdec, tab_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&t->fi, fb)) != cudaSuccess ||
+      (e = cudaMalloc(&t->fflip, 3 * fb)) != cudaSuccess ||
+      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
+    g_required = need;
+    cudaGetLastError();
+    swg_tables_destroy(t);
+    return fail(SWG_ERR_CAPACITY, "decay tables need %zu device bytes: %s", need,
+                cudaGetErrorString(e));
+  }
+  t->bytes = need;
+  swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
+  if (st == SWG_OK) st = run_build_decay(t);
+  if (st != SWG_OK) {
+    swg_tables_destroy(t);
+    return st;
+  }
+  *out = t;
+  return SWG_OK;
+}
+
 swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
                               size_t pitch_bytes) {
   ST_TRY(check_tables(t));
@@ -524,6 +674,7 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
+  if (t->tdec) ST_TRY(run_build_decay(t));
   return SWG_OK;
 }
 
@@ -590,6 +741,8 @@ swg_status swg_tables_destroy(swg_tables* t) {
     cudaFree(t->t16);
     cudaFree(t->t32);
     cudaFree(t->t64);
+    cudaFree(t->tdec);
+    cudaFree(t->fflip);
     cudaFree(t->fi);
     cudaFree(t->in);
     cudaFree(t->lb);
@@ -613,7 +766,7 @@ swg_status swg_tables_info(const swg_tables* t, int* w, int* h, int* bins, int* 
 swg_status swg_tables_device_layout(const swg_tables* t, const void** base, size_t* ps,
                                     size_t* pitch, int* bins_per_record) {
   ST_TRY(check_tables(t));
-  if (base) *base = t->t32;
+  if (base) *base = t->tdec ? (const void*)t->tdec : (const void*)t->t32;
   if (ps) *ps = t->ps;
   if (pitch) *pitch = t->pitch;
   if (bins_per_record) *bins_per_record = kOct;
@@ -666,12 +819,22 @@ swg_status swg_tables_export_i64(swg_tables* t, int kind, int b0, int b1, int64_
 
 swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32_t* out) {
   ST_TRY(check_export(t, kind, b0, b1, out));
+  if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   if (kind >= 3) return fail(SWG_ERR_OUT_OF_RANGE, "quadratic planes are 64-bit only");
   ST_TRY(ensure_t32(t));
   return export_planes<uint32_t, uint32_t>(t, t->t32, kind, b0, b1, out);
+}
+
+swg_status swg_tables_export_f64(swg_tables* t, int kind, int b0, int b1, double* out) {
+  ST_TRY(check_export(t, kind, b0, b1, out));
+  if (!t->tdec) return fail(SWG_ERR_CONFIG, "fp64 export is for decay tables");
+  if (b0 == b1) return SWG_OK;
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  return export_planes<double, double>(t, t->tdec, kind, b0, b1, out);
 }
 
 swg_status swg_tables_feature_image(swg_tables* t, uint16_t* out) {
@@ -984,7 +1147,14 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     if (r.method < 0 || r.method > 3) return fail(SWG_ERR_ARG, "method %d", r.method);
     if (r.sim < 0 || r.sim > 1) return fail(SWG_ERR_ARG, "similarity %d", r.sim);
     const bool quad = r.kernel.kind == SWG_KERNEL_EUCLID_QUAD;
-    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel) && !quad)
+    const bool expo = r.kernel.kind == SWG_KERNEL_EXP_L1;
+    if (r.method == SWG_METHOD_SWIH && expo && !(t->tdec && r.kernel.sigma == t->decay))
+      return fail(SWG_ERR_CONFIG,
+                  "likelihood map: exponential swih needs decay tables built with decay %g",
+                  r.kernel.sigma);
+    if (t->tdec && r.method != SWG_METHOD_BRUTE && !(r.method == SWG_METHOD_SWIH && expo))
+      return fail(SWG_ERR_CONFIG, "decay tables serve exponential swih and brute force only");
+    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel) && !quad && !expo)
       return fail(SWG_ERR_UNSUPPORTED_KERNEL,
                   "likelihood map: method swih requires a quadrant-affine kernel");
     if (r.method == SWG_METHOD_SWIH && quad) {
@@ -1025,7 +1195,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // and shares its kernel; a Uniform box is a one-ring cake with coefficient
   // 1.0 (exact integer weights, same scores: score_counts == score_weights on
   // integers), so on narrow tables it runs the 16-bit cake sweep.
-  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad64 };
+  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad64, kExp64 };
   std::vector<dim3> grid(n);
   std::vector<int> engine(n);
   std::vector<swg_kernel> kern(n);
@@ -1043,12 +1213,13 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       k.kind = SWG_KERNEL_UNIFORM;
       method = SWG_METHOD_SWIH;
     }
-    if (method == SWG_METHOD_BRUTE && (k.kind == SWG_KERNEL_UNIFORM ||
+    if (method == SWG_METHOD_BRUTE && !t->tdec && (k.kind == SWG_KERNEL_UNIFORM ||
                                        (k.kind == SWG_KERNEL_MANHATTAN && t->planes == 3)))
       method = SWG_METHOD_SWIH;
     const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
     if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
     else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad64;
+    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EXP_L1) engine[i] = kExp64;
     else if (method == SWG_METHOD_CAKE) engine[i] = (t->t16 && small) ? kCake16 : kCake32;
     else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
     else engine[i] = kAffine32;
@@ -1081,6 +1252,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       const swg_kernel k = kern[i];
       a.tab = engine[i] == kCake16   ? (const void*)t->t16
               : engine[i] == kQuad64 ? (const void*)t->t64
+              : engine[i] == kExp64  ? (const void*)t->tdec
                                      : (const void*)t->t32;
       a.plane_stride = t->ps;
       a.pitch = t->pitch;
@@ -1097,7 +1269,61 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       a.parts = parts;
       std::memset(a.model, 0, sizeof(a.model));
       std::memcpy(a.model, r.model, sizeof(double) * t->bins);
-      if (engine[i] == kQuad64) {
+      if (engine[i] == kExp64) {
+        // quadrant rectangles in their orientation's SE table (k_exp.cu);
+        // coefficients in powers of the table's decay
+        static thread_local ExpSweep es;
+        const double dd = t->decay;
+        auto pw = [&](int n) { return std::pow(dd, (double)n); };
+        const int hx = a.hx, hy = a.hy;
+        const long long p = (long long)t->pitch;
+        // corners (dx, dy) from the centre record, per orientation, and rect extents
+        const int cx0[4] = {1, 0, 1, 0}, cy0[4] = {1, 1, 0, 0};   // (x1+1, y1+1) offset
+        const int ax[4] = {hx + 1, hx, hx + 1, hx}, by[4] = {hy + 1, hy + 1, hy, hy};
+        const double qf[4] = {1.0, dd, dd, dd * dd};
+        for (int o = 0; o < 4; ++o) {
+          const int xs[4] = {cx0[o], cx0[o] - ax[o], cx0[o], cx0[o] - ax[o]};
+          const int ys[4] = {cy0[o], cy0[o], cy0[o] - by[o], cy0[o] - by[o]};
+          const double cf[4] = {qf[o], -qf[o] * pw(ax[o]), -qf[o] * pw(by[o]),
+                                qf[o] * pw(ax[o] + by[o])};
+          for (int q = 0; q < 4; ++q) {
+            es.off[4 * o + q] = (int)(8 * (ys[q] * p + xs[q]) * kOct);
+            es.coef[4 * o + q] = cf[q];
+          }
+        }
+        es.w = t->w;
+        es.h = t->h;
+        // fp64 rounding floor of an empty bin: table values are bounded by
+        // 1/(1-d)^2, the rectangle formula's error by ~1e-16 of that
+        es.snap = 1e-13 / ((1.0 - dd) * (1.0 - dd));
+        CUDA_TRY(launch_sweep_exp(a, es, grid[i], c->stream));
+        c->launches += 2;
+        CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
+                                    dpeaks + i, c->stream));
+        // phase 2: exact fp64 brute-force re-score of the near-maximum windows
+        RescoreArgs ra{};
+        ST_TRY(weight_grid(c, k, &ra.grid));
+        ra.fi = t->fi;
+        ra.fi_pitch = t->fip;
+        ra.kw = k.kw;
+        ra.kh = k.kh;
+        ra.cap = 4096;
+        ra.eps = 1e-4;
+        const size_t hb = (size_t)ra.cap * t->bins * 8, cb = (size_t)ra.cap * 8;
+        const size_t pb = (size_t)((ra.cap + 127) / 128) * sizeof(PeakPart);
+        ST_TRY(c->resc.ensure(hb + cb + pb + 256 + (size_t)t->bins * 8));
+        char* rb = static_cast<char*>(c->resc.p);
+        ra.hist = reinterpret_cast<double*>(rb);
+        ra.cand = reinterpret_cast<long long*>(rb + hb);
+        ra.parts = reinterpret_cast<PeakPart*>(rb + hb + cb);
+        ra.count = reinterpret_cast<int*>(rb + hb + cb + pb);
+        double* dmodel = reinterpret_cast<double*>(rb + hb + cb + pb + 256);
+        ra.model = dmodel;
+        CUDA_TRY(cudaMemcpyAsync(dmodel, a.model, (size_t)t->bins * 8, cudaMemcpyHostToDevice,
+                                 c->stream));
+        CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, c->stream));
+        c->launches += 3;
+      } else if (engine[i] == kQuad64) {
         a.mass = (double)quad_mass(k);
         // box corners (TL, TR, BL, BR) of the whole window, per plane, as byte
         // offsets from the centre record of the 64-bit tables
@@ -1151,29 +1377,23 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       } else {
         // direct per-pixel weighted histogram (baselines.cpp:24-69)
         const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);
-        std::vector<double> wgrid((size_t)kw * kh);
-        for (int dy = -hy; dy <= hy; ++dy)
-          for (int dx = -hx; dx <= hx; ++dx)
-            wgrid[(size_t)(dy + hy) * kw + dx + hx] = weight_at(k, dx, dy);
-        if (k_integer(k))
-          for (auto& w : wgrid) w = (double)std::llround(w);
-        ST_TRY(c->grid.ensure(wgrid.size() * 8));
-        CUDA_TRY(cudaMemcpyAsync(c->grid.p, wgrid.data(), wgrid.size() * 8,
-                                 cudaMemcpyHostToDevice, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));  // grid is reused per request
+        (void)hx;
+        (void)hy;
         BruteArgs ba{};
+        ST_TRY(weight_grid(c, k, &ba.grid));
         ba.fi = t->fi;
         ba.fi_pitch = t->fip;
-        ba.grid = static_cast<const double*>(c->grid.p);
         ba.kw = kw;
         ba.kh = kh;
         ba.integer = k_integer(k);
         CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, c->stream));
       }
-      c->launches += 1;
-      CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
-                                  dpeaks + i, c->stream));
-      c->launches += 1;
+      if (engine[i] != kExp64) {  // (the exponential branch reduces its own peaks)
+        c->launches += 1;
+        CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
+                                    dpeaks + i, c->stream));
+        c->launches += 1;
+      }
     }
     if (scores_host && scores_host[i] && rows > 0)
       CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)rows * mws[i] * 8,

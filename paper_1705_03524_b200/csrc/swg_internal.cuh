@@ -118,6 +118,32 @@ struct CakeSweep {
   double coeff[kMaxRings];
 };
 
+// Exponential sweep constants: per orientation k (0 SE = TL quadrant,
+// 1 h-flip = TR, 2 v-flip = BL, 3 hv-flip = BR) the byte offsets of the four
+// rectangle corners from the window's centre record in that orientation and
+// their coefficients (sign x decay powers x the quadrant's offset factor).
+struct ExpSweep {
+  int off[16];
+  double coef[16];
+  int w, h;     // image size (flip mapping)
+  double snap;  // values below this are fp32 noise of an empty bin
+};
+
+// Two-phase exact peak of a tolerance-based map.
+struct RescoreArgs {
+  const uint16_t* fi;  // feature image (unflipped)
+  size_t fi_pitch;
+  const double* grid;  // kh x kw exact kernel weights (host-computed)
+  int kw, kh;
+  const double* model; // device copy of the model
+  int* count;          // device candidate counter
+  long long* cand;     // candidates (absolute map index)
+  int cap;
+  double* hist;        // cap x bins scratch
+  PeakPart* parts;     // one per rescore CTA
+  double eps;
+};
+
 struct BruteArgs {
   const uint16_t* fi;  // quantised image
   size_t fi_pitch;
@@ -154,6 +180,13 @@ cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cud
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);
+cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
+                        uint16_t* fv, uint16_t* fhv, cudaStream_t s);
+cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
+                               int* launches);
+cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s);
+cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak* peak,
+                              cudaStream_t s);
 cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                                 cudaStream_t s);
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,

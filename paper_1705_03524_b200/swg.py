@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("SWG_LIB", _build.LIB)
 
 # enums (include/swg.h)
 FMT_GRAY8, FMT_GRAY16, FMT_RGB8, FMT_BINS16 = 0, 1, 2, 3
-PLANES_PLAIN, PLANES_AFFINE, PLANES_QUADRATIC = 1, 3, 5
+PLANES_PLAIN, PLANES_AFFINE, PLANES_QUADRATIC, PLANES_DECAY = 1, 3, 5, 4
 TABLE_PLAIN, TABLE_XRAMP, TABLE_YRAMP = 0, 1, 2
 UNIFORM, MANHATTAN, CHEBYSHEV, GAUSS_CHEB = 0, 1, 2, 3
 EUCLID_QUAD, EXP_L1 = 4, 5  # declared extensions
@@ -148,6 +148,8 @@ def lib():
         "swg_ctx_launch_count": [vp, C.POINTER(C.c_uint64)],
         "swg_tables_build": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_size_t, C.POINTER(vp)],
+        "swg_tables_build_decay": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.c_double, C.c_size_t, C.POINTER(vp)],
         "swg_tables_rebuild": [vp, vp, C.c_int, C.c_size_t],
         "swg_tables_upload_i64": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)],
         "swg_tables_destroy": [vp],
@@ -155,6 +157,7 @@ def lib():
                             C.POINTER(C.c_int), C.POINTER(C.c_size_t)],
         "swg_tables_export_i64": [vp, C.c_int, C.c_int, C.c_int, vp],
         "swg_tables_export_u32": [vp, C.c_int, C.c_int, C.c_int, vp],
+        "swg_tables_export_f64": [vp, C.c_int, C.c_int, C.c_int, vp],
         "swg_tables_feature_image": [vp, vp],
         "swg_tables_device_layout": [vp, C.POINTER(vp), C.POINTER(C.c_size_t),
                                      C.POINTER(C.c_size_t), C.POINTER(C.c_int)],
@@ -246,6 +249,20 @@ class Context:
               width=None, height=None, pitch=0) -> "Tables":
         return Tables(self, pixels, fmt, bins, planes, budget, width, height, pitch)
 
+    def build_decay(self, pixels, decay, fmt=FMT_GRAY8, bins=16, budget=0, width=None,
+                    height=None, pitch=0) -> "Tables":
+        """Decayed directional tables for EXP_L1 maps with sigma == decay."""
+        t = Tables.__new__(Tables)
+        t.ctx = self
+        t._h = C.c_void_p()
+        is_dev, ptr, w, h = Tables._src(pixels, fmt, width, height)
+        t._keep = pixels
+        _check(lib().swg_tables_build_decay(self._h, ptr, is_dev, pitch, w, h, fmt, bins,
+                                            float(decay), budget, C.byref(t._h)))
+        t._info()
+        t.decay = float(decay)
+        return t
+
     def upload_i64(self, plain, xramp, yramp) -> "Tables":
         plain, xramp, yramp = (np.ascontiguousarray(a, np.int64) for a in (plain, xramp, yramp))
         b, h1, w1 = plain.shape
@@ -311,6 +328,13 @@ class Tables:
         b1 = self.bins if b1 is None else b1
         out = np.empty((b1 - b0, self.height + 1, self.width + 1), np.int64)
         _check(lib().swg_tables_export_i64(self._h, kind, b0, b1, _ptr(out)))
+        return out
+
+    def export_f64(self, kind=0, b0=0, b1=None):
+        """Decay tables: fp64 planes of orientation `kind` (0 SE .. 3 hv-flip)."""
+        b1 = self.bins if b1 is None else b1
+        out = np.empty((b1 - b0, self.height + 1, self.width + 1), np.float64)
+        _check(lib().swg_tables_export_f64(self._h, kind, b0, b1, _ptr(out)))
         return out
 
     def export_u32(self, kind=TABLE_PLAIN, b0=0, b1=None):

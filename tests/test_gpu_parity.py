@@ -461,7 +461,7 @@ def test_exponential_brute_and_cake(ctx, oracle):
     bins = 8
     fi = oracle.quantize_gray8(img, bins)
     t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
-    for kw, lam in ((9, 0.25), (21, 0.1)):
+    for kw, lam in ((9, 0.75), (21, 0.9375)):
         ok = O.kernel(O.EXP_L1, kw, kw, lam)
         mdl = oracle.target_model(fi[:kw, :kw].copy(), bins, ok, O.BRUTE)
         want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)
@@ -473,3 +473,76 @@ def test_exponential_brute_and_cake(ctx, oracle):
         want_c = oracle.likelihood_map(fi, bins, mc, ok, O.CAKE, rings=r)
         got_c, _ = t.likelihood_map(K(swg.EXP_L1, kw, kw, lam), mc, swg.CAKE, rings=r)
         assert (got_c == want_c).all()
+
+
+def _decayed_se(fi, bins, d):
+    """numpy restatement of the decayed SE table: E(X,Y) = sum over x<X, y<Y
+    of [fi==b] d^(X-1-x) d^(Y-1-y), zero row/column 0."""
+    h, w = fi.shape
+    out = np.zeros((bins, h + 1, w + 1))
+    for b in range(bins):
+        one = (fi == b).astype(np.float64)
+        r = np.zeros((h, w + 1))
+        for x in range(w):
+            r[:, x + 1] = d * r[:, x] + one[:, x]
+        for y in range(h):
+            out[b, y + 1] = d * out[b, y] + r[y]
+    return out
+
+
+@pytest.mark.parametrize("w,h,bins,d", [(70, 53, 12, 0.9375), (33, 61, 5, 0.5), (1, 1, 3, 0.75)])
+def test_decay_tables_vs_numpy(ctx, oracle, w, h, bins, d):
+    img = oracle.random_gray(w, h, 11)
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+    assert t.planes == swg.PLANES_DECAY
+    flips = (fi, fi[:, ::-1], fi[::-1, :], fi[::-1, ::-1])
+    for k, f in enumerate(flips):
+        want = _decayed_se(np.ascontiguousarray(f), bins, d)
+        got = t.export_f64(k)
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    with pytest.raises(swg.ConfigError):
+        t.export_u32(0)
+
+
+def test_exponential_swih_maps(ctx, oracle):
+    """O(1) exponential maps on decay tables: map values within 1e-4 of the
+    fp64 brute force; the peak (index AND score) is exact through the
+    candidate re-score."""
+    img = oracle.random_gray(120, 90, 21)
+    bins = 8
+    fi = oracle.quantize_gray8(img, bins)
+    for d in (0.75, 0.9375):
+        t = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+        for kw, kh in ((1, 1), (9, 9), (21, 15), (41, 41)):
+            ok = O.kernel(O.EXP_L1, kw, kh, d)
+            mdl = oracle.target_model(fi[30:30 + kh, 40:40 + kw].copy(), bins, ok, O.BRUTE)
+            for sim in (swg.BHATTACHARYYA, swg.INTERSECTION):
+                want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE, sim)
+                got, pk = t.likelihood_map(K(swg.EXP_L1, kw, kh, d), mdl, swg.SWIH, sim)
+                np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
+                assert pk == oracle.peak(want, kw // 2, kh // 2), (d, kw, kh, sim)
+        with pytest.raises(swg.ConfigError):  # sigma must match the tables' decay
+            t.likelihood_map(K(swg.EXP_L1, 9, 9, 0.5), np.full(bins, 1 / bins), swg.SWIH)
+        with pytest.raises(swg.ConfigError):  # decay tables serve EXP_L1 / brute only
+            t.likelihood_map(K(swg.UNIFORM, 9, 9), np.full(bins, 1 / bins), swg.SWIH)
+        # brute force from the decay tables' feature image
+        ok = O.kernel(O.EXP_L1, 9, 9, d)
+        mdl = oracle.target_model(fi[:9, :9].copy(), bins, ok, O.BRUTE)
+        got_b, _ = t.likelihood_map(K(swg.EXP_L1, 9, 9, d), mdl, swg.BRUTE)
+        assert (got_b == oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)).all()
+
+
+def test_exponential_swih_flat_image(ctx, oracle):
+    """Every window ties: more candidates than the re-score capacity, the
+    full-map fallback must still return the reference's first maximum."""
+    img = np.full((96, 128), 77, np.uint8)
+    bins = 4
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build_decay(img, 0.9375, swg.FMT_GRAY8, bins)
+    ok = O.kernel(O.EXP_L1, 9, 9, 0.9375)
+    mdl = oracle.target_model(fi[:9, :9].copy(), bins, ok, O.BRUTE)
+    want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)
+    got, pk = t.likelihood_map(K(swg.EXP_L1, 9, 9, 0.9375), mdl, swg.SWIH)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
+    assert pk == oracle.peak(want, 4, 4)
