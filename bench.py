@@ -2,18 +2,30 @@
 """bench.py — SWIH hot path on B200: IH build + multi-scale likelihood maps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1]
+                    [--config c2|c1|c3|c4|c5|c5m]
 
-One step = one frame through the hot path: quantise + weighted integral
-histogram build, then the full strict likelihood map + peak at every scale
-(BASELINE.json configs[1] by default: 1024x1024 u8, 32 bins, Gaussian kernel
-(GaussianChebyshev sigma=0.5, exact full-ring wedding cake), windows
-33/65/97).  `value` = weighted windows/s over all ranks with the frame
-resident in HBM; `e2e` = the same through the C-ABI with a pinned host frame
-in and host maps + peaks out.  N>1 (torchrun): one frame per GPU, no
-data-path collective (weak scaling); the timed region is the max over ranks.
+One step = one pass of the hot path over one batch of input: quantise +
+weighted integral histogram build, then the full strict likelihood map +
+peak at every scale.  Default (BASELINE.json configs[1]): one 1024x1024 u8
+frame, 32 bins, Gaussian kernel (GaussianChebyshev sigma=0.5, exact
+full-ring wedding cake), windows 33/65/97.  The other configs:
+  c1   256x256 u8, 16 bins, Manhattan 33x33                      (configs[0])
+  c3   64 RGB 1920x1080 frames (tracking sequence), 4x4x4 bins, Euclidean
+       (declared quadratic form), windows 45x59/49x65/53x71 on a 256x256
+       search region around the previous ground truth           (configs[2])
+  c4   3840x2160 RGB, 8x8x8 bins, exponential (decay 15/16 per pixel),
+       windows 25/37/57/85/129, processed in row bands              (configs[3])
+  c5   2048x2048 u16, 64 bins, Manhattan + Gaussian + Euclidean +
+       exponential at windows 17..257 (8 scales each)             (configs[4])
+  c5m  c5's Manhattan subset
+`value` = weighted windows/s over all ranks with the input resident in HBM;
+`e2e` = the same through the C-ABI with pinned host input and host maps /
+peaks out.  N>1 (torchrun): frames (c1/c2/c5: one per GPU, weak scaling),
+sequence frames (c3) or row bands (c4) sharded over ranks (strong scaling);
+no data-path collective; the timed region is the max over ranks.
 --impl reference times the reference CPU implementation (oracle/_ref, the
-unmodified reference sources) on this host's cores.
+unmodified reference sources; the oracle restatement for the kernels the
+reference lacks) on this host's cores.
 """
 from __future__ import annotations
 
@@ -32,6 +44,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "weighted windows/s"
 UNIT = "windows/s"
+EXP_DECAY = 15.0 / 16.0  # declared exponential kernel: weight 15/16 per pixel of L1 distance
 
 
 def peaks_json():
@@ -42,29 +55,95 @@ def peaks_json():
     return 6650.0, "fallback"
 
 
-# ------------------------------------------------------------------ workload
+# ------------------------------------------------------------------ workloads
 def workload(name):
+    """A workload = input generator + table groups; a group = one table set
+    (planes / decay) and the scales (kernel, method, rings, target index)
+    it serves."""
     from paper_1705_03524_b200 import swg, synth
+    K = swg.Kernel
     if name == "c1":
-        return dict(name="config1: 256x256 u8, 16 bins, Manhattan, window 33x33",
-                    gen=synth.config1, bins=16, planes=swg.PLANES_AFFINE,
-                    scales=[(swg.Kernel(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)],
-                    P=3, elem=4)
-    if name == "c5m":
+        return dict(name="config1: 256x256 u8, 16 bins, Manhattan, window 33x33", kind="frame",
+                    gen=synth.config1, fmt=swg.FMT_GRAY8, bins=16, nbins=16, scaling="weak",
+                    groups=[dict(planes=swg.PLANES_AFFINE,
+                                 scales=[(K(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)])])
+    if name in ("c5", "c5m"):
         ks = (17, 25, 37, 53, 79, 117, 173, 257)
-        return dict(name="config5 (Manhattan subset): 2048x2048 u16, 64 bins, Manhattan, windows "
-                         + "/".join(map(str, ks)),
-                    gen=synth.config5, bins=64, planes=swg.PLANES_AFFINE, fmt=swg.FMT_GRAY16,
-                    scales=[(swg.Kernel(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks],
-                    P=3, elem=4)
+        groups = [dict(planes=swg.PLANES_AFFINE,
+                       scales=[(K(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks])]
+        label = "Manhattan"
+        if name == "c5":
+            groups += [
+                dict(planes=swg.PLANES_PLAIN,
+                     scales=[(K(swg.GAUSS_CHEB, k, k, 0.5), swg.CAKE, k // 2 + 1, None)
+                             for k in ks]),
+                dict(planes=swg.PLANES_QUADRATIC,
+                     scales=[(K(swg.EUCLID_QUAD, k, k), swg.SWIH, 1, None) for k in ks]),
+                dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY,
+                     scales=[(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None) for k in ks]),
+            ]
+            label = ("Manhattan + Gaussian (exact full-ring cake) + Euclidean (quadratic) + "
+                     "exponential (decay 15/16)")
+        return dict(name=f"config5{' (Manhattan subset)' if name == 'c5m' else ''}: 2048x2048 "
+                         f"u16, 64 bins, {label}, windows " + "/".join(map(str, ks)),
+                    kind="frame", gen=synth.config5, fmt=swg.FMT_GRAY16, bins=64, nbins=64,
+                    scaling="weak", groups=groups)
+    if name == "c3":
+        scales = [(K(swg.EUCLID_QUAD, kw, kh), swg.SWIH, 1, 0)
+                  for kw, kh in ((45, 59), (49, 65), (53, 71))]
+        return dict(name="config3: 64 RGB 1920x1080 frames, 4x4x4 bins, Euclidean (quadratic), "
+                         "windows 45x59/49x65/53x71, 256x256 search region",
+                    kind="sequence", gen=synth.config3, fmt=swg.FMT_RGB8, bins=4, nbins=64,
+                    scaling="strong", groups=[dict(planes=swg.PLANES_QUADRATIC, scales=scales)])
+    if name == "c4":
+        scales = [(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None)
+                  for k in (25, 37, 57, 85, 129)]
+        return dict(name="config4: 3840x2160 RGB, 8x8x8 bins, exponential (decay 15/16), "
+                         "windows 25/37/57/85/129, row bands",
+                    kind="bands", gen=synth.config4, fmt=swg.FMT_RGB8, bins=8, nbins=512,
+                    scaling="strong",
+                    groups=[dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, scales=scales)])
     scales = []
     for i, s in enumerate((32, 64, 96)):
         kw = synth.odd_window(s)
-        scales.append((swg.Kernel(swg.GAUSS_CHEB, kw, kw, 0.5), swg.CAKE, kw // 2 + 1, i))
+        scales.append((K(swg.GAUSS_CHEB, kw, kw, 0.5), swg.CAKE, kw // 2 + 1, i))
     return dict(name="config2: 1024x1024 u8, 32 bins, Gaussian (GaussianChebyshev sigma=0.5, "
                      "exact full-ring cake), windows 33/65/97",
-                gen=synth.config2, bins=32, planes=swg.PLANES_PLAIN, scales=scales, P=1,
-                elem=2)
+                kind="frame", gen=synth.config2, fmt=swg.FMT_GRAY8, bins=32, nbins=32,
+                scaling="weak", groups=[dict(planes=swg.PLANES_PLAIN, scales=scales)])
+
+
+def engine_of(group, k, method):
+    """(sweep kernel, planes read, bytes per entry) the library picks
+    (swg_abi.cu likelihood_maps engine choice)."""
+    from paper_1705_03524_b200 import swg
+    if group["planes"] == swg.PLANES_DECAY:
+        return "k_sweep_exp", 4, 8
+    if group["planes"] == swg.PLANES_QUADRATIC:
+        return "k_sweep_quad", 5, 8
+    if method == swg.CAKE or k.kind == swg.UNIFORM:
+        small = k.kw * k.kh < 65536
+        if group["planes"] == swg.PLANES_PLAIN and small:
+            return "k_sweep_cake16", 1, 2
+        return "k_sweep_cake", 1, 4
+    return "k_sweep_affine", 3, 4
+
+
+def group_build_bytes(group, w, h, nbins):
+    """Plane bytes one rebuild writes (every plane set the tables hold)."""
+    from paper_1705_03524_b200 import swg
+    cells = (w + 1) * (h + 1) * nbins
+    p = group["planes"]
+    if p == swg.PLANES_DECAY:
+        return cells * 4 * 8
+    if p == swg.PLANES_QUADRATIC:
+        return cells * 5 * 8
+    if p == swg.PLANES_AFFINE:
+        return cells * 3 * 4
+    b = cells * 2  # narrow 16-bit plain planes
+    if any(engine_of(group, k, m)[0] == "k_sweep_cake" for k, m, _, _ in group["scales"]):
+        b += cells * 4  # 32-bit plain planes for the large windows
+    return b
 
 
 def target_center(scene, ti):
@@ -74,16 +153,44 @@ def target_center(scene, ti):
     return scene.targets[ti][:2]
 
 
-def make_requests(ctx, wl, scene):
-    from paper_1705_03524_b200 import api, swg, synth
-    reqs = []
-    for k, method, rings, ti in wl["scales"]:
-        cx, cy = target_center(scene, ti)
-        templ = synth.crop(scene.image, cx, cy, k.kw, k.kh)
-        model = api.target_model(ctx, templ, k, fmt=wl.get("fmt", swg.FMT_GRAY8),
-                                 bins=wl["bins"], method=method, rings=rings)
-        reqs.append(swg.MapRequest(k, model, method, swg.BHATTACHARYYA, rings))
-    return reqs
+def make_models(ctx, wl, data):
+    """Per group, per scale: model = target_model_for_method of the kw x kh
+    template centred on the target (matching.cpp:84-106)."""
+    from paper_1705_03524_b200 import api, synth
+    out = []
+    for g in wl["groups"]:
+        ms = []
+        for k, method, rings, ti in g["scales"]:
+            if wl["kind"] == "sequence":
+                cx, cy = data.track[0]
+                img = data.frames[0]
+            else:
+                cx, cy = target_center(data, ti)
+                img = data.image
+            templ = synth.crop(img, cx, cy, k.kw, k.kh)
+            ms.append(api.target_model(ctx, templ, k, fmt=wl["fmt"], bins=wl["bins"],
+                                       method=method, rings=rings))
+        out.append(ms)
+    return out
+
+
+def band_plan(H, scales, n_bands):
+    """Row bands of the frame (c4): band b owns map rows [b*S, (b+1)*S) of
+    every scale and is built from pixel rows [p0, p0 + BH), BH = S + the
+    largest kh - 1 (the last band is shifted up to keep one table shape)."""
+    kh_max = max(k.kh for k, _, _, _ in scales)
+    S = -(-H // n_bands)
+    BH = min(H, S + kh_max - 1)
+    bands = []
+    for b in range(n_bands):
+        p0 = min(b * S, H - BH)
+        rows = []
+        for k, _, _, _ in scales:
+            mh = H - k.kh + 1
+            v0, v1 = min(b * S, mh), min((b + 1) * S, mh)
+            rows.append((v0, v1))
+        bands.append((p0, rows))
+    return BH, bands
 
 
 # ------------------------------------------------------------------ clocks
@@ -133,45 +240,82 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU reference
-def cpu_reference(wl, scene, models, budget_s=12.0, threads=None):
-    """Reference CPU path (best-use): one reference build_tables
-    (single-threaded; the reference has no parallel build) + per-scale sweep
-    of reference queries + the restated scorer on `threads` host threads, on
-    a bounded band of map rows per scale; returns projected full-frame rates."""
+def _quantize_host(wl, img):
     from oracle import oracle as O
+    from paper_1705_03524_b200 import swg
+    orc = O.Oracle()
+    if wl["fmt"] == swg.FMT_GRAY16:  # declared uint16 quantiser (no reference counterpart)
+        return orc.quantize_gray16(img, wl["nbins"])
+    if wl["fmt"] == swg.FMT_RGB8:    # declared RGB quantiser (no reference counterpart)
+        return orc.quantize_rgb8(img, wl["bins"])
+    return O.Ref().quantize(img, wl["bins"])
+
+
+def cpu_reference(wl, data, models, budget_s=12.0, threads=None):
+    """Reference CPU path (best-use) on `threads` host threads:
+    kernels the reference implements (Manhattan swih, GaussianChebyshev
+    wedding cake) run the unmodified reference sources (oracle/_ref: one
+    build_tables, single-threaded as in the reference, + a row-band sweep of
+    reference queries and the restated scorer); the declared kernels the
+    reference lacks (Euclidean, exponential) run the oracle's brute-force
+    restatement (baselines.cpp:53-69 order).  Each scale is timed on a
+    bounded band of map rows and projected to the step's full work."""
+    from oracle import oracle as O
+    from paper_1705_03524_b200 import swg, synth
     threads = threads or os.cpu_count()
     R = O.Ref()
-    img = scene.image
-    bins = wl["bins"]
-    t0 = time.perf_counter()
-    if img.dtype == np.uint16:  # declared uint16 quantiser (no reference counterpart)
-        fi = O.Oracle().quantize_gray16(img, bins)
+    orc = O.Oracle()
+    if wl["kind"] == "sequence":
+        f = 1
+        x0, y0 = synth.search_origin(data, f)
+        s = data.search
+        img = data.frames[f, y0:y0 + s, x0:x0 + s]
+        mult = data.frames.shape[0]
     else:
-        fi = R.quantize(img, bins)
-    tabs = R.tables(fi, bins, budget=1 << 40)
-    t_build = time.perf_counter() - t0
-    per_scale = []
-    total_win = 0
-    proj = t_build
-    sample_win = 0
-    for (k, method, rings, _), model in zip(wl["scales"], models):
-        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
-        mw, mh = img.shape[1] - k.kw + 1, img.shape[0] - k.kh + 1
-        rows = max(threads // 2, 1)
-        while True:
-            t0 = time.perf_counter()
-            tabs.sweep_rows(model, ok, method, 0, rings, 0, threads, 0, rows)
-            dt = time.perf_counter() - t0
-            if dt > budget_s / (3 * len(wl["scales"])) or rows >= mh:
-                break
-            rows = min(mh, rows * 2)
-        rate = rows * mw / dt
-        per_scale.append(rate)
-        total_win += mw * mh
-        sample_win += rows * mw
-        proj += mw * mh / rate
-    return {"value": total_win / proj, "t_build_s": t_build, "scale_rates": per_scale,
-            "threads": threads, "sample_windows": sample_win, "frame_windows": total_win}
+        img = data.image
+        mult = 1
+    t0 = time.perf_counter()
+    fi = _quantize_host(wl, img)
+    t_q = time.perf_counter() - t0
+    nb = wl["nbins"]
+    H, W = fi.shape
+    tabs, t_build = None, 0.0
+    proj = t_q * mult
+    total_win = sample_win = 0
+    kinds = set()
+    rates = []
+    for g, ms in zip(wl["groups"], models):
+        for (k, method, rings, _), model in zip(g["scales"], ms):
+            ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+            mw, mh = W - k.kw + 1, H - k.kh + 1
+            ref_ok = k.kind in (swg.MANHATTAN, swg.UNIFORM, swg.GAUSS_CHEB)
+            if ref_ok and tabs is None:
+                t0 = time.perf_counter()
+                tabs = R.tables(fi, nb, budget=1 << 40)
+                t_build = time.perf_counter() - t0
+                proj += t_build * mult
+            rows = max(threads // 2, 1)
+            while True:
+                t0 = time.perf_counter()
+                if ref_ok:
+                    tabs.sweep_rows(model, ok, method, 0, rings, 0, threads, 0, rows)
+                else:
+                    orc.likelihood_map(fi, nb, model, ok, O.BRUTE, 0, rows=(0, rows),
+                                       threads=threads)
+                dt = time.perf_counter() - t0
+                if dt > budget_s / (3 * sum(len(x["scales"]) for x in wl["groups"])) or rows >= mh:
+                    break
+                rows = min(mh, rows * 2)
+            rate = rows * mw / dt
+            rates.append(rate)
+            kinds.add("reference" if ref_ok else "port")
+            total_win += mw * mh * mult
+            sample_win += rows * mw
+            proj += mw * mh * mult / rate
+    return {"value": total_win / proj, "t_build_s": t_build, "scale_rates": rates,
+            "threads": threads, "sample_windows": sample_win, "frame_windows": total_win,
+            "kind": "reference" if kinds == {"reference"} else "port",
+            "mixed": sorted(kinds)}
 
 
 def cpu_model_name():
@@ -184,6 +328,19 @@ def cpu_model_name():
     return "unknown"
 
 
+def cpu_sample_text(wl, c):
+    parts = []
+    if "reference" in c["mixed"]:
+        parts.append(f"oracle/_ref (unmodified reference sources): build_tables "
+                     f"({c['t_build_s']:.2f} s, 1 thread) + reference-query sweeps")
+    if "port" in c["mixed"]:
+        parts.append("oracle brute-force restatement for the declared kernels the reference "
+                     "lacks")
+    return ("; ".join(parts) + f"; {c['sample_windows']} windows sampled (row bands of each "
+            f"scale, {c['threads']} threads), projected to the step's {c['frame_windows']} "
+            f"windows; CPU {cpu_model_name()}")
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -191,9 +348,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5m"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,7 +364,7 @@ def main():
         return run_reference(args, wl, rank, world)
 
     import torch
-    from paper_1705_03524_b200 import swg
+    from paper_1705_03524_b200 import swg, synth
     # SWG_BENCH_SHARE_GPU=1: test mode for the N>1 code path on a 1-GPU box
     # (every rank on cuda:0, gloo collectives; ranks never wait on each
     # other's kernels, only on host barriers).  Never used for a reported run.
@@ -222,34 +380,99 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    scene = wl["gen"](1 + rank)
-    H, W = scene.image.shape
+    weak = wl["scaling"] == "weak"
+    data = wl["gen"](1 + rank if weak else 1)
     ctx = swg.Context(local)
     # a non-default torch stream: our launches and the CUDA events share it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    reqs = make_requests(ctx, wl, scene)
-    frame_dev = torch.from_numpy(scene.image).cuda()
-    fmt = wl.get("fmt", swg.FMT_GRAY8)
-    tables = ctx.build(frame_dev, fmt, wl["bins"], wl["planes"])
-    maps_dev = [torch.empty(tables.map_shape(r.kernel), dtype=torch.float64, device="cuda")
-                for r in reqs]
-    peaks_dev = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
-    n_win = sum(m.numel() for m in maps_dev)
+    models = make_models(ctx, wl, data)
+    fmt, nb = wl["fmt"], wl["nbins"]
+
+    def new_tables(g, src, pitch=0):
+        if g.get("decay"):
+            return ctx.build_decay(src, g["decay"], fmt, wl["bins"], pitch=pitch)
+        return ctx.build(src, fmt, wl["bins"], g["planes"], pitch=pitch)
+
+    # ---- units: (tables, device source view, pitch, requests, score outputs, peaks)
+    units = []
+    if wl["kind"] == "frame":
+        frame_dev = torch.from_numpy(data.image).cuda()
+        H, W = data.image.shape[:2]
+        for gi, (g, ms) in enumerate(zip(wl["groups"], models)):
+            t = new_tables(g, frame_dev)
+            reqs = [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
+                    for (k, meth, rings, _), m in zip(g["scales"], ms)]
+            maps = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
+                    for r in reqs]
+            units.append(dict(t=t, src=frame_dev, pitch=0, reqs=reqs, maps=maps, g=gi,
+                              sidx=list(range(len(reqs))), h2d=data.image.nbytes))
+        tab_w, tab_h = W, H
+    elif wl["kind"] == "sequence":
+        F, H, W = data.frames.shape[:3]
+        frames_dev = torch.from_numpy(data.frames).cuda()
+        S = data.search
+        g, ms = wl["groups"][0], models[0]
+        mine = [f for f in range(F) if f % world == rank]
+        x0, y0 = synth.search_origin(data, mine[0])
+        t = new_tables(g, frames_dev[mine[0], y0:y0 + S, x0:x0 + S], pitch=W * 3)
+        reqs = [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
+                for (k, meth, rings, _), m in zip(g["scales"], ms)]
+        maps = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
+                for r in reqs]  # one map per scale, overwritten frame after frame
+        for f in mine:
+            x0, y0 = synth.search_origin(data, f)
+            units.append(dict(t=t, src=frames_dev[f, y0:y0 + S, x0:x0 + S], pitch=W * 3,
+                              reqs=reqs, maps=maps, g=0, sidx=list(range(len(reqs))),
+                              frame=f, origin=(x0, y0), h2d=S * S * 3))
+        tab_w = tab_h = S
+    else:  # row bands
+        H, W = data.image.shape[:2]
+        frame_dev = torch.from_numpy(data.image).cuda()
+        g, ms = wl["groups"][0], models[0]
+        n_bands = max(4, world)
+        BH, plan = band_plan(H, g["scales"], n_bands)
+        full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
+                     for k, _, _, _ in g["scales"]]
+        mine = [b for b in range(n_bands) if b % world == rank]
+        t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+        for b in mine:
+            p0, rows = plan[b]
+            reqs, maps, sidx = [], [], []
+            for si, ((k, meth, rings, _), m) in enumerate(zip(g["scales"], ms)):
+                v0, v1 = rows[si]
+                if v1 <= v0:
+                    continue
+                reqs.append(swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings,
+                                           rows=(v0 - p0, v1 - p0)))
+                maps.append(full_maps[si][v0:v1])
+                sidx.append(si)
+            units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
+                              g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
+        tab_w, tab_h = W, BH
+    for u in units:
+        u["peaks"] = torch.zeros(len(u["reqs"]), 3, dtype=torch.float64, device="cuda")
+    n_win = sum(m.numel() for u in units for m in u["maps"]) if wl["kind"] != "sequence" else \
+        sum(m.numel() for m in units[0]["maps"]) * len(units)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step(ev=None):
-        if ev:
-            ev[0].record()
-        tables.rebuild(frame_dev)
-        if ev:
-            ev[1].record()
-        for i, r in enumerate(reqs):
-            tables.likelihood_maps([r], scores="none", scores_dev=[maps_dev[i]],
-                                   peaks_dev=peaks_dev[i])
+        j = 0
+        for u in units:
             if ev:
-                ev[2 + i].record()
+                ev[j].record()
+                j += 1
+            u["t"].rebuild(u["src"], u["pitch"])
+            if ev:
+                ev[j].record()
+                j += 1
+            for i, r in enumerate(u["reqs"]):
+                u["t"].likelihood_maps([r], scores="none", scores_dev=[u["maps"][i]],
+                                       peaks_dev=u["peaks"][i])
+                if ev:
+                    ev[j].record()
+                    j += 1
 
     for _ in range(args.warmup):
         step()
@@ -265,7 +488,7 @@ def main():
             graph.replay()
         torch.cuda.synchronize()
 
-    nev = 2 + len(reqs)
+    nev = sum(2 + len(u["reqs"]) for u in units)
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     clocks = Clocks(local)
     if dist:
@@ -273,15 +496,21 @@ def main():
     torch.cuda.synchronize()
     launches0 = ctx.launches
     clocks.start()
+    t_host = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    enqueue_s = time.perf_counter() - t_host  # host time of one eager step (sizes the spin)
+    launches0 = ctx.launches
     for s in range(args.steps):
-        # a ~1 ms spin lets the host enqueue the whole step before the GPU
-        # reaches it, so the per-kernel events carry no host launch gaps
-        torch.cuda._sleep(2_000_000)
+        # a spin longer than the host's enqueue time lets the whole step queue
+        # up before the GPU reaches it, so the per-kernel events carry no host
+        # launch gaps
+        torch.cuda._sleep(int(max(2e6, 2.5e9 * enqueue_s)))
         flush.zero_()  # evict L2 (256 MiB > 126 MB) between timed steps; not timed
         step(events[s])
     torch.cuda.synchronize()
     clk = clocks.stop()
-    launches = ctx.launches - launches0
+    launches = ctx.launches - launches0  # over the K timed steps
     if dist:
         dist.barrier()
     per_step = [events[s][0].elapsed_time(events[s][-1]) for s in range(args.steps)]
@@ -298,7 +527,7 @@ def main():
         # (100 ms period) sees it; the timed steps follow immediately
         t_soak = time.perf_counter()
         while time.perf_counter() - t_soak < 1.0:
-            for _ in range(20):
+            for _ in range(4):
                 graph.replay()
             torch.cuda.synchronize()
         for s in range(args.steps):
@@ -311,126 +540,205 @@ def main():
         if dist:
             dist.barrier()
         per_step = [gev[s][0].elapsed_time(gev[s][1]) for s in range(args.steps)]
-    build_ms = [events[s][0].elapsed_time(events[s][1]) for s in range(args.steps)]
-    scale_ms = [[events[s][1 + i].elapsed_time(events[s][2 + i]) for s in range(args.steps)]
-                for i in range(len(reqs))]
+
+    # per-launch times: build per unit, sweep per (unit, request)
+    build_ms, sweep_ms = [], {}  # sweep_ms[(group, scale)] = list of per-launch ms
+    for s in range(args.steps):
+        j = 0
+        for ui, u in enumerate(units):
+            e = events[s]
+            build_ms.append(e[j].elapsed_time(e[j + 1]))
+            j += 1
+            for i in range(len(u["reqs"])):
+                sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
+                    e[j].elapsed_time(e[j + 1]))
+                j += 1
+            j += 1
     total_ms = sum(per_step)
     if dist:
         t = torch.tensor([total_ms], device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * n_win * args.steps / (total_ms / 1e3)
+        nw = torch.tensor([float(n_win)], device="cpu" if share else "cuda")
+        dist.all_reduce(nw, op=dist.ReduceOp.SUM)
+        job_win = float(nw.item())
+    else:
+        job_win = float(n_win)
+    value = job_win * args.steps / (total_ms / 1e3)
 
-    # correctness spot check of the timed outputs (peak on the planted target)
-    pk = peaks_dev.cpu().numpy()
-    ok_peaks = True
-    for i, (k, _, _, ti) in enumerate(wl["scales"]):
-        ints = pk[i, :2].view(np.int32)
-        cxp, cyp = int(ints[2]), int(ints[3])
-        tx, ty = target_center(scene, ti)
-        ok_peaks &= abs(cxp - tx) <= 1 and abs(cyp - ty) <= 1
+    # correctness spot check of the timed outputs (peaks on the planted targets)
+    ok_peaks = None
+    if wl["kind"] == "frame":
+        ok_peaks = True
+        for u in units:
+            pk = u["peaks"].cpu().numpy()
+            g = wl["groups"][u["g"]]
+            for i, si in enumerate(u["sidx"]):
+                ti = g["scales"][si][3]
+                if ti is None:
+                    continue
+                ints = pk[i, :2].view(np.int32)
+                tx, ty = target_center(data, ti)
+                ok_peaks &= abs(int(ints[2]) - tx) <= 1 and abs(int(ints[3]) - ty) <= 1
+        ok_peaks = bool(ok_peaks)
+    elif wl["kind"] == "sequence":
+        hits = tot = 0
+        for u in units:
+            pk = u["peaks"].cpu().numpy()
+            gx, gy = data.track[u["frame"]]
+            for i in range(len(u["reqs"])):
+                ints = pk[i, :2].view(np.int32)
+                cx, cy = int(ints[2]) + u["origin"][0], int(ints[3]) + u["origin"][1]
+                hits += abs(cx - gx) <= 2 and abs(cy - gy) <= 2
+                tot += 1
+        ok_peaks = f"{hits}/{tot} frame-scale peaks within 2 px of ground truth"
 
-    # ---- e2e through the C-ABI with host buffers (pinned), same frame
-    frame_pin = swg.PinnedBuffer(scene.image.shape, scene.image.dtype)
-    frame_pin.array[...] = scene.image
-    maps_pin = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in maps_dev]
+    # ---- e2e through the C-ABI with host buffers (pinned)
     import ctypes as C
     from paper_1705_03524_b200.swg import Peak, _Req, _check, lib
-    creqs = (_Req * len(reqs))()
-    for i, r in enumerate(reqs):
-        creqs[i] = _Req(r.kernel, r.method, r.sim, r.rings, r.ring_rule, 0, 0,
-                        r.model.ctypes.data_as(C.POINTER(C.c_double)))
-    host_ptrs = (C.c_void_p * len(reqs))(*[m.array.ctypes.data for m in maps_pin])
-    peaks_host = (Peak * len(reqs))()
+    e2e = None
+    if not args.no_e2e:
+        h2d = d2h = 0
+        if wl["kind"] == "sequence":
+            pin = swg.PinnedBuffer(data.frames.shape, np.uint8)
+            pin.array[...] = data.frames
+            base = pin.array.ctypes.data
+            addrs = [base + ((u["frame"] * H + u["origin"][1]) * W + u["origin"][0]) * 3
+                     for u in units]
+            fr = (C.c_void_p * len(addrs))(*addrs)
+            t = units[0]["t"]
+            creqs, _keep = swg.Tables._creqs(units[0]["reqs"], nb)
+            nreq = len(units[0]["reqs"])
+            peaks_host = (Peak * (len(addrs) * nreq))()
 
-    def e2e_step():
-        _check(lib().swg_tables_rebuild(tables._h, frame_pin.array.ctypes.data, 0, 0))
-        _check(lib().swg_likelihood_maps(tables._h, len(reqs), C.addressof(creqs),
-                                         C.addressof(host_ptrs), None, C.addressof(peaks_host),
-                                         None))
+            def e2e_step():
+                _check(lib().swg_likelihood_batch(t._h, len(addrs), C.addressof(fr), 0, W * 3,
+                                                  nreq, C.addressof(creqs),
+                                                  C.addressof(peaks_host), None))
+            h2d = len(addrs) * S * S * 3
+            d2h = C.sizeof(peaks_host)
+            check = None
+        else:
+            pin = swg.PinnedBuffer(data.image.shape, data.image.dtype)
+            pin.array[...] = data.image
+            row_bytes = data.image.strides[0]
+            calls = []
+            maps_pin = []
+            for u in units:
+                creqs, keep = swg.Tables._creqs(u["reqs"], nb)
+                mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
+                maps_pin.append(mp)
+                hp = (C.c_void_p * len(mp))(*[m.array.ctypes.data for m in mp])
+                pk = (Peak * len(u["reqs"]))()
+                src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
+                calls.append((u["t"], src, creqs, keep, hp, pk, len(u["reqs"])))
+                h2d += u["h2d"]
+                d2h += sum(m.nbytes for m in mp) + C.sizeof(pk)
 
-    for _ in range(args.warmup):
-        e2e_step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e2e_t = []
-    for _ in range(args.steps):
-        flush.zero_()
+            def e2e_step():
+                for t, src, creqs, _k, hp, pk, n in calls:
+                    _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
+                    _check(lib().swg_likelihood_maps(t._h, n, C.addressof(creqs),
+                                                     C.addressof(hp), None, C.addressof(pk),
+                                                     None))
+
+            def check():
+                for u, mp in zip(units, maps_pin):
+                    for m, mpin in zip(u["maps"], mp):
+                        assert (mpin.array == m.cpu().numpy()).all()
+
+        for _ in range(args.warmup):
+            e2e_step()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e2e_step()  # returns after the host maps + peaks are filled
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_total = sum(e2e_t)
-    if dist:
-        t = torch.tensor([e2e_total], device="cpu" if share else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_value = world * n_win * args.steps / e2e_total
-    for i in range(len(reqs)):
-        assert (maps_pin[i].array == maps_dev[i].cpu().numpy()).all()
+        if dist:
+            dist.barrier()
+        e2e_t = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()  # returns after the host maps + peaks are filled
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_total = sum(e2e_t)
+        if dist:
+            t_ = torch.tensor([e2e_total], device="cpu" if share else "cuda")
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            e2e_total = float(t_.item())
+        if check:
+            check()
+        e2e = {"value": job_win * args.steps / e2e_total, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_total / args.steps * 1e3}
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel and of the IH build (SURVEY §8d bytes)
+    # ---- roofline of the dominant launch and of the IH build (SURVEY §8d bytes)
     hbm, src = peaks_json()
-    b, P, e = wl["bins"], wl["P"], wl["elem"]  # e: bytes per table entry
-    ih_bytes = (W + 1) * (H + 1) * b * P * e
-    scale_avg = [sum(x) / args.steps for x in scale_ms]
-    dom = max(range(len(reqs)), key=lambda i: scale_avg[i])  # the largest share of the step
-    dom_bytes = ih_bytes + 8 * maps_dev[dom].numel()
-    kname = {swg.CAKE: "k_sweep_cake16" if e == 2 else "k_sweep_cake",
-             swg.SWIH: "k_sweep_affine"}.get(reqs[dom].method, "sweep")
+    cells = (tab_w + 1) * (tab_h + 1) * nb
+    per_scale = {}
+    for (gi, si), ts in sweep_ms.items():
+        per_scale[(gi, si)] = sum(ts) / args.steps  # ms per step
+    dom = max(sweep_ms, key=lambda key: sum(sweep_ms[key]) / len(sweep_ms[key]))
+    gi, si = dom
+    g = wl["groups"][gi]
+    k, meth = g["scales"][si][0], g["scales"][si][1]
+    kname, P, e = engine_of(g, k, meth)
+    dom_ms = sum(sweep_ms[dom]) / len(sweep_ms[dom])
+    win_launch = {}
+    for u in units:
+        for i, s_ in enumerate(u["sidx"]):
+            win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
+    dom_win = sum(win_launch[dom]) / len(win_launch[dom])
+    dom_bytes = cells * P * e + 8 * dom_win
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        t = json.load(open(tp)).get(args.config)
-        if t and kname in t.get("kernel", ""):
-            traffic = t["dram_bytes"]
-    roofline = {"bound": "hbm", "achieved": dom_bytes / (scale_avg[dom] / 1e3) / 1e9,
+        tr = json.load(open(tp)).get(args.config)
+        if tr and kname in tr.get("kernel", ""):
+            traffic = tr["dram_bytes"]
+    roofline = {"bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9,
                 "peak": hbm, "unit": "GB/s", "traffic": traffic, "peak_source": src,
-                "kernel": f"{kname} at {reqs[dom].kernel.kw}x{reqs[dom].kernel.kh} "
-                          f"(IH read once + 8 B/window = {dom_bytes} B per launch, "
-                          f"{scale_avg[dom]:.3f} ms)"}
+                "kernel": f"{kname} at {k.kw}x{k.kh} (planes read once + 8 B/window = "
+                          f"{int(dom_bytes)} B per launch, {dom_ms:.4f} ms)"}
     roofline["frac"] = roofline["achieved"] / hbm
-    build_avg = sum(build_ms) / args.steps
-    build_bytes = scene.image.nbytes + ih_bytes
+    build_avg = sum(build_ms) / args.steps  # ms per step, all rebuilds
+    in_bytes = sum(u["h2d"] for u in units)
+    build_bytes = in_bytes + sum(group_build_bytes(wl["groups"][u["g"]], tab_w, tab_h, nb)
+                                 for u in units)
     build_roof = {"bound": "hbm", "achieved": build_bytes / (build_avg / 1e3) / 1e9, "peak": hbm,
-                  "unit": "GB/s", "kernel": "k_quantize + k_colsum + k_bandscan + k_build",
-                  "ms": build_avg}
+                  "unit": "GB/s", "ms": build_avg, "bytes": build_bytes,
+                  "kernel": "k_quantize + k_colsum + k_bandscan + k_build (per table set)"}
     build_roof["frac"] = build_roof["achieved"] / hbm
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        models = [r.model for r in reqs]
-        c = cpu_reference(wl, scene, models)
-        cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": "reference",
-               "sample": (f"oracle/_ref (unmodified reference sources): one build_tables "
-                          f"({c['t_build_s']:.2f} s, 1 thread) + WeddingCakePlan sweep of "
-                          f"{c['sample_windows']} windows (row bands of each scale, "
-                          f"{c['threads']} threads), projected to the full frame of "
-                          f"{c['frame_windows']} windows; CPU {cpu_model_name()}")}
+        c = cpu_reference(wl, data, models)
+        cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": c["kind"],
+               "sample": cpu_sample_text(wl, c)}
 
+    scale_names = [f"{['uniform', 'manhattan', 'chebyshev', 'gauss_cheb', 'euclid_quad', 'exp_l1'][g['scales'][s][0].kind]}"
+                   f"{g['scales'][s][0].kw}x{g['scales'][s][0].kh}"
+                   for g in wl["groups"] for s in range(len(g["scales"]))]
+    flat = [per_scale.get((gi, s), 0.0) for gi, g in enumerate(wl["groups"])
+            for s in range(len(g["scales"]))]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
-        "data": "synthetic (seeded blurred-noise frame with planted targets, config generator "
-                "in paper_1705_03524_b200/synth.py)",
-        "config": {"workload": wl["name"], "frames_per_gpu": 1, "width": W, "height": H,
-                   "bins": wl["bins"], "windows_per_frame": n_win,
+        "scaling": wl["scaling"], "vs_baseline": None,
+        "dtype": "u16/u32/u64 tables + f64 scores",
+        "data": "synthetic (seeded generators in paper_1705_03524_b200/synth.py)",
+        "config": {"workload": wl["name"], "bins": nb, "windows_per_step": int(job_win),
+                   "table_shape": [tab_w, tab_h], "units_per_rank": len(units),
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
-                   "parallelism": f"frames sharded over {world} GPU(s), no collective"},
+                   "parallelism": (f"{'frames' if weak else wl['kind']} sharded over {world} "
+                                   f"GPU(s), no collective")},
         "ih_build": {"ms": build_avg, "gbps": build_roof["achieved"], "frac": build_roof["frac"]},
-        "per_scale_ms": scale_avg,
+        "per_scale_ms": dict(zip(scale_names, flat)),
         "roofline": roofline, "build_roofline": build_roof,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": scene.image.nbytes,
-                "d2h_bytes_per_step": 8 * n_win + 24 * len(reqs),
-                "ms_per_step": e2e_total / args.steps * 1e3},
-        "gpu_launches": launches, "peaks_on_targets": bool(ok_peaks),
+        "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches // args.steps, "peaks_on_targets": ok_peaks,
         "cpu_baseline": cpu, "clocks": clk,
     }
     print(json.dumps(out), flush=True)
@@ -441,26 +749,37 @@ def main():
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
-    import ctypes as C  # noqa: F401
     from oracle import oracle as O
-    from paper_1705_03524_b200 import swg, synth  # noqa: F401
-    scene = wl["gen"](1)
+    from paper_1705_03524_b200 import swg, synth
+    data = wl["gen"](1)
     # models with the reference's own target_model_for_method (matching.cpp:84-106)
+    # where it applies; the oracle restatement for the declared formats/kernels
     R = O.Ref()
+    orc = O.Oracle()
     models = []
-    for k, method, rings, ti in wl["scales"]:
-        cx, cy = target_center(scene, ti)
-        templ = synth.crop(scene.image, cx, cy, k.kw, k.kh)
-        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
-        if templ.dtype == np.uint16:
-            orc = O.Oracle()
-            models.append(orc.target_model(orc.quantize_gray16(templ, wl["bins"]), wl["bins"], ok,
-                                           method, rings))
-        else:
-            models.append(R.target_model(templ, wl["bins"], ok, method, rings))
+    for g in wl["groups"]:
+        ms = []
+        for k, method, rings, ti in g["scales"]:
+            if wl["kind"] == "sequence":
+                cx, cy = data.track[0]
+                img = data.frames[0]
+            else:
+                cx, cy = target_center(data, ti)
+                img = data.image
+            templ = synth.crop(img, cx, cy, k.kw, k.kh)
+            ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+            if wl["fmt"] == swg.FMT_GRAY8 and k.kind in (swg.MANHATTAN, swg.UNIFORM,
+                                                         swg.GAUSS_CHEB):
+                ms.append(R.target_model(templ, wl["bins"], ok, method, rings))
+            else:
+                ms.append(orc.target_model(_quantize_host(wl, templ), wl["nbins"], ok,
+                                           O.BRUTE if method == swg.SWIH and
+                                           k.kind not in (swg.MANHATTAN, swg.UNIFORM)
+                                           else method, rings))
+        models.append(ms)
     vals = []
     for s in range(args.warmup + args.steps):
-        c = cpu_reference(wl, scene, models, budget_s=max(60.0 / (args.warmup + args.steps), 1.5))
+        c = cpu_reference(wl, data, models, budget_s=max(60.0 / (args.warmup + args.steps), 1.5))
         if s >= args.warmup:
             vals.append(c)
     value = statistics.mean(v["value"] for v in vals)
@@ -468,14 +787,11 @@ def run_reference(args, wl, rank, world):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": n_win / value * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "i64+f64", "impl": "reference",
+        "scaling": wl["scaling"], "vs_baseline": None, "dtype": "i64+f64", "impl": "reference",
         "data": "synthetic (same generator and seed as --impl ours)",
-        "config": {"workload": wl["name"], "frames_per_gpu": 1},
+        "config": {"workload": wl["name"], "bins": wl["nbins"], "windows_per_step": n_win},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": vals[0]["threads"],
-                         "kind": "reference",
-                         "sample": "per step: one reference build_tables (1 thread) + row-band "
-                                   "sample of each scale's WeddingCakePlan sweep on all host "
-                                   "threads, projected to the full frame; CPU " + cpu_model_name()},
+                         "kind": vals[0]["kind"], "sample": "per step: " + cpu_sample_text(wl, vals[0])},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

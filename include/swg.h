@@ -269,6 +269,18 @@ swg_status swg_likelihood_maps(swg_tables* t, int n,
                                double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev);
 
+/* Batch of frames of the tables' geometry (tracking sequences, config 3):
+ * for each frame f, rebuild the tables from frames[f] (pitch_bytes, host or
+ * device as is_device; a search-region crop is a pointer into the full frame
+ * plus the full frame's pitch) and run the n requests, peaks only.  Peak of
+ * frame f, request i -> [f * n + i] of peaks_dev (device, asynchronous)
+ * and/or peaks_host (filled on return).  Frames are processed in order
+ * through the one table set. */
+swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* frames,
+                                int is_device, size_t pitch_bytes, int n,
+                                const swg_map_request* reqs, swg_peak* peaks_host,
+                                swg_peak* peaks_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,7 +50,12 @@ def target_model(ctx: swg.Context, templ: np.ndarray, kernel: swg.Kernel, fmt=sw
 
 
 def _brute_model(t: swg.Tables, kernel: swg.Kernel) -> np.ndarray:
-    raise NotImplementedError("brute-force target model for non-affine kernels: use method=CAKE")
+    """BruteForcePlan on the template's one strict window (matching.cpp:84-106
+    with MapMethod::BruteForce; baselines.cpp:24-69): counts for integer
+    kernels, fp64 weight sums otherwise, then normalize."""
+    fi = t.feature_image()
+    raw = t.ctx.brute_windows(fi, t.bins, [kernel.hx], [kernel.hy], kernel)[0]
+    return normalize(raw.astype(np.float64))
 
 
 class MultiScaleMatcher:

@@ -166,13 +166,19 @@ __global__ void k_select_cand(const double* scores, size_t n, int row0, int mw,
 // + score_weights order), written back into the map; one window per thread.
 // When more than `cap` windows qualified, the same threads stride over the
 // whole map and re-score every qualifying cell instead (slow but exact).
-__global__ void k_rescore(const uint16_t* fi, size_t fi_pitch, const double* grid, int kw,
-                          int kh, int mw, int row0, int rows, int bins, int sim,
-                          const double* model, const swg_peak* fast, double eps,
-                          const int* count, const long long* cand, int cap, double* hist,
-                          double* scores, PeakPart* parts) {
+__global__ void k_rescore(const SweepArgs a, const RescoreArgs r, const swg_peak* fast) {
+  const uint16_t* fi = r.fi;
+  const size_t fi_pitch = r.fi_pitch;
+  const double* grid = r.grid;
+  const int kw = r.kw, kh = r.kh, mw = a.mw, row0 = a.row0, rows = a.rows, bins = a.bins;
+  const double* model = a.model;
+  double* hist = r.hist;
+  double* scores = a.scores;
+  const int cap = r.cap;
+  const long long* cand = r.cand;
+  const double eps = r.eps;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
-  const int cnt = *count;
+  const int cnt = *r.count;
   const bool overflow = cnt > cap;
   const double lim = fast->score - eps;
   const long long total = overflow ? (long long)rows * mw : cnt;
@@ -198,7 +204,7 @@ __global__ void k_rescore(const uint16_t* fi, size_t fi_pitch, const double* gri
     }
     double mass = 0.0, acc = 0.0;
     for (int b = 0; b < bins; ++b) mass = __dadd_rn(mass, h[b]);
-    if (sim == SWG_SIM_BHATTACHARYYA) {
+    if (a.sim == SWG_SIM_BHATTACHARYYA) {
       for (int b = 0; b < bins; ++b) acc = __dadd_rn(acc, __dsqrt_rn(__dmul_rn(model[b], h[b])));
       acc = mass > 0.0 ? __ddiv_rn(acc, __dsqrt_rn(mass)) : 0.0;
     } else if (mass > 0.0) {
@@ -214,7 +220,7 @@ __global__ void k_rescore(const uint16_t* fi, size_t fi_pitch, const double* gri
       bidx = idx;
     }
   }
-  block_peak_e(best, bidx, parts + blockIdx.x);
+  block_peak_e(best, bidx, r.parts + blockIdx.x);
 }
 
 }  // namespace
@@ -234,9 +240,7 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (r.cap + 127) / 128;
-  k_rescore<<<blocks, 128, 0, s>>>(r.fi, r.fi_pitch, r.grid, r.kw, r.kh, a.mw, a.row0, a.rows,
-                                   a.bins, a.sim, r.model, peak, r.eps, r.count, r.cand, r.cap,
-                                   r.hist, a.scores, r.parts);
+  k_rescore<<<blocks, 128, 0, s>>>(a, r, peak);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return launch_peak_reduce(r.parts, blocks, a.mw, a.hx, a.hy, peak, s);
 }

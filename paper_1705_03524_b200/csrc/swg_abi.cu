@@ -192,7 +192,7 @@ struct swg_ctx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
-  DevBuf parts, scores, peaks, terms, qout, grid, io, resc;
+  DevBuf parts, scores, peaks, terms, qout, grid, io, resc, bpeaks;
   // exact kernel-weight grids, uploaded once per kernel (graph-capture safe)
   struct Grid {
     swg_kernel k;
@@ -475,6 +475,7 @@ static void ctx_release(swg_ctx* c) {
     c->grid.release();
     c->io.release();
     c->resc.release();
+    c->bpeaks.release();
     for (auto* g : c->grids) {
       g->buf.release();
       delete g;
@@ -1311,16 +1312,12 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ra.eps = 1e-4;
         const size_t hb = (size_t)ra.cap * t->bins * 8, cb = (size_t)ra.cap * 8;
         const size_t pb = (size_t)((ra.cap + 127) / 128) * sizeof(PeakPart);
-        ST_TRY(c->resc.ensure(hb + cb + pb + 256 + (size_t)t->bins * 8));
+        ST_TRY(c->resc.ensure(hb + cb + pb + 256));
         char* rb = static_cast<char*>(c->resc.p);
         ra.hist = reinterpret_cast<double*>(rb);
         ra.cand = reinterpret_cast<long long*>(rb + hb);
         ra.parts = reinterpret_cast<PeakPart*>(rb + hb + cb);
         ra.count = reinterpret_cast<int*>(rb + hb + cb + pb);
-        double* dmodel = reinterpret_cast<double*>(rb + hb + cb + pb + 256);
-        ra.model = dmodel;
-        CUDA_TRY(cudaMemcpyAsync(dmodel, a.model, (size_t)t->bins * 8, cudaMemcpyHostToDevice,
-                                 c->stream));
         CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, c->stream));
         c->launches += 3;
       } else if (engine[i] == kQuad64) {
@@ -1408,6 +1405,41 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     sync = true;
   }
   if (sync) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* frames,
+                                int is_device, size_t pitch_bytes, int n,
+                                const swg_map_request* reqs, swg_peak* peaks_host,
+                                swg_peak* peaks_dev) {
+  ST_TRY(check_tables(t));
+  if (n_frames < 0 || n < 0 || (n_frames && !frames) || (n && !reqs))
+    return fail(SWG_ERR_ARG, "bad frame or request list");
+  if (!n_frames || !n) return SWG_OK;
+  swg_ctx* c = t->ctx;
+  swg_peak* dst = peaks_dev;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (!dst) {
+      ST_TRY(c->bpeaks.ensure((size_t)n_frames * n * sizeof(swg_peak)));
+      dst = static_cast<swg_peak*>(c->bpeaks.p);
+    }
+  }
+  // frames run back to back through the one table set, stream ordered: the
+  // upload + build of frame f+1 queues behind the sweeps of frame f
+  for (int f = 0; f < n_frames; ++f) {
+    if (!frames[f]) return fail(SWG_ERR_ARG, "NULL frame %d", f);
+    ST_TRY(swg_tables_rebuild(t, frames[f], is_device, pitch_bytes));
+    ST_TRY(swg_likelihood_maps(t, n, reqs, nullptr, nullptr, nullptr, dst + (size_t)f * n));
+  }
+  if (peaks_host) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaMemcpyAsync(peaks_host, dst, (size_t)n_frames * n * sizeof(swg_peak),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
   return SWG_OK;
 }
 

@@ -135,7 +135,6 @@ struct RescoreArgs {
   size_t fi_pitch;
   const double* grid;  // kh x kw exact kernel weights (host-computed)
   int kw, kh;
-  const double* model; // device copy of the model
   int* count;          // device candidate counter
   long long* cand;     // candidates (absolute map index)
   int cap;

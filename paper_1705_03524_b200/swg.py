@@ -167,6 +167,9 @@ def lib():
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
         "swg_likelihood_maps": [vp, C.c_int, vp, vp, vp, vp, vp],
+        "swg_likelihood_batch": [vp, C.c_int, vp, C.c_int, C.c_size_t, C.c_int, vp, vp, vp],
+        "swg_brute_windows": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
+                              C.POINTER(Kernel), C.c_int, vp, vp],
         "swg_host_alloc": [C.c_size_t, C.POINTER(vp)],
         "swg_host_free": [vp],
     }.items():
@@ -262,6 +265,23 @@ class Context:
         t._info()
         t.decay = float(decay)
         return t
+
+    def brute_windows(self, fi, bins, cx, cy, kernel, border=STRICT, integer=None):
+        """swg_brute_windows: brute-force weighted histograms of explicit
+        windows of a host feature image (BruteForcePlan, baselines.cpp:24-69).
+        integer=True -> int64 counts (integer kernels), else fp64 sums."""
+        fi = np.ascontiguousarray(fi, np.uint16)
+        h, w = fi.shape
+        cx = np.ascontiguousarray(cx, np.int32)
+        cy = np.ascontiguousarray(cy, np.int32)
+        if integer is None:
+            integer = kernel.kind not in (GAUSS_CHEB, EXP_L1)
+        out = np.empty((len(cx), bins), np.int64 if integer else np.float64)
+        _check(lib().swg_brute_windows(self._h, _ptr(fi), w, h, bins, len(cx), _ptr(cx),
+                                       _ptr(cy), C.byref(kernel), border,
+                                       _ptr(out) if integer else None,
+                                       None if integer else _ptr(out)))
+        return out
 
     def upload_i64(self, plain, xramp, yramp) -> "Tables":
         plain, xramp, yramp = (np.ascontiguousarray(a, np.int64) for a in (plain, xramp, yramp))
@@ -417,6 +437,45 @@ class Tables:
             C.addressof(peaks) if peaks is not None else None,
             _ptr(peaks_dev) if peaks_dev is not None else None))
         return maps, ([p.astuple() for p in peaks] if peaks is not None else None)
+
+    @staticmethod
+    def _creqs(reqs, bins):
+        creqs = (_Req * len(reqs))()
+        models = []
+        for i, r in enumerate(reqs):
+            m = np.ascontiguousarray(r.model, np.float64)
+            if m.shape != (bins,):
+                raise ModelError(f"likelihood map: model must be normalized with {bins} bins")
+            models.append(m)
+            r0, r1 = r.rows if r.rows else (0, 0)
+            creqs[i] = _Req(r.kernel, r.method, r.sim, r.rings, r.ring_rule, r0, r1,
+                            m.ctypes.data_as(C.POINTER(C.c_double)))
+        return creqs, models
+
+    def likelihood_batch(self, frames, reqs: Sequence[MapRequest], pitch=0, is_device=None,
+                         peaks_dev=None):
+        """swg_likelihood_batch: rebuild from each frame (numpy arrays / torch
+        tensors, or raw addresses with is_device given) and run `reqs`, peaks
+        only.  Returns peaks[f][i] (host) unless peaks_dev is given."""
+        addrs = []
+        for f in frames:
+            if isinstance(f, int):
+                addrs.append(f)
+            else:
+                addrs.append(_ptr(f))
+                if is_device is None:
+                    is_device = 0 if isinstance(f, np.ndarray) else int(f.is_cuda)
+        nf, n = len(frames), len(reqs)
+        fr = (C.c_void_p * max(nf, 1))(*addrs)
+        creqs, _keep = self._creqs(reqs, self.bins)
+        peaks = (Peak * (nf * n))() if peaks_dev is None else None
+        _check(lib().swg_likelihood_batch(
+            self._h, nf, C.addressof(fr), int(is_device or 0), pitch, n, C.addressof(creqs),
+            C.addressof(peaks) if peaks is not None else None,
+            _ptr(peaks_dev) if peaks_dev is not None else None))
+        if peaks is None:
+            return None
+        return [[peaks[f * n + i].astuple() for i in range(n)] for f in range(nf)]
 
     def likelihood_map(self, kernel, model, method=SWIH, sim=BHATTACHARYYA, rings=4,
                        ring_rule=RING_MEAN, rows=None):

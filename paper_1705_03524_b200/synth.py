@@ -111,3 +111,72 @@ def config5(seed: int = 1) -> Scene:
     g = _blur_axis(_blur_axis(g, taps, 0), taps, 1)
     g = np.clip(g * 65535 // max(int(np.percentile(g, 99.9)), 1), 0, 65535)
     return Scene(g.astype(np.uint16), [])
+
+
+def _texture(ph: int, pw: int, channels: int, seed: int, base: int, maxval: int = 255):
+    """A target's own appearance: blurred texture around a base level."""
+    rng = np.random.default_rng(seed)
+    shape = (ph, pw) + ((channels,) if channels else ())
+    tex = rng.integers(-40, 41, size=shape, dtype=np.int64)
+    tex = _blur_axis(_blur_axis(tex, gaussian_taps(1.0), 0), gaussian_taps(1.0), 1)
+    return np.clip(base + tex, 0, maxval)
+
+
+@dataclass
+class Sequence:
+    frames: np.ndarray                 # (F, H, W, 3) uint8
+    track: list                        # ground-truth (cx, cy) per frame
+    size: tuple                        # target (w, h)
+    search: int                        # search-region side
+
+
+def config3(seed: int = 1, n_frames: int = 64, h: int = 1080, w: int = 1920,
+            target=(48, 64), search: int = 256) -> Sequence:
+    """64 RGB frames 1920x1080: static blurred colour noise, one 48x64 (w x h)
+    target translating 0-4 px/frame per axis (BASELINE config 3).  The
+    target's appearance is fixed (pasted), so the tracker's model from
+    frame 0 applies to every frame."""
+    bg = blurred_noise(h, w, seed, channels=3).astype(np.uint8)
+    tw, th = target
+    rng = np.random.default_rng(seed + 7)
+    base = rng.integers(40, 216, size=3)
+    tex = _texture(th, tw, 3, seed + 11, 0) + base
+    tex = np.clip(tex, 0, 255).astype(np.uint8)
+    cx, cy = w // 3, h // 3
+    frames = np.empty((n_frames, h, w, 3), np.uint8)
+    track = []
+    for f in range(n_frames):
+        if f:
+            cx += int(rng.integers(0, 5))
+            cy += int(rng.integers(0, 5))
+        frames[f] = bg
+        frames[f, cy - th // 2:cy - th // 2 + th, cx - tw // 2:cx - tw // 2 + tw] = tex
+        track.append((cx, cy))
+    return Sequence(frames, track, (tw, th), search)
+
+
+def search_origin(seq: Sequence, f: int):
+    """Open-loop search region of frame f: centred on frame f-1's ground
+    truth (frame 0: its own), clamped to the frame."""
+    cx, cy = seq.track[max(f - 1, 0)]
+    h, w = seq.frames.shape[1:3]
+    s = seq.search
+    return (int(np.clip(cx - s // 2, 0, w - s)), int(np.clip(cy - s // 2, 0, h - s)))
+
+
+def config4(seed: int = 1, h: int = 2160, w: int = 3840, n_targets: int = 16) -> Scene:
+    """3840x2160 RGB blurred colour noise with 16 planted targets of sizes
+    24..128 (BASELINE config 4)."""
+    img = blurred_noise(h, w, seed, channels=3)
+    rng = np.random.default_rng(seed + 1)
+    sizes = np.round(np.geomspace(24, 128, n_targets)).astype(int)
+    placed = []
+    for i, s in enumerate(sizes):
+        s = int(s)
+        cx = int(rng.integers(s, w - s))
+        cy = int(rng.integers(s, h - s))
+        base = rng.integers(30, 226, size=3)
+        tex = _texture(s, s, 3, seed + 200 + i, 0) + base
+        img[cy - s // 2:cy - s // 2 + s, cx - s // 2:cx - s // 2 + s] = np.clip(tex, 0, 255)
+        placed.append((cx, cy, s, s))
+    return Scene(img.astype(np.uint8), placed)
