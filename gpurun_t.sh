@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+for c in c5; do
+  timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err; echo "$c rc=$?"
+done

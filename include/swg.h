@@ -173,7 +173,8 @@ swg_status swg_tables_build(swg_ctx* ctx, const void* pixels, int is_device,
  * of [bin] decay^(X-1-x) decay^(Y-1-y), for the image and its horizontal,
  * vertical and double flip.  EXP_L1 maps with sigma == decay run in O(1) per
  * window and bin; their peak is made exact by an fp64 brute-force re-score
- * of every window within 1e-4 of the fast maximum. */
+ * of every window whose fast score is within a derived error bound of
+ * the fast maximum. */
 swg_status swg_tables_build_decay(swg_ctx* ctx, const void* pixels, int is_device,
                                   size_t pitch_bytes, int width, int height, int format,
                                   int bins, double decay, size_t memory_budget,

@@ -471,8 +471,6 @@ template cudaError_t launch_export<uint32_t, uint32_t>(const uint32_t*, size_t, 
 template cudaError_t launch_export<uint64_t, int64_t>(const uint64_t*, size_t, size_t, int,
                                                       int, int, int, int, int, int64_t*,
                                                       cudaStream_t);
-template cudaError_t launch_export<double, double>(const double*, size_t, size_t, int, int, int,
-                                                   int, int, int, double*, cudaStream_t);
 
 cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int kind,
                               uint64_t* tab, size_t ps, size_t pitch, int planes,

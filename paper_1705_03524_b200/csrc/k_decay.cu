@@ -13,8 +13,15 @@
 // The four orientations are the same SE table built on the feature image
 // flipped horizontally / vertically / both (k_flip), so one build pipeline
 // serves all four.  It mirrors the integer build: K1a' decayed column sums
-// per band, K1b' decayed scan over bands, K1c' per (band, octet) CTA with a
-// block-wide affine scan per row and t = d*t + R per column.  fp64 storage
+// per band, K1b' decayed scan over bands, K1c' per (band, bin pair) CTA with
+// a block-wide affine scan per row and t = d*t + R per column.
+// Layout: BIN PAIRS, not octets -- a record is the 2 bins of one pair at one
+// cell (16 B of fp64), element (b, kind k, x, y) at
+//   (((b/2)*4 + k)*plane_stride + y*pitch + x)*2 + b%2,
+// with the pair count padded to a multiple of 4 (whole octets).  Two fp64
+// bins per thread and column keep a full-row CTA's state in registers at
+// widths up to 4096 (8 columns per thread); the sweep reads 16-B records,
+// 16 windows' records contiguous per half-warp.  fp64 storage
 // and recurrences: fp32 noise (~1e-7 of the table values) is comparable to
 // the smallest quadrant contributions at large windows and Bhattacharyya's
 // sqrt amplifies it; fp64 keeps every map value within 1e-9 of the exact
@@ -32,17 +39,18 @@ using real = double;
 // Exclusive block scan of y -> alpha*y + B_t over threads (alpha shared by
 // all threads, 8 independent B components): returns the value entering each
 // thread.  One __syncthreads; `buf` ([8][32]) alternates between calls.
-__device__ __forceinline__ void block_exscan_decay(const real (&B)[kOct], real alpha,
-                                                   real (&enter)[kOct], real* buf, int lane,
+template <int N>
+__device__ __forceinline__ void block_exscan_decay(const real (&B)[N], real alpha,
+                                                   real (&enter)[N], real* buf, int lane,
                                                    int warp, int nwarps) {
-  real inc[kOct];
+  real inc[N];
 #pragma unroll
-  for (int j = 0; j < kOct; ++j) inc[j] = B[j];
+  for (int j = 0; j < N; ++j) inc[j] = B[j];
   real ap = alpha;  // alpha^off
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
-    for (int j = 0; j < kOct; ++j) {
+    for (int j = 0; j < N; ++j) {
       const real t = __shfl_up_sync(0xFFFFFFFFu, inc[j], off);
       if (lane >= off) inc[j] = fma(ap, t, inc[j]);
     }
@@ -51,7 +59,7 @@ __device__ __forceinline__ void block_exscan_decay(const real (&B)[kOct], real a
   const real a32 = ap;  // alpha^32
   if (lane == 31) {
 #pragma unroll
-    for (int j = 0; j < kOct; ++j) buf[j * 32 + warp] = inc[j];
+    for (int j = 0; j < N; ++j) buf[j * 32 + warp] = inc[j];
   }
   __syncthreads();
   // value entering warp w: sum_{v<w} a32^(w-1-v) W_v (each warp scans the totals)
@@ -64,7 +72,7 @@ __device__ __forceinline__ void block_exscan_decay(const real (&B)[kOct], real a
     }
   }
 #pragma unroll
-  for (int j = 0; j < kOct; ++j) {
+  for (int j = 0; j < N; ++j) {
     real wt = lane < nwarps ? buf[j * 32 + lane] : 0.0;
     real bp = a32;
 #pragma unroll
@@ -96,27 +104,22 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 }
 
 // K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
-__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec) {
-  const int band = blockIdx.x, grp = blockIdx.y;
+// agg: [nbands][pairs][wa] double2.
+__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs) {
+  const int band = blockIdx.x, pr = blockIdx.y;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)grp * kOct;
-  real c[kOct];
-#pragma unroll
-  for (int j = 0; j < kOct; ++j) c[j] = 0.0;
+  const uint32_t gb = (uint32_t)pr * kDP;
+  real c0 = 0.0, c1 = 0.0;
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
     const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
-#pragma unroll
-    for (int j = 0; j < kOct; ++j) c[j] = fma(dec, c[j], d == (uint32_t)j ? 1.0 : 0.0);
+    c0 = fma(dec, c0, d == 0u ? 1.0 : 0.0);
+    c1 = fma(dec, c1, d == 1u ? 1.0 : 0.0);
   }
-  double2* dst = reinterpret_cast<double2*>(reinterpret_cast<real*>(g.agg) +
-                                             (((size_t)band * g.groups + grp) * g.wa + x) * kOct);
-  dst[0] = make_double2(c[0], c[1]);
-  dst[1] = make_double2(c[2], c[3]);
-  dst[2] = make_double2(c[4], c[5]);
-  dst[3] = make_double2(c[6], c[7]);
+  reinterpret_cast<double2*>(g.agg)[((size_t)band * pairs + pr) * g.wa + x] =
+      make_double2(c0, c1);
 }
 
 // K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place);
@@ -161,27 +164,20 @@ __device__ __forceinline__ void load_bins_d(const uint16_t* p, uint16_t (&v)[CPT
   }
 }
 
-__device__ __forceinline__ void store_rec_f(real* dst, const real (&v)[kOct]) {
-  double2* d = reinterpret_cast<double2*>(dst);
-  d[0] = make_double2(v[0], v[1]);
-  d[1] = make_double2(v[2], v[3]);
-  d[2] = make_double2(v[4], v[5]);
-  d[3] = make_double2(v[6], v[7]);
-}
-
-// K1c': decayed SE table of one orientation: one CTA per (band, octet).
+// K1c': decayed SE table of one orientation: one CTA per (band, bin pair).
 template <int CPT>
-__global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec, int kind) {
-  __shared__ real s_row[2][kOct * 32];
-  __shared__ real s_carry[kOct * 32];
-  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
+__global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec, int kind,
+                                                     int pairs) {
+  __shared__ real s_row[2][kDP * 32];
+  __shared__ real s_carry[kDP * 32];
+  const int band = blockIdx.x / pairs, pr = blockIdx.x % pairs;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
   const int xb = tid * CPT;
   const bool live = xb < g.w;
   const uint16_t* fi = g.fi + (live ? xb : 0);
-  const uint32_t gb = (uint32_t)grp * kOct;
+  const uint32_t gb = (uint32_t)pr * kDP;
   real dp[CPT + 1];  // d^i
   dp[0] = 1.0;
 #pragma unroll
@@ -189,10 +185,10 @@ __global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec
   const real alpha = dp[CPT];
 
   // decayed row prefix of per-column values v[i][j] along x, into r[i][j]
-  auto row_prefix = [&](const real (&v)[CPT][kOct], real (&r)[CPT][kOct], real* buf) {
-    real tot[kOct], ent[kOct];
+  auto row_prefix = [&](const real (&v)[CPT][kDP], real (&r)[CPT][kDP], real* buf) {
+    real tot[kDP], ent[kDP];
 #pragma unroll
-    for (int j = 0; j < kOct; ++j) {
+    for (int j = 0; j < kDP; ++j) {
       real run = 0.0;
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
@@ -201,66 +197,78 @@ __global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec
       }
       tot[j] = run;
     }
-    block_exscan_decay(tot, alpha, ent, buf, lane, warp, nwarps);
+    block_exscan_decay<kDP>(tot, alpha, ent, buf, lane, warp, nwarps);
 #pragma unroll
     for (int i = 0; i < CPT; ++i)
 #pragma unroll
-      for (int j = 0; j < kOct; ++j) r[i][j] = fma(dp[i + 1], ent[j], r[i][j]);
+      for (int j = 0; j < kDP; ++j) r[i][j] = fma(dp[i + 1], ent[j], r[i][j]);
   };
 
   // carry row E(x+1, y0) from the decayed column sums above the band
-  real t[CPT][kOct];
+  real t[CPT][kDP];
   {
-    real cc[CPT][kOct];
+    real cc[CPT][kDP];
 #pragma unroll
     for (int i = 0; i < CPT; ++i)
 #pragma unroll
-      for (int j = 0; j < kOct; ++j) cc[i][j] = 0.0;
+      for (int j = 0; j < kDP; ++j) cc[i][j] = 0.0;
     if (live && band > 0) {
-      const real* src = reinterpret_cast<const real*>(g.agg) +
-                        (((size_t)band * g.groups + grp) * g.wa + xb) * kOct;
+      const double2* src = reinterpret_cast<const double2*>(g.agg) +
+                           ((size_t)band * pairs + pr) * g.wa + xb;
 #pragma unroll
-      for (int i = 0; i < CPT; ++i)
-#pragma unroll
-        for (int j = 0; j < kOct; ++j) cc[i][j] = src[i * kOct + j];
+      for (int i = 0; i < CPT; ++i) {
+        const double2 v = src[i];
+        cc[i][0] = v.x;
+        cc[i][1] = v.y;
+      }
     }
     row_prefix(cc, t, s_carry);
   }
 
-  real* plane = reinterpret_cast<real*>(g.out) +
-                 ((size_t)grp * g.planes + kind) * g.plane_stride * kOct;
-  const real zero[kOct] = {};
+  double2* plane = reinterpret_cast<double2*>(g.out) +
+                   ((size_t)pr * g.planes + kind) * g.plane_stride;
+  const double2 zero = make_double2(0.0, 0.0);
   if (band == 0) {
     if (live)
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) store_rec_f(plane + (size_t)(xb + 1 + i) * kOct, zero);
-    if (tid == 0) store_rec_f(plane, zero);
+      for (int i = 0; i < CPT; ++i) plane[xb + 1 + i] = zero;
+    if (tid == 0) plane[0] = zero;
   }
   uint16_t vn[CPT];
 #pragma unroll
   for (int i = 0; i < CPT; ++i) vn[i] = kNoBin;
   if (live && y0 < y1) load_bins_d<CPT>(fi + (size_t)y0 * g.fi_pitch, vn);
   for (int y = y0; y < y1; ++y) {
-    real ind[CPT][kOct];
+    real ind[CPT][kDP];
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
       const uint32_t d = (uint32_t)vn[i] - gb;
-#pragma unroll
-      for (int j = 0; j < kOct; ++j) ind[i][j] = d == (uint32_t)j ? 1.0 : 0.0;
+      ind[i][0] = d == 0u ? 1.0 : 0.0;
+      ind[i][1] = d == 1u ? 1.0 : 0.0;
     }
     if (live && y + 1 < y1) load_bins_d<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
-    real r[CPT][kOct];
+    real r[CPT][kDP];
     row_prefix(ind, r, s_row[y & 1]);
 #pragma unroll
     for (int i = 0; i < CPT; ++i)
 #pragma unroll
-      for (int j = 0; j < kOct; ++j) t[i][j] = fma(dec, t[i][j], r[i][j]);
-    real* row = plane + (size_t)(y + 1) * g.pitch * kOct;
+      for (int j = 0; j < kDP; ++j) t[i][j] = fma(dec, t[i][j], r[i][j]);
+    double2* row = plane + (size_t)(y + 1) * g.pitch;
     if (live)
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) store_rec_f(row + (size_t)(xb + 1 + i) * kOct, t[i]);
-    if (tid == 0) store_rec_f(row, zero);
+      for (int i = 0; i < CPT; ++i) row[xb + 1 + i] = make_double2(t[i][0], t[i][1]);
+    if (tid == 0) row[0] = zero;
   }
+}
+
+// Decay-table export: planes [b0, b1) of orientation `kind` -> (W+1)x(H+1) each.
+__global__ void k_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
+                               int kind, int b0, double* out) {
+  const int b = b0 + blockIdx.z, y = blockIdx.y;
+  const size_t base = ((size_t)(b >> 1) * 4 + kind) * ps + (size_t)y * pitch;
+  double* o = out + ((size_t)blockIdx.z * (h + 1) + y) * (w + 1);
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x <= w; x += gridDim.x * blockDim.x)
+    o[x] = tab[(base + x) * kDP + (b & 1)];
 }
 
 }  // namespace
@@ -275,12 +283,13 @@ cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
                                int* launches) {
   *launches = 0;
+  const int pairs = a.groups * (kOct / kDP);
   if (a.nbands > 1) {
-    dim3 grid((unsigned)a.nbands, (unsigned)a.groups, (unsigned)((a.w + 255) / 256));
-    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec);
+    dim3 grid((unsigned)a.nbands, (unsigned)pairs, (unsigned)((a.w + 255) / 256));
+    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t per_band = (size_t)a.groups * a.wa * kOct;
+    const size_t per_band = (size_t)pairs * a.wa * kDP;
     k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
         reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dec, per_band);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -288,10 +297,17 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
   }
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
-  const unsigned grid = (unsigned)(a.nbands * a.groups);
-  if (cpt == 4) k_build_decay<4><<<grid, threads, 0, s>>>(a, dec, kind);
-  else k_build_decay<8><<<grid, threads, 0, s>>>(a, dec, kind);
+  const unsigned grid = (unsigned)(a.nbands * pairs);
+  if (cpt == 4) k_build_decay<4><<<grid, threads, 0, s>>>(a, dec, kind, pairs);
+  else k_build_decay<8><<<grid, threads, 0, s>>>(a, dec, kind, pairs);
   *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
+                                int kind, int b0, int b1, double* out, cudaStream_t s) {
+  dim3 grid((unsigned)((w + 1 + 255) / 256), (unsigned)(h + 1), (unsigned)(b1 - b0));
+  k_export_decay<<<grid, 256, 0, s>>>(tab, ps, pitch, w, h, kind, b0, out);
   return cudaGetLastError();
 }
 

@@ -51,14 +51,9 @@ __device__ __forceinline__ void block_peak_e(double s, long long idx, PeakPart* 
   }
 }
 
-// four consecutive fp64 table values (a lane's half record)
-struct D4 {
-  double x, y, z, w;
-};
-__device__ __forceinline__ D4 ldd4(const char* p) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p + 16));
-  return D4{a.x, a.y, b.x, b.y};
+// one 16-B bin-pair record
+__device__ __forceinline__ double2 ldd2(const char* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
 }
 
 template <int SIM>
@@ -70,32 +65,36 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, 
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
   const int cx = u + a.hx, cy = v + a.hy;
-  const size_t ps8 = a.plane_stride * kOct;
-  // centre record of the window in each orientation's coordinates
+  // centre record of the window in each orientation's coordinates (bytes
+  // within a pair's 4-plane block; 16-B records)
   size_t cen[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const size_t x = (k & 1) ? (size_t)(e.w - 1 - cx) : (size_t)cx;
     const size_t y = (k & 2) ? (size_t)(e.h - 1 - cy) : (size_t)cy;
-    cen[k] = (k * ps8 + (y * a.pitch + x) * kOct + half * 4) * sizeof(double);
+    cen[k] = (k * a.plane_stride + y * a.pitch + x) * 16;
   }
+  const size_t pair_bytes = 4 * a.plane_stride * 16;
 
+  // lane `half` of octet g: bins 8g + 4*half + {0,1} (pair 4g+2h) and
+  // {2,3} (pair 4g+2h+1); a half-warp's 16 windows read 256 contiguous bytes
   auto octet = [&](int g, double (&out)[4]) {
-    const char* base = reinterpret_cast<const char*>(reinterpret_cast<const double*>(a.tab) +
-                                                     (size_t)g * a.planes * ps8);
+    const char* b0 = reinterpret_cast<const char*>(a.tab) + (size_t)(4 * g + 2 * half) * pair_bytes;
+    const char* b1 = b0 + pair_bytes;
 #pragma unroll
     for (int k = 0; k < 4; ++k) out[k] = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // orientation / quadrant
-      const char* w = base + cen[k];
-      const D4 c0 = ldd4(w + e.off[4 * k]), c1 = ldd4(w + e.off[4 * k + 1]);
-      const D4 c2 = ldd4(w + e.off[4 * k + 2]), c3 = ldd4(w + e.off[4 * k + 3]);
       const double k0 = e.coef[4 * k], k1 = e.coef[4 * k + 1], k2 = e.coef[4 * k + 2],
                    k3 = e.coef[4 * k + 3];
-      out[0] += k0 * c0.x + k1 * c1.x + k2 * c2.x + k3 * c3.x;
-      out[1] += k0 * c0.y + k1 * c1.y + k2 * c2.y + k3 * c3.y;
-      out[2] += k0 * c0.z + k1 * c1.z + k2 * c2.z + k3 * c3.z;
-      out[3] += k0 * c0.w + k1 * c1.w + k2 * c2.w + k3 * c3.w;
+      const size_t o0 = cen[k] + e.off[4 * k], o1 = cen[k] + e.off[4 * k + 1];
+      const size_t o2 = cen[k] + e.off[4 * k + 2], o3 = cen[k] + e.off[4 * k + 3];
+      const double2 p0 = ldd2(b0 + o0), p1 = ldd2(b0 + o1), p2 = ldd2(b0 + o2), p3 = ldd2(b0 + o3);
+      const double2 q0 = ldd2(b1 + o0), q1 = ldd2(b1 + o1), q2 = ldd2(b1 + o2), q3 = ldd2(b1 + o3);
+      out[0] += k0 * p0.x + k1 * p1.x + k2 * p2.x + k3 * p3.x;
+      out[1] += k0 * p0.y + k1 * p1.y + k2 * p2.y + k3 * p3.y;
+      out[2] += k0 * q0.x + k1 * q1.x + k2 * q2.x + k3 * q3.x;
+      out[3] += k0 * q0.y + k1 * q1.y + k2 * q2.y + k3 * q3.y;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) out[k] = out[k] > e.snap ? out[k] : 0.0;  // rounding floor
@@ -163,62 +162,95 @@ __global__ void k_select_cand(const double* scores, size_t n, int row0, int mw,
 }
 
 // Phase 2b: exact fp64 brute-force re-score of the candidates (weights_into
-// + score_weights order), written back into the map; one window per thread.
-// When more than `cap` windows qualified, the same threads stride over the
-// whole map and re-score every qualifying cell instead (slow but exact).
-__global__ void k_rescore(const SweepArgs a, const RescoreArgs r, const swg_peak* fast) {
-  const uint16_t* fi = r.fi;
-  const size_t fi_pitch = r.fi_pitch;
-  const double* grid = r.grid;
-  const int kw = r.kw, kh = r.kh, mw = a.mw, row0 = a.row0, rows = a.rows, bins = a.bins;
-  const double* model = a.model;
-  double* hist = r.hist;
-  double* scores = a.scores;
-  const int cap = r.cap;
-  const long long* cand = r.cand;
-  const double eps = r.eps;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+// + score_weights order, baselines.cpp:53-69, matching.cpp:37-52), written
+// back into the map.  One WARP per candidate: every lane walks the window's
+// pixels in row-major order and lane j accumulates the bins b = j (mod 32)
+// in registers -- each bin's sum keeps the reference's pixel order, with no
+// memory dependency between consecutive pixels.  Lane 0 then forms the mass
+// and the score in bin order.  When more than `cap` windows qualified, the
+// warps stride over the whole map and re-score every qualifying cell.
+template <int SLOTS>
+__global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const RescoreArgs r,
+                                                 const swg_peak* fast) {
+  __shared__ double s_h[4][SLOTS * 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * 4 + wib, nw = gridDim.x * 4;
   const int cnt = *r.count;
-  const bool overflow = cnt > cap;
-  const double lim = fast->score - eps;
-  const long long total = overflow ? (long long)rows * mw : cnt;
+  const bool overflow = cnt > r.cap;
+  const double lim = fast->score - r.eps;
+  const long long total = overflow ? (long long)a.rows * a.mw : cnt;
   double best = -2.0;
   long long bidx = 0x7FFFFFFFFFFFFFFFLL;
-  double* h = hist + (size_t)tid * bins;
-  for (long long c = tid; c < total; c += nthr) {
+  double* h = s_h[wib];
+  for (long long c = gw; c < total; c += nw) {
     long long idx;
     if (overflow) {
-      if (!(scores[c] >= lim)) continue;
-      idx = (long long)row0 * mw + c;
+      if (!(a.scores[c] >= lim)) continue;  // warp-uniform
+      idx = (long long)a.row0 * a.mw + c;
     } else {
-      idx = cand[c];
+      idx = r.cand[c];
     }
-    const int u = (int)(idx % mw), v = (int)(idx / mw);
-    for (int b = 0; b < bins; ++b) h[b] = 0.0;
-    for (int dy = 0; dy < kh; ++dy) {
-      const uint16_t* row = fi + (size_t)(v + dy) * fi_pitch + u;
-      for (int dx = 0; dx < kw; ++dx) {
-        const int b = row[dx];
-        if (b < bins) h[b] = __dadd_rn(h[b], grid[dy * kw + dx]);
+    const int u = (int)(idx % a.mw), v = (int)(idx / a.mw);
+    double acc[SLOTS];
+#pragma unroll
+    for (int k = 0; k < SLOTS; ++k) acc[k] = 0.0;
+    // branch-free: a pixel adds its weight to the owner lane's slot and an
+    // exact 0.0 everywhere else (x + 0.0 == x), so each bin's sum is the
+    // reference's sequence; loads are batched 8 pixels ahead of the adds
+    auto add_px = [&](int b, double w) {
+      const double we = ((b & 31) == lane && b < a.bins) ? w : 0.0;
+      const int slot = b >> 5;
+#pragma unroll
+      for (int k = 0; k < SLOTS; ++k) acc[k] = __dadd_rn(acc[k], slot == k ? we : 0.0);
+    };
+    // pixels stream through the warp 32 at a time: lane l loads pixel
+    // (dx0 + l) of the row (coalesced, next batch prefetched), then the
+    // batch is broadcast pixel by pixel in row-major order
+    const int per_row = (r.kw + 31) >> 5, nb = r.kh * per_row;
+    auto load = [&](int i, int& bl, double& wl) {
+      const int dy = i / per_row, dx = (i - dy * per_row) * 32 + lane;
+      bl = 0xFFFF;
+      wl = 0.0;
+      if (i < nb && dx < r.kw) {
+        bl = __ldg(r.fi + (size_t)(v + dy) * r.fi_pitch + u + dx);
+        wl = __ldg(r.grid + (size_t)dy * r.kw + dx);
+      }
+    };
+    int bn;
+    double wn;
+    load(0, bn, wn);
+    for (int i = 0; i < nb; ++i) {
+      const int bc = bn;
+      const double wc = wn;
+      load(i + 1, bn, wn);
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) add_px(__shfl_sync(0xFFFFFFFFu, bc, l),
+                                          __shfl_sync(0xFFFFFFFFu, wc, l));
+    }
+#pragma unroll
+    for (int k = 0; k < SLOTS; ++k) h[k * 32 + lane] = acc[k];
+    __syncwarp();
+    if (lane == 0) {
+      double mass = 0.0, sc = 0.0;
+      for (int b = 0; b < a.bins; ++b) mass = __dadd_rn(mass, h[b]);
+      if (a.sim == SWG_SIM_BHATTACHARYYA) {
+        for (int b = 0; b < a.bins; ++b)
+          sc = __dadd_rn(sc, __dsqrt_rn(__dmul_rn(a.model[b], h[b])));
+        sc = mass > 0.0 ? __ddiv_rn(sc, __dsqrt_rn(mass)) : 0.0;
+      } else if (mass > 0.0) {
+        for (int b = 0; b < a.bins; ++b) {
+          const double q = __ddiv_rn(h[b], mass);
+          sc = __dadd_rn(sc, (q < a.model[b]) ? q : a.model[b]);
+        }
+      }
+      sc = clamp01e(sc);
+      a.scores[(size_t)(v - a.row0) * a.mw + u] = sc;
+      if (better_e(sc, idx, best, bidx)) {
+        best = sc;
+        bidx = idx;
       }
     }
-    double mass = 0.0, acc = 0.0;
-    for (int b = 0; b < bins; ++b) mass = __dadd_rn(mass, h[b]);
-    if (a.sim == SWG_SIM_BHATTACHARYYA) {
-      for (int b = 0; b < bins; ++b) acc = __dadd_rn(acc, __dsqrt_rn(__dmul_rn(model[b], h[b])));
-      acc = mass > 0.0 ? __ddiv_rn(acc, __dsqrt_rn(mass)) : 0.0;
-    } else if (mass > 0.0) {
-      for (int b = 0; b < bins; ++b) {
-        const double q = __ddiv_rn(h[b], mass);
-        acc = __dadd_rn(acc, (q < model[b]) ? q : model[b]);
-      }
-    }
-    const double s = clamp01e(acc);
-    scores[(size_t)(v - row0) * mw + u] = s;
-    if (better_e(s, idx, best, bidx)) {
-      best = s;
-      bidx = idx;
-    }
+    __syncwarp();
   }
   block_peak_e(best, bidx, r.parts + blockIdx.x);
 }
@@ -239,8 +271,14 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
       a.scores, n, a.row0, a.mw, peak, r.eps, r.cap, r.count, r.cand);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int blocks = (r.cap + 127) / 128;
-  k_rescore<<<blocks, 128, 0, s>>>(a, r, peak);
+  const int blocks = (r.cap + 3) / 4;  // one warp per candidate
+  const int slots = (a.bins + 31) / 32;
+  if (slots <= 1) k_rescore<1><<<blocks, 128, 0, s>>>(a, r, peak);
+  else if (slots <= 2) k_rescore<2><<<blocks, 128, 0, s>>>(a, r, peak);
+  else if (slots <= 4) k_rescore<4><<<blocks, 128, 0, s>>>(a, r, peak);
+  else if (slots <= 8) k_rescore<8><<<blocks, 128, 0, s>>>(a, r, peak);
+  else if (slots <= 16) k_rescore<16><<<blocks, 128, 0, s>>>(a, r, peak);
+  else k_rescore<32><<<blocks, 128, 0, s>>>(a, r, peak);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return launch_peak_reduce(r.parts, blocks, a.mw, a.hx, a.hy, peak, s);
 }

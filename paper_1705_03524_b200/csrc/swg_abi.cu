@@ -770,7 +770,7 @@ swg_status swg_tables_device_layout(const swg_tables* t, const void** base, size
   if (base) *base = t->tdec ? (const void*)t->tdec : (const void*)t->t32;
   if (ps) *ps = t->ps;
   if (pitch) *pitch = t->pitch;
-  if (bins_per_record) *bins_per_record = kOct;
+  if (bins_per_record) *bins_per_record = t->tdec ? kDP : kOct;
   return SWG_OK;
 }
 
@@ -835,7 +835,21 @@ swg_status swg_tables_export_f64(swg_tables* t, int kind, int b0, int b1, double
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
-  return export_planes<double, double>(t, t->tdec, kind, b0, b1, out);
+  swg_ctx* c = t->ctx;
+  const size_t per_bin = (size_t)(t->w + 1) * (t->h + 1);
+  const int chunk = (int)std::max<size_t>(1, (256u << 20) / (per_bin * 8));
+  ST_TRY(c->qout.ensure((size_t)std::min(chunk, b1 - b0) * per_bin * 8));
+  for (int b = b0; b < b1; b += chunk) {
+    const int e = std::min(b1, b + chunk);
+    double* dev = static_cast<double*>(c->qout.p);
+    CUDA_TRY(launch_export_decay(t->tdec, t->ps, t->pitch, t->w, t->h, kind, b, e, dev,
+                                 c->stream));
+    c->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(out + (size_t)(b - b0) * per_bin, dev, (size_t)(e - b) * per_bin * 8,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return SWG_OK;
 }
 
 swg_status swg_tables_feature_image(swg_tables* t, uint16_t* out) {
@@ -1271,7 +1285,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       std::memset(a.model, 0, sizeof(a.model));
       std::memcpy(a.model, r.model, sizeof(double) * t->bins);
       if (engine[i] == kExp64) {
-        // quadrant rectangles in their orientation's SE table (k_exp.cu);
+        // quadrant rectangles in their orientation's SE table (k_exp.cu, bin-pair
+        // records);
         // coefficients in powers of the table's decay
         static thread_local ExpSweep es;
         const double dd = t->decay;
@@ -1288,15 +1303,32 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
           const double cf[4] = {qf[o], -qf[o] * pw(ax[o]), -qf[o] * pw(by[o]),
                                 qf[o] * pw(ax[o] + by[o])};
           for (int q = 0; q < 4; ++q) {
-            es.off[4 * o + q] = (int)(8 * (ys[q] * p + xs[q]) * kOct);
+            es.off[4 * o + q] = (int)(16 * (ys[q] * p + xs[q]));  // 16-B pair records
             es.coef[4 * o + q] = cf[q];
           }
         }
         es.w = t->w;
         es.h = t->h;
-        // fp64 rounding floor of an empty bin: table values are bounded by
-        // 1/(1-d)^2, the rectangle formula's error by ~1e-16 of that
-        es.snap = 1e-13 / ((1.0 - dd) * (1.0 - dd));
+        // Error budget of the fast path:
+        // table values <= T = 1/(1-d)^2; the damped recurrences keep each
+        // entry within ~T u / (1-d) of exact (u = 2^-53), so one assembled
+        // bin is within dh = 8 * 16 * T * u / (1-d) (16 corners, slack 8).
+        // Bins below snap = 2 dh are rounding noise of an empty bin; every
+        // real bin value is >= h_min = d^(hx+hy) (the smallest weight).
+        const double u = std::ldexp(1.0, -53);
+        const double T = 1.0 / ((1.0 - dd) * (1.0 - dd));
+        const double dh = 8.0 * 16.0 * T * u / (1.0 - dd);
+        const double hmin = pw(hx + hy);
+        es.snap = 2.0 * dh;
+        double err;
+        if (es.snap >= 0.5 * hmin) {
+          err = 1.0;  // no separation of noise and data: re-score everything
+        } else if (r.sim == SWG_SIM_BHATTACHARYYA) {
+          // |d sum sqrt(m h)| <= sqrt(bins) dh / (2 sqrt(h_min)); mass term <= bins dh / 2
+          err = std::sqrt((double)t->bins) * dh / (2.0 * std::sqrt(hmin)) + t->bins * dh;
+        } else {
+          err = 2.0 * t->bins * dh;
+        }
         CUDA_TRY(launch_sweep_exp(a, es, grid[i], c->stream));
         c->launches += 2;
         CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
@@ -1309,16 +1341,24 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ra.kw = k.kw;
         ra.kh = k.kh;
         ra.cap = 4096;
-        ra.eps = 1e-4;
-        const size_t hb = (size_t)ra.cap * t->bins * 8, cb = (size_t)ra.cap * 8;
-        const size_t pb = (size_t)((ra.cap + 127) / 128) * sizeof(PeakPart);
+        // a window outside [fast max - eps] cannot be the exact maximum when
+        // eps >= 2 err (+ the fp64 rounding of the scores themselves)
+        ra.eps = std::min(4.0, 2.0 * err + 1e-12);
+        const size_t hb = 0, cb = (size_t)ra.cap * 8;
+        const size_t pb = (size_t)((ra.cap + 3) / 4) * sizeof(PeakPart);
         ST_TRY(c->resc.ensure(hb + cb + pb + 256));
         char* rb = static_cast<char*>(c->resc.p);
-        ra.hist = reinterpret_cast<double*>(rb);
         ra.cand = reinterpret_cast<long long*>(rb + hb);
         ra.parts = reinterpret_cast<PeakPart*>(rb + hb + cb);
         ra.count = reinterpret_cast<int*>(rb + hb + cb + pb);
         CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, c->stream));
+        if (std::getenv("SWG_DEBUG_RESCORE")) {  // diagnostics: candidate count
+          int cnt = 0;
+          cudaMemcpyAsync(&cnt, ra.count, 4, cudaMemcpyDeviceToHost, c->stream);
+          cudaStreamSynchronize(c->stream);
+          std::fprintf(stderr, "swg rescore: kernel %dx%d eps %.3g candidates %d\n", k.kw, k.kh,
+                       ra.eps, cnt);
+        }
         c->launches += 3;
       } else if (engine[i] == kQuad64) {
         a.mass = (double)quad_mass(k);

@@ -27,7 +27,8 @@ namespace swg {
 
 constexpr int kMaxBins = SWG_MAX_BINS;
 constexpr int kMaxRings = SWG_MAX_RINGS;
-constexpr int kOct = 8;              // bins per record
+constexpr int kOct = 8;              // bins per record (integral tables)
+constexpr int kDP = 2;               // bins per record (fp64 decay tables: bin pairs)
 constexpr uint16_t kNoBin = 0xFFFF;  // feature-image padding sentinel
 constexpr int kMaxWidth = 4096;      // build CTA spans a full row (CPT <= 8)
 
@@ -138,7 +139,6 @@ struct RescoreArgs {
   int* count;          // device candidate counter
   long long* cand;     // candidates (absolute map index)
   int cap;
-  double* hist;        // cap x bins scratch
   PeakPart* parts;     // one per rescore CTA
   double eps;
 };
@@ -183,6 +183,8 @@ cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s);
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
                                int* launches);
+cudaError_t launch_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
+                                int kind, int b0, int b1, double* out, cudaStream_t s);
 cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s);
 cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak* peak,
                               cudaStream_t s);
