@@ -546,3 +546,71 @@ def test_exponential_swih_flat_image(ctx, oracle):
     got, pk = t.likelihood_map(K(swg.EXP_L1, 9, 9, 0.9375), mdl, swg.SWIH)
     np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
     assert pk == oracle.peak(want, 4, 4)
+
+
+def test_likelihood_batch_matches_per_frame(ctx, oracle):
+    """swg_likelihood_batch over search-region crops (pointer + full-frame
+    pitch) == one build + map per frame == the oracle's brute force."""
+    from paper_1705_03524_b200 import api, synth
+    seq = synth.config3(5, n_frames=4, h=200, w=320, search=96)
+    F, H, W = seq.frames.shape[:3]
+    S = seq.search
+    scales = [K(swg.EUCLID_QUAD, 21, 27), K(swg.EUCLID_QUAD, 25, 31)]
+    cx, cy = seq.track[0]
+    models = [api.target_model(ctx, synth.crop(seq.frames[0], cx, cy, k.kw, k.kh), k,
+                               fmt=swg.FMT_RGB8, bins=4) for k in scales]
+    reqs = [swg.MapRequest(k, m) for k, m in zip(scales, models)]
+    crops = []
+    for f in range(F):
+        x0, y0 = synth.search_origin(seq, f)
+        crops.append(seq.frames[f, y0:y0 + S, x0:x0 + S])
+    t = ctx.build(np.ascontiguousarray(crops[0]), swg.FMT_RGB8, 4, swg.PLANES_QUADRATIC)
+    got = t.likelihood_batch(crops, reqs, pitch=W * 3)
+    for f in range(F):
+        fi = oracle.quantize_rgb8(np.ascontiguousarray(crops[f]), 4)
+        t1 = ctx.build(np.ascontiguousarray(crops[f]), swg.FMT_RGB8, 4, swg.PLANES_QUADRATIC)
+        _, pk1 = t1.likelihood_maps(reqs, scores="none")
+        for i, k in enumerate(scales):
+            ok = O.kernel(O.EUCLID_QUAD, k.kw, k.kh)
+            want = oracle.likelihood_map(fi, 64, models[i], ok, O.BRUTE)
+            assert got[f][i] == pk1[i] == oracle.peak(want, k.hx, k.hy), (f, i)
+    # device crops with the same pitch
+    import torch
+    fd = torch.from_numpy(seq.frames).cuda()
+    dev = [fd[f, y0:y0 + S, x0:x0 + S] for f, (x0, y0) in
+           ((f, synth.search_origin(seq, f)) for f in range(F))]
+    assert t.likelihood_batch(dev, reqs, pitch=W * 3) == got
+
+
+def test_decay_row_bands_match_full_frame(ctx, oracle):
+    """Row bands (config 4 on N GPUs): decay tables built on a band's pixel
+    rows give the full frame's map rows (the band's carry cancels in the
+    rectangle formula) within 1e-9, and the band peaks combine (max score,
+    then smallest global index) to the full frame's exact peak."""
+    import bench
+    img = oracle.random_gray(97, 150, 8)
+    bins, d = 6, 0.9375
+    fi = oracle.quantize_gray8(img, bins)
+    scales = [(K(swg.EXP_L1, 9, 9, d), swg.SWIH, 1, None), (K(swg.EXP_L1, 15, 13, d), swg.SWIH, 1, None)]
+    full = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+    BH, plan = bench.band_plan(150, scales, 3)
+    for si, (k, _, _, _) in enumerate(scales):
+        ok = O.kernel(O.EXP_L1, k.kw, k.kh, d)
+        mdl = oracle.target_model(fi[40:40 + k.kh, 30:30 + k.kw].copy(), bins, ok, O.BRUTE)
+        want = oracle.likelihood_map(fi, bins, mdl, ok, O.BRUTE)
+        fmap, fpk = full.likelihood_map(k, mdl, swg.SWIH)
+        mw = fmap.shape[1]
+        best = None
+        for p0, rows in plan:
+            v0, v1 = rows[si]
+            if v1 <= v0:
+                continue
+            tb = ctx.build_decay(np.ascontiguousarray(img[p0:p0 + BH]), d, swg.FMT_GRAY8, bins)
+            bmap, bpk = tb.likelihood_map(k, mdl, swg.SWIH, rows=(v0 - p0, v1 - p0))
+            np.testing.assert_allclose(bmap, fmap[v0:v1], rtol=0, atol=1e-9)
+            gidx = (bpk[1] + p0) * mw + bpk[0]
+            if best is None or bpk[4] > best[0] or (bpk[4] == best[0] and gidx < best[1]):
+                best = (bpk[4], gidx)
+        pk = oracle.peak(want, k.hx, k.hy)
+        assert fpk == pk
+        assert best == (pk[4], pk[1] * mw + pk[0])
