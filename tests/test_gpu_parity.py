@@ -614,3 +614,117 @@ def test_decay_row_bands_match_full_frame(ctx, oracle):
         pk = oracle.peak(want, k.hx, k.hy)
         assert fpk == pk
         assert best == (pk[4], pk[1] * mw + pk[0])
+
+
+# ---------------------------------------------------------------- full-size spot checks
+def _region_check(oracle, fi, bins, model, k, method, rings, got_map, regions, tol):
+    """Map values of window regions of a full-size GPU map against the
+    oracle on the pixel crop holding exactly those windows (window
+    histograms do not depend on the crop: test_row_band_crop_identity)."""
+    ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+    for (u0, v0, nu, nv) in regions:
+        crop = np.ascontiguousarray(fi[v0:v0 + nv + k.kh - 1, u0:u0 + nu + k.kw - 1])
+        want = oracle.likelihood_map(crop, bins, model, ok, method, rings=rings)
+        sub = got_map[v0:v0 + nv, u0:u0 + nu]
+        if tol == 0:
+            assert (sub == want).all(), (k.kind, k.kw, u0, v0)
+        else:
+            np.testing.assert_allclose(sub, want, rtol=0, atol=tol)
+
+
+def _peak_check(oracle, fi, bins, model, k, method, rings, pk, got_map):
+    """The reported peak is the map's first maximum and its score is the
+    oracle's score of that window."""
+    assert pk[4] == got_map.max()
+    assert (pk[0], pk[1]) == tuple(np.unravel_index(np.argmax(got_map), got_map.shape)[::-1])
+    u, v = pk[0], pk[1]
+    crop = np.ascontiguousarray(fi[v:v + k.kh, u:u + k.kw])
+    ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+    assert oracle.likelihood_map(crop, bins, model, ok, method, rings=rings)[0, 0] == pk[4]
+
+
+def test_config5_full_size_spot_checks(ctx, oracle):
+    """BASELINE config 5 at full size (2048x2048 u16, 64 bins): all four
+    kernels at the smallest, a middle and the largest scale."""
+    from paper_1705_03524_b200 import api, synth
+    sc = synth.config5(1)
+    img, bins = sc.image, 64
+    fi = oracle.quantize_gray16(img, bins)
+    d = 15.0 / 16.0
+    tabs = {swg.PLANES_AFFINE: ctx.build(img, swg.FMT_GRAY16, bins, swg.PLANES_AFFINE),
+            swg.PLANES_PLAIN: ctx.build(img, swg.FMT_GRAY16, bins, swg.PLANES_PLAIN),
+            swg.PLANES_QUADRATIC: ctx.build(img, swg.FMT_GRAY16, bins, swg.PLANES_QUADRATIC),
+            swg.PLANES_DECAY: ctx.build_decay(img, d, swg.FMT_GRAY16, bins)}
+    rng = np.random.default_rng(5)
+    for kw in (17, 117, 257):
+        cases = [(K(swg.MANHATTAN, kw, kw), swg.SWIH, 1, swg.PLANES_AFFINE, O.SWIH, 0),
+                 (K(swg.GAUSS_CHEB, kw, kw, 0.5), swg.CAKE, kw // 2 + 1, swg.PLANES_PLAIN,
+                  O.CAKE, 0),
+                 (K(swg.EUCLID_QUAD, kw, kw), swg.SWIH, 1, swg.PLANES_QUADRATIC, O.BRUTE, 0),
+                 (K(swg.EXP_L1, kw, kw, d), swg.SWIH, 1, swg.PLANES_DECAY, O.BRUTE, 1e-4)]
+        mw = mh = 2048 - kw + 1
+        regions = [(int(rng.integers(0, mw - 8)), int(rng.integers(0, mh - 4)), 8, 4),
+                   (0, 0, 6, 3), (mw - 6, mh - 3, 6, 3)]
+        for k, method, rings, planes, omethod, tol in cases:
+            templ = synth.crop(img, 700, 1300, kw, kw)
+            model = api.target_model(ctx, templ, k, fmt=swg.FMT_GRAY16, bins=bins,
+                                     method=method, rings=rings)
+            got, pk = tabs[planes].likelihood_map(k, model, method, rings=rings)
+            _region_check(oracle, fi, bins, model, k, omethod, rings, got, regions, tol)
+            _peak_check(oracle, fi, bins, model, k, omethod, rings, pk, got)
+
+
+def test_config4_band_full_size_spot_checks(ctx, oracle):
+    """BASELINE config 4 at full width (3840 RGB, 512 bins, exponential):
+    the first row band's decay tables, every scale."""
+    import bench
+    from paper_1705_03524_b200 import api, synth
+    sc = synth.config4(1)
+    img = sc.image
+    fi = oracle.quantize_rgb8(img, 8)
+    d = 15.0 / 16.0
+    wl = bench.workload("c4")
+    scales = wl["groups"][0]["scales"]
+    BH, plan = bench.band_plan(img.shape[0], scales, 4)
+    p0, rows = plan[0]
+    band = np.ascontiguousarray(img[p0:p0 + BH])
+    t = ctx.build_decay(band, d, swg.FMT_RGB8, 8)
+    bfi = fi[p0:p0 + BH]
+    rng = np.random.default_rng(4)
+    for si, (k, method, rings, _) in enumerate(scales):
+        v0, v1 = rows[si]
+        cx, cy = sc.targets[si][:2]
+        model = api.target_model(ctx, synth.crop(img, cx, cy, k.kw, k.kh), k, fmt=swg.FMT_RGB8,
+                                 bins=8)
+        got, pk = t.likelihood_map(k, model, swg.SWIH, rows=(v0 - p0, v1 - p0))
+        mw = got.shape[1]
+        regions = [(int(rng.integers(0, mw - 4)), int(rng.integers(0, v1 - v0 - 2)), 4, 2),
+                   (mw - 3, v1 - v0 - 2, 3, 2)]
+        _region_check(oracle, bfi, 512, model, k, O.BRUTE, 1, got, regions, 1e-4)
+        _peak_check(oracle, bfi, 512, model, k, O.BRUTE, 1, pk, got)
+
+
+def test_config3_full_size_frames(ctx, oracle):
+    """BASELINE config 3 frames at full size: search-region maps of all
+    three Euclidean scales == the oracle's brute force, bit for bit."""
+    from paper_1705_03524_b200 import api, synth
+    seq = synth.config3(1, n_frames=3)
+    W = seq.frames.shape[2]
+    S = seq.search
+    scales = [K(swg.EUCLID_QUAD, kw, kh) for kw, kh in ((45, 59), (49, 65), (53, 71))]
+    cx, cy = seq.track[0]
+    models = [api.target_model(ctx, synth.crop(seq.frames[0], cx, cy, k.kw, k.kh), k,
+                               fmt=swg.FMT_RGB8, bins=4) for k in scales]
+    for f in (1, 2):
+        x0, y0 = synth.search_origin(seq, f)
+        crop = np.ascontiguousarray(seq.frames[f, y0:y0 + S, x0:x0 + S])
+        t = ctx.build(crop, swg.FMT_RGB8, 4, swg.PLANES_QUADRATIC)
+        fi = oracle.quantize_rgb8(crop, 4)
+        maps, pks = t.likelihood_maps([swg.MapRequest(k, m) for k, m in zip(scales, models)])
+        for k, m, got, pk in zip(scales, models, maps, pks):
+            want = oracle.likelihood_map(fi, 64, m, O.kernel(O.EUCLID_QUAD, k.kw, k.kh), O.BRUTE)
+            assert (got == want).all()
+            assert pk == oracle.peak(want, k.hx, k.hy)
+            # the planted target is found within 2 px at the middle scale
+        gx, gy = seq.track[f]
+        assert abs(pks[1][2] + x0 - gx) <= 2 and abs(pks[1][3] + y0 - gy) <= 2
