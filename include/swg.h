@@ -127,6 +127,20 @@ typedef struct swg_map_request {
   int row_begin;
   int row_end;
   const double* model;
+  /* Bin-range chains (SURVEY 8e "bin ranges"; NULL = off).  Tables built
+   * for bins [b0, b1) of B (swg_tables_build_bins) add their bins to a
+   * window's running Bhattacharyya sum and mass in bin order, so a chain of
+   * ranges 0 -> G-1 reproduces the single-table operation sequence bit for
+   * bit.  Device arrays of (row_end-row_begin) x map_width {s, mass} pairs:
+   *   partial_in   running sums over bins [0, b0) (NULL: start at zero);
+   *   partial_out  when non-NULL, receives the sums over [0, b1) and the
+   *                request produces no scores and no peak;
+   * the last range (partial_in set, partial_out NULL) finishes the scores,
+   * the map and the peak.  `model` is always the full B-bin model.
+   * Bhattacharyya on every table sweep; intersection on swih Manhattan /
+   * Uniform / Euclidean (closed-form window mass). */
+  const void* partial_in;
+  void* partial_out;
 } swg_map_request;
 
 /* One quadrant term of a window query (QuadrantTerm, engine.hpp:27-32). */
@@ -179,6 +193,17 @@ swg_status swg_tables_build_decay(swg_ctx* ctx, const void* pixels, int is_devic
                                   size_t pitch_bytes, int width, int height, int format,
                                   int bins, double decay, size_t memory_budget,
                                   swg_tables** out);
+/* Tables for the bin range [bin_begin, bin_end) of the quantiser's bins
+ * (bin-range sharding: one range per GPU, partial sums chained through
+ * swg_map_request.partial_in / partial_out).  planes as swg_tables_build,
+ * or SWG_PLANES_DECAY with `decay`; bin_begin = bin_end = 0: every bin.
+ * Window queries and exports address local bins 0 .. bin_end-bin_begin-1. */
+swg_status swg_tables_build_bins(swg_ctx* ctx, const void* pixels, int is_device,
+                                 size_t pitch_bytes, int width, int height, int format,
+                                 int bins, int planes, double decay, int bin_begin,
+                                 int bin_end, size_t memory_budget, swg_tables** out);
+swg_status swg_tables_bin_range(const swg_tables* t, int* bin_begin, int* bin_end,
+                                int* total_bins);
 /* Re-run quantise + build for a new frame of the same geometry into the
  * same device buffers (no allocation; stream ordered, asynchronous). */
 swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,

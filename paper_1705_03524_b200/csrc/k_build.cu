@@ -107,13 +107,15 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)grp * kOct;
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp * kOct;
+  const uint32_t lim = (uint32_t)(g.bins - grp * kOct);  // bins of this octet in range
   uint32_t cnt[kOct], ys[kOct], y2[kOct];
 #pragma unroll
   for (int j = 0; j < kOct; ++j) cnt[j] = ys[j] = y2[j] = 0;
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
-    const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+    uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+    d = d < lim ? d : 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < kOct; ++j) {
       const bool hit = d == (uint32_t)j;
@@ -181,7 +183,8 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
   // memory; the last live thread may straddle the edge (padding = kNoBin).
   const bool live = xb < g.w;
   const uint16_t* fi = g.fi + (live ? xb : 0);
-  const uint32_t gb = (uint32_t)grp * kOct;
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp * kOct;
+  const uint32_t lim = (uint32_t)(g.bins - grp * kOct);  // bins of this octet in range
 
   // ---- carry row T(x+1, y0) from the column sums of all rows above y0
   T t[CPT][kOct];
@@ -241,7 +244,10 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
   for (int y = y0; y < y1; ++y) {
     uint32_t d[CPT];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) d[i] = (uint32_t)vn[i] - gb;
+    for (int i = 0; i < CPT; ++i) {
+      d[i] = (uint32_t)vn[i] - gb;
+      d[i] = d[i] < lim ? d[i] : 0xFFFFFFFFu;
+    }
     if (live && y + 1 < y1) load_bins<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
     uint32_t* buf = s_row[y & 1];
     if constexpr (KIND == 3) {

@@ -110,11 +110,13 @@ __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real de
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)pr * kDP;
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr * kDP;
+  const uint32_t lim = (uint32_t)max(g.bins - pr * kDP, 0);  // bins of this pair in range
   real c0 = 0.0, c1 = 0.0;
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
-    const uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+    uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
+    d = d < lim ? d : 0xFFFFFFFFu;
     c0 = fma(dec, c0, d == 0u ? 1.0 : 0.0);
     c1 = fma(dec, c1, d == 1u ? 1.0 : 0.0);
   }
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec
   const int xb = tid * CPT;
   const bool live = xb < g.w;
   const uint16_t* fi = g.fi + (live ? xb : 0);
-  const uint32_t gb = (uint32_t)pr * kDP;
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr * kDP;
+  const uint32_t lim = (uint32_t)max(g.bins - pr * kDP, 0);  // bins of this pair in range
   real dp[CPT + 1];  // d^i
   dp[0] = 1.0;
 #pragma unroll
@@ -242,7 +245,8 @@ __global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec
     real ind[CPT][kDP];
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
-      const uint32_t d = (uint32_t)vn[i] - gb;
+      uint32_t d = (uint32_t)vn[i] - gb;
+      d = d < lim ? d : 0xFFFFFFFFu;
       ind[i][0] = d == 0u ? 1.0 : 0.0;
       ind[i][1] = d == 1u ? 1.0 : 0.0;
     }

@@ -118,6 +118,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, 
   };
 
   double s = 0.0, mass = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) {  // bin-range chain (Bhattacharyya): running sums of earlier bins
+    s = a.pin[widx].x;
+    mass = a.pin[widx].y;
+  }
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
     for (int g = 0; g < a.groups; ++g) {
       double out[4], term[4];
@@ -126,7 +131,6 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, 
       for (int k = 0; k < 4; ++k) term[k] = sqrt(a.model[g * kOct + half * 4 + k] * out[k]);
       add_oct(out, term, mass, s, true, true);
     }
-    s = mass > 0.0 ? s / sqrt(mass) : 0.0;
   } else {
     double unused = 0.0;
     for (int g = 0; g < a.groups; ++g) {
@@ -142,8 +146,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, 
       add_oct(out, term, unused, s, false, true);
     }
   }
-  s = clamp01e(s);
-  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  if (a.pout) {
+    if (active && half == 0) a.pout[widx] = make_double2(s, mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = mass > 0.0 ? s / sqrt(mass) : 0.0;
+    s = clamp01e(s);
+    if (active && half == 0) a.scores[widx] = s;
+  }
   block_peak_e(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
                a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
     // exact 0.0 everywhere else (x + 0.0 == x), so each bin's sum is the
     // reference's sequence; loads are batched 8 pixels ahead of the adds
     auto add_px = [&](int b, double w) {
-      const double we = ((b & 31) == lane && b < a.bins) ? w : 0.0;
+      const double we = ((b & 31) == lane && b < r.bins) ? w : 0.0;
       const int slot = b >> 5;
 #pragma unroll
       for (int k = 0; k < SLOTS; ++k) acc[k] = __dadd_rn(acc[k], slot == k ? we : 0.0);
@@ -232,15 +242,15 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
     __syncwarp();
     if (lane == 0) {
       double mass = 0.0, sc = 0.0;
-      for (int b = 0; b < a.bins; ++b) mass = __dadd_rn(mass, h[b]);
+      for (int b = 0; b < r.bins; ++b) mass = __dadd_rn(mass, h[b]);
       if (a.sim == SWG_SIM_BHATTACHARYYA) {
-        for (int b = 0; b < a.bins; ++b)
-          sc = __dadd_rn(sc, __dsqrt_rn(__dmul_rn(a.model[b], h[b])));
+        for (int b = 0; b < r.bins; ++b)
+          sc = __dadd_rn(sc, __dsqrt_rn(__dmul_rn(r.model[b], h[b])));
         sc = mass > 0.0 ? __ddiv_rn(sc, __dsqrt_rn(mass)) : 0.0;
       } else if (mass > 0.0) {
-        for (int b = 0; b < a.bins; ++b) {
+        for (int b = 0; b < r.bins; ++b) {
           const double q = __ddiv_rn(h[b], mass);
-          sc = __dadd_rn(sc, (q < a.model[b]) ? q : a.model[b]);
+          sc = __dadd_rn(sc, (q < r.model[b]) ? q : r.model[b]);
         }
       }
       sc = clamp01e(sc);
@@ -272,7 +282,7 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (r.cap + 3) / 4;  // one warp per candidate
-  const int slots = (a.bins + 31) / 32;
+  const int slots = (r.bins + 31) / 32;
   if (slots <= 1) k_rescore<1><<<blocks, 128, 0, s>>>(a, r, peak);
   else if (slots <= 2) k_rescore<2><<<blocks, 128, 0, s>>>(a, r, peak);
   else if (slots <= 4) k_rescore<4><<<blocks, 128, 0, s>>>(a, r, peak);

@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
   const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
 
   double s = 0.0, mass_unused = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
   for (int g = 0; g < a.groups; ++g) {
     const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
@@ -181,9 +183,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
     }
     add_octet(val, term, half, mass_unused, s, false);
   }
-  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
-  s = clamp01(s);
-  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  if (a.pout) {  // partial: hand the running sum to the next bin range
+    if (active && half == 0) a.pout[widx] = make_double2(s, a.mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
+    s = clamp01(s);
+    if (active && half == 0) a.scores[widx] = s;
+  }
   block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
@@ -209,6 +216,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a)
   const uint64_t A = 2 * kx * ky, ucx = (uint64_t)cx, ucy = (uint64_t)cy;
 
   double s = 0.0, unused = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
   for (int g = 0; g < a.groups; ++g) {
     const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint64_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
@@ -244,9 +253,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a)
     }
     add_octet(val, term, half, unused, s, false);
   }
-  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
-  s = clamp01(s);
-  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  if (a.pout) {  // partial: hand the running sum to the next bin range
+    if (active && half == 0) a.pout[widx] = make_double2(s, a.mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
+    s = clamp01(s);
+    if (active && half == 0) a.scores[widx] = s;
+  }
   block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
@@ -305,6 +319,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
   };
 
   double s = 0.0, mass = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) {  // bin-range chain (Bhattacharyya): running sums of earlier bins
+    s = a.pin[widx].x;
+    mass = a.pin[widx].y;
+  }
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
     for (int g = 0; g < a.groups; ++g) {
       double out[4], term[4];
@@ -316,7 +335,6 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
                       : 0.0;
       add_octet(out, term, half, mass, s, true);
     }
-    s = __ddiv_rn(s, __dsqrt_rn(mass));
   } else {
     double unused = 0.0;
     for (int g = 0; g < a.groups; ++g) {
@@ -336,8 +354,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
       add_octet(out, term, half, unused, s, false);
     }
   }
-  s = clamp01(s);
-  if (active && half == 0) a.scores[(size_t)r * a.mw + u] = s;
+  if (a.pout) {
+    if (active && half == 0) a.pout[widx] = make_double2(s, mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(mass));
+    s = clamp01(s);
+    if (active && half == 0) a.scores[widx] = s;
+  }
   block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
@@ -387,6 +411,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
   };
 
   double s = 0.0, mass = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) {  // bin-range chain (Bhattacharyya): running sums of earlier bins
+    s = a.pin[widx].x;
+    mass = a.pin[widx].y;
+  }
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
     for (int g = 0; g < a.groups; ++g) {
       double out[kOct];
@@ -397,7 +426,6 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
         if (out[j] != 0.0) s = __dadd_rn(s, __dsqrt_rn(__dmul_rn(a.model[g * kOct + j], out[j])));
       }
     }
-    s = __ddiv_rn(s, __dsqrt_rn(mass));
   } else {
     for (int g = 0; g < a.groups; ++g) {
       double out[kOct];
@@ -416,8 +444,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
         }
     }
   }
-  s = clamp01(s);
-  if (active) a.scores[(size_t)r * a.mw + u] = s;
+  if (a.pout) {
+    if (active) a.pout[widx] = make_double2(s, mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(mass));
+    s = clamp01(s);
+    if (active) a.scores[widx] = s;
+  }
   block_peak(active ? s : -2.0, (long long)v * a.mw + u,
              a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }

@@ -205,6 +205,7 @@ struct swg_ctx {
 struct swg_tables {
   swg_ctx* ctx = nullptr;
   int w = 0, h = 0, bins = 0, planes = 0, format = 0, levels = 0;
+  int bin0 = 0, total_bins = 0;  // planes hold bins [bin0, bin0 + bins) of total_bins
   bool has_fi = false;
   uint16_t* fi = nullptr;
   size_t fip = 0;
@@ -277,6 +278,7 @@ swg_status run_build(swg_tables* t, T* out) {
   a.wa = t->wa;
   a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : 16;
   a.agg = t->lb;
+  a.bin0 = t->bin0;
   if (t->nbands > 1) {
     CUDA_TRY(launch_colsum(a, c->stream));
     c->launches += 2;
@@ -307,7 +309,7 @@ swg_status upload_and_quantize(swg_tables* t, const void* pixels, int is_device,
     src_pitch = t->in_pitch;
   }
   QuantArgs q{src, src_pitch, t->w, t->h, t->format,
-              t->format == SWG_FMT_RGB8 ? t->levels : t->bins, t->fi, t->fip};
+              t->format == SWG_FMT_RGB8 ? t->levels : t->total_bins, t->fi, t->fip};
   CUDA_TRY(launch_quantize(q, c->stream));
   c->launches += 1;
   t->has_fi = true;
@@ -403,6 +405,7 @@ swg_status run_build_decay(swg_tables* t) {
   a.wa = t->wa;
   a.aw = 16;
   a.agg = t->lb;
+  a.bin0 = t->bin0;
   const uint16_t* src[4] = {t->fi, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz};
   for (int k = 0; k < 4; ++k) {
     a.fi = src[k];
@@ -522,17 +525,19 @@ swg_status swg_ctx_launch_count(swg_ctx* c, uint64_t* n) {
   return SWG_OK;
 }
 
-swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
-                            size_t pitch_bytes, int width, int height,
-                            int format, int bins, int planes,
-                            size_t memory_budget, swg_tables** out) {
+static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
+                               size_t pitch_bytes, int width, int height, int format,
+                               int bins, int planes, double decay, int bin_begin, int bin_end,
+                               size_t memory_budget, swg_tables** out) {
   if (!c || !pixels || !out) return fail(SWG_ERR_ARG, "NULL argument");
   *out = nullptr;
   if (width < 1 || height < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
   if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
   if (planes != SWG_PLANES_PLAIN && planes != SWG_PLANES_AFFINE &&
-      planes != SWG_PLANES_QUADRATIC)
+      planes != SWG_PLANES_QUADRATIC && planes != SWG_PLANES_DECAY)
     return fail(SWG_ERR_ARG, "planes %d", planes);
+  if (planes == SWG_PLANES_DECAY && !(decay > 0.0 && decay < 1.0))
+    return fail(SWG_ERR_INVALID_KERNEL, "decay must be in (0, 1)");
   if (planes == SWG_PLANES_QUADRATIC && height > 2340)  // column y^2-sums stay < 2^32
     return fail(SWG_ERR_SIZE, "quadratic planes: height %d > 2340", height);
   int nb = bins;
@@ -543,6 +548,9 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   if (nb < 1) return fail(SWG_ERR, "bin count must be >= 1");
   if (nb > 65535) return fail(SWG_ERR, "bin count must be <= 65535");
   if (width > kMaxWidth) return fail(SWG_ERR_SIZE, "width %d > %d", width, kMaxWidth);
+  if (bin_begin == 0 && bin_end == 0) bin_end = nb;
+  if (bin_begin < 0 || bin_end > nb || bin_begin >= bin_end)
+    return fail(SWG_ERR_OUT_OF_RANGE, "bin range [%d, %d) of %d", bin_begin, bin_end, nb);
 
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
@@ -551,116 +559,97 @@ swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
   c->refs++;
   t->w = width;
   t->h = height;
-  t->bins = nb;
+  t->total_bins = nb;
+  t->bin0 = bin_begin;
+  t->bins = bin_end - bin_begin;
   t->levels = bins;
   t->planes = planes;
   t->format = format;
+  t->decay = planes == SWG_PLANES_DECAY ? decay : 0.0;
   t->fip = fi_pitch(width);
-  t->groups = (nb + kOct - 1) / kOct;
+  t->groups = (t->bins + kOct - 1) / kOct;
   t->pitch = record_pitch(width);
   t->ps = t->pitch * (size_t)(height + 1);
   choose_bands(t);
   // plain-only tables keep narrow uint16 planes (32-bit ones are built on
-  // demand); affine tables keep uint32 planes
-  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_QUADRATIC ? 8 : 4;
+  // demand); affine tables keep uint32 planes; quadratic uint64; decay fp64
+  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_AFFINE ? 4 : 8;
   const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * elem;
-  const size_t lb_bytes =
-      (size_t)t->nbands * t->groups * t->wa * (planes == SWG_PLANES_QUADRATIC ? 24 : 16) * 4;
-  const size_t need = tab_bytes + lb_bytes + t->fip * height * 2;
+  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct *
+                          (planes == SWG_PLANES_QUADRATIC ? 12 : 8);
+  const size_t fb = t->fip * height * 2;
+  const size_t need = tab_bytes + lb_bytes + fb * (planes == SWG_PLANES_DECAY ? 4 : 1);
   if (memory_budget && need > memory_budget) {
     swg_tables_destroy(t);
     g_required = need;
-    return fail(SWG_ERR_CAPACITY, "integral tables need %zu bytes, budget is %zu", need,
-                memory_budget);
+    return fail(SWG_ERR_CAPACITY, "%s tables need %zu bytes, budget is %zu",
+                planes == SWG_PLANES_DECAY ? "decay" : "integral", need, memory_budget);
   }
-  auto cleanup = [&](swg_status st) {
-    swg_tables_destroy(t);
-    return st;
-  };
   cudaError_t e;
-  if ((e = elem == 2   ? cudaMalloc(&t->t16, tab_bytes)
-           : elem == 8 ? cudaMalloc(&t->t64, tab_bytes)
-                       : cudaMalloc(&t->t32, tab_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&t->fi, t->fip * height * 2)) != cudaSuccess ||
-      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
+  void** tab = elem == 2                           ? reinterpret_cast<void**>(&t->t16)
+               : elem == 4                         ? reinterpret_cast<void**>(&t->t32)
+               : planes == SWG_PLANES_QUADRATIC    ? reinterpret_cast<void**>(&t->t64)
+                                                   : reinterpret_cast<void**>(&t->tdec);
+  if ((e = cudaMalloc(tab, tab_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&t->fi, fb)) != cudaSuccess ||
+      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
+      (planes == SWG_PLANES_DECAY && (e = cudaMalloc(&t->fflip, 3 * fb)) != cudaSuccess)) {
     g_required = need;
     cudaGetLastError();
-    return cleanup(fail(SWG_ERR_CAPACITY, "integral tables need %zu device bytes: %s", need,
-                        cudaGetErrorString(e)));
+    swg_tables_destroy(t);
+    return fail(SWG_ERR_CAPACITY, "tables need %zu device bytes: %s", need,
+                cudaGetErrorString(e));
   }
   t->bytes = need;
   swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
   if (st == SWG_OK)
-    st = t->t16   ? run_build<uint16_t>(t, t->t16)
+    st = t->tdec  ? run_build_decay(t)
+         : t->t16 ? run_build<uint16_t>(t, t->t16)
          : t->t64 ? run_build<uint64_t>(t, t->t64)
                   : run_build<uint32_t>(t, t->t32);
-  if (st != SWG_OK) return cleanup(st);
+  if (st != SWG_OK) {
+    swg_tables_destroy(t);
+    return st;
+  }
   *out = t;
   return SWG_OK;
+}
+
+swg_status swg_tables_build(swg_ctx* c, const void* pixels, int is_device,
+                            size_t pitch_bytes, int width, int height,
+                            int format, int bins, int planes,
+                            size_t memory_budget, swg_tables** out) {
+  if (planes == SWG_PLANES_DECAY) return fail(SWG_ERR_ARG, "decay tables: swg_tables_build_decay");
+  return build_common(c, pixels, is_device, pitch_bytes, width, height, format, bins, planes,
+                      0.0, 0, 0, memory_budget, out);
 }
 
 swg_status swg_tables_build_decay(swg_ctx* c, const void* pixels, int is_device,
                                   size_t pitch_bytes, int width, int height, int format,
                                   int bins, double decay, size_t memory_budget,
                                   swg_tables** out) {
-  if (!c || !pixels || !out) return fail(SWG_ERR_ARG, "NULL argument");
-  *out = nullptr;
-  if (!(decay > 0.0 && decay < 1.0)) return fail(SWG_ERR_INVALID_KERNEL, "decay must be in (0, 1)");
-  if (width < 1 || height < 1) return fail(SWG_ERR, "image dimensions must be >= 1");
-  if (format < SWG_FMT_GRAY8 || format > SWG_FMT_BINS16) return fail(SWG_ERR_ARG, "format %d", format);
-  int nb = bins;
-  if (format == SWG_FMT_RGB8) {
-    if (bins < 1 || bins > 40) return fail(SWG_ERR, "RGB levels must be in [1, 40]");
-    nb = bins * bins * bins;
+  if (!(decay > 0.0 && decay < 1.0)) {
+    if (out) *out = nullptr;
+    return fail(SWG_ERR_INVALID_KERNEL, "decay must be in (0, 1)");
   }
-  if (nb < 1 || nb > 65535) return fail(SWG_ERR, "bin count must be in [1, 65535]");
-  if (width > kMaxWidth) return fail(SWG_ERR_SIZE, "width %d > %d", width, kMaxWidth);
-  std::lock_guard<std::mutex> lk(c->mu);
-  DeviceGuard g(c->device);
-  swg_tables* t = new swg_tables;
-  t->ctx = c;
-  c->refs++;
-  t->w = width;
-  t->h = height;
-  t->bins = nb;
-  t->levels = bins;
-  t->planes = SWG_PLANES_DECAY;
-  t->format = format;
-  t->decay = decay;
-  t->fip = fi_pitch(width);
-  t->groups = (nb + kOct - 1) / kOct;
-  t->pitch = record_pitch(width);
-  t->ps = t->pitch * (size_t)(height + 1);
-  choose_bands(t);
-  const size_t tab_bytes = t->ps * 4 * (size_t)t->groups * kOct * 8;
-  const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct * 8;
-  const size_t fb = t->fip * height * 2;
-  const size_t need = tab_bytes + lb_bytes + 4 * fb;
-  if (memory_budget && need > memory_budget) {
-    swg_tables_destroy(t);
-    g_required = need;
-    return fail(SWG_ERR_CAPACITY, "decay tables need %zu bytes, budget is %zu", need,
-                memory_budget);
-  }
-  cudaError_t e;
-  if ((e = cudaMalloc(&t->tdec, tab_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&t->fi, fb)) != cudaSuccess ||
-      (e = cudaMalloc(&t->fflip, 3 * fb)) != cudaSuccess ||
-      (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess) {
-    g_required = need;
-    cudaGetLastError();
-    swg_tables_destroy(t);
-    return fail(SWG_ERR_CAPACITY, "decay tables need %zu device bytes: %s", need,
-                cudaGetErrorString(e));
-  }
-  t->bytes = need;
-  swg_status st = upload_and_quantize(t, pixels, is_device, pitch_bytes);
-  if (st == SWG_OK) st = run_build_decay(t);
-  if (st != SWG_OK) {
-    swg_tables_destroy(t);
-    return st;
-  }
-  *out = t;
+  return build_common(c, pixels, is_device, pitch_bytes, width, height, format, bins,
+                      SWG_PLANES_DECAY, decay, 0, 0, memory_budget, out);
+}
+
+swg_status swg_tables_build_bins(swg_ctx* c, const void* pixels, int is_device,
+                                 size_t pitch_bytes, int width, int height, int format,
+                                 int bins, int planes, double decay, int bin_begin,
+                                 int bin_end, size_t memory_budget, swg_tables** out) {
+  return build_common(c, pixels, is_device, pitch_bytes, width, height, format, bins, planes,
+                      decay, bin_begin, bin_end, memory_budget, out);
+}
+
+swg_status swg_tables_bin_range(const swg_tables* t, int* bin_begin, int* bin_end,
+                                int* total_bins) {
+  ST_TRY(check_tables(t));
+  if (bin_begin) *bin_begin = t->bin0;
+  if (bin_end) *bin_end = t->bin0 + t->bins;
+  if (total_bins) *total_bins = t->total_bins;
   return SWG_OK;
 }
 
@@ -694,6 +683,7 @@ swg_status swg_tables_upload_i64(swg_ctx* c, int w, int h, int bins,
   t->w = w;
   t->h = h;
   t->bins = bins;
+  t->total_bins = bins;
   t->planes = 3;
   t->format = SWG_FMT_BINS16;
   t->groups = (bins + kOct - 1) / kOct;
@@ -1180,6 +1170,17 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
                     r.kernel.kw, r.kernel.kh);
     }
     if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
+    const bool ranged = t->bins != t->total_bins;
+    if (ranged && !r.partial_in && !r.partial_out)
+      return fail(SWG_ERR_CONFIG,
+                  "bin-range tables [%d, %d) of %d compute partial sums: give partial_out "
+                  "(or partial_in on the last range)", t->bin0, t->bin0 + t->bins, t->total_bins);
+    if ((r.partial_in || r.partial_out) && r.method == SWG_METHOD_BRUTE)
+      return fail(SWG_ERR_CONFIG, "bin-range chains run on the table sweeps, not brute force");
+    if (r.partial_out && scores_host && scores_host[i])
+      return fail(SWG_ERR_ARG, "a partial (partial_out) request produces no scores");
+    if (expo && r.partial_in && !r.partial_out && t->total_bins > kMaxBins)
+      return fail(SWG_ERR_CONFIG, "exact exponential peak: more than %d bins", kMaxBins);
     const bool needs_ramps = (r.method == SWG_METHOD_SWIH || r.method == SWG_METHOD_BRUTE) &&
                              r.kernel.kind == SWG_KERNEL_MANHATTAN;
     if (needs_ramps && t->planes < 3 && !(r.method == SWG_METHOD_BRUTE && t->has_fi))
@@ -1239,6 +1240,13 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
     else engine[i] = kAffine32;
     kern[i] = k;
+    if (r.partial_in || r.partial_out) {  // engines that can continue a bin-range chain
+      const bool closed_mass = engine[i] == kAffine32 || engine[i] == kQuad64;
+      if (engine[i] == kBrute || (!closed_mass && r.sim != SWG_SIM_BHATTACHARYYA))
+        return fail(SWG_ERR_CONFIG,
+                    "bin-range chains: Bhattacharyya, or intersection on swih Manhattan / "
+                    "Uniform / Euclidean");
+    }
     if (engine[i] == kBrute)
       grid[i] = dim3((unsigned)((mws[i] + kBruteThreads - 1) / kBruteThreads),
                      (unsigned)std::max(rows, 1));
@@ -1283,7 +1291,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       a.scores = dscores;
       a.parts = parts;
       std::memset(a.model, 0, sizeof(a.model));
-      std::memcpy(a.model, r.model, sizeof(double) * t->bins);
+      std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
+      a.pin = static_cast<const double2*>(r.partial_in);
+      a.pout = static_cast<double2*>(r.partial_out);
       if (engine[i] == kExp64) {
         // quadrant rectangles in their orientation's SE table (k_exp.cu, bin-pair
         // records);
@@ -1325,21 +1335,28 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
           err = 1.0;  // no separation of noise and data: re-score everything
         } else if (r.sim == SWG_SIM_BHATTACHARYYA) {
           // |d sum sqrt(m h)| <= sqrt(bins) dh / (2 sqrt(h_min)); mass term <= bins dh / 2
-          err = std::sqrt((double)t->bins) * dh / (2.0 * std::sqrt(hmin)) + t->bins * dh;
+          err = std::sqrt((double)t->total_bins) * dh / (2.0 * std::sqrt(hmin)) +
+                t->total_bins * dh;
         } else {
-          err = 2.0 * t->bins * dh;
+          err = 2.0 * t->total_bins * dh;
         }
         CUDA_TRY(launch_sweep_exp(a, es, grid[i], c->stream));
-        c->launches += 2;
+        c->launches += 1;
+        if (r.partial_out) continue;  // partial sums only: no scores, no peak
+        c->launches += 1;
         CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
                                     dpeaks + i, c->stream));
         // phase 2: exact fp64 brute-force re-score of the near-maximum windows
-        RescoreArgs ra{};
+        static thread_local RescoreArgs ra;  // 8 KB of model: keep off the stack
+        ra = RescoreArgs{};
         ST_TRY(weight_grid(c, k, &ra.grid));
         ra.fi = t->fi;
         ra.fi_pitch = t->fip;
         ra.kw = k.kw;
         ra.kh = k.kh;
+        ra.bins = t->total_bins;  // every bin: the re-score is the whole histogram
+        std::memset(ra.model, 0, sizeof(ra.model));
+        std::memcpy(ra.model, r.model, sizeof(double) * t->total_bins);
         ra.cap = 4096;
         // a window outside [fast max - eps] cannot be the exact maximum when
         // eps >= 2 err (+ the fp64 rounding of the scores themselves)
@@ -1425,7 +1442,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ba.integer = k_integer(k);
         CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, c->stream));
       }
-      if (engine[i] != kExp64) {  // (the exponential branch reduces its own peaks)
+      if (engine[i] != kExp64 && !r.partial_out) {  // (exp reduces its own peaks)
         c->launches += 1;
         CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
                                     dpeaks + i, c->stream));

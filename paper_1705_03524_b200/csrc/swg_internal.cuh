@@ -59,6 +59,7 @@ struct BuildArgs {
   int band_h, nbands;
   size_t wa;           // padded width (columns) of the carry array
   int aw;              // carry words per column: 16, or 24 with quadratic planes
+  int bin0;            // global bin of local bin 0 (bin-range tables)
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
                        // then of all rows above the band (K1b, exclusive scan)
@@ -100,6 +101,10 @@ struct SweepArgs {
   int lat[20];
   double* scores;      // rows x mw, row r = map row row0 + r
   PeakPart* parts;     // one per CTA
+  // bin-range chain (tables holding bins [bin0, bin0 + bins) of a larger
+  // set): running (s, mass) per window in, and out instead of scores
+  const double2* pin;
+  double2* pout;
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
@@ -141,6 +146,8 @@ struct RescoreArgs {
   int cap;
   PeakPart* parts;     // one per rescore CTA
   double eps;
+  int bins;            // all bins of the histogram (bin-range tables: the total)
+  double model[kMaxBins];  // the full model
 };
 
 struct BruteArgs {

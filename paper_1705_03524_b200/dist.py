@@ -17,6 +17,14 @@ data-path collective:
 * peak         — `gather_peak`: all-gather of each rank's (score, global
                  row-major index) and the reference tie rule
                  (matching.cpp:211-223): max score, then smallest index.
+* bin ranges   — `bin_ranges` / `run_bin_chain`: rank g holds the tables of
+                 bins [b_g, b_g+1) only (1/G of the planes: config 4's 512
+                 bins) and continues each window's running Bhattacharyya sum
+                 and mass in bin order: partial sums flow g -> g+1 with
+                 point-to-point send/recv, pipelined by row chunks, and the
+                 last rank finishes scores, map and peak.  Same fp64
+                 operation sequence as one GPU -> bit-identical (an
+                 all-reduce would reorder the sum: SURVEY §8e).
 """
 from __future__ import annotations
 
@@ -125,3 +133,43 @@ def gather_peak(score: float, index: int, map_width: int, hx: int, hy: int,
     s, i = reduce_peaks(cands)
     u, v = i % map_width, i // map_width
     return (u, v, u + hx, v + hy, s)
+
+
+def bin_ranges(bins: int, world: int, align: int = 8) -> List[Tuple[int, int]]:
+    """Contiguous bin ranges, one per rank, split on `align`-bin boundaries
+    (whole table records) as evenly as the octet count allows."""
+    units = -(-bins // align)
+    out, start = [], 0
+    for g in range(world):
+        n = units // world + (1 if g < units % world else 0)
+        b0, b1 = min(start * align, bins), min((start + n) * align, bins)
+        out.append((b0, b1))
+        start += n
+    return out
+
+
+def row_chunks(rows: int, n_chunks: int) -> List[Tuple[int, int]]:
+    step = -(-rows // max(n_chunks, 1))
+    return [(r, min(r + step, rows)) for r in range(0, rows, step)]
+
+
+def run_bin_chain(rank: int, world: int, chunks: Sequence[Tuple[int, int]], compute,
+                  make_buffer, group=None):
+    """Pipelined chain over ranks.  For each row chunk c: receive the running
+    sums from rank-1 (unless first), compute(c, partial_in) -> partial_out
+    (None on the last rank, which finishes the chunk), send to rank+1.
+    `make_buffer(c)` allocates a receive buffer for chunk c.  Returns the
+    last rank's per-chunk results."""
+    import torch.distributed as dist
+    results = []
+    for c in chunks:
+        pin = None
+        if rank > 0:
+            pin = make_buffer(c)
+            dist.recv(pin, src=rank - 1, group=group)
+        out = compute(c, pin)
+        if rank < world - 1:
+            dist.send(out, dst=rank + 1, group=group)
+        else:
+            results.append(out)
+    return results

@@ -104,7 +104,8 @@ class Peak(C.Structure):
 class _Req(C.Structure):
     _fields_ = [("kernel", Kernel), ("method", C.c_int), ("sim", C.c_int), ("rings", C.c_int),
                 ("ring_rule", C.c_int), ("row_begin", C.c_int), ("row_end", C.c_int),
-                ("model", C.POINTER(C.c_double))]
+                ("model", C.POINTER(C.c_double)), ("partial_in", C.c_void_p),
+                ("partial_out", C.c_void_p)]
 
 
 class Term(C.Structure):
@@ -122,6 +123,8 @@ class MapRequest:
     rings: int = 4
     ring_rule: int = RING_MEAN
     rows: Optional[tuple] = None
+    partial_in: object = None   # device (rows, mw, 2) float64 tensor / address
+    partial_out: object = None
 
 
 _lib = None
@@ -150,6 +153,10 @@ def lib():
                              C.c_int, C.c_size_t, C.POINTER(vp)],
         "swg_tables_build_decay": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
                                    C.c_int, C.c_double, C.c_size_t, C.POINTER(vp)],
+        "swg_tables_build_bins": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_size_t,
+                                  C.POINTER(vp)],
+        "swg_tables_bin_range": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "swg_tables_rebuild": [vp, vp, C.c_int, C.c_size_t],
         "swg_tables_upload_i64": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)],
         "swg_tables_destroy": [vp],
@@ -283,6 +290,24 @@ class Context:
                                        None if integer else _ptr(out)))
         return out
 
+    def build_bins(self, pixels, bin_begin, bin_end, fmt=FMT_GRAY8, bins=16,
+                   planes=PLANES_AFFINE, decay=0.0, budget=0, width=None, height=None,
+                   pitch=0) -> "Tables":
+        """Tables for the quantiser's bins [bin_begin, bin_end) (bin-range
+        sharding); maps chain through MapRequest.partial_in / partial_out."""
+        t = Tables.__new__(Tables)
+        t.ctx = self
+        t._h = C.c_void_p()
+        is_dev, ptr, w, h = Tables._src(pixels, fmt, width, height)
+        t._keep = pixels
+        _check(lib().swg_tables_build_bins(self._h, ptr, is_dev, pitch, w, h, fmt, bins, planes,
+                                           float(decay), bin_begin, bin_end, budget,
+                                           C.byref(t._h)))
+        t._info()
+        if planes == PLANES_DECAY:
+            t.decay = float(decay)
+        return t
+
     def upload_i64(self, plain, xramp, yramp) -> "Tables":
         plain, xramp, yramp = (np.ascontiguousarray(a, np.int64) for a in (plain, xramp, yramp))
         b, h1, w1 = plain.shape
@@ -326,6 +351,9 @@ class Tables:
                                      C.byref(nbytes)))
         self.width, self.height, self.bins, self.planes = w.value, h.value, b.value, p.value
         self.device_bytes = nbytes.value
+        b0, b1, tot = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().swg_tables_bin_range(self._h, C.byref(b0), C.byref(b1), C.byref(tot)))
+        self.bin_begin, self.bin_end, self.total_bins = b0.value, b1.value, tot.value
 
     def close(self):
         if getattr(self, "_h", None):
@@ -407,16 +435,7 @@ class Tables:
         "none" skips them (peaks only); device outputs may be given as torch
         tensors (then the call is asynchronous).  Returns (maps, peaks)."""
         n = len(reqs)
-        creqs = (_Req * n)()
-        models = []
-        for i, r in enumerate(reqs):
-            m = np.ascontiguousarray(r.model, np.float64)
-            if m.shape != (self.bins,):
-                raise ModelError(f"likelihood map: model must be normalized with {self.bins} bins")
-            models.append(m)
-            r0, r1 = r.rows if r.rows else (0, 0)
-            creqs[i] = _Req(r.kernel, r.method, r.sim, r.rings, r.ring_rule, r0, r1,
-                            m.ctypes.data_as(C.POINTER(C.c_double)))
+        creqs, _keep = self._creqs(reqs, self.total_bins)
         maps = [None] * n
         host_ptrs = None
         if any(min(self.map_shape(r.kernel, r.rows)) <= 0 for r in reqs):
@@ -424,8 +443,9 @@ class Tables:
         if scores == "host":
             host_ptrs = (C.c_void_p * n)()
             for i, r in enumerate(reqs):
-                maps[i] = np.empty(self.map_shape(r.kernel, r.rows), np.float64)
-                host_ptrs[i] = maps[i].ctypes.data
+                if r.partial_out is None:
+                    maps[i] = np.empty(self.map_shape(r.kernel, r.rows), np.float64)
+                    host_ptrs[i] = maps[i].ctypes.data
         dev_ptrs = None
         if scores_dev is not None:
             dev_ptrs = (C.c_void_p * n)(*[_ptr(x) for x in scores_dev])
@@ -436,7 +456,10 @@ class Tables:
             C.addressof(dev_ptrs) if dev_ptrs is not None else None,
             C.addressof(peaks) if peaks is not None else None,
             _ptr(peaks_dev) if peaks_dev is not None else None))
-        return maps, ([p.astuple() for p in peaks] if peaks is not None else None)
+        if peaks is None:
+            return maps, None
+        return maps, [None if r.partial_out is not None else p.astuple()
+                      for p, r in zip(peaks, reqs)]
 
     @staticmethod
     def _creqs(reqs, bins):
@@ -449,7 +472,9 @@ class Tables:
             models.append(m)
             r0, r1 = r.rows if r.rows else (0, 0)
             creqs[i] = _Req(r.kernel, r.method, r.sim, r.rings, r.ring_rule, r0, r1,
-                            m.ctypes.data_as(C.POINTER(C.c_double)))
+                            m.ctypes.data_as(C.POINTER(C.c_double)),
+                            _ptr(r.partial_in) if r.partial_in is not None else None,
+                            _ptr(r.partial_out) if r.partial_out is not None else None)
         return creqs, models
 
     def likelihood_batch(self, frames, reqs: Sequence[MapRequest], pitch=0, is_device=None,
@@ -467,7 +492,7 @@ class Tables:
                     is_device = 0 if isinstance(f, np.ndarray) else int(f.is_cuda)
         nf, n = len(frames), len(reqs)
         fr = (C.c_void_p * max(nf, 1))(*addrs)
-        creqs, _keep = self._creqs(reqs, self.bins)
+        creqs, _keep = self._creqs(reqs, self.total_bins)
         peaks = (Peak * (nf * n))() if peaks_dev is None else None
         _check(lib().swg_likelihood_batch(
             self._h, nf, C.addressof(fr), int(is_device or 0), pitch, n, C.addressof(creqs),

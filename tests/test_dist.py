@@ -86,3 +86,79 @@ def test_band_geometry_covers_the_map():
             assert bd.pixel_rows[1] - bd.pixel_rows[0] == (bd.map_rows[1] - bd.map_rows[0]) + \
                 (kh - 1 if bd.map_rows[1] > bd.map_rows[0] else 0)
     assert D.frame_shards(64, 8, 3) == list(range(3, 64, 8))
+
+
+def _chain_worker(rank, world, port, q):
+    """Bin-range chain (config 4 on N GPUs): rank g owns bins [b_g, b_g+1),
+    continues each window's running Bhattacharyya sum and mass in bin order
+    and passes them on; the oracle's window histograms stand in for the
+    rank's table sweep.  The last rank's map must equal the single-table
+    map bit for bit."""
+    import math
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        orc = O.Oracle()
+        img = orc.random_gray(40, 31, 6)
+        bins = 20
+        fi = orc.quantize_gray8(img, bins)
+        k = O.kernel(O.MANHATTAN, 7, 5)
+        model = orc.target_model(np.ascontiguousarray(fi[10:15, 12:19]), bins, k)
+        mw, mh = 40 - 7 + 1, 31 - 5 + 1
+        raw = np.array([[orc.brute_counts(fi, bins, u + 3, v + 2, k) for u in range(mw)]
+                        for v in range(mh)])
+        b0, b1 = D.bin_ranges(bins, world)[rank]
+
+        def compute(chunk, pin):
+            r0, r1 = chunk
+            out = torch.zeros(r1 - r0, mw, 2, dtype=torch.float64)
+            for v in range(r0, r1):
+                for u in range(mw):
+                    s, mass = (0.0, 0.0) if pin is None else (float(pin[v - r0, u, 0]),
+                                                              float(pin[v - r0, u, 1]))
+                    for b in range(b0, b1):  # score_counts order (matching.cpp:20-35)
+                        mass += float(raw[v, u, b])
+                        s += math.sqrt(model[b] * float(raw[v, u, b]))
+                    out[v - r0, u, 0], out[v - r0, u, 1] = s, mass
+            if rank < world - 1:
+                return out
+            sc = out[..., 0] / torch.sqrt(out[..., 1])
+            return sc.clamp(0.0, 1.0)
+
+        chunks = D.row_chunks(mh, 4)
+        res = D.run_bin_chain(rank, world, chunks, compute,
+                              lambda c: torch.zeros(c[1] - c[0], mw, 2, dtype=torch.float64))
+        ok = True
+        if rank == world - 1:
+            got = torch.cat(res).numpy()
+            want = orc.likelihood_map(fi, bins, model, k)
+            ok = bool((got == want).all())
+        q.put((rank, (b0, b1), ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bin_range_chain_three_ranks():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert [r[1] for r in res] == [(0, 8), (8, 16), (16, 20)]
+    assert all(r[2] for r in res)
+
+
+def test_bin_range_geometry():
+    assert D.bin_ranges(512, 8) == [(64 * g, 64 * g + 64) for g in range(8)]
+    assert D.bin_ranges(20, 2) == [(0, 16), (16, 20)]
+    assert D.bin_ranges(8, 3) == [(0, 8), (8, 8), (8, 8)]
+    assert D.row_chunks(10, 3) == [(0, 4), (4, 8), (8, 10)]

@@ -728,3 +728,86 @@ def test_config3_full_size_frames(ctx, oracle):
             # the planted target is found within 2 px at the middle scale
         gx, gy = seq.track[f]
         assert abs(pks[1][2] + x0 - gx) <= 2 and abs(pks[1][3] + y0 - gy) <= 2
+
+
+# ---------------------------------------------------------------- bin-range chains
+def _chain_maps(ctx, img, bins, planes, ranges, req_kw, decay=0.0, rows=None):
+    """Run a bin-range chain on one GPU (the ranks in sequence): returns the
+    last range's (map, peak)."""
+    import torch
+    pin = None
+    for g, (b0, b1) in enumerate(ranges):
+        t = ctx.build_bins(img, b0, b1, swg.FMT_GRAY8, bins, planes, decay=decay)
+        assert (t.bin_begin, t.bin_end, t.total_bins) == (b0, b1, bins)
+        shape = t.map_shape(req_kw["kernel"], rows)
+        last = g == len(ranges) - 1
+        # fully written by the sweep; torch.empty issues no work on torch's
+        # stream that could race the library's own stream
+        pout = None if last else torch.empty(shape + (2,), dtype=torch.float64, device="cuda")
+        r = swg.MapRequest(rows=rows, partial_in=pin, partial_out=pout, **req_kw)
+        maps, pks = t.likelihood_maps([r], scores="host" if last else "none")
+        if last:
+            return maps[0], pks[0]
+        assert pks[0] is None
+        pin = pout
+
+
+@pytest.mark.parametrize("ranges", [[(0, 8), (8, 16), (16, 20)], [(0, 3), (3, 11), (11, 20)],
+                                    [(0, 20)]])
+def test_bin_range_chain_bit_exact(ctx, oracle, ranges):
+    """Config 4's bin-range sharding: tables holding only bins [b0, b1)
+    continue each window's running sums; the chain's last map and peak are
+    bit-identical to the single-table ones, for every table sweep."""
+    img = oracle.random_gray(96, 70, 13)
+    bins = 20
+    fi = oracle.quantize_gray8(img, bins)
+    d = 0.9375
+    cases = [(K(swg.MANHATTAN, 9, 7), swg.SWIH, 1, swg.PLANES_AFFINE, swg.BHATTACHARYYA),
+             (K(swg.MANHATTAN, 9, 7), swg.SWIH, 1, swg.PLANES_AFFINE, swg.INTERSECTION),
+             (K(swg.GAUSS_CHEB, 11, 11, 0.5), swg.CAKE, 6, swg.PLANES_PLAIN, swg.BHATTACHARYYA),
+             (K(swg.UNIFORM, 13, 9), swg.SWIH, 1, swg.PLANES_PLAIN, swg.BHATTACHARYYA),
+             (K(swg.EUCLID_QUAD, 15, 11), swg.SWIH, 1, swg.PLANES_QUADRATIC, swg.INTERSECTION),
+             (K(swg.EUCLID_QUAD, 15, 11), swg.SWIH, 1, swg.PLANES_QUADRATIC, swg.BHATTACHARYYA),
+             (K(swg.EXP_L1, 13, 13, d), swg.SWIH, 1, swg.PLANES_DECAY, swg.BHATTACHARYYA)]
+    for k, method, rings, planes, sim in cases:
+        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+        om = O.CAKE if method == swg.CAKE else (O.BRUTE if k.kind in (swg.EUCLID_QUAD, swg.EXP_L1)
+                                                else O.SWIH)
+        model = oracle.target_model(fi[20:20 + k.kh, 30:30 + k.kw].copy(), bins, ok, om, rings)
+        if planes == swg.PLANES_DECAY:
+            full = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+        else:
+            full = ctx.build(img, swg.FMT_GRAY8, bins, planes)
+        req = dict(kernel=k, model=model, method=method, sim=sim, rings=rings)
+        want, wpk = full.likelihood_map(k, model, method, sim, rings=rings)
+        got, gpk = _chain_maps(ctx, img, bins, planes, ranges, req, decay=d)
+        assert (got == want).all(), (k.kind, sim, ranges)
+        assert gpk == wpk
+        # and the chain over a row range (vs the single table over the same
+        # rows: the exponential peak re-score depends on the rows searched)
+        want_r, wpk_r = full.likelihood_map(k, model, method, sim, rings=rings, rows=(5, 17))
+        got_r, gpk_r = _chain_maps(ctx, img, bins, planes, ranges, req, decay=d, rows=(5, 17))
+        assert (got_r == want_r).all() and gpk_r == wpk_r, ("rows", k.kind, sim, ranges)
+        if k.kind != swg.EXP_L1:
+            assert (want_r == want[5:17]).all()
+
+
+def test_bin_range_errors(ctx, oracle):
+    import torch
+    img = oracle.random_gray(40, 30, 2)
+    bins = 16
+    t = ctx.build_bins(img, 0, 8, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    m = np.full(bins, 1.0 / bins)
+    k = K(swg.GAUSS_CHEB, 9, 9, 0.5)
+    with pytest.raises(swg.ConfigError):  # a range without a chain
+        t.likelihood_map(k, m, swg.CAKE, rings=5)
+    buf = torch.zeros(t.map_shape(k) + (2,), dtype=torch.float64, device="cuda")
+    with pytest.raises(swg.ConfigError):  # intersection needs the full mass first
+        t.likelihood_maps([swg.MapRequest(k, m, swg.CAKE, swg.INTERSECTION, 5, partial_out=buf)],
+                          scores="none")
+    with pytest.raises(swg.ConfigError):  # brute force does not chain
+        t.likelihood_maps([swg.MapRequest(k, m, swg.BRUTE, partial_out=buf)], scores="none")
+    with pytest.raises(swg.OutOfRangeError):
+        ctx.build_bins(img, 8, 20, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    with pytest.raises(swg.OutOfRangeError):
+        ctx.build_bins(img, 5, 5, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
