@@ -123,6 +123,8 @@ def engine_of(group, k, method):
         return "k_sweep_quad", 5, 8
     if method == swg.CAKE or k.kind == swg.UNIFORM:
         small = k.kw * k.kh < 65536
+        if method == swg.CAKE and not small:  # full-ring plan: ring 1 box + ring 0 frame
+            small = (k.kw - 2) * (k.kh - 2) < 65536 and k.kw * k.kh - (k.kw - 2) * (k.kh - 2) < 65536
         if group["planes"] == swg.PLANES_PLAIN and small:
             return "k_sweep_cake16", 1, 2
         return "k_sweep_cake", 1, 4

@@ -59,8 +59,10 @@ __device__ __forceinline__ double2 ldd2(const char* p) {
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, const ExpSweep e) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
-  const int r0 = blockIdx.y * kSweepTileY + warp;
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  const int u0 = tx * kSweepTileX + (lane >> 1);
+  const int r0 = ty * kSweepTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;

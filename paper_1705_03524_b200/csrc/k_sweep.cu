@@ -122,8 +122,10 @@ __device__ __forceinline__ void add_octet(const double (&val)[4], const double (
 template <int SIM, bool UNIFORM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
-  const int r0 = blockIdx.y * kSweepTileY + warp;
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  const int u0 = tx * kSweepTileX + (lane >> 1);
+  const int r0 = ty * kSweepTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -204,8 +206,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
-  const int r0 = blockIdx.y * kSweepTileY + warp;
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  const int u0 = tx * kSweepTileX + (lane >> 1);
+  const int r0 = ty * kSweepTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -270,8 +274,10 @@ template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
                                                               const CakeSweep rg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  const int u0 = blockIdx.x * kSweepTileX + (lane >> 1);
-  const int r0 = blockIdx.y * kSweepTileY + warp;
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  const int u0 = tx * kSweepTileX + (lane >> 1);
+  const int r0 = ty * kSweepTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -389,7 +395,34 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
                                                   (size_t)g * a.planes * ps8 + centre);
 #pragma unroll
     for (int k = 0; k < kOct; ++k) out[k] = 0.0;
-    for (int i = 0; i < a.rings; ++i) {
+    int i0 = 0;
+    if (a.wide0) {
+      // ring 0's box may hold >= 2^16 pixels; ring 1's box and ring 0's frame
+      // hold fewer (host-checked), so c0 = c1 + ((c0 - c1) mod 2^16) exactly
+      auto box16 = [&](int i) {
+        const int4 o = rg.off[i];
+        const uint4 br = ldqb(w + o.w), bl = ldqb(w + o.z), tr = ldqb(w + o.y), tl = ldqb(w + o.x);
+        return make_uint4(__vsub2(__vadd2(br.x, tl.x), __vadd2(bl.x, tr.x)),
+                          __vsub2(__vadd2(br.y, tl.y), __vadd2(bl.y, tr.y)),
+                          __vsub2(__vadd2(br.z, tl.z), __vadd2(bl.z, tr.z)),
+                          __vsub2(__vadd2(br.w, tl.w), __vadd2(bl.w, tr.w)));
+      };
+      const uint4 k0 = box16(0), k1 = box16(1);
+      const uint32_t d[4] = {__vsub2(k0.x, k1.x), __vsub2(k0.y, k1.y), __vsub2(k0.z, k1.z),
+                             __vsub2(k0.w, k1.w)};
+      const uint32_t c1[4] = {k1.x, k1.y, k1.z, k1.w};
+      if (((d[0] | d[1] | d[2] | d[3]) | (k1.x | k1.y | k1.z | k1.w)) == 0u) return;
+      const double c = rg.coeff[0];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t lo = (c1[q] & 0xFFFFu) + (d[q] & 0xFFFFu);
+        const uint32_t hi = (c1[q] >> 16) + (d[q] >> 16);
+        out[2 * q] = __dadd_rn(out[2 * q], __dmul_rn(c, u2d(lo)));
+        out[2 * q + 1] = __dadd_rn(out[2 * q + 1], __dmul_rn(c, __uint2double_rn(hi)));
+      }
+      i0 = 1;
+    }
+    for (int i = i0; i < a.rings; ++i) {
       const int4 o = rg.off[i];
       const uint4 br = ldqb(w + o.w), bl = ldqb(w + o.z), tr = ldqb(w + o.y), tl = ldqb(w + o.x);
       // (br + tl) - (bl + tr) on packed 16-bit pairs

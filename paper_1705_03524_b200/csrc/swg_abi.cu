@@ -226,6 +226,10 @@ struct swg_tables {
   size_t bytes = 0;
 };
 
+#ifndef SWG_L2_BUDGET_MB
+#define SWG_L2_BUDGET_MB 64  // share of the 126 MB L2 a sweep's corner rows may use
+#endif
+
 namespace {
 
 struct DeviceGuard {
@@ -414,6 +418,16 @@ swg_status run_build_decay(swg_tables* t) {
     c->launches += (uint64_t)nl;
   }
   return SWG_OK;
+}
+
+// A cake whose outer box holds >= 2^16 pixels still runs on 16-bit planes
+// when ring 1's box and ring 0's frame hold fewer (k_sweep_cake16 wide0).
+bool cake16_wide0(const swg_kernel& k, const swg_map_request& r) {
+  static thread_local CakeRings pl;
+  if (r.rings < 2 || cake_plan(k, r.rings, r.ring_rule, pl) != SWG_OK) return false;
+  const long long a0 = (2LL * pl.a[0] + 1) * (2LL * pl.c[0] + 1);
+  const long long a1 = (2LL * pl.a[1] + 1) * (2LL * pl.c[1] + 1);
+  return a1 < 65536 && a0 - a1 < 65536;
 }
 
 swg_status check_tables(const swg_tables* t) {
@@ -1236,7 +1250,10 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
     else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad64;
     else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EXP_L1) engine[i] = kExp64;
-    else if (method == SWG_METHOD_CAKE) engine[i] = (t->t16 && small) ? kCake16 : kCake32;
+    else if (method == SWG_METHOD_CAKE) {
+      engine[i] = (t->t16 && small) ? kCake16 : kCake32;
+      if (engine[i] == kCake32 && t->t16 && cake16_wide0(k, r)) engine[i] = kCake16;
+    }
     else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
     else engine[i] = kAffine32;
     kern[i] = k;
@@ -1294,6 +1311,26 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
       a.pin = static_cast<const double2*>(r.partial_in);
       a.pout = static_cast<double2*>(r.partial_out);
+      {
+        // super-column CTA order for the table sweeps whose corner span
+        // (2hy+2 table rows of the whole width) does not fit in L2: a strip
+        // of sw windows needs (2hy+2+tile) rows x (sw+2hx+2) cells resident
+        size_t cell = 0;
+        if (engine[i] == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
+        else if (engine[i] == kQuad64) cell = (size_t)t->groups * kOct * 5 * 8;
+        else if (engine[i] == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
+        else if (engine[i] == kCake32) cell = (size_t)t->groups * kOct * 4;
+        a.sc_tiles = 0;
+        if (cell) {
+          const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
+          const double span = 2.0 * a.hy + 2 + kSweepTileY;
+          if (span * (t->w + 1) * cell > budget) {
+            const double sw = budget / (span * cell) - (2.0 * a.hx + 2);
+            if (sw >= 2 * kSweepTileX && (sw + 2.0 * a.hx + 2) / sw < 1.7)
+              a.sc_tiles = std::max(1, (int)(sw / kSweepTileX));
+          }
+        }
+      }
       if (engine[i] == kExp64) {
         // quadrant rectangles in their orientation's SE table (k_exp.cu, bin-pair
         // records);
@@ -1426,6 +1463,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
           cs.coeff[q] = rg.coeff[q];
         }
         a.rings = rings;
+        a.wide0 = engine[i] == kCake16 && (long long)k.kw * k.kh >= 65536;
         if (engine[i] == kCake16) CUDA_TRY(launch_sweep_cake16(a, cs, grid[i], c->stream));
         else CUDA_TRY(launch_sweep_cake(a, cs, grid[i], c->stream));
       } else {

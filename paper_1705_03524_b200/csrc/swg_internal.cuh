@@ -105,6 +105,11 @@ struct SweepArgs {
   // set): running (s, mass) per window in, and out instead of scores
   const double2* pin;
   double2* pout;
+  // CTA order: 0 = raster over the map; > 0 = super-columns of this many
+  // tiles, each swept top to bottom, so the table rows between a window's
+  // top and bottom corners stay in L2 (sweep_tile)
+  int sc_tiles;
+  int wide0;           // cake16: ring 0's box count may exceed 16 bits
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
@@ -168,6 +173,27 @@ struct QueryArgs {
   const double* coeff;    // cake: per-term ring coefficient (n x tpw)
   double* outd;           // cake: device n x bins
 };
+
+// Map tile of this CTA.  Super-column order: the linear CTA index walks
+// column strips of `sc_tiles` tiles, each from the top row to the bottom;
+// CTAs are dispatched in linear order, so the CTAs in flight cover a strip
+// of full height and every table row of the strip is read from DRAM once
+// (as a window's bottom corner) and hit in L2 later (as a top corner).
+__device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
+  const int gx = gridDim.x, gy = gridDim.y;
+  if (sc_tiles <= 0 || sc_tiles >= gx) {
+    tx = blockIdx.x;
+    ty = blockIdx.y;
+    return;
+  }
+  const int lin = blockIdx.y * gx + blockIdx.x;
+  const int per_sc = sc_tiles * gy;
+  const int sc = lin / per_sc, x0 = sc * sc_tiles;
+  const int wsc = min(sc_tiles, gx - x0);
+  const int rem = lin - sc * per_sc;
+  ty = rem / wsc;
+  tx = x0 + (rem - ty * wsc);
+}
 
 // Sweep CTA geometry: 8 warps; a warp = 16 windows of one map row, two lanes
 // per window (lane parity = which half of each bin octet).

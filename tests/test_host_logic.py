@@ -78,11 +78,13 @@ def test_workloads_and_engines():
     kinds = [g["scales"][0][0].kind for g in c5["groups"]]
     assert kinds == [swg.MANHATTAN, swg.GAUSS_CHEB, swg.EUCLID_QUAD, swg.EXP_L1]
     assert all(len(g["scales"]) == 8 for g in c5["groups"])
-    # 257x257 Gaussian rings exceed 16-bit box counts -> 32-bit plain planes
+    # 257x257 Gaussian: ring 0's box exceeds 16-bit counts, but ring 1's box
+    # and ring 0's frame do not -> still the 16-bit sweep (wide ring 0)
     plain = c5["groups"][1]
-    assert bench.engine_of(plain, plain["scales"][-1][0], swg.CAKE)[0] == "k_sweep_cake"
-    assert bench.engine_of(plain, plain["scales"][0][0], swg.CAKE)[0] == "k_sweep_cake16"
-    assert bench.group_build_bytes(plain, 10, 10, 4) == 11 * 11 * 4 * 6
+    assert bench.engine_of(plain, plain["scales"][-1][0], swg.CAKE)[0] == "k_sweep_cake16"
+    assert bench.engine_of(plain, swg.Kernel(swg.GAUSS_CHEB, 261, 261, 0.5), swg.CAKE)[0] == \
+        "k_sweep_cake"
+    assert bench.group_build_bytes(plain, 10, 10, 4) == 11 * 11 * 4 * 2
 
 
 def _decayed_se(fi, bins, d):
