@@ -120,7 +120,7 @@ def engine_of(group, k, method):
     if group["planes"] == swg.PLANES_DECAY:
         return "k_sweep_exp", 4, 8
     if group["planes"] == swg.PLANES_QUADRATIC:
-        return "k_sweep_quad", 5, 8
+        return "k_sweep_quad", 5, 4
     if method == swg.CAKE or k.kind == swg.UNIFORM:
         small = k.kw * k.kh < 65536
         if method == swg.CAKE and not small:  # full-ring plan: ring 1 box + ring 0 frame
@@ -139,7 +139,7 @@ def group_build_bytes(group, w, h, nbins):
     if p == swg.PLANES_DECAY:
         return cells * 4 * 8
     if p == swg.PLANES_QUADRATIC:
-        return cells * 5 * 8
+        return cells * 5 * 4
     if p == swg.PLANES_AFFINE:
         return cells * 3 * 4
     b = cells * 2  # narrow 16-bit plain planes
@@ -730,7 +730,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None,
-        "dtype": "u16/u32/u64 tables + f64 scores",
+        "dtype": "u16/u32 integral tables (f64 decay tables) + f64 scores",
         "data": "synthetic (seeded generators in paper_1705_03524_b200/synth.py)",
         "config": {"workload": wl["name"], "bins": nb, "windows_per_step": int(job_win),
                    "table_shape": [tab_w, tab_h], "units_per_rank": len(units),

@@ -75,7 +75,7 @@ typedef enum swg_format {
 typedef enum swg_planes {
   SWG_PLANES_PLAIN = 1,
   SWG_PLANES_AFFINE = 3,
-  SWG_PLANES_QUADRATIC = 5, /* {1, x, y, x^2, y^2}, uint64 (EUCLID_QUAD maps) */
+  SWG_PLANES_QUADRATIC = 5, /* {1, x, y, x^2, y^2}, uint32 (EUCLID_QUAD maps) */
   SWG_PLANES_DECAY = 4      /* SE/SW/NE/NW decayed tables, fp64 (EXP_L1 maps);
                                built by swg_tables_build_decay          */
 } swg_planes;

@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t
 }
 
 // K1c body.  KIND 0 = plain {1}, 1 = xramp {x}, 2 = yramp {y}, and for the
-// quadratic planes 3 = {x^2}, 4 = {y^2} (64-bit tables only).
+// quadratic planes 3 = {x^2}, 4 = {y^2} (32- or 64-bit tables; everything
+// wraps consistently mod 2^32 / 2^64).
 template <typename T, int KIND, int CPT>
 __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp) {
   __shared__ uint32_t s_row[2][kOct * 32];
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(512) k_build_fused(const BuildArgs g) {
     case 1: build_body<T, 1, CPT>(g, band, grp); break;
     case 2: build_body<T, 2, CPT>(g, band, grp); break;
     default:
-      if constexpr (sizeof(T) == 8) {
+      if constexpr (sizeof(T) >= 4) {
         if (blockIdx.y == 3) build_body<T, 3, CPT>(g, band, grp);
         else build_body<T, 4, CPT>(g, band, grp);
       }
@@ -441,7 +442,7 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
       if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
       else if (kind == 1) k_build<T, 1, 4><<<grid, threads, 0, s>>>(a);
       else if (kind == 2) k_build<T, 2, 4><<<grid, threads, 0, s>>>(a);
-      else if constexpr (sizeof(T) == 8) {
+      else if constexpr (sizeof(T) >= 4) {
         if (kind == 3) k_build<T, 3, 4><<<grid, threads, 0, s>>>(a);
         else k_build<T, 4, 4><<<grid, threads, 0, s>>>(a);
       }
@@ -449,7 +450,7 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
       if (kind == 0) k_build<T, 0, 8><<<grid, threads, 0, s>>>(a);
       else if (kind == 1) k_build<T, 1, 8><<<grid, threads, 0, s>>>(a);
       else if (kind == 2) k_build<T, 2, 8><<<grid, threads, 0, s>>>(a);
-      else if constexpr (sizeof(T) == 8) {
+      else if constexpr (sizeof(T) >= 4) {
         if (kind == 3) k_build<T, 3, 8><<<grid, threads, 0, s>>>(a);
         else k_build<T, 4, 8><<<grid, threads, 0, s>>>(a);
       }

@@ -199,10 +199,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 
 // K2q: declared Euclidean extension, w = A - ky*dx^2 - kx*dy^2 with
 // kx = (hx+1)^2, ky = (hy+1)^2, A = 2*kx*ky.  Over the whole window box,
-//   H = A*N - ky*(Sxx - 2cx*Sx + cx^2*N) - kx*(Syy - 2cy*Sy + cy^2*N)
-// from the five planes {1, x, y, x^2, y^2}; exact modulo 2^64, and the true
-// value is < 2^53 (checked on the host), so the double conversion is exact.
-// Tables are uint64: a lane reads 32 bytes (4 bins) per corner.
+//   H = A*N - ky*Dxx - kx*Dyy,  Dxx = Sxx - 2cx*Sx + cx^2*N = sum (x-cx)^2
+// from the five planes {1, x, y, x^2, y^2}.  The tables are uint32: every
+// box sum is exact mod 2^32, and so are Dxx and Dyy computed mod 2^32 --
+// their true values are <= N*hx^2, N*hy^2 < 2^32 (host-checked), hence
+// exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
+// exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
 template <int SIM>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
@@ -217,33 +219,29 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a)
   const size_t centre = ((size_t)cy * a.pitch + (size_t)cx) * kOct + half * 4;
   const size_t ps8 = a.plane_stride * kOct;
   const uint64_t kx = (uint64_t)(a.hx + 1) * (a.hx + 1), ky = (uint64_t)(a.hy + 1) * (a.hy + 1);
-  const uint64_t A = 2 * kx * ky, ucx = (uint64_t)cx, ucy = (uint64_t)cy;
+  const uint64_t A = 2 * kx * ky;
+  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
 
   double s = 0.0, unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;
   if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
   for (int g = 0; g < a.groups; ++g) {
-    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint64_t*>(a.tab) +
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
-    uint64_t box[5][4];
+    uint4 box[5];
 #pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      uint64_t c4[4][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const ulonglong2 lo = __ldg(reinterpret_cast<const ulonglong2*>(w + a.lat[4 * p + q]));
-        const ulonglong2 hi = __ldg(reinterpret_cast<const ulonglong2*>(w + a.lat[4 * p + q] + 16));
-        c4[q][0] = lo.x; c4[q][1] = lo.y; c4[q][2] = hi.x; c4[q][3] = hi.y;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) box[p][k] = c4[3][k] - c4[2][k] - c4[1][k] + c4[0][k];
+    for (int p = 0; p < 5; ++p) {  // lat: corner offsets within a plane (bytes)
+      const char* wp = w + (size_t)p * ps8 * sizeof(uint32_t);
+      box[p] = box4(ldqb(wp + a.lat[4 * p + 3]), ldqb(wp + a.lat[4 * p + 2]),
+                    ldqb(wp + a.lat[4 * p + 1]), ldqb(wp + a.lat[4 * p]));
     }
     double val[4], term[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint64_t n = box[0][k];
-      const uint64_t h = A * n - ky * (box[3][k] - 2 * ucx * box[1][k] + ucx * ucx * n) -
-                         kx * (box[4][k] - 2 * ucy * box[2][k] + ucy * ucy * n);
+      const uint32_t n = comp(box[0], k);
+      const uint32_t dxx = comp(box[3], k) - 2u * ucx * comp(box[1], k) + ucx * ucx * n;
+      const uint32_t dyy = comp(box[4], k) - 2u * ucy * comp(box[2], k) + ucy * ucy * n;
+      const uint64_t h = A * n - ky * dxx - kx * dyy;
       val[k] = (double)h;
       const double model = a.model[g * kOct + half * 4 + k];
       if (h == 0) {

@@ -340,6 +340,8 @@ swg_status ensure_t32(swg_tables* t) {
 swg_status ensure_t64(swg_tables* t) {
   if (t->t64) return SWG_OK;
   if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
+  if (t->planes == SWG_PLANES_QUADRATIC && t->h > 2340)  // 32-bit column y^2 carries
+    return fail(SWG_ERR_SIZE, "exact 64-bit quadratic planes: height %d > 2340", t->h);
   if (!t->has_fi) return fail(SWG_ERR, "tables: no 64-bit planes and no feature image");
   const size_t bytes = t->ps * t->planes * t->groups * kOct * 8;
   cudaError_t e = cudaMalloc(&t->t64, bytes);
@@ -552,8 +554,6 @@ static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
     return fail(SWG_ERR_ARG, "planes %d", planes);
   if (planes == SWG_PLANES_DECAY && !(decay > 0.0 && decay < 1.0))
     return fail(SWG_ERR_INVALID_KERNEL, "decay must be in (0, 1)");
-  if (planes == SWG_PLANES_QUADRATIC && height > 2340)  // column y^2-sums stay < 2^32
-    return fail(SWG_ERR_SIZE, "quadratic planes: height %d > 2340", height);
   int nb = bins;
   if (format == SWG_FMT_RGB8) {
     if (bins < 1 || bins > 40) return fail(SWG_ERR, "RGB levels must be in [1, 40]");
@@ -586,8 +586,8 @@ static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
   t->ps = t->pitch * (size_t)(height + 1);
   choose_bands(t);
   // plain-only tables keep narrow uint16 planes (32-bit ones are built on
-  // demand); affine tables keep uint32 planes; quadratic uint64; decay fp64
-  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_AFFINE ? 4 : 8;
+  // demand); affine and quadratic tables uint32 planes; decay fp64
+  const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_DECAY ? 8 : 4;
   const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * elem;
   const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct *
                           (planes == SWG_PLANES_QUADRATIC ? 12 : 8);
@@ -600,10 +600,9 @@ static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
                 planes == SWG_PLANES_DECAY ? "decay" : "integral", need, memory_budget);
   }
   cudaError_t e;
-  void** tab = elem == 2                           ? reinterpret_cast<void**>(&t->t16)
-               : elem == 4                         ? reinterpret_cast<void**>(&t->t32)
-               : planes == SWG_PLANES_QUADRATIC    ? reinterpret_cast<void**>(&t->t64)
-                                                   : reinterpret_cast<void**>(&t->tdec);
+  void** tab = elem == 2   ? reinterpret_cast<void**>(&t->t16)
+               : elem == 4 ? reinterpret_cast<void**>(&t->t32)
+                           : reinterpret_cast<void**>(&t->tdec);
   if ((e = cudaMalloc(tab, tab_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&t->fi, fb)) != cudaSuccess ||
       (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
@@ -1182,6 +1181,11 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       if (quad_mass(r.kernel) >= (int64_t(1) << 53))
         return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the exact fp64 range",
                     r.kernel.kw, r.kernel.kh);
+      // the 32-bit planes give sum (x-cx)^2 exactly while it stays < 2^32
+      const int64_t hm = std::max(k_hx(r.kernel), k_hy(r.kernel));
+      if ((int64_t)r.kernel.kw * r.kernel.kh * hm * hm >= (int64_t(1) << 32))
+        return fail(SWG_ERR_CONFIG, "kernel %dx%d: squared offsets exceed the 32-bit planes",
+                    r.kernel.kw, r.kernel.kh);
     }
     if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
     const bool ranged = t->bins != t->total_bins;
@@ -1225,7 +1229,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // and shares its kernel; a Uniform box is a one-ring cake with coefficient
   // 1.0 (exact integer weights, same scores: score_counts == score_weights on
   // integers), so on narrow tables it runs the 16-bit cake sweep.
-  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad64, kExp64 };
+  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
   std::vector<dim3> grid(n);
   std::vector<int> engine(n);
   std::vector<swg_kernel> kern(n);
@@ -1248,7 +1252,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       method = SWG_METHOD_SWIH;
     const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
     if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
-    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad64;
+    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad;
     else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EXP_L1) engine[i] = kExp64;
     else if (method == SWG_METHOD_CAKE) {
       engine[i] = (t->t16 && small) ? kCake16 : kCake32;
@@ -1258,7 +1262,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     else engine[i] = kAffine32;
     kern[i] = k;
     if (r.partial_in || r.partial_out) {  // engines that can continue a bin-range chain
-      const bool closed_mass = engine[i] == kAffine32 || engine[i] == kQuad64;
+      const bool closed_mass = engine[i] == kAffine32 || engine[i] == kQuad;
       if (engine[i] == kBrute || (!closed_mass && r.sim != SWG_SIM_BHATTACHARYYA))
         return fail(SWG_ERR_CONFIG,
                     "bin-range chains: Bhattacharyya, or intersection on swih Manhattan / "
@@ -1291,7 +1295,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
       const swg_kernel k = kern[i];
       a.tab = engine[i] == kCake16   ? (const void*)t->t16
-              : engine[i] == kQuad64 ? (const void*)t->t64
+              : engine[i] == kQuad ? (const void*)t->t32
               : engine[i] == kExp64  ? (const void*)t->tdec
                                      : (const void*)t->t32;
       a.plane_stride = t->ps;
@@ -1317,7 +1321,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         // of sw windows needs (2hy+2+tile) rows x (sw+2hx+2) cells resident
         size_t cell = 0;
         if (engine[i] == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
-        else if (engine[i] == kQuad64) cell = (size_t)t->groups * kOct * 5 * 8;
+        else if (engine[i] == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
         else if (engine[i] == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
         else if (engine[i] == kCake32) cell = (size_t)t->groups * kOct * 4;
         a.sc_tiles = 0;
@@ -1414,15 +1418,15 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
                        ra.eps, cnt);
         }
         c->launches += 3;
-      } else if (engine[i] == kQuad64) {
+      } else if (engine[i] == kQuad) {
         a.mass = (double)quad_mass(k);
-        // box corners (TL, TR, BL, BR) of the whole window, per plane, as byte
-        // offsets from the centre record of the 64-bit tables
-        const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
+        // box corners (TL, TR, BL, BR) of the whole window as byte offsets
+        // from the centre record within a plane of the 32-bit tables
+        const long long p8 = (long long)t->pitch * kOct;
         const long long xs[2] = {-a.hx, a.hx + 1}, ys[2] = {-a.hy, a.hy + 1};
         for (int pl = 0; pl < 5; ++pl)
           for (int q = 0; q < 4; ++q)
-            a.lat[4 * pl + q] = (int)(8 * (pl * ps8 + ys[q >> 1] * p8 + xs[q & 1] * kOct));
+            a.lat[4 * pl + q] = (int)(4 * (ys[q >> 1] * p8 + xs[q & 1] * kOct));
         CUDA_TRY(launch_sweep_quad(a, grid[i], c->stream));
       } else if (engine[i] == kAffine32) {
         a.mass = (double)affine_mass(k);
