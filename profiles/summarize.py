@@ -49,11 +49,14 @@ def launches(path):
     tot = collections.OrderedDict()
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in rows[1:]:
+        if "swg::" not in r[ki]:  # bench scaffolding: the spin before a step, L2 flush fills
+            continue
         name = re.sub(r"[(].*", "", r[ki]).replace("swg::<unnamed>::", "")
         us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         n, t = tot.get(name, (0, 0.0))
         tot[name] = (n + 1, t + us)
     all_us = sum(t for _, t in tot.values())
+    print("# libswg kernels only (the bench's spin kernel and L2-flush fills excluded)")
     print(f"{'kernel':70s} {'launches':>8s} {'total us':>12s} {'share':>7s}")
     for k, (n, t) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
         print(f"{k:70s} {n:8d} {t:12.1f} {100 * t / all_us:6.1f}%")
