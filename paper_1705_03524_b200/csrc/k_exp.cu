@@ -57,7 +57,11 @@ __device__ __forceinline__ double2 ldd2(const char* p) {
 }
 
 template <int SIM>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_exp(const SweepArgs a, const ExpSweep e) {
+#ifndef SWG_EXP_MINB
+#define SWG_EXP_MINB 3  // 80 registers: 3 CTAs per SM (latency-bound DRAM reads)
+#endif
+__global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const SweepArgs a,
+                                                                         const ExpSweep e) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   int tx, ty;
   sweep_tile(a.sc_tiles, tx, ty);
