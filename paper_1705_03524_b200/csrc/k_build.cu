@@ -57,6 +57,31 @@ __device__ __forceinline__ void store_record(T* dst, const T (&v)[kOct]) {
   }
 }
 
+// Chunk q (16 bytes) of an 8-element record.
+template <typename T>
+__device__ __forceinline__ uint4 record_chunk(const T (&v)[kOct], int q) {
+  if constexpr (sizeof(T) == 2) {
+    return make_uint4(uint32_t(v[0]) | uint32_t(v[1]) << 16, uint32_t(v[2]) | uint32_t(v[3]) << 16,
+                      uint32_t(v[4]) | uint32_t(v[5]) << 16, uint32_t(v[6]) | uint32_t(v[7]) << 16);
+  } else if constexpr (sizeof(T) == 4) {
+    return q == 0 ? make_uint4(v[0], v[1], v[2], v[3]) : make_uint4(v[4], v[5], v[6], v[7]);
+  } else {
+    return make_uint4((uint32_t)v[2 * q], (uint32_t)(v[2 * q] >> 32), (uint32_t)v[2 * q + 1],
+                      (uint32_t)(v[2 * q + 1] >> 32));
+  }
+}
+
+// 16-byte chunks per record build_body stages through shared memory (0:
+// direct per-thread stores; the 64-bit export tables would need 256 KB).
+template <typename T>
+__host__ __device__ constexpr int stage_chunks_per_record() {
+#ifdef SWG_NO_STAGE
+  return 0;
+#else
+  return sizeof(T) == 8 ? 0 : (int)(kOct * sizeof(T) / 16);
+#endif
+}
+
 template <typename T>
 __device__ __forceinline__ void store_zero_record(T* dst) {
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -313,9 +338,33 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
       }
     }
     T* row = plane + (size_t)(y + 1) * g.pitch * kOct;
-    if (live)
+    constexpr int NQ = stage_chunks_per_record<T>();
+    if constexpr (NQ > 0) {
+      // coalesced row stores: the warp's 32*CPT records are staged in shared
+      // memory (XOR-swizzled 16-byte chunks) and written back as 512
+      // contiguous bytes per store instruction; per-thread record runs touch
+      // 32 lines per instruction and throttle the LSU (lg_throttle)
+      extern __shared__ uint4 s_stage[];
+      uint4* st = s_stage + warp * 32 * CPT * NQ;
+      auto swz = [](int c) { return c ^ ((c >> 3) & 7); };
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+      for (int i = 0; i < CPT; ++i)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) st[swz((lane * CPT + i) * NQ + q)] = record_chunk<T>(t[i], q);
+      __syncwarp();
+      const int wrec0 = warp * 32 * CPT;
+      uint4* dst = reinterpret_cast<uint4*>(row) + (size_t)(wrec0 + 1) * NQ;
+#pragma unroll
+      for (int m = 0; m < CPT * NQ; ++m) {
+        const int c = m * 32 + lane;
+        if (wrec0 + c / NQ < g.w) dst[c] = st[swz(c)];
+      }
+      __syncwarp();
+    } else {
+      if (live)
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+    }
     if (tid == 0) store_zero_record<T>(row);
   }
 }
@@ -423,36 +472,53 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Opt a build kernel into the dynamic shared memory its row staging needs.
+template <typename K>
+static void allow_smem(K* kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)bytes);
+}
+
 template <typename T>
 cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
+  const size_t smem = (size_t)threads * cpt * stage_chunks_per_record<T>() * 16;
   const unsigned grid = (unsigned)(a.nbands * a.groups);
   const int kinds = sizeof(T) == 2 ? 1 : a.planes;  // narrow tables: plain only
   if (kinds > 1 && grid < 2u * 148u) {
     dim3 g3(grid, (unsigned)kinds);
-    if (cpt == 4) k_build_fused<T, 4><<<g3, threads, 0, s>>>(a);
-    else k_build_fused<T, 8><<<g3, threads, 0, s>>>(a);
+    if (cpt == 4) {
+      allow_smem(k_build_fused<T, 4>, smem);
+      k_build_fused<T, 4><<<g3, threads, smem, s>>>(a);
+    } else {
+      allow_smem(k_build_fused<T, 8>, smem);
+      k_build_fused<T, 8><<<g3, threads, smem, s>>>(a);
+    }
     *launches = 1;
     return cudaGetLastError();
   }
   *launches = kinds;
+  auto go = [&](auto kernel) {
+    allow_smem(kernel, smem);
+    kernel<<<grid, threads, smem, s>>>(a);
+  };
   for (int kind = 0; kind < kinds; ++kind) {
     if (cpt == 4) {
-      if (kind == 0) k_build<T, 0, 4><<<grid, threads, 0, s>>>(a);
-      else if (kind == 1) k_build<T, 1, 4><<<grid, threads, 0, s>>>(a);
-      else if (kind == 2) k_build<T, 2, 4><<<grid, threads, 0, s>>>(a);
+      if (kind == 0) go(k_build<T, 0, 4>);
+      else if (kind == 1) go(k_build<T, 1, 4>);
+      else if (kind == 2) go(k_build<T, 2, 4>);
       else if constexpr (sizeof(T) >= 4) {
-        if (kind == 3) k_build<T, 3, 4><<<grid, threads, 0, s>>>(a);
-        else k_build<T, 4, 4><<<grid, threads, 0, s>>>(a);
+        if (kind == 3) go(k_build<T, 3, 4>);
+        else go(k_build<T, 4, 4>);
       }
     } else {
-      if (kind == 0) k_build<T, 0, 8><<<grid, threads, 0, s>>>(a);
-      else if (kind == 1) k_build<T, 1, 8><<<grid, threads, 0, s>>>(a);
-      else if (kind == 2) k_build<T, 2, 8><<<grid, threads, 0, s>>>(a);
+      if (kind == 0) go(k_build<T, 0, 8>);
+      else if (kind == 1) go(k_build<T, 1, 8>);
+      else if (kind == 2) go(k_build<T, 2, 8>);
       else if constexpr (sizeof(T) >= 4) {
-        if (kind == 3) k_build<T, 3, 8><<<grid, threads, 0, s>>>(a);
-        else k_build<T, 4, 8><<<grid, threads, 0, s>>>(a);
+        if (kind == 3) go(k_build<T, 3, 8>);
+        else go(k_build<T, 4, 8>);
       }
     }
     const cudaError_t e = cudaGetLastError();
