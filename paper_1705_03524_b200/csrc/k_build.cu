@@ -473,10 +473,11 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
 }
 
 // Opt a build kernel into the dynamic shared memory its row staging needs.
+// (static + dynamic shared memory above 48 KB needs the opt-in; the fused
+// kernel's static arrays add up over its table kinds)
 template <typename K>
 static void allow_smem(K* kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)bytes);
+  if (bytes) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <typename T>
