@@ -126,7 +126,7 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V*
 
 // K1a: column count, y-sum (and y^2-sum for quadratic planes) of each bin of
 // one octet over one row band.  agg[band][group][column][aw]: words 0-7
-// counts, 8-15 y-sums, 16-23 y^2-sums (aw = 24 only).
+// counts, 8-15 y-sums (aw >= 16: ramp planes), 16-23 y^2-sums (aw = 24).
 __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
   const int band = blockIdx.x, grp = blockIdx.y;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
   uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * g.aw);
   dst[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
   dst[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
+  if (g.aw == 8) return;  // plain tables carry counts only
   dst[2] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
   dst[3] = make_uint4(ys[4], ys[5], ys[6], ys[7]);
   if (g.aw == 24) {

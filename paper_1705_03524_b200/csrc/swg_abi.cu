@@ -280,7 +280,7 @@ swg_status run_build(swg_tables* t, T* out) {
   a.band_h = t->band_h;
   a.nbands = t->nbands;
   a.wa = t->wa;
-  a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : 16;
+  a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : t->planes == SWG_PLANES_PLAIN ? 8 : 16;
   a.agg = t->lb;
   a.bin0 = t->bin0;
   if (t->nbands > 1) {

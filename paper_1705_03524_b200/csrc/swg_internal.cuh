@@ -58,7 +58,7 @@ struct BuildArgs {
   int w, h, bins, groups, planes;
   int band_h, nbands;
   size_t wa;           // padded width (columns) of the carry array
-  int aw;              // carry words per column: 16, or 24 with quadratic planes
+  int aw;              // carry words per column: 8 (plain), 16 (ramps), 24 (quadratic)
   int bin0;            // global bin of local bin 0 (bin-range tables)
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
