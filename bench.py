@@ -706,6 +706,20 @@ def main():
                 "kernel": f"{kname} at {k.kw}x{k.kh} (planes read once + 8 B/window = "
                           f"{int(dom_bytes)} B per launch, {dom_ms:.4f} ms)"}
     roofline["frac"] = roofline["achieved"] / hbm
+    # on-chip side of the same launch: the table records every window reads
+    # (corners x bins x entry bytes; the cake's full ring count, early exits
+    # not deducted) against the L1 load bandwidth (148 SMs x 128 B/clk at the
+    # SM clock sampled during the run)
+    rings = g["scales"][si][2]
+    corners = {"k_sweep_affine": 20 if k.kind != swg.UNIFORM else 4, "k_sweep_quad": 20,
+               "k_sweep_exp": 16}.get(kname, 4 * rings)
+    onchip_bytes = corners * nb * e * dom_win
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+    roofline["onchip"] = {"achieved": onchip_bytes / (dom_ms / 1e3) / 1e12, "peak": l1_peak,
+                          "unit": "TB/s", "bytes": int(onchip_bytes),
+                          "frac": onchip_bytes / (dom_ms / 1e3) / 1e12 / l1_peak,
+                          "peak_source": "148 SMs x 128 B/clk L1 at the sampled SM clock"}
     build_avg = sum(build_ms) / args.steps  # ms per step, all rebuilds
     in_bytes = sum(u["h2d"] for u in units)
     build_bytes = in_bytes + sum(group_build_bytes(wl["groups"][u["g"]], tab_w, tab_h, nb)

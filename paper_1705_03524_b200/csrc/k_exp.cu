@@ -179,16 +179,20 @@ __global__ void k_select_cand(const double* scores, size_t n, int row0, int mw,
 
 // Phase 2b: exact fp64 brute-force re-score of the candidates (weights_into
 // + score_weights order, baselines.cpp:53-69, matching.cpp:37-52), written
-// back into the map.  One WARP per candidate: every lane walks the window's
-// pixels in row-major order and lane j accumulates the bins b = j (mod 32)
-// in registers -- each bin's sum keeps the reference's pixel order, with no
-// memory dependency between consecutive pixels.  Lane 0 then forms the mass
-// and the score in bin order.  When more than `cap` windows qualified, the
-// warps stride over the whole map and re-score every qualifying cell.
-template <int SLOTS>
+// back into the map.  One WARP per candidate.  The window's pixels stream
+// through the warp 32 at a time (lane l holds pixel l of a row segment);
+// __match_any_sync groups the lanes of equal bin and each group's lowest
+// lane adds its members' weights, in lane (= row-major pixel) order, to that
+// bin's running total in shared memory -- every bin's sum is the reference's
+// sequential sum, and different bins advance in parallel (one dependent add
+// per pixel of the same bin, not per pixel of the window).  Lane 0 then forms
+// the mass and the score in bin order.  When more than `cap` windows
+// qualified, the warps stride over the whole map and re-score every
+// qualifying cell.
 __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const RescoreArgs r,
                                                  const swg_peak* fast) {
-  __shared__ double s_h[4][SLOTS * 32];
+  __shared__ double s_tot[4][kMaxBins];
+  __shared__ double s_w[4][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * 4 + wib, nw = gridDim.x * 4;
   const int cnt = *r.count;
@@ -197,7 +201,8 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
   const long long total = overflow ? (long long)a.rows * a.mw : cnt;
   double best = -2.0;
   long long bidx = 0x7FFFFFFFFFFFFFFFLL;
-  double* h = s_h[wib];
+  double* h = s_tot[wib];
+  double* wv = s_w[wib];
   for (long long c = gw; c < total; c += nw) {
     long long idx;
     if (overflow) {
@@ -207,21 +212,7 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
       idx = r.cand[c];
     }
     const int u = (int)(idx % a.mw), v = (int)(idx / a.mw);
-    double acc[SLOTS];
-#pragma unroll
-    for (int k = 0; k < SLOTS; ++k) acc[k] = 0.0;
-    // branch-free: a pixel adds its weight to the owner lane's slot and an
-    // exact 0.0 everywhere else (x + 0.0 == x), so each bin's sum is the
-    // reference's sequence; loads are batched 8 pixels ahead of the adds
-    auto add_px = [&](int b, double w) {
-      const double we = ((b & 31) == lane && b < r.bins) ? w : 0.0;
-      const int slot = b >> 5;
-#pragma unroll
-      for (int k = 0; k < SLOTS; ++k) acc[k] = __dadd_rn(acc[k], slot == k ? we : 0.0);
-    };
-    // pixels stream through the warp 32 at a time: lane l loads pixel
-    // (dx0 + l) of the row (coalesced, next batch prefetched), then the
-    // batch is broadcast pixel by pixel in row-major order
+    for (int b = lane; b < r.bins; b += 32) h[b] = 0.0;
     const int per_row = (r.kw + 31) >> 5, nb = r.kh * per_row;
     auto load = [&](int i, int& bl, double& wl) {
       const int dy = i / per_row, dx = (i - dy * per_row) * 32 + lane;
@@ -235,17 +226,20 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
     int bn;
     double wn;
     load(0, bn, wn);
-    for (int i = 0; i < nb; ++i) {
-      const int bc = bn;
-      const double wc = wn;
-      load(i + 1, bn, wn);
-#pragma unroll 8
-      for (int l = 0; l < 32; ++l) add_px(__shfl_sync(0xFFFFFFFFu, bc, l),
-                                          __shfl_sync(0xFFFFFFFFu, wc, l));
-    }
-#pragma unroll
-    for (int k = 0; k < SLOTS; ++k) h[k * 32 + lane] = acc[k];
     __syncwarp();
+    for (int i = 0; i < nb; ++i) {
+      const int bl = bn;
+      wv[lane] = wn;
+      load(i + 1, bn, wn);  // prefetch the next segment
+      const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
+      __syncwarp();
+      if (bl < r.bins && lane == __ffs(grp) - 1) {
+        double t = h[bl];
+        for (unsigned m = grp; m; m &= m - 1) t = __dadd_rn(t, wv[__ffs(m) - 1]);
+        h[bl] = t;
+      }
+      __syncwarp();
+    }
     if (lane == 0) {
       double mass = 0.0, sc = 0.0;
       for (int b = 0; b < r.bins; ++b) mass = __dadd_rn(mass, h[b]);
@@ -271,6 +265,7 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
   block_peak_e(best, bidx, r.parts + blockIdx.x);
 }
 
+
 }  // namespace
 
 cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s) {
@@ -288,13 +283,7 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (r.cap + 3) / 4;  // one warp per candidate
-  const int slots = (r.bins + 31) / 32;
-  if (slots <= 1) k_rescore<1><<<blocks, 128, 0, s>>>(a, r, peak);
-  else if (slots <= 2) k_rescore<2><<<blocks, 128, 0, s>>>(a, r, peak);
-  else if (slots <= 4) k_rescore<4><<<blocks, 128, 0, s>>>(a, r, peak);
-  else if (slots <= 8) k_rescore<8><<<blocks, 128, 0, s>>>(a, r, peak);
-  else if (slots <= 16) k_rescore<16><<<blocks, 128, 0, s>>>(a, r, peak);
-  else k_rescore<32><<<blocks, 128, 0, s>>>(a, r, peak);
+  k_rescore<<<blocks, 128, 0, s>>>(a, r, peak);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return launch_peak_reduce(r.parts, blocks, a.mw, a.hx, a.hy, peak, s);
 }
