@@ -190,6 +190,9 @@ struct swg_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  // device -> host copies of finished maps overlap the next scale's sweep
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> events;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
   DevBuf parts, scores, peaks, terms, qout, grid, io, resc, bpeaks;
@@ -477,6 +480,11 @@ swg_status swg_ctx_create(int device, swg_ctx** out) {
     return fail(SWG_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
   }
   c->stream = c->own;
+  if ((e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking)) != cudaSuccess) {
+    cudaStreamDestroy(c->own);
+    delete c;
+    return fail(SWG_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
+  }
   *out = c;
   return SWG_OK;
 }
@@ -499,6 +507,9 @@ static void ctx_release(swg_ctx* c) {
       g->buf.release();
       delete g;
     }
+    cudaStreamSynchronize(c->copy);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    cudaStreamDestroy(c->copy);
     cudaStreamDestroy(c->own);
   }
   delete c;
@@ -1283,6 +1294,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   ST_TRY(c->peaks.ensure((size_t)n * sizeof(swg_peak)));
   swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(c->peaks.p);
 
+  bool copies = false;
   for (int i = 0; i < n; ++i) {
     const swg_map_request& r = reqs[i];
     const int rows = v1[i] - v0[i];
@@ -1491,19 +1503,28 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         c->launches += 1;
       }
     }
-    if (scores_host && scores_host[i] && rows > 0)
+    if (scores_host && scores_host[i] && rows > 0) {
+      // the copy stream takes the finished map while the next scale sweeps
+      while (c->events.size() <= (size_t)i) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->events.push_back(ev);
+      }
+      CUDA_TRY(cudaEventRecord(c->events[i], c->stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[i], 0));
       CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)rows * mws[i] * 8,
-                               cudaMemcpyDeviceToHost, c->stream));
+                               cudaMemcpyDeviceToHost, c->copy));
+      copies = true;
+    }
   }
-  bool sync = false;
-  if (scores_host)
-    for (int i = 0; i < n; ++i) sync |= scores_host[i] != nullptr;
+  bool sync = copies;
   if (peaks_host) {
     CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
                              cudaMemcpyDeviceToHost, c->stream));
     sync = true;
   }
   if (sync) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (copies) CUDA_TRY(cudaStreamSynchronize(c->copy));
   return SWG_OK;
 }
 
