@@ -64,14 +64,18 @@ class MultiScaleMatcher:
     likelihood_map (matching.cpp:108-209) + peak (211-223) once per scale."""
 
     def __init__(self, ctx: swg.Context, width: int, height: int, fmt=swg.FMT_GRAY8, bins=16,
-                 planes=swg.PLANES_AFFINE):
+                 planes=swg.PLANES_AFFINE, decay=None):
         self.ctx, self.fmt, self.bins, self.planes = ctx, fmt, bins, planes
         self.width, self.height = width, height
+        self.decay = decay  # PLANES_DECAY: the exponential kernel's per-pixel decay
         self.tables = None
 
     def load(self, pixels):
         if self.tables is None:
-            self.tables = self.ctx.build(pixels, self.fmt, self.bins, self.planes)
+            if self.planes == swg.PLANES_DECAY:
+                self.tables = self.ctx.build_decay(pixels, self.decay, self.fmt, self.bins)
+            else:
+                self.tables = self.ctx.build(pixels, self.fmt, self.bins, self.planes)
         else:
             self.tables.rebuild(pixels)
         return self.tables
