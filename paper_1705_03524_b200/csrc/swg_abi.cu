@@ -142,8 +142,8 @@ int64_t affine_mass(const swg_kernel& k) {
 }
 
 // WeddingCakePlan constructor (baselines.cpp:84-131), same arithmetic order.
-swg_status cake_plan(const swg_kernel& k, int m, int rule, CakeRings& out,
-                     std::vector<double>* weights = nullptr) {
+swg_status cake_plan_compute(const swg_kernel& k, int m, int rule, CakeRings& out,
+                             std::vector<double>* weights) {
   const int hx = k_hx(k), hy = k_hy(k);
   const int max_rings = std::min(hx, hy) + 1;
   if (m < 1 || m > max_rings)
@@ -180,6 +180,46 @@ swg_status cake_plan(const swg_kernel& k, int m, int rule, CakeRings& out,
     out.coeff[i] = rw[i] - (i > 0 ? rw[i - 1] : 0.0);  // baselines.cpp:141
   }
   if (weights) *weights = rw;
+  return SWG_OK;
+}
+
+// Ring plans are pure functions of (kernel, rings, rule) and the MEAN rule
+// visits every window cell (~1e4 weight evaluations at 97x97): memoised so a
+// per-frame likelihood_maps call does no O(kw*kh) host work.
+swg_status cake_plan(const swg_kernel& k, int m, int rule, CakeRings& out,
+                     std::vector<double>* weights = nullptr) {
+  struct Entry {
+    swg_kernel k;
+    int m, rule;
+    CakeRings plan;
+    std::vector<double> w;
+  };
+  static std::mutex mu;
+  static std::vector<Entry*> cache;  // small; lives for the process
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry* e : cache)
+      if (e->k.kind == k.kind && e->k.kw == k.kw && e->k.kh == k.kh && e->k.sigma == k.sigma &&
+          e->m == m && e->rule == rule) {
+        out = e->plan;
+        if (weights) *weights = e->w;
+        return SWG_OK;
+      }
+  }
+  auto* e = new Entry{k, m, rule, {}, {}};
+  const swg_status st = cake_plan_compute(k, m, rule, e->plan, &e->w);
+  if (st != SWG_OK) {
+    delete e;
+    return st;
+  }
+  out = e->plan;
+  if (weights) *weights = e->w;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 256) {
+    delete cache.front();
+    cache.erase(cache.begin());
+  }
+  cache.push_back(e);
   return SWG_OK;
 }
 
