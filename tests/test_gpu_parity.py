@@ -811,3 +811,31 @@ def test_bin_range_errors(ctx, oracle):
         ctx.build_bins(img, 8, 20, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
     with pytest.raises(swg.OutOfRangeError):
         ctx.build_bins(img, 5, 5, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+
+
+def test_decay_tables_max_width(ctx, oracle):
+    """Decay build at the width limit (8 columns per thread, staged stores)."""
+    img = oracle.random_gray(4096, 5, 3)
+    bins = 3
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build_decay(img, 0.5, swg.FMT_GRAY8, bins)
+    for k, f in enumerate((fi, fi[:, ::-1], fi[::-1, :], fi[::-1, ::-1])):
+        np.testing.assert_allclose(t.export_f64(k), _decayed_se(np.ascontiguousarray(f), bins, 0.5),
+                                   rtol=1e-12, atol=1e-12)
+
+
+def test_quadratic_tall_image(ctx, oracle):
+    """32-bit quadratic planes have no height limit (the 64-bit export keeps
+    the 2340-row limit of its y^2 carries): maps of a 40 x 3000 image."""
+    img = oracle.random_gray(40, 3000, 12)
+    bins = 5
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC)
+    k = K(swg.EUCLID_QUAD, 15, 21)
+    ok = O.kernel(O.EUCLID_QUAD, 15, 21)
+    mdl = oracle.target_model(fi[100:121, 10:25].copy(), bins, ok, O.BRUTE)
+    got, pk = t.likelihood_map(k, mdl, swg.SWIH, rows=(2900, 2980))
+    want = oracle.likelihood_map(np.ascontiguousarray(fi[2900:3000]), bins, mdl, ok, O.BRUTE)
+    assert (got == want).all()
+    with pytest.raises(swg.SizeError):
+        t.export_i64(0)
