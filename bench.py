@@ -354,6 +354,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default="rows", choices=["rows", "bins"],
+                    help="config 4 over N>1 ranks: row bands per rank (default) or every "
+                         "band on every rank with bin ranges chained rank to rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -433,12 +436,20 @@ def main():
         H, W = data.image.shape[:2]
         frame_dev = torch.from_numpy(data.image).cuda()
         g, ms = wl["groups"][0], models[0]
-        n_bands = max(4, world)
+        bins_mode = args.shard == "bins" and world > 1
+        n_bands = 4 if bins_mode else max(4, world)
         BH, plan = band_plan(H, g["scales"], n_bands)
         full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
                      for k, _, _, _ in g["scales"]]
-        mine = [b for b in range(n_bands) if b % world == rank]
-        t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+        mine = list(range(n_bands)) if bins_mode else \
+            [b for b in range(n_bands) if b % world == rank]
+        if bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e bin ranges)
+            from paper_1705_03524_b200 import dist as D
+            b0, b1 = D.bin_ranges(nb, world)[rank]
+            t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, fmt, wl["bins"],
+                               g["planes"], decay=g.get("decay") or 0.0)
+        else:
+            t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
         for b in mine:
             p0, rows = plan[b]
             reqs, maps, sidx = [], [], []
@@ -452,12 +463,39 @@ def main():
                 sidx.append(si)
             units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
                               g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
+        if bins_mode:
+            # running (s, mass) per window: received from rank-1, sent to rank+1
+            last = rank == world - 1
+            for u in units:
+                u["pin"] = [torch.empty(tuple(m.shape) + (2,), dtype=torch.float64,
+                                        device="cuda") if rank > 0 else None for m in u["maps"]]
+                u["pout"] = [None if last else torch.empty(tuple(m.shape) + (2,),
+                                                           dtype=torch.float64, device="cuda")
+                             for m in u["maps"]]
+                for i, r in enumerate(u["reqs"]):
+                    r.partial_in, r.partial_out = u["pin"][i], u["pout"][i]
+                if not last:
+                    u["maps"] = [m[:0] for m in u["maps"]]  # no scores off the last rank
         tab_w, tab_h = W, BH
     for u in units:
         u["peaks"] = torch.zeros(len(u["reqs"]), 3, dtype=torch.float64, device="cuda")
     n_win = sum(m.numel() for u in units for m in u["maps"]) if wl["kind"] != "sequence" else \
         sum(m.numel() for m in units[0]["maps"]) * len(units)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def p2p_send(x, dst):  # NCCL over NVLink; gloo (shared-GPU test mode) stages on the host
+        if share:
+            dist.send(x.cpu(), dst=dst)
+        else:
+            dist.send(x, dst=dst)
+
+    def p2p_recv(x, src):
+        if share:
+            h = torch.empty(x.shape, dtype=x.dtype)
+            dist.recv(h, src=src)
+            x.copy_(h)
+        else:
+            dist.recv(x, src=src)
 
     def step(ev=None):
         j = 0
@@ -470,8 +508,13 @@ def main():
                 ev[j].record()
                 j += 1
             for i, r in enumerate(u["reqs"]):
-                u["t"].likelihood_maps([r], scores="none", scores_dev=[u["maps"][i]],
-                                       peaks_dev=u["peaks"][i])
+                if "pin" in u and rank > 0:
+                    p2p_recv(u["pin"][i], rank - 1)
+                u["t"].likelihood_maps([r], scores="none",
+                                       scores_dev=None if r.partial_out is not None
+                                       else [u["maps"][i]], peaks_dev=u["peaks"][i])
+                if "pin" in u and rank < world - 1:
+                    p2p_send(u["pout"][i], rank + 1)
                 if ev:
                     ev[j].record()
                     j += 1
@@ -482,7 +525,7 @@ def main():
 
     # The step as one CUDA graph (no host launch gaps between the kernels).
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and not any("pin" in u for u in units):  # (p2p chain: eager)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             step()
@@ -599,7 +642,7 @@ def main():
     import ctypes as C
     from paper_1705_03524_b200.swg import Peak, _Req, _check, lib
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not any("pin" in u for u in units):
         h2d = d2h = 0
         if wl["kind"] == "sequence":
             pin = swg.PinnedBuffer(data.frames.shape, np.uint8)
@@ -749,7 +792,9 @@ def main():
         "config": {"workload": wl["name"], "bins": nb, "windows_per_step": int(job_win),
                    "table_shape": [tab_w, tab_h], "units_per_rank": len(units),
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
-                   "parallelism": (f"{'frames' if weak else wl['kind']} sharded over {world} "
+                   "parallelism": (f"bin ranges chained over {world} GPU(s) (p2p partial sums)"
+                                   if any("pin" in u for u in units) else
+                                   f"{'frames' if weak else wl['kind']} sharded over {world} "
                                    f"GPU(s), no collective")},
         "ih_build": {"ms": build_avg, "gbps": build_roof["achieved"], "frac": build_roof["frac"]},
         "per_scale_ms": dict(zip(scale_names, flat)),
