@@ -507,6 +507,13 @@ def main():
             if ev:
                 ev[j].record()
                 j += 1
+            if ev is None and "pin" not in u:
+                # one call for all scales: the library overlaps their sweeps
+                # on its worker streams (the per-scale timing path below
+                # records an event between scales instead)
+                u["t"].likelihood_maps(u["reqs"], scores="none", scores_dev=u["maps"],
+                                       peaks_dev=u["peaks"])
+                continue
             for i, r in enumerate(u["reqs"]):
                 if "pin" in u and rank > 0:
                     p2p_recv(u["pin"][i], rank - 1)

@@ -233,6 +233,11 @@ struct swg_ctx {
   // device -> host copies of finished maps overlap the next scale's sweep
   cudaStream_t copy = nullptr;
   std::vector<cudaEvent_t> events;
+  // the requests of one likelihood_maps call fan out over worker streams
+  // (their sweeps overlap: no partial last wave per scale)
+  static constexpr int kWorkers = 3;
+  cudaStream_t work[kWorkers] = {};
+  cudaEvent_t fork = nullptr, join[kWorkers] = {};
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
   DevBuf parts, scores, peaks, terms, qout, grid, io, resc, bpeaks;
@@ -498,6 +503,8 @@ swg_status swg_device_count(int* n) {
   return SWG_OK;
 }
 
+static void ctx_release(swg_ctx* c);
+
 swg_status swg_ctx_create(int device, swg_ctx** out) {
   if (!out) return fail(SWG_ERR_ARG, "NULL out");
   *out = nullptr;
@@ -525,6 +532,16 @@ swg_status swg_ctx_create(int device, swg_ctx** out) {
     delete c;
     return fail(SWG_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
   }
+  e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  for (int w = 0; w < swg_ctx::kWorkers && e == cudaSuccess; ++w) {
+    e = cudaStreamCreateWithFlags(&c->work[w], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[w], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    c->refs = 1;
+    ctx_release(c);
+    return fail(SWG_ERR_CUDA, "worker streams: %s", cudaGetErrorString(e));
+  }
   *out = c;
   return SWG_OK;
 }
@@ -549,6 +566,14 @@ static void ctx_release(swg_ctx* c) {
     }
     cudaStreamSynchronize(c->copy);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    for (int w = 0; w < swg_ctx::kWorkers; ++w) {
+      if (c->work[w]) {
+        cudaStreamSynchronize(c->work[w]);
+        cudaStreamDestroy(c->work[w]);
+      }
+      if (c->join[w]) cudaEventDestroy(c->join[w]);
+    }
+    if (c->fork) cudaEventDestroy(c->fork);
     cudaStreamDestroy(c->copy);
     cudaStreamDestroy(c->own);
   }
@@ -1334,16 +1359,40 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   ST_TRY(c->peaks.ensure((size_t)n * sizeof(swg_peak)));
   swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(c->peaks.p);
 
+  // lazily built 32-bit planes and the exact-peak scratch (one slice per
+  // request) are set up on the main stream before the requests fan out
+  constexpr int kCap = 4096;  // exact-peak candidates re-scored per request
+  const size_t rs_cand = (size_t)kCap * 8, rs_parts = (size_t)((kCap + 3) / 4) * sizeof(PeakPart);
+  const size_t rs_slice = round_up(rs_cand + rs_parts + 256, 256);
+  for (int i = 0; i < n; ++i)
+    if (v1[i] > v0[i] && (engine[i] == kAffine32 || engine[i] == kCake32)) ST_TRY(ensure_t32(t));
+  ST_TRY(c->resc.ensure(rs_slice * n));
+  int nwork = 0;
+  bool host_maps = false;
+  if (scores_host)
+    for (int i = 0; i < n; ++i) host_maps |= scores_host[i] != nullptr;
+#ifndef SWG_NO_FANOUT
+  // device outputs: overlap the scales' sweeps; host maps: keep the scales
+  // in sequence so each map's copy overlaps the next scale's sweep
+  nwork = host_maps ? 0 : std::min(n, (int)swg_ctx::kWorkers);
+  if (nwork > 1) {
+    CUDA_TRY(cudaEventRecord(c->fork, c->stream));
+    for (int w = 0; w < nwork; ++w) CUDA_TRY(cudaStreamWaitEvent(c->work[w], c->fork, 0));
+  } else {
+    nwork = 0;
+  }
+#endif
+
   bool copies = false;
   for (int i = 0; i < n; ++i) {
     const swg_map_request& r = reqs[i];
     const int rows = v1[i] - v0[i];
+    const cudaStream_t st = nwork ? c->work[i % nwork] : c->stream;
     double* dscores = (scores_dev && scores_dev[i])
                           ? scores_dev[i]
                           : static_cast<double*>(c->scores.p) + soff[i];
     PeakPart* parts = static_cast<PeakPart*>(c->parts.p) + poff[i];
     if (rows > 0) {
-      if (engine[i] == kAffine32 || engine[i] == kCake32) ST_TRY(ensure_t32(t));
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
       const swg_kernel k = kern[i];
       a.tab = engine[i] == kCake16   ? (const void*)t->t16
@@ -1433,12 +1482,12 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         } else {
           err = 2.0 * t->total_bins * dh;
         }
-        CUDA_TRY(launch_sweep_exp(a, es, grid[i], c->stream));
+        CUDA_TRY(launch_sweep_exp(a, es, grid[i], st));
         c->launches += 1;
         if (r.partial_out) continue;  // partial sums only: no scores, no peak
         c->launches += 1;
         CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
-                                    dpeaks + i, c->stream));
+                                    dpeaks + i, st));
         // phase 2: exact fp64 brute-force re-score of the near-maximum windows
         static thread_local RescoreArgs ra;  // 8 KB of model: keep off the stack
         ra = RescoreArgs{};
@@ -1450,22 +1499,19 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ra.bins = t->total_bins;  // every bin: the re-score is the whole histogram
         std::memset(ra.model, 0, sizeof(ra.model));
         std::memcpy(ra.model, r.model, sizeof(double) * t->total_bins);
-        ra.cap = 4096;
+        ra.cap = kCap;
         // a window outside [fast max - eps] cannot be the exact maximum when
         // eps >= 2 err (+ the fp64 rounding of the scores themselves)
         ra.eps = std::min(4.0, 2.0 * err + 1e-12);
-        const size_t hb = 0, cb = (size_t)ra.cap * 8;
-        const size_t pb = (size_t)((ra.cap + 3) / 4) * sizeof(PeakPart);
-        ST_TRY(c->resc.ensure(hb + cb + pb + 256));
-        char* rb = static_cast<char*>(c->resc.p);
-        ra.cand = reinterpret_cast<long long*>(rb + hb);
-        ra.parts = reinterpret_cast<PeakPart*>(rb + hb + cb);
-        ra.count = reinterpret_cast<int*>(rb + hb + cb + pb);
-        CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, c->stream));
+        char* rb = static_cast<char*>(c->resc.p) + rs_slice * i;
+        ra.cand = reinterpret_cast<long long*>(rb);
+        ra.parts = reinterpret_cast<PeakPart*>(rb + rs_cand);
+        ra.count = reinterpret_cast<int*>(rb + rs_cand + rs_parts);
+        CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, st));
         if (std::getenv("SWG_DEBUG_RESCORE")) {  // diagnostics: candidate count
           int cnt = 0;
-          cudaMemcpyAsync(&cnt, ra.count, 4, cudaMemcpyDeviceToHost, c->stream);
-          cudaStreamSynchronize(c->stream);
+          cudaMemcpyAsync(&cnt, ra.count, 4, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
           std::fprintf(stderr, "swg rescore: kernel %dx%d eps %.3g candidates %d\n", k.kw, k.kh,
                        ra.eps, cnt);
         }
@@ -1479,7 +1525,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         for (int pl = 0; pl < 5; ++pl)
           for (int q = 0; q < 4; ++q)
             a.lat[4 * pl + q] = (int)(4 * (ys[q >> 1] * p8 + xs[q & 1] * kOct));
-        CUDA_TRY(launch_sweep_quad(a, grid[i], c->stream));
+        CUDA_TRY(launch_sweep_quad(a, grid[i], st));
       } else if (engine[i] == kAffine32) {
         a.mass = (double)affine_mass(k);
         {  // corner byte offsets from the centre record (SweepArgs::lat order)
@@ -1495,7 +1541,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
           for (int q = 0; q < 20; ++q)
             a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
         }
-        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], c->stream));
+        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], st));
       } else if (engine[i] == kCake16 || engine[i] == kCake32) {
         static thread_local CakeRings rg;
         static thread_local CakeSweep cs;
@@ -1520,8 +1566,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         }
         a.rings = rings;
         a.wide0 = engine[i] == kCake16 && (long long)k.kw * k.kh >= 65536;
-        if (engine[i] == kCake16) CUDA_TRY(launch_sweep_cake16(a, cs, grid[i], c->stream));
-        else CUDA_TRY(launch_sweep_cake(a, cs, grid[i], c->stream));
+        if (engine[i] == kCake16) CUDA_TRY(launch_sweep_cake16(a, cs, grid[i], st));
+        else CUDA_TRY(launch_sweep_cake(a, cs, grid[i], st));
       } else {
         // direct per-pixel weighted histogram (baselines.cpp:24-69)
         const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);
@@ -1534,12 +1580,12 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         ba.kw = kw;
         ba.kh = kh;
         ba.integer = k_integer(k);
-        CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, c->stream));
+        CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, st));
       }
       if (engine[i] != kExp64 && !r.partial_out) {  // (exp reduces its own peaks)
         c->launches += 1;
         CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
-                                    dpeaks + i, c->stream));
+                                    dpeaks + i, st));
         c->launches += 1;
       }
     }
@@ -1550,12 +1596,16 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         c->events.push_back(ev);
       }
-      CUDA_TRY(cudaEventRecord(c->events[i], c->stream));
+      CUDA_TRY(cudaEventRecord(c->events[i], st));
       CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[i], 0));
       CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)rows * mws[i] * 8,
                                cudaMemcpyDeviceToHost, c->copy));
       copies = true;
     }
+  }
+  for (int w = 0; w < nwork; ++w) {  // join the worker streams
+    CUDA_TRY(cudaEventRecord(c->join[w], c->work[w]));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->join[w], 0));
   }
   bool sync = copies;
   if (peaks_host) {
