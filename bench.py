@@ -497,7 +497,19 @@ def main():
         else:
             dist.recv(x, src=src)
 
+    batch_peaks = None
+    if wl["kind"] == "sequence":
+        batch_peaks = torch.zeros(len(units) * len(units[0]["reqs"]), 3, dtype=torch.float64,
+                                  device="cuda")
+
     def step(ev=None):
+        if ev is None and batch_peaks is not None:
+            # the tracking batch through swg_likelihood_batch: frames round-robin
+            # over the library's table sets / worker streams (build of one
+            # frame overlaps the sweeps of another)
+            units[0]["t"].likelihood_batch([u["src"] for u in units], units[0]["reqs"],
+                                           pitch=units[0]["pitch"], peaks_dev=batch_peaks)
+            return
         j = 0
         for u in units:
             if ev:

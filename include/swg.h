@@ -300,8 +300,12 @@ swg_status swg_likelihood_maps(swg_tables* t, int n,
  * device as is_device; a search-region crop is a pointer into the full frame
  * plus the full frame's pitch) and run the n requests, peaks only.  Peak of
  * frame f, request i -> [f * n + i] of peaks_dev (device, asynchronous)
- * and/or peaks_host (filled on return).  Frames are processed in order
- * through the one table set. */
+ * and/or peaks_host (filled on return).  Frames round-robin over up to
+ * three table sets of this geometry (`t` plus two the library creates on
+ * first use and frees with `t`) on the context's worker streams, so one
+ * frame's build overlaps another's sweeps; the call forks from and joins
+ * back to the context stream (graph-capturable with device outputs).  Not
+ * to be called concurrently with other calls on the same context. */
 swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* frames,
                                 int is_device, size_t pitch_bytes, int n,
                                 const swg_map_request* reqs, swg_peak* peaks_host,

@@ -238,9 +238,17 @@ struct swg_ctx {
   static constexpr int kWorkers = 3;
   cudaStream_t work[kWorkers] = {};
   cudaEvent_t fork = nullptr, join[kWorkers] = {};
+  // map scratch (CTA candidates, unrequested maps, peaks, exact-peak
+  // candidates): one set per worker so a frame batch can run its frames'
+  // calls concurrently (swg_likelihood_batch sets `slot` and `fanout_off`)
+  struct Scratch {
+    DevBuf parts, scores, peaks, resc;
+  } scr[kWorkers];
+  int slot = 0;
+  bool fanout_off = false;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
-  DevBuf parts, scores, peaks, terms, qout, grid, io, resc, bpeaks;
+  DevBuf terms, qout, grid, io, bpeaks;
   // exact kernel-weight grids, uploaded once per kernel (graph-capture safe)
   struct Grid {
     swg_kernel k;
@@ -269,6 +277,8 @@ struct swg_tables {
   double decay = 0.0;
   uint16_t* fflip = nullptr; // h / v / hv flipped feature images (decay tables)
   uint32_t* lb = nullptr;  // band carry scratch (BuildArgs::agg)
+  // same-geometry table sets for concurrent frames (swg_likelihood_batch)
+  swg_tables* clone[2] = {nullptr, nullptr};
   int band_h = 0, nbands = 0;
   size_t wa = 0;
   size_t bytes = 0;
@@ -551,14 +561,16 @@ static void ctx_release(swg_ctx* c) {
   {
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
-    c->parts.release();
-    c->scores.release();
-    c->peaks.release();
+    for (auto& x : c->scr) {
+      x.parts.release();
+      x.scores.release();
+      x.peaks.release();
+      x.resc.release();
+    }
     c->terms.release();
     c->qout.release();
     c->grid.release();
     c->io.release();
-    c->resc.release();
     c->bpeaks.release();
     for (auto* g : c->grids) {
       g->buf.release();
@@ -815,6 +827,7 @@ swg_status swg_tables_upload_i64(swg_ctx* c, int w, int h, int bins,
 
 swg_status swg_tables_destroy(swg_tables* t) {
   if (!t) return SWG_OK;
+  for (swg_tables* cl : t->clone) swg_tables_destroy(cl);
   if (t->ctx) {
     DeviceGuard g(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
@@ -1211,14 +1224,15 @@ swg_status swg_map_peak(swg_ctx* c, const double* scores, int mw, int mh, int hx
   const size_t n = (size_t)mw * mh;
   const int nparts = (int)std::min<size_t>((n + 255) / 256, 148 * 4);
   ST_TRY(c->io.ensure(round_up(n * 8, 256)));
-  ST_TRY(c->parts.ensure((size_t)nparts * sizeof(PeakPart)));
-  ST_TRY(c->peaks.ensure(sizeof(swg_peak)));
+  swg_ctx::Scratch& S = c->scr[0];
+  ST_TRY(S.parts.ensure((size_t)nparts * sizeof(PeakPart)));
+  ST_TRY(S.peaks.ensure(sizeof(swg_peak)));
   CUDA_TRY(cudaMemcpyAsync(c->io.p, scores, n * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(launch_map_peak(static_cast<const double*>(c->io.p), n, mw, hx, hy,
-                           static_cast<PeakPart*>(c->parts.p), nparts,
-                           static_cast<swg_peak*>(c->peaks.p), c->stream));
+                           static_cast<PeakPart*>(S.parts.p), nparts,
+                           static_cast<swg_peak*>(S.peaks.p), c->stream));
   c->launches += 2;
-  CUDA_TRY(cudaMemcpyAsync(out, c->peaks.p, sizeof(swg_peak), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(out, S.peaks.p, sizeof(swg_peak), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return SWG_OK;
 }
@@ -1354,10 +1368,11 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     poff[i] = ptot;
     ptot += (size_t)grid[i].x * grid[i].y;
   }
-  ST_TRY(c->scores.ensure(std::max<size_t>(stot, 1) * 8));
-  ST_TRY(c->parts.ensure(ptot * sizeof(PeakPart)));
-  ST_TRY(c->peaks.ensure((size_t)n * sizeof(swg_peak)));
-  swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(c->peaks.p);
+  swg_ctx::Scratch& S = c->scr[c->slot];
+  ST_TRY(S.scores.ensure(std::max<size_t>(stot, 1) * 8));
+  ST_TRY(S.parts.ensure(ptot * sizeof(PeakPart)));
+  ST_TRY(S.peaks.ensure((size_t)n * sizeof(swg_peak)));
+  swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(S.peaks.p);
 
   // lazily built 32-bit planes and the exact-peak scratch (one slice per
   // request) are set up on the main stream before the requests fan out
@@ -1366,7 +1381,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   const size_t rs_slice = round_up(rs_cand + rs_parts + 256, 256);
   for (int i = 0; i < n; ++i)
     if (v1[i] > v0[i] && (engine[i] == kAffine32 || engine[i] == kCake32)) ST_TRY(ensure_t32(t));
-  ST_TRY(c->resc.ensure(rs_slice * n));
+  ST_TRY(S.resc.ensure(rs_slice * n));
   int nwork = 0;
   bool host_maps = false;
   if (scores_host)
@@ -1374,7 +1389,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
 #ifndef SWG_NO_FANOUT
   // device outputs: overlap the scales' sweeps; host maps: keep the scales
   // in sequence so each map's copy overlaps the next scale's sweep
-  nwork = host_maps ? 0 : std::min(n, (int)swg_ctx::kWorkers);
+  nwork = host_maps || c->fanout_off ? 0 : std::min(n, (int)swg_ctx::kWorkers);
   if (nwork > 1) {
     CUDA_TRY(cudaEventRecord(c->fork, c->stream));
     for (int w = 0; w < nwork; ++w) CUDA_TRY(cudaStreamWaitEvent(c->work[w], c->fork, 0));
@@ -1390,8 +1405,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     const cudaStream_t st = nwork ? c->work[i % nwork] : c->stream;
     double* dscores = (scores_dev && scores_dev[i])
                           ? scores_dev[i]
-                          : static_cast<double*>(c->scores.p) + soff[i];
-    PeakPart* parts = static_cast<PeakPart*>(c->parts.p) + poff[i];
+                          : static_cast<double*>(S.scores.p) + soff[i];
+    PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + poff[i];
     if (rows > 0) {
       static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
       const swg_kernel k = kern[i];
@@ -1503,7 +1518,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         // a window outside [fast max - eps] cannot be the exact maximum when
         // eps >= 2 err (+ the fp64 rounding of the scores themselves)
         ra.eps = std::min(4.0, 2.0 * err + 1e-12);
-        char* rb = static_cast<char*>(c->resc.p) + rs_slice * i;
+        char* rb = static_cast<char*>(S.resc.p) + rs_slice * i;
         ra.cand = reinterpret_cast<long long*>(rb);
         ra.parts = reinterpret_cast<PeakPart*>(rb + rs_cand);
         ra.count = reinterpret_cast<int*>(rb + rs_cand + rs_parts);
@@ -1636,12 +1651,53 @@ swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* 
       dst = static_cast<swg_peak*>(c->bpeaks.p);
     }
   }
-  // frames run back to back through the one table set, stream ordered: the
-  // upload + build of frame f+1 queues behind the sweeps of frame f
-  for (int f = 0; f < n_frames; ++f) {
+  for (int f = 0; f < n_frames; ++f)
     if (!frames[f]) return fail(SWG_ERR_ARG, "NULL frame %d", f);
-    ST_TRY(swg_tables_rebuild(t, frames[f], is_device, pitch_bytes));
-    ST_TRY(swg_likelihood_maps(t, n, reqs, nullptr, nullptr, nullptr, dst + (size_t)f * n));
+  // Frames round-robin over up to three table sets (this one + two clones of
+  // its geometry, made on first use) on the context's worker streams: the
+  // build of one frame overlaps the sweeps of another.  Each frame's calls
+  // run on its worker stream with that worker's scratch; the caller's stream
+  // forks to the workers first and joins them at the end (graph-capturable).
+  const int K = std::min(n_frames, (int)swg_ctx::kWorkers);
+  swg_tables* sets[swg_ctx::kWorkers] = {t, nullptr, nullptr};
+  for (int k = 1; k < K; ++k) {
+    if (!t->clone[k - 1])
+      ST_TRY(build_common(c, frames[k], is_device, pitch_bytes, t->w, t->h, t->format,
+                          t->levels, t->planes, t->decay, t->bin0, t->bin0 + t->bins, 0,
+                          &t->clone[k - 1]));
+    sets[k] = t->clone[k - 1];
+  }
+  const cudaStream_t orig = c->stream;
+  struct Restore {  // the caller's stream and the context defaults, on every exit
+    swg_ctx* c;
+    cudaStream_t s;
+    ~Restore() {
+      c->stream = s;
+      c->slot = 0;
+      c->fanout_off = false;
+    }
+  } restore{c, orig};
+  {
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaEventRecord(c->fork, orig));
+    for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(c->work[k], c->fork, 0));
+  }
+  c->fanout_off = true;
+  for (int f = 0; f < n_frames; ++f) {
+    const int k = f % K;
+    c->stream = c->work[k];
+    c->slot = k;
+    ST_TRY(swg_tables_rebuild(sets[k], frames[f], is_device, pitch_bytes));
+    ST_TRY(swg_likelihood_maps(sets[k], n, reqs, nullptr, nullptr, nullptr,
+                               dst + (size_t)f * n));
+  }
+  c->stream = orig;
+  {
+    DeviceGuard g(c->device);
+    for (int k = 0; k < K; ++k) {
+      CUDA_TRY(cudaEventRecord(c->join[k], c->work[k]));
+      CUDA_TRY(cudaStreamWaitEvent(orig, c->join[k], 0));
+    }
   }
   if (peaks_host) {
     std::lock_guard<std::mutex> lk(c->mu);
