@@ -253,7 +253,7 @@ def _quantize_host(wl, img):
     return O.Ref().quantize(img, wl["bins"])
 
 
-def cpu_reference(wl, data, models, budget_s=12.0, threads=None):
+def cpu_reference(wl, data, models, budget_s=12.0, threads=None, public_api=False):
     """Reference CPU path (best-use) on `threads` host threads:
     kernels the reference implements (Manhattan swih, GaussianChebyshev
     wedding cake) run the unmodified reference sources (oracle/_ref: one
@@ -314,10 +314,23 @@ def cpu_reference(wl, data, models, budget_s=12.0, threads=None):
             total_win += mw * mh * mult
             sample_win += rows * mw
             proj += mw * mh * mult / rate
+    # SURVEY §8d's second variant: the reference's public API as a user calls
+    # it (one likelihood_map per scale, each rebuilding the tables), for the
+    # gray-u8 configs whose kernels the reference implements; full maps
+    public = None
+    if (public_api and wl["fmt"] == swg.FMT_GRAY8 and wl["kind"] == "frame"
+            and kinds == {"reference"} and img.size <= 1024 * 1024):
+        t0 = time.perf_counter()
+        for g, ms in zip(wl["groups"], models):
+            for (k, method, rings, _), model in zip(g["scales"], ms):
+                R.likelihood_map(img, wl["bins"], model, O.kernel(k.kind, k.kw, k.kh, k.sigma),
+                                 method, 0, rings, 0, threads=threads, budget=1 << 40,
+                                 want_scores=True)
+        public = total_win / (time.perf_counter() - t0)
     return {"value": total_win / proj, "t_build_s": t_build, "scale_rates": rates,
             "threads": threads, "sample_windows": sample_win, "frame_windows": total_win,
             "kind": "reference" if kinds == {"reference"} else "port",
-            "mixed": sorted(kinds)}
+            "mixed": sorted(kinds), "public_api": public}
 
 
 def cpu_model_name():
@@ -793,9 +806,13 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        c = cpu_reference(wl, data, models)
+        c = cpu_reference(wl, data, models, public_api=True)
         cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": c["kind"],
                "sample": cpu_sample_text(wl, c)}
+        if c["public_api"]:
+            cpu["public_api_value"] = c["public_api"]
+            cpu["public_api_sample"] = ("reference likelihood_map per scale (full maps, "
+                                        "tables rebuilt per call, all threads)")
 
     scale_names = [f"{['uniform', 'manhattan', 'chebyshev', 'gauss_cheb', 'euclid_quad', 'exp_l1'][g['scales'][s][0].kind]}"
                    f"{g['scales'][s][0].kw}x{g['scales'][s][0].kh}"
