@@ -313,7 +313,10 @@ size_t pixel_bytes(int format) {
 
 void choose_bands(swg_tables* t) {
   // ~4 row-wide CTAs per SM and table kind
-  const int target = 148 * 4;
+#ifndef SWG_BAND_TARGET
+#define SWG_BAND_TARGET (148 * 2)  // ~2 row-wide CTAs per SM and table kind
+#endif
+  const int target = SWG_BAND_TARGET;
   int nb = (target + t->groups - 1) / t->groups;
   nb = std::max(1, std::min(nb, (t->h + 7) / 8));
   t->band_h = (t->h + nb - 1) / nb;
