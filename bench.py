@@ -14,7 +14,7 @@ full-ring wedding cake), windows 33/65/97.  The other configs:
        (declared quadratic form), windows 45x59/49x65/53x71 on a 256x256
        search region around the previous ground truth           (configs[2])
   c4   3840x2160 RGB, 8x8x8 bins, exponential (decay 15/16 per pixel),
-       windows 25/37/57/85/129, processed in row bands              (configs[3])
+       windows 25/37/57/85/129; one row band per rank             (configs[3])
   c5   2048x2048 u16, 64 bins, Manhattan + Gaussian + Euclidean +
        exponential at windows 17..257 (8 scales each)             (configs[4])
   c5m  c5's Manhattan subset
@@ -450,19 +450,30 @@ def main():
         frame_dev = torch.from_numpy(data.image).cuda()
         g, ms = wl["groups"][0], models[0]
         bins_mode = args.shard == "bins" and world > 1
-        n_bands = 4 if bins_mode else max(4, world)
-        BH, plan = band_plan(H, g["scales"], n_bands)
         full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
                      for k, _, _, _ in g["scales"]]
-        mine = list(range(n_bands)) if bins_mode else \
-            [b for b in range(n_bands) if b % world == rank]
-        if bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e bin ranges)
-            from paper_1705_03524_b200 import dist as D
-            b0, b1 = D.bin_ranges(nb, world)[rank]
-            t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, fmt, wl["bins"],
-                               g["planes"], decay=g.get("decay") or 0.0)
-        else:
-            t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+        # one row band per rank (the whole frame on one GPU: 136 GB of decay
+        # tables, the band halo costs more than it saves); twice as many if a
+        # band's tables do not fit
+        n_bands = int(os.environ.get("SWG_C4_BANDS", 1 if not bins_mode else 4))
+        n_bands = max(n_bands, world) if not bins_mode else n_bands
+        while True:
+            BH, plan = band_plan(H, g["scales"], n_bands)
+            mine = list(range(n_bands)) if bins_mode else \
+                [b for b in range(n_bands) if b % world == rank]
+            try:
+                if bins_mode:  # rank g: bins [b_g, b_g+1) of every band
+                    from paper_1705_03524_b200 import dist as D
+                    b0, b1 = D.bin_ranges(nb, world)[rank]
+                    t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, fmt,
+                                       wl["bins"], g["planes"], decay=g.get("decay") or 0.0)
+                else:
+                    t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+                break
+            except swg.CapacityError:
+                if n_bands >= 64:
+                    raise
+                n_bands *= 2
         for b in mine:
             p0, rows = plan[b]
             reqs, maps, sidx = [], [], []
