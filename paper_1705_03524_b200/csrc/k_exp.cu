@@ -233,11 +233,17 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
       load(i + 1, bn, wn);  // prefetch the next segment
       const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
       __syncwarp();
-      if (bl < r.bins && lane == __ffs(grp) - 1) {
-        double t = h[bl];
-        for (unsigned m = grp; m; m &= m - 1) t = __dadd_rn(t, wv[__ffs(m) - 1]);
-        h[bl] = t;
+      // every group's lowest lane adds its members' weights in lane order;
+      // all groups of the segment advance together through one unrolled
+      // pass (weights broadcast from shared memory, predicated adds)
+      const bool leader = bl < r.bins && lane == __ffs(grp) - 1;
+      double t = leader ? h[bl] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double wj = wv[j];
+        if (leader && ((grp >> j) & 1u)) t = __dadd_rn(t, wj);
       }
+      if (leader) h[bl] = t;
       __syncwarp();
     }
     if (lane == 0) {
