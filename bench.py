@@ -367,6 +367,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--bin-chunks", type=int, default=None,
+                    help="config 4: walk the bins in this many ranges on each GPU, chaining "
+                         "the partial sums (smaller tables stay in L2 between a window's "
+                         "corners); default 8 for config 4, 1 elsewhere")
     ap.add_argument("--shard", default="rows", choices=["rows", "bins"],
                     help="config 4 over N>1 ranks: row bands per rank (default) or every "
                          "band on every rank with bin ranges chained rank to rank")
@@ -487,6 +491,28 @@ def main():
                 sidx.append(si)
             units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
                               g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
+        chunks = args.bin_chunks if args.bin_chunks is not None else 8
+        if chunks > 1 and not bins_mode:
+            # bins walked in `chunks` ranges per step with the running sums
+            # chained range to range on this GPU (the same partial-sum chain as
+            # the multi-GPU bin split): 1/chunks of the decay planes per sweep
+            from dataclasses import replace
+            from paper_1705_03524_b200 import dist as D
+            ranges = D.bin_ranges(nb, chunks)
+            p0 = plan[mine[0]][0]
+            t = ctx.build_bins(frame_dev[p0:p0 + BH], ranges[0][0], ranges[0][1], fmt,
+                               wl["bins"], g["planes"], decay=g.get("decay") or 0.0)
+            for u in units:
+                u["t"] = t
+                bufs = [[torch.empty(tuple(m.shape) + (2,), dtype=torch.float64, device="cuda")
+                         for _ in range(2)] for m in u["maps"]]
+                u["chunks"] = []
+                for c, (b0, _) in enumerate(ranges):
+                    creqs = [replace(r, partial_in=bufs[i][(c - 1) % 2] if c else None,
+                                     partial_out=bufs[i][c % 2] if c < chunks - 1 else None)
+                             for i, r in enumerate(u["reqs"])]
+                    u["chunks"].append((b0 if c else None, creqs))
+                u["bins_per_launch"] = ranges[0][1] - ranges[0][0]
         if bins_mode:
             # running (s, mass) per window: received from rank-1, sent to rank+1
             last = rank == world - 1
@@ -503,6 +529,7 @@ def main():
         tab_w, tab_h = W, BH
     for u in units:
         u["peaks"] = torch.zeros(len(u["reqs"]), 3, dtype=torch.float64, device="cuda")
+        u.setdefault("chunks", [(None, u["reqs"])])
     n_win = sum(m.numel() for u in units for m in u["maps"]) if wl["kind"] != "sequence" else \
         sum(m.numel() for m in units[0]["maps"]) * len(units)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -536,31 +563,37 @@ def main():
             return
         j = 0
         for u in units:
-            if ev:
-                ev[j].record()
-                j += 1
-            u["t"].rebuild(u["src"], u["pitch"])
-            if ev:
-                ev[j].record()
-                j += 1
-            if ev is None and "pin" not in u:
-                # one call for all scales: the library overlaps their sweeps
-                # on its worker streams (the per-scale timing path below
-                # records an event between scales instead)
-                u["t"].likelihood_maps(u["reqs"], scores="none", scores_dev=u["maps"],
-                                       peaks_dev=u["peaks"])
-                continue
-            for i, r in enumerate(u["reqs"]):
-                if "pin" in u and rank > 0:
-                    p2p_recv(u["pin"][i], rank - 1)
-                u["t"].likelihood_maps([r], scores="none",
-                                       scores_dev=None if r.partial_out is not None
-                                       else [u["maps"][i]], peaks_dev=u["peaks"][i])
-                if "pin" in u and rank < world - 1:
-                    p2p_send(u["pout"][i], rank + 1)
+            for c, (b0, creqs) in enumerate(u["chunks"]):
                 if ev:
                     ev[j].record()
                     j += 1
+                if c == 0:
+                    u["t"].rebuild(u["src"], u["pitch"])
+                else:
+                    u["t"].rebuild_bins(b0)
+                if ev:
+                    ev[j].record()
+                    j += 1
+                last = c == len(u["chunks"]) - 1
+                if ev is None and "pin" not in u:
+                    # one call for all scales: the library overlaps their sweeps
+                    # on its worker streams (the per-scale timing path below
+                    # records an event between scales instead)
+                    u["t"].likelihood_maps(creqs, scores="none",
+                                           scores_dev=u["maps"] if last else None,
+                                           peaks_dev=u["peaks"])
+                    continue
+                for i, r in enumerate(creqs):
+                    if "pin" in u and rank > 0:
+                        p2p_recv(u["pin"][i], rank - 1)
+                    u["t"].likelihood_maps([r], scores="none",
+                                           scores_dev=None if r.partial_out is not None
+                                           else [u["maps"][i]], peaks_dev=u["peaks"][i])
+                    if "pin" in u and rank < world - 1:
+                        p2p_send(u["pout"][i], rank + 1)
+                    if ev:
+                        ev[j].record()
+                        j += 1
 
     for _ in range(args.warmup):
         step()
@@ -576,7 +609,7 @@ def main():
             graph.replay()
         torch.cuda.synchronize()
 
-    nev = sum(2 + len(u["reqs"]) for u in units)
+    nev = sum(2 + len(cr) for u in units for _, cr in u["chunks"])
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     clocks = Clocks(local)
     if dist:
@@ -635,13 +668,14 @@ def main():
         j = 0
         for ui, u in enumerate(units):
             e = events[s]
-            build_ms.append(e[j].elapsed_time(e[j + 1]))
-            j += 1
-            for i in range(len(u["reqs"])):
-                sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
-                    e[j].elapsed_time(e[j + 1]))
+            for _, creqs in u["chunks"]:
+                build_ms.append(e[j].elapsed_time(e[j + 1]))
                 j += 1
-            j += 1
+                for i in range(len(creqs)):
+                    sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
+                        e[j].elapsed_time(e[j + 1]))
+                    j += 1
+                j += 1
     total_ms = sum(per_step)
     if dist:
         t = torch.tensor([total_ms], device="cpu" if share else "cuda")
@@ -780,7 +814,8 @@ def main():
         for i, s_ in enumerate(u["sidx"]):
             win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
     dom_win = sum(win_launch[dom]) / len(win_launch[dom])
-    dom_bytes = cells * P * e + 8 * dom_win
+    launch_bins = units[0].get("bins_per_launch", nb)  # bin-range chunks: planes per launch
+    dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -799,7 +834,7 @@ def main():
     rings = g["scales"][si][2]
     corners = {"k_sweep_affine": 20 if k.kind != swg.UNIFORM else 4, "k_sweep_quad": 20,
                "k_sweep_exp": 16}.get(kname, 4 * rings)
-    onchip_bytes = corners * nb * e * dom_win
+    onchip_bytes = corners * launch_bins * e * dom_win
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
     l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
     roofline["onchip"] = {"achieved": onchip_bytes / (dom_ms / 1e3) / 1e12, "peak": l1_peak,

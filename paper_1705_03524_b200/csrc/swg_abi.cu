@@ -772,6 +772,22 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   return SWG_OK;
 }
 
+swg_status swg_tables_rebuild_bins(swg_tables* t, int bin_begin) {
+  ST_TRY(check_tables(t));
+  if (!t->has_fi) return fail(SWG_ERR, "tables were loaded, not built: cannot rebuild");
+  if (bin_begin < 0 || bin_begin + t->bins > t->total_bins)
+    return fail(SWG_ERR_OUT_OF_RANGE, "bin range [%d, %d) of %d", bin_begin,
+                bin_begin + t->bins, t->total_bins);
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  t->bin0 = bin_begin;
+  if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
+  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
+  if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
+  if (t->tdec) ST_TRY(run_build_decay(t));
+  return SWG_OK;
+}
+
 swg_status swg_tables_upload_i64(swg_ctx* c, int w, int h, int bins,
                                  const int64_t* plain, const int64_t* xramp,
                                  const int64_t* yramp, swg_tables** out) {

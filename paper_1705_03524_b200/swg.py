@@ -158,6 +158,7 @@ def lib():
                                   C.POINTER(vp)],
         "swg_tables_bin_range": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "swg_tables_rebuild": [vp, vp, C.c_int, C.c_size_t],
+        "swg_tables_rebuild_bins": [vp, C.c_int],
         "swg_tables_upload_i64": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)],
         "swg_tables_destroy": [vp],
         "swg_tables_info": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -371,6 +372,12 @@ class Tables:
         is_dev = 0 if isinstance(pixels, np.ndarray) else int(pixels.is_cuda)
         self._keep = pixels
         _check(lib().swg_tables_rebuild(self._h, _ptr(pixels), is_dev, pitch))
+
+    def rebuild_bins(self, bin_begin):
+        """Rebuild for bins [bin_begin, bin_begin + bins) from the resident
+        feature image (bin-range tables)."""
+        _check(lib().swg_tables_rebuild_bins(self._h, bin_begin))
+        self.bin_begin, self.bin_end = bin_begin, bin_begin + self.bins
 
     def export_i64(self, kind=TABLE_PLAIN, b0=0, b1=None):
         b1 = self.bins if b1 is None else b1
