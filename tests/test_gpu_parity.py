@@ -839,3 +839,36 @@ def test_quadratic_tall_image(ctx, oracle):
     assert (got == want).all()
     with pytest.raises(swg.SizeError):
         t.export_i64(0)
+
+
+def test_bin_range_chain_rebuild_bins(ctx, oracle):
+    """One table set walks the bin ranges (swg_tables_rebuild_bins from the
+    resident feature image): the chain's last map == the full table's map."""
+    import torch
+    img = oracle.random_gray(90, 64, 21)
+    bins, d = 24, 0.9375
+    fi = oracle.quantize_gray8(img, bins)
+    for planes, k, method, rings in ((swg.PLANES_DECAY, K(swg.EXP_L1, 11, 11, d), swg.SWIH, 1),
+                                     (swg.PLANES_AFFINE, K(swg.MANHATTAN, 9, 13), swg.SWIH, 1),
+                                     (swg.PLANES_PLAIN, K(swg.GAUSS_CHEB, 13, 13, 0.5), swg.CAKE, 7)):
+        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+        om = O.CAKE if method == swg.CAKE else (O.BRUTE if k.kind == swg.EXP_L1 else O.SWIH)
+        model = oracle.target_model(fi[10:10 + k.kh, 20:20 + k.kw].copy(), bins, ok, om, rings)
+        full = (ctx.build_decay(img, d, swg.FMT_GRAY8, bins) if planes == swg.PLANES_DECAY
+                else ctx.build(img, swg.FMT_GRAY8, bins, planes))
+        want, wpk = full.likelihood_map(k, model, method, rings=rings)
+        t = ctx.build_bins(img, 0, 8, swg.FMT_GRAY8, bins, planes, decay=d)
+        shape = t.map_shape(k) + (2,)
+        bufs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+        for c, b0 in enumerate((0, 8, 16)):
+            if c:
+                t.rebuild_bins(b0)
+                assert (t.bin_begin, t.bin_end) == (b0, b0 + 8)
+            last = c == 2
+            r = swg.MapRequest(k, model, method, rings=rings,
+                               partial_in=bufs[(c - 1) % 2] if c else None,
+                               partial_out=None if last else bufs[c % 2])
+            maps, pks = t.likelihood_maps([r], scores="host" if last else "none")
+        assert (maps[0] == want).all() and pks[0] == wpk, planes
+    with pytest.raises(swg.OutOfRangeError):
+        t.rebuild_bins(20)
