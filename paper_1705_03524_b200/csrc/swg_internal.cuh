@@ -36,7 +36,10 @@ inline size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
 // Columns per build thread: 8 from 1024 wide (half the threads of a
 // row-wide CTA, two CTAs per SM; measured faster at 2048 than 4 columns).
-inline int choose_cpt(int w) { return w <= 1024 ? 4 : 8; }
+#ifndef SWG_CPT8_FROM
+#define SWG_CPT8_FROM 1024
+#endif
+inline int choose_cpt(int w) { return w < SWG_CPT8_FROM ? 4 : 8; }
 
 // Row pitch in records (room for the straddling last build thread).
 inline size_t record_pitch(int w) { return round_up((size_t)w + 1 + 8, 4); }
