@@ -291,7 +291,12 @@ swg_status swg_map_peak(swg_ctx* ctx, const double* scores, int map_width,
  *   scores_dev[i]    device array (same size), or NULL
  *   peaks_host[i]    filled when peaks_host != NULL
  *   peaks_dev        device array of n swg_peak, or NULL
- * With only device outputs the call is asynchronous on the context stream.
+ * With only device outputs the call is asynchronous on the context stream:
+ * the requests fork from it onto the context's worker streams (their sweeps
+ * overlap) and join back into it before the call returns, so work queued on
+ * the context stream afterwards sees every output (graph-capturable).  With
+ * host maps the requests run in order and each map is copied while the next
+ * one sweeps; the call returns when the host outputs are filled.
  * Any of the per-request pointer arrays may itself be NULL. */
 swg_status swg_likelihood_maps(swg_tables* t, int n,
                                const swg_map_request* reqs,
