@@ -872,3 +872,20 @@ def test_bin_range_chain_rebuild_bins(ctx, oracle):
         assert (maps[0] == want).all() and pks[0] == wpk, planes
     with pytest.raises(swg.OutOfRangeError):
         t.rebuild_bins(20)
+
+
+def test_cake16_wide_ring0_both_sims(ctx, oracle):
+    """257x257 full-ring cake on 16-bit planes: ring 0's box holds >= 2^16
+    pixels and is recovered exactly from ring 1 (wide ring 0)."""
+    img = oracle.random_gray(300, 270, 31)
+    bins = 6
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    k = K(swg.GAUSS_CHEB, 257, 257, 0.5)
+    ok = O.kernel(O.GAUSS_CHEB, 257, 257, 0.5)
+    model = oracle.target_model(fi[5:262, 20:277].copy(), bins, ok, O.CAKE, 129)
+    for sim in (swg.BHATTACHARYYA, swg.INTERSECTION):
+        want = oracle.likelihood_map(fi, bins, model, ok, O.CAKE, sim, rings=129)
+        got, pk = t.likelihood_map(k, model, swg.CAKE, sim, rings=129)
+        assert (got == want).all(), sim
+        assert pk == oracle.peak(want, 128, 128)
