@@ -56,16 +56,20 @@ __device__ __forceinline__ double2 ldd2(const char* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// One lane per window, 32 windows of one map row per warp (CTA tile 32 x 8):
+// for each of an octet's four bin pairs a warp's corner load reads 32
+// consecutive 16-byte records of one plane (512 contiguous bytes), and the
+// lane holds all 8 bins of the octet, so the ordered sums need no shuffles.
 template <int SIM>
 #ifndef SWG_EXP_MINB
-#define SWG_EXP_MINB 3  // 80 registers: 3 CTAs per SM (latency-bound DRAM reads)
+#define SWG_EXP_MINB 3  // <= 80 registers: 3 CTAs per SM (latency-bound reads)
 #endif
 __global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const SweepArgs a,
                                                                          const ExpSweep e) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int tx, ty;
   sweep_tile(a.sc_tiles, tx, ty);
-  const int u0 = tx * kSweepTileX + (lane >> 1);
+  const int u0 = tx * 32 + lane;
   const int r0 = ty * kSweepTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
@@ -82,44 +86,24 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const
   }
   const size_t pair_bytes = 4 * a.plane_stride * 16;
 
-  // lane `half` of octet g: bins 8g + 4*half + {0,1} (pair 4g+2h) and
-  // {2,3} (pair 4g+2h+1); a half-warp's 16 windows read 256 contiguous bytes
-  auto octet = [&](int g, double (&out)[4]) {
-    const char* b0 = reinterpret_cast<const char*>(a.tab) + (size_t)(4 * g + 2 * half) * pair_bytes;
-    const char* b1 = b0 + pair_bytes;
+  // the 8 bins of octet g: pair q holds bins 8g + 2q, 8g + 2q + 1
+  auto octet = [&](int g, double (&out)[kOct]) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) out[k] = 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const char* base = reinterpret_cast<const char*>(a.tab) + (size_t)(4 * g + q) * pair_bytes;
+      double o0 = 0.0, o1 = 0.0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // orientation / quadrant
-      const double k0 = e.coef[4 * k], k1 = e.coef[4 * k + 1], k2 = e.coef[4 * k + 2],
-                   k3 = e.coef[4 * k + 3];
-      const size_t o0 = cen[k] + e.off[4 * k], o1 = cen[k] + e.off[4 * k + 1];
-      const size_t o2 = cen[k] + e.off[4 * k + 2], o3 = cen[k] + e.off[4 * k + 3];
-      const double2 p0 = ldd2(b0 + o0), p1 = ldd2(b0 + o1), p2 = ldd2(b0 + o2), p3 = ldd2(b0 + o3);
-      const double2 q0 = ldd2(b1 + o0), q1 = ldd2(b1 + o1), q2 = ldd2(b1 + o2), q3 = ldd2(b1 + o3);
-      out[0] += k0 * p0.x + k1 * p1.x + k2 * p2.x + k3 * p3.x;
-      out[1] += k0 * p0.y + k1 * p1.y + k2 * p2.y + k3 * p3.y;
-      out[2] += k0 * q0.x + k1 * q1.x + k2 * q2.x + k3 * q3.x;
-      out[3] += k0 * q0.y + k1 * q1.y + k2 * q2.y + k3 * q3.y;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) out[k] = out[k] > e.snap ? out[k] : 0.0;  // rounding floor
-  };
-
-  auto add_oct = [&](const double (&val)[4], const double (&term)[4], double& mass, double& s,
-                     bool with_mass, bool with_s) {
-    double pv[4], pt[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      pv[k] = __shfl_xor_sync(0xFFFFFFFFu, val[k], 1);
-      pt[k] = __shfl_xor_sync(0xFFFFFFFFu, term[k], 1);
-    }
-#pragma unroll
-    for (int j = 0; j < kOct; ++j) {
-      const bool own = (j >> 2) == half;
-      const double vv = own ? val[j & 3] : pv[j & 3], tt = own ? term[j & 3] : pt[j & 3];
-      if (with_mass) mass += vv;
-      if (with_s && vv != 0.0) s += tt;
+      for (int k = 0; k < 4; ++k) {  // orientation / quadrant
+        const double k0 = e.coef[4 * k], k1 = e.coef[4 * k + 1], k2 = e.coef[4 * k + 2],
+                     k3 = e.coef[4 * k + 3];
+        const char* w = base + cen[k];
+        const double2 p0 = ldd2(w + e.off[4 * k]), p1 = ldd2(w + e.off[4 * k + 1]);
+        const double2 p2 = ldd2(w + e.off[4 * k + 2]), p3 = ldd2(w + e.off[4 * k + 3]);
+        o0 += k0 * p0.x + k1 * p1.x + k2 * p2.x + k3 * p3.x;
+        o1 += k0 * p0.y + k1 * p1.y + k2 * p2.y + k3 * p3.y;
+      }
+      out[2 * q] = o0 > e.snap ? o0 : 0.0;  // rounding floor of an empty bin
+      out[2 * q + 1] = o1 > e.snap ? o1 : 0.0;
     }
   };
 
@@ -131,36 +115,38 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const
   }
   if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
     for (int g = 0; g < a.groups; ++g) {
-      double out[4], term[4];
+      double out[kOct];
       octet(g, out);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) term[k] = sqrt(a.model[g * kOct + half * 4 + k] * out[k]);
-      add_oct(out, term, mass, s, true, true);
+      for (int j = 0; j < kOct; ++j) {
+        mass += out[j];
+        if (out[j] != 0.0) s += sqrt(a.model[g * kOct + j] * out[j]);
+      }
     }
   } else {
-    double unused = 0.0;
     for (int g = 0; g < a.groups; ++g) {
-      double out[4];
-      octet(g, out);
-      add_oct(out, out, mass, unused, true, false);
-    }
-    for (int g = 0; g < a.groups; ++g) {
-      double out[4], term[4];
+      double out[kOct];
       octet(g, out);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) term[k] = fmin(a.model[g * kOct + half * 4 + k], out[k] / mass);
-      add_oct(out, term, unused, s, false, true);
+      for (int j = 0; j < kOct; ++j) mass += out[j];
+    }
+    for (int g = 0; g < a.groups; ++g) {
+      double out[kOct];
+      octet(g, out);
+#pragma unroll
+      for (int j = 0; j < kOct; ++j)
+        if (out[j] != 0.0) s += fmin(a.model[g * kOct + j], out[j] / mass);
     }
   }
   if (a.pout) {
-    if (active && half == 0) a.pout[widx] = make_double2(s, mass);
+    if (active) a.pout[widx] = make_double2(s, mass);
     s = -2.0;
   } else {
     if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = mass > 0.0 ? s / sqrt(mass) : 0.0;
     s = clamp01e(s);
-    if (active && half == 0) a.scores[widx] = s;
+    if (active) a.scores[widx] = s;
   }
-  block_peak_e(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
+  block_peak_e(active ? s : -2.0, (long long)v * a.mw + u,
                a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 

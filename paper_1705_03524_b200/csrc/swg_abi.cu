@@ -1380,10 +1380,11 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     if (engine[i] == kBrute)
       grid[i] = dim3((unsigned)((mws[i] + kBruteThreads - 1) / kBruteThreads),
                      (unsigned)std::max(rows, 1));
-    else
-      grid[i] = dim3((unsigned)((mws[i] + (engine[i] == kCake16 ? 32 : kSweepTileX) - 1) /
-                                (engine[i] == kCake16 ? 32 : kSweepTileX)),
+    else {
+      const int tw = (engine[i] == kCake16 || engine[i] == kExp64) ? 32 : kSweepTileX;
+      grid[i] = dim3((unsigned)((mws[i] + tw - 1) / tw),
                      (unsigned)std::max((rows + kSweepTileY - 1) / kSweepTileY, 1));
+    }
     poff[i] = ptot;
     ptot += (size_t)grid[i].x * grid[i].y;
   }
@@ -1465,8 +1466,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
           const double span = 2.0 * a.hy + 2 + kSweepTileY;
           if (span * (t->w + 1) * cell > budget) {
             const double sw = budget / (span * cell) - (2.0 * a.hx + 2);
-            if (sw >= 2 * kSweepTileX && (sw + 2.0 * a.hx + 2) / sw < 1.7)
-              a.sc_tiles = std::max(1, (int)(sw / kSweepTileX));
+            const int tw = engine[i] == kExp64 ? 32 : kSweepTileX;  // windows per tile
+            if (sw >= 2 * tw && (sw + 2.0 * a.hx + 2) / sw < 1.7)
+              a.sc_tiles = std::max(1, (int)(sw / tw));
           }
         }
       }
