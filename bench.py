@@ -102,7 +102,8 @@ def workload(name):
                          "windows 25/37/57/85/129, row bands",
                     kind="bands", gen=synth.config4, fmt=swg.FMT_RGB8, bins=8, nbins=512,
                     scaling="strong",
-                    groups=[dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, scales=scales)])
+                    groups=[dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, bin_chunks=8,
+                                 scales=scales)])
     scales = []
     for i, s in enumerate((32, 64, 96)):
         kw = synth.odd_window(s)
@@ -412,7 +413,24 @@ def main():
     models = make_models(ctx, wl, data)
     fmt, nb = wl["fmt"], wl["nbins"]
 
+    bins_mode = args.shard == "bins" and world > 1
+
+    def group_chunks(g):
+        """Bin ranges one GPU walks for this group (1: all bins at once)."""
+        if bins_mode:
+            return 1
+        if args.bin_chunks is not None:
+            return args.bin_chunks
+        if g.get("decay") and os.environ.get("SWG_DECAY_CHUNKS"):  # tuning override
+            return int(os.environ["SWG_DECAY_CHUNKS"])
+        return g.get("bin_chunks", 1)
+
     def new_tables(g, src, pitch=0):
+        if group_chunks(g) > 1:  # the first bin range; the rest via rebuild_bins
+            from paper_1705_03524_b200 import dist as D
+            b0, b1 = D.bin_ranges(nb, group_chunks(g))[0]
+            return ctx.build_bins(src, b0, b1, fmt, wl["bins"], g["planes"],
+                                  decay=g.get("decay") or 0.0, pitch=pitch)
         if g.get("decay"):
             return ctx.build_decay(src, g["decay"], fmt, wl["bins"], pitch=pitch)
         return ctx.build(src, fmt, wl["bins"], g["planes"], pitch=pitch)
@@ -453,7 +471,6 @@ def main():
         H, W = data.image.shape[:2]
         frame_dev = torch.from_numpy(data.image).cuda()
         g, ms = wl["groups"][0], models[0]
-        bins_mode = args.shard == "bins" and world > 1
         full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
                      for k, _, _, _ in g["scales"]]
         # one row band per rank (the whole frame on one GPU: 136 GB of decay
@@ -491,28 +508,6 @@ def main():
                 sidx.append(si)
             units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
                               g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
-        chunks = args.bin_chunks if args.bin_chunks is not None else 8
-        if chunks > 1 and not bins_mode:
-            # bins walked in `chunks` ranges per step with the running sums
-            # chained range to range on this GPU (the same partial-sum chain as
-            # the multi-GPU bin split): 1/chunks of the decay planes per sweep
-            from dataclasses import replace
-            from paper_1705_03524_b200 import dist as D
-            ranges = D.bin_ranges(nb, chunks)
-            p0 = plan[mine[0]][0]
-            t = ctx.build_bins(frame_dev[p0:p0 + BH], ranges[0][0], ranges[0][1], fmt,
-                               wl["bins"], g["planes"], decay=g.get("decay") or 0.0)
-            for u in units:
-                u["t"] = t
-                bufs = [[torch.empty(tuple(m.shape) + (2,), dtype=torch.float64, device="cuda")
-                         for _ in range(2)] for m in u["maps"]]
-                u["chunks"] = []
-                for c, (b0, _) in enumerate(ranges):
-                    creqs = [replace(r, partial_in=bufs[i][(c - 1) % 2] if c else None,
-                                     partial_out=bufs[i][c % 2] if c < chunks - 1 else None)
-                             for i, r in enumerate(u["reqs"])]
-                    u["chunks"].append((b0 if c else None, creqs))
-                u["bins_per_launch"] = ranges[0][1] - ranges[0][0]
         if bins_mode:
             # running (s, mass) per window: received from rank-1, sent to rank+1
             last = rank == world - 1
@@ -529,6 +524,24 @@ def main():
         tab_w, tab_h = W, BH
     for u in units:
         u["peaks"] = torch.zeros(len(u["reqs"]), 3, dtype=torch.float64, device="cuda")
+        nchunk = group_chunks(wl["groups"][u["g"]])
+        if nchunk > 1:
+            # bins walked in `nchunk` ranges per step with the running sums
+            # chained range to range on this GPU (the partial-sum chain of the
+            # multi-GPU bin split): 1/nchunk of the decay planes per sweep, so a
+            # window's corner rows stay in L2
+            from dataclasses import replace
+            from paper_1705_03524_b200 import dist as D
+            ranges = D.bin_ranges(nb, nchunk)
+            bufs = [[torch.empty(tuple(m.shape) + (2,), dtype=torch.float64, device="cuda")
+                     for _ in range(2)] for m in u["maps"]]
+            u["chunks"] = []
+            for c, (b0, _) in enumerate(ranges):
+                creqs = [replace(r, partial_in=bufs[i][(c - 1) % 2] if c else None,
+                                 partial_out=bufs[i][c % 2] if c < nchunk - 1 else None)
+                         for i, r in enumerate(u["reqs"])]
+                u["chunks"].append((b0, creqs))
+            u["bins_per_launch"] = ranges[0][1] - ranges[0][0]
         u.setdefault("chunks", [(None, u["reqs"])])
     n_win = sum(m.numel() for u in units for m in u["maps"]) if wl["kind"] != "sequence" else \
         sum(m.numel() for m in units[0]["maps"]) * len(units)
@@ -567,10 +580,10 @@ def main():
                 if ev:
                     ev[j].record()
                     j += 1
-                if c == 0:
+                if len(u["chunks"]) == 1:
                     u["t"].rebuild(u["src"], u["pitch"])
-                else:
-                    u["t"].rebuild_bins(b0)
+                else:  # bin-range walk: the new frame with the first range, then ranges
+                    u["t"].rebuild_bins(b0, u["src"] if c == 0 else None, u["pitch"])
                 if ev:
                     ev[j].record()
                     j += 1
@@ -747,22 +760,33 @@ def main():
             calls = []
             maps_pin = []
             for u in units:
-                creqs, keep = swg.Tables._creqs(u["reqs"], nb)
                 mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
                 maps_pin.append(mp)
                 hp = (C.c_void_p * len(mp))(*[m.array.ctypes.data for m in mp])
                 pk = (Peak * len(u["reqs"]))()
                 src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
-                calls.append((u["t"], src, creqs, keep, hp, pk, len(u["reqs"])))
+                # per bin range (one range unless the bins are walked in chunks):
+                # rebuild (upload the frame on the first), requests; host maps
+                # and peaks from the last range
+                for c, (b0, cr) in enumerate(u["chunks"]):
+                    creqs, keep = swg.Tables._creqs(cr, nb)
+                    last = c == len(u["chunks"]) - 1
+                    calls.append((u["t"], src if c == 0 else None, b0,
+                                  len(u["chunks"]) > 1, creqs, keep,
+                                  hp if last else None, pk, len(cr)))
                 h2d += u["h2d"]
                 d2h += sum(m.nbytes for m in mp) + C.sizeof(pk)
 
             def e2e_step():
-                for t, src, creqs, _k, hp, pk, n in calls:
-                    _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
-                    _check(lib().swg_likelihood_maps(t._h, n, C.addressof(creqs),
-                                                     C.addressof(hp), None, C.addressof(pk),
-                                                     None))
+                for t, src, b0, walk, creqs, _k, hp, pk, n in calls:
+                    if walk:  # bin ranges: the frame with the first range, then ranges
+                        _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
+                    else:
+                        _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
+                    _check(lib().swg_likelihood_maps(
+                        t._h, n, C.addressof(creqs),
+                        C.addressof(hp) if hp is not None else None, None, C.addressof(pk),
+                        None))
 
             def check():
                 for u, mp in zip(units, maps_pin):
@@ -814,7 +838,7 @@ def main():
         for i, s_ in enumerate(u["sidx"]):
             win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
     dom_win = sum(win_launch[dom]) / len(win_launch[dom])
-    launch_bins = units[0].get("bins_per_launch", nb)  # bin-range chunks: planes per launch
+    launch_bins = next((u.get("bins_per_launch", nb) for u in units if u["g"] == gi), nb)
     dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")

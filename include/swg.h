@@ -204,10 +204,13 @@ swg_status swg_tables_build_bins(swg_ctx* ctx, const void* pixels, int is_device
                                  int bin_end, size_t memory_budget, swg_tables** out);
 swg_status swg_tables_bin_range(const swg_tables* t, int* bin_begin, int* bin_end,
                                 int* total_bins);
-/* Rebuild every plane set from the resident feature image for the bin range
- * [bin_begin, bin_begin + bins) of the same width (no upload, no quantise):
- * one GPU walks a large bin set range by range, chaining partial sums. */
-swg_status swg_tables_rebuild_bins(swg_tables* t, int bin_begin);
+/* Rebuild every plane set for the bin range [bin_begin, bin_begin + bins)
+ * of the same width: from `pixels` (uploaded and quantised as in
+ * swg_tables_rebuild) or, with pixels = NULL, from the resident feature
+ * image -- one GPU walks a large bin set range by range, chaining partial
+ * sums.  (swg_tables_rebuild keeps the current range.) */
+swg_status swg_tables_rebuild_bins(swg_tables* t, const void* pixels, int is_device,
+                                   size_t pitch_bytes, int bin_begin);
 /* Re-run quantise + build for a new frame of the same geometry into the
  * same device buffers (no allocation; stream ordered, asynchronous). */
 swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,

@@ -772,14 +772,17 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   return SWG_OK;
 }
 
-swg_status swg_tables_rebuild_bins(swg_tables* t, int bin_begin) {
+swg_status swg_tables_rebuild_bins(swg_tables* t, const void* pixels, int is_device,
+                                   size_t pitch_bytes, int bin_begin) {
   ST_TRY(check_tables(t));
-  if (!t->has_fi) return fail(SWG_ERR, "tables were loaded, not built: cannot rebuild");
+  if (!t->fi || (!pixels && !t->has_fi))
+    return fail(SWG_ERR, "tables were loaded, not built: cannot rebuild");
   if (bin_begin < 0 || bin_begin + t->bins > t->total_bins)
     return fail(SWG_ERR_OUT_OF_RANGE, "bin range [%d, %d) of %d", bin_begin,
                 bin_begin + t->bins, t->total_bins);
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
+  if (pixels) ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
   t->bin0 = bin_begin;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));

@@ -158,7 +158,7 @@ def lib():
                                   C.POINTER(vp)],
         "swg_tables_bin_range": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "swg_tables_rebuild": [vp, vp, C.c_int, C.c_size_t],
-        "swg_tables_rebuild_bins": [vp, C.c_int],
+        "swg_tables_rebuild_bins": [vp, vp, C.c_int, C.c_size_t, C.c_int],
         "swg_tables_upload_i64": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)],
         "swg_tables_destroy": [vp],
         "swg_tables_info": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -373,10 +373,14 @@ class Tables:
         self._keep = pixels
         _check(lib().swg_tables_rebuild(self._h, _ptr(pixels), is_dev, pitch))
 
-    def rebuild_bins(self, bin_begin):
-        """Rebuild for bins [bin_begin, bin_begin + bins) from the resident
-        feature image (bin-range tables)."""
-        _check(lib().swg_tables_rebuild_bins(self._h, bin_begin))
+    def rebuild_bins(self, bin_begin, pixels=None, pitch=0):
+        """Rebuild for bins [bin_begin, bin_begin + bins): from `pixels` (a
+        new frame) or, by default, from the resident feature image."""
+        is_dev = 0 if pixels is None or isinstance(pixels, np.ndarray) else int(pixels.is_cuda)
+        if pixels is not None:
+            self._keep = pixels
+        _check(lib().swg_tables_rebuild_bins(self._h, _ptr(pixels) if pixels is not None
+                                             else None, is_dev, pitch, bin_begin))
         self.bin_begin, self.bin_end = bin_begin, bin_begin + self.bins
 
     def export_i64(self, kind=TABLE_PLAIN, b0=0, b1=None):

@@ -857,19 +857,20 @@ def test_bin_range_chain_rebuild_bins(ctx, oracle):
         full = (ctx.build_decay(img, d, swg.FMT_GRAY8, bins) if planes == swg.PLANES_DECAY
                 else ctx.build(img, swg.FMT_GRAY8, bins, planes))
         want, wpk = full.likelihood_map(k, model, method, rings=rings)
-        t = ctx.build_bins(img, 0, 8, swg.FMT_GRAY8, bins, planes, decay=d)
+        t = ctx.build_bins(oracle.random_gray(90, 64, 5), 0, 8, swg.FMT_GRAY8, bins, planes,
+                           decay=d)  # another frame first: the walk uploads the real one
         shape = t.map_shape(k) + (2,)
         bufs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
-        for c, b0 in enumerate((0, 8, 16)):
-            if c:
-                t.rebuild_bins(b0)
+        for rep in range(2):  # two walks: each starts from a fresh upload at range 0
+            for c, b0 in enumerate((0, 8, 16)):
+                t.rebuild_bins(b0, img if c == 0 else None)
                 assert (t.bin_begin, t.bin_end) == (b0, b0 + 8)
-            last = c == 2
-            r = swg.MapRequest(k, model, method, rings=rings,
-                               partial_in=bufs[(c - 1) % 2] if c else None,
-                               partial_out=None if last else bufs[c % 2])
-            maps, pks = t.likelihood_maps([r], scores="host" if last else "none")
-        assert (maps[0] == want).all() and pks[0] == wpk, planes
+                last = c == 2
+                r = swg.MapRequest(k, model, method, rings=rings,
+                                   partial_in=bufs[(c - 1) % 2] if c else None,
+                                   partial_out=None if last else bufs[c % 2])
+                maps, pks = t.likelihood_maps([r], scores="host" if last else "none")
+            assert (maps[0] == want).all() and pks[0] == wpk, (planes, rep)
     with pytest.raises(swg.OutOfRangeError):
         t.rebuild_bins(20)
 
