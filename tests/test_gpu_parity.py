@@ -890,3 +890,51 @@ def test_cake16_wide_ring0_both_sims(ctx, oracle):
         got, pk = t.likelihood_map(k, model, swg.CAKE, sim, rings=129)
         assert (got == want).all(), sim
         assert pk == oracle.peak(want, 128, 128)
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303])
+def test_random_configurations_all_engines(ctx, oracle, seed):
+    """Randomised shapes, bin counts, kernel sizes, row ranges and both
+    similarities through every table sweep, against the oracle (bit-exact;
+    the exponential map within 1e-4 with an exact peak)."""
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(40, 130)), int(rng.integers(40, 130))
+    bins = int(rng.choice([3, 8, 13, 24]))
+    img = oracle.random_gray(w, h, seed)
+    fi = oracle.quantize_gray8(img, bins)
+    d = float(rng.choice([0.75, 0.875, 0.9375]))
+    tabs = {swg.PLANES_AFFINE: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_AFFINE),
+            swg.PLANES_PLAIN: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN),
+            swg.PLANES_QUADRATIC: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC),
+            swg.PLANES_DECAY: ctx.build_decay(img, d, swg.FMT_GRAY8, bins)}
+    for trial in range(6):
+        kw = 2 * int(rng.integers(0, min(w, h) // 2 - 1)) + 1
+        kh = 2 * int(rng.integers(0, min(w, h) // 2 - 1)) + 1
+        sq = min(kw, kh)
+        cases = [(K(swg.MANHATTAN, kw, kh), swg.SWIH, 1, swg.PLANES_AFFINE, O.SWIH, True),
+                 (K(swg.UNIFORM, kw, kh), swg.SWIH, 1, swg.PLANES_PLAIN, O.SWIH, True),
+                 (K(swg.GAUSS_CHEB, sq, sq, 0.5), swg.CAKE, sq // 2 + 1, swg.PLANES_PLAIN,
+                  O.CAKE, True),
+                 (K(swg.GAUSS_CHEB, kw, kh, 0.5), swg.CAKE, min(kw, kh) // 2 + 1,
+                  swg.PLANES_AFFINE, O.CAKE, True),
+                 (K(swg.EUCLID_QUAD, kw, kh), swg.SWIH, 1, swg.PLANES_QUADRATIC, O.BRUTE, True),
+                 (K(swg.EXP_L1, kw, kh, d), swg.SWIH, 1, swg.PLANES_DECAY, O.BRUTE, False),
+                 (K(swg.GAUSS_CHEB, kw, kh, 0.5), swg.BRUTE, 1, swg.PLANES_PLAIN, O.BRUTE, True)]
+        mh = h - kh + 1
+        r0 = int(rng.integers(0, mh))
+        rows = (r0, int(rng.integers(r0 + 1, mh + 1)))
+        for k, method, rings, planes, om, exact in cases:
+            ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+            y0, x0 = int(rng.integers(0, h - k.kh + 1)), int(rng.integers(0, w - k.kw + 1))
+            model = oracle.target_model(fi[y0:y0 + k.kh, x0:x0 + k.kw].copy(), bins, ok, om,
+                                        rings)
+            sim = int(rng.integers(0, 2))
+            want = oracle.likelihood_map(fi, bins, model, ok, om, sim, rings=rings, rows=rows)
+            got, pk = tabs[planes].likelihood_map(k, model, method, sim, rings, rows=rows)
+            if exact:
+                assert (got == want).all(), (seed, trial, k.kind, kw, kh, method, sim, rows)
+            else:
+                np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
+            u, v = pk[0], pk[1] - rows[0]
+            assert pk[4] == want.max() and want[v, u] == want.max()
+            assert (v, u) == tuple(np.unravel_index(np.argmax(want), want.shape))
