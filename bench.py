@@ -372,6 +372,9 @@ def main():
                     help="config 4: walk the bins in this many ranges on each GPU, chaining "
                          "the partial sums (smaller tables stay in L2 between a window's "
                          "corners); default 8 for config 4, 1 elsewhere")
+    ap.add_argument("--p2p", default="peer", choices=["peer", "nccl"],
+                    help="--shard bins: running sums written by the sweep straight into the "
+                         "next rank's buffer (peer memory), or sent with NCCL")
     ap.add_argument("--shard", default="rows", choices=["rows", "bins"],
                     help="config 4 over N>1 ranks: row bands per rank (default) or every "
                          "band on every rank with bin ranges chained rank to rank")
@@ -508,7 +511,35 @@ def main():
                 sidx.append(si)
             units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
                               g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
-        if bins_mode:
+        if bins_mode and args.p2p == "peer":
+            # running (s, mass) per window written by rank g's sweep STRAIGHT
+            # into rank g+1's input buffer (peer memory mapped with an IPC
+            # handle; NVLink stores from the kernel's epilogue); only a 4-byte
+            # token per request goes through the process group, stream-ordered
+            # behind the kernel
+            last = rank == world - 1
+            mine_h = []
+            for u in units:
+                u["pin"] = []
+                for m in u["maps"]:
+                    buf = swg.device_alloc(m.numel() * 16) if rank > 0 else None
+                    u["pin"].append(buf)
+                    mine_h.append(swg.ipc_export(buf) if buf else None)
+            every = [None] * world
+            dist.all_gather_object(every, mine_h)
+            k = 0
+            for u in units:
+                u["pout"] = []
+                for i, r in enumerate(u["reqs"]):
+                    peer = None if last else swg.ipc_import(every[rank + 1][k])
+                    u["pout"].append(peer)
+                    r.partial_in, r.partial_out = u["pin"][i], peer
+                    k += 1
+                if not last:
+                    u["maps"] = [m[:0] for m in u["maps"]]  # no scores off the last rank
+                u["token"] = torch.zeros(1, dtype=torch.float32,
+                                         device="cpu" if share else "cuda")
+        elif bins_mode:
             # running (s, mass) per window: received from rank-1, sent to rank+1
             last = rank == world - 1
             for u in units:
@@ -598,12 +629,20 @@ def main():
                     continue
                 for i, r in enumerate(creqs):
                     if "pin" in u and rank > 0:
-                        p2p_recv(u["pin"][i], rank - 1)
+                        if "token" in u:  # the sums are already in u["pin"][i]
+                            p2p_recv(u["token"], rank - 1)
+                        else:
+                            p2p_recv(u["pin"][i], rank - 1)
                     u["t"].likelihood_maps([r], scores="none",
                                            scores_dev=None if r.partial_out is not None
                                            else [u["maps"][i]], peaks_dev=u["peaks"][i])
                     if "pin" in u and rank < world - 1:
-                        p2p_send(u["pout"][i], rank + 1)
+                        if "token" in u:  # stream-ordered behind the sweep's peer stores
+                            if share:
+                                torch.cuda.synchronize()
+                            p2p_send(u["token"], rank + 1)
+                        else:
+                            p2p_send(u["pout"][i], rank + 1)
                     if ev:
                         ev[j].record()
                         j += 1

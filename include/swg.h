@@ -159,6 +159,17 @@ swg_status swg_device_count(int* n);
 /* Page-locked host memory for asynchronous host<->device copies. */
 swg_status swg_host_alloc(size_t bytes, void** out);
 swg_status swg_host_free(void* p);
+/* Peer memory between processes (one process per GPU): export a device
+ * allocation's handle, map another process's allocation into this one.  A
+ * mapped pointer can be given to a kernel output directly -- e.g. as
+ * swg_map_request.partial_out, so a bin-range sweep writes its running sums
+ * straight into the next GPU's input buffer over NVLink. */
+#define SWG_IPC_HANDLE_BYTES 64
+swg_status swg_device_alloc(size_t bytes, void** out);  /* exportable (whole allocation) */
+swg_status swg_device_free(void* p);
+swg_status swg_ipc_export(const void* dev_ptr, unsigned char* handle);
+swg_status swg_ipc_import(const unsigned char* handle, void** dev_ptr);
+swg_status swg_ipc_close(void* dev_ptr);
 
 /* ---- context --------------------------------------------------------- */
 /* Contexts are reference counted by the tables built on them: destroying a

@@ -612,6 +612,45 @@ swg_status swg_host_free(void* p) {
   return SWG_OK;
 }
 
+swg_status swg_device_alloc(size_t bytes, void** out) {
+  if (!out) return fail(SWG_ERR_ARG, "NULL out");
+  cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g_required = bytes;
+    return fail(SWG_ERR_CAPACITY, "device allocation of %zu bytes: %s", bytes,
+                cudaGetErrorString(e));
+  }
+  return SWG_OK;
+}
+
+swg_status swg_device_free(void* p) {
+  if (p) CUDA_TRY(cudaFree(p));
+  return SWG_OK;
+}
+
+swg_status swg_ipc_export(const void* dev_ptr, unsigned char* handle) {
+  if (!dev_ptr || !handle) return fail(SWG_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == SWG_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  return SWG_OK;
+}
+
+swg_status swg_ipc_import(const unsigned char* handle, void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(SWG_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SWG_OK;
+}
+
+swg_status swg_ipc_close(void* dev_ptr) {
+  if (dev_ptr) CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return SWG_OK;
+}
+
 swg_status swg_ctx_synchronize(swg_ctx* c) {
   if (!c) return fail(SWG_ERR_ARG, "NULL ctx");
   DeviceGuard g(c->device);

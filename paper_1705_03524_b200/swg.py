@@ -179,6 +179,11 @@ def lib():
         "swg_brute_windows": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
                               C.POINTER(Kernel), C.c_int, vp, vp],
         "swg_host_alloc": [C.c_size_t, C.POINTER(vp)],
+        "swg_device_alloc": [C.c_size_t, C.POINTER(vp)],
+        "swg_device_free": [vp],
+        "swg_ipc_export": [vp, vp],
+        "swg_ipc_import": [vp, C.POINTER(vp)],
+        "swg_ipc_close": [vp],
         "swg_host_free": [vp],
     }.items():
         f = getattr(L, name)
@@ -545,3 +550,35 @@ def cake_plan(kernel: Kernel, rings: int, rule=RING_MEAN):
     rw = np.zeros(max(rings, 1), np.float64)
     _check(lib().swg_cake_plan(C.byref(kernel), rings, rule, _ptr(sx), _ptr(sy), _ptr(rw)))
     return sx, sy, rw
+
+
+def device_alloc(nbytes: int) -> int:
+    """Raw device allocation (its own base address, so its IPC handle maps
+    exactly this buffer); free with device_free."""
+    p = C.c_void_p()
+    _check(lib().swg_device_alloc(nbytes, C.byref(p)))
+    return p.value
+
+
+def device_free(address: int) -> None:
+    _check(lib().swg_device_free(address))
+
+
+def ipc_export(tensor) -> bytes:
+    """Handle of a device allocation for another process (swg_ipc_export)."""
+    buf = (C.c_ubyte * 64)()
+    _check(lib().swg_ipc_export(_ptr(tensor), buf))
+    return bytes(buf)
+
+
+def ipc_import(handle: bytes) -> int:
+    """Map another process's device allocation; returns its device address
+    (pass it anywhere a device pointer is taken, e.g. MapRequest.partial_out)."""
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().swg_ipc_import(buf, C.byref(p)))
+    return p.value
+
+
+def ipc_close(address: int) -> None:
+    _check(lib().swg_ipc_close(address))

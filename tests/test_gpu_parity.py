@@ -938,3 +938,66 @@ def test_random_configurations_all_engines(ctx, oracle, seed):
             u, v = pk[0], pk[1] - rows[0]
             assert pk[4] == want.max() and want[v, u] == want.max()
             assert (v, u) == tuple(np.unravel_index(np.argmax(want), want.shape))
+
+
+def _peer_chain_worker(rank, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        orc = O.Oracle()
+        ctx = swg.Context(0)
+        img = orc.random_gray(80, 60, 44)
+        bins, d = 16, 0.9375
+        fi = orc.quantize_gray8(img, bins)
+        k = K(swg.EXP_L1, 13, 11, d)
+        ok = O.kernel(O.EXP_L1, 13, 11, d)
+        model = orc.target_model(fi[20:31, 30:43].copy(), bins, ok, O.BRUTE)
+        b0, b1 = (0, 8) if rank == 0 else (8, 16)
+        t = ctx.build_bins(img, b0, b1, swg.FMT_GRAY8, bins, swg.PLANES_DECAY, decay=d)
+        nbytes = t.map_shape(k)[0] * t.map_shape(k)[1] * 16
+        mine = swg.device_alloc(nbytes) if rank == 1 else None
+        handles = [None, None]
+        dist.all_gather_object(handles, swg.ipc_export(mine) if mine else None)
+        token = torch.zeros(1)
+        if rank == 0:  # the sweep writes its running sums into rank 1's buffer
+            peer = swg.ipc_import(handles[1])
+            t.likelihood_maps([swg.MapRequest(k, model, partial_out=peer)], scores="none")
+            ctx.synchronize()
+            dist.send(token, dst=1)
+            q.put((0, True))
+        else:
+            dist.recv(token, src=0)
+            maps, pks = t.likelihood_maps([swg.MapRequest(k, model, partial_in=mine)])
+            full = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+            want, wpk = full.likelihood_map(k, model, swg.SWIH)
+            q.put((1, bool((maps[0] == want).all()) and pks[0] == wpk))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bin_chain_through_peer_memory():
+    """Two processes (one per GPU on a multi-GPU box; both on cuda:0 here):
+    rank 0's sweep writes its running sums straight into rank 1's buffer
+    through an IPC-mapped pointer (swg_ipc_export / swg_ipc_import), rank 1
+    finishes the chain; the map equals the single-table map bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    procs = [ctxm.Process(target=_peer_chain_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert res[0] and res[1]
