@@ -1298,156 +1298,385 @@ swg_status swg_map_peak(swg_ctx* c, const double* scores, int mw, int mh, int hx
   return SWG_OK;
 }
 
+namespace {
+
+// Sweep engine of one map request (plan_request).
+enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
+
+struct MapPlan {
+  int row0 = 0, rows = 0, mw = 0;  // map rows [row0, row0 + rows) of width mw
+  Engine engine = kAffine32;
+  swg_kernel k{};  // the kernel the engine sweeps (Plain maps: Uniform)
+  dim3 grid;
+  size_t soff = 0, poff = 0;  // offsets into the score / CTA-peak scratch
+};
+
+constexpr int kRescoreCap = 4096;  // exact-peak candidates re-scored per request
+
+// Request checks in the reference order (matching.cpp:112-124), then the
+// exactness limits of this implementation; fills the plan's row range.
+swg_status validate_request(const swg_tables* t, const swg_map_request& r, bool host_scores,
+                            MapPlan& p) {
+  ST_TRY(validate_kernel(r.kernel));
+  if (t->w < r.kernel.kw || t->h < r.kernel.kh)
+    return fail(SWG_ERR_SIZE, "likelihood map: kernel %dx%d larger than search image %dx%d",
+                r.kernel.kw, r.kernel.kh, t->w, t->h);
+  if (!r.model) return fail(SWG_ERR_MODEL, "likelihood map: model must be normalized with %d bins", t->bins);
+  if (r.method < 0 || r.method > 3) return fail(SWG_ERR_ARG, "method %d", r.method);
+  if (r.sim < 0 || r.sim > 1) return fail(SWG_ERR_ARG, "similarity %d", r.sim);
+  const bool quad = r.kernel.kind == SWG_KERNEL_EUCLID_QUAD;
+  const bool expo = r.kernel.kind == SWG_KERNEL_EXP_L1;
+  if (r.method == SWG_METHOD_SWIH && expo && !(t->tdec && r.kernel.sigma == t->decay))
+    return fail(SWG_ERR_CONFIG,
+                "likelihood map: exponential swih needs decay tables built with decay %g",
+                r.kernel.sigma);
+  if (t->tdec && r.method != SWG_METHOD_BRUTE && !(r.method == SWG_METHOD_SWIH && expo))
+    return fail(SWG_ERR_CONFIG, "decay tables serve exponential swih and brute force only");
+  if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel) && !quad && !expo)
+    return fail(SWG_ERR_UNSUPPORTED_KERNEL,
+                "likelihood map: method swih requires a quadrant-affine kernel");
+  if (r.method == SWG_METHOD_SWIH && quad) {
+    if (t->planes != SWG_PLANES_QUADRATIC)
+      return fail(SWG_ERR_CONFIG, "likelihood map: Euclidean swih needs quadratic planes");
+    if (quad_mass(r.kernel) >= (int64_t(1) << 53))
+      return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the exact fp64 range",
+                  r.kernel.kw, r.kernel.kh);
+    // the 32-bit planes give sum (x-cx)^2 exactly while it stays < 2^32
+    const int64_t hm = std::max(k_hx(r.kernel), k_hy(r.kernel));
+    if ((int64_t)r.kernel.kw * r.kernel.kh * hm * hm >= (int64_t(1) << 32))
+      return fail(SWG_ERR_CONFIG, "kernel %dx%d: squared offsets exceed the 32-bit planes",
+                  r.kernel.kw, r.kernel.kh);
+  }
+  if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
+  const bool ranged = t->bins != t->total_bins;
+  if (ranged && !r.partial_in && !r.partial_out)
+    return fail(SWG_ERR_CONFIG,
+                "bin-range tables [%d, %d) of %d compute partial sums: give partial_out "
+                "(or partial_in on the last range)", t->bin0, t->bin0 + t->bins, t->total_bins);
+  if ((r.partial_in || r.partial_out) && r.method == SWG_METHOD_BRUTE)
+    return fail(SWG_ERR_CONFIG, "bin-range chains run on the table sweeps, not brute force");
+  if (r.partial_out && host_scores)
+    return fail(SWG_ERR_ARG, "a partial (partial_out) request produces no scores");
+  if (expo && r.partial_in && !r.partial_out && t->total_bins > kMaxBins)
+    return fail(SWG_ERR_CONFIG, "exact exponential peak: more than %d bins", kMaxBins);
+  const bool needs_ramps = (r.method == SWG_METHOD_SWIH || r.method == SWG_METHOD_BRUTE) &&
+                           r.kernel.kind == SWG_KERNEL_MANHATTAN;
+  if (needs_ramps && t->planes < 3 && !(r.method == SWG_METHOD_BRUTE && t->has_fi))
+    return fail(SWG_ERR_CONFIG, "likelihood map: Manhattan swih needs the ramp planes");
+  if (r.method == SWG_METHOD_BRUTE && !k_affine(r.kernel) && !t->has_fi)
+    return fail(SWG_ERR_CONFIG, "likelihood map: brute force needs the feature image");
+  const int mw = t->w - r.kernel.kw + 1, mh = t->h - r.kernel.kh + 1;
+  int a = r.row_begin, b = r.row_end;
+  if (a == 0 && b == 0) b = mh;
+  if (a < 0 || b > mh || a > b) return fail(SWG_ERR_OUT_OF_RANGE, "map rows [%d, %d) of %d", a, b, mh);
+  if (r.kernel.kind == SWG_KERNEL_MANHATTAN && affine_mass(r.kernel) >= (int64_t(1) << 32))
+    return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the 32-bit exact range", r.kernel.kw,
+                r.kernel.kh);
+  p.row0 = a;
+  p.rows = b - a;
+  p.mw = mw;
+  return SWG_OK;
+}
+
+// Engine and grid of a validated request.  The kernel-independent choices:
+// Plain maps are Uniform-kernel maps; brute force on an integer affine kernel
+// gives the quadrant path's exact counts (engine.hpp:62-66,
+// test_matching.cpp:115-141) and shares its kernel; a Uniform box is a
+// one-ring cake with coefficient 1.0 (exact integer weights, same scores:
+// score_counts == score_weights on integers), so on narrow tables it runs the
+// 16-bit cake sweep.
+swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& p) {
+  swg_kernel k = r.kernel;
+  int method = r.method;
+  if (method == SWG_METHOD_PLAIN) {
+    k.kind = SWG_KERNEL_UNIFORM;
+    method = SWG_METHOD_SWIH;
+  }
+  if (method == SWG_METHOD_BRUTE && !t->tdec && (k.kind == SWG_KERNEL_UNIFORM ||
+                                     (k.kind == SWG_KERNEL_MANHATTAN && t->planes == 3)))
+    method = SWG_METHOD_SWIH;
+  const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
+  Engine e;
+  if (method == SWG_METHOD_BRUTE) e = kBrute;
+  else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) e = kQuad;
+  else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EXP_L1) e = kExp64;
+  else if (method == SWG_METHOD_CAKE)
+    e = t->t16 && (small || cake16_wide0(k, r)) ? kCake16 : kCake32;
+  else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) e = kCake16;
+  else e = kAffine32;
+  if (r.partial_in || r.partial_out) {  // engines that can continue a bin-range chain
+    const bool closed_mass = e == kAffine32 || e == kQuad;
+    if (e == kBrute || (!closed_mass && r.sim != SWG_SIM_BHATTACHARYYA))
+      return fail(SWG_ERR_CONFIG,
+                  "bin-range chains: Bhattacharyya, or intersection on swih Manhattan / "
+                  "Uniform / Euclidean");
+  }
+  p.engine = e;
+  p.k = k;
+  if (e == kBrute) {
+    p.grid = dim3((unsigned)((p.mw + kBruteThreads - 1) / kBruteThreads),
+                  (unsigned)std::max(p.rows, 1));
+  } else {
+    const int tw = (e == kCake16 || e == kExp64) ? 32 : kSweepTileX;
+    p.grid = dim3((unsigned)((p.mw + tw - 1) / tw),
+                  (unsigned)std::max((p.rows + kSweepTileY - 1) / kSweepTileY, 1));
+  }
+  return SWG_OK;
+}
+
+// Super-column CTA order for the table sweeps whose corner span (2hy+2
+// table rows of the whole width) does not fit in L2: a strip of sw windows
+// needs (2hy+2+tile) rows x (sw+2hx+2) cells resident.  0 = row-major order.
+int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int hx, int hy) {
+  size_t cell = 0;  // table bytes per pixel the engine reads
+  if (e == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
+  else if (e == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
+  else if (e == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
+  else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
+  if (!cell) return 0;
+  const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
+  const double span = 2.0 * hy + 2 + kSweepTileY;
+  if (span * (t->w + 1) * cell <= budget) return 0;
+  const double sw = budget / (span * cell) - (2.0 * hx + 2);
+  const int tw = e == kExp64 ? 32 : kSweepTileX;  // windows per tile
+  if (sw >= 2 * tw && (sw + 2.0 * hx + 2) / sw < 1.7) return std::max(1, (int)(sw / tw));
+  return 0;
+}
+
+// The kernel-independent sweep arguments of one request.
+void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r,
+                     const MapPlan& p, double* scores, PeakPart* parts) {
+  a.tab = p.engine == kCake16 ? (const void*)t->t16
+          : p.engine == kExp64 ? (const void*)t->tdec
+                               : (const void*)t->t32;
+  a.plane_stride = t->ps;
+  a.pitch = t->pitch;
+  a.planes = t->planes;
+  a.bins = t->bins;
+  a.groups = t->groups;
+  a.hx = k_hx(p.k);
+  a.hy = k_hy(p.k);
+  a.mw = p.mw;
+  a.row0 = p.row0;
+  a.rows = p.rows;
+  a.sim = r.sim;
+  a.scores = scores;
+  a.parts = parts;
+  std::memset(a.model, 0, sizeof(a.model));
+  std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
+  a.pin = static_cast<const double2*>(r.partial_in);
+  a.pout = static_cast<double2*>(r.partial_out);
+  a.sc_tiles = super_column_tiles(t, p.engine, p.k, a.hx, a.hy);
+}
+
+// Exponential kernel: quadrant rectangles in their orientation's SE table
+// (k_exp.cu, bin-pair records), coefficients in powers of the table's decay.
+// Returns the fast path's score error bound.
+double exp_plan(const swg_tables* t, const swg_map_request& r, int hx, int hy, ExpSweep& es) {
+  const double dd = t->decay;
+  auto pw = [&](int n) { return std::pow(dd, (double)n); };
+  const long long p = (long long)t->pitch;
+  // corners (dx, dy) from the centre record, per orientation, and rect extents
+  const int cx0[4] = {1, 0, 1, 0}, cy0[4] = {1, 1, 0, 0};  // (x1+1, y1+1) offset
+  const int ax[4] = {hx + 1, hx, hx + 1, hx}, by[4] = {hy + 1, hy + 1, hy, hy};
+  const double qf[4] = {1.0, dd, dd, dd * dd};
+  for (int o = 0; o < 4; ++o) {
+    const int xs[4] = {cx0[o], cx0[o] - ax[o], cx0[o], cx0[o] - ax[o]};
+    const int ys[4] = {cy0[o], cy0[o], cy0[o] - by[o], cy0[o] - by[o]};
+    const double cf[4] = {qf[o], -qf[o] * pw(ax[o]), -qf[o] * pw(by[o]),
+                          qf[o] * pw(ax[o] + by[o])};
+    for (int q = 0; q < 4; ++q) {
+      es.off[4 * o + q] = (int)(16 * (ys[q] * p + xs[q]));  // 16-B pair records
+      es.coef[4 * o + q] = cf[q];
+    }
+  }
+  es.w = t->w;
+  es.h = t->h;
+  // Table values <= T = 1/(1-d)^2; the damped recurrences keep each entry
+  // within ~T u / (1-d) of exact (u = 2^-53), so one assembled bin is within
+  // dh = 8 * 16 * T * u / (1-d) (16 corners, slack 8).  Bins below snap = 2 dh
+  // are rounding noise of an empty bin; every real bin value is >= h_min =
+  // d^(hx+hy) (the smallest weight).
+  const double u = std::ldexp(1.0, -53);
+  const double T = 1.0 / ((1.0 - dd) * (1.0 - dd));
+  const double dh = 8.0 * 16.0 * T * u / (1.0 - dd);
+  const double hmin = pw(hx + hy);
+  es.snap = 2.0 * dh;
+  if (es.snap >= 0.5 * hmin) return 1.0;  // no separation of noise and data: re-score everything
+  if (r.sim == SWG_SIM_BHATTACHARYYA)
+    // |d sum sqrt(m h)| <= sqrt(bins) dh / (2 sqrt(h_min)); mass term <= bins dh / 2
+    return std::sqrt((double)t->total_bins) * dh / (2.0 * std::sqrt(hmin)) + t->total_bins * dh;
+  return 2.0 * t->total_bins * dh;
+}
+
+// Exact-peak scratch of one request: candidates, their CTA peaks, a count.
+struct RescoreSlice {
+  static constexpr size_t kCand = (size_t)kRescoreCap * 8;
+  static constexpr size_t kParts = (size_t)((kRescoreCap + 3) / 4) * sizeof(PeakPart);
+  static constexpr size_t kBytes = (kCand + kParts + 256 + 255) / 256 * 256;
+};
+
+// Exponential sweep, then (full maps) the fast peak and the exact fp64
+// re-score of the windows within 2 err of it.
+swg_status run_exp(swg_ctx* c, const swg_tables* t, const swg_map_request& r, const MapPlan& p,
+                   const SweepArgs& a, PeakPart* parts, swg_peak* peak, char* slice,
+                   cudaStream_t st) {
+  static thread_local ExpSweep es;
+  const double err = exp_plan(t, r, a.hx, a.hy, es);
+  CUDA_TRY(launch_sweep_exp(a, es, p.grid, st));
+  c->launches += 1;
+  if (r.partial_out) return SWG_OK;  // partial sums only: no scores, no peak
+  CUDA_TRY(launch_peak_reduce(parts, (int)(p.grid.x * p.grid.y), p.mw, a.hx, a.hy, peak, st));
+  c->launches += 1;
+  static thread_local RescoreArgs ra;  // 8 KB of model: keep off the stack
+  ra = RescoreArgs{};
+  ST_TRY(weight_grid(c, p.k, &ra.grid));
+  ra.fi = t->fi;
+  ra.fi_pitch = t->fip;
+  ra.kw = p.k.kw;
+  ra.kh = p.k.kh;
+  ra.bins = t->total_bins;  // every bin: the re-score is the whole histogram
+  std::memset(ra.model, 0, sizeof(ra.model));
+  std::memcpy(ra.model, r.model, sizeof(double) * t->total_bins);
+  ra.cap = kRescoreCap;
+  // a window outside [fast max - eps] cannot be the exact maximum when
+  // eps >= 2 err (+ the fp64 rounding of the scores themselves)
+  ra.eps = std::min(4.0, 2.0 * err + 1e-12);
+  ra.cand = reinterpret_cast<long long*>(slice);
+  ra.parts = reinterpret_cast<PeakPart*>(slice + RescoreSlice::kCand);
+  ra.count = reinterpret_cast<int*>(slice + RescoreSlice::kCand + RescoreSlice::kParts);
+  CUDA_TRY(launch_exact_peak(a, ra, peak, st));
+  c->launches += 3;
+  if (std::getenv("SWG_DEBUG_RESCORE")) {  // diagnostics: candidate count
+    int cnt = 0;
+    cudaMemcpyAsync(&cnt, ra.count, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr, "swg rescore: kernel %dx%d eps %.3g candidates %d\n", p.k.kw, p.k.kh,
+                 ra.eps, cnt);
+  }
+  return SWG_OK;
+}
+
+// Euclidean: box corners (TL, TR, BL, BR) of the whole window as byte
+// offsets from the centre record within a plane of the 32-bit tables.
+swg_status run_quad(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
+  a.mass = (double)quad_mass(p.k);
+  const long long p8 = (long long)t->pitch * kOct;
+  const long long xs[2] = {-a.hx, a.hx + 1}, ys[2] = {-a.hy, a.hy + 1};
+  for (int pl = 0; pl < 5; ++pl)
+    for (int q = 0; q < 4; ++q)
+      a.lat[4 * pl + q] = (int)(4 * (ys[q >> 1] * p8 + xs[q & 1] * kOct));
+  CUDA_TRY(launch_sweep_quad(a, p.grid, st));
+  return SWG_OK;
+}
+
+// Quadrant-affine: corner byte offsets from the centre record (SweepArgs::lat order).
+swg_status run_affine(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
+  a.mass = (double)affine_mass(p.k);
+  const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
+  const long long xs[3] = {-a.hx, 1, a.hx + 1}, ys[3] = {-a.hy, 1, a.hy + 1};
+  auto off = [&](int plane, int xi, int yi) {
+    return (int)(4 * (plane * ps8 + ys[yi] * p8 + xs[xi] * kOct));
+  };
+  const int pts[20][3] = {{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, 1}, {0, 2, 1},
+                          {0, 0, 2}, {0, 1, 2}, {0, 2, 2}, {1, 0, 0}, {1, 1, 0},
+                          {1, 2, 0}, {1, 0, 2}, {1, 1, 2}, {1, 2, 2}, {2, 0, 0},
+                          {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
+  for (int q = 0; q < 20; ++q)
+    a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
+  CUDA_TRY(launch_sweep_affine(a, p.k.kind == SWG_KERNEL_UNIFORM, p.grid, st));
+  return SWG_OK;
+}
+
+// Cake (or a Uniform box as a one-ring cake): ring corner byte offsets from
+// the centre record and the ring coefficients.
+swg_status run_cake(const swg_tables* t, const swg_map_request& r, const MapPlan& p,
+                    SweepArgs& a, cudaStream_t st) {
+  static thread_local CakeRings rg;
+  static thread_local CakeSweep cs;
+  int rings = 1;
+  if (r.method == SWG_METHOD_CAKE) {
+    ST_TRY(cake_plan(p.k, r.rings, r.ring_rule, rg));
+    rings = r.rings;
+  } else {  // Uniform box: one ring, coefficient 1
+    rg.a[0] = a.hx;
+    rg.c[0] = a.hy;
+    rg.coeff[0] = 1.0;
+  }
+  const bool narrow = p.engine == kCake16;
+  const long long p8 = (long long)t->pitch * kOct;
+  const long long eb = narrow ? 2 : 4;  // element bytes
+  for (int q = 0; q < rings; ++q) {
+    const long long ax = rg.a[q], cy = rg.c[q];
+    cs.off[q] = make_int4((int)(eb * (-cy * p8 - ax * kOct)),
+                          (int)(eb * (-cy * p8 + (ax + 1) * kOct)),
+                          (int)(eb * ((cy + 1) * p8 - ax * kOct)),
+                          (int)(eb * ((cy + 1) * p8 + (ax + 1) * kOct)));
+    cs.coeff[q] = rg.coeff[q];
+  }
+  a.rings = rings;
+  a.wide0 = narrow && (long long)p.k.kw * p.k.kh >= 65536;
+  if (narrow) CUDA_TRY(launch_sweep_cake16(a, cs, p.grid, st));
+  else CUDA_TRY(launch_sweep_cake(a, cs, p.grid, st));
+  return SWG_OK;
+}
+
+// Direct per-pixel weighted histogram (baselines.cpp:24-69).
+swg_status run_brute(swg_ctx* c, const swg_tables* t, const MapPlan& p, const SweepArgs& a,
+                     cudaStream_t st) {
+  BruteArgs ba{};
+  ST_TRY(weight_grid(c, p.k, &ba.grid));
+  ba.fi = t->fi;
+  ba.fi_pitch = t->fip;
+  ba.kw = p.k.kw;
+  ba.kh = p.k.kh;
+  ba.integer = k_integer(p.k);
+  CUDA_TRY(launch_sweep_brute(a, ba, p.grid.x, st));
+  return SWG_OK;
+}
+
+}  // namespace
+
 swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs,
                                double* const* scores_host, double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev) {
   ST_TRY(check_tables(t));
   if (n < 0 || (n && !reqs)) return fail(SWG_ERR_ARG, "bad request list");
   if (n == 0) return SWG_OK;
-  // ---- validation in the reference order (matching.cpp:112-124)
-  std::vector<int> v0(n), v1(n), mws(n);
-  for (int i = 0; i < n; ++i) {
-    const swg_map_request& r = reqs[i];
-    ST_TRY(validate_kernel(r.kernel));
-    if (t->w < r.kernel.kw || t->h < r.kernel.kh)
-      return fail(SWG_ERR_SIZE, "likelihood map: kernel %dx%d larger than search image %dx%d",
-                  r.kernel.kw, r.kernel.kh, t->w, t->h);
-    if (!r.model) return fail(SWG_ERR_MODEL, "likelihood map: model must be normalized with %d bins", t->bins);
-    if (r.method < 0 || r.method > 3) return fail(SWG_ERR_ARG, "method %d", r.method);
-    if (r.sim < 0 || r.sim > 1) return fail(SWG_ERR_ARG, "similarity %d", r.sim);
-    const bool quad = r.kernel.kind == SWG_KERNEL_EUCLID_QUAD;
-    const bool expo = r.kernel.kind == SWG_KERNEL_EXP_L1;
-    if (r.method == SWG_METHOD_SWIH && expo && !(t->tdec && r.kernel.sigma == t->decay))
-      return fail(SWG_ERR_CONFIG,
-                  "likelihood map: exponential swih needs decay tables built with decay %g",
-                  r.kernel.sigma);
-    if (t->tdec && r.method != SWG_METHOD_BRUTE && !(r.method == SWG_METHOD_SWIH && expo))
-      return fail(SWG_ERR_CONFIG, "decay tables serve exponential swih and brute force only");
-    if (r.method == SWG_METHOD_SWIH && !k_affine(r.kernel) && !quad && !expo)
-      return fail(SWG_ERR_UNSUPPORTED_KERNEL,
-                  "likelihood map: method swih requires a quadrant-affine kernel");
-    if (r.method == SWG_METHOD_SWIH && quad) {
-      if (t->planes != SWG_PLANES_QUADRATIC)
-        return fail(SWG_ERR_CONFIG, "likelihood map: Euclidean swih needs quadratic planes");
-      if (quad_mass(r.kernel) >= (int64_t(1) << 53))
-        return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the exact fp64 range",
-                    r.kernel.kw, r.kernel.kh);
-      // the 32-bit planes give sum (x-cx)^2 exactly while it stays < 2^32
-      const int64_t hm = std::max(k_hx(r.kernel), k_hy(r.kernel));
-      if ((int64_t)r.kernel.kw * r.kernel.kh * hm * hm >= (int64_t(1) << 32))
-        return fail(SWG_ERR_CONFIG, "kernel %dx%d: squared offsets exceed the 32-bit planes",
-                    r.kernel.kw, r.kernel.kh);
-    }
-    if (t->bins > kMaxBins) return fail(SWG_ERR_CONFIG, "more than %d bins", kMaxBins);
-    const bool ranged = t->bins != t->total_bins;
-    if (ranged && !r.partial_in && !r.partial_out)
-      return fail(SWG_ERR_CONFIG,
-                  "bin-range tables [%d, %d) of %d compute partial sums: give partial_out "
-                  "(or partial_in on the last range)", t->bin0, t->bin0 + t->bins, t->total_bins);
-    if ((r.partial_in || r.partial_out) && r.method == SWG_METHOD_BRUTE)
-      return fail(SWG_ERR_CONFIG, "bin-range chains run on the table sweeps, not brute force");
-    if (r.partial_out && scores_host && scores_host[i])
-      return fail(SWG_ERR_ARG, "a partial (partial_out) request produces no scores");
-    if (expo && r.partial_in && !r.partial_out && t->total_bins > kMaxBins)
-      return fail(SWG_ERR_CONFIG, "exact exponential peak: more than %d bins", kMaxBins);
-    const bool needs_ramps = (r.method == SWG_METHOD_SWIH || r.method == SWG_METHOD_BRUTE) &&
-                             r.kernel.kind == SWG_KERNEL_MANHATTAN;
-    if (needs_ramps && t->planes < 3 && !(r.method == SWG_METHOD_BRUTE && t->has_fi))
-      return fail(SWG_ERR_CONFIG, "likelihood map: Manhattan swih needs the ramp planes");
-    if (r.method == SWG_METHOD_BRUTE && !k_affine(r.kernel) && !t->has_fi)
-      return fail(SWG_ERR_CONFIG, "likelihood map: brute force needs the feature image");
-    const int mw = t->w - r.kernel.kw + 1, mh = t->h - r.kernel.kh + 1;
-    int a = r.row_begin, b = r.row_end;
-    if (a == 0 && b == 0) b = mh;
-    if (a < 0 || b > mh || a > b) return fail(SWG_ERR_OUT_OF_RANGE, "map rows [%d, %d) of %d", a, b, mh);
-    if (r.kernel.kind == SWG_KERNEL_MANHATTAN && affine_mass(r.kernel) >= (int64_t(1) << 32))
-      return fail(SWG_ERR_CONFIG, "kernel %dx%d mass exceeds the 32-bit exact range", r.kernel.kw,
-                  r.kernel.kh);
-    v0[i] = a;
-    v1[i] = b;
-    mws[i] = mw;
-  }
+  auto host_map = [&](int i) { return scores_host && scores_host[i]; };
+  auto dev_map = [&](int i) { return scores_dev && scores_dev[i]; };
+  // every request is checked before anything launches
+  std::vector<MapPlan> plan(n);
+  for (int i = 0; i < n; ++i) ST_TRY(validate_request(t, reqs[i], host_map(i), plan[i]));
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   swg_ctx* c = t->ctx;
-  // ---- scratch: per-request score buffers (when the caller gave no device
-  // output), CTA peak candidates, device peaks
-  std::vector<size_t> soff(n, 0), poff(n, 0);
+  // scratch: per-request score buffers (when the caller gave no device
+  // output), CTA peak candidates, device peaks, exact-peak slices
   size_t stot = 0, ptot = 0;
-  // Engine per request.  The kernel-independent choices: Plain maps are
-  // Uniform-kernel maps; brute force on an integer affine kernel gives the
-  // quadrant path's exact counts (engine.hpp:62-66, test_matching.cpp:115-141)
-  // and shares its kernel; a Uniform box is a one-ring cake with coefficient
-  // 1.0 (exact integer weights, same scores: score_counts == score_weights on
-  // integers), so on narrow tables it runs the 16-bit cake sweep.
-  enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
-  std::vector<dim3> grid(n);
-  std::vector<int> engine(n);
-  std::vector<swg_kernel> kern(n);
   for (int i = 0; i < n; ++i) {
-    const swg_map_request& r = reqs[i];
-    const int rows = v1[i] - v0[i];
-    const size_t cells = (size_t)rows * mws[i];
-    if (!(scores_dev && scores_dev[i])) {
-      soff[i] = stot;
-      stot += round_up(cells, 32);
+    MapPlan& p = plan[i];
+    ST_TRY(plan_request(t, reqs[i], p));
+    if (!dev_map(i)) {
+      p.soff = stot;
+      stot += round_up((size_t)p.rows * p.mw, 32);
     }
-    swg_kernel k = r.kernel;
-    int method = r.method;
-    if (method == SWG_METHOD_PLAIN) {
-      k.kind = SWG_KERNEL_UNIFORM;
-      method = SWG_METHOD_SWIH;
-    }
-    if (method == SWG_METHOD_BRUTE && !t->tdec && (k.kind == SWG_KERNEL_UNIFORM ||
-                                       (k.kind == SWG_KERNEL_MANHATTAN && t->planes == 3)))
-      method = SWG_METHOD_SWIH;
-    const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
-    if (method == SWG_METHOD_BRUTE) engine[i] = kBrute;
-    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EUCLID_QUAD) engine[i] = kQuad;
-    else if (method == SWG_METHOD_SWIH && k.kind == SWG_KERNEL_EXP_L1) engine[i] = kExp64;
-    else if (method == SWG_METHOD_CAKE) {
-      engine[i] = (t->t16 && small) ? kCake16 : kCake32;
-      if (engine[i] == kCake32 && t->t16 && cake16_wide0(k, r)) engine[i] = kCake16;
-    }
-    else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) engine[i] = kCake16;
-    else engine[i] = kAffine32;
-    kern[i] = k;
-    if (r.partial_in || r.partial_out) {  // engines that can continue a bin-range chain
-      const bool closed_mass = engine[i] == kAffine32 || engine[i] == kQuad;
-      if (engine[i] == kBrute || (!closed_mass && r.sim != SWG_SIM_BHATTACHARYYA))
-        return fail(SWG_ERR_CONFIG,
-                    "bin-range chains: Bhattacharyya, or intersection on swih Manhattan / "
-                    "Uniform / Euclidean");
-    }
-    if (engine[i] == kBrute)
-      grid[i] = dim3((unsigned)((mws[i] + kBruteThreads - 1) / kBruteThreads),
-                     (unsigned)std::max(rows, 1));
-    else {
-      const int tw = (engine[i] == kCake16 || engine[i] == kExp64) ? 32 : kSweepTileX;
-      grid[i] = dim3((unsigned)((mws[i] + tw - 1) / tw),
-                     (unsigned)std::max((rows + kSweepTileY - 1) / kSweepTileY, 1));
-    }
-    poff[i] = ptot;
-    ptot += (size_t)grid[i].x * grid[i].y;
+    p.poff = ptot;
+    ptot += (size_t)p.grid.x * p.grid.y;
   }
   swg_ctx::Scratch& S = c->scr[c->slot];
   ST_TRY(S.scores.ensure(std::max<size_t>(stot, 1) * 8));
   ST_TRY(S.parts.ensure(ptot * sizeof(PeakPart)));
   ST_TRY(S.peaks.ensure((size_t)n * sizeof(swg_peak)));
+  ST_TRY(S.resc.ensure(RescoreSlice::kBytes * n));
   swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(S.peaks.p);
+  // the lazily built 32-bit planes go on the main stream before the fan-out
+  for (const MapPlan& p : plan)
+    if (p.rows > 0 && (p.engine == kAffine32 || p.engine == kCake32)) ST_TRY(ensure_t32(t));
 
-  // lazily built 32-bit planes and the exact-peak scratch (one slice per
-  // request) are set up on the main stream before the requests fan out
-  constexpr int kCap = 4096;  // exact-peak candidates re-scored per request
-  const size_t rs_cand = (size_t)kCap * 8, rs_parts = (size_t)((kCap + 3) / 4) * sizeof(PeakPart);
-  const size_t rs_slice = round_up(rs_cand + rs_parts + 256, 256);
-  for (int i = 0; i < n; ++i)
-    if (v1[i] > v0[i] && (engine[i] == kAffine32 || engine[i] == kCake32)) ST_TRY(ensure_t32(t));
-  ST_TRY(S.resc.ensure(rs_slice * n));
-  int nwork = 0;
   bool host_maps = false;
-  if (scores_host)
-    for (int i = 0; i < n; ++i) host_maps |= scores_host[i] != nullptr;
+  for (int i = 0; i < n; ++i) host_maps |= host_map(i);
+  int nwork = 0;
 #ifndef SWG_NO_FANOUT
   // device outputs: overlap the scales' sweeps; host maps: keep the scales
   // in sequence so each map's copy overlaps the next scale's sweep
@@ -1463,211 +1692,29 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   bool copies = false;
   for (int i = 0; i < n; ++i) {
     const swg_map_request& r = reqs[i];
-    const int rows = v1[i] - v0[i];
+    const MapPlan& p = plan[i];
+    if (p.rows == 0) continue;
     const cudaStream_t st = nwork ? c->work[i % nwork] : c->stream;
-    double* dscores = (scores_dev && scores_dev[i])
-                          ? scores_dev[i]
-                          : static_cast<double*>(S.scores.p) + soff[i];
-    PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + poff[i];
-    if (rows > 0) {
-      static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
-      const swg_kernel k = kern[i];
-      a.tab = engine[i] == kCake16   ? (const void*)t->t16
-              : engine[i] == kQuad ? (const void*)t->t32
-              : engine[i] == kExp64  ? (const void*)t->tdec
-                                     : (const void*)t->t32;
-      a.plane_stride = t->ps;
-      a.pitch = t->pitch;
-      a.planes = t->planes;
-      a.bins = t->bins;
-      a.groups = t->groups;
-      a.hx = k_hx(k);
-      a.hy = k_hy(k);
-      a.mw = mws[i];
-      a.row0 = v0[i];
-      a.rows = rows;
-      a.sim = r.sim;
-      a.scores = dscores;
-      a.parts = parts;
-      std::memset(a.model, 0, sizeof(a.model));
-      std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
-      a.pin = static_cast<const double2*>(r.partial_in);
-      a.pout = static_cast<double2*>(r.partial_out);
-      {
-        // super-column CTA order for the table sweeps whose corner span
-        // (2hy+2 table rows of the whole width) does not fit in L2: a strip
-        // of sw windows needs (2hy+2+tile) rows x (sw+2hx+2) cells resident
-        size_t cell = 0;
-        if (engine[i] == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
-        else if (engine[i] == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
-        else if (engine[i] == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
-        else if (engine[i] == kCake32) cell = (size_t)t->groups * kOct * 4;
-        a.sc_tiles = 0;
-        if (cell) {
-          const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
-          const double span = 2.0 * a.hy + 2 + kSweepTileY;
-          if (span * (t->w + 1) * cell > budget) {
-            const double sw = budget / (span * cell) - (2.0 * a.hx + 2);
-            const int tw = engine[i] == kExp64 ? 32 : kSweepTileX;  // windows per tile
-            if (sw >= 2 * tw && (sw + 2.0 * a.hx + 2) / sw < 1.7)
-              a.sc_tiles = std::max(1, (int)(sw / tw));
-          }
-        }
-      }
-      if (engine[i] == kExp64) {
-        // quadrant rectangles in their orientation's SE table (k_exp.cu, bin-pair
-        // records);
-        // coefficients in powers of the table's decay
-        static thread_local ExpSweep es;
-        const double dd = t->decay;
-        auto pw = [&](int n) { return std::pow(dd, (double)n); };
-        const int hx = a.hx, hy = a.hy;
-        const long long p = (long long)t->pitch;
-        // corners (dx, dy) from the centre record, per orientation, and rect extents
-        const int cx0[4] = {1, 0, 1, 0}, cy0[4] = {1, 1, 0, 0};   // (x1+1, y1+1) offset
-        const int ax[4] = {hx + 1, hx, hx + 1, hx}, by[4] = {hy + 1, hy + 1, hy, hy};
-        const double qf[4] = {1.0, dd, dd, dd * dd};
-        for (int o = 0; o < 4; ++o) {
-          const int xs[4] = {cx0[o], cx0[o] - ax[o], cx0[o], cx0[o] - ax[o]};
-          const int ys[4] = {cy0[o], cy0[o], cy0[o] - by[o], cy0[o] - by[o]};
-          const double cf[4] = {qf[o], -qf[o] * pw(ax[o]), -qf[o] * pw(by[o]),
-                                qf[o] * pw(ax[o] + by[o])};
-          for (int q = 0; q < 4; ++q) {
-            es.off[4 * o + q] = (int)(16 * (ys[q] * p + xs[q]));  // 16-B pair records
-            es.coef[4 * o + q] = cf[q];
-          }
-        }
-        es.w = t->w;
-        es.h = t->h;
-        // Error budget of the fast path:
-        // table values <= T = 1/(1-d)^2; the damped recurrences keep each
-        // entry within ~T u / (1-d) of exact (u = 2^-53), so one assembled
-        // bin is within dh = 8 * 16 * T * u / (1-d) (16 corners, slack 8).
-        // Bins below snap = 2 dh are rounding noise of an empty bin; every
-        // real bin value is >= h_min = d^(hx+hy) (the smallest weight).
-        const double u = std::ldexp(1.0, -53);
-        const double T = 1.0 / ((1.0 - dd) * (1.0 - dd));
-        const double dh = 8.0 * 16.0 * T * u / (1.0 - dd);
-        const double hmin = pw(hx + hy);
-        es.snap = 2.0 * dh;
-        double err;
-        if (es.snap >= 0.5 * hmin) {
-          err = 1.0;  // no separation of noise and data: re-score everything
-        } else if (r.sim == SWG_SIM_BHATTACHARYYA) {
-          // |d sum sqrt(m h)| <= sqrt(bins) dh / (2 sqrt(h_min)); mass term <= bins dh / 2
-          err = std::sqrt((double)t->total_bins) * dh / (2.0 * std::sqrt(hmin)) +
-                t->total_bins * dh;
-        } else {
-          err = 2.0 * t->total_bins * dh;
-        }
-        CUDA_TRY(launch_sweep_exp(a, es, grid[i], st));
-        c->launches += 1;
-        if (r.partial_out) continue;  // partial sums only: no scores, no peak
-        c->launches += 1;
-        CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
-                                    dpeaks + i, st));
-        // phase 2: exact fp64 brute-force re-score of the near-maximum windows
-        static thread_local RescoreArgs ra;  // 8 KB of model: keep off the stack
-        ra = RescoreArgs{};
-        ST_TRY(weight_grid(c, k, &ra.grid));
-        ra.fi = t->fi;
-        ra.fi_pitch = t->fip;
-        ra.kw = k.kw;
-        ra.kh = k.kh;
-        ra.bins = t->total_bins;  // every bin: the re-score is the whole histogram
-        std::memset(ra.model, 0, sizeof(ra.model));
-        std::memcpy(ra.model, r.model, sizeof(double) * t->total_bins);
-        ra.cap = kCap;
-        // a window outside [fast max - eps] cannot be the exact maximum when
-        // eps >= 2 err (+ the fp64 rounding of the scores themselves)
-        ra.eps = std::min(4.0, 2.0 * err + 1e-12);
-        char* rb = static_cast<char*>(S.resc.p) + rs_slice * i;
-        ra.cand = reinterpret_cast<long long*>(rb);
-        ra.parts = reinterpret_cast<PeakPart*>(rb + rs_cand);
-        ra.count = reinterpret_cast<int*>(rb + rs_cand + rs_parts);
-        CUDA_TRY(launch_exact_peak(a, ra, dpeaks + i, st));
-        if (std::getenv("SWG_DEBUG_RESCORE")) {  // diagnostics: candidate count
-          int cnt = 0;
-          cudaMemcpyAsync(&cnt, ra.count, 4, cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          std::fprintf(stderr, "swg rescore: kernel %dx%d eps %.3g candidates %d\n", k.kw, k.kh,
-                       ra.eps, cnt);
-        }
-        c->launches += 3;
-      } else if (engine[i] == kQuad) {
-        a.mass = (double)quad_mass(k);
-        // box corners (TL, TR, BL, BR) of the whole window as byte offsets
-        // from the centre record within a plane of the 32-bit tables
-        const long long p8 = (long long)t->pitch * kOct;
-        const long long xs[2] = {-a.hx, a.hx + 1}, ys[2] = {-a.hy, a.hy + 1};
-        for (int pl = 0; pl < 5; ++pl)
-          for (int q = 0; q < 4; ++q)
-            a.lat[4 * pl + q] = (int)(4 * (ys[q >> 1] * p8 + xs[q & 1] * kOct));
-        CUDA_TRY(launch_sweep_quad(a, grid[i], st));
-      } else if (engine[i] == kAffine32) {
-        a.mass = (double)affine_mass(k);
-        {  // corner byte offsets from the centre record (SweepArgs::lat order)
-          const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
-          const long long xs[3] = {-a.hx, 1, a.hx + 1}, ys[3] = {-a.hy, 1, a.hy + 1};
-          auto off = [&](int plane, int xi, int yi) {
-            return (int)(4 * (plane * ps8 + ys[yi] * p8 + xs[xi] * kOct));
-          };
-          const int pts[20][3] = {{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, 1}, {0, 2, 1},
-                                  {0, 0, 2}, {0, 1, 2}, {0, 2, 2}, {1, 0, 0}, {1, 1, 0},
-                                  {1, 2, 0}, {1, 0, 2}, {1, 1, 2}, {1, 2, 2}, {2, 0, 0},
-                                  {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
-          for (int q = 0; q < 20; ++q)
-            a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
-        }
-        CUDA_TRY(launch_sweep_affine(a, k.kind == SWG_KERNEL_UNIFORM, grid[i], st));
-      } else if (engine[i] == kCake16 || engine[i] == kCake32) {
-        static thread_local CakeRings rg;
-        static thread_local CakeSweep cs;
-        int rings = 1;
-        if (r.method == SWG_METHOD_CAKE) {
-          ST_TRY(cake_plan(k, r.rings, r.ring_rule, rg));
-          rings = r.rings;
-        } else {  // Uniform box: one ring, coefficient 1
-          rg.a[0] = a.hx;
-          rg.c[0] = a.hy;
-          rg.coeff[0] = 1.0;
-        }
-        const long long p8 = (long long)t->pitch * kOct;
-        const long long eb = engine[i] == kCake16 ? 2 : 4;  // element bytes
-        for (int q = 0; q < rings; ++q) {  // corner byte offsets from the centre record
-          const long long ax = rg.a[q], cy_ = rg.c[q];
-          cs.off[q] = make_int4((int)(eb * (-cy_ * p8 - ax * kOct)),
-                                (int)(eb * (-cy_ * p8 + (ax + 1) * kOct)),
-                                (int)(eb * ((cy_ + 1) * p8 - ax * kOct)),
-                                (int)(eb * ((cy_ + 1) * p8 + (ax + 1) * kOct)));
-          cs.coeff[q] = rg.coeff[q];
-        }
-        a.rings = rings;
-        a.wide0 = engine[i] == kCake16 && (long long)k.kw * k.kh >= 65536;
-        if (engine[i] == kCake16) CUDA_TRY(launch_sweep_cake16(a, cs, grid[i], st));
-        else CUDA_TRY(launch_sweep_cake(a, cs, grid[i], st));
-      } else {
-        // direct per-pixel weighted histogram (baselines.cpp:24-69)
-        const int kw = k.kw, kh = k.kh, hx = k_hx(k), hy = k_hy(k);
-        (void)hx;
-        (void)hy;
-        BruteArgs ba{};
-        ST_TRY(weight_grid(c, k, &ba.grid));
-        ba.fi = t->fi;
-        ba.fi_pitch = t->fip;
-        ba.kw = kw;
-        ba.kh = kh;
-        ba.integer = k_integer(k);
-        CUDA_TRY(launch_sweep_brute(a, ba, grid[i].x, st));
-      }
-      if (engine[i] != kExp64 && !r.partial_out) {  // (exp reduces its own peaks)
-        c->launches += 1;
-        CUDA_TRY(launch_peak_reduce(parts, (int)(grid[i].x * grid[i].y), mws[i], a.hx, a.hy,
+    double* dscores = dev_map(i) ? scores_dev[i] : static_cast<double*>(S.scores.p) + p.soff;
+    PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + p.poff;
+    static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
+    fill_sweep_args(a, t, r, p, dscores, parts);
+    if (p.engine == kExp64) {  // reduces (and re-scores) its own peak
+      char* slice = static_cast<char*>(S.resc.p) + RescoreSlice::kBytes * i;
+      ST_TRY(run_exp(c, t, r, p, a, parts, dpeaks + i, slice, st));
+    } else {
+      if (p.engine == kQuad) ST_TRY(run_quad(t, p, a, st));
+      else if (p.engine == kAffine32) ST_TRY(run_affine(t, p, a, st));
+      else if (p.engine == kBrute) ST_TRY(run_brute(c, t, p, a, st));
+      else ST_TRY(run_cake(t, r, p, a, st));
+      c->launches += 1;
+      if (!r.partial_out) {
+        CUDA_TRY(launch_peak_reduce(parts, (int)(p.grid.x * p.grid.y), p.mw, a.hx, a.hy,
                                     dpeaks + i, st));
         c->launches += 1;
       }
     }
-    if (scores_host && scores_host[i] && rows > 0) {
+    if (host_map(i)) {
       // the copy stream takes the finished map while the next scale sweeps
       while (c->events.size() <= (size_t)i) {
         cudaEvent_t ev;
@@ -1676,7 +1723,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       }
       CUDA_TRY(cudaEventRecord(c->events[i], st));
       CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[i], 0));
-      CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)rows * mws[i] * 8,
+      CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)p.rows * p.mw * 8,
                                cudaMemcpyDeviceToHost, c->copy));
       copies = true;
     }
