@@ -358,7 +358,7 @@ def cpu_sample_text(wl, c):
 
 
 # ------------------------------------------------------------------ main
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -378,121 +378,152 @@ def main():
     ap.add_argument("--shard", default="rows", choices=["rows", "bins"],
                     help="config 4 over N>1 ranks: row bands per rank (default) or every "
                          "band on every rank with bin ranges chained rank to rank")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    return args
 
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    wl = workload(args.config)
 
-    if args.impl == "reference":
-        return run_reference(args, wl, rank, world)
+class OursArm:
+    """One rank of `bench.py --impl ours`.
 
-    import torch
-    from paper_1705_03524_b200 import swg, synth
-    # SWG_BENCH_SHARE_GPU=1: test mode for the N>1 code path on a 1-GPU box
-    # (every rank on cuda:0, gloo collectives; ranks never wait on each
-    # other's kernels, only on host barriers).  Never used for a reported run.
-    share = os.environ.get("SWG_BENCH_SHARE_GPU") == "1"
-    if share:
-        local = 0
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    A UNIT is one table set and the requests swept on it per step: dict with
+    t (Tables), src (device source view), pitch, reqs, maps (device score
+    outputs), peaks, g (group index), sidx (scale index per request), h2d
+    (input bytes), chunks [(bin0, requests)] (one entry unless the bins are
+    walked in ranges), and for the rank-to-rank bin chain pin / pout (/ token).
+    """
 
-    weak = wl["scaling"] == "weak"
-    data = wl["gen"](1 + rank if weak else 1)
-    ctx = swg.Context(local)
-    # a non-default torch stream: our launches and the CUDA events share it
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    ctx.set_stream(stream.cuda_stream)
-    models = make_models(ctx, wl, data)
-    fmt, nb = wl["fmt"], wl["nbins"]
+    def __init__(self, args, wl):
+        import torch
+        from paper_1705_03524_b200 import swg
+        self.torch, self.swg = torch, swg
+        self.args, self.wl = args, wl
+        self.rank = int(os.environ.get("RANK", 0))
+        self.world = int(os.environ.get("WORLD_SIZE", 1))
+        self.local = int(os.environ.get("LOCAL_RANK", 0))
+        # SWG_BENCH_SHARE_GPU=1: test mode for the N>1 code path on a 1-GPU box
+        # (every rank on cuda:0, gloo collectives; ranks never wait on each
+        # other's kernels, only on host barriers).  Never used for a reported run.
+        self.share = os.environ.get("SWG_BENCH_SHARE_GPU") == "1"
+        if self.share:
+            self.local = 0
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        self.weak = wl["scaling"] == "weak"
+        self.data = wl["gen"](1 + self.rank if self.weak else 1)
+        self.ctx = swg.Context(self.local)
+        # a non-default torch stream: our launches and the CUDA events share it
+        self.stream = torch.cuda.Stream()
+        torch.cuda.set_stream(self.stream)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.models = make_models(self.ctx, wl, self.data)
+        self.fmt, self.nb = wl["fmt"], wl["nbins"]
+        self.bins_mode = args.shard == "bins" and self.world > 1
+        self.units = []
+        self.batch_peaks = None
+        self.build_units()
 
-    bins_mode = args.shard == "bins" and world > 1
-
-    def group_chunks(g):
+    # ------------------------------------------------------------ set-up
+    def group_chunks(self, g):
         """Bin ranges one GPU walks for this group (1: all bins at once)."""
-        if bins_mode:
+        if self.bins_mode:
             return 1
-        if args.bin_chunks is not None:
-            return args.bin_chunks
+        if self.args.bin_chunks is not None:
+            return self.args.bin_chunks
         if g.get("decay") and os.environ.get("SWG_DECAY_CHUNKS"):  # tuning override
             return int(os.environ["SWG_DECAY_CHUNKS"])
         return g.get("bin_chunks", 1)
 
-    def new_tables(g, src, pitch=0):
-        if group_chunks(g) > 1:  # the first bin range; the rest via rebuild_bins
+    def new_tables(self, g, src, pitch=0):
+        wl, ctx = self.wl, self.ctx
+        if self.group_chunks(g) > 1:  # the first bin range; the rest via rebuild_bins
             from paper_1705_03524_b200 import dist as D
-            b0, b1 = D.bin_ranges(nb, group_chunks(g))[0]
-            return ctx.build_bins(src, b0, b1, fmt, wl["bins"], g["planes"],
+            b0, b1 = D.bin_ranges(self.nb, self.group_chunks(g))[0]
+            return ctx.build_bins(src, b0, b1, self.fmt, wl["bins"], g["planes"],
                                   decay=g.get("decay") or 0.0, pitch=pitch)
         if g.get("decay"):
-            return ctx.build_decay(src, g["decay"], fmt, wl["bins"], pitch=pitch)
-        return ctx.build(src, fmt, wl["bins"], g["planes"], pitch=pitch)
+            return ctx.build_decay(src, g["decay"], self.fmt, wl["bins"], pitch=pitch)
+        return ctx.build(src, self.fmt, wl["bins"], g["planes"], pitch=pitch)
 
-    # ---- units: (tables, device source view, pitch, requests, score outputs, peaks)
-    units = []
-    if wl["kind"] == "frame":
-        frame_dev = torch.from_numpy(data.image).cuda()
+    def _requests(self, g, ms):
+        swg = self.swg
+        return [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
+                for (k, meth, rings, _), m in zip(g["scales"], ms)]
+
+    def _map_buffers(self, t, reqs):
+        torch = self.torch
+        return [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
+                for r in reqs]
+
+    def _frame_units(self):
+        """c1 / c2 / c5: one table set per group over the whole frame."""
+        data = self.data
+        frame_dev = self.torch.from_numpy(data.image).cuda()
         H, W = data.image.shape[:2]
-        for gi, (g, ms) in enumerate(zip(wl["groups"], models)):
-            t = new_tables(g, frame_dev)
-            reqs = [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
-                    for (k, meth, rings, _), m in zip(g["scales"], ms)]
-            maps = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
-                    for r in reqs]
-            units.append(dict(t=t, src=frame_dev, pitch=0, reqs=reqs, maps=maps, g=gi,
-                              sidx=list(range(len(reqs))), h2d=data.image.nbytes))
-        tab_w, tab_h = W, H
-    elif wl["kind"] == "sequence":
+        for gi, (g, ms) in enumerate(zip(self.wl["groups"], self.models)):
+            t = self.new_tables(g, frame_dev)
+            reqs = self._requests(g, ms)
+            self.units.append(dict(t=t, src=frame_dev, pitch=0, reqs=reqs,
+                                   maps=self._map_buffers(t, reqs), g=gi,
+                                   sidx=list(range(len(reqs))), h2d=data.image.nbytes))
+        self.tab_w, self.tab_h = W, H
+
+    def _sequence_units(self):
+        """c3: this rank's frames, each a search region swept on one table set."""
+        from paper_1705_03524_b200 import synth
+        data, rank, world = self.data, self.rank, self.world
         F, H, W = data.frames.shape[:3]
-        frames_dev = torch.from_numpy(data.frames).cuda()
+        frames_dev = self.torch.from_numpy(data.frames).cuda()
         S = data.search
-        g, ms = wl["groups"][0], models[0]
+        g, ms = self.wl["groups"][0], self.models[0]
         mine = [f for f in range(F) if f % world == rank]
         x0, y0 = synth.search_origin(data, mine[0])
-        t = new_tables(g, frames_dev[mine[0], y0:y0 + S, x0:x0 + S], pitch=W * 3)
-        reqs = [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
-                for (k, meth, rings, _), m in zip(g["scales"], ms)]
-        maps = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
-                for r in reqs]  # one map per scale, overwritten frame after frame
+        t = self.new_tables(g, frames_dev[mine[0], y0:y0 + S, x0:x0 + S], pitch=W * 3)
+        reqs = self._requests(g, ms)
+        maps = self._map_buffers(t, reqs)  # one map per scale, overwritten frame after frame
         for f in mine:
             x0, y0 = synth.search_origin(data, f)
-            units.append(dict(t=t, src=frames_dev[f, y0:y0 + S, x0:x0 + S], pitch=W * 3,
-                              reqs=reqs, maps=maps, g=0, sidx=list(range(len(reqs))),
-                              frame=f, origin=(x0, y0), h2d=S * S * 3))
-        tab_w = tab_h = S
-    else:  # row bands
+            self.units.append(dict(t=t, src=frames_dev[f, y0:y0 + S, x0:x0 + S], pitch=W * 3,
+                                   reqs=reqs, maps=maps, g=0, sidx=list(range(len(reqs))),
+                                   frame=f, origin=(x0, y0), h2d=S * S * 3))
+        self.tab_w = self.tab_h = S
+        self.frame_hw, self.search = (H, W), S
+        self.batch_peaks = self.torch.zeros(len(self.units) * len(reqs), 3,
+                                            dtype=self.torch.float64, device="cuda")
+
+    def _band_units(self):
+        """c4: row bands (one per rank, or more if a band's tables do not fit)."""
+        torch, swg, ctx, wl = self.torch, self.swg, self.ctx, self.wl
+        data, rank, world = self.data, self.rank, self.world
         H, W = data.image.shape[:2]
         frame_dev = torch.from_numpy(data.image).cuda()
-        g, ms = wl["groups"][0], models[0]
+        g, ms = wl["groups"][0], self.models[0]
         full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
                      for k, _, _, _ in g["scales"]]
         # one row band per rank (the whole frame on one GPU: 136 GB of decay
         # tables, the band halo costs more than it saves); twice as many if a
         # band's tables do not fit
-        n_bands = int(os.environ.get("SWG_C4_BANDS", 1 if not bins_mode else 4))
-        n_bands = max(n_bands, world) if not bins_mode else n_bands
+        n_bands = int(os.environ.get("SWG_C4_BANDS", 1 if not self.bins_mode else 4))
+        n_bands = max(n_bands, world) if not self.bins_mode else n_bands
         while True:
             BH, plan = band_plan(H, g["scales"], n_bands)
-            mine = list(range(n_bands)) if bins_mode else \
+            mine = list(range(n_bands)) if self.bins_mode else \
                 [b for b in range(n_bands) if b % world == rank]
             try:
-                if bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e)
+                if self.bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e)
                     from paper_1705_03524_b200 import dist as D
-                    b0, b1 = D.bin_ranges(nb, world)[rank]
-                    t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, fmt,
+                    b0, b1 = D.bin_ranges(self.nb, world)[rank]
+                    t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, self.fmt,
                                        wl["bins"], g["planes"], decay=g.get("decay") or 0.0)
                 else:
-                    t = new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+                    t = self.new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
                 break
             except swg.CapacityError:
                 if n_bands >= 64:
@@ -509,26 +540,33 @@ def main():
                                            rows=(v0 - p0, v1 - p0)))
                 maps.append(full_maps[si][v0:v1])
                 sidx.append(si)
-            units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs, maps=maps,
-                              g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
-        if bins_mode and args.p2p == "peer":
+            self.units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs,
+                                   maps=maps, g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
+        if self.bins_mode:
+            self._attach_rank_chain()
+        self.tab_w, self.tab_h = W, BH
+
+    def _attach_rank_chain(self):
+        """--shard bins: running (s, mass) per window passed rank to rank."""
+        torch, swg, rank, world = self.torch, self.swg, self.rank, self.world
+        last = rank == world - 1
+        if self.args.p2p == "peer":
             # running (s, mass) per window written by rank g's sweep STRAIGHT
             # into rank g+1's input buffer (peer memory mapped with an IPC
             # handle; NVLink stores from the kernel's epilogue); only a 4-byte
             # token per request goes through the process group, stream-ordered
             # behind the kernel
-            last = rank == world - 1
             mine_h = []
-            for u in units:
+            for u in self.units:
                 u["pin"] = []
                 for m in u["maps"]:
                     buf = swg.device_alloc(m.numel() * 16) if rank > 0 else None
                     u["pin"].append(buf)
                     mine_h.append(swg.ipc_export(buf) if buf else None)
             every = [None] * world
-            dist.all_gather_object(every, mine_h)
+            self.dist.all_gather_object(every, mine_h)
             k = 0
-            for u in units:
+            for u in self.units:
                 u["pout"] = []
                 for i, r in enumerate(u["reqs"]):
                     peer = None if last else swg.ipc_import(every[rank + 1][k])
@@ -538,72 +576,104 @@ def main():
                 if not last:
                     u["maps"] = [m[:0] for m in u["maps"]]  # no scores off the last rank
                 u["token"] = torch.zeros(1, dtype=torch.float32,
-                                         device="cpu" if share else "cuda")
-        elif bins_mode:
-            # running (s, mass) per window: received from rank-1, sent to rank+1
-            last = rank == world - 1
-            for u in units:
-                u["pin"] = [torch.empty(tuple(m.shape) + (2,), dtype=torch.float64,
-                                        device="cuda") if rank > 0 else None for m in u["maps"]]
-                u["pout"] = [None if last else torch.empty(tuple(m.shape) + (2,),
-                                                           dtype=torch.float64, device="cuda")
-                             for m in u["maps"]]
-                for i, r in enumerate(u["reqs"]):
-                    r.partial_in, r.partial_out = u["pin"][i], u["pout"][i]
-                if not last:
-                    u["maps"] = [m[:0] for m in u["maps"]]  # no scores off the last rank
-        tab_w, tab_h = W, BH
-    for u in units:
-        u["peaks"] = torch.zeros(len(u["reqs"]), 3, dtype=torch.float64, device="cuda")
-        nchunk = group_chunks(wl["groups"][u["g"]])
-        if nchunk > 1:
-            # bins walked in `nchunk` ranges per step with the running sums
-            # chained range to range on this GPU (the partial-sum chain of the
-            # multi-GPU bin split): 1/nchunk of the decay planes per sweep, so a
-            # window's corner rows stay in L2
-            from dataclasses import replace
-            from paper_1705_03524_b200 import dist as D
-            ranges = D.bin_ranges(nb, nchunk)
-            bufs = [[torch.empty(tuple(m.shape) + (2,), dtype=torch.float64, device="cuda")
-                     for _ in range(2)] for m in u["maps"]]
-            u["chunks"] = []
-            for c, (b0, _) in enumerate(ranges):
-                creqs = [replace(r, partial_in=bufs[i][(c - 1) % 2] if c else None,
-                                 partial_out=bufs[i][c % 2] if c < nchunk - 1 else None)
-                         for i, r in enumerate(u["reqs"])]
-                u["chunks"].append((b0, creqs))
-            u["bins_per_launch"] = ranges[0][1] - ranges[0][0]
-        u.setdefault("chunks", [(None, u["reqs"])])
-    n_win = sum(m.numel() for u in units for m in u["maps"]) if wl["kind"] != "sequence" else \
-        sum(m.numel() for m in units[0]["maps"]) * len(units)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+                                         device="cpu" if self.share else "cuda")
+            return
+        # NCCL: received from rank-1, sent to rank+1
+        for u in self.units:
+            u["pin"] = [torch.empty(tuple(m.shape) + (2,), dtype=torch.float64,
+                                    device="cuda") if rank > 0 else None for m in u["maps"]]
+            u["pout"] = [None if last else torch.empty(tuple(m.shape) + (2,),
+                                                       dtype=torch.float64, device="cuda")
+                         for m in u["maps"]]
+            for i, r in enumerate(u["reqs"]):
+                r.partial_in, r.partial_out = u["pin"][i], u["pout"][i]
+            if not last:
+                u["maps"] = [m[:0] for m in u["maps"]]  # no scores off the last rank
 
-    def p2p_send(x, dst):  # NCCL over NVLink; gloo (shared-GPU test mode) stages on the host
-        if share:
-            dist.send(x.cpu(), dst=dst)
+    def _attach_bin_walk(self, u):
+        """Bins walked in ranges on this GPU with the running sums chained range
+        to range (the partial-sum chain of the multi-GPU bin split): 1/nchunk of
+        the decay planes per sweep, so a window's corner rows stay in L2."""
+        torch = self.torch
+        nchunk = self.group_chunks(self.wl["groups"][u["g"]])
+        if nchunk <= 1:
+            u["chunks"] = [(None, u["reqs"])]
+            return
+        from dataclasses import replace
+        from paper_1705_03524_b200 import dist as D
+        ranges = D.bin_ranges(self.nb, nchunk)
+        bufs = [[torch.empty(tuple(m.shape) + (2,), dtype=torch.float64, device="cuda")
+                 for _ in range(2)] for m in u["maps"]]
+        u["chunks"] = []
+        for c, (b0, _) in enumerate(ranges):
+            creqs = [replace(r, partial_in=bufs[i][(c - 1) % 2] if c else None,
+                             partial_out=bufs[i][c % 2] if c < nchunk - 1 else None)
+                     for i, r in enumerate(u["reqs"])]
+            u["chunks"].append((b0, creqs))
+        u["bins_per_launch"] = ranges[0][1] - ranges[0][0]
+
+    def build_units(self):
+        kind = self.wl["kind"]
+        if kind == "frame":
+            self._frame_units()
+        elif kind == "sequence":
+            self._sequence_units()
         else:
-            dist.send(x, dst=dst)
+            self._band_units()
+        for u in self.units:
+            u["peaks"] = self.torch.zeros(len(u["reqs"]), 3, dtype=self.torch.float64,
+                                          device="cuda")
+            self._attach_bin_walk(u)
+        if kind == "sequence":
+            self.n_win = sum(m.numel() for m in self.units[0]["maps"]) * len(self.units)
+        else:
+            self.n_win = sum(m.numel() for u in self.units for m in u["maps"])
+        self.chained = any("pin" in u for u in self.units)
+        self.flush = self.torch.empty(256 << 20, dtype=self.torch.uint8, device="cuda")
 
-    def p2p_recv(x, src):
-        if share:
-            h = torch.empty(x.shape, dtype=x.dtype)
-            dist.recv(h, src=src)
+    # ------------------------------------------------------------ the step
+    def p2p_send(self, x, dst):  # NCCL over NVLink; gloo (shared-GPU test mode) stages on the host
+        if self.share:
+            self.dist.send(x.cpu(), dst=dst)
+        else:
+            self.dist.send(x, dst=dst)
+
+    def p2p_recv(self, x, src):
+        if self.share:
+            h = self.torch.empty(x.shape, dtype=x.dtype)
+            self.dist.recv(h, src=src)
             x.copy_(h)
         else:
-            dist.recv(x, src=src)
+            self.dist.recv(x, src=src)
 
-    batch_peaks = None
-    if wl["kind"] == "sequence":
-        batch_peaks = torch.zeros(len(units) * len(units[0]["reqs"]), 3, dtype=torch.float64,
-                                  device="cuda")
+    def _chain_sweep(self, u, i, r):
+        """One request of the rank-to-rank bin chain: receive, sweep, send."""
+        rank, world = self.rank, self.world
+        if rank > 0:
+            if "token" in u:  # the sums are already in u["pin"][i]
+                self.p2p_recv(u["token"], rank - 1)
+            else:
+                self.p2p_recv(u["pin"][i], rank - 1)
+        u["t"].likelihood_maps([r], scores="none",
+                               scores_dev=None if r.partial_out is not None else [u["maps"][i]],
+                               peaks_dev=u["peaks"][i])
+        if rank < world - 1:
+            if "token" in u:  # stream-ordered behind the sweep's peer stores
+                if self.share:
+                    self.torch.cuda.synchronize()
+                self.p2p_send(u["token"], rank + 1)
+            else:
+                self.p2p_send(u["pout"][i], rank + 1)
 
-    def step(ev=None):
-        if ev is None and batch_peaks is not None:
+    def step(self, ev=None):
+        """One pass of the hot path.  ev: per-launch timing events (eager)."""
+        units = self.units
+        if ev is None and self.batch_peaks is not None:
             # the tracking batch through swg_likelihood_batch: frames round-robin
             # over the library's table sets / worker streams (build of one
             # frame overlaps the sweeps of another)
             units[0]["t"].likelihood_batch([u["src"] for u in units], units[0]["reqs"],
-                                           pitch=units[0]["pitch"], peaks_dev=batch_peaks)
+                                           pitch=units[0]["pitch"], peaks_dev=self.batch_peaks)
             return
         j = 0
         for u in units:
@@ -628,346 +698,381 @@ def main():
                                            peaks_dev=u["peaks"])
                     continue
                 for i, r in enumerate(creqs):
-                    if "pin" in u and rank > 0:
-                        if "token" in u:  # the sums are already in u["pin"][i]
-                            p2p_recv(u["token"], rank - 1)
-                        else:
-                            p2p_recv(u["pin"][i], rank - 1)
-                    u["t"].likelihood_maps([r], scores="none",
-                                           scores_dev=None if r.partial_out is not None
-                                           else [u["maps"][i]], peaks_dev=u["peaks"][i])
-                    if "pin" in u and rank < world - 1:
-                        if "token" in u:  # stream-ordered behind the sweep's peer stores
-                            if share:
-                                torch.cuda.synchronize()
-                            p2p_send(u["token"], rank + 1)
-                        else:
-                            p2p_send(u["pout"][i], rank + 1)
+                    if "pin" in u:
+                        self._chain_sweep(u, i, r)
+                    else:
+                        u["t"].likelihood_maps([r], scores="none",
+                                               scores_dev=None if r.partial_out is not None
+                                               else [u["maps"][i]], peaks_dev=u["peaks"][i])
                     if ev:
                         ev[j].record()
                         j += 1
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    # ------------------------------------------------------------ timing
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
 
-    # The step as one CUDA graph (no host launch gaps between the kernels).
-    graph = None
-    if not args.no_graph and not any("pin" in u for u in units):  # (p2p chain: eager)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            step()
+    def reduce_ranks(self, v, op="max"):
+        if not self.dist:
+            return float(v)
+        t = self.torch.tensor([float(v)], device="cpu" if self.share else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def time_device(self):
+        """Per-launch events over K eager steps, then (headline) K graph replays.
+
+        Returns (per-step ms, eager events, clocks, launches over the K steps)."""
+        torch, args = self.torch, self.args
         for _ in range(args.warmup):
-            graph.replay()
+            self.step()
         torch.cuda.synchronize()
-
-    nev = sum(2 + len(cr) for u in units for _, cr in u["chunks"])
-    events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
-    clocks = Clocks(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = ctx.launches
-    clocks.start()
-    t_host = time.perf_counter()
-    step()
-    torch.cuda.synchronize()
-    enqueue_s = time.perf_counter() - t_host  # host time of one eager step (sizes the spin)
-    launches0 = ctx.launches
-    for s in range(args.steps):
-        # a spin longer than the host's enqueue time lets the whole step queue
-        # up before the GPU reaches it, so the per-kernel events carry no host
-        # launch gaps
-        torch.cuda._sleep(int(max(2e6, 2.5e9 * enqueue_s)))
-        flush.zero_()  # evict L2 (256 MiB > 126 MB) between timed steps; not timed
-        step(events[s])
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    launches = ctx.launches - launches0  # over the K timed steps
-    if dist:
-        dist.barrier()
-    per_step = [events[s][0].elapsed_time(events[s][-1]) for s in range(args.steps)]
-    # headline timing: graph replays (same kernels, no launch gaps)
-    if graph is not None:
-        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
-               for _ in range(args.steps)]
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        clocks = Clocks(local)
-        clocks.start()
-        # soak: keep the GPU under this load for >= 1 s so the clock sampler
-        # (100 ms period) sees it; the timed steps follow immediately
-        t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 1.0:
-            for _ in range(4):
+        # the step as one CUDA graph (no host launch gaps between the kernels)
+        graph = None
+        if not args.no_graph and not self.chained:  # (p2p chain: eager)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=self.stream):
+                self.step()
+            for _ in range(args.warmup):
                 graph.replay()
             torch.cuda.synchronize()
+
+        nev = sum(2 + len(cr) for u in self.units for _, cr in u["chunks"])
+        events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+                  for _ in range(args.steps)]
+        clocks = Clocks(self.local)
+        self.barrier()
+        torch.cuda.synchronize()
+        clocks.start()
+        t_host = time.perf_counter()
+        self.step()
+        torch.cuda.synchronize()
+        enqueue_s = time.perf_counter() - t_host  # host time of one eager step (sizes the spin)
+        launches0 = self.ctx.launches
         for s in range(args.steps):
-            flush.zero_()
-            gev[s][0].record()
-            graph.replay()
-            gev[s][1].record()
+            # a spin longer than the host's enqueue time lets the whole step queue
+            # up before the GPU reaches it, so the per-kernel events carry no host
+            # launch gaps
+            torch.cuda._sleep(int(max(2e6, 2.5e9 * enqueue_s)))
+            self.flush.zero_()  # evict L2 (256 MiB > 126 MB) between timed steps; not timed
+            self.step(events[s])
         torch.cuda.synchronize()
         clk = clocks.stop()
-        if dist:
-            dist.barrier()
-        per_step = [gev[s][0].elapsed_time(gev[s][1]) for s in range(args.steps)]
+        launches = self.ctx.launches - launches0  # over the K timed steps
+        self.barrier()
+        per_step = [events[s][0].elapsed_time(events[s][-1]) for s in range(args.steps)]
+        if graph is not None:  # headline timing: graph replays (same kernels, no launch gaps)
+            gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                   for _ in range(args.steps)]
+            self.barrier()
+            torch.cuda.synchronize()
+            clocks = Clocks(self.local)
+            clocks.start()
+            # soak: keep the GPU under this load for >= 1 s so the clock sampler
+            # (100 ms period) sees it; the timed steps follow immediately
+            t_soak = time.perf_counter()
+            while time.perf_counter() - t_soak < 1.0:
+                for _ in range(4):
+                    graph.replay()
+                torch.cuda.synchronize()
+            for s in range(args.steps):
+                self.flush.zero_()
+                gev[s][0].record()
+                graph.replay()
+                gev[s][1].record()
+            torch.cuda.synchronize()
+            clk = clocks.stop()
+            self.barrier()
+            per_step = [gev[s][0].elapsed_time(gev[s][1]) for s in range(args.steps)]
+        return per_step, events, clk, launches
 
-    # per-launch times: build per unit, sweep per (unit, request)
-    build_ms, sweep_ms = [], {}  # sweep_ms[(group, scale)] = list of per-launch ms
-    for s in range(args.steps):
-        j = 0
-        for ui, u in enumerate(units):
-            e = events[s]
-            for _, creqs in u["chunks"]:
-                build_ms.append(e[j].elapsed_time(e[j + 1]))
-                j += 1
-                for i in range(len(creqs)):
-                    sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
-                        e[j].elapsed_time(e[j + 1]))
+    def launch_times(self, events):
+        """Per-launch ms from the eager events: builds, and sweeps per (group, scale)."""
+        build_ms, sweep_ms = [], {}
+        for e in events:
+            j = 0
+            for u in self.units:
+                for _, creqs in u["chunks"]:
+                    build_ms.append(e[j].elapsed_time(e[j + 1]))
                     j += 1
-                j += 1
-    total_ms = sum(per_step)
-    if dist:
-        t = torch.tensor([total_ms], device="cpu" if share else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        nw = torch.tensor([float(n_win)], device="cpu" if share else "cuda")
-        dist.all_reduce(nw, op=dist.ReduceOp.SUM)
-        job_win = float(nw.item())
-    else:
-        job_win = float(n_win)
-    value = job_win * args.steps / (total_ms / 1e3)
+                    for i in range(len(creqs)):
+                        sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
+                            e[j].elapsed_time(e[j + 1]))
+                        j += 1
+                    j += 1
+        return build_ms, sweep_ms
 
-    # correctness spot check of the timed outputs (peaks on the planted targets)
-    ok_peaks = None
-    if wl["kind"] == "frame":
-        ok_peaks = True
-        for u in units:
-            pk = u["peaks"].cpu().numpy()
-            g = wl["groups"][u["g"]]
-            for i, si in enumerate(u["sidx"]):
-                ti = g["scales"][si][3]
-                if ti is None:
-                    continue
-                ints = pk[i, :2].view(np.int32)
-                tx, ty = target_center(data, ti)
-                ok_peaks &= abs(int(ints[2]) - tx) <= 1 and abs(int(ints[3]) - ty) <= 1
-        ok_peaks = bool(ok_peaks)
-    elif wl["kind"] == "sequence":
-        hits = tot = 0
-        for u in units:
-            pk = u["peaks"].cpu().numpy()
-            gx, gy = data.track[u["frame"]]
-            for i in range(len(u["reqs"])):
-                ints = pk[i, :2].view(np.int32)
-                cx, cy = int(ints[2]) + u["origin"][0], int(ints[3]) + u["origin"][1]
-                hits += abs(cx - gx) <= 2 and abs(cy - gy) <= 2
-                tot += 1
-        ok_peaks = f"{hits}/{tot} frame-scale peaks within 2 px of ground truth"
-
-    # ---- e2e through the C-ABI with host buffers (pinned)
-    import ctypes as C
-    from paper_1705_03524_b200.swg import Peak, _Req, _check, lib
-    e2e = None
-    if not args.no_e2e and not any("pin" in u for u in units):
-        h2d = d2h = 0
+    def peaks_on_targets(self):
+        """Spot check of the timed outputs: peaks on the planted targets."""
+        wl, data = self.wl, self.data
+        if wl["kind"] == "frame":
+            ok = True
+            for u in self.units:
+                pk = u["peaks"].cpu().numpy()
+                g = wl["groups"][u["g"]]
+                for i, si in enumerate(u["sidx"]):
+                    ti = g["scales"][si][3]
+                    if ti is None:
+                        continue
+                    ints = pk[i, :2].view(np.int32)
+                    tx, ty = target_center(data, ti)
+                    ok &= abs(int(ints[2]) - tx) <= 1 and abs(int(ints[3]) - ty) <= 1
+            return bool(ok)
         if wl["kind"] == "sequence":
-            pin = swg.PinnedBuffer(data.frames.shape, np.uint8)
-            pin.array[...] = data.frames
-            base = pin.array.ctypes.data
-            addrs = [base + ((u["frame"] * H + u["origin"][1]) * W + u["origin"][0]) * 3
-                     for u in units]
-            fr = (C.c_void_p * len(addrs))(*addrs)
-            t = units[0]["t"]
-            creqs, _keep = swg.Tables._creqs(units[0]["reqs"], nb)
-            nreq = len(units[0]["reqs"])
-            peaks_host = (Peak * (len(addrs) * nreq))()
+            hits = tot = 0
+            for u in self.units:
+                pk = u["peaks"].cpu().numpy()
+                gx, gy = data.track[u["frame"]]
+                for i in range(len(u["reqs"])):
+                    ints = pk[i, :2].view(np.int32)
+                    cx, cy = int(ints[2]) + u["origin"][0], int(ints[3]) + u["origin"][1]
+                    hits += abs(cx - gx) <= 2 and abs(cy - gy) <= 2
+                    tot += 1
+            return f"{hits}/{tot} frame-scale peaks within 2 px of ground truth"
+        return None
 
-            def e2e_step():
-                _check(lib().swg_likelihood_batch(t._h, len(addrs), C.addressof(fr), 0, W * 3,
-                                                  nreq, C.addressof(creqs),
-                                                  C.addressof(peaks_host), None))
-            h2d = len(addrs) * S * S * 3
-            d2h = C.sizeof(peaks_host)
-            check = None
+    # ------------------------------------------------------------ e2e
+    def _e2e_sequence(self):
+        """c3: the frames' search regions from pinned host memory through
+        swg_likelihood_batch, host peaks out."""
+        import ctypes as C
+        from paper_1705_03524_b200.swg import Peak, _check, lib
+        swg, data, units = self.swg, self.data, self.units
+        (H, W), S = self.frame_hw, self.search
+        pin = swg.PinnedBuffer(data.frames.shape, np.uint8)
+        pin.array[...] = data.frames
+        base = pin.array.ctypes.data
+        addrs = [base + ((u["frame"] * H + u["origin"][1]) * W + u["origin"][0]) * 3
+                 for u in units]
+        fr = (C.c_void_p * len(addrs))(*addrs)
+        t = units[0]["t"]
+        creqs, _keep = swg.Tables._creqs(units[0]["reqs"], self.nb)
+        nreq = len(units[0]["reqs"])
+        peaks_host = (Peak * (len(addrs) * nreq))()
+
+        def e2e_step():
+            _check(lib().swg_likelihood_batch(t._h, len(addrs), C.addressof(fr), 0, W * 3,
+                                              nreq, C.addressof(creqs),
+                                              C.addressof(peaks_host), None))
+        keep = (pin, fr, creqs, _keep, peaks_host)
+        return e2e_step, None, len(addrs) * S * S * 3, C.sizeof(peaks_host), keep
+
+    def _e2e_tables(self):
+        """Frames / bands: rebuild from the pinned host frame, host maps + peaks out."""
+        import ctypes as C
+        from paper_1705_03524_b200.swg import Peak, _check, lib
+        swg, data, units, nb = self.swg, self.data, self.units, self.nb
+        pin = swg.PinnedBuffer(data.image.shape, data.image.dtype)
+        pin.array[...] = data.image
+        row_bytes = data.image.strides[0]
+        calls, maps_pin = [], []
+        h2d = d2h = 0
+        for u in units:
+            mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
+            maps_pin.append(mp)
+            hp = (C.c_void_p * len(mp))(*[m.array.ctypes.data for m in mp])
+            pk = (Peak * len(u["reqs"]))()
+            src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
+            # per bin range (one range unless the bins are walked in chunks):
+            # rebuild (upload the frame on the first), requests; host maps
+            # and peaks from the last range
+            for c, (b0, cr) in enumerate(u["chunks"]):
+                creqs, keep = swg.Tables._creqs(cr, nb)
+                last = c == len(u["chunks"]) - 1
+                calls.append((u["t"], src if c == 0 else None, b0, len(u["chunks"]) > 1,
+                              creqs, keep, hp if last else None, pk, len(cr)))
+            h2d += u["h2d"]
+            d2h += sum(m.nbytes for m in mp) + C.sizeof(pk)
+
+        def e2e_step():
+            for t, src, b0, walk, creqs, _k, hp, pk, n in calls:
+                if walk:  # bin ranges: the frame with the first range, then ranges
+                    _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
+                else:
+                    _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
+                _check(lib().swg_likelihood_maps(
+                    t._h, n, C.addressof(creqs),
+                    C.addressof(hp) if hp is not None else None, None, C.addressof(pk), None))
+
+        def check():
+            for u, mp in zip(units, maps_pin):
+                for m, mpin in zip(u["maps"], mp):
+                    assert (mpin.array == m.cpu().numpy()).all()
+        return e2e_step, check, h2d, d2h, (pin, calls, maps_pin)
+
+    def e2e(self, job_win):
+        """The metric through the C-ABI with pinned host input and host outputs,
+        host<->device copies inside the timed region (wall clock per step)."""
+        args, torch = self.args, self.torch
+        if args.no_e2e or self.chained:
+            return None
+        if self.wl["kind"] == "sequence":
+            e2e_step, check, h2d, d2h, _keep = self._e2e_sequence()
         else:
-            pin = swg.PinnedBuffer(data.image.shape, data.image.dtype)
-            pin.array[...] = data.image
-            row_bytes = data.image.strides[0]
-            calls = []
-            maps_pin = []
-            for u in units:
-                mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
-                maps_pin.append(mp)
-                hp = (C.c_void_p * len(mp))(*[m.array.ctypes.data for m in mp])
-                pk = (Peak * len(u["reqs"]))()
-                src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
-                # per bin range (one range unless the bins are walked in chunks):
-                # rebuild (upload the frame on the first), requests; host maps
-                # and peaks from the last range
-                for c, (b0, cr) in enumerate(u["chunks"]):
-                    creqs, keep = swg.Tables._creqs(cr, nb)
-                    last = c == len(u["chunks"]) - 1
-                    calls.append((u["t"], src if c == 0 else None, b0,
-                                  len(u["chunks"]) > 1, creqs, keep,
-                                  hp if last else None, pk, len(cr)))
-                h2d += u["h2d"]
-                d2h += sum(m.nbytes for m in mp) + C.sizeof(pk)
-
-            def e2e_step():
-                for t, src, b0, walk, creqs, _k, hp, pk, n in calls:
-                    if walk:  # bin ranges: the frame with the first range, then ranges
-                        _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
-                    else:
-                        _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
-                    _check(lib().swg_likelihood_maps(
-                        t._h, n, C.addressof(creqs),
-                        C.addressof(hp) if hp is not None else None, None, C.addressof(pk),
-                        None))
-
-            def check():
-                for u, mp in zip(units, maps_pin):
-                    for m, mpin in zip(u["maps"], mp):
-                        assert (mpin.array == m.cpu().numpy()).all()
-
+            e2e_step, check, h2d, d2h, _keep = self._e2e_tables()
         for _ in range(args.warmup):
             e2e_step()
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+        self.barrier()
         e2e_t = []
         for _ in range(args.steps):
-            flush.zero_()
+            self.flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e2e_step()  # returns after the host maps + peaks are filled
             e2e_t.append(time.perf_counter() - t0)
-        e2e_total = sum(e2e_t)
-        if dist:
-            t_ = torch.tensor([e2e_total], device="cpu" if share else "cuda")
-            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
-            e2e_total = float(t_.item())
+        e2e_total = self.reduce_ranks(sum(e2e_t))
         if check:
             check()
-        e2e = {"value": job_win * args.steps / e2e_total, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e2e_total / args.steps * 1e3}
+        return {"value": job_win * args.steps / e2e_total, "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_total / args.steps * 1e3}
 
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of the dominant launch and of the IH build (SURVEY §8d bytes)
-    hbm, src = peaks_json()
-    cells = (tab_w + 1) * (tab_h + 1) * nb
-    per_scale = {}
-    for (gi, si), ts in sweep_ms.items():
-        per_scale[(gi, si)] = sum(ts) / args.steps  # ms per step
-    dom = max(sweep_ms, key=lambda key: sum(sweep_ms[key]) / len(sweep_ms[key]))
-    gi, si = dom
-    g = wl["groups"][gi]
-    k, meth = g["scales"][si][0], g["scales"][si][1]
-    kname, P, e = engine_of(g, k, meth)
-    dom_ms = sum(sweep_ms[dom]) / len(sweep_ms[dom])
-    win_launch = {}
-    for u in units:
-        for i, s_ in enumerate(u["sidx"]):
-            win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
-    dom_win = sum(win_launch[dom]) / len(win_launch[dom])
-    launch_bins = next((u.get("bins_per_launch", nb) for u in units if u["g"] == gi), nb)
-    dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        tr = json.load(open(tp)).get(args.config)
-        if tr and kname in tr.get("kernel", ""):
-            traffic = tr["dram_bytes"]
-    roofline = {"bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9,
-                "peak": hbm, "unit": "GB/s", "traffic": traffic, "peak_source": src,
-                "kernel": f"{kname} at {k.kw}x{k.kh} (planes read once + 8 B/window = "
-                          f"{int(dom_bytes)} B per launch, {dom_ms:.4f} ms)"}
-    roofline["frac"] = roofline["achieved"] / hbm
-    # on-chip side of the same launch: the table records every window reads
-    # (corners x bins x entry bytes; the cake's full ring count, early exits
-    # not deducted) against the L1 load bandwidth (148 SMs x 128 B/clk at the
-    # SM clock sampled during the run)
-    # (the cake's ring count is cut short per window by its nested-box early
-    # exit, so its corner bytes are not known up front: its L1 utilisation is
-    # the ncu figure in profiles/, not an estimate here)
-    corners = {"k_sweep_affine": 20 if k.kind != swg.UNIFORM else 4, "k_sweep_quad": 20,
-               "k_sweep_exp": 16}.get(kname)
-    if corners:
-        onchip_bytes = corners * launch_bins * e * dom_win
-        sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
-        l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-        roofline["onchip"] = {"achieved": onchip_bytes / (dom_ms / 1e3) / 1e12,
-                              "peak": l1_peak, "unit": "TB/s", "bytes": int(onchip_bytes),
-                              "frac": onchip_bytes / (dom_ms / 1e3) / 1e12 / l1_peak,
-                              "peak_source": "148 SMs x 128 B/clk L1 at the sampled SM clock"}
-    else:
-        roofline["onchip"] = {"note": "the wedding-cake sweep is L1-load / issue bound; "
-                                      "L1TEX throughput from the ncu capture"}
-        src_txt = None
+    # ------------------------------------------------------------ rooflines
+    def _traffic_entry(self, kname):
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            tr = json.load(open(tp)).get(args.config)
+            tr = json.load(open(tp)).get(self.args.config)
             if tr and kname in tr.get("kernel", ""):
-                src_txt = os.path.join(ROOT, tr["source"])
-        if src_txt and os.path.exists(src_txt):
-            import re
-            m = re.search(r"l1tex__throughput\.avg\.pct_of_peak_sustained_active\s+([\d.]+)",
-                          open(src_txt).read())
-            if m:
-                roofline["onchip"]["l1tex_throughput_pct"] = float(m.group(1))
-                roofline["onchip"]["source"] = os.path.relpath(src_txt, ROOT)
-    build_avg = sum(build_ms) / args.steps  # ms per step, all rebuilds
-    in_bytes = sum(u["h2d"] for u in units)
-    build_bytes = in_bytes + sum(group_build_bytes(wl["groups"][u["g"]], tab_w, tab_h, nb)
-                                 for u in units)
-    build_roof = {"bound": "hbm", "achieved": build_bytes / (build_avg / 1e3) / 1e9, "peak": hbm,
-                  "unit": "GB/s", "ms": build_avg, "bytes": build_bytes,
-                  "kernel": "k_quantize + k_colsum + k_bandscan + k_build (per table set)"}
-    build_roof["frac"] = build_roof["achieved"] / hbm
+                return tr
+        return None
 
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        c = cpu_reference(wl, data, models, public_api=True)
+    def sweep_roofline(self, sweep_ms, clk):
+        """The dominant sweep launch against HBM (SURVEY §8d bytes), plus its
+        on-chip side."""
+        swg, wl, nb = self.swg, self.wl, self.nb
+        hbm, src = peaks_json()
+        cells = (self.tab_w + 1) * (self.tab_h + 1) * nb
+        dom = max(sweep_ms, key=lambda key: sum(sweep_ms[key]) / len(sweep_ms[key]))
+        gi, si = dom
+        g = wl["groups"][gi]
+        k, meth = g["scales"][si][0], g["scales"][si][1]
+        kname, P, e = engine_of(g, k, meth)
+        dom_ms = sum(sweep_ms[dom]) / len(sweep_ms[dom])
+        win_launch = {}
+        for u in self.units:
+            for i, s_ in enumerate(u["sidx"]):
+                win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
+        dom_win = sum(win_launch[dom]) / len(win_launch[dom])
+        launch_bins = next((u.get("bins_per_launch", nb) for u in self.units if u["g"] == gi), nb)
+        dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
+        tr = self._traffic_entry(kname)
+        roofline = {"bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9,
+                    "peak": hbm, "unit": "GB/s", "traffic": tr["dram_bytes"] if tr else None,
+                    "peak_source": src,
+                    "kernel": f"{kname} at {k.kw}x{k.kh} (planes read once + 8 B/window = "
+                              f"{int(dom_bytes)} B per launch, {dom_ms:.4f} ms)"}
+        roofline["frac"] = roofline["achieved"] / hbm
+        # on-chip side of the same launch: the table records every window reads
+        # (corners x bins x entry bytes) against the L1 load bandwidth (148 SMs
+        # x 128 B/clk at the SM clock sampled during the run).  The cake's ring
+        # count is cut short per window by its nested-box early exit, so its
+        # corner bytes are not known up front: its L1 utilisation is the ncu
+        # figure in profiles/, not an estimate here.
+        corners = {"k_sweep_affine": 20 if k.kind != swg.UNIFORM else 4, "k_sweep_quad": 20,
+                   "k_sweep_exp": 16}.get(kname)
+        if corners:
+            onchip_bytes = corners * launch_bins * e * dom_win
+            sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+            l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+            roofline["onchip"] = {"achieved": onchip_bytes / (dom_ms / 1e3) / 1e12,
+                                  "peak": l1_peak, "unit": "TB/s", "bytes": int(onchip_bytes),
+                                  "frac": onchip_bytes / (dom_ms / 1e3) / 1e12 / l1_peak,
+                                  "peak_source": "148 SMs x 128 B/clk L1 at the sampled SM clock"}
+        else:
+            roofline["onchip"] = {"note": "the wedding-cake sweep is L1-load / issue bound; "
+                                          "L1TEX throughput from the ncu capture"}
+            src_txt = os.path.join(ROOT, tr["source"]) if tr else None
+            if src_txt and os.path.exists(src_txt):
+                import re
+                m = re.search(r"l1tex__throughput\.avg\.pct_of_peak_sustained_active\s+([\d.]+)",
+                              open(src_txt).read())
+                if m:
+                    roofline["onchip"]["l1tex_throughput_pct"] = float(m.group(1))
+                    roofline["onchip"]["source"] = os.path.relpath(src_txt, ROOT)
+        return roofline
+
+    def build_roofline(self, build_ms):
+        hbm, _ = peaks_json()
+        build_avg = sum(build_ms) / self.args.steps  # ms per step, all rebuilds
+        in_bytes = sum(u["h2d"] for u in self.units)
+        build_bytes = in_bytes + sum(group_build_bytes(self.wl["groups"][u["g"]], self.tab_w,
+                                                       self.tab_h, self.nb) for u in self.units)
+        roof = {"bound": "hbm", "achieved": build_bytes / (build_avg / 1e3) / 1e9, "peak": hbm,
+                "unit": "GB/s", "ms": build_avg, "bytes": build_bytes,
+                "kernel": "k_quantize + k_colsum + k_bandscan + k_build (per table set)"}
+        roof["frac"] = roof["achieved"] / hbm
+        return roof
+
+    def cpu_baseline(self):
+        if self.world != 1 or self.args.no_cpu_baseline:
+            return None
+        c = cpu_reference(self.wl, self.data, self.models, public_api=True)
         cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": c["kind"],
-               "sample": cpu_sample_text(wl, c)}
+               "sample": cpu_sample_text(self.wl, c)}
         if c["public_api"]:
             cpu["public_api_value"] = c["public_api"]
             cpu["public_api_sample"] = ("reference likelihood_map per scale (full maps, "
                                         "tables rebuilt per call, all threads)")
+        return cpu
 
-    scale_names = [f"{['uniform', 'manhattan', 'chebyshev', 'gauss_cheb', 'euclid_quad', 'exp_l1'][g['scales'][s][0].kind]}"
-                   f"{g['scales'][s][0].kw}x{g['scales'][s][0].kh}"
-                   for g in wl["groups"] for s in range(len(g["scales"]))]
-    flat = [per_scale.get((gi, s), 0.0) for gi, g in enumerate(wl["groups"])
-            for s in range(len(g["scales"]))]
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": wl["scaling"], "vs_baseline": None,
-        "dtype": "u16/u32 integral tables (f64 decay tables) + f64 scores",
-        "data": "synthetic (seeded generators in paper_1705_03524_b200/synth.py)",
-        "config": {"workload": wl["name"], "bins": nb, "windows_per_step": int(job_win),
-                   "table_shape": [tab_w, tab_h], "units_per_rank": len(units),
-                   "l2": "flushed between timed steps (256 MiB write, untimed)",
-                   "parallelism": (f"bin ranges chained over {world} GPU(s) (p2p partial sums)"
-                                   if any("pin" in u for u in units) else
-                                   f"{'frames' if weak else wl['kind']} sharded over {world} "
-                                   f"GPU(s), no collective")},
-        "ih_build": {"ms": build_avg, "gbps": build_roof["achieved"], "frac": build_roof["frac"]},
-        "per_scale_ms": dict(zip(scale_names, flat)),
-        "roofline": roofline, "build_roofline": build_roof,
-        "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches // args.steps, "peaks_on_targets": ok_peaks,
-        "cpu_baseline": cpu, "clocks": clk,
-    }
-    print(json.dumps(out), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    # ------------------------------------------------------------ the run
+    def run(self):
+        args, wl = self.args, self.wl
+        per_step, events, clk, launches = self.time_device()
+        build_ms, sweep_ms = self.launch_times(events)
+        total_ms = self.reduce_ranks(sum(per_step))
+        job_win = self.reduce_ranks(self.n_win, op="sum")
+        value = job_win * args.steps / (total_ms / 1e3)
+        ok_peaks = self.peaks_on_targets()
+        e2e = self.e2e(job_win)
+        if self.rank != 0:
+            if self.dist:
+                self.dist.destroy_process_group()
+            return
+        roofline = self.sweep_roofline(sweep_ms, clk)
+        build_roof = self.build_roofline(build_ms)
+        cpu = self.cpu_baseline()
+        kinds = ["uniform", "manhattan", "chebyshev", "gauss_cheb", "euclid_quad", "exp_l1"]
+        per_scale = {}
+        for gi, g in enumerate(wl["groups"]):
+            for s, sc in enumerate(g["scales"]):
+                ts = sweep_ms.get((gi, s))
+                per_scale[f"{kinds[sc[0].kind]}{sc[0].kw}x{sc[0].kh}"] = \
+                    sum(ts) / args.steps if ts else 0.0
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": self.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
+            "dtype": "u16/u32 integral tables (f64 decay tables) + f64 scores",
+            "data": "synthetic (seeded generators in paper_1705_03524_b200/synth.py)",
+            "config": {"workload": wl["name"], "bins": self.nb, "windows_per_step": int(job_win),
+                       "table_shape": [self.tab_w, self.tab_h], "units_per_rank": len(self.units),
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "parallelism": (f"bin ranges chained over {self.world} GPU(s) (p2p "
+                                       f"partial sums)" if self.chained else
+                                       f"{'frames' if self.weak else wl['kind']} sharded over "
+                                       f"{self.world} GPU(s), no collective")},
+            "ih_build": {"ms": build_roof["ms"], "gbps": build_roof["achieved"],
+                         "frac": build_roof["frac"]},
+            "per_scale_ms": per_scale,
+            "roofline": roofline, "build_roofline": build_roof,
+            "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches // args.steps,
+            "peaks_on_targets": ok_peaks, "cpu_baseline": cpu, "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    wl = workload(args.config)
+    if args.impl == "reference":
+        return run_reference(args, wl, int(os.environ.get("RANK", 0)),
+                             int(os.environ.get("WORLD_SIZE", 1)))
+    OursArm(args, wl).run()
 
 
 def run_reference(args, wl, rank, world):
