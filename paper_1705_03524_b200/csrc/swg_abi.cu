@@ -1417,9 +1417,10 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
     p.grid = dim3((unsigned)((p.mw + kBruteThreads - 1) / kBruteThreads),
                   (unsigned)std::max(p.rows, 1));
   } else {
-    const int tw = (e == kCake16 || e == kExp64) ? 32 : kSweepTileX;
+    const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
+    const int th = e == kExp64 ? kExpTileY : kSweepTileY;
     p.grid = dim3((unsigned)((p.mw + tw - 1) / tw),
-                  (unsigned)std::max((p.rows + kSweepTileY - 1) / kSweepTileY, 1));
+                  (unsigned)std::max((p.rows + th - 1) / th, 1));
   }
   return SWG_OK;
 }
@@ -1435,10 +1436,10 @@ int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int h
   else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
   if (!cell) return 0;
   const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
-  const double span = 2.0 * hy + 2 + kSweepTileY;
+  const double span = 2.0 * hy + 2 + (e == kExp64 ? kExpTileY : kSweepTileY);
   if (span * (t->w + 1) * cell <= budget) return 0;
   const double sw = budget / (span * cell) - (2.0 * hx + 2);
-  const int tw = e == kExp64 ? 32 : kSweepTileX;  // windows per tile
+  const int tw = e == kExp64 ? kExpTileX : kSweepTileX;  // windows per tile
   if (sw >= 2 * tw && (sw + 2.0 * hx + 2) / sw < 1.7) return std::max(1, (int)(sw / tw));
   return 0;
 }

@@ -204,6 +204,13 @@ __device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
 constexpr int kSweepThreads = 256;
 constexpr int kSweepTileX = 16;
 constexpr int kSweepTileY = 8;
+// Exponential sweep CTA tile: kExpWarpsX warps side by side on one map row
+// (32 windows each), kSweepTileY / kExpWarpsX rows.
+#ifndef SWG_EXP_WX
+#define SWG_EXP_WX 4
+#endif
+constexpr int kExpWarpsX = SWG_EXP_WX;
+constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kSweepTileY / kExpWarpsX;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
 
