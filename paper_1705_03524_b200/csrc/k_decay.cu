@@ -13,15 +13,13 @@
 // The four orientations are the same SE table built on the feature image
 // flipped horizontally / vertically / both (k_flip), so one build pipeline
 // serves all four.  It mirrors the integer build: K1a' decayed column sums
-// per band, K1b' decayed scan over bands, K1c' per (band, bin pair) CTA with
-// a block-wide affine scan per row and t = d*t + R per column.
+// per band, K1b' decayed scan over bands, K1c' per (band, bin pair) CTA in
+// column strips (column recurrence, then one warp scan per row segment).
 // Layout: BIN PAIRS, not octets -- a record is the 2 bins of one pair at one
 // cell (16 B of fp64), element (b, kind k, x, y) at
 //   (((b/2)*4 + k)*plane_stride + y*pitch + x)*2 + b%2,
-// with the pair count padded to a multiple of 4 (whole octets).  Two fp64
-// bins per thread and column keep a full-row CTA's state in registers at
-// widths up to 4096 (8 columns per thread); the sweep reads 16-B records,
-// 16 windows' records contiguous per half-warp.  fp64 storage
+// with the pair count padded to a multiple of 4 (whole octets); the sweep
+// reads 16-B records, 32 windows' records contiguous per warp.  fp64 storage
 // and recurrences: fp32 noise (~1e-7 of the table values) is comparable to
 // the smallest quadrant contributions at large windows and Bhattacharyya's
 // sqrt amplifies it; fp64 keeps every map value within 1e-9 of the exact
@@ -35,57 +33,6 @@ namespace swg {
 namespace {
 
 using real = double;
-
-// Exclusive block scan of y -> alpha*y + B_t over threads (alpha shared by
-// all threads, 8 independent B components): returns the value entering each
-// thread.  One __syncthreads; `buf` ([8][32]) alternates between calls.
-template <int N>
-__device__ __forceinline__ void block_exscan_decay(const real (&B)[N], real alpha,
-                                                   real (&enter)[N], real* buf, int lane,
-                                                   int warp, int nwarps) {
-  real inc[N];
-#pragma unroll
-  for (int j = 0; j < N; ++j) inc[j] = B[j];
-  real ap = alpha;  // alpha^off
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const real t = __shfl_up_sync(0xFFFFFFFFu, inc[j], off);
-      if (lane >= off) inc[j] = fma(ap, t, inc[j]);
-    }
-    ap *= ap;
-  }
-  const real a32 = ap;  // alpha^32
-  if (lane == 31) {
-#pragma unroll
-    for (int j = 0; j < N; ++j) buf[j * 32 + warp] = inc[j];
-  }
-  __syncthreads();
-  // value entering warp w: sum_{v<w} a32^(w-1-v) W_v (each warp scans the totals)
-  real alane = 1.0;  // alpha^lane
-  {
-    real p = alpha;
-    for (int k = lane; k; k >>= 1) {
-      if (k & 1) alane *= p;
-      p *= p;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    real wt = lane < nwarps ? buf[j * 32 + lane] : 0.0;
-    real bp = a32;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const real t = __shfl_up_sync(0xFFFFFFFFu, wt, off);
-      if (lane >= off) wt = fma(bp, t, wt);
-      bp *= bp;
-    }
-    const real warp_enter = warp > 0 ? __shfl_sync(0xFFFFFFFFu, wt, warp - 1) : 0.0;
-    const real lane_prev = __shfl_up_sync(0xFFFFFFFFu, inc[j], 1);
-    enter[j] = fma(alane, warp_enter, lane > 0 ? lane_prev : 0.0);
-  }
-}
 
 // K0': flipped copies of the feature image (h: x -> W-1-x, v: y -> H-1-y).
 __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
@@ -154,138 +101,159 @@ __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, i
   }
 }
 
-template <int CPT>
-__device__ __forceinline__ void load_bins_d(const uint16_t* p, uint16_t (&v)[CPT]) {
-  if constexpr (CPT == 4) {
-    const uint2 q = *reinterpret_cast<const uint2*>(p);
-    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
-  } else {
-    const uint4 q = *reinterpret_cast<const uint4*>(p);
-    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
-    v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
-  }
-}
+// K1c': decayed SE table of one orientation, column recurrence first.  With
+//   c(x, y) = d c(x, y-1) + f(x, y)        (c(x, y0-1) = the band's carry, K1b')
+//   E(x+1, y+1) = sum_{x' <= x} d^(x-x') c(x', y)
+// one CTA per (band, bin pair) walks the row in strips of kStripW columns and
+// the band in blocks of kStripRows rows: phase A (thread per column) runs the
+// column recurrence down the block into a shared tile; phase B (warp per row,
+// lane = 8 consecutive columns) forms the decayed row prefix with one warp
+// scan per row and the carry E(x0-1, y) of the strip to the left; phase C
+// (thread per column, fused with the next block's phase A) writes the tile
+// out as 512-byte warp stores.  Two block barriers per 16 rows instead of a
+// block-wide scan and barrier per row.
+#ifndef SWG_STRIP_ROWS
+#define SWG_STRIP_ROWS 16
+#endif
+#ifndef SWG_STRIP_MINB
+#define SWG_STRIP_MINB 3
+#endif
+constexpr int kStripW = 256, kStripRows = SWG_STRIP_ROWS;
 
-// K1c': decayed SE table of one orientation: one CTA per (band, bin pair).
-template <int CPT>
-__global__ void __launch_bounds__(512) k_build_decay(const BuildArgs g, real dec, int kind,
-                                                     int pairs) {
-  __shared__ real s_row[2][kDP * 32];
-  __shared__ real s_carry[kDP * 32];
-  extern __shared__ double2 s_stage[];  // [warps][32 * CPT] store staging
+__device__ __forceinline__ int strip_swz(int x) { return x ^ ((x >> 3) & 7); }
+
+__global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
+    k_build_decay_strip(const BuildArgs g, real dec, int kind, int pairs) {
+  extern __shared__ double2 s_tile[];  // [kStripRows][kStripW] swizzled, then carry[band_h]
+  double2* carry = s_tile + kStripRows * kStripW;
   const int band = blockIdx.x / pairs, pr = blockIdx.x % pairs;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
+  constexpr int kWarps = kStripW / 32;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const int xb = tid * CPT;
-  const bool live = xb < g.w;
-  const uint16_t* fi = g.fi + (live ? xb : 0);
-  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr * kDP;
-  const uint32_t lim = (uint32_t)max(g.bins - pr * kDP, 0);  // bins of this pair in range
-  real dp[CPT + 1];  // d^i
-  dp[0] = 1.0;
-#pragma unroll
-  for (int i = 1; i <= CPT; ++i) dp[i] = dp[i - 1] * dec;
-  const real alpha = dp[CPT];
-
-  // decayed row prefix of per-column values v[i][j] along x, into r[i][j]
-  auto row_prefix = [&](const real (&v)[CPT][kDP], real (&r)[CPT][kDP], real* buf) {
-    real tot[kDP], ent[kDP];
-#pragma unroll
-    for (int j = 0; j < kDP; ++j) {
-      real run = 0.0;
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        run = fma(dec, run, v[i][j]);
-        r[i][j] = run;
-      }
-      tot[j] = run;
-    }
-    block_exscan_decay<kDP>(tot, alpha, ent, buf, lane, warp, nwarps);
-#pragma unroll
-    for (int i = 0; i < CPT; ++i)
-#pragma unroll
-      for (int j = 0; j < kDP; ++j) r[i][j] = fma(dp[i + 1], ent[j], r[i][j]);
-  };
-
-  // carry row E(x+1, y0) from the decayed column sums above the band
-  real t[CPT][kDP];
+  const int nrows = y1 - y0;
+  // the pair's two global bins (~0: bin out of range, no pixel matches)
+  const int nin = g.bins - pr * kDP;  // bins of this pair in range
+  const uint32_t gb0 = nin > 0 ? (uint32_t)g.bin0 + (uint32_t)pr * kDP : 0xFFFFFFFFu;
+  const uint32_t gb1 = nin > 1 ? gb0 + 1 : 0xFFFFFFFFu;
+  const real d2 = dec * dec, d4 = d2 * d2, d8 = d4 * d4;
+  real p8l = 1.0;  // d^(8 lane): carry from the left strip to this lane's first column
   {
-    real cc[CPT][kDP];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i)
-#pragma unroll
-      for (int j = 0; j < kDP; ++j) cc[i][j] = 0.0;
-    if (live && band > 0) {
-      const double2* src = reinterpret_cast<const double2*>(g.agg) +
-                           ((size_t)band * pairs + pr) * g.wa + xb;
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const double2 v = src[i];
-        cc[i][0] = v.x;
-        cc[i][1] = v.y;
-      }
+    real p = d8;
+    for (int k = lane; k; k >>= 1) {
+      if (k & 1) p8l *= p;
+      p *= p;
     }
-    row_prefix(cc, t, s_carry);
   }
-
   double2* plane = reinterpret_cast<double2*>(g.out) +
                    ((size_t)pr * g.planes + kind) * g.plane_stride;
   const double2 zero = make_double2(0.0, 0.0);
-  if (band == 0) {
-    if (live)
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) plane[xb + 1 + i] = zero;
-    if (tid == 0) plane[0] = zero;
+  if (band == 0)
+    for (int x = tid; x <= g.w; x += kStripW) plane[x] = zero;
+  for (int r = tid; r < nrows; r += kStripW) {
+    plane[(size_t)(y0 + r + 1) * g.pitch] = zero;
+    carry[r] = zero;
   }
-  uint16_t vn[CPT];
-#pragma unroll
-  for (int i = 0; i < CPT; ++i) vn[i] = kNoBin;
-  if (live && y0 < y1) load_bins_d<CPT>(fi + (size_t)y0 * g.fi_pitch, vn);
-  for (int y = y0; y < y1; ++y) {
-    real ind[CPT][kDP];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      uint32_t d = (uint32_t)vn[i] - gb;
-      d = d < lim ? d : 0xFFFFFFFFu;
-      ind[i][0] = d == 0u ? 1.0 : 0.0;
-      ind[i][1] = d == 1u ? 1.0 : 0.0;
+  const double2* agg = reinterpret_cast<const double2*>(g.agg) + ((size_t)band * pairs + pr) * g.wa;
+  const int sw = strip_swz(tid);
+  auto step = [&](uint32_t v, real& c0, real& c1) {
+    c0 = fma(dec, c0, v == gb0 ? 1.0 : 0.0);
+    c1 = fma(dec, c1, v == gb1 ? 1.0 : 0.0);
+  };
+  for (int x0 = 0; x0 < g.w; x0 += kStripW) {
+    const int x = x0 + tid;
+    const bool in = x < g.w;
+    real c0 = 0.0, c1 = 0.0;
+    if (in && band > 0) {
+      const double2 v = agg[x];
+      c0 = v.x;
+      c1 = v.y;
     }
-    if (live && y + 1 < y1) load_bins_d<CPT>(fi + (size_t)(y + 1) * g.fi_pitch, vn);
-    real r[CPT][kDP];
-    row_prefix(ind, r, s_row[y & 1]);
+    // pixel column x of the band (kNoBin beyond the image) and its table column
+    const uint16_t* col = g.fi + (size_t)y0 * g.fi_pitch + (in ? x : 0);
+    const size_t fstep = in ? g.fi_pitch : 0;
+    const uint32_t vor = in ? 0u : 0x10000u;  // beyond the image: a value no bin matches
+    double2* out = plane + (size_t)(y0 + 1) * g.pitch + x + 1;
+    int prev = 0;  // rows of the previous block still in the tile (phase C pending)
+    for (int rb = 0;; rb += kStripRows) {
+      const int nr = min(kStripRows, nrows - rb);
+      // C (previous block) + A (this block): the same thread, the same tile slots
+      if (in) {
+        if (prev == kStripRows) {
 #pragma unroll
-    for (int i = 0; i < CPT; ++i)
-#pragma unroll
-      for (int j = 0; j < kDP; ++j) t[i][j] = fma(dec, t[i][j], r[i][j]);
-    double2* row = plane + (size_t)(y + 1) * g.pitch;
-#ifndef SWG_DECAY_DIRECT_STORES
-    // coalesced row stores (8 columns per thread): the warp's 32*CPT records
-    // go through shared memory so each store instruction writes 512
-    // contiguous bytes; per-thread stores of 128-byte runs touch 32 lines
-    // per instruction and throttle the LSU (measured: 5.7 -> ~4 ms per
-    // launch at 3840 x 669 x 512 bins; no gain at 4 columns per thread)
-    if constexpr (CPT == 8) {
-      double2* st = s_stage + warp * 32 * CPT;
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) st[(lane * CPT + i) ^ (lane & (CPT - 1))] =
-          make_double2(t[i][0], t[i][1]);
-      __syncwarp();
-      const int wcol = warp * 32 * CPT;
-#pragma unroll
-      for (int m = 0; m < CPT; ++m) {
-        const int rec = m * 32 + lane, col = wcol + rec;
-        if (col < g.w) row[col + 1] = st[rec ^ ((rec / CPT) & (CPT - 1))];
+          for (int r = 0; r < kStripRows; ++r) {
+            *out = s_tile[r * kStripW + sw];
+            out += g.pitch;
+          }
+        } else {
+          for (int r = 0; r < prev; ++r) {
+            *out = s_tile[r * kStripW + sw];
+            out += g.pitch;
+          }
+        }
       }
-      __syncwarp();
-    } else
-#endif
-    {
-      if (live)
+      if (nr <= 0) break;
+      if (nr == kStripRows) {
+        uint32_t fv[kStripRows];
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) row[xb + 1 + i] = make_double2(t[i][0], t[i][1]);
+        for (int r = 0; r < kStripRows; ++r) fv[r] = col[r * fstep];
+        col += kStripRows * fstep;
+#pragma unroll
+        for (int r = 0; r < kStripRows; ++r) {
+          step(fv[r] | vor, c0, c1);
+          s_tile[r * kStripW + sw] = make_double2(c0, c1);
+        }
+      } else {
+        for (int r = 0; r < nr; ++r) {
+          step(col[0] | vor, c0, c1);
+          col += fstep;
+          s_tile[r * kStripW + sw] = make_double2(c0, c1);
+        }
+      }
+      __syncthreads();
+      // B: decayed row prefix, one warp per row
+      for (int r = warp; r < nr; r += kWarps) {
+        double2* trow = s_tile + r * kStripW;
+        real v0[8], v1[8];
+        real run0 = 0.0, run1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double2 q = trow[8 * lane + (i ^ (lane & 7))];
+          run0 = fma(dec, run0, q.x);
+          run1 = fma(dec, run1, q.y);
+          v0[i] = run0;
+          v1[i] = run1;
+        }
+        real i0 = run0, i1 = run1;  // inclusive scan of the lanes' totals
+        real sk = d8;               // (d^8)^(2^k)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const real t0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1 << k);
+          const real t1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1 << k);
+          if (lane >= (1 << k)) {
+            i0 = fma(sk, t0, i0);
+            i1 = fma(sk, t1, i1);
+          }
+          sk *= sk;
+        }
+        real e0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1), e1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1);
+        if (lane == 0) e0 = e1 = 0.0;
+        const double2 cin = carry[rb + r];
+        const real q0 = fma(p8l, cin.x, e0), q1 = fma(p8l, cin.y, e1);
+        real pw = dec;  // d^(i+1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v0[i] = fma(pw, q0, v0[i]);
+          v1[i] = fma(pw, q1, v1[i]);
+          trow[8 * lane + (i ^ (lane & 7))] = make_double2(v0[i], v1[i]);
+          pw *= dec;
+        }
+        const real n0 = __shfl_sync(0xFFFFFFFFu, v0[7], 31);
+        const real n1 = __shfl_sync(0xFFFFFFFFu, v1[7], 31);
+        if (lane == 0) carry[rb + r] = make_double2(n0, n1);  // E(x0 + kStripW - 1, y)
+      }
+      __syncthreads();
+      prev = nr;
     }
-    if (tid == 0) row[0] = zero;
   }
 }
 
@@ -323,18 +291,16 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }
-  const int cpt = choose_cpt(a.w);
-  const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const unsigned grid = (unsigned)(a.nbands * pairs);
-  const size_t smem = cpt == 8 ? (size_t)threads * cpt * sizeof(double2) : 0;  // staging
+  const size_t smem = (size_t)(kStripRows * kStripW + a.band_h) * sizeof(double2);
+  if (smem > (200 << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~8500 rows
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_build_decay<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-    cudaFuncSetAttribute(k_build_decay<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+    cudaFuncSetAttribute(k_build_decay_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 << 10);
     attr = true;
   }
-  if (cpt == 4) k_build_decay<4><<<grid, threads, smem, s>>>(a, dec, kind, pairs);
-  else k_build_decay<8><<<grid, threads, smem, s>>>(a, dec, kind, pairs);
+  k_build_decay_strip<<<grid, kStripW, smem, s>>>(a, dec, kind, pairs);
   *launches += 1;
   return cudaGetLastError();
 }
