@@ -20,34 +20,6 @@ __device__ __forceinline__ double clamp01b(double v) {
   return (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
 }
 
-__device__ __forceinline__ bool better_b(double s, long long i, double s2, long long i2) {
-  return s > s2 || (s == s2 && i < i2);
-}
-
-__device__ void block_peak_b(double s, long long idx, PeakPart* out) {
-  __shared__ double ss[32];
-  __shared__ long long si[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int off = 16; off > 0; off >>= 1) {
-    const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-    const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-    if (better_b(s2, i2, s, idx)) { s = s2; idx = i2; }
-  }
-  if (lane == 0) { ss[warp] = s; si[warp] = idx; }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    s = lane < nw ? ss[lane] : -2.0;
-    idx = lane < nw ? si[lane] : 0x7FFFFFFFFFFFFFFFLL;
-    for (int off = 16; off > 0; off >>= 1) {
-      const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-      const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-      if (better_b(s2, i2, s, idx)) { s = s2; idx = i2; }
-    }
-    if (lane == 0) *out = PeakPart{s, idx};
-  }
-}
-
 __global__ void __launch_bounds__(kBruteThreads) k_sweep_brute(const SweepArgs a,
                                                                const BruteArgs g) {
   __shared__ double acc[kChunk * kBruteThreads];
@@ -107,8 +79,7 @@ __global__ void __launch_bounds__(kBruteThreads) k_sweep_brute(const SweepArgs a
   }
   s = clamp01b(s);
   if (active) a.scores[(size_t)blockIdx.y * a.mw + u] = s;
-  block_peak_b(active ? s : -2.0, (long long)v * a.mw + u,
-               a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // Brute-force histograms of explicit windows: one thread per window walks

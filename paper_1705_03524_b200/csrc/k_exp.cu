@@ -23,34 +23,6 @@ namespace {
 __device__ __forceinline__ double clamp01e(double v) {
   return (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
 }
-__device__ __forceinline__ bool better_e(double s, long long i, double s2, long long i2) {
-  return s > s2 || (s == s2 && i < i2);
-}
-
-__device__ __forceinline__ void block_peak_e(double s, long long idx, PeakPart* out) {
-  __shared__ double ss[32];
-  __shared__ long long si[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int off = 16; off > 0; off >>= 1) {
-    const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-    const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-    if (better_e(s2, i2, s, idx)) { s = s2; idx = i2; }
-  }
-  if (lane == 0) { ss[warp] = s; si[warp] = idx; }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    s = lane < nw ? ss[lane] : -2.0;
-    idx = lane < nw ? si[lane] : 0x7FFFFFFFFFFFFFFFLL;
-    for (int off = 16; off > 0; off >>= 1) {
-      const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-      const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-      if (better_e(s2, i2, s, idx)) { s = s2; idx = i2; }
-    }
-    if (lane == 0) *out = PeakPart{s, idx};
-  }
-}
-
 // one 16-B bin-pair record
 __device__ __forceinline__ double2 ldd2(const char* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
@@ -148,8 +120,7 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const
     s = clamp01e(s);
     if (active) a.scores[widx] = s;
   }
-  block_peak_e(active ? s : -2.0, (long long)v * a.mw + u,
-               a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // Phase 2a: windows within eps of the fast maximum.
@@ -249,14 +220,14 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
       }
       sc = clamp01e(sc);
       a.scores[(size_t)(v - a.row0) * a.mw + u] = sc;
-      if (better_e(sc, idx, best, bidx)) {
+      if (peak_better(sc, idx, best, bidx)) {
         best = sc;
         bidx = idx;
       }
     }
     __syncwarp();
   }
-  block_peak_e(best, bidx, r.parts + blockIdx.x);
+  cta_peak(best, bidx, r.parts + blockIdx.x);
 }
 
 

@@ -41,46 +41,6 @@ __device__ __forceinline__ double clamp01(double v) {
   return (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);  // std::clamp(v, 0, 1)
 }
 
-__device__ __forceinline__ bool better(double s, long long i, double s2, long long i2) {
-  return s > s2 || (s == s2 && i < i2);
-}
-
-// Block argmax with the tie rule; thread 0 writes the CTA's candidate.
-__device__ __forceinline__ void block_peak(double s, long long idx, PeakPart* out) {
-  __shared__ double ss[32];
-  __shared__ long long si[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-    const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-    if (better(s2, i2, s, idx)) {
-      s = s2;
-      idx = i2;
-    }
-  }
-  if (lane == 0) {
-    ss[warp] = s;
-    si[warp] = idx;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    s = lane < nw ? ss[lane] : -2.0;
-    idx = lane < nw ? si[lane] : 0x7FFFFFFFFFFFFFFFLL;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
-      const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
-      if (better(s2, i2, s, idx)) {
-        s = s2;
-        idx = i2;
-      }
-    }
-    if (lane == 0) *out = PeakPart{s, idx};
-  }
-}
-
 __device__ __forceinline__ uint4 ldqb(const char* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
@@ -193,8 +153,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
     s = clamp01(s);
     if (active && half == 0) a.scores[widx] = s;
   }
-  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
-             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // K2q: declared Euclidean extension, w = A - ky*dx^2 - kx*dy^2 with
@@ -263,8 +222,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a)
     s = clamp01(s);
     if (active && half == 0) a.scores[widx] = s;
   }
-  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
-             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // K2c: wedding-cake telescoping over nested boxes of the plain table.
@@ -366,8 +324,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
     s = clamp01(s);
     if (active && half == 0) a.scores[widx] = s;
   }
-  block_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u,
-             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // K2c16: the cake sweep over NARROW (uint16) plain planes.  Every box of a
@@ -483,8 +440,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs 
     s = clamp01(s);
     if (active) a.scores[widx] = s;
   }
-  block_peak(active ? s : -2.0, (long long)v * a.mw + u,
-             a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  sweep_peak(active ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
 // K3: reduce CTA candidates to the map peak (one CTA).
@@ -502,13 +458,13 @@ __global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int
     }
 #pragma unroll
     for (int k = 0; k < kBatch; ++k)
-      if (better(p[k].score, p[k].idx, s, idx)) {
+      if (peak_better(p[k].score, p[k].idx, s, idx)) {
         s = p[k].score;
         idx = p[k].idx;
       }
   }
   __shared__ PeakPart res;
-  block_peak(s, idx, &res);
+  cta_peak(s, idx, &res);
   __syncthreads();
   if (threadIdx.x == 0) {
     swg_peak pk;
@@ -528,12 +484,12 @@ __global__ void __launch_bounds__(256) k_map_peak(const double* sc, size_t n, Pe
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     const double v = sc[i];
-    if (better(v, (long long)i, best, bi)) {
+    if (peak_better(v, (long long)i, best, bi)) {
       best = v;
       bi = (long long)i;
     }
   }
-  block_peak(best, bi, parts + blockIdx.x);
+  cta_peak(best, bi, parts + blockIdx.x);
 }
 
 // Window queries from explicit quadrant terms (engine.cpp:39-79 semantics).

@@ -178,6 +178,57 @@ struct QueryArgs {
   double* outd;           // cake: device n x bins
 };
 
+// ---------------------------------------------------------------- peaks
+// The reference's argmax rule (matching.cpp:211-223): strict `>` in
+// row-major order, i.e. higher score, then smaller index.
+__device__ __forceinline__ bool peak_better(double s, long long i, double s2, long long i2) {
+  return s > s2 || (s == s2 && i < i2);
+}
+
+// Block argmax with the tie rule; thread 0 writes the CTA's candidate.
+__device__ __forceinline__ void cta_peak(double s, long long idx, PeakPart* out) {
+  __shared__ double ss[32];
+  __shared__ long long si[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
+    const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
+    if (peak_better(s2, i2, s, idx)) {
+      s = s2;
+      idx = i2;
+    }
+  }
+  if (lane == 0) {
+    ss[warp] = s;
+    si[warp] = idx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? ss[lane] : -2.0;
+    idx = lane < nw ? si[lane] : 0x7FFFFFFFFFFFFFFFLL;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double s2 = __shfl_down_sync(0xFFFFFFFFu, s, off);
+      const long long i2 = __shfl_down_sync(0xFFFFFFFFu, idx, off);
+      if (peak_better(s2, i2, s, idx)) {
+        s = s2;
+        idx = i2;
+      }
+    }
+    if (lane == 0) *out = PeakPart{s, idx};
+  }
+}
+
+// Sweep epilogue: this CTA's candidate into a.parts (k_peak_reduce, one
+// CTA, then reduces them into the map peak).  A fused variant -- the last
+// CTA of the sweep reducing them behind a ticket counter -- measured 0.35 %
+// slower on config 2 (a fence + atomic in every CTA, a serial tail).
+__device__ __forceinline__ void sweep_peak(double s, long long idx, const SweepArgs& a) {
+  cta_peak(s, idx, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
 // Map tile of this CTA.  Super-column order: the linear CTA index walks
 // column strips of `sc_tiles` tiles, each from the top row to the bottom;
 // CTAs are dispatched in linear order, so the CTAs in flight cover a strip
