@@ -324,8 +324,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n,
  * plus the full frame's pitch) and run the n requests, peaks only.  Peak of
  * frame f, request i -> [f * n + i] of peaks_dev (device, asynchronous)
  * and/or peaks_host (filled on return).  Frames round-robin over up to
- * three table sets of this geometry (`t` plus two the library creates on
- * first use and frees with `t`) on the context's worker streams, so one
+ * eight table sets of this geometry (`t` plus up to seven the library
+ * creates on first use and frees with `t`) on the context's worker streams, so one
  * frame's build overlaps another's sweeps; the call forks from and joins
  * back to the context stream (graph-capturable with device outputs).  Not
  * to be called concurrently with other calls on the same context. */
