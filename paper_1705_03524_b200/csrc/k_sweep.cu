@@ -333,11 +333,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
 // 16-byte records (8 bins) per corner: half the bytes of the 32-bit path,
 // box arithmetic on packed 16-bit pairs (vsub2/vadd2).
 template <int SIM>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_cake16(const SweepArgs a,
+__global__ void __launch_bounds__(kCakeThreads) k_sweep_cake16(const SweepArgs a,
                                                                 const CakeSweep rg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u0 = blockIdx.x * 32 + lane;
-  const int r0 = blockIdx.y * kSweepTileY + warp;
+  const int r0 = blockIdx.y * kCakeTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -577,8 +577,8 @@ cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s) {
 
 cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                                 cudaStream_t s) {
-  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake16<0><<<grid, kSweepThreads, 0, s>>>(a, r);
-  else k_sweep_cake16<1><<<grid, kSweepThreads, 0, s>>>(a, r);
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake16<0><<<grid, kCakeThreads, 0, s>>>(a, r);
+  else k_sweep_cake16<1><<<grid, kCakeThreads, 0, s>>>(a, r);
   return cudaGetLastError();
 }
 

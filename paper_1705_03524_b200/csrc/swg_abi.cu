@@ -1421,7 +1421,7 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
                   (unsigned)std::max(p.rows, 1));
   } else {
     const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
-    const int th = e == kExp64 ? kExpTileY : kSweepTileY;
+    const int th = e == kExp64 ? kExpTileY : e == kCake16 ? kCakeTileY : kSweepTileY;
     p.grid = dim3((unsigned)((p.mw + tw - 1) / tw),
                   (unsigned)std::max((p.rows + th - 1) / th, 1));
   }

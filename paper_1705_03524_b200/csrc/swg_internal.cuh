@@ -262,6 +262,14 @@ constexpr int kSweepTileY = 8;
 #endif
 constexpr int kExpWarpsX = SWG_EXP_WX;
 constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kSweepTileY / kExpWarpsX;
+// 16-bit cake sweep CTA tile: 32 windows x kCakeTileY map rows, a warp per
+// row (measured on config 2: 4 rows 1.138 ms per step, 8 rows 1.151, 2 rows
+// 1.153, 16 rows 1.211 -- taller tiles raise the L1 hit rate but cost
+// occupancy and tail balance).
+#ifndef SWG_CAKE_TY
+#define SWG_CAKE_TY 4
+#endif
+constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
 
