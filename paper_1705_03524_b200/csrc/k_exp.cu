@@ -29,16 +29,18 @@ __device__ __forceinline__ double2 ldd2(const char* p) {
 }
 
 // One lane per window, 32 windows of one map row per warp; the CTA tile is
-// kExpWarpsX warps side by side (128 x 2 windows): for each of an octet's
-// four bin pairs a corner load of the CTA reads 128 consecutive 16-byte
-// records of one plane per map row (2 KB runs: measured 3-5 % faster per
-// launch than the 32 x 8 tile's 512-byte runs), and the lane holds all 8
-// bins of the octet, so the ordered sums need no shuffles.
+// kExpWarpsX warps side by side (128 windows of one map row): for each of an
+// octet's four bin pairs a corner load of the CTA reads 128 consecutive
+// 16-byte records of one plane (2 KB runs: measured 3-5 % faster per launch
+// than 32 x 8 tiles' 512-byte runs), and the lane holds all 8 bins of the
+// octet, so the ordered sums need no shuffles.
 template <int SIM>
 #ifndef SWG_EXP_MINB
-#define SWG_EXP_MINB 3  // <= 80 registers: 3 CTAs per SM (latency-bound reads)
+// <= 128 registers at 128 threads: deep per-lane load batches (measured: 80
+// registers +3-5 %, 252 registers +14 %; 128 and 168 equal)
+#define SWG_EXP_MINB 4
 #endif
-__global__ void __launch_bounds__(kSweepThreads, SWG_EXP_MINB) k_sweep_exp(const SweepArgs a,
+__global__ void __launch_bounds__(kExpThreads, SWG_EXP_MINB) k_sweep_exp(const SweepArgs a,
                                                                          const ExpSweep e) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int tx, ty;
@@ -234,8 +236,8 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
 }  // namespace
 
 cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s) {
-  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_exp<0><<<grid, kSweepThreads, 0, s>>>(a, e);
-  else k_sweep_exp<1><<<grid, kSweepThreads, 0, s>>>(a, e);
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_exp<0><<<grid, kExpThreads, 0, s>>>(a, e);
+  else k_sweep_exp<1><<<grid, kExpThreads, 0, s>>>(a, e);
   return cudaGetLastError();
 }
 

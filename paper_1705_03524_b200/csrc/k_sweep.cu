@@ -165,12 +165,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 // exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
 // exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
 template <int SIM>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_quad(const SweepArgs a) {
+__global__ void __launch_bounds__(kQuadThreads) k_sweep_quad(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   int tx, ty;
   sweep_tile(a.sc_tiles, tx, ty);
   const int u0 = tx * kSweepTileX + (lane >> 1);
-  const int r0 = ty * kSweepTileY + warp;
+  const int r0 = ty * kQuadTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -570,8 +570,8 @@ cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
 }
 
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s) {
-  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad<0><<<grid, kSweepThreads, 0, s>>>(a);
-  else k_sweep_quad<1><<<grid, kSweepThreads, 0, s>>>(a);
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad<0><<<grid, kQuadThreads, 0, s>>>(a);
+  else k_sweep_quad<1><<<grid, kQuadThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

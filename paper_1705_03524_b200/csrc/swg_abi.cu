@@ -1421,7 +1421,10 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
                   (unsigned)std::max(p.rows, 1));
   } else {
     const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
-    const int th = e == kExp64 ? kExpTileY : e == kCake16 ? kCakeTileY : kSweepTileY;
+    const int th = e == kExp64    ? kExpTileY
+                   : e == kCake16 ? kCakeTileY
+                   : e == kQuad   ? kQuadTileY
+                                  : kSweepTileY;
     p.grid = dim3((unsigned)((p.mw + tw - 1) / tw),
                   (unsigned)std::max((p.rows + th - 1) / th, 1));
   }
@@ -1439,7 +1442,8 @@ int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int h
   else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
   if (!cell) return 0;
   const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
-  const double span = 2.0 * hy + 2 + (e == kExp64 ? kExpTileY : kSweepTileY);
+  const double span =
+      2.0 * hy + 2 + (e == kExp64 ? kExpTileY : e == kQuad ? kQuadTileY : kSweepTileY);
   if (span * (t->w + 1) * cell <= budget) return 0;
   const double sw = budget / (span * cell) - (2.0 * hx + 2);
   const int tw = e == kExp64 ? kExpTileX : kSweepTileX;  // windows per tile

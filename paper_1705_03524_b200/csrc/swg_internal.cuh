@@ -250,18 +250,35 @@ __device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
   tx = x0 + (rem - ty * wsc);
 }
 
-// Sweep CTA geometry: 8 warps; a warp = 16 windows of one map row, two lanes
-// per window (lane parity = which half of each bin octet).
-constexpr int kSweepThreads = 256;
+// Sweep CTA geometry (affine, quadratic, 32-bit cake): kSweepTileY warps; a
+// warp = 16 windows of one map row, two lanes per window (lane parity =
+// which half of each bin octet).
+#ifndef SWG_SWEEP_TY
+#define SWG_SWEEP_TY 8
+#endif
+constexpr int kSweepTileY = SWG_SWEEP_TY;
+constexpr int kSweepThreads = 32 * kSweepTileY;
 constexpr int kSweepTileX = 16;
-constexpr int kSweepTileY = 8;
+// The quadratic sweep's CTA: 4 warps (measured against 8 warps: config 3
+// 6.27 -> 5.95 ms per step, config 5's Euclidean scales -7 %; the affine
+// sweep loses 3 % at 4 warps and keeps 8).
+#ifndef SWG_QUAD_TY
+#define SWG_QUAD_TY 4
+#endif
+constexpr int kQuadTileY = SWG_QUAD_TY, kQuadThreads = 32 * kQuadTileY;
 // Exponential sweep CTA tile: kExpWarpsX warps side by side on one map row
-// (32 windows each), kSweepTileY / kExpWarpsX rows.
+// (32 windows each), kExpThreads / 32 / kExpWarpsX rows: 128 x 1 windows
+// (measured: 128 x 2 +3 % on config 4 and +7 % on config 5's exponential
+// scales; 64 x 2 and 256 x 1 slower too).
 #ifndef SWG_EXP_WX
 #define SWG_EXP_WX 4
 #endif
+#ifndef SWG_EXP_THREADS
+#define SWG_EXP_THREADS 128
+#endif
+constexpr int kExpThreads = SWG_EXP_THREADS;
 constexpr int kExpWarpsX = SWG_EXP_WX;
-constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kSweepTileY / kExpWarpsX;
+constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kExpThreads / 32 / kExpWarpsX;
 // 16-bit cake sweep CTA tile: 32 windows x kCakeTileY map rows, a warp per
 // row (measured on config 2: 4 rows 1.138 ms per step, 8 rows 1.151, 2 rows
 // 1.153, 16 rows 1.211 -- taller tiles raise the L1 hit rate but cost
