@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 // exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
 // exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
 template <int SIM>
-__global__ void __launch_bounds__(kQuadThreads) k_sweep_quad(const SweepArgs a) {
+__global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   int tx, ty;
   sweep_tile(a.sc_tiles, tx, ty);

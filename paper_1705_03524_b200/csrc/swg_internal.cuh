@@ -265,6 +265,9 @@ constexpr int kSweepTileX = 16;
 #ifndef SWG_QUAD_TY
 #define SWG_QUAD_TY 4
 #endif
+#ifndef SWG_QUAD_MINB
+#define SWG_QUAD_MINB 8  // 64 registers, 8 CTAs per SM (96: config 5's Euclidean +6 %)
+#endif
 constexpr int kQuadTileY = SWG_QUAD_TY, kQuadThreads = 32 * kQuadTileY;
 // Exponential sweep CTA tile: kExpWarpsX warps side by side on one map row
 // (32 windows each), kExpThreads / 32 / kExpWarpsX rows: 128 x 1 windows
