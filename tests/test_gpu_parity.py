@@ -824,6 +824,20 @@ def test_decay_tables_max_width(ctx, oracle):
                                    rtol=1e-12, atol=1e-12)
 
 
+def test_decay_tables_strips_and_blocks(ctx, oracle):
+    """Decay build across column strips (600 wide: three 256-column strips
+    with the strip-to-strip carry) and row blocks (64 bins: bands of 17 rows,
+    one full 16-row block plus a partial one), slow decay so every carry
+    matters."""
+    img = oracle.random_gray(600, 600, 5)
+    bins, d = 64, 0.9375
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build_decay(img, d, swg.FMT_GRAY8, bins)
+    for k, f in ((0, fi), (3, fi[::-1, ::-1])):
+        np.testing.assert_allclose(t.export_f64(k), _decayed_se(np.ascontiguousarray(f), bins, d),
+                                   rtol=1e-12, atol=1e-10)
+
+
 def test_quadratic_tall_image(ctx, oracle):
     """32-bit quadratic planes have no height limit (the 64-bit export keeps
     the 2340-row limit of its y^2 carries): maps of a 40 x 3000 image."""
