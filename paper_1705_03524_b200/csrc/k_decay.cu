@@ -192,22 +192,17 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
         }
       }
       if (nr <= 0) break;
-      if (nr == kStripRows) {
+      {  // all of the block's loads in flight at once (a partial block predicates)
         uint32_t fv[kStripRows];
 #pragma unroll
-        for (int r = 0; r < kStripRows; ++r) fv[r] = col[r * fstep];
+        for (int r = 0; r < kStripRows; ++r) fv[r] = r < nr ? col[r * fstep] : 0u;
         col += kStripRows * fstep;
 #pragma unroll
-        for (int r = 0; r < kStripRows; ++r) {
-          step(fv[r] | vor, c0, c1);
-          s_tile[r * kStripW + sw] = make_double2(c0, c1);
-        }
-      } else {
-        for (int r = 0; r < nr; ++r) {
-          step(col[0] | vor, c0, c1);
-          col += fstep;
-          s_tile[r * kStripW + sw] = make_double2(c0, c1);
-        }
+        for (int r = 0; r < kStripRows; ++r)
+          if (r < nr) {
+            step(fv[r] | vor, c0, c1);
+            s_tile[r * kStripW + sw] = make_double2(c0, c1);
+          }
       }
       __syncthreads();
       // B: decayed row prefix, one warp per row
