@@ -981,16 +981,26 @@ class OursArm:
                                   "frac": onchip_bytes / (dom_ms / 1e3) / 1e12 / l1_peak,
                                   "peak_source": "148 SMs x 128 B/clk L1 at the sampled SM clock"}
         else:
-            roofline["onchip"] = {"note": "the wedding-cake sweep is L1-load / issue bound; "
-                                          "L1TEX throughput from the ncu capture"}
+            roofline["onchip"] = {"note": "the wedding-cake sweep is bound by the L1 -> register "
+                                          "data path (ring corners, O(rings*bins) per window); "
+                                          "figures from the ncu capture of this launch"}
             src_txt = os.path.join(ROOT, tr["source"]) if tr else None
             if src_txt and os.path.exists(src_txt):
                 import re
-                m = re.search(r"l1tex__throughput\.avg\.pct_of_peak_sustained_active\s+([\d.]+)",
-                              open(src_txt).read())
-                if m:
-                    roofline["onchip"]["l1tex_throughput_pct"] = float(m.group(1))
-                    roofline["onchip"]["source"] = os.path.relpath(src_txt, ROOT)
+                txt = open(src_txt).read()
+                for key, pat in (
+                        ("l1tex_throughput_pct",
+                         r"l1tex__throughput\.avg\.pct_of_peak_sustained_active\s+([\d.]+)"),
+                        ("lsu_writeback_pct",
+                         r"l1tex__lsu_writeback_active\.avg\.pct_of_peak_sustained_elapsed\s+([\d.]+)"),
+                        ("lsu_writeback_bytes_per_s",
+                         r"derived__l1tex__lsu_writeback_bytes_mem_lgds\.sum\.per_second\s+([\d.]+)")):
+                    m = re.search(pat, txt)
+                    if m:
+                        roofline["onchip"][key] = float(m.group(1))
+                if "lsu_writeback_pct" in roofline["onchip"]:
+                    roofline["onchip"]["frac"] = roofline["onchip"]["lsu_writeback_pct"] / 100.0
+                roofline["onchip"]["source"] = os.path.relpath(src_txt, ROOT)
         return roofline
 
     def build_roofline(self, build_ms):

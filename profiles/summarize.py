@@ -14,6 +14,9 @@ METRICS = [
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed",
+    "derived__l1tex__lsu_writeback_bytes_mem_lgds.sum.per_second",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
