@@ -250,7 +250,7 @@ __device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
   tx = x0 + (rem - ty * wsc);
 }
 
-// Sweep CTA geometry (affine, quadratic, 32-bit cake): kSweepTileY warps; a
+// Sweep CTA geometry (affine, 32-bit cake): kSweepTileY warps; a
 // warp = 16 windows of one map row, two lanes per window (lane parity =
 // which half of each bin octet).
 #ifndef SWG_SWEEP_TY
