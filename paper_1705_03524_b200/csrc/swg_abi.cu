@@ -1402,6 +1402,18 @@ swg_status validate_request(const swg_tables* t, const swg_map_request& r, bool 
   return SWG_OK;
 }
 
+// CTA grid of a sweep over `rows` map rows of width mw.
+dim3 sweep_grid(Engine e, int mw, int rows) {
+  if (e == kBrute)
+    return dim3((unsigned)((mw + kBruteThreads - 1) / kBruteThreads), (unsigned)std::max(rows, 1));
+  const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
+  const int th = e == kExp64    ? kExpTileY
+                 : e == kCake16 ? kCakeTileY
+                 : e == kQuad   ? kQuadTileY
+                                : kSweepTileY;
+  return dim3((unsigned)((mw + tw - 1) / tw), (unsigned)std::max((rows + th - 1) / th, 1));
+}
+
 // Engine and grid of a validated request.  The kernel-independent choices:
 // Plain maps are Uniform-kernel maps; brute force on an integer affine kernel
 // gives the quadrant path's exact counts (engine.hpp:62-66,
@@ -1437,18 +1449,7 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
   }
   p.engine = e;
   p.k = k;
-  if (e == kBrute) {
-    p.grid = dim3((unsigned)((p.mw + kBruteThreads - 1) / kBruteThreads),
-                  (unsigned)std::max(p.rows, 1));
-  } else {
-    const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
-    const int th = e == kExp64    ? kExpTileY
-                   : e == kCake16 ? kCakeTileY
-                   : e == kQuad   ? kQuadTileY
-                                  : kSweepTileY;
-    p.grid = dim3((unsigned)((p.mw + tw - 1) / tw),
-                  (unsigned)std::max((p.rows + th - 1) / th, 1));
-  }
+  p.grid = sweep_grid(e, p.mw, p.rows);
   return SWG_OK;
 }
 
@@ -1691,7 +1692,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       stot += round_up((size_t)p.rows * p.mw, 32);
     }
     p.poff = ptot;
-    ptot += (size_t)p.grid.x * p.grid.y;
+    ptot += (size_t)p.grid.x * (p.grid.y + 1);  // + a spare CTA row: the split last map
   }
   swg_ctx::Scratch& S = c->scr[c->slot];
   ST_TRY(S.scores.ensure(std::max<size_t>(stot, 1) * 8));
@@ -1740,34 +1741,67 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     double* dscores = dev_map(i) ? scores_dev[i] : static_cast<double*>(S.scores.p) + p.soff;
     PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + p.poff;
     static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
-    fill_sweep_args(a, t, r, p, dscores, parts);
+    // the copy stream takes a finished map (or row range of it) while later
+    // sweeps run
+    auto copy_rows = [&](int slot, int row_off, int rows) -> swg_status {
+      while (c->events.size() <= (size_t)slot) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->events.push_back(ev);
+      }
+      CUDA_TRY(cudaEventRecord(c->events[slot], st));
+      CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[slot], 0));
+      CUDA_TRY(cudaMemcpyAsync(scores_host[i] + (size_t)row_off * p.mw,
+                               dscores + (size_t)row_off * p.mw, (size_t)rows * p.mw * 8,
+                               cudaMemcpyDeviceToHost, c->copy));
+      copies = true;
+      return SWG_OK;
+    };
+    auto sweep = [&](const MapPlan& q, double* sc, PeakPart* pp) -> swg_status {
+      fill_sweep_args(a, t, r, q, sc, pp);
+      if (q.engine == kQuad) ST_TRY(run_quad(t, q, a, st));
+      else if (q.engine == kAffine32) ST_TRY(run_affine(t, q, a, st));
+      else if (q.engine == kBrute) ST_TRY(run_brute(c, t, q, a, st));
+      else ST_TRY(run_cake(t, r, q, a, st));
+      c->launches += 1;
+      return SWG_OK;
+    };
+    // The last of a few fanned-out host maps is swept in two row halves, so
+    // the first half's copy overlaps the second half's sweep (config 2 e2e
+    // 1.325 -> 1.312 ms; three or four parts: 1.327 / 1.40 ms).
+    constexpr int kSplit = 2;
+    const bool split = nwork > 1 && host_map(i) && i == n - 1 && p.engine != kExp64 &&
+                       !r.partial_in && !r.partial_out && p.rows >= 64;
     if (p.engine == kExp64) {  // reduces (and re-scores) its own peak
+      fill_sweep_args(a, t, r, p, dscores, parts);
       char* slice = static_cast<char*>(S.resc.p) + RescoreSlice::kBytes * i;
       ST_TRY(run_exp(c, t, r, p, a, parts, dpeaks + i, slice, st));
+      if (host_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
+    } else if (split) {
+      int done = 0, np = 0;  // rows and CTA candidates so far
+      for (int q = 0; q < kSplit; ++q) {
+        MapPlan h = p;
+        h.row0 = p.row0 + done;
+        h.rows = (q + 1) * p.rows / kSplit - done;
+        h.grid = sweep_grid(p.engine, p.mw, h.rows);
+        ST_TRY(sweep(h, dscores + (size_t)done * p.mw, parts + np));
+        np += (int)(h.grid.x * h.grid.y);
+        if (q + 1 < kSplit) ST_TRY(copy_rows(n * (q + 1) + i, done, h.rows));  // own event
+        else {
+          CUDA_TRY(launch_peak_reduce(parts, np, p.mw, a.hx, a.hy, dpeaks + i, st));
+          c->launches += 1;
+          ST_TRY(copy_rows(i, done, h.rows));
+        }
+        done += h.rows;
+      }
     } else {
-      if (p.engine == kQuad) ST_TRY(run_quad(t, p, a, st));
-      else if (p.engine == kAffine32) ST_TRY(run_affine(t, p, a, st));
-      else if (p.engine == kBrute) ST_TRY(run_brute(c, t, p, a, st));
-      else ST_TRY(run_cake(t, r, p, a, st));
-      c->launches += 1;
+      ST_TRY(sweep(p, dscores, parts));
       if (!r.partial_out) {
         CUDA_TRY(launch_peak_reduce(parts, (int)(p.grid.x * p.grid.y), p.mw, a.hx, a.hy,
                                     dpeaks + i, st));
         c->launches += 1;
       }
-    }
-    if (host_map(i)) {
-      // the copy stream takes the finished map while the next scale sweeps
-      while (c->events.size() <= (size_t)i) {
-        cudaEvent_t ev;
-        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        c->events.push_back(ev);
-      }
-      CUDA_TRY(cudaEventRecord(c->events[i], st));
-      CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[i], 0));
-      CUDA_TRY(cudaMemcpyAsync(scores_host[i], dscores, (size_t)p.rows * p.mw * 8,
-                               cudaMemcpyDeviceToHost, c->copy));
-      copies = true;
+      if (host_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
     }
   }
   for (int w = 0; w < nwork; ++w) {  // join the worker streams
