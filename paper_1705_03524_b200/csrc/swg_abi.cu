@@ -1329,6 +1329,7 @@ enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
 
 struct MapPlan {
   int row0 = 0, rows = 0, mw = 0;  // map rows [row0, row0 + rows) of width mw
+  int chain_s = 0, chain_k = 0, chain_j = 0;  // exponential chain order (0: off)
   Engine engine = kAffine32;
   swg_kernel k{};  // the kernel the engine sweeps (Plain maps: Uniform)
   dim3 grid;
@@ -1402,6 +1403,26 @@ swg_status validate_request(const swg_tables* t, const swg_map_request& r, bool 
   return SWG_OK;
 }
 
+// Super-column CTA order for the table sweeps whose corner span (2hy+2
+// table rows of the whole width) does not fit in L2: a strip of sw windows
+// needs (2hy+2+tile) rows x (sw+2hx+2) cells resident.  0 = row-major order.
+int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int hx, int hy) {
+  size_t cell = 0;  // table bytes per pixel the engine reads
+  if (e == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
+  else if (e == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
+  else if (e == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
+  else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
+  if (!cell) return 0;
+  const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
+  const double span =
+      2.0 * hy + 2 + (e == kExp64 ? kExpTileY : e == kQuad ? kQuadTileY : kSweepTileY);
+  if (span * (t->w + 1) * cell <= budget) return 0;
+  const double sw = budget / (span * cell) - (2.0 * hx + 2);
+  const int tw = e == kExp64 ? kExpTileX : kSweepTileX;  // windows per tile
+  if (sw >= 2 * tw && (sw + 2.0 * hx + 2) / sw < 1.7) return std::max(1, (int)(sw / tw));
+  return 0;
+}
+
 // CTA grid of a sweep over `rows` map rows of width mw.
 dim3 sweep_grid(Engine e, int mw, int rows) {
   if (e == kBrute)
@@ -1450,28 +1471,29 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
   p.engine = e;
   p.k = k;
   p.grid = sweep_grid(e, p.mw, p.rows);
+  if (e == kExp64 && kExpTileY == 1) {
+    // Chain order when a window's corner rows (2hy+2 table rows apart) do not
+    // stay in L2 under raster order and super-columns would be too narrow:
+    // window rows v and v + (hy+1) share the table row between v's bottom and
+    // (v+hy+1)'s top corners (the SE and h-flipped tables), and residue
+    // groups of 4 keep v + hy (the v-flipped tables' partner) close too
+    // (measured: 129^2 on config 4 38.9 -> 34.3 ms, config 5's 117-257
+    // scales -13 to -17 %; where super-columns apply they stay faster).
+    const double cell = (double)t->groups * kOct * 4 * 8;
+    const int hy = k_hy(k);
+    if ((2.0 * hy + 3) * (t->w + 1) * cell > (double)SWG_L2_BUDGET_MB * 1048576.0 &&
+        super_column_tiles(t, e, k, k_hx(k), hy) == 0) {
+      p.chain_s = hy + 1;
+      p.chain_k = std::min(4, p.chain_s);
+      p.chain_j = (p.rows + p.chain_s - 1) / p.chain_s;
+      const unsigned gx = (unsigned)((p.mw + kExpTileX - 1) / kExpTileX);
+      p.grid = dim3(gx * (unsigned)(p.chain_k * p.chain_j),
+                    (unsigned)((p.chain_s + p.chain_k - 1) / p.chain_k));
+    }
+  }
   return SWG_OK;
 }
 
-// Super-column CTA order for the table sweeps whose corner span (2hy+2
-// table rows of the whole width) does not fit in L2: a strip of sw windows
-// needs (2hy+2+tile) rows x (sw+2hx+2) cells resident.  0 = row-major order.
-int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int hx, int hy) {
-  size_t cell = 0;  // table bytes per pixel the engine reads
-  if (e == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
-  else if (e == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
-  else if (e == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
-  else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
-  if (!cell) return 0;
-  const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
-  const double span =
-      2.0 * hy + 2 + (e == kExp64 ? kExpTileY : e == kQuad ? kQuadTileY : kSweepTileY);
-  if (span * (t->w + 1) * cell <= budget) return 0;
-  const double sw = budget / (span * cell) - (2.0 * hx + 2);
-  const int tw = e == kExp64 ? kExpTileX : kSweepTileX;  // windows per tile
-  if (sw >= 2 * tw && (sw + 2.0 * hx + 2) / sw < 1.7) return std::max(1, (int)(sw / tw));
-  return 0;
-}
 
 // The kernel-independent sweep arguments of one request.
 void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r,
@@ -1496,7 +1518,10 @@ void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r
   std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
   a.pin = static_cast<const double2*>(r.partial_in);
   a.pout = static_cast<double2*>(r.partial_out);
-  a.sc_tiles = super_column_tiles(t, p.engine, p.k, a.hx, a.hy);
+  a.sc_tiles = p.chain_s ? 0 : super_column_tiles(t, p.engine, p.k, a.hx, a.hy);
+  a.chain_s = p.chain_s;
+  a.chain_k = p.chain_k;
+  a.chain_j = p.chain_j;
 }
 
 // Exponential kernel: quadrant rectangles in their orientation's SE table

@@ -113,6 +113,11 @@ struct SweepArgs {
   // tiles, each swept top to bottom, so the table rows between a window's
   // top and bottom corners stay in L2 (sweep_tile)
   int sc_tiles;
+  // chain order (exponential sweep): CTA (blockIdx.x = (tile column, chain
+  // step j, residue offset dv), blockIdx.y = residue group q) sweeps map row
+  // j*chain_s + q*chain_k + dv, so the rows sharing a table row (window v's
+  // bottom corners = window v+chain_s's top corners) run back to back
+  int chain_s, chain_k, chain_j;  // 0: off
   int wide0;           // cake16: ring 0's box count may exceed 16 bits
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
