@@ -930,11 +930,12 @@ class OursArm:
                 "ms_per_step": e2e_total / args.steps * 1e3}
 
     # ------------------------------------------------------------ rooflines
-    def _traffic_entry(self, kname):
+    def _traffic_entry(self, kname, k):
+        """The ncu capture of this launch (same kernel AND scale), if committed."""
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             tr = json.load(open(tp)).get(self.args.config)
-            if tr and kname in tr.get("kernel", ""):
+            if tr and kname in tr.get("kernel", "") and f"{k.kw}x{k.kh}" in tr["kernel"]:
                 return tr
         return None
 
@@ -957,7 +958,7 @@ class OursArm:
         dom_win = sum(win_launch[dom]) / len(win_launch[dom])
         launch_bins = next((u.get("bins_per_launch", nb) for u in self.units if u["g"] == gi), nb)
         dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
-        tr = self._traffic_entry(kname)
+        tr = self._traffic_entry(kname, k)
         roofline = {"bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9,
                     "peak": hbm, "unit": "GB/s", "traffic": tr["dram_bytes"] if tr else None,
                     "peak_source": src,
