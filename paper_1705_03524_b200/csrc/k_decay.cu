@@ -28,6 +28,8 @@
 
 #include <math.h>
 
+#include <cmath>
+
 namespace swg {
 
 namespace {
@@ -51,38 +53,46 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 }
 
 // K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
-// agg: [nbands][pairs][wa] double2.
+// agg: [nbands][pairs][wa] double2.  A thread covers kColPairs bin pairs of
+// one column, so each pixel is read once per 8 bins.
+constexpr int kColPairs = 4;
 __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs) {
-  const int band = blockIdx.x, pr = blockIdx.y;
+  const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr * kDP;
-  const uint32_t lim = (uint32_t)max(g.bins - pr * kDP, 0);  // bins of this pair in range
-  real c0 = 0.0, c1 = 0.0;
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr0 * kDP;
+  const uint32_t lim = (uint32_t)max(g.bins - pr0 * kDP, 0);  // bins of these pairs in range
+  real c[2 * kColPairs];
+#pragma unroll
+  for (int j = 0; j < 2 * kColPairs; ++j) c[j] = 0.0;
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
     uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
     d = d < lim ? d : 0xFFFFFFFFu;
-    c0 = fma(dec, c0, d == 0u ? 1.0 : 0.0);
-    c1 = fma(dec, c1, d == 1u ? 1.0 : 0.0);
+#pragma unroll
+    for (int j = 0; j < 2 * kColPairs; ++j) c[j] = fma(dec, c[j], d == (uint32_t)j ? 1.0 : 0.0);
   }
-  reinterpret_cast<double2*>(g.agg)[((size_t)band * pairs + pr) * g.wa + x] =
-      make_double2(c0, c1);
+  double2* dst = reinterpret_cast<double2*>(g.agg);
+#pragma unroll
+  for (int q = 0; q < kColPairs; ++q)
+    if (pr0 + q < pairs)
+      dst[((size_t)band * pairs + pr0 + q) * g.wa + x] = make_double2(c[2 * q], c[2 * q + 1]);
 }
 
 // K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place);
 // one warp per column word, lanes = 32 bands, affine shuffle scan.
 __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, int band_h,
-                                                        int h, real dec, size_t per_band) {
+                                                        int h, real dband, real dlast,
+                                                        size_t per_band) {
   const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (col >= per_band) return;
   real run = 0.0;
   for (int b0 = 0; b0 < nbands; b0 += 32) {
     const int b = b0 + lane;
-    const int hb = b < nbands ? min(band_h, h - b * band_h) : 0;
-    real ia = b < nbands ? pow(dec, (real)hb) : 1.0;
+    // d^(rows of band b): every band but the last has band_h rows (host powers)
+    real ia = b < nbands ? (b == nbands - 1 ? dlast : dband) : 1.0;
     real inc = b < nbands ? agg[(size_t)b * per_band + col] : 0.0;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -276,13 +286,16 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
   *launches = 0;
   const int pairs = a.groups * (kOct / kDP);
   if (a.nbands > 1) {
-    dim3 grid((unsigned)a.nbands, (unsigned)pairs, (unsigned)((a.w + 255) / 256));
+    dim3 grid((unsigned)a.nbands, (unsigned)((pairs + kColPairs - 1) / kColPairs),
+              (unsigned)((a.w + 255) / 256));
     k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t per_band = (size_t)pairs * a.wa * kDP;
+    const double dband = std::pow(dec, (double)a.band_h);
+    const double dlast = std::pow(dec, (double)(a.h - (a.nbands - 1) * a.band_h));
     k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dec, per_band);
+        reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }
