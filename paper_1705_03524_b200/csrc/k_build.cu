@@ -3,7 +3,7 @@
 // K1 replaces IntegralTableSet::build (proj/src/integral_tables.cpp:72-115),
 // which walks bin -> row -> column with running row sums plus the row above.
 // The GPU splits the rows into bands and builds every band independently:
-//   K1a k_colsum    per (band, bin octet, column): count and y-sum of each
+//   K1a k_colsum    per (band, bin octets, column): count and y-sum of each
 //                   bin over the band's rows;
 //   K1b k_bandscan  exclusive scan of those column sums over bands, so each
 //                   band knows the column sums of all rows above it;
@@ -125,39 +125,54 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V*
 }
 
 // K1a: column count, y-sum (and y^2-sum for quadratic planes) of each bin of
-// one octet over one row band.  agg[band][group][column][aw]: words 0-7
-// counts, 8-15 y-sums (aw >= 16: ramp planes), 16-23 y^2-sums (aw = 24).
+// G octets over one row band (each pixel read once per G octets).
+// agg[band][group][column][aw]: words 0-7 counts, 8-15 y-sums (aw >= 16: ramp
+// planes), 16-23 y^2-sums (aw = 24).
+template <int G, int AW>
 __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
-  const int band = blockIdx.x, grp = blockIdx.y;
+  const int band = blockIdx.x, grp0 = blockIdx.y * G;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp * kOct;
-  const uint32_t lim = (uint32_t)(g.bins - grp * kOct);  // bins of this octet in range
-  uint32_t cnt[kOct], ys[kOct], y2[kOct];
+  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp0 * kOct;
+  const uint32_t lim = (uint32_t)(g.bins - grp0 * kOct);  // bins of these octets in range
+  uint32_t cnt[G * kOct], ys[AW >= 16 ? G * kOct : 1], y2[AW == 24 ? G * kOct : 1];
 #pragma unroll
-  for (int j = 0; j < kOct; ++j) cnt[j] = ys[j] = y2[j] = 0;
+  for (int j = 0; j < G * kOct; ++j) {
+    cnt[j] = 0;
+    if constexpr (AW >= 16) ys[j] = 0;
+    if constexpr (AW == 24) y2[j] = 0;
+  }
   const uint16_t* col = g.fi + x;
   for (int y = y0; y < y1; ++y) {
     uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
     d = d < lim ? d : 0xFFFFFFFFu;
 #pragma unroll
-    for (int j = 0; j < kOct; ++j) {
+    for (int j = 0; j < G * kOct; ++j) {
       const bool hit = d == (uint32_t)j;
       cnt[j] += hit ? 1u : 0u;
-      ys[j] += hit ? (uint32_t)y : 0u;
-      y2[j] += hit ? (uint32_t)y * (uint32_t)y : 0u;
+      if constexpr (AW >= 16) ys[j] += hit ? (uint32_t)y : 0u;
+      if constexpr (AW == 24) y2[j] += hit ? (uint32_t)y * (uint32_t)y : 0u;
     }
   }
-  uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * g.aw);
-  dst[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
-  dst[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
-  if (g.aw == 8) return;  // plain tables carry counts only
-  dst[2] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
-  dst[3] = make_uint4(ys[4], ys[5], ys[6], ys[7]);
-  if (g.aw == 24) {
-    dst[4] = make_uint4(y2[0], y2[1], y2[2], y2[3]);
-    dst[5] = make_uint4(y2[4], y2[5], y2[6], y2[7]);
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    if (grp0 + q >= g.groups) break;
+    uint4* dst = reinterpret_cast<uint4*>(
+        g.agg + (((size_t)band * g.groups + grp0 + q) * g.wa + x) * AW);
+    const uint32_t* c = cnt + q * kOct;
+    dst[0] = make_uint4(c[0], c[1], c[2], c[3]);
+    dst[1] = make_uint4(c[4], c[5], c[6], c[7]);
+    if constexpr (AW >= 16) {
+      const uint32_t* t = ys + q * kOct;
+      dst[2] = make_uint4(t[0], t[1], t[2], t[3]);
+      dst[3] = make_uint4(t[4], t[5], t[6], t[7]);
+    }
+    if constexpr (AW == 24) {
+      const uint32_t* t = y2 + q * kOct;
+      dst[4] = make_uint4(t[0], t[1], t[2], t[3]);
+      dst[5] = make_uint4(t[4], t[5], t[6], t[7]);
+    }
   }
 }
 
@@ -463,8 +478,20 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)a.nbands, (unsigned)a.groups, (unsigned)((a.w + 255) / 256));
-  k_colsum<<<grid, 256, 0, s>>>(a);
+  // several octets per thread (up to 32 column sums in registers) while the
+  // grid keeps >= 2 CTAs per SM; small tables keep one octet per thread
+  // (config 1: 2 octets per thread +6 % per step, config 2: 4 octets -3 % build)
+  const unsigned cols = (unsigned)((a.w + 255) / 256);
+  auto ctas = [&](int gpt) { return (unsigned)a.nbands * ((a.groups + gpt - 1) / gpt) * cols; };
+  auto go = [&](auto kernel, int gpt) {
+    dim3 grid((unsigned)a.nbands, (unsigned)((a.groups + gpt - 1) / gpt), cols);
+    kernel<<<grid, 256, 0, s>>>(a);
+  };
+  if (a.aw == 8 && ctas(4) >= 296) go(k_colsum<4, 8>, 4);
+  else if (a.aw == 8) go(k_colsum<1, 8>, 1);
+  else if (a.aw == 16 && ctas(2) >= 296) go(k_colsum<2, 16>, 2);
+  else if (a.aw == 16) go(k_colsum<1, 16>, 1);
+  else go(k_colsum<1, 24>, 1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t per_band = (size_t)a.groups * a.wa * a.aw / 4;
