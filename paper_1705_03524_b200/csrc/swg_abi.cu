@@ -1706,13 +1706,31 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   swg_ctx* c = t->ctx;
-  // scratch: per-request score buffers (when the caller gave no device
-  // output), CTA peak candidates, device peaks, exact-peak slices
-  size_t stot = 0, ptot = 0;
+  // Zero-copy host maps: a host map in page-locked, device-mapped memory
+  // (swg_host_alloc / cudaMallocHost) is written by the sweep itself over
+  // PCIe, so no copy trails the last sweep (the exponential sweep's re-score
+  // reads its map back: it keeps the device scratch and a copy).
+  std::vector<double*> zc(n, nullptr);
   for (int i = 0; i < n; ++i) {
     MapPlan& p = plan[i];
     ST_TRY(plan_request(t, reqs[i], p));
-    if (!dev_map(i)) {
+    if (!host_map(i) || dev_map(i) || p.engine == kExp64 || std::getenv("SWG_NO_ZEROCOPY"))
+      continue;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, scores_host[i]) == cudaSuccess) {
+      if (at.type == cudaMemoryTypeHost && at.devicePointer)
+        zc[i] = static_cast<double*>(at.devicePointer);
+    } else {
+      cudaGetLastError();
+    }
+  }
+  auto copy_map = [&](int i) { return host_map(i) && !zc[i]; };
+  // scratch: per-request score buffers (when the caller gave no device or
+  // mapped output), CTA peak candidates, device peaks, exact-peak slices
+  size_t stot = 0, ptot = 0;
+  for (int i = 0; i < n; ++i) {
+    MapPlan& p = plan[i];
+    if (!dev_map(i) && !zc[i]) {
       p.soff = stot;
       stot += round_up((size_t)p.rows * p.mw, 32);
     }
@@ -1729,8 +1747,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   for (const MapPlan& p : plan)
     if (p.rows > 0 && (p.engine == kAffine32 || p.engine == kCake32)) ST_TRY(ensure_t32(t));
 
-  bool host_maps = false;
-  for (int i = 0; i < n; ++i) host_maps |= host_map(i);
+  bool host_maps = false;  // maps that still need a device-to-host copy
+  for (int i = 0; i < n; ++i) host_maps |= copy_map(i);
   int nwork = 0;
   cudaStream_t* wk = c->work;
   cudaEvent_t* wj = c->join;
@@ -1763,7 +1781,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     const MapPlan& p = plan[i];
     if (p.rows == 0) continue;
     const cudaStream_t st = nwork ? wk[i % nwork] : c->stream;
-    double* dscores = dev_map(i) ? scores_dev[i] : static_cast<double*>(S.scores.p) + p.soff;
+    double* dscores = dev_map(i) ? scores_dev[i]
+                      : zc[i]    ? zc[i]
+                                 : static_cast<double*>(S.scores.p) + p.soff;
     PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + p.poff;
     static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
     // the copy stream takes a finished map (or row range of it) while later
@@ -1795,13 +1815,13 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     // the first half's copy overlaps the second half's sweep (config 2 e2e
     // 1.325 -> 1.312 ms; three or four parts: 1.327 / 1.40 ms).
     constexpr int kSplit = 2;
-    const bool split = nwork > 1 && host_map(i) && i == n - 1 && p.engine != kExp64 &&
+    const bool split = nwork > 1 && copy_map(i) && i == n - 1 && p.engine != kExp64 &&
                        !r.partial_in && !r.partial_out && p.rows >= 64;
     if (p.engine == kExp64) {  // reduces (and re-scores) its own peak
       fill_sweep_args(a, t, r, p, dscores, parts);
       char* slice = static_cast<char*>(S.resc.p) + RescoreSlice::kBytes * i;
       ST_TRY(run_exp(c, t, r, p, a, parts, dpeaks + i, slice, st));
-      if (host_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
+      if (copy_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
     } else if (split) {
       int done = 0, np = 0;  // rows and CTA candidates so far
       for (int q = 0; q < kSplit; ++q) {
@@ -1826,7 +1846,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
                                     dpeaks + i, st));
         c->launches += 1;
       }
-      if (host_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
+      if (copy_map(i)) ST_TRY(copy_rows(i, 0, p.rows));
     }
   }
   for (int w = 0; w < nwork; ++w) {  // join the worker streams
@@ -1834,6 +1854,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     CUDA_TRY(cudaStreamWaitEvent(c->stream, wj[w], 0));
   }
   bool sync = copies;
+  for (int i = 0; i < n; ++i) sync |= zc[i] != nullptr;  // mapped maps: filled on return
   if (peaks_host) {
     CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
                              cudaMemcpyDeviceToHost, c->stream));

@@ -447,20 +447,28 @@ class Tables:
 
     def likelihood_maps(self, reqs: Sequence[MapRequest], scores: str = "host",
                         scores_dev=None, peaks_dev=None):
-        """Run len(reqs) map requests.  scores="host" returns numpy maps,
-        "none" skips them (peaks only); device outputs may be given as torch
-        tensors (then the call is asynchronous).  Returns (maps, peaks)."""
+        """Run len(reqs) map requests.  scores="host" returns numpy maps
+        (pageable memory: the library copies them), "pinned" the same in
+        page-locked memory (the sweeps write them directly), "none" skips them
+        (peaks only); device outputs may be given as torch tensors (then the
+        call is asynchronous).  Returns (maps, peaks)."""
         n = len(reqs)
         creqs, _keep = self._creqs(reqs, self.total_bins)
         maps = [None] * n
         host_ptrs = None
+        pinned = []
         if any(min(self.map_shape(r.kernel, r.rows)) <= 0 for r in reqs):
             scores = "none"  # invalid geometry: let the library raise SizeError
-        if scores == "host":
+        if scores in ("host", "pinned"):
             host_ptrs = (C.c_void_p * n)()
             for i, r in enumerate(reqs):
                 if r.partial_out is None:
-                    maps[i] = np.empty(self.map_shape(r.kernel, r.rows), np.float64)
+                    shape = self.map_shape(r.kernel, r.rows)
+                    if scores == "pinned":
+                        pinned.append(PinnedBuffer(shape, np.float64))
+                        maps[i] = pinned[-1].array
+                    else:
+                        maps[i] = np.empty(shape, np.float64)
                     host_ptrs[i] = maps[i].ctypes.data
         dev_ptrs = None
         if scores_dev is not None:
@@ -472,6 +480,8 @@ class Tables:
             C.addressof(dev_ptrs) if dev_ptrs is not None else None,
             C.addressof(peaks) if peaks is not None else None,
             _ptr(peaks_dev) if peaks_dev is not None else None))
+        if pinned:  # own copies: the page-locked buffers are freed with `pinned`
+            maps = [None if m is None else m.copy() for m in maps]
         if peaks is None:
             return maps, None
         return maps, [None if r.partial_out is not None else p.astuple()

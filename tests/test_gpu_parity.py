@@ -838,6 +838,38 @@ def test_decay_tables_strips_and_blocks(ctx, oracle):
                                    rtol=1e-12, atol=1e-10)
 
 
+def test_pinned_host_maps_zero_copy(ctx, oracle):
+    """Host maps in page-locked memory are written by the sweeps directly
+    (zero-copy): identical to the copied maps for every engine, one request
+    or several fanned out (the exponential sweep keeps its copy path)."""
+    img = oracle.random_gray(150, 120, 31)
+    bins, d = 16, 0.9375
+    fi = oracle.quantize_gray8(img, bins)
+    tabs = {swg.PLANES_PLAIN: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN),
+            swg.PLANES_AFFINE: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_AFFINE),
+            swg.PLANES_QUADRATIC: ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC),
+            swg.PLANES_DECAY: ctx.build_decay(img, d, swg.FMT_GRAY8, bins)}
+    cases = [(swg.PLANES_PLAIN, K(swg.GAUSS_CHEB, 21, 21, 0.5), swg.CAKE, 11),
+             (swg.PLANES_PLAIN, K(swg.UNIFORM, 15, 9), swg.PLAIN, 1),
+             (swg.PLANES_AFFINE, K(swg.MANHATTAN, 17, 13), swg.SWIH, 1),
+             (swg.PLANES_QUADRATIC, K(swg.EUCLID_QUAD, 19, 15), swg.SWIH, 1),
+             (swg.PLANES_DECAY, K(swg.EXP_L1, 13, 13, d), swg.SWIH, 1)]
+    by_tab = {}
+    for planes, k, method, rings in cases:
+        mdl = oracle.target_model(fi[20:20 + k.kh, 30:30 + k.kw].copy(), bins,
+                                  O.kernel(k.kind, k.kw, k.kh, k.sigma),
+                                  O.BRUTE if k.kind == swg.EXP_L1 else method, rings)
+        by_tab.setdefault(planes, []).append(swg.MapRequest(k, mdl, method, swg.BHATTACHARYYA,
+                                                            rings))
+    for planes, reqs in by_tab.items():
+        for group in ([r] for r in reqs) if len(reqs) == 1 else (reqs[:1], reqs):
+            want, wpk = tabs[planes].likelihood_maps(group, scores="host")
+            got, gpk = tabs[planes].likelihood_maps(group, scores="pinned")
+            assert gpk == wpk
+            for g_, w_ in zip(got, want):
+                assert (g_ == w_).all()
+
+
 def test_quadratic_tall_image(ctx, oracle):
     """32-bit quadratic planes have no height limit (the 64-bit export keeps
     the 2340-row limit of its y^2 carries): maps of a 40 x 3000 image."""
