@@ -156,7 +156,8 @@ const char* swg_last_error(void);
 size_t swg_last_required_bytes(void);
 swg_status swg_device_count(int* n);
 
-/* Page-locked host memory for asynchronous host<->device copies. */
+/* Page-locked, device-mapped host memory (portable across devices): fast
+ * asynchronous copies, and host maps the sweeps write directly. */
 swg_status swg_host_alloc(size_t bytes, void** out);
 swg_status swg_host_free(void* p);
 /* Peer memory between processes (one process per GPU): export a device

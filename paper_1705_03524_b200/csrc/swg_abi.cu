@@ -627,7 +627,8 @@ swg_status swg_ctx_destroy(swg_ctx* c) {
 
 swg_status swg_host_alloc(size_t bytes, void** out) {
   if (!out) return fail(SWG_ERR_ARG, "NULL out");
-  CUDA_TRY(cudaMallocHost(out, bytes));
+  // portable + mapped: every device may write it directly (zero-copy maps)
+  CUDA_TRY(cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
   return SWG_OK;
 }
 
