@@ -746,7 +746,9 @@ class OursArm:
         torch.cuda.synchronize()
         clocks.start()
         t_host = time.perf_counter()
+        l0 = self.ctx.launches
         self.step()
+        step_launches = self.ctx.launches - l0  # the step the graph replays
         torch.cuda.synchronize()
         enqueue_s = time.perf_counter() - t_host  # host time of one eager step (sizes the spin)
         launches0 = self.ctx.launches
@@ -759,10 +761,11 @@ class OursArm:
             self.step(events[s])
         torch.cuda.synchronize()
         clk = clocks.stop()
-        launches = self.ctx.launches - launches0  # over the K timed steps
+        launches = self.ctx.launches - launches0  # over the K timed (per-launch) steps
         self.barrier()
         per_step = [events[s][0].elapsed_time(events[s][-1]) for s in range(args.steps)]
         if graph is not None:  # headline timing: graph replays (same kernels, no launch gaps)
+            launches = step_launches * args.steps  # the replayed step's kernels
             gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
                    for _ in range(args.steps)]
             self.barrier()

@@ -165,10 +165,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs 
 // exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
 // exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
 template <int SIM>
-__global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(const SweepArgs a) {
+__device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, PeakPart* part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  int tx, ty;
-  sweep_tile(a.sc_tiles, tx, ty);
   const int u0 = tx * kSweepTileX + (lane >> 1);
   const int r0 = ty * kQuadTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
@@ -222,7 +220,25 @@ __global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(cons
     s = clamp01(s);
     if (active && half == 0) a.scores[widx] = s;
   }
-  sweep_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, a);
+  cta_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, part);
+}
+
+template <int SIM>
+__global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(const SweepArgs a) {
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  quad_body<SIM>(a, tx, ty, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+// Several quadratic maps of ONE table in one launch (a frame's scales):
+// CTA b sweeps tile b / n of map b % n, so the maps' tiles over the same
+// image region run together and share the table rows they read in L2.
+template <int SIM>
+__global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad_multi(
+    const QuadMulti m) {
+  const int k = blockIdx.x % m.n, tile = blockIdx.x / m.n;
+  if (tile >= m.gx[k] * m.gy[k]) return;  // (a shorter map: no CTA here)
+  quad_body<SIM>(m.a[k], tile % m.gx[k], tile / m.gx[k], m.a[k].parts + tile);
 }
 
 // K2c: wedding-cake telescoping over nested boxes of the plain table.
@@ -566,6 +582,15 @@ cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake<0><<<grid, kSweepThreads, 0, s>>>(a, r);
   else k_sweep_cake<1><<<grid, kSweepThreads, 0, s>>>(a, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s) {
+  int most = 0;
+  for (int k = 0; k < m.n; ++k) most = max(most, m.gx[k] * m.gy[k]);
+  const unsigned grid = (unsigned)(most * m.n);
+  if (m.a[0].sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad_multi<0><<<grid, kQuadThreads, 0, s>>>(m);
+  else k_sweep_quad_multi<1><<<grid, kQuadThreads, 0, s>>>(m);
   return cudaGetLastError();
 }
 

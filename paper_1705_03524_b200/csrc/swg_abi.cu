@@ -1615,13 +1615,17 @@ swg_status run_exp(swg_ctx* c, const swg_tables* t, const swg_map_request& r, co
 
 // Euclidean: box corners (TL, TR, BL, BR) of the whole window as byte
 // offsets from the centre record within a plane of the 32-bit tables.
-swg_status run_quad(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
+void quad_args(const swg_tables* t, const MapPlan& p, SweepArgs& a) {
   a.mass = (double)quad_mass(p.k);
   const long long p8 = (long long)t->pitch * kOct;
   const long long xs[2] = {-a.hx, a.hx + 1}, ys[2] = {-a.hy, a.hy + 1};
   for (int pl = 0; pl < 5; ++pl)
     for (int q = 0; q < 4; ++q)
       a.lat[4 * pl + q] = (int)(4 * (ys[q >> 1] * p8 + xs[q & 1] * kOct));
+}
+
+swg_status run_quad(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
+  quad_args(t, p, a);
   CUDA_TRY(launch_sweep_quad(a, p.grid, st));
   return SWG_OK;
 }
@@ -1777,7 +1781,39 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
 #endif
 
   bool copies = false;
-  for (int i = 0; i < n; ++i) {
+  // A frame's quadratic scales in sequence (frame batches): one launch over
+  // all of them, so they read the table's rows together (L2) instead of the
+  // table once per scale.
+  bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti &&
+               !std::getenv("SWG_NO_QUAD_MULTI");
+  for (int i = 0; i < n && fused; ++i)
+    fused = plan[i].engine == kQuad && plan[i].rows > 0 && !reqs[i].partial_in &&
+            !reqs[i].partial_out && !copy_map(i) &&
+            super_column_tiles(t, kQuad, plan[i].k, k_hx(plan[i].k), k_hy(plan[i].k)) == 0;
+  if (fused) {
+    static thread_local QuadMulti m;  // ~25 KB of kernel parameters
+    m.n = n;
+    for (int i = 0; i < n; ++i) {
+      const MapPlan& p = plan[i];
+      double* dscores = dev_map(i) ? scores_dev[i]
+                        : zc[i]    ? zc[i]
+                                   : static_cast<double*>(S.scores.p) + p.soff;
+      fill_sweep_args(m.a[i], t, reqs[i], p, dscores, static_cast<PeakPart*>(S.parts.p) + p.poff);
+      quad_args(t, p, m.a[i]);
+      m.gx[i] = (int)p.grid.x;
+      m.gy[i] = (int)p.grid.y;
+    }
+    CUDA_TRY(launch_sweep_quad_multi(m, c->stream));
+    c->launches += 1;
+    for (int i = 0; i < n; ++i) {
+      const MapPlan& p = plan[i];
+      CUDA_TRY(launch_peak_reduce(static_cast<PeakPart*>(S.parts.p) + p.poff,
+                                  (int)(p.grid.x * p.grid.y), p.mw, m.a[i].hx, m.a[i].hy,
+                                  dpeaks + i, c->stream));
+      c->launches += 1;
+    }
+  }
+  for (int i = 0; i < n && !fused; ++i) {
     const swg_map_request& r = reqs[i];
     const MapPlan& p = plan[i];
     if (p.rows == 0) continue;

@@ -122,6 +122,14 @@ struct SweepArgs {
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
+// Up to kQuadMulti quadratic maps of one table swept by one launch.
+constexpr int kQuadMulti = 3;
+struct QuadMulti {
+  SweepArgs a[kQuadMulti];
+  int gx[kQuadMulti], gy[kQuadMulti];  // each map's CTA tiles
+  int n;
+};
+
 // Host-side ring plan of a wedding-cake configuration.
 struct CakeRings {
   int a[kMaxRings];        // ring i box half-extent in x: hx - shrink_x[i]
@@ -307,6 +315,7 @@ cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cud
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);
+cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s);
 cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s);
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
