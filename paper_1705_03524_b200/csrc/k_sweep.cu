@@ -460,8 +460,21 @@ __global__ void __launch_bounds__(kCakeThreads) k_sweep_cake16(const SweepArgs a
 }
 
 // K3: reduce CTA candidates to the map peak (one CTA).
+__device__ __forceinline__ void peak_reduce_body(const PeakPart* parts, int n, int mw, int hx,
+                                                 int hy, swg_peak* out);
 __global__ void __launch_bounds__(1024) k_peak_reduce(const PeakPart* parts, int n, int mw,
                                                       int hx, int hy, swg_peak* out) {
+  peak_reduce_body(parts, n, mw, hx, hy, out);
+}
+
+// K3 for the maps of one k_sweep_quad_multi launch: CTA k reduces map k.
+__global__ void __launch_bounds__(1024) k_peak_reduce_multi(const PeakMulti m) {
+  const int k = blockIdx.x;
+  peak_reduce_body(m.parts[k], m.n[k], m.mw[k], m.hx[k], m.hy[k], m.out[k]);
+}
+
+__device__ __forceinline__ void peak_reduce_body(const PeakPart* parts, int n, int mw, int hx,
+                                                 int hy, swg_peak* out) {
   double s = -2.0;
   long long idx = 0x7FFFFFFFFFFFFFFFLL;
   constexpr int kBatch = 8;  // independent loads in flight per thread
@@ -604,6 +617,11 @@ cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 gri
                                 cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake16<0><<<grid, kCakeThreads, 0, s>>>(a, r);
   else k_sweep_cake16<1><<<grid, kCakeThreads, 0, s>>>(a, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peak_reduce_multi(const PeakMulti& m, int maps, cudaStream_t s) {
+  k_peak_reduce_multi<<<maps, 1024, 0, s>>>(m);
   return cudaGetLastError();
 }
 

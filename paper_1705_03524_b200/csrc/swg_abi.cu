@@ -1804,14 +1804,18 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       m.gy[i] = (int)p.grid.y;
     }
     CUDA_TRY(launch_sweep_quad_multi(m, c->stream));
-    c->launches += 1;
+    PeakMulti pm;
     for (int i = 0; i < n; ++i) {
       const MapPlan& p = plan[i];
-      CUDA_TRY(launch_peak_reduce(static_cast<PeakPart*>(S.parts.p) + p.poff,
-                                  (int)(p.grid.x * p.grid.y), p.mw, m.a[i].hx, m.a[i].hy,
-                                  dpeaks + i, c->stream));
-      c->launches += 1;
+      pm.parts[i] = static_cast<PeakPart*>(S.parts.p) + p.poff;
+      pm.n[i] = (int)(p.grid.x * p.grid.y);
+      pm.mw[i] = p.mw;
+      pm.hx[i] = m.a[i].hx;
+      pm.hy[i] = m.a[i].hy;
+      pm.out[i] = dpeaks + i;
     }
+    CUDA_TRY(launch_peak_reduce_multi(pm, n, c->stream));
+    c->launches += 2;
   }
   for (int i = 0; i < n && !fused; ++i) {
     const swg_map_request& r = reqs[i];

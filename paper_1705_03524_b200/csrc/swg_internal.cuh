@@ -130,6 +130,12 @@ struct QuadMulti {
   int n;
 };
 
+struct PeakMulti {  // k_peak_reduce over the maps of one multi-map launch
+  const PeakPart* parts[kQuadMulti];
+  int n[kQuadMulti], mw[kQuadMulti], hx[kQuadMulti], hy[kQuadMulti];
+  swg_peak* out[kQuadMulti];
+};
+
 // Host-side ring plan of a wedding-cake configuration.
 struct CakeRings {
   int a[kMaxRings];        // ring i box half-extent in x: hx - shrink_x[i]
@@ -316,6 +322,7 @@ cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s);
+cudaError_t launch_peak_reduce_multi(const PeakMulti& m, int maps, cudaStream_t s);
 cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s);
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
