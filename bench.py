@@ -937,9 +937,10 @@ class OursArm:
         """The ncu capture of this launch (same kernel AND scale), if committed."""
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            tr = json.load(open(tp)).get(self.args.config)
-            if tr and kname in tr.get("kernel", "") and f"{k.kw}x{k.kh}" in tr["kernel"]:
-                return tr
+            entries = json.load(open(tp)).get(self.args.config) or []
+            for tr in entries if isinstance(entries, list) else [entries]:
+                if kname in tr.get("kernel", "") and f"{k.kw}x{k.kh} " in tr["kernel"] + " ":
+                    return tr
         return None
 
     def sweep_roofline(self, sweep_ms, clk):
