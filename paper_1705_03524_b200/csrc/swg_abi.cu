@@ -1681,6 +1681,45 @@ swg_status run_cake(const swg_tables* t, const swg_map_request& r, const MapPlan
   return SWG_OK;
 }
 
+// Device address of a page-locked, device-mapped host buffer (zero-copy
+// maps), or nullptr for pageable / device memory.
+double* mapped_host(void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? static_cast<double*>(at.devicePointer) : nullptr;
+}
+
+// A frame's quadratic scales (frame batches) in one launch over all of them,
+// so they read the table's rows together (L2) instead of the table once per
+// scale, and one launch for their peaks.
+swg_status run_quad_multi(swg_ctx* c, const swg_tables* t, int n, const swg_map_request* reqs,
+                          const std::vector<MapPlan>& plan, double* const* scores,
+                          PeakPart* parts, swg_peak* peaks) {
+  static thread_local QuadMulti m;  // ~25 KB of kernel parameters
+  PeakMulti pm;
+  m.n = n;
+  for (int i = 0; i < n; ++i) {
+    const MapPlan& p = plan[i];
+    fill_sweep_args(m.a[i], t, reqs[i], p, scores[i], parts + p.poff);
+    quad_args(t, p, m.a[i]);
+    m.gx[i] = (int)p.grid.x;
+    m.gy[i] = (int)p.grid.y;
+    pm.parts[i] = parts + p.poff;
+    pm.n[i] = (int)(p.grid.x * p.grid.y);
+    pm.mw[i] = p.mw;
+    pm.hx[i] = m.a[i].hx;
+    pm.hy[i] = m.a[i].hy;
+    pm.out[i] = peaks + i;
+  }
+  CUDA_TRY(launch_sweep_quad_multi(m, c->stream));
+  CUDA_TRY(launch_peak_reduce_multi(pm, n, c->stream));
+  c->launches += 2;
+  return SWG_OK;
+}
+
 // Direct per-pixel weighted histogram (baselines.cpp:24-69).
 swg_status run_brute(swg_ctx* c, const swg_tables* t, const MapPlan& p, const SweepArgs& a,
                      cudaStream_t st) {
@@ -1717,17 +1756,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // reads its map back: it keeps the device scratch and a copy).
   std::vector<double*> zc(n, nullptr);
   for (int i = 0; i < n; ++i) {
-    MapPlan& p = plan[i];
-    ST_TRY(plan_request(t, reqs[i], p));
-    if (!host_map(i) || dev_map(i) || p.engine == kExp64 || std::getenv("SWG_NO_ZEROCOPY"))
-      continue;
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, scores_host[i]) == cudaSuccess) {
-      if (at.type == cudaMemoryTypeHost && at.devicePointer)
-        zc[i] = static_cast<double*>(at.devicePointer);
-    } else {
-      cudaGetLastError();
-    }
+    ST_TRY(plan_request(t, reqs[i], plan[i]));
+    if (host_map(i) && !dev_map(i) && plan[i].engine != kExp64) zc[i] = mapped_host(scores_host[i]);
   }
   auto copy_map = [&](int i) { return host_map(i) && !zc[i]; };
   // scratch: per-request score buffers (when the caller gave no device or
@@ -1781,51 +1811,27 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
 #endif
 
   bool copies = false;
-  // A frame's quadratic scales in sequence (frame batches): one launch over
-  // all of them, so they read the table's rows together (L2) instead of the
-  // table once per scale.
-  bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti &&
-               !std::getenv("SWG_NO_QUAD_MULTI");
+  // the score output of request i: the caller's device map, its mapped host
+  // map, or device scratch
+  std::vector<double*> out(n);
+  for (int i = 0; i < n; ++i)
+    out[i] = dev_map(i) ? scores_dev[i]
+             : zc[i]    ? zc[i]
+                        : static_cast<double*>(S.scores.p) + plan[i].soff;
+  PeakPart* parts0 = static_cast<PeakPart*>(S.parts.p);
+  bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti;
   for (int i = 0; i < n && fused; ++i)
     fused = plan[i].engine == kQuad && plan[i].rows > 0 && !reqs[i].partial_in &&
             !reqs[i].partial_out && !copy_map(i) &&
             super_column_tiles(t, kQuad, plan[i].k, k_hx(plan[i].k), k_hy(plan[i].k)) == 0;
-  if (fused) {
-    static thread_local QuadMulti m;  // ~25 KB of kernel parameters
-    m.n = n;
-    for (int i = 0; i < n; ++i) {
-      const MapPlan& p = plan[i];
-      double* dscores = dev_map(i) ? scores_dev[i]
-                        : zc[i]    ? zc[i]
-                                   : static_cast<double*>(S.scores.p) + p.soff;
-      fill_sweep_args(m.a[i], t, reqs[i], p, dscores, static_cast<PeakPart*>(S.parts.p) + p.poff);
-      quad_args(t, p, m.a[i]);
-      m.gx[i] = (int)p.grid.x;
-      m.gy[i] = (int)p.grid.y;
-    }
-    CUDA_TRY(launch_sweep_quad_multi(m, c->stream));
-    PeakMulti pm;
-    for (int i = 0; i < n; ++i) {
-      const MapPlan& p = plan[i];
-      pm.parts[i] = static_cast<PeakPart*>(S.parts.p) + p.poff;
-      pm.n[i] = (int)(p.grid.x * p.grid.y);
-      pm.mw[i] = p.mw;
-      pm.hx[i] = m.a[i].hx;
-      pm.hy[i] = m.a[i].hy;
-      pm.out[i] = dpeaks + i;
-    }
-    CUDA_TRY(launch_peak_reduce_multi(pm, n, c->stream));
-    c->launches += 2;
-  }
+  if (fused) ST_TRY(run_quad_multi(c, t, n, reqs, plan, out.data(), parts0, dpeaks));
   for (int i = 0; i < n && !fused; ++i) {
     const swg_map_request& r = reqs[i];
     const MapPlan& p = plan[i];
     if (p.rows == 0) continue;
     const cudaStream_t st = nwork ? wk[i % nwork] : c->stream;
-    double* dscores = dev_map(i) ? scores_dev[i]
-                      : zc[i]    ? zc[i]
-                                 : static_cast<double*>(S.scores.p) + p.soff;
-    PeakPart* parts = static_cast<PeakPart*>(S.parts.p) + p.poff;
+    double* dscores = out[i];
+    PeakPart* parts = parts0 + p.poff;
     static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
     // the copy stream takes a finished map (or row range of it) while later
     // sweeps run
