@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_cake(const SweepArgs a,
 // 16-byte records (8 bins) per corner: half the bytes of the 32-bit path,
 // box arithmetic on packed 16-bit pairs (vsub2/vadd2).
 template <int SIM>
-__global__ void __launch_bounds__(kCakeThreads) k_sweep_cake16(const SweepArgs a,
-                                                                const CakeSweep rg) {
+__global__ void __launch_bounds__(kCakeThreads, SIM == SWG_SIM_BHATTACHARYYA ? SWG_CAKE_MINB : 1)
+    k_sweep_cake16(const SweepArgs a, const CakeSweep rg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u0 = blockIdx.x * 32 + lane;
   const int r0 = blockIdx.y * kCakeTileY + warp;

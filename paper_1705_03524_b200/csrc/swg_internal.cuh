@@ -308,6 +308,9 @@ constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kExpThreads / 32 / kExpWa
 #ifndef SWG_CAKE_TY
 #define SWG_CAKE_TY 4
 #endif
+#ifndef SWG_CAKE_MINB
+#define SWG_CAKE_MINB 10  // <= 48 registers: 10 CTAs (40 warps) per SM; 40 registers spill (+3 %)
+#endif
 constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
