@@ -80,7 +80,7 @@ __device__ __forceinline__ void add_octet(const double (&val)[4], const double (
 
 // K2a: Uniform (4 cells per bin) or Manhattan (20 cells per bin).
 template <int SIM, bool UNIFORM>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_affine(const SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   int tx, ty;
   sweep_tile(a.sc_tiles, tx, ty);

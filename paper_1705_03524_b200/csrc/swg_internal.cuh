@@ -275,6 +275,9 @@ __device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
 #ifndef SWG_SWEEP_TY
 #define SWG_SWEEP_TY 8
 #endif
+#ifndef SWG_AFFINE_MINB
+#define SWG_AFFINE_MINB 4  // 64 registers (explicit: config 5 Manhattan -4 % against the implicit 64)
+#endif
 constexpr int kSweepTileY = SWG_SWEEP_TY;
 constexpr int kSweepThreads = 32 * kSweepTileY;
 constexpr int kSweepTileX = 16;
