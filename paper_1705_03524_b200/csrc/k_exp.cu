@@ -36,9 +36,9 @@ __device__ __forceinline__ double2 ldd2(const char* p) {
 // octet, so the ordered sums need no shuffles.
 template <int SIM>
 #ifndef SWG_EXP_MINB
-// <= 128 registers at 128 threads: deep per-lane load batches (measured: 80
-// registers +3-5 %, 252 registers +14 %; 128 and 168 equal)
-#define SWG_EXP_MINB 4
+// <= 96 registers at 128 threads: deep per-lane load batches, 5 CTAs per SM
+// (measured on config 4: 96 registers 230 ms, 128 233 ms, 80 +3-5 %, 252 +14 %)
+#define SWG_EXP_MINB 5
 #endif
 __global__ void __launch_bounds__(kExpThreads, SWG_EXP_MINB) k_sweep_exp(const SweepArgs a,
                                                                          const ExpSweep e) {
