@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(cons
 // CTA b sweeps tile b / n of map b % n, so the maps' tiles over the same
 // image region run together and share the table rows they read in L2.
 template <int SIM>
-__global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad_multi(
+__global__ void __launch_bounds__(kQuadThreads, SWG_QUADM_MINB) k_sweep_quad_multi(
     const QuadMulti m) {
   const int k = blockIdx.x % m.n, tile = blockIdx.x / m.n;
   if (tile >= m.gx[k] * m.gy[k]) return;  // (a shorter map: no CTA here)

@@ -288,7 +288,10 @@ constexpr int kSweepTileX = 16;
 #define SWG_QUAD_TY 4
 #endif
 #ifndef SWG_QUAD_MINB
-#define SWG_QUAD_MINB 8  // 64 registers, 8 CTAs per SM (96: config 5's Euclidean +6 %)
+#define SWG_QUAD_MINB 7  // 72 registers (64: config 5's Euclidean +6 %, 96: +6 %)
+#endif
+#ifndef SWG_QUADM_MINB
+#define SWG_QUADM_MINB 8  // the multi-map launch: 64 registers (72: config 3 +2 %)
 #endif
 constexpr int kQuadTileY = SWG_QUAD_TY, kQuadThreads = 32 * kQuadTileY;
 // Exponential sweep CTA tile: kExpWarpsX warps side by side on one map row
