@@ -130,3 +130,25 @@ def test_exponential_rectangle_identity(oracle, d, kw, kh):
                     acc += cf[q] * E[o][:, y + ys[q], x + xs[q]]
             want = oracle.brute_weights(fi, bins, cx, cy, ok)
             np.testing.assert_allclose(acc, want, rtol=0, atol=1e-12)
+
+
+def test_profiles_traffic_entries_resolve():
+    """Every committed ncu traffic entry names a kernel and a scale of its
+    config's workload and points at a committed summary holding the DRAM
+    bytes it quotes (bench.py's roofline `traffic` comes from these)."""
+    import json
+    import os
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tr = json.load(open(os.path.join(root, "profiles", "traffic.json")))
+    for cfg, entries in tr.items():
+        wl = bench.workload(cfg)
+        sizes = {f"{k.kw}x{k.kh}" for g in wl["groups"] for k, _, _, _ in g["scales"]}
+        for e in entries if isinstance(entries, list) else [entries]:
+            assert e["kernel"].startswith("k_sweep_"), e
+            scale = re.search(r"\((\d+x\d+) scale", e["kernel"]).group(1)
+            assert scale in sizes, (cfg, scale)
+            src = os.path.join(root, e["source"])
+            assert os.path.exists(src), src
+            assert "dram__bytes_read.sum" in open(src).read()
+            assert e["dram_bytes"] > 0
