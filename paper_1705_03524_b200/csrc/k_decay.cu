@@ -54,8 +54,11 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 
 // K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
 // agg: [nbands][pairs][wa] double2.  A thread covers kColPairs bin pairs of
-// one column, so each pixel is read once per 8 bins.
-constexpr int kColPairs = 4;
+// one column, so each pixel is read once per 2 * kColPairs bins.
+#ifndef SWG_COL_PAIRS
+#define SWG_COL_PAIRS 8  // 16 bins per thread (4 pairs: config 4 builds +0.4 ms)
+#endif
+constexpr int kColPairs = SWG_COL_PAIRS;
 __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs) {
   const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
