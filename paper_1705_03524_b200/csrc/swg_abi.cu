@@ -1681,15 +1681,18 @@ swg_status run_cake(const swg_tables* t, const swg_map_request& r, const MapPlan
   return SWG_OK;
 }
 
-// Device address of a page-locked, device-mapped host buffer (zero-copy
-// maps), or nullptr for pageable / device memory.
-double* mapped_host(void* p) {
+// Device address of a page-locked, device-mapped host buffer allocated
+// against this context's device (zero-copy maps), or nullptr for pageable,
+// device or other devices' page-locked memory (those take the copy path).
+double* mapped_host(void* p, int device) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  return at.type == cudaMemoryTypeHost ? static_cast<double*>(at.devicePointer) : nullptr;
+  return at.type == cudaMemoryTypeHost && at.device == device
+             ? static_cast<double*>(at.devicePointer)
+             : nullptr;
 }
 
 // A frame's quadratic scales (frame batches) in one launch over all of them,
@@ -1757,7 +1760,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   std::vector<double*> zc(n, nullptr);
   for (int i = 0; i < n; ++i) {
     ST_TRY(plan_request(t, reqs[i], plan[i]));
-    if (host_map(i) && !dev_map(i) && plan[i].engine != kExp64) zc[i] = mapped_host(scores_host[i]);
+    if (host_map(i) && !dev_map(i) && plan[i].engine != kExp64) zc[i] = mapped_host(scores_host[i], c->device);
   }
   auto copy_map = [&](int i) { return host_map(i) && !zc[i]; };
   // scratch: per-request score buffers (when the caller gave no device or
