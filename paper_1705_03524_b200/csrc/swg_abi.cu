@@ -1828,11 +1828,28 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
             !reqs[i].partial_out && !copy_map(i) &&
             super_column_tiles(t, kQuad, plan[i].k, k_hx(plan[i].k), k_hy(plan[i].k)) == 0;
   if (fused) ST_TRY(run_quad_multi(c, t, n, reqs, plan, out.data(), parts0, dpeaks));
-  for (int i = 0; i < n && !fused; ++i) {
+  // Device-output fan-out issues the costliest sweeps first (longest-first
+  // packing: the last scale to start is a short one; config 2 1.130 ->
+  // 1.114 ms); host-map fan-out keeps request order (its streams'
+  // priorities order the copies).
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  if (nwork > 1 && !host_maps) {
+    auto cost = [&](int i) {
+      const MapPlan& p = plan[i];
+      const double rings = p.engine == kCake16 || p.engine == kCake32
+                               ? (reqs[i].method == SWG_METHOD_CAKE ? reqs[i].rings : 1)
+                               : 1;
+      return (double)p.rows * p.mw * rings;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+  }
+  for (int q = 0; q < n && !fused; ++q) {
+    const int i = order[q];
     const swg_map_request& r = reqs[i];
     const MapPlan& p = plan[i];
     if (p.rows == 0) continue;
-    const cudaStream_t st = nwork ? wk[i % nwork] : c->stream;
+    const cudaStream_t st = nwork ? wk[q % nwork] : c->stream;
     double* dscores = out[i];
     PeakPart* parts = parts0 + p.poff;
     static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
