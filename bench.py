@@ -6,23 +6,28 @@
 
 One step = one pass of the hot path over one batch of input: quantise +
 weighted integral histogram build, then the full strict likelihood map +
-peak at every scale.  Default (BASELINE.json configs[1]): one 1024x1024 u8
-frame, 32 bins, Gaussian kernel (GaussianChebyshev sigma=0.5, exact
-full-ring wedding cake), windows 33/65/97.  The other configs:
+peak at every scale.  Default: BASELINE.json configs[4], the config the
+metric is quoted on ("windows/s and IH GB/s per kernel and scale"): one
+2048x2048 u16 frame, 64 bins, Manhattan + Gaussian (GaussianChebyshev
+sigma=0.5, exact full-ring wedding cake) + Euclidean (declared quadratic) +
+exponential (declared, decay 15/16 per pixel) at windows 17..257 (8 scales
+each).  The other configs:
   c1   256x256 u8, 16 bins, Manhattan 33x33                      (configs[0])
+  c2   1024x1024 u8, 32 bins, Gaussian (exact cake), 33/65/97   (configs[1])
   c3   64 RGB 1920x1080 frames (tracking sequence), 4x4x4 bins, Euclidean
        (declared quadratic form), windows 45x59/49x65/53x71 on a 256x256
        search region around the previous ground truth           (configs[2])
   c4   3840x2160 RGB, 8x8x8 bins, exponential (decay 15/16 per pixel),
        windows 25/37/57/85/129; one row band per rank             (configs[3])
-  c5   2048x2048 u16, 64 bins, Manhattan + Gaussian + Euclidean +
-       exponential at windows 17..257 (8 scales each)             (configs[4])
   c5m  c5's Manhattan subset
 `value` = weighted windows/s over all ranks with the input resident in HBM;
 `e2e` = the same through the C-ABI with pinned host input and host maps /
-peaks out.  N>1 (torchrun): frames (c1/c2/c5: one per GPU, weak scaling),
-sequence frames (c3) or row bands (c4) sharded over ranks (strong scaling);
-no data-path collective; the timed region is the max over ranks.
+peaks out.  N>1 (torchrun), strong scaling throughout: one frame's
+(kernel, scale) requests partitioned over ranks (c1/c2/c5: LPT by
+estimated cost, the largest split by map rows, each rank building only the
+table sets its requests read -- dist.plan_frame), sequence frames (c3) or
+row bands (c4); no data-path collective; the timed region is the max over
+ranks.
 --impl reference times the reference CPU implementation (oracle/_ref, the
 unmodified reference sources; the oracle restatement for the kernels the
 reference lacks) on this host's cores.
@@ -45,6 +50,12 @@ sys.path.insert(0, ROOT)
 METRIC = "weighted windows/s"
 UNIT = "windows/s"
 EXP_DECAY = 15.0 / 16.0  # declared exponential kernel: weight 15/16 per pixel of L1 distance
+# the one decay serves every scale (one decayed table set per frame): the
+# weight falls to 1/e at 15.5 px and to 1e-2 at 71 px of L1 distance from
+# the centre, so the larger windows share that support
+EXP_NOTE = ("exponential w = (15/16)^(|dx|+|dy|) at every scale (one decayed table set; "
+            "weight 1/e at 15.5 px, 1e-2 at 71 px L1)")
+L2_NOTE = "GPU arm: L2 flushed between timed steps (256 MiB write, untimed)"
 
 
 def peaks_json():
@@ -64,7 +75,7 @@ def workload(name):
     K = swg.Kernel
     if name == "c1":
         return dict(name="config1: 256x256 u8, 16 bins, Manhattan, window 33x33", kind="frame",
-                    gen=synth.config1, fmt=swg.FMT_GRAY8, bins=16, nbins=16, scaling="weak",
+                    gen=synth.config1, fmt=swg.FMT_GRAY8, bins=16, nbins=16, scaling="strong",
                     groups=[dict(planes=swg.PLANES_AFFINE,
                                  scales=[(K(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)])])
     if name in ("c5", "c5m"):
@@ -83,11 +94,11 @@ def workload(name):
                      scales=[(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None) for k in ks]),
             ]
             label = ("Manhattan + Gaussian (exact full-ring cake) + Euclidean (quadratic) + "
-                     "exponential (decay 15/16)")
+                     + EXP_NOTE)
         return dict(name=f"config5{' (Manhattan subset)' if name == 'c5m' else ''}: 2048x2048 "
                          f"u16, 64 bins, {label}, windows " + "/".join(map(str, ks)),
                     kind="frame", gen=synth.config5, fmt=swg.FMT_GRAY16, bins=64, nbins=64,
-                    scaling="weak", groups=groups)
+                    scaling="strong", groups=groups)
     if name == "c3":
         scales = [(K(swg.EUCLID_QUAD, kw, kh), swg.SWIH, 1, 0)
                   for kw, kh in ((45, 59), (49, 65), (53, 71))]
@@ -98,8 +109,8 @@ def workload(name):
     if name == "c4":
         scales = [(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None)
                   for k in (25, 37, 57, 85, 129)]
-        return dict(name="config4: 3840x2160 RGB, 8x8x8 bins, exponential (decay 15/16), "
-                         "windows 25/37/57/85/129, row bands",
+        return dict(name="config4: 3840x2160 RGB, 8x8x8 bins, " + EXP_NOTE +
+                         ", windows 25/37/57/85/129, row bands",
                     kind="bands", gen=synth.config4, fmt=swg.FMT_RGB8, bins=8, nbins=512,
                     scaling="strong",
                     groups=[dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, bin_chunks=8,
@@ -111,7 +122,7 @@ def workload(name):
     return dict(name="config2: 1024x1024 u8, 32 bins, Gaussian (GaussianChebyshev sigma=0.5, "
                      "exact full-ring cake), windows 33/65/97",
                 kind="frame", gen=synth.config2, fmt=swg.FMT_GRAY8, bins=32, nbins=32,
-                scaling="weak", groups=[dict(planes=swg.PLANES_PLAIN, scales=scales)])
+                scaling="strong", groups=[dict(planes=swg.PLANES_PLAIN, scales=scales)])
 
 
 def engine_of(group, k, method):
@@ -147,6 +158,25 @@ def group_build_bytes(group, w, h, nbins):
     if any(engine_of(group, k, m)[0] == "k_sweep_cake" for k, m, _, _ in group["scales"]):
         b += cells * 4  # 32-bit plain planes for the large windows
     return b
+
+
+def est_request_ms(group, k, method, rings, rows, w, h, nbins):
+    """Rough sweep cost of map rows `rows` of one request (ms), for the
+    multi-GPU plan only (round-1 B200 measurements: table sweeps at ~3 TB/s
+    of algorithmic bytes, the cake at ~9.4e-9 ms per window-ring at 64 bins)."""
+    from paper_1705_03524_b200 import swg
+    mw = w - k.kw + 1
+    kname, P, e = engine_of(group, k, method)
+    tab = min(h + 1, rows + k.kh) * (w + 1) * nbins * P * e
+    if kname in ("k_sweep_cake16", "k_sweep_cake"):
+        return 0.05 + 9.4e-9 * rows * mw * rings * nbins / 64 * (2 if kname == "k_sweep_cake" else 1)
+    if method == swg.BRUTE:
+        return 0.05 + 1e-9 * rows * mw * k.kw * k.kh
+    return 0.05 + tab / 3.0e9
+
+
+def est_build_ms(group, w, h, nbins):
+    return 0.1 + group_build_bytes(group, w, h, nbins) / 3.0e9
 
 
 def target_center(scene, ti):
@@ -194,6 +224,12 @@ def band_plan(H, scales, n_bands):
             rows.append((v0, v1))
         bands.append((p0, rows))
     return BH, bands
+
+
+def config_dict(wl, job_win):
+    """The `config` both arms print (identical keys and values)."""
+    return {"workload": wl["name"], "bins": wl["nbins"], "windows_per_step": int(job_win),
+            "l2": L2_NOTE}
 
 
 # ------------------------------------------------------------------ clocks
@@ -364,7 +400,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5m"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c5m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -418,6 +454,7 @@ class OursArm:
             self.dist = dist
         self.weak = wl["scaling"] == "weak"
         self.data = wl["gen"](1 + self.rank if self.weak else 1)
+        self.plan = None
         self.ctx = swg.Context(self.local)
         # a non-default torch stream: our launches and the CUDA events share it
         self.stream = torch.cuda.Stream()
@@ -463,16 +500,40 @@ class OursArm:
                 for r in reqs]
 
     def _frame_units(self):
-        """c1 / c2 / c5: one table set per group over the whole frame."""
-        data = self.data
-        frame_dev = self.torch.from_numpy(data.image).cuda()
+        """c1 / c2 / c5: ONE frame; its (kernel, scale) requests partitioned
+        over the ranks (dist.plan_frame: LPT by estimated cost, the largest
+        split by map rows); a rank builds only the table sets its requests
+        read, over the whole frame (replicated build)."""
+        from paper_1705_03524_b200 import dist as D
+        swg, torch = self.swg, self.torch
+        data, groups = self.data, self.wl["groups"]
+        frame_dev = torch.from_numpy(data.image).cuda()
         H, W = data.image.shape[:2]
-        for gi, (g, ms) in enumerate(zip(self.wl["groups"], self.models)):
+        reqs_all = []
+        for gi, g in enumerate(groups):
+            for si, (k, meth, rings, _) in enumerate(g["scales"]):
+                mh = H - k.kh + 1
+                reqs_all.append(((gi, si), gi, mh,
+                                 est_request_ms(g, k, meth, rings, mh, W, H, self.nb)))
+        build = [est_build_ms(g, W, H, self.nb) for g in groups]
+        self.plan = D.plan_frame(reqs_all, build, self.world, min_rows=8)
+        mine = self.plan[self.rank]
+        for gi, (g, ms) in enumerate(zip(groups, self.models)):
+            work = [w for w in mine if w.group == gi]
+            if not work:
+                continue
             t = self.new_tables(g, frame_dev)
-            reqs = self._requests(g, ms)
-            self.units.append(dict(t=t, src=frame_dev, pitch=0, reqs=reqs,
-                                   maps=self._map_buffers(t, reqs), g=gi,
-                                   sidx=list(range(len(reqs))), h2d=data.image.nbytes))
+            reqs, maps = [], []
+            for w in work:
+                k, meth, rings, _ = g["scales"][w.key[1]]
+                mh = H - k.kh + 1
+                reqs.append(swg.MapRequest(k, ms[w.key[1]], meth, swg.BHATTACHARYYA, rings,
+                                           rows=None if w.rows == (0, mh) else w.rows))
+                maps.append(torch.empty((w.rows[1] - w.rows[0], W - k.kw + 1),
+                                        dtype=torch.float64, device="cuda"))
+            self.units.append(dict(t=t, src=frame_dev, pitch=0, reqs=reqs, maps=maps, g=gi,
+                                   sidx=[w.key[1] for w in work],
+                                   rows=[w.rows for w in work], h2d=data.image.nbytes))
         self.tab_w, self.tab_h = W, H
 
     def _sequence_units(self):
@@ -730,7 +791,7 @@ class OursArm:
         torch.cuda.synchronize()
         # the step as one CUDA graph (no host launch gaps between the kernels)
         graph = None
-        if not args.no_graph and not self.chained:  # (p2p chain: eager)
+        if not args.no_graph and not self.chained and self.units:  # (p2p chain: eager)
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=self.stream):
                 self.step()
@@ -791,17 +852,17 @@ class OursArm:
         return per_step, events, clk, launches
 
     def launch_times(self, events):
-        """Per-launch ms from the eager events: builds, and sweeps per (group, scale)."""
+        """Per-launch ms from the eager events: builds, and sweeps per
+        (unit, request index) -- one entry per timed step and bin range."""
         build_ms, sweep_ms = [], {}
         for e in events:
             j = 0
-            for u in self.units:
+            for ui, u in enumerate(self.units):
                 for _, creqs in u["chunks"]:
                     build_ms.append(e[j].elapsed_time(e[j + 1]))
                     j += 1
                     for i in range(len(creqs)):
-                        sweep_ms.setdefault((u["g"], u["sidx"][i]), []).append(
-                            e[j].elapsed_time(e[j + 1]))
+                        sweep_ms.setdefault((ui, i), []).append(e[j].elapsed_time(e[j + 1]))
                         j += 1
                     j += 1
         return build_ms, sweep_ms
@@ -810,17 +871,36 @@ class OursArm:
         """Spot check of the timed outputs: peaks on the planted targets."""
         wl, data = self.wl, self.data
         if wl["kind"] == "frame":
-            ok = True
+            # every rank's row-chunk peaks -> each request's frame peak
+            # (reference tie rule), then the planted targets
+            from paper_1705_03524_b200 import dist as D
+            parts, widths = [], {}
             for u in self.units:
                 pk = u["peaks"].cpu().numpy()
-                g = wl["groups"][u["g"]]
                 for i, si in enumerate(u["sidx"]):
-                    ti = g["scales"][si][3]
-                    if ti is None:
-                        continue
                     ints = pk[i, :2].view(np.int32)
-                    tx, ty = target_center(data, ti)
-                    ok &= abs(int(ints[2]) - tx) <= 1 and abs(int(ints[3]) - ty) <= 1
+                    mw = u["maps"][i].shape[1]
+                    key = (u["g"], si)
+                    parts.append((key, u["rows"][i], float(pk[i, 2]),
+                                  int(ints[1]) * mw + int(ints[0]) - u["rows"][i][0] * mw))
+            if self.dist:
+                every = [None] * self.world
+                self.dist.all_gather_object(every, parts)
+                parts = [p for e in every for p in e]
+            H, W = data.image.shape[:2]
+            for gi, g in enumerate(wl["groups"]):
+                for si, sc in enumerate(g["scales"]):
+                    widths[(gi, si)] = W - sc[0].kw + 1
+            best = D.combine_request_peaks(parts, widths)
+            self.frame_peaks = best
+            ok = len(best) == sum(len(g["scales"]) for g in wl["groups"])
+            for (gi, si), (_, idx) in best.items():
+                k, _, _, ti = wl["groups"][gi]["scales"][si]
+                if ti is None:
+                    continue
+                tx, ty = target_center(data, ti)
+                mw = widths[(gi, si)]
+                ok &= abs(idx % mw + k.hx - tx) <= 1 and abs(idx // mw + k.hy - ty) <= 1
             return bool(ok)
         if wl["kind"] == "sequence":
             hits = tot = 0
@@ -943,82 +1023,88 @@ class OursArm:
                     return tr
         return None
 
-    def sweep_roofline(self, sweep_ms, clk):
-        """The dominant sweep launch against HBM (SURVEY §8d bytes), plus its
-        on-chip side."""
-        swg, wl, nb = self.swg, self.wl, self.nb
-        hbm, src = peaks_json()
-        cells = (self.tab_w + 1) * (self.tab_h + 1) * nb
-        dom = max(sweep_ms, key=lambda key: sum(sweep_ms[key]) / len(sweep_ms[key]))
-        gi, si = dom
-        g = wl["groups"][gi]
-        k, meth = g["scales"][si][0], g["scales"][si][1]
-        kname, P, e = engine_of(g, k, meth)
-        dom_ms = sum(sweep_ms[dom]) / len(sweep_ms[dom])
-        win_launch = {}
-        for u in self.units:
-            for i, s_ in enumerate(u["sidx"]):
-                win_launch.setdefault((u["g"], s_), []).append(u["maps"][i].numel())
-        dom_win = sum(win_launch[dom]) / len(win_launch[dom])
-        launch_bins = next((u.get("bins_per_launch", nb) for u in self.units if u["g"] == gi), nb)
-        dom_bytes = (cells // nb) * launch_bins * P * e + 8 * dom_win
-        tr = self._traffic_entry(kname, k)
-        roofline = {"bound": "hbm", "achieved": dom_bytes / (dom_ms / 1e3) / 1e9,
-                    "peak": hbm, "unit": "GB/s", "traffic": tr["dram_bytes"] if tr else None,
-                    "peak_source": src,
-                    "kernel": f"{kname} at {k.kw}x{k.kh} (planes read once + 8 B/window = "
-                              f"{int(dom_bytes)} B per launch, {dom_ms:.4f} ms)"}
-        roofline["frac"] = roofline["achieved"] / hbm
-        # on-chip side of the same launch: the table records every window reads
-        # (corners x bins x entry bytes) against the L1 load bandwidth (148 SMs
-        # x 128 B/clk at the SM clock sampled during the run).  The cake's ring
-        # count is cut short per window by its nested-box early exit, so its
-        # corner bytes are not known up front: its L1 utilisation is the ncu
-        # figure in profiles/, not an estimate here.
-        corners = {"k_sweep_affine": 20 if k.kind != swg.UNIFORM else 4, "k_sweep_quad": 20,
-                   "k_sweep_exp": 16}.get(kname)
-        if corners:
-            onchip_bytes = corners * launch_bins * e * dom_win
-            sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
-            l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-            roofline["onchip"] = {"achieved": onchip_bytes / (dom_ms / 1e3) / 1e12,
-                                  "peak": l1_peak, "unit": "TB/s", "bytes": int(onchip_bytes),
-                                  "frac": onchip_bytes / (dom_ms / 1e3) / 1e12 / l1_peak,
-                                  "peak_source": "148 SMs x 128 B/clk L1 at the sampled SM clock"}
-        else:
-            roofline["onchip"] = {"note": "the wedding-cake sweep is bound by the L1 -> register "
-                                          "data path (ring corners, O(rings*bins) per window); "
-                                          "figures from the ncu capture of this launch"}
-            src_txt = os.path.join(ROOT, tr["source"]) if tr else None
-            if src_txt and os.path.exists(src_txt):
-                import re
-                txt = open(src_txt).read()
-                for key, pat in (
-                        ("l1tex_throughput_pct",
-                         r"l1tex__throughput\.avg\.pct_of_peak_sustained_active\s+([\d.]+)"),
-                        ("lsu_writeback_pct",
-                         r"l1tex__lsu_writeback_active\.avg\.pct_of_peak_sustained_elapsed\s+([\d.]+)"),
-                        ("lsu_writeback_bytes_per_s",
-                         r"derived__l1tex__lsu_writeback_bytes_mem_lgds\.sum\.per_second\s+([\d.]+)")):
-                    m = re.search(pat, txt)
-                    if m:
-                        roofline["onchip"][key] = float(m.group(1))
-                if "lsu_writeback_pct" in roofline["onchip"]:
-                    roofline["onchip"]["frac"] = roofline["onchip"]["lsu_writeback_pct"] / 100.0
-                roofline["onchip"]["source"] = os.path.relpath(src_txt, ROOT)
-        return roofline
-
-    def build_roofline(self, build_ms):
+    def kernel_table(self, build_ms, sweep_ms):
+        """Per kernel function: launches, ms and algorithmic bytes per step
+        (the table rows a launch's windows read, each once, + 8 B
+        per window; builds: input + every plane entry written once), and the
+        per-launch list.  The dominant kernel is the one with the largest
+        share of the step."""
+        swg, wl, steps = self.swg, self.wl, self.args.steps
         hbm, _ = peaks_json()
-        build_avg = sum(build_ms) / self.args.steps  # ms per step, all rebuilds
-        in_bytes = sum(u["h2d"] for u in self.units)
-        build_bytes = in_bytes + sum(group_build_bytes(self.wl["groups"][u["g"]], self.tab_w,
-                                                       self.tab_h, self.nb) for u in self.units)
-        roof = {"bound": "hbm", "achieved": build_bytes / (build_avg / 1e3) / 1e9, "peak": hbm,
-                "unit": "GB/s", "ms": build_avg, "bytes": build_bytes,
-                "kernel": "k_quantize + k_colsum + k_bandscan + k_build (per table set)"}
-        roof["frac"] = roof["achieved"] / hbm
-        return roof
+        kt = {}
+        W = self.tab_w
+        for (ui, i), ts in sweep_ms.items():
+            u = self.units[ui]
+            g = wl["groups"][u["g"]]
+            k, meth = g["scales"][u["sidx"][i]][:2]
+            kname, P, e = engine_of(g, k, meth)
+            bins = u.get("bins_per_launch", self.nb)
+            r = u["reqs"][i]
+            rows = r.rows[1] - r.rows[0] if r.rows else self.tab_h - k.kh + 1
+            mw = self.tab_w - k.kw + 1
+            win = rows * mw
+            byts = min(self.tab_h + 1, rows + k.kh) * (W + 1) * bins * P * e + 8 * win
+            ms = sum(ts) / len(ts)
+            ent = kt.setdefault(kname, {"launches_per_step": 0, "ms_per_step": 0.0,
+                                        "bytes_per_step": 0, "launches": []})
+            n = len(ts) // steps
+            ent["launches_per_step"] += n
+            ent["ms_per_step"] += ms * n
+            ent["bytes_per_step"] += byts * n
+            ent["launches"].append({"window": f"{k.kw}x{k.kh}", "rows": int(rows),
+                                    "bins": int(bins), "ms": ms, "bytes": int(byts),
+                                    "hbm_frac": byts / (ms / 1e3) / 1e9 / hbm})
+        if build_ms:
+            bms = sum(build_ms) / steps
+            in_bytes = sum(u["h2d"] for u in self.units)
+            bb = in_bytes + sum(group_build_bytes(wl["groups"][u["g"]], self.tab_w, self.tab_h,
+                                                  self.nb) for u in self.units)
+            kt["ih_build"] = {"launches_per_step": len(build_ms) // steps, "ms_per_step": bms,
+                              "bytes_per_step": int(bb), "launches": [],
+                              "kernels": "k_quantize + k_colsum + k_bandscan + k_build / "
+                                         "k_build_fused (+ decayed: k_flip, k_colsum_decay, "
+                                         "k_bandscan_decay, k_build_decay_strip)"}
+        for ent in kt.values():
+            ent["gbps"] = ent["bytes_per_step"] / (ent["ms_per_step"] / 1e3) / 1e9
+            ent["hbm_frac"] = ent["gbps"] / hbm
+        return kt
+
+    def sweep_roofline(self, kt, clk):
+        """`roofline` of the kernel with the largest share of the step: its
+        algorithmic bytes per launch / its average launch time (summed over
+        its launches in a step), against the measured HBM copy bandwidth."""
+        hbm, src = peaks_json()
+        dom = max(kt, key=lambda n: kt[n]["ms_per_step"])
+        ent = kt[dom]
+        step_ms = sum(e["ms_per_step"] for e in kt.values())
+        roofline = {"bound": "hbm", "achieved": ent["gbps"], "peak": hbm, "unit": "GB/s",
+                    "frac": ent["hbm_frac"], "traffic": None, "peak_source": src,
+                    "kernel": dom, "share_of_step": ent["ms_per_step"] / step_ms,
+                    "launches_per_step": ent["launches_per_step"],
+                    "bytes_per_step": ent["bytes_per_step"],
+                    "avg_launch_ms": ent["ms_per_step"] / max(ent["launches_per_step"], 1)}
+        # ncu DRAM bytes of one launch of this kernel (profiles/traffic.json,
+        # this config), next to that launch's algorithmic bytes
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            entries = json.load(open(tp)).get(self.args.config) or []
+            for tr in entries if isinstance(entries, list) else [entries]:
+                if not tr.get("kernel", "").startswith(dom):
+                    continue
+                for ln in ent["launches"]:
+                    if f" {ln['window']} " in " " + tr["kernel"].replace("at ", "") + " ":
+                        roofline["traffic"] = tr["dram_bytes"]
+                        roofline["traffic_launch"] = {"window": ln["window"],
+                                                      "algorithmic_bytes": ln["bytes"],
+                                                      "ncu_source": tr.get("source")}
+                        break
+                if roofline["traffic"] is not None:
+                    break
+        if dom.startswith("k_sweep_cake"):
+            roofline["onchip"] = {"note": "the wedding-cake sweep is bound by the L1 -> register "
+                                          "data path (ring corners, O(rings*bins) per window), "
+                                          "not HBM: see profiles/ for its L1 utilisation"}
+        return roofline
 
     def cpu_baseline(self):
         if self.world != 1 or self.args.no_cpu_baseline:
@@ -1046,33 +1132,37 @@ class OursArm:
             if self.dist:
                 self.dist.destroy_process_group()
             return
-        roofline = self.sweep_roofline(sweep_ms, clk)
-        build_roof = self.build_roofline(build_ms)
+        kt = self.kernel_table(build_ms, sweep_ms)
+        roofline = self.sweep_roofline(kt, clk)
         cpu = self.cpu_baseline()
         kinds = ["uniform", "manhattan", "chebyshev", "gauss_cheb", "euclid_quad", "exp_l1"]
         per_scale = {}
-        for gi, g in enumerate(wl["groups"]):
-            for s, sc in enumerate(g["scales"]):
-                ts = sweep_ms.get((gi, s))
-                per_scale[f"{kinds[sc[0].kind]}{sc[0].kw}x{sc[0].kh}"] = \
-                    sum(ts) / args.steps if ts else 0.0
+        for (ui, i), ts in sweep_ms.items():
+            u = self.units[ui]
+            sc = wl["groups"][u["g"]]["scales"][u["sidx"][i]]
+            key = f"{kinds[sc[0].kind]}{sc[0].kw}x{sc[0].kh}"
+            per_scale[key] = per_scale.get(key, 0.0) + sum(ts) / args.steps
+        ih = kt.get("ih_build")
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": self.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
             "dtype": "u16/u32 integral tables (f64 decay tables) + f64 scores",
             "data": "synthetic (seeded generators in paper_1705_03524_b200/synth.py)",
-            "config": {"workload": wl["name"], "bins": self.nb, "windows_per_step": int(job_win),
-                       "table_shape": [self.tab_w, self.tab_h], "units_per_rank": len(self.units),
-                       "l2": "flushed between timed steps (256 MiB write, untimed)",
-                       "parallelism": (f"bin ranges chained over {self.world} GPU(s) (p2p "
-                                       f"partial sums)" if self.chained else
-                                       f"{'frames' if self.weak else wl['kind']} sharded over "
-                                       f"{self.world} GPU(s), no collective")},
-            "ih_build": {"ms": build_roof["ms"], "gbps": build_roof["achieved"],
-                         "frac": build_roof["frac"]},
+            "config": config_dict(wl, job_win),
+            "parallelism": (f"bin ranges chained over {self.world} GPU(s) (p2p partial sums)"
+                            if self.chained else
+                            f"one frame's (kernel, scale) requests over {self.world} GPU(s) "
+                            f"(LPT, row-split; tables built per rank), no collective"
+                            if wl["kind"] == "frame" else
+                            f"{wl['kind']} sharded over {self.world} GPU(s), no collective"),
+            "tables": {"shape": [self.tab_w, self.tab_h], "units_rank0": len(self.units)},
+            "ih_build": ({"ms": ih["ms_per_step"], "gbps": ih["gbps"], "frac": ih["hbm_frac"],
+                          "bytes": ih["bytes_per_step"]} if ih else None),
             "per_scale_ms": per_scale,
-            "roofline": roofline, "build_roofline": build_roof,
+            "kernels": {n: {k: v for k, v in e.items() if k != "launches"} | (
+                {"launches": e["launches"]} if n != "ih_build" else {}) for n, e in kt.items()},
+            "roofline": roofline,
             "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches // args.steps,
             "peaks_on_targets": ok_peaks, "cpu_baseline": cpu, "clocks": clk,
         }
@@ -1133,7 +1223,7 @@ def run_reference(args, wl, rank, world):
         "warmup": args.warmup, "ms_per_step": n_win / value * 1e3, "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None, "dtype": "i64+f64", "impl": "reference",
         "data": "synthetic (same generator and seed as --impl ours)",
-        "config": {"workload": wl["name"], "bins": wl["nbins"], "windows_per_step": n_win},
+        "config": config_dict(wl, n_win),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": vals[0]["threads"],
                          "kind": vals[0]["kind"], "sample": "per step: " + cpu_sample_text(wl, vals[0])},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -102,6 +102,9 @@ class Oracle:
                                             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                             C.c_int, C.c_int, _f64]
         L.orc_peak.argtypes = [_f64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_Peak)]
+        L.orc_fast_map.argtypes = [_u16, C.c_int, C.c_int, C.c_int, _f64, K, C.c_int,
+                                   C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _f64,
+                                   C.POINTER(_Peak), C.POINTER(C.c_longlong)]
 
     @staticmethod
     def _check(st):
@@ -246,6 +249,22 @@ class Oracle:
                                              v1, out)
         self._check(st)
         return out
+
+    def fast_map(self, fi, bins, model, k, method=SWIH, sim=BHATTACHARYYA, rings=1,
+                 rule=RING_MEAN, threads=None, eps=1e-8):
+        """Full strict map computed bin-outer (swih_fastmap.c): bit-identical
+        to likelihood_map for the exact methods; for the exponential brute
+        force a tolerance map with every window within `eps` of its maximum
+        re-scored exactly.  Returns (map, peak tuple, re-scored count)."""
+        fi = np.ascontiguousarray(fi, np.uint16)
+        h, w = fi.shape
+        out = np.empty((h - k.kh + 1, w - k.kw + 1), np.float64)
+        p, n = _Peak(), C.c_longlong(0)
+        self._check(self.lib.orc_fast_map(fi, w, h, bins, np.ascontiguousarray(model, np.float64),
+                                          C.byref(k), method, sim, rings, rule,
+                                          threads or os.cpu_count(), eps, out, C.byref(p),
+                                          C.byref(n)))
+        return out, (p.map_x, p.map_y, p.center_x, p.center_y, p.score), n.value
 
     def peak(self, scores, hx, hy):
         scores = np.ascontiguousarray(scores, np.float64)

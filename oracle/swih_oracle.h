@@ -150,6 +150,20 @@ int orc_likelihood_map_mt(const uint16_t* fi, int w, int h, int b,
                           int sim, int rings, int rule, int v0, int v1,
                           int threads, double* scores);
 
+/* Full-size maps (swih_fastmap.c): the same per-window fp64 operation
+ * sequence as orc_likelihood_map, computed bin-outer on `threads` threads.
+ * method SWIH (Uniform, Manhattan), PLAIN, CAKE (any ring plan), BRUTE with
+ * Uniform / Manhattan / Euclidean-quadratic: bit-identical full maps.
+ * BRUTE with the exponential kernel: two phases -- a separable-filter map,
+ * then every window within eps of its maximum re-scored by orc_brute_weights
+ * in the reference's pixel order; `peak` is exact, n_exact = re-scored
+ * windows.  Full strict map: (w-kw+1)*(h-kh+1) scores. */
+#define SWIH_FM_MAX_RINGS 512
+int orc_fast_map(const uint16_t* fi, int w, int h, int b, const double* model,
+                 const orc_kernel* k, int method, int sim, int rings, int rule,
+                 int threads, double eps, double* scores, orc_peak_t* peak,
+                 long long* n_exact);
+
 #ifdef __cplusplus
 }
 #endif

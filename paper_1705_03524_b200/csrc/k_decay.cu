@@ -305,12 +305,10 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
   const unsigned grid = (unsigned)(a.nbands * pairs);
   const size_t smem = (size_t)(kStripRows * kStripW + a.band_h) * sizeof(double2);
   if (smem > (200 << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~8500 rows
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_build_decay_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 << 10);
-    attr = true;
-  }
+  // set on every launch: the attribute is per device (a process-wide cache
+  // would skip it on a second device and race between host threads)
+  cudaFuncSetAttribute(k_build_decay_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       200 << 10);
   k_build_decay_strip<<<grid, kStripW, smem, s>>>(a, dec, kind, pairs);
   *launches += 1;
   return cudaGetLastError();

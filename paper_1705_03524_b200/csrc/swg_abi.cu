@@ -448,7 +448,11 @@ swg_status weight_grid(swg_ctx* c, const swg_kernel& k, const double** out) {
   auto* g = new swg_ctx::Grid{k, integer, {}};
   swg_status st = g->buf.ensure(w.size() * 8);
   if (st == SWG_OK) {
-    cudaError_t e = cudaMemcpy(g->buf.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+    // ordered on the context stream and completed before any worker stream
+    // (forked later) can read it; once per kernel
+    cudaError_t e = cudaMemcpyAsync(g->buf.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice,
+                                    c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) st = fail(SWG_ERR_CUDA, "weight grid: %s", cudaGetErrorString(e));
   }
   if (st != SWG_OK) {
@@ -1690,7 +1694,10 @@ double* mapped_host(void* p, int device) {
     cudaGetLastError();
     return nullptr;
   }
-  return at.type == cudaMemoryTypeHost && at.device == device
+  // page-locked, device-mapped host memory is reachable from every device
+  // under unified addressing (the caller holds the context's device)
+  (void)device;
+  return at.type == cudaMemoryTypeHost && at.devicePointer
              ? static_cast<double*>(at.devicePointer)
              : nullptr;
 }

@@ -173,3 +173,76 @@ def run_bin_chain(rank: int, world: int, chunks: Sequence[Tuple[int, int]], comp
         else:
             results.append(out)
     return results
+
+
+# ---------------------------------------------------------------- one frame
+@dataclass(frozen=True)
+class Work:
+    """One sweep request of a frame, or a row chunk of it: (kernel, scale)
+    index `key` on table set `group`, map rows [v0, v1), estimated cost."""
+    key: Tuple[int, int]
+    group: int
+    rows: Tuple[int, int]
+    cost: float
+
+
+def _lpt(items: Sequence[Work], build: Sequence[float], world: int):
+    """Longest-processing-time assignment; a rank pays a table set's build
+    the first time it takes a request on it (the build is replicated on
+    every rank that sweeps it: a local rebuild at HBM speed beats shipping
+    the tables over NVLink)."""
+    load = [0.0] * world
+    sets: List[set] = [set() for _ in range(world)]
+    out: List[List[Work]] = [[] for _ in range(world)]
+    for it in sorted(items, key=lambda w: (-w.cost, w.key, w.rows)):
+        best, best_load = 0, None
+        for r in range(world):
+            l = load[r] + it.cost + (0.0 if it.group in sets[r] else build[it.group])
+            if best_load is None or l < best_load - 1e-12:
+                best, best_load = r, l
+        load[best] = best_load
+        sets[best].add(it.group)
+        out[best].append(it)
+    return out, load
+
+
+def plan_frame(requests: Sequence[Tuple[Tuple[int, int], int, int, float]],
+               build: Sequence[float], world: int, min_rows: int = 64,
+               max_splits: int = 256) -> List[List[Work]]:
+    """Partition ONE frame's (kernel, scale) requests over `world` ranks
+    (SURVEY §8e "Scales / kernels"): requests = (key, group, map rows, cost).
+    LPT over whole requests first; while the busiest rank's largest item can
+    be halved by map rows (>= 2 * min_rows) and halving shortens the
+    makespan, split it.  Deterministic, so every rank derives the same plan
+    with no communication; every (request, map row) lands on exactly one
+    rank.  Returns per-rank Work lists (requests in their original order)."""
+    items = [Work(k, g, (0, rows), c) for k, g, rows, c in requests if rows > 0]
+    plan, load = _lpt(items, build, world)
+    for _ in range(max_splits if world > 1 else 0):
+        top = max(range(world), key=lambda r: (load[r], -r))
+        big = max(plan[top], key=lambda w: (w.cost, w.rows[1] - w.rows[0]), default=None)
+        if big is None or big.rows[1] - big.rows[0] < 2 * min_rows:
+            break
+        mid = (big.rows[0] + big.rows[1]) // 2
+        trial = [w for w in items if w != big] + [
+            Work(big.key, big.group, (big.rows[0], mid), big.cost / 2),
+            Work(big.key, big.group, (mid, big.rows[1]), big.cost / 2)]
+        p2, l2 = _lpt(trial, build, world)
+        if max(l2) >= max(load) - 1e-12:
+            break
+        items, plan, load = trial, p2, l2
+    order = {k: i for i, (k, _, _, _) in enumerate(requests)}
+    return [sorted(p, key=lambda w: (order[w.key], w.rows)) for p in plan]
+
+
+def combine_request_peaks(parts: Sequence[Tuple[Tuple[int, int], Tuple[int, int], float, int]],
+                          map_widths) -> dict:
+    """Per request key: the global peak (score, row-major index) over the row
+    chunks the ranks swept.  parts: (key, rows, score, index within the
+    chunk's rows); map_widths[key] = map width.  Reference tie rule."""
+    best = {}
+    for key, (v0, _), s, i in parts:
+        gi = i + v0 * map_widths[key]
+        if key not in best or better((s, gi), best[key]):
+            best[key] = (s, gi)
+    return best
