@@ -429,13 +429,16 @@ class OursArm:
     walked in ranges), and for the rank-to-rank bin chain pin / pout (/ token).
     """
 
-    def __init__(self, args, wl):
+    def __init__(self, args, wl, rank=None, world=None):
+        """rank / world override the torchrun environment (tests: one rank's
+        share of the plan on one GPU, no process group)."""
         import torch
         from paper_1705_03524_b200 import swg
         self.torch, self.swg = torch, swg
         self.args, self.wl = args, wl
-        self.rank = int(os.environ.get("RANK", 0))
-        self.world = int(os.environ.get("WORLD_SIZE", 1))
+        injected = rank is not None
+        self.rank = int(os.environ.get("RANK", 0)) if rank is None else rank
+        self.world = int(os.environ.get("WORLD_SIZE", 1)) if world is None else world
         self.local = int(os.environ.get("LOCAL_RANK", 0))
         # SWG_BENCH_SHARE_GPU=1: test mode for the N>1 code path on a 1-GPU box
         # (every rank on cuda:0, gloo collectives; ranks never wait on each
@@ -445,7 +448,7 @@ class OursArm:
             self.local = 0
         torch.cuda.set_device(self.local)
         self.dist = None
-        if self.world > 1:
+        if self.world > 1 and not injected:
             import torch.distributed as dist
             if self.share:
                 dist.init_process_group("gloo")

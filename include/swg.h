@@ -279,6 +279,13 @@ swg_status swg_query_windows(swg_tables* t, int n, const int* cx, const int* cy,
 swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
                             const swg_kernel* kernel, int rings, int ring_rule,
                             int border, double* host_out);
+/* Declared exponential kernel (EXP_L1, sigma == the tables' decay) on
+ * decayed tables (swg_tables_build_decay): weighted window histograms at
+ * strict centres from the sweep's 16 corners per bin, out[n][bins] doubles
+ * (tolerance-exact: the brute force sums the same weights in pixel order,
+ * baselines.cpp:53-69). */
+swg_status swg_decay_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                             const swg_kernel* kernel, double* host_out);
 /* Ring plan of a wedding-cake configuration: per ring the box half extents
  * and the ring weight (WeddingCakePlan::shrink_x/shrink_y/ring_weight). */
 swg_status swg_cake_plan(const swg_kernel* kernel, int rings, int ring_rule,

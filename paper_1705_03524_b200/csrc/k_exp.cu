@@ -242,7 +242,39 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
 }
 
 
+// Exponential window histograms at explicit centres (swg_decay_windows):
+// per (window, bin) the 16 corners of the sweep, summed per orientation in
+// the sweep's order, the same snap of empty-bin noise.
+__global__ void k_exp_query(const double* tab, size_t ps, size_t pitch, int bins,
+                            const ExpSweep e, int n, const int* wcx, const int* wcy,
+                            double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (b >= bins || i >= n) return;
+  const int cx = wcx[i], cy = wcy[i];
+  const char* base = reinterpret_cast<const char*>(tab) + (size_t)(b >> 1) * 4 * ps * 16 +
+                     (b & 1) * 8;
+  double o = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const size_t x = (k & 1) ? (size_t)(e.w - 1 - cx) : (size_t)cx;
+    const size_t y = (k & 2) ? (size_t)(e.h - 1 - cy) : (size_t)cy;
+    const char* w = base + (k * ps + y * pitch + x) * 16;
+    auto at = [&](int q) { return *reinterpret_cast<const double*>(w + e.off[4 * k + q]); };
+    o += e.coef[4 * k] * at(0) + e.coef[4 * k + 1] * at(1) + e.coef[4 * k + 2] * at(2) +
+         e.coef[4 * k + 3] * at(3);
+  }
+  out[(size_t)i * bins + b] = o > e.snap ? o : 0.0;
+}
+
 }  // namespace
+
+cudaError_t launch_exp_query(const double* tab, size_t ps, size_t pitch, int bins,
+                             const ExpSweep& e, int n, const int* cx, const int* cy,
+                             double* out, cudaStream_t s) {
+  dim3 grid((unsigned)((bins + 127) / 128), (unsigned)n);
+  k_exp_query<<<grid, 128, 0, s>>>(tab, ps, pitch, bins, e, n, cx, cy, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_exp<0><<<grid, kExpThreads, 0, s>>>(a, e);

@@ -2019,4 +2019,37 @@ swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* 
   return SWG_OK;
 }
 
+swg_status swg_decay_windows(swg_tables* t, int n, const int* cx, const int* cy,
+                             const swg_kernel* k, double* out) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || !k || (n && (!cx || !cy || !out))) return fail(SWG_ERR_ARG, "bad query arguments");
+  ST_TRY(validate_kernel(*k));
+  if (!t->tdec || k->kind != SWG_KERNEL_EXP_L1 || k->sigma != t->decay)
+    return fail(SWG_ERR_UNSUPPORTED_KERNEL,
+                "decay windows: exponential kernel with the tables' decay on decayed tables");
+  for (int i = 0; i < n; ++i)
+    ST_TRY(validate_window(t->w, t->h, cx[i], cy[i], *k, SWG_BORDER_STRICT));
+  if (n == 0) return SWG_OK;
+  swg_map_request r{};
+  r.sim = SWG_SIM_BHATTACHARYYA;
+  static thread_local ExpSweep es;
+  exp_plan(t, r, k_hx(*k), k_hy(*k), es);
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  swg_ctx* c = t->ctx;
+  const size_t cb = round_up((size_t)n * 4, 256), ob = (size_t)n * t->bins * 8;
+  ST_TRY(c->terms.ensure(2 * cb));
+  ST_TRY(c->qout.ensure(ob));
+  int* dcx = static_cast<int*>(c->terms.p);
+  int* dcy = reinterpret_cast<int*>(static_cast<char*>(c->terms.p) + cb);
+  CUDA_TRY(cudaMemcpyAsync(dcx, cx, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dcy, cy, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_exp_query(t->tdec, t->ps, t->pitch, t->bins, es, n, dcx, dcy,
+                            static_cast<double*>(c->qout.p), c->stream));
+  c->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(out, c->qout.p, ob, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
 }  // extern "C"

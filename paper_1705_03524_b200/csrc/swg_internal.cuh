@@ -339,6 +339,9 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
 cudaError_t launch_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
                                 int kind, int b0, int b1, double* out, cudaStream_t s);
 cudaError_t launch_sweep_exp(const SweepArgs& a, const ExpSweep& e, dim3 grid, cudaStream_t s);
+cudaError_t launch_exp_query(const double* tab, size_t ps, size_t pitch, int bins,
+                             const ExpSweep& e, int n, const int* cx, const int* cy,
+                             double* out, cudaStream_t s);
 cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak* peak,
                               cudaStream_t s);
 cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,

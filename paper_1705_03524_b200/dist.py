@@ -206,6 +206,13 @@ def _lpt(items: Sequence[Work], build: Sequence[float], world: int):
     return out, load
 
 
+def _objective(load):
+    """Makespan, then how many ranks share it (a split that only removes one
+    of several equally busiest ranks is progress)."""
+    top = max(load)
+    return (round(top, 9), sum(1 for l in load if l >= top - 1e-9))
+
+
 def plan_frame(requests: Sequence[Tuple[Tuple[int, int], int, int, float]],
                build: Sequence[float], world: int, min_rows: int = 64,
                max_splits: int = 256) -> List[List[Work]]:
@@ -213,7 +220,7 @@ def plan_frame(requests: Sequence[Tuple[Tuple[int, int], int, int, float]],
     (SURVEY §8e "Scales / kernels"): requests = (key, group, map rows, cost).
     LPT over whole requests first; while the busiest rank's largest item can
     be halved by map rows (>= 2 * min_rows) and halving shortens the
-    makespan, split it.  Deterministic, so every rank derives the same plan
+    makespan (or leaves fewer ranks at it), split it.  Deterministic, so every rank derives the same plan
     with no communication; every (request, map row) lands on exactly one
     rank.  Returns per-rank Work lists (requests in their original order)."""
     items = [Work(k, g, (0, rows), c) for k, g, rows, c in requests if rows > 0]
@@ -228,7 +235,7 @@ def plan_frame(requests: Sequence[Tuple[Tuple[int, int], int, int, float]],
             Work(big.key, big.group, (big.rows[0], mid), big.cost / 2),
             Work(big.key, big.group, (mid, big.rows[1]), big.cost / 2)]
         p2, l2 = _lpt(trial, build, world)
-        if max(l2) >= max(load) - 1e-12:
+        if _objective(l2) >= _objective(load):
             break
         items, plan, load = trial, p2, l2
     order = {k: i for i, (k, _, _, _) in enumerate(requests)}

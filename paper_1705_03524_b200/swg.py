@@ -171,6 +171,7 @@ def lib():
                                      C.POINTER(C.c_size_t), C.POINTER(C.c_int)],
         "swg_query_terms": [vp, C.c_int, C.c_int, vp, vp],
         "swg_query_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), C.c_int, C.c_int, vp],
+        "swg_decay_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), vp],
         "swg_cake_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), C.c_int, C.c_int, C.c_int,
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
@@ -430,6 +431,15 @@ class Tables:
         out = np.empty((len(cx), self.bins), np.int64)
         _check(lib().swg_query_windows(self._h, len(cx), _ptr(cx), _ptr(cy), C.byref(kernel),
                                        method, border, _ptr(out)))
+        return out
+
+    def decay_windows(self, cx, cy, kernel: Kernel):
+        """Exponential-kernel window histograms (strict) from decayed tables."""
+        cx = np.ascontiguousarray(np.atleast_1d(cx), np.int32)
+        cy = np.ascontiguousarray(np.atleast_1d(cy), np.int32)
+        out = np.empty((len(cx), self.bins), np.float64)
+        _check(lib().swg_decay_windows(self._h, len(cx), _ptr(cx), _ptr(cy), C.byref(kernel),
+                                       _ptr(out)))
         return out
 
     def cake_windows(self, cx, cy, kernel: Kernel, rings, rule=RING_MEAN, border=STRICT):

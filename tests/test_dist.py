@@ -162,3 +162,101 @@ def test_bin_range_geometry():
     assert D.bin_ranges(20, 2) == [(0, 16), (16, 20)]
     assert D.bin_ranges(8, 3) == [(0, 8), (8, 8), (8, 8)]
     assert D.row_chunks(10, 3) == [(0, 4), (4, 8), (8, 10)]
+
+
+def _plan_worker(rank, world, port, q):
+    """One frame's (kernel, scale) requests over ranks (config 2 / 5 on N
+    GPUs, dist.plan_frame): each rank sweeps only its Work items -- row
+    chunks of the maps, on the table sets it builds -- and the ranks gather
+    the chunk peaks.  The oracle stands in for the rank's GPU sweeps; the
+    stitched maps and combined peaks must equal the single-rank result."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        orc = O.Oracle()
+        img = orc.random_gray(70, 64, 9)
+        bins = 8
+        fi = orc.quantize_gray8(img, bins)
+        h, w = fi.shape
+        kernels = [(0, O.kernel(O.MANHATTAN, 9, 9), O.SWIH, 1),
+                   (0, O.kernel(O.MANHATTAN, 21, 15), O.SWIH, 1),
+                   (1, O.kernel(O.GAUSS_CHEB, 13, 13), O.CAKE, 7),
+                   (1, O.kernel(O.GAUSS_CHEB, 31, 31), O.CAKE, 16)]
+        models = [orc.target_model(np.ascontiguousarray(fi[5:5 + k.kh, 7:7 + k.kw]), bins, k,
+                                   m, r) for _, k, m, r in kernels]
+        reqs = [((g, i), g, h - k.kh + 1, float((h - k.kh + 1) * r * (1 + g)))
+                for i, (g, k, m, r) in enumerate(kernels)]
+        plan = D.plan_frame(reqs, [3.0, 1.0], world, min_rows=4)
+        parts, maps = [], {}
+        for wk in plan[rank]:
+            g, k, m, r = kernels[wk.key[1]]
+            v0, v1 = wk.rows
+            # the window rows [v0, v1) from the pixel rows they touch
+            part = orc.likelihood_map(np.ascontiguousarray(fi[v0:v1 + k.kh - 1]), bins,
+                                      models[wk.key[1]], k, m, rings=r)
+            u, v, _, _, s = orc.peak(part, k.kw // 2, k.kh // 2)
+            parts.append((wk.key, (v0, v1), s, v * part.shape[1] + u))
+            maps[(wk.key, wk.rows)] = part
+        every = [None] * world
+        dist.all_gather_object(every, (parts, maps))
+        allparts = [p for e, _ in every for p in e]
+        widths = {(g, i): w - k.kw + 1 for i, (g, k, _, _) in enumerate(kernels)}
+        best = D.combine_request_peaks(allparts, widths)
+        ok = True
+        for i, (g, k, m, r) in enumerate(kernels):
+            full = orc.likelihood_map(fi, bins, models[i], k, m, rings=r)
+            st = np.full_like(full, np.nan)
+            for _, mp_ in every:
+                for (key, (v0, v1)), part in mp_.items():
+                    if key == (g, i):
+                        st[v0:v1] = part
+            pk = orc.peak(full, k.kw // 2, k.kh // 2)
+            ok &= bool((st == full).all())
+            ok &= best[(g, i)] == (pk[4], pk[1] * full.shape[1] + pk[0])
+        covered = sorted((wk.key, wk.rows) for p in plan for wk in p)
+        q.put((rank, ok, len(plan[rank]), covered))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_one_frame_plan_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(r[1] for r in res), res
+    assert all(r[2] >= 1 for r in res)  # both ranks have work
+
+
+def test_plan_frame_geometry():
+    """Every (request, map row) on exactly one rank; LPT balance; ranks pay
+    only the builds of the table sets they sweep; deterministic."""
+    reqs = [((g, s), g, 2048 - 16 * s, 1.0 + 0.4 * s + 0.5 * g) for g in range(4)
+            for s in range(8)]
+    build = [1.0, 0.3, 1.6, 2.5]
+    for world in (1, 2, 3, 4, 8):
+        plan = D.plan_frame(reqs, build, world)
+        assert plan == D.plan_frame(reqs, build, world)
+        rows = {}
+        for p in plan:
+            for wk in p:
+                rows.setdefault(wk.key, []).append(wk.rows)
+        for key, g, mh, _ in reqs:
+            rs = sorted(rows[key])
+            assert rs[0][0] == 0 and rs[-1][1] == mh
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        loads = [sum(wk.cost for wk in p) + sum(build[g] for g in {wk.group for wk in p})
+                 for p in plan]
+        total = sum(c for *_, c in reqs)
+        assert max(loads) <= (total + sum(build)) / world * 1.35 + 0.6
+    one = D.plan_frame([((0, 0), 0, 100, 5.0)], [0.1], 4, min_rows=8)
+    assert sum(len(p) for p in one) == 4  # a single request splits by rows

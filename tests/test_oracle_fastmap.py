@@ -92,3 +92,15 @@ def test_fast_map_errors():
     with pytest.raises(O.OracleError) as e:
         orc.fast_map(fi, 4, m, O.kernel(O.MANHATTAN, 21, 5), O.SWIH)
     assert e.value.code == 11  # SizeError
+
+
+def test_numpy_prefix_tables_equal_oracle_build():
+    """The numpy table form the full-size GPU table tests use
+    (test_gpu_fullsize._prefix_u32) equals the oracle build (pinned to the
+    reference's IntegralTableSet::build) for plain / xramp / yramp."""
+    from test_gpu_fullsize import _prefix_u32
+    fi = _scene(37, 29, 6, 2)
+    p, x, y = orc.build_tables(fi, 6)
+    for b in range(6):
+        want = _prefix_u32(fi, b, planes=3)
+        assert (want[0] == p[b]).all() and (want[1] == x[b]).all() and (want[2] == y[b]).all()
