@@ -56,6 +56,10 @@ def build(ref: bool = True) -> None:
     targets = ["all"]
     if ref and os.path.isdir("/root/reference/proj/src"):
         targets.append("ref")
+        # the reference's own unit tests against libswih_b200.so (built first)
+        if os.path.exists(os.path.join(HERE, "..", "paper_1705_03524_b200", "lib",
+                                       "libswih_b200.so")):
+            targets.append("reftests")
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
@@ -303,6 +307,13 @@ class Ref:
         L.ref_directional.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_int64)]
         L.ref_tables_save.argtypes = [vp, C.c_char_p]
+        L.ref_tables_load.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_write_map_files.argtypes = [_f64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                          C.c_char_p]
+        L.ref_write_bench_csv.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_double, C.c_double, C.c_double,
+                                          C.c_char_p]
         L.ref_swih_query.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.c_double, C.c_int, _i64]
         L.ref_plain_query.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i64]
@@ -414,6 +425,35 @@ class Ref:
             k.kind, k.kw, k.kh, k.sigma, method, sim, rings, rule, threads, budget,
             out.ctypes.data_as(C.c_void_p) if out is not None else None, pk, C.byref(ps)))
         return out, (int(pk[0]), int(pk[1]), int(pk[2]), int(pk[3]), ps.value)
+
+    def load_tables(self, path):
+        """IntegralTableSet::load_file -> (w, h, bins, plain, xramp, yramp) int64."""
+        h_, w, hh, b = C.c_void_p(), C.c_int(), C.c_int(), C.c_int()
+        self._check(self.lib.ref_tables_load(path.encode(), C.byref(h_), C.byref(w),
+                                             C.byref(hh), C.byref(b)))
+        try:
+            out = []
+            for kind in range(3):
+                a = np.empty((b.value, hh.value + 1, w.value + 1), np.int64)
+                self._check(self.lib.ref_tables_export(h_, kind, a))
+                out.append(a)
+        finally:
+            self.lib.ref_tables_free(h_)
+        return (w.value, hh.value, b.value, *out)
+
+    def write_map_files(self, scores, hx, hy, csv_path=None, pgm_path=None):
+        """write_map_csv_file / write_pgm_file(map_to_gray) of a map."""
+        scores = np.ascontiguousarray(scores, np.float64)
+        self._check(self.lib.ref_write_map_files(
+            scores, scores.shape[1], scores.shape[0], hx, hy,
+            csv_path.encode() if csv_path else None, pgm_path.encode() if pgm_path else None))
+
+    def write_bench_csv(self, rec, path):
+        """write_bench_csv_header + write_bench_csv_row of one record."""
+        self._check(self.lib.ref_write_bench_csv(
+            rec["method"].encode(), rec["width"], rec["height"], rec["kw"], rec["kh"],
+            rec["bins"], rec["build_ms"], rec["query_total_ms"], rec["query_mean_us"],
+            path.encode()))
 
     def peak(self, scores, hx, hy):
         scores = np.ascontiguousarray(scores, np.float64)

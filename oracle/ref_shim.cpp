@@ -23,6 +23,7 @@
 #include "swih/engine.hpp"
 #include "swih/integral_tables.hpp"
 #include "swih/matching.hpp"
+#include "swih/pgm.hpp"
 
 using namespace swih;
 
@@ -204,6 +205,51 @@ int ref_directional(void* tv, int dir, int x, int y, int bin,
 
 int ref_tables_save(void* tv, const char* path) {
   return guarded([&] { static_cast<Tables*>(tv)->t.save_file(path); });
+}
+
+// IntegralTableSet::load_file (integral_tables.cpp:186-206) of a dump.
+int ref_tables_load(const char* path, void** out, int* w, int* h, int* b) {
+  return guarded([&] {
+    IntegralTableSet t = IntegralTableSet::load_file(path);
+    *w = t.width();
+    *h = t.height();
+    *b = t.bins();
+    *out = new Tables{FeatureImage(1, 1, 1), std::move(t)};
+  });
+}
+
+// Harness outputs (matching.cpp:225-252, pgm.cpp, bench.cpp:132-143).
+int ref_write_map_files(const double* scores, int mw, int mh, int hx, int hy,
+                        const char* csv_path, const char* pgm_path) {
+  return guarded([&] {
+    LikelihoodMap map;
+    map.width = mw;
+    map.height = mh;
+    map.hx = hx;
+    map.hy = hy;
+    map.scores.assign(scores, scores + std::size_t(mw) * mh);
+    if (csv_path) write_map_csv_file(map, csv_path);
+    if (pgm_path) write_pgm_file(map_to_gray(map), pgm_path);
+  });
+}
+
+int ref_write_bench_csv(const char* method, int w, int h, int kw, int kh, int bins,
+                        double build_ms, double total_ms, double mean_us, const char* path) {
+  return guarded([&] {
+    BenchRecord r;
+    r.method = method;
+    r.width = w;
+    r.height = h;
+    r.kw = kw;
+    r.kh = kh;
+    r.bins = bins;
+    r.build_ms = build_ms;
+    r.query_total_ms = total_ms;
+    r.query_mean_us = mean_us;
+    std::ofstream out(path, std::ios::binary);
+    write_bench_csv_header(out);
+    write_bench_csv_row(r, out);
+  });
 }
 
 int ref_swih_query(void* tv, int cx, int cy, int kind, int kw, int kh,

@@ -40,7 +40,7 @@ def _stale(target, deps):
 
 
 CPP_DIR = os.path.join(PKG, "cpp")
-CPP_SOURCES = ["core.cpp", "tables.cpp", "engine.cpp", "matching.cpp"]
+CPP_SOURCES = ["core.cpp", "tables.cpp", "engine.cpp", "matching.cpp", "pgm.cpp", "bench.cpp"]
 CPP_LIB = os.path.join(LIBDIR, "libswih_b200.so")
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra",
@@ -75,6 +75,11 @@ def build_cpp_tests(verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    tool = os.path.join(tdir, "build", "io_tool")
+    if _stale(tool, [os.path.join(tdir, "io_tool.cpp"), CPP_LIB]):
+        subprocess.run([CXX, *CXX_FLAGS, os.path.join(tdir, "io_tool.cpp"), "-o", tool,
+                        "-L" + LIBDIR, "-lswih_b200", "-lswg", "-Wl,-rpath," + LIBDIR,
+                        "-lpthread"], check=True)
     return out
 
 
