@@ -80,16 +80,20 @@ def workload(name):
                                  scales=[(K(swg.MANHATTAN, 33, 33), swg.SWIH, 1, 0)])])
     if name in ("c5", "c5m"):
         ks = (17, 25, 37, 53, 79, 117, 173, 257)
-        groups = [dict(planes=swg.PLANES_AFFINE,
-                       scales=[(K(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks])]
+        manhattan = [(K(swg.MANHATTAN, k, k), swg.SWIH, 1, None) for k in ks]
+        groups = [dict(planes=swg.PLANES_AFFINE, scales=manhattan)]
         label = "Manhattan"
         if name == "c5":
-            groups += [
+            # one integral-table set per weight-plane family: the quadratic
+            # set's planes {1, x, y, x^2, y^2} include Manhattan's {1, x, y},
+            # so the Manhattan and Euclidean scales share one build
+            groups = [
+                dict(planes=swg.PLANES_QUADRATIC,
+                     scales=manhattan + [(K(swg.EUCLID_QUAD, k, k), swg.SWIH, 1, None)
+                                         for k in ks]),
                 dict(planes=swg.PLANES_PLAIN,
                      scales=[(K(swg.GAUSS_CHEB, k, k, 0.5), swg.CAKE, k // 2 + 1, None)
                              for k in ks]),
-                dict(planes=swg.PLANES_QUADRATIC,
-                     scales=[(K(swg.EUCLID_QUAD, k, k), swg.SWIH, 1, None) for k in ks]),
                 dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY,
                      scales=[(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None) for k in ks]),
             ]
@@ -132,6 +136,8 @@ def engine_of(group, k, method):
     if group["planes"] == swg.PLANES_DECAY:
         return "k_sweep_exp", 4, 8
     if group["planes"] == swg.PLANES_QUADRATIC:
+        if k.kind == swg.MANHATTAN:  # planes {1, x, y} of the quadratic set
+            return "k_sweep_affine", 3, 4
         return "k_sweep_quad", 5, 4
     if method == swg.CAKE or k.kind == swg.UNIFORM:
         small = k.kw * k.kh < 65536

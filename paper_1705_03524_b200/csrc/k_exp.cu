@@ -45,12 +45,7 @@ __global__ void __launch_bounds__(kExpThreads, SWG_EXP_MINB) k_sweep_exp(const S
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int tx, ty;
   if (a.chain_s > 0) {  // (kExpTileY == 1: a tile row is a map row)
-    int rem = blockIdx.x;
-    const int dv = rem % a.chain_k;
-    rem /= a.chain_k;
-    const int j = rem % a.chain_j, res = blockIdx.y * a.chain_k + dv;
-    tx = rem / a.chain_j;
-    ty = res < a.chain_s ? j * a.chain_s + res : a.rows;  // a.rows: no row (inactive)
+    ty = chain_row(a, tx);
   } else {
     sweep_tile(a.sc_tiles, tx, ty);
   }

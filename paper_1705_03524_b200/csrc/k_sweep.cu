@@ -82,10 +82,15 @@ __device__ __forceinline__ void add_octet(const double (&val)[4], const double (
 template <int SIM, bool UNIFORM>
 __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  int tx, ty;
-  sweep_tile(a.sc_tiles, tx, ty);
-  const int u0 = tx * kSweepTileX + (lane >> 1);
-  const int r0 = ty * kSweepTileY + warp;
+  int tx, ty, u0, r0;
+  if (a.chain_s > 0) {  // chain order: the CTA's warps side by side on one map row
+    r0 = chain_row(a, tx);
+    u0 = tx * (kSweepThreads / 2) + warp * kSweepTileX + (lane >> 1);
+  } else {
+    sweep_tile(a.sc_tiles, tx, ty);
+    u0 = tx * kSweepTileX + (lane >> 1);
+    r0 = ty * kSweepTileY + warp;
+  }
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -164,11 +169,13 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
 // their true values are <= N*hx^2, N*hy^2 < 2^32 (host-checked), hence
 // exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
 // exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
+// ty < 0: chain order, map row -ty - 1 with the CTA's warps side by side.
 template <int SIM>
 __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, PeakPart* part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
-  const int u0 = tx * kSweepTileX + (lane >> 1);
-  const int r0 = ty * kQuadTileY + warp;
+  const int u0 = ty < 0 ? tx * (kQuadThreads / 2) + warp * kSweepTileX + (lane >> 1)
+                        : tx * kSweepTileX + (lane >> 1);
+  const int r0 = ty < 0 ? -ty - 1 : ty * kQuadTileY + warp;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;
@@ -226,7 +233,8 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
 template <int SIM>
 __global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(const SweepArgs a) {
   int tx, ty;
-  sweep_tile(a.sc_tiles, tx, ty);
+  if (a.chain_s > 0) ty = -chain_row(a, tx) - 1;
+  else sweep_tile(a.sc_tiles, tx, ty);
   quad_body<SIM>(a, tx, ty, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 

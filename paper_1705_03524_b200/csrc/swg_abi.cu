@@ -1334,7 +1334,7 @@ enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
 
 struct MapPlan {
   int row0 = 0, rows = 0, mw = 0;  // map rows [row0, row0 + rows) of width mw
-  int chain_s = 0, chain_k = 0, chain_j = 0;  // exponential chain order (0: off)
+  int chain_s = 0, chain_k = 0, chain_j = 0;  // chain order (0: off; SweepArgs)
   Engine engine = kAffine32;
   swg_kernel k{};  // the kernel the engine sweeps (Plain maps: Uniform)
   dim3 grid;
@@ -1455,7 +1455,7 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
     method = SWG_METHOD_SWIH;
   }
   if (method == SWG_METHOD_BRUTE && !t->tdec && (k.kind == SWG_KERNEL_UNIFORM ||
-                                     (k.kind == SWG_KERNEL_MANHATTAN && t->planes == 3)))
+                                     (k.kind == SWG_KERNEL_MANHATTAN && t->planes >= 3)))
     method = SWG_METHOD_SWIH;
   const bool small = (long long)k.kw * k.kh < 65536;  // every box count < 2^16
   Engine e;
@@ -1476,6 +1476,36 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
   p.engine = e;
   p.k = k;
   p.grid = sweep_grid(e, p.mw, p.rows);
+  // Chain order for the affine and quadratic sweeps (SWG_CHAIN_AFFINE /
+  // SWG_CHAIN_QUAD: 0 off, 1 on, unset auto): window row v reads table rows
+  // {v, v+hy+1, v+2hy+1} (affine) or {v, v+2hy+1} (quadratic), so chains of
+  // step hy+1 (affine, residue groups of 8 so v+2hy+1 -- the lower row of
+  // residue r-1's chain -- is close too) or 2hy+1 (quadratic) read each table
+  // row once while it is in L2.
+  if ((e == kAffine32 && k.kind != SWG_KERNEL_UNIFORM) || e == kQuad) {
+    const bool aff = e == kAffine32;
+    const char* env = std::getenv(aff ? "SWG_CHAIN_AFFINE" : "SWG_CHAIN_QUAD");
+    const int hy = k_hy(k);
+    const double cell = (double)t->groups * kOct * (aff ? 3 : 5) * 4;
+    // measured on config 5 (A/B per scale, profiles/ab_sweep.py): the
+    // affine sweep gains from 37^2 up (footprint > the 64 MB budget), the
+    // quadratic one at every scale from 17^2 (footprint 58 MB): budgets 64 / 32 MB
+    // (chain order also beats super-columns wherever those apply)
+    bool on = (2.0 * hy + 2 + (aff ? kSweepTileY : kQuadTileY)) * (t->w + 1) * cell >
+              (aff ? 1.0 : 0.5) * SWG_L2_BUDGET_MB * 1048576.0;
+    if (env) on = std::atoi(env) != 0;
+    if (on) {
+      const int ck = std::getenv("SWG_CHAIN_K") ? std::atoi(std::getenv("SWG_CHAIN_K"))
+                                                 : (aff ? 4 : 1);
+      p.chain_s = aff ? hy + 1 : 2 * hy + 1;
+      p.chain_k = std::max(1, std::min(ck, p.chain_s));
+      p.chain_j = (p.rows + p.chain_s - 1) / p.chain_s;
+      const int tw = aff ? kSweepThreads / 2 : kQuadThreads / 2;
+      const unsigned gx = (unsigned)((p.mw + tw - 1) / tw);
+      p.grid = dim3(gx * (unsigned)(p.chain_k * p.chain_j),
+                    (unsigned)((p.chain_s + p.chain_k - 1) / p.chain_k));
+    }
+  }
   if (e == kExp64 && kExpTileY == 1) {
     // Chain order when a window's corner rows (2hy+2 table rows apart) do not
     // stay in L2 under raster order and super-columns would be too narrow:
@@ -1486,10 +1516,13 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
     // scales -13 to -17 %; where super-columns apply they stay faster).
     const double cell = (double)t->groups * kOct * 4 * 8;
     const int hy = k_hy(k);
-    if ((2.0 * hy + 3) * (t->w + 1) * cell > (double)SWG_L2_BUDGET_MB * 1048576.0 &&
-        super_column_tiles(t, e, k, k_hx(k), hy) == 0) {
+    bool on = (2.0 * hy + 3) * (t->w + 1) * cell > (double)SWG_L2_BUDGET_MB * 1048576.0 &&
+              super_column_tiles(t, e, k, k_hx(k), hy) == 0;
+    if (const char* env = std::getenv("SWG_CHAIN_EXP")) on = std::atoi(env) != 0;
+    if (on) {
+      const char* ek = std::getenv("SWG_CHAIN_KE");
       p.chain_s = hy + 1;
-      p.chain_k = std::min(4, p.chain_s);
+      p.chain_k = std::min(ek ? std::max(1, std::atoi(ek)) : 4, p.chain_s);
       p.chain_j = (p.rows + p.chain_s - 1) / p.chain_s;
       const unsigned gx = (unsigned)((p.mw + kExpTileX - 1) / kExpTileX);
       p.grid = dim3(gx * (unsigned)(p.chain_k * p.chain_j),
@@ -1836,7 +1869,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti;
   for (int i = 0; i < n && fused; ++i)
     fused = plan[i].engine == kQuad && plan[i].rows > 0 && !reqs[i].partial_in &&
-            !reqs[i].partial_out && !copy_map(i) &&
+            !reqs[i].partial_out && !copy_map(i) && plan[i].chain_s == 0 &&
             super_column_tiles(t, kQuad, plan[i].k, k_hx(plan[i].k), k_hy(plan[i].k)) == 0;
   if (fused) ST_TRY(run_quad_multi(c, t, n, reqs, plan, out.data(), parts0, dpeaks));
   // Device-output fan-out issues the costliest sweeps first (longest-first

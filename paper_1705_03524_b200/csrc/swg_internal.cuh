@@ -269,6 +269,24 @@ __device__ __forceinline__ void sweep_tile(int sc_tiles, int& tx, int& ty) {
   tx = x0 + (rem - ty * wsc);
 }
 
+// Chain order (SweepArgs::chain_*): CTA (blockIdx.x = (tile column tx,
+// chain step j, residue offset dv), blockIdx.y = residue group q) sweeps map
+// row j * chain_s + q * chain_k + dv, so the CTAs in flight cover, for a
+// few tile columns, every chain_s-th map row of the whole height: the table
+// rows a window row reads as its lower corners are the rows the window row
+// chain_s below reads as its upper corners, and both reads happen while the
+// row is in L2 (the raster order's reuse distance of 2hy+1 map rows at full
+// width does not fit in L2 at large windows).  Returns the map row, or
+// a.rows (no row) for the padding residues of the last group.
+__device__ __forceinline__ int chain_row(const SweepArgs& a, int& tx) {
+  int rem = blockIdx.x;
+  const int dv = rem % a.chain_k;
+  rem /= a.chain_k;
+  const int j = rem % a.chain_j, res = blockIdx.y * a.chain_k + dv;
+  tx = rem / a.chain_j;
+  return res < a.chain_s ? j * a.chain_s + res : a.rows;
+}
+
 // Sweep CTA geometry (affine, 32-bit cake): kSweepTileY warps; a
 // warp = 16 windows of one map row, two lanes per window (lane parity =
 // which half of each bin octet).

@@ -75,9 +75,13 @@ def test_workloads_and_engines():
                 kname, P, e = bench.engine_of(g, k, m)
                 assert kname.startswith("k_sweep_") and P in (1, 3, 4, 5) and e in (2, 4, 8)
     c5 = bench.workload("c5")
-    kinds = [g["scales"][0][0].kind for g in c5["groups"]]
-    assert kinds == [swg.MANHATTAN, swg.GAUSS_CHEB, swg.EUCLID_QUAD, swg.EXP_L1]
-    assert all(len(g["scales"]) == 8 for g in c5["groups"])
+    kinds = [[k.kind for k, _, _, _ in g["scales"]] for g in c5["groups"]]
+    # Manhattan and Euclidean share the quadratic table set ({1, x, y} of {1, x, y, x^2, y^2})
+    assert kinds == [[swg.MANHATTAN] * 8 + [swg.EUCLID_QUAD] * 8, [swg.GAUSS_CHEB] * 8,
+                     [swg.EXP_L1] * 8]
+    quad = c5["groups"][0]
+    assert bench.engine_of(quad, quad["scales"][0][0], swg.SWIH) == ("k_sweep_affine", 3, 4)
+    assert bench.engine_of(quad, quad["scales"][8][0], swg.SWIH) == ("k_sweep_quad", 5, 4)
     # 257x257 Gaussian: ring 0's box exceeds 16-bit counts, but ring 1's box
     # and ring 0's frame do not -> still the 16-bit sweep (wide ring 0)
     plain = c5["groups"][1]
