@@ -13,6 +13,7 @@
 // maximum is re-scored by fp64 brute force in the reference's pixel order
 // (baselines.cpp:53-69) and the reference tie rule picks among them.
 #include <algorithm>
+#include <cstdlib>
 
 #include "swg_internal.cuh"
 
@@ -237,6 +238,151 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
 }
 
 
+// Phase 2b, bin-sorted (windows up to 512 wide and 92k pixels): one CTA per
+// candidate.  The reference sums each bin's weights in row-major pixel
+// order (baselines.cpp:53-69), a dependent chain per bin; k_rescore walks
+// the window segment by segment, so every segment costs a 32-add chain
+// whatever its bins.  Here the window's pixels are first sorted STABLY by
+// bin (a counting sort: each of the 8 warps counts, then scatters, the
+// pixels of its row block with __match_any_sync ranks), then thread b adds
+// bin b's weights in that order -- the same sequence of rounded additions,
+// with the critical path the most populous bin's pixel count instead of the
+// whole window (config 5 257^2: one candidate 240 -> ~40 us).
+constexpr int kRsWarps = 8;
+__global__ void __launch_bounds__(32 * kRsWarps) k_rescore_sorted(const SweepArgs a,
+                                                                 const RescoreArgs r,
+                                                                 const swg_peak* fast) {
+  extern __shared__ __align__(16) unsigned char s_mem[];
+  const int bins = r.bins, kw = r.kw, kh = r.kh;
+  double* h = reinterpret_cast<double*>(s_mem);                     // [bins]
+  int* off = reinterpret_cast<int*>(h + bins);                       // [kRsWarps][bins]
+  uint16_t* pos = reinterpret_cast<uint16_t*>(off + kRsWarps * bins);  // [kw * kh]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int R = (kh + kRsWarps - 1) / kRsWarps;  // rows per warp's block
+  const int rb0 = warp * R, rb1 = min(kh, rb0 + R);
+  const int segs = (kw + 31) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int cnt = *r.count;
+  const bool overflow = cnt > r.cap;
+  const double lim = fast->score - r.eps;
+  const long long total = overflow ? (long long)a.rows * a.mw : cnt;
+  double best = -2.0;
+  long long bidx = 0x7FFFFFFFFFFFFFFFLL;
+  for (long long c = blockIdx.x; c < total; c += gridDim.x) {
+    long long idx;
+    if (overflow) {
+      if (!(a.scores[c] >= lim)) continue;  // CTA-uniform
+      idx = (long long)a.row0 * a.mw + c;
+    } else {
+      idx = r.cand[c];
+    }
+    const int u = (int)(idx % a.mw), v = (int)(idx / a.mw);
+    const uint16_t* fi = r.fi + (size_t)v * r.fi_pitch + u;
+    int* mine = off + warp * bins;
+    for (int b = lane; b < bins; b += 32) mine[b] = 0;
+    __syncwarp();
+    // count: this warp's rows, 32 pixels at a time
+    for (int y = rb0; y < rb1; ++y)
+      for (int sgi = 0; sgi < segs; ++sgi) {
+        const int dx = sgi * 32 + lane;
+        const int bl = dx < kw ? __ldg(fi + (size_t)y * r.fi_pitch + dx) : 0xFFFF;
+        const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
+        if (bl < bins && (grp & lt) == 0) mine[bl] += __popc(grp);
+        __syncwarp();
+      }
+    __syncthreads();
+    // offsets: bin-major, then row block (bin b's pixels contiguous in pixel order)
+    if (threadIdx.x < 32) {
+      int run = 0;  // running total over bins (chunks of 32 bins)
+      for (int b0 = 0; b0 < bins; b0 += 32) {
+        const int b = b0 + lane;
+        int tot = 0;
+        if (b < bins)
+          for (int w = 0; w < kRsWarps; ++w) tot += off[w * bins + b];
+        int inc = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int t2 = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+          if (lane >= d) inc += t2;
+        }
+        if (b < bins) {
+          int o = run + inc - tot;
+          for (int w = 0; w < kRsWarps; ++w) {
+            const int n = off[w * bins + b];
+            off[w * bins + b] = o;
+            o += n;
+          }
+        }
+        run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+      }
+    }
+    __syncthreads();
+    // scatter: stable ranks within each segment, segments in pixel order
+    for (int y = rb0; y < rb1; ++y)
+      for (int sgi = 0; sgi < segs; ++sgi) {
+        const int dx = sgi * 32 + lane;
+        const int bl = dx < kw ? __ldg(fi + (size_t)y * r.fi_pitch + dx) : 0xFFFF;
+        const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
+        const int base = bl < bins ? mine[bl] : 0;
+        __syncwarp();
+        if (bl < bins) {
+          pos[base + __popc(grp & lt)] = (uint16_t)(((y - rb0) << 9) | dx);
+          if ((grp & lt) == 0) mine[bl] = base + __popc(grp);
+        }
+        __syncwarp();
+      }
+    __syncthreads();
+    // per bin: its weights in pixel order (mine[] now holds each (block, bin)
+    // segment's END; bin b's list starts where bin b-1's last block ended)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) {
+      double t = 0.0;
+      int k = b > 0 ? off[(kRsWarps - 1) * bins + b - 1] : 0;
+      for (int w = 0; w < kRsWarps; ++w) {
+        const int end = off[w * bins + b];
+        const double* gw = r.grid + (size_t)(w * R) * kw;
+        for (; k + 4 <= end; k += 4) {
+          double wt[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int code = pos[k + q];
+            wt[q] = __ldg(gw + (code >> 9) * kw + (code & 511));
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t = __dadd_rn(t, wt[q]);
+        }
+        for (; k < end; ++k) {
+          const int code = pos[k];
+          t = __dadd_rn(t, __ldg(gw + (code >> 9) * kw + (code & 511)));
+        }
+      }
+      h[b] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mass = 0.0, sc = 0.0;
+      for (int b = 0; b < bins; ++b) mass = __dadd_rn(mass, h[b]);
+      if (a.sim == SWG_SIM_BHATTACHARYYA) {
+        for (int b = 0; b < bins; ++b)
+          sc = __dadd_rn(sc, __dsqrt_rn(__dmul_rn(r.model[b], h[b])));
+        sc = mass > 0.0 ? __ddiv_rn(sc, __dsqrt_rn(mass)) : 0.0;
+      } else if (mass > 0.0) {
+        for (int b = 0; b < bins; ++b) {
+          const double q = __ddiv_rn(h[b], mass);
+          sc = __dadd_rn(sc, (q < r.model[b]) ? q : r.model[b]);
+        }
+      }
+      sc = clamp01e(sc);
+      a.scores[(size_t)(v - a.row0) * a.mw + u] = sc;
+      if (peak_better(sc, idx, best, bidx)) {
+        best = sc;
+        bidx = idx;
+      }
+    }
+    __syncthreads();
+  }
+  cta_peak(threadIdx.x == 0 ? best : -2.0, bidx, r.parts + blockIdx.x);
+}
+
 // Exponential window histograms at explicit centres (swg_decay_windows):
 // per (window, bin) the 16 corners of the sweep, summed per orientation in
 // the sweep's order, the same snap of empty-bin noise.
@@ -285,6 +431,19 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
       a.scores, n, a.row0, a.mw, peak, r.eps, r.cap, r.count, r.cand);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)r.bins * 8 + (size_t)kRsWarps * r.bins * 4 +
+                      round_up((size_t)r.kw * r.kh * 2, 16);
+  const int R = (r.kh + kRsWarps - 1) / kRsWarps;
+  const char* rw = std::getenv("SWG_RESCORE_WARP");  // A/B: 1 = the per-warp kernel
+  if (!(rw && std::atoi(rw)) && r.kw <= 512 && R <= 127 && smem <= (200u << 10)) {
+    // bin-sorted re-score: one CTA per candidate, persistent over them
+    cudaFuncSetAttribute(k_rescore_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const int blocks = std::min(148, (r.cap + 3) / 4);
+    k_rescore_sorted<<<blocks, 32 * kRsWarps, smem, s>>>(a, r, peak);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return launch_peak_reduce(r.parts, blocks, a.mw, a.hx, a.hy, peak, s);
+  }
   const int blocks = (r.cap + 3) / 4;  // one warp per candidate
   k_rescore<<<blocks, 128, 0, s>>>(a, r, peak);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

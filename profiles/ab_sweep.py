@@ -17,14 +17,20 @@ from paper_1705_03524_b200 import swg  # noqa: E402
 cfg, group = sys.argv[1], sys.argv[2]
 axes = [(a.split("=")[0], a.split("=")[1].split(",")) for a in sys.argv[3:]]
 wl = bench.workload(cfg)
-gi = {"manhattan": 0, "gauss": 1, "euclid": 2, "exp": 3}.get(group, 0)
-g = wl["groups"][gi]
+KIND = {"manhattan": swg.MANHATTAN, "gauss": swg.GAUSS_CHEB, "euclid": swg.EUCLID_QUAD,
+        "exp": swg.EXP_L1}
+gi = next((i for i, g_ in enumerate(wl["groups"])
+           if any(k.kind == KIND.get(group, -1) for k, _, _, _ in g_["scales"])), 0)
+g = dict(wl["groups"][gi])
+sel = [i for i, (k, _, _, _) in enumerate(g["scales"])
+       if group not in KIND or k.kind == KIND[group]]
+g["scales"] = [g["scales"][i] for i in sel]
 data = wl["gen"](1)
 ctx = swg.Context(0)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx.set_stream(stream.cuda_stream)
-models = bench.make_models(ctx, wl, data)[gi]
+models = [bench.make_models(ctx, wl, data)[gi][i] for i in sel]
 dev = torch.from_numpy(data.image).cuda()
 if g.get("decay"):
     t = ctx.build_decay(dev, g["decay"], wl["fmt"], wl["bins"])

@@ -17,11 +17,17 @@ cfg, group = sys.argv[1], sys.argv[2]
 want = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 wl = bench.workload(cfg)
-gi = {"manhattan": 0, "gauss": 1, "euclid": 2, "exp": 3}.get(group, 0)
-g = wl["groups"][gi]
+KIND = {"manhattan": swg.MANHATTAN, "gauss": swg.GAUSS_CHEB, "euclid": swg.EUCLID_QUAD,
+        "exp": swg.EXP_L1}
+gi = next((i for i, g_ in enumerate(wl["groups"])
+           if any(k.kind == KIND.get(group, -1) for k, _, _, _ in g_["scales"])), 0)
+g = dict(wl["groups"][gi])
+sel = [i for i, (k, _, _, _) in enumerate(g["scales"])
+       if group not in KIND or k.kind == KIND[group]]
+g["scales"] = [g["scales"][i] for i in sel]
 data = wl["gen"](1)
 ctx = swg.Context(0)
-models = bench.make_models(ctx, wl, data)[gi]
+models = [bench.make_models(ctx, wl, data)[gi][i] for i in sel]
 dev = torch.from_numpy(data.image).cuda()
 if g.get("decay"):
     t = ctx.build_decay(dev, g["decay"], wl["fmt"], wl["bins"])
