@@ -279,6 +279,19 @@ swg_status swg_query_windows(swg_tables* t, int n, const int* cx, const int* cy,
 swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
                             const swg_kernel* kernel, int rings, int ring_rule,
                             int border, double* host_out);
+/* Boundary prefix-row exchange on the device (SURVEY 8e "row bands"): a
+ * band built from pixel rows [y0, y0+h) holds local tables (zero at its row
+ * 0).  swg_tables_last_row writes its last record row of every 32-bit plane
+ * -- planes x octets x (width+1) records of 8 uint32 bins, record order
+ * (octet, plane, x) -- to device memory; all-gather those rows (NCCL over
+ * NVLink), form the carry = exclusive sum over the earlier bands of their
+ * rows (each already global), and swg_tables_add_carry(t, y0, carry) turns
+ * the band's 32-bit planes into the GLOBAL tables' rows y0 .. y0+h (mod
+ * 2^32, like the tables).  Sweeps on carried tables use global rows.  The
+ * exact int64 export of a carried table is refused (SWG_ERR_CONFIG). */
+swg_status swg_tables_last_row(swg_tables* t, void* dev_out);
+swg_status swg_tables_add_carry(swg_tables* t, int y0, const void* dev_carry);
+
 /* Declared exponential kernel (EXP_L1, sigma == the tables' decay) on
  * decayed tables (swg_tables_build_decay): weighted window histograms at
  * strict centres from the sweep's 16 corners per bin, out[n][bins] doubles

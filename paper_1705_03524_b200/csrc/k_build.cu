@@ -462,6 +462,74 @@ __global__ void k_import(const int64_t* src, int w, int h, int kind, uint64_t* t
         (uint64_t)src[((size_t)b * (h + 1) + y) * (w + 1) + x];
 }
 
+// Boundary prefix-row exchange on the device (SURVEY §8e "row bands"): a
+// band built from pixel rows [y0, y0 + h) holds LOCAL tables (zero at its
+// own row 0).  k_last_row copies its last record row (row h) of kinds
+// 0 .. kinds-1 for every octet -- the band's contribution to the prefix row
+// below it -- into out[(g * kinds + k) * (w+1) + x] (records); after an
+// all-gather, k_add_carry turns the local tables into the global ones:
+//   plain  p' = p + c0             xramp  x' = x + c1
+//   yramp  y' = y + y0 p + c2      (rows shift by y0: sum(y_l + y0) = y + y0 N)
+//   x^2    xx' = xx + c3           y^2    yy' = yy + 2 y0 y + y0^2 p + c4
+// with c the exclusive sum of the earlier bands' (already shifted) last
+// rows, all modulo 2^32 like the tables themselves.
+__global__ void k_last_row(const uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds,
+                           int w, int h, int groups, uint4* out) {
+  const size_t n = (size_t)groups * kinds * (w + 1) * 2;  // uint4 halves of records
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t rec = i >> 1;
+    const int x = (int)(rec % (w + 1));
+    const int gk = (int)(rec / (w + 1)), g = gk / kinds, k = gk % kinds;
+    const uint4* src = reinterpret_cast<const uint4*>(
+        tab + (((size_t)g * planes + k) * ps + (size_t)h * pitch + x) * kOct);
+    out[i] = src[i & 1];
+  }
+}
+
+__global__ void k_add_carry(uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds,
+                            int w, int h, int groups, uint32_t y0, const uint32_t* carry) {
+  const size_t n = (size_t)groups * (h + 1) * (w + 1) * 2;  // half records (4 bins)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int half = (int)(i & 1);
+    const size_t rec = i >> 1;
+    const int x = (int)(rec % (w + 1));
+    const size_t gy = rec / (w + 1);
+    const int y = (int)(gy % (h + 1)), g = (int)(gy / (h + 1));
+    uint4 v[5], c[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k >= kinds) break;
+      v[k] = reinterpret_cast<const uint4*>(
+          tab + (((size_t)g * planes + k) * ps + (size_t)y * pitch + x) * kOct)[half];
+      c[k] = reinterpret_cast<const uint4*>(
+          carry + (((size_t)g * kinds + k) * (w + 1) + x) * kOct)[half];
+    }
+    uint32_t p[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+    uint32_t out[5][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t cj[5] = {(&c[0].x)[j], kinds > 1 ? (&c[1].x)[j] : 0u,
+                              kinds > 2 ? (&c[2].x)[j] : 0u, kinds > 3 ? (&c[3].x)[j] : 0u,
+                              kinds > 4 ? (&c[4].x)[j] : 0u};
+      out[0][j] = p[j] + cj[0];
+      if (kinds > 1) out[1][j] = (&v[1].x)[j] + cj[1];
+      if (kinds > 2) out[2][j] = (&v[2].x)[j] + y0 * p[j] + cj[2];
+      if (kinds > 3) out[3][j] = (&v[3].x)[j] + cj[3];
+      if (kinds > 4)
+        out[4][j] = (&v[4].x)[j] + 2u * y0 * (&v[2].x)[j] + y0 * y0 * p[j] + cj[4];
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k >= kinds) break;
+      reinterpret_cast<uint4*>(tab + (((size_t)g * planes + k) * ps + (size_t)y * pitch + x) *
+                                         kOct)[half] =
+          make_uint4(out[k][0], out[k][1], out[k][2], out[k][3]);
+    }
+  }
+}
+
 __global__ void k_narrow(const uint64_t* src, uint32_t* dst, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -579,6 +647,20 @@ cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int ki
                               cudaStream_t s) {
   dim3 grid((unsigned)((w + 1 + 255) / 256), (unsigned)(h + 1), (unsigned)bins);
   k_import<<<grid, 256, 0, s>>>(src, w, h, kind, tab, ps, pitch, planes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_last_row(const uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds,
+                            int w, int h, int groups, void* out, cudaStream_t s) {
+  k_last_row<<<148 * 4, 256, 0, s>>>(tab, ps, pitch, planes, kinds, w, h, groups,
+                                      static_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_carry(uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds, int w,
+                             int h, int groups, int y0, const void* carry, cudaStream_t s) {
+  k_add_carry<<<148 * 8, 256, 0, s>>>(tab, ps, pitch, planes, kinds, w, h, groups, (uint32_t)y0,
+                                       static_cast<const uint32_t*>(carry));
   return cudaGetLastError();
 }
 

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
   const uint32_t centre = ((uint32_t)cy * (uint32_t)a.pitch + (uint32_t)cx) * kOct + half * 4;
   const size_t ps8 = a.plane_stride * kOct;
   const uint32_t M = (uint32_t)(a.hx + a.hy + 1);
-  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
+  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)(cy + a.y_off);
 
   double s = 0.0, mass_unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;
@@ -184,7 +184,7 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
   const size_t ps8 = a.plane_stride * kOct;
   const uint64_t kx = (uint64_t)(a.hx + 1) * (a.hx + 1), ky = (uint64_t)(a.hy + 1) * (a.hy + 1);
   const uint64_t A = 2 * kx * ky;
-  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)cy;
+  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)(cy + a.y_off);
 
   double s = 0.0, unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;

@@ -272,6 +272,8 @@ struct swg_tables {
   swg_ctx* ctx = nullptr;
   int w = 0, h = 0, bins = 0, planes = 0, format = 0, levels = 0;
   int bin0 = 0, total_bins = 0;  // planes hold bins [bin0, bin0 + bins) of total_bins
+  int carry_y0 = 0;     // 32-bit planes hold GLOBAL rows y0.. (swg_tables_add_carry)
+  bool carried = false;
   bool has_fi = false;
   uint16_t* fi = nullptr;
   size_t fip = 0;
@@ -833,6 +835,8 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
+  t->carried = false;
+  t->carry_y0 = 0;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
@@ -993,6 +997,8 @@ extern "C" {
 
 swg_status swg_tables_export_i64(swg_tables* t, int kind, int b0, int b1, int64_t* out) {
   ST_TRY(check_export(t, kind, b0, b1, out));
+  if (t->carried)
+    return fail(SWG_ERR_CONFIG, "tables carry a boundary prefix row: export their 32-bit words");
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
@@ -1557,6 +1563,7 @@ void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r
   a.pin = static_cast<const double2*>(r.partial_in);
   a.pout = static_cast<double2*>(r.partial_out);
   a.sc_tiles = p.chain_s ? 0 : super_column_tiles(t, p.engine, p.k, a.hx, a.hy);
+  a.y_off = p.engine == kCake16 ? 0 : t->carry_y0;  // global-row tables (add_carry)
   a.chain_s = p.chain_s;
   a.chain_k = p.chain_k;
   a.chain_j = p.chain_j;
@@ -2082,6 +2089,40 @@ swg_status swg_decay_windows(swg_tables* t, int n, const int* cx, const int* cy,
   c->launches += 1;
   CUDA_TRY(cudaMemcpyAsync(out, c->qout.p, ob, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SWG_OK;
+}
+
+// Boundary prefix-row exchange on the device: the band's last
+// record row of the 32-bit planes (k_last_row), and the carry that turns a
+// band's local tables into the global ones (k_add_carry).
+swg_status swg_tables_last_row(swg_tables* t, void* dev_out) {
+  ST_TRY(check_tables(t));
+  if (!dev_out) return fail(SWG_ERR_ARG, "NULL output");
+  if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  ST_TRY(ensure_t32(t));
+  const int kinds = t->planes;
+  CUDA_TRY(launch_last_row(t->t32, t->ps, t->pitch, t->planes, kinds, t->w, t->h, t->groups,
+                           dev_out, t->ctx->stream));
+  t->ctx->launches += 1;
+  return SWG_OK;
+}
+
+swg_status swg_tables_add_carry(swg_tables* t, int y0, const void* dev_carry) {
+  ST_TRY(check_tables(t));
+  if (!dev_carry) return fail(SWG_ERR_ARG, "NULL carry");
+  if (t->tdec) return fail(SWG_ERR_CONFIG, "decay tables hold no integral planes");
+  if (y0 < 0) return fail(SWG_ERR_OUT_OF_RANGE, "band origin %d", y0);
+  if (t->carried) return fail(SWG_ERR_CONFIG, "tables already carry a boundary prefix row");
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  ST_TRY(ensure_t32(t));
+  CUDA_TRY(launch_add_carry(t->t32, t->ps, t->pitch, t->planes, t->planes, t->w, t->h,
+                            t->groups, y0, dev_carry, t->ctx->stream));
+  t->ctx->launches += 1;
+  t->carried = true;
+  t->carry_y0 = y0;
   return SWG_OK;
 }
 

@@ -119,6 +119,7 @@ struct SweepArgs {
   // bottom corners = window v+chain_s's top corners) run back to back
   int chain_s, chain_k, chain_j;  // 0: off
   int wide0;           // cake16: ring 0's box count may exceed 16 bits
+  int y_off;           // table row 0 is image row y_off (carried band tables)
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
@@ -378,6 +379,10 @@ cudaError_t launch_import_i64(const int64_t* src, int w, int h, int bins, int ki
                               uint64_t* tab, size_t ps, size_t pitch, int planes,
                               cudaStream_t s);
 cudaError_t launch_narrow(const uint64_t* src, uint32_t* dst, size_t n, cudaStream_t s);
+cudaError_t launch_last_row(const uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds,
+                            int w, int h, int groups, void* out, cudaStream_t s);
+cudaError_t launch_add_carry(uint32_t* tab, size_t ps, size_t pitch, int planes, int kinds, int w,
+                             int h, int groups, int y0, const void* carry, cudaStream_t s);
 // Brute-force histograms of explicit windows (API queries).
 struct BruteQueryArgs {
   const uint16_t* fi;  // w*h, tight rows

@@ -253,3 +253,56 @@ def combine_request_peaks(parts: Sequence[Tuple[Tuple[int, int], Tuple[int, int]
         if key not in best or better((s, gi), best[key]):
             best[key] = (s, gi)
     return best
+
+
+# ---------------------------------------------------------------- device rows
+def _wrap32(x):
+    """int64 tensor -> the same values modulo 2^32 as int32 (two's complement)."""
+    import torch
+    x = x & 0xFFFFFFFF
+    return torch.where(x >= 2 ** 31, x - 2 ** 32, x).to(torch.int32)
+
+
+def band_contribution(last, y0: int):
+    """A band's contribution to the global prefix row below it, from its
+    LOCAL last record row (device int32 tensor (octets, planes, w+1, 8) of
+    swg_tables_last_row): rows shift by y0, so the y-ramp gains y0 * count
+    (and the y^2 ramp 2 y0 y + y0^2 count).  Modulo 2^32 like the tables."""
+    c = last.to("cpu" if not last.is_cuda else last.device).long() & 0xFFFFFFFF
+    out = c.clone()
+    if c.shape[1] > 2:
+        out[:, 2] = c[:, 2] + y0 * c[:, 0]
+    if c.shape[1] > 4:
+        out[:, 4] = c[:, 4] + 2 * y0 * c[:, 2] + y0 * y0 * c[:, 0]
+    return out
+
+
+def device_carry(lasts, y0s, rank: int):
+    """Exclusive sum of the earlier bands' contributions (the carry rank
+    `rank` adds to its local tables), as int32 words."""
+    import torch
+    acc = torch.zeros_like(lasts[0], dtype=torch.int64)
+    for r in range(rank):
+        acc = acc + band_contribution(lasts[r], y0s[r])
+    return _wrap32(acc)
+
+
+def exchange_last_rows_device(tables, y0: int, group=None):
+    """The boundary prefix-row exchange on the device: all-gather every
+    band's last record row (NCCL over NVLink on the box; gloo stages through
+    the host in the CPU tests) and each band's origin, then turn this band's
+    local 32-bit tables into the global rows y0.. (swg_tables_add_carry).
+    Returns the carry."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    last = tables.last_row()
+    nccl = dist.get_backend(group) == "nccl"
+    send = last if nccl else last.cpu()
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send, group=group)
+    origins = [None] * world
+    dist.all_gather_object(origins, int(y0), group=group)
+    carry = device_carry([p.to(last.device) for p in parts], origins, rank).to(last.device)
+    tables.add_carry(y0, carry.contiguous())
+    return carry

@@ -172,6 +172,8 @@ def lib():
         "swg_query_terms": [vp, C.c_int, C.c_int, vp, vp],
         "swg_query_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), C.c_int, C.c_int, vp],
         "swg_decay_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), vp],
+        "swg_tables_last_row": [vp, vp],
+        "swg_tables_add_carry": [vp, C.c_int, vp],
         "swg_cake_windows": [vp, C.c_int, vp, vp, C.POINTER(Kernel), C.c_int, C.c_int, C.c_int,
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
@@ -432,6 +434,20 @@ class Tables:
         _check(lib().swg_query_windows(self._h, len(cx), _ptr(cx), _ptr(cy), C.byref(kernel),
                                        method, border, _ptr(out)))
         return out
+
+    def last_row(self, out=None):
+        """Device uint32 tensor (octets, planes, width+1, 8): this band's last
+        record row (swg_tables_last_row)."""
+        import torch
+        if out is None:
+            out = torch.empty((-(-self.bins // 8), self.planes, self.width + 1, 8),
+                              dtype=torch.int32, device="cuda")
+        _check(lib().swg_tables_last_row(self._h, C.c_void_p(out.data_ptr())))
+        return out
+
+    def add_carry(self, y0, carry):
+        """Local band tables -> global rows y0.. (swg_tables_add_carry)."""
+        _check(lib().swg_tables_add_carry(self._h, int(y0), C.c_void_p(carry.data_ptr())))
 
     def decay_windows(self, cx, cy, kernel: Kernel):
         """Exponential-kernel window histograms (strict) from decayed tables."""

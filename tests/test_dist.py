@@ -260,3 +260,87 @@ def test_plan_frame_geometry():
         assert max(loads) <= (total + sum(build)) / world * 1.35 + 0.6
     one = D.plan_frame([((0, 0), 0, 100, 5.0)], [0.1], 4, min_rows=8)
     assert sum(len(p) for p in one) == 4  # a single request splits by rows
+
+
+def _records(tables, bins):
+    """Oracle int64 tables (3, bins, h+1, w+1) -> the device record layout of
+    the last row (octets, planes, w+1, 8) as int32 words mod 2^32."""
+    import torch
+    p = np.stack([t[:, -1, :] for t in tables])  # (3, bins, w+1)
+    g = -(-bins // 8)
+    out = np.zeros((g, 3, p.shape[2], 8), np.int64)
+    for b in range(bins):
+        out[b // 8, :, :, b % 8] = p[:, b, :]
+    return D._wrap32(torch.from_numpy(out))
+
+
+def test_device_carry_equals_host_exchange():
+    """dist.device_carry (the device boundary-row exchange's arithmetic, on
+    int32 record rows mod 2^32) == the exact host exchange (band_carry)."""
+    import torch
+    from oracle import oracle as O
+    orc = O.Oracle()
+    img = orc.random_gray(40, 90, 12)
+    bins = 11
+    fi = orc.quantize_gray8(img, bins)
+    bands = D.table_bands(90, 4)
+    local = [orc.build_tables(np.ascontiguousarray(fi[y0:y1]), bins) for y0, y1 in bands]
+    lasts = [_records(t, bins) for t in local]
+    rows = [D.last_rows(t, y0) for t, (y0, _) in zip(local, bands)]
+    for r in range(4):
+        host = D.band_carry(rows, r)  # (3, bins, w+1) exact
+        dev = D.device_carry(lasts, [y0 for y0, _ in bands], r)
+        want = _records([host[k][:, None, :] for k in range(3)], bins)
+        assert torch.equal(dev, want), r
+
+
+class _FakeBand:
+    """CPU stand-in for a device table set (last_row / add_carry)."""
+
+    def __init__(self, last):
+        self.last, self.carry = last, None
+
+    def last_row(self):
+        return self.last
+
+    def add_carry(self, y0, carry):
+        self.carry = (y0, carry)
+
+
+def _xchg_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from oracle import oracle as O
+        orc = O.Oracle()
+        img = orc.random_gray(33, 61, 3)
+        bins = 9
+        fi = orc.quantize_gray8(img, bins)
+        bands = D.table_bands(61, world)
+        y0, y1 = bands[rank]
+        local = orc.build_tables(np.ascontiguousarray(fi[y0:y1]), bins)
+        band = _FakeBand(_records(local, bins))
+        carry = D.exchange_last_rows_device(band, y0)
+        rows = [D.last_rows(orc.build_tables(np.ascontiguousarray(fi[a:b]), bins), a)
+                for a, b in bands]
+        want = _records([D.band_carry(rows, rank)[k][:, None, :] for k in range(3)], bins)
+        q.put((rank, bool(torch.equal(carry, want)) and band.carry[0] == y0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_row_exchange_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for _, ok in res), res

@@ -1047,3 +1047,42 @@ def test_bin_chain_through_peer_memory():
         p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
     assert res[0] and res[1]
+
+
+# ---------------------------------------------------------------- device boundary rows
+@pytest.mark.parametrize("planes", [swg.PLANES_AFFINE, swg.PLANES_QUADRATIC])
+def test_device_boundary_row_exchange(ctx, oracle, planes):
+    """Row bands built separately; their last record rows exchanged on the
+    device (the all-gather simulated by a list) and carried
+    (swg_tables_add_carry): every band's 32-bit planes equal the full frame's
+    rows, and sweeps on the carried (global-row) tables give the full frame's
+    map rows bit for bit."""
+    import torch
+    from paper_1705_03524_b200 import dist as D
+    img = oracle.random_gray(301, 170, 77)
+    bins = 12
+    full = ctx.build(img, swg.FMT_GRAY8, bins, planes)
+    want = [full.export_u32(k) for k in range(3)]
+    if planes == swg.PLANES_QUADRATIC:
+        want += [(full.export_i64(k) & 0xFFFFFFFF).astype(np.uint32) for k in (3, 4)]
+    bands = D.table_bands(170, 3)
+    tabs = [ctx.build(np.ascontiguousarray(img[y0:y1]), swg.FMT_GRAY8, bins, planes)
+            for y0, y1 in bands]
+    lasts = [t.last_row() for t in tabs]
+    y0s = [y0 for y0, _ in bands]
+    for r, (t, (y0, y1)) in enumerate(zip(tabs, bands)):
+        t.add_carry(y0, D.device_carry(lasts, y0s, r).cuda().contiguous())
+        for k in range(3):
+            assert (t.export_u32(k)[:, :, :] == want[k][:, y0:y1 + 1]).all(), (r, k)
+        with pytest.raises(swg.ConfigError):
+            t.export_i64(0)
+    # maps on the carried tables: map rows of windows inside each band
+    kk = K(swg.EUCLID_QUAD if planes == swg.PLANES_QUADRATIC else swg.MANHATTAN, 9, 7)
+    fi = oracle.quantize_gray8(img, bins)
+    ok = O.kernel(kk.kind, 9, 7)
+    mdl = oracle.target_model(fi[40:47, 50:59].copy(), bins, ok,
+                              O.BRUTE if planes == swg.PLANES_QUADRATIC else O.SWIH)
+    fmap, _ = full.likelihood_map(kk, mdl)
+    for t, (y0, y1) in zip(tabs, bands):
+        got, _ = t.likelihood_map(kk, mdl)
+        assert (got == fmap[y0:y1 - 6]).all()
