@@ -67,12 +67,39 @@ def peaks_json():
 
 
 # ------------------------------------------------------------------ workloads
-def workload(name):
+def exp_decay_of(kw, mode):
+    """Declared exponential kernel's decay per pixel: one d = 15/16 for every
+    scale ("fixed", one decayed table set), or d = exp(-4/kw) per scale
+    ("scale": SURVEY App. A's lambda ~ 1/kw, the weight at the window corner
+    e^(-4 (kw-1)/kw) ~ 0.018 at every scale; one decayed table set per scale)."""
+    import math
+    return EXP_DECAY if mode == "fixed" else math.exp(-4.0 / kw)
+
+
+def exp_groups(ks, mode, bin_chunks=None):
+    from paper_1705_03524_b200 import swg
+    K = swg.Kernel
+    extra = {"bin_chunks": bin_chunks} if bin_chunks else {}
+    if mode == "fixed":
+        return [dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, **extra,
+                     scales=[(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None) for k in ks])]
+    return [dict(planes=swg.PLANES_DECAY, decay=exp_decay_of(k, mode), **extra,
+                 scales=[(K(swg.EXP_L1, k, k, exp_decay_of(k, mode)), swg.SWIH, 1, None)])
+            for k in ks]
+
+
+EXP_SCALE_NOTE = ("exponential w = d^(|dx|+|dy|) with d = exp(-4/kw) per scale (one decayed "
+                  "table set per scale; corner weight ~0.018 at every scale)")
+
+
+def workload(name, exp_decay="fixed"):
     """A workload = input generator + table groups; a group = one table set
     (planes / decay) and the scales (kernel, method, rings, target index)
-    it serves."""
+    it serves.  exp_decay: "fixed" (one decay for every scale) or "scale"
+    (exp_decay_of)."""
     from paper_1705_03524_b200 import swg, synth
     K = swg.Kernel
+    enote = EXP_NOTE if exp_decay == "fixed" else EXP_SCALE_NOTE
     if name == "c1":
         return dict(name="config1: 256x256 u8, 16 bins, Manhattan, window 33x33", kind="frame",
                     gen=synth.config1, fmt=swg.FMT_GRAY8, bins=16, nbins=16, scaling="strong",
@@ -94,11 +121,9 @@ def workload(name):
                 dict(planes=swg.PLANES_PLAIN,
                      scales=[(K(swg.GAUSS_CHEB, k, k, 0.5), swg.CAKE, k // 2 + 1, None)
                              for k in ks]),
-                dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY,
-                     scales=[(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None) for k in ks]),
-            ]
+            ] + exp_groups(ks, exp_decay)
             label = ("Manhattan + Gaussian (exact full-ring cake) + Euclidean (quadratic) + "
-                     + EXP_NOTE)
+                     + enote)
         return dict(name=f"config5{' (Manhattan subset)' if name == 'c5m' else ''}: 2048x2048 "
                          f"u16, 64 bins, {label}, windows " + "/".join(map(str, ks)),
                     kind="frame", gen=synth.config5, fmt=swg.FMT_GRAY16, bins=64, nbins=64,
@@ -111,14 +136,10 @@ def workload(name):
                     kind="sequence", gen=synth.config3, fmt=swg.FMT_RGB8, bins=4, nbins=64,
                     scaling="strong", groups=[dict(planes=swg.PLANES_QUADRATIC, scales=scales)])
     if name == "c4":
-        scales = [(K(swg.EXP_L1, k, k, EXP_DECAY), swg.SWIH, 1, None)
-                  for k in (25, 37, 57, 85, 129)]
-        return dict(name="config4: 3840x2160 RGB, 8x8x8 bins, " + EXP_NOTE +
+        return dict(name="config4: 3840x2160 RGB, 8x8x8 bins, " + enote +
                          ", windows 25/37/57/85/129, row bands",
                     kind="bands", gen=synth.config4, fmt=swg.FMT_RGB8, bins=8, nbins=512,
-                    scaling="strong",
-                    groups=[dict(planes=swg.PLANES_DECAY, decay=EXP_DECAY, bin_chunks=8,
-                                 scales=scales)])
+                    scaling="strong", groups=exp_groups((25, 37, 57, 85, 129), exp_decay, 8))
     scales = []
     for i, s in enumerate((32, 64, 96)):
         kw = synth.odd_window(s)
@@ -407,6 +428,9 @@ def parse_args(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c5m"])
+    ap.add_argument("--exp-decay", default="fixed", choices=["fixed", "scale"],
+                    help="declared exponential kernel: one decay 15/16 for every scale "
+                         "(default) or exp(-4/kw) per scale (one decayed table set each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -569,49 +593,65 @@ class OursArm:
                                             dtype=self.torch.float64, device="cuda")
 
     def _band_units(self):
-        """c4: row bands (one per rank, or more if a band's tables do not fit)."""
+        """c4: row bands (one per rank, or more if a band's tables do not fit);
+        every table group (one decay per scale with --exp-decay scale) builds
+        its own tables over the same bands."""
         torch, swg, ctx, wl = self.torch, self.swg, self.ctx, self.wl
         data, rank, world = self.data, self.rank, self.world
         H, W = data.image.shape[:2]
         frame_dev = torch.from_numpy(data.image).cuda()
-        g, ms = wl["groups"][0], self.models[0]
+        groups = wl["groups"]
+        if self.bins_mode:
+            assert len(groups) == 1, "--shard bins: one table group"
+        scales = [sc for g in groups for sc in g["scales"]]
         full_maps = [torch.empty((H - k.kh + 1, W - k.kw + 1), dtype=torch.float64, device="cuda")
-                     for k, _, _, _ in g["scales"]]
+                     for k, _, _, _ in scales]
         # one row band per rank (the whole frame on one GPU: 136 GB of decay
         # tables, the band halo costs more than it saves); twice as many if a
         # band's tables do not fit
         n_bands = int(os.environ.get("SWG_C4_BANDS", 1 if not self.bins_mode else 4))
         n_bands = max(n_bands, world) if not self.bins_mode else n_bands
         while True:
-            BH, plan = band_plan(H, g["scales"], n_bands)
+            BH, plan = band_plan(H, scales, n_bands)
             mine = list(range(n_bands)) if self.bins_mode else \
                 [b for b in range(n_bands) if b % world == rank]
+            tabs = []
             try:
-                if self.bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e)
-                    from paper_1705_03524_b200 import dist as D
-                    b0, b1 = D.bin_ranges(self.nb, world)[rank]
-                    t = ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1, self.fmt,
-                                       wl["bins"], g["planes"], decay=g.get("decay") or 0.0)
-                else:
-                    t = self.new_tables(g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH])
+                for g in groups:
+                    if self.bins_mode:  # rank g: bins [b_g, b_g+1) of every band (SURVEY §8e)
+                        from paper_1705_03524_b200 import dist as D
+                        b0, b1 = D.bin_ranges(self.nb, world)[rank]
+                        tabs.append(ctx.build_bins(frame_dev[plan[0][0]:plan[0][0] + BH], b0, b1,
+                                                   self.fmt, wl["bins"], g["planes"],
+                                                   decay=g.get("decay") or 0.0))
+                    else:
+                        tabs.append(self.new_tables(
+                            g, frame_dev[plan[mine[0]][0]:plan[mine[0]][0] + BH]))
                 break
             except swg.CapacityError:
+                for t in tabs:
+                    t.close()
                 if n_bands >= 64:
                     raise
                 n_bands *= 2
         for b in mine:
             p0, rows = plan[b]
-            reqs, maps, sidx = [], [], []
-            for si, ((k, meth, rings, _), m) in enumerate(zip(g["scales"], ms)):
-                v0, v1 = rows[si]
-                if v1 <= v0:
-                    continue
-                reqs.append(swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings,
-                                           rows=(v0 - p0, v1 - p0)))
-                maps.append(full_maps[si][v0:v1])
-                sidx.append(si)
-            self.units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs,
-                                   maps=maps, g=0, sidx=sidx, band=b, p0=p0, h2d=BH * W * 3))
+            off = 0
+            for gi, (g, ms, t) in enumerate(zip(groups, self.models, tabs)):
+                reqs, maps, sidx = [], [], []
+                for si, ((k, meth, rings, _), m) in enumerate(zip(g["scales"], ms)):
+                    v0, v1 = rows[off + si]
+                    if v1 <= v0:
+                        continue
+                    reqs.append(swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings,
+                                               rows=(v0 - p0, v1 - p0)))
+                    maps.append(full_maps[off + si][v0:v1])
+                    sidx.append(si)
+                off += len(g["scales"])
+                if reqs:
+                    self.units.append(dict(t=t, src=frame_dev[p0:p0 + BH], pitch=0, reqs=reqs,
+                                           maps=maps, g=gi, sidx=sidx, band=b, p0=p0,
+                                           h2d=BH * W * 3))
         if self.bins_mode:
             self._attach_rank_chain()
         self.tab_w, self.tab_h = W, BH
@@ -1182,7 +1222,7 @@ class OursArm:
 
 def main():
     args = parse_args()
-    wl = workload(args.config)
+    wl = workload(args.config, args.exp_decay)
     if args.impl == "reference":
         return run_reference(args, wl, int(os.environ.get("RANK", 0)),
                              int(os.environ.get("WORLD_SIZE", 1)))

@@ -183,6 +183,9 @@ swg_status swg_ctx_synchronize(swg_ctx* ctx);
 swg_status swg_ctx_set_stream(swg_ctx* ctx, void* cuda_stream);
 /* Number of kernels this context launched so far (bench evidence). */
 swg_status swg_ctx_launch_count(swg_ctx* ctx, uint64_t* n);
+/* Device-to-host copies of host maps issued so far (maps written zero-copy
+ * into page-locked host memory issue none). */
+swg_status swg_ctx_map_copy_count(swg_ctx* ctx, uint64_t* n);
 
 /* ---- integral tables ------------------------------------------------- */
 /* Quantise + build one plane set.  `pixels` is host memory

@@ -258,6 +258,7 @@ struct swg_ctx {
   bool fanout_off = false;
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
+  std::atomic<uint64_t> map_copies{0};  // device->host map copies issued (zero-copy check)
   DevBuf terms, qout, grid, io, bpeaks;
   // exact kernel-weight grids, uploaded once per kernel (graph-capture safe)
   struct Grid {
@@ -693,6 +694,12 @@ swg_status swg_ctx_set_stream(swg_ctx* c, void* s) {
   if (!c) return fail(SWG_ERR_ARG, "NULL ctx");
   std::lock_guard<std::mutex> lk(c->mu);
   c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  return SWG_OK;
+}
+
+swg_status swg_ctx_map_copy_count(swg_ctx* c, uint64_t* n) {
+  if (!c || !n) return fail(SWG_ERR_ARG, "NULL");
+  *n = c->map_copies.load();
   return SWG_OK;
 }
 
@@ -1917,6 +1924,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       CUDA_TRY(cudaMemcpyAsync(scores_host[i] + (size_t)row_off * p.mw,
                                dscores + (size_t)row_off * p.mw, (size_t)rows * p.mw * 8,
                                cudaMemcpyDeviceToHost, c->copy));
+      c->map_copies += 1;
       copies = true;
       return SWG_OK;
     };

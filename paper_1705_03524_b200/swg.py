@@ -149,6 +149,7 @@ def lib():
         "swg_ctx_synchronize": [vp],
         "swg_ctx_set_stream": [vp, vp],
         "swg_ctx_launch_count": [vp, C.POINTER(C.c_uint64)],
+        "swg_ctx_map_copy_count": [vp, C.POINTER(C.c_uint64)],
         "swg_tables_build": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_size_t, C.POINTER(vp)],
         "swg_tables_build_decay": [vp, vp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
@@ -262,6 +263,13 @@ class Context:
     def launches(self) -> int:
         n = C.c_uint64()
         _check(lib().swg_ctx_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    @property
+    def map_copies(self) -> int:
+        """Device->host map copies issued so far (zero-copy maps issue none)."""
+        n = C.c_uint64()
+        _check(lib().swg_ctx_map_copy_count(self._h, C.byref(n)))
         return n.value
 
     def build(self, pixels, fmt=FMT_GRAY8, bins=16, planes=PLANES_AFFINE, budget=0,

@@ -39,7 +39,7 @@ def bench_step(config, rank=None, world=None, extra=()):
     import bench
     args = bench.parse_args(["--config", config, "--steps", "1", "--warmup", "3",
                              "--no-cpu-baseline", "--no-e2e", *extra])
-    arm = bench.OursArm(args, bench.workload(config), rank=rank, world=world)
+    arm = bench.OursArm(args, bench.workload(config, args.exp_decay), rank=rank, world=world)
     try:
         arm.step()
         torch.cuda.synchronize()
@@ -133,6 +133,18 @@ def test_config5_full_maps(oracle, group, label, nmaps):
         assert n == nmaps
         if label == "exp_l1":
             print(f"config 5 exponential: max |gpu - oracle| = {worst:.3g}")
+
+
+def test_config5_exponential_per_scale_decay(oracle):
+    """bench.py --exp-decay scale: one decayed table set per scale with
+    d = exp(-4/kw) -- every map within 1e-4 of the oracle, every peak exact."""
+    with bench_step("c5", extra=("--exp-decay", "scale")) as arm:
+        fi = _quantized(oracle, arm.wl, arm.data.image)
+        groups = {gi for gi, g in enumerate(arm.wl["groups"]) if g.get("decay")}
+        assert len(groups) == 8
+        n, worst = _check_maps(oracle, arm, fi, groups=groups)
+        assert n == 8
+        print(f"config 5 exponential per-scale decay: max |gpu - oracle| = {worst:.3g}")
 
 
 def test_config5_multi_gpu_plan_union(oracle):

@@ -863,11 +863,52 @@ def test_pinned_host_maps_zero_copy(ctx, oracle):
                                                             rings))
     for planes, reqs in by_tab.items():
         for group in ([r] for r in reqs) if len(reqs) == 1 else (reqs[:1], reqs):
+            c0 = ctx.map_copies
             want, wpk = tabs[planes].likelihood_maps(group, scores="host")
+            c1 = ctx.map_copies
             got, gpk = tabs[planes].likelihood_maps(group, scores="pinned")
+            c2 = ctx.map_copies
+            assert c1 - c0 >= len(group)  # pageable maps are copied
+            # page-locked maps: the sweeps write them, no copy (the exponential
+            # sweep's exact-peak re-score keeps its device map and a copy)
+            assert c2 - c1 == (len(group) if planes == swg.PLANES_DECAY else 0)
             assert gpk == wpk
             for g_, w_ in zip(got, want):
                 assert (g_ == w_).all()
+
+
+def test_fanout_reorders_costliest_first_outputs_stay_put(ctx, oracle):
+    """Device-output requests given in ASCENDING cost order (the fan-out
+    issues the costliest first): every map and peak still lands at its own
+    index and equals the single-request result; host, device and no-map
+    outputs mixed."""
+    import torch
+    img = oracle.random_gray(180, 150, 41)
+    bins = 16
+    fi = oracle.quantize_gray8(img, bins)
+    t = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+    ks = [(K(swg.UNIFORM, 5, 5), swg.PLAIN, 1), (K(swg.GAUSS_CHEB, 11, 11, 0.5), swg.CAKE, 6),
+          (K(swg.GAUSS_CHEB, 21, 21, 0.5), swg.CAKE, 11),
+          (K(swg.GAUSS_CHEB, 31, 31, 0.5), swg.CAKE, 16),
+          (K(swg.GAUSS_CHEB, 41, 41, 0.5), swg.BRUTE, 1)]
+    reqs = []
+    for k, method, rings in ks:
+        ok = O.kernel(k.kind, k.kw, k.kh, k.sigma)
+        mdl = oracle.target_model(fi[10:10 + k.kh, 20:20 + k.kw].copy(), bins, ok,
+                                  O.SWIH if method == swg.PLAIN else method, rings)
+        reqs.append(swg.MapRequest(k, mdl, method, swg.BHATTACHARYYA, rings))
+    single = [t.likelihood_map(r.kernel, r.model, r.method, rings=r.rings) for r in reqs]
+    dev = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda") for r in reqs]
+    peaks = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
+    t.likelihood_maps(reqs, scores="none", scores_dev=dev, peaks_dev=peaks)
+    ctx.synchronize()
+    pk = peaks.cpu().numpy()
+    for i, (m, p) in enumerate(single):
+        assert (dev[i].cpu().numpy() == m).all(), i
+        ints = pk[i, :2].view(np.int32)
+        assert (int(ints[0]), int(ints[1]), float(pk[i, 2])) == (p[0], p[1], p[4]), i
+    maps, pks = t.likelihood_maps(reqs, scores="none")  # peaks only
+    assert [tuple(p) for p in pks] == [tuple(p) for _, p in single]
 
 
 def test_quadratic_tall_image(ctx, oracle):
