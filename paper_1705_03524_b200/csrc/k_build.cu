@@ -23,6 +23,8 @@
 // them; T = uint64_t reproduces the reference's int64 tables.
 #include "swg_internal.cuh"
 
+#include <cstdlib>
+
 namespace swg {
 
 namespace {
@@ -205,6 +207,29 @@ __global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t
     run.y += __shfl_sync(0xFFFFFFFFu, inc.y, 31);
     run.z += __shfl_sync(0xFFFFFFFFu, inc.z, 31);
     run.w += __shfl_sync(0xFFFFFFFFu, inc.w, 31);
+  }
+}
+
+// K1b, sequential form: one thread per uint4 column word walks the bands in
+// order (a running sum; the loads of 8 bands in flight at a time).  The
+// warp-per-word shuffle scan above keeps 32 lanes busy per word, but with a
+// few dozen bands most lanes idle and the shuffles throttle the MIO pipe
+// (config 5: 53 us for 58 MB).
+__global__ void __launch_bounds__(256) k_bandscan_seq(uint4* agg, int nbands, size_t per_band) {
+  const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (col >= per_band) return;
+  uint4 run = make_uint4(0, 0, 0, 0);
+  constexpr int kB = 8;
+  for (int b0 = 0; b0 < nbands; b0 += kB) {
+    uint4 v[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k)
+      v[k] = b0 + k < nbands ? agg[(size_t)(b0 + k) * per_band + col] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      if (b0 + k < nbands) agg[(size_t)(b0 + k) * per_band + col] = run;
+      run.x += v[k].x; run.y += v[k].y; run.z += v[k].z; run.w += v[k].w;
+    }
   }
 }
 
@@ -563,8 +588,13 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t per_band = (size_t)a.groups * a.wa * a.aw / 4;
-  k_bandscan<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-      reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
+  const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
+  if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
+    k_bandscan<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
+  else
+    k_bandscan_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
   return cudaGetLastError();
 }
 

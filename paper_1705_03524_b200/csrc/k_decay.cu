@@ -29,6 +29,7 @@
 #include <math.h>
 
 #include <cmath>
+#include <cstdlib>
 
 namespace swg {
 
@@ -111,6 +112,29 @@ __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, i
     const real ent = lane > 0 ? fma(pa, run, pv) : run;
     if (b < nbands) agg[(size_t)b * per_band + col] = ent;
     run = fma(__shfl_sync(0xFFFFFFFFu, ia, 31), run, __shfl_sync(0xFFFFFFFFu, inc, 31));
+  }
+}
+
+// K1b', sequential form: one thread per column word walks the bands in order
+// (loads of 8 bands in flight); see k_bandscan_seq.
+__global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nbands, real dband,
+                                                            real dlast, size_t per_band) {
+  const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (col >= per_band) return;
+  real run = 0.0;
+  constexpr int kB = 8;
+  for (int b0 = 0; b0 < nbands; b0 += kB) {
+    real v[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) v[k] = b0 + k < nbands ? agg[(size_t)(b0 + k) * per_band + col] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int b = b0 + k;
+      if (b < nbands) {
+        agg[(size_t)b * per_band + col] = run;
+        run = fma(b == nbands - 1 ? dlast : dband, run, v[k]);
+      }
+    }
   }
 }
 
@@ -297,8 +321,13 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     const size_t per_band = (size_t)pairs * a.wa * kDP;
     const double dband = std::pow(dec, (double)a.band_h);
     const double dlast = std::pow(dec, (double)(a.h - (a.nbands - 1) * a.band_h));
-    k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band);
+    const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
+    if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
+      k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
+          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band);
+    else
+      k_bandscan_decay_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
+          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }
