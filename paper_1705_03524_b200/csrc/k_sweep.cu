@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
 // exact; H is then formed in 64 bits (< 2^53, host-checked) and converted
 // exactly.  A lane reads 16 bytes (4 bins) per corner, as the affine sweep.
 // ty < 0: chain order, map row -ty - 1 with the CTA's warps side by side.
-template <int SIM>
+template <int SIM, bool YOFF = false>
 __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, PeakPart* part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane & 1;
   const int u0 = ty < 0 ? tx * (kQuadThreads / 2) + warp * kSweepTileX + (lane >> 1)
@@ -184,7 +184,9 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
   const size_t ps8 = a.plane_stride * kOct;
   const uint64_t kx = (uint64_t)(a.hx + 1) * (a.hx + 1), ky = (uint64_t)(a.hy + 1) * (a.hy + 1);
   const uint64_t A = 2 * kx * ky;
-  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)(cy + a.y_off);
+  // global-row tables (carried bands) offset the centre row; a separate
+  // instantiation keeps the common path's registers (72, no extra spill)
+  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)(YOFF ? cy + a.y_off : cy);
 
   double s = 0.0, unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;
@@ -230,12 +232,12 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
   cta_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, part);
 }
 
-template <int SIM>
+template <int SIM, bool YOFF>
 __global__ void __launch_bounds__(kQuadThreads, SWG_QUAD_MINB) k_sweep_quad(const SweepArgs a) {
   int tx, ty;
   if (a.chain_s > 0) ty = -chain_row(a, tx) - 1;
   else sweep_tile(a.sc_tiles, tx, ty);
-  quad_body<SIM>(a, tx, ty, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  quad_body<SIM, YOFF>(a, tx, ty, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
 // Several quadratic maps of ONE table in one launch (a frame's scales):
@@ -616,8 +618,14 @@ cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s) {
 }
 
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s) {
-  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad<0><<<grid, kQuadThreads, 0, s>>>(a);
-  else k_sweep_quad<1><<<grid, kQuadThreads, 0, s>>>(a);
+  if (a.y_off) {
+    if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_quad<0, true><<<grid, kQuadThreads, 0, s>>>(a);
+    else k_sweep_quad<1, true><<<grid, kQuadThreads, 0, s>>>(a);
+  } else if (a.sim == SWG_SIM_BHATTACHARYYA) {
+    k_sweep_quad<0, false><<<grid, kQuadThreads, 0, s>>>(a);
+  } else {
+    k_sweep_quad<1, false><<<grid, kQuadThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

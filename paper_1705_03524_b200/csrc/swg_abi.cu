@@ -1880,7 +1880,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
              : zc[i]    ? zc[i]
                         : static_cast<double*>(S.scores.p) + plan[i].soff;
   PeakPart* parts0 = static_cast<PeakPart*>(S.parts.p);
-  bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti;
+  bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti && t->carry_y0 == 0;
   for (int i = 0; i < n && fused; ++i)
     fused = plan[i].engine == kQuad && plan[i].rows > 0 && !reqs[i].partial_in &&
             !reqs[i].partial_out && !copy_map(i) && plan[i].chain_s == 0 &&
