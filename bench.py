@@ -150,12 +150,22 @@ def workload(name, exp_decay="fixed"):
                 scaling="strong", groups=[dict(planes=swg.PLANES_PLAIN, scales=scales)])
 
 
+def manhattan_mass(k):
+    """Strict-window weight sum of the Manhattan kernel (kernel.cpp:68-75)."""
+    hx, hy = k.hx, k.hy
+    return k.kw * k.kh * (hx + hy + 1) - k.kh * hx * (hx + 1) - k.kw * hy * (hy + 1)
+
+
 def engine_of(group, k, method):
     """(sweep kernel, planes read, bytes per entry) the library picks
     (swg_abi.cu likelihood_maps engine choice)."""
     from paper_1705_03524_b200 import swg
     if group["planes"] == swg.PLANES_DECAY:
         return "k_sweep_exp", 4, 8
+    if (group["planes"] in (swg.PLANES_AFFINE, swg.PLANES_QUADRATIC) and
+            k.kind == swg.MANHATTAN and method in (swg.SWIH, swg.BRUTE) and
+            manhattan_mass(k) < 65536 and os.environ.get("SWG_AFFINE16", "1") != "0"):
+        return "k_sweep_affine16", 3, 2  # narrow {1, x, y} planes: H < 2^16
     if group["planes"] == swg.PLANES_QUADRATIC:
         if k.kind == swg.MANHATTAN:  # planes {1, x, y} of the quadratic set
             return "k_sweep_affine", 3, 4
@@ -175,12 +185,14 @@ def group_build_bytes(group, w, h, nbins):
     from paper_1705_03524_b200 import swg
     cells = (w + 1) * (h + 1) * nbins
     p = group["planes"]
+    narrow = cells * 3 * 2 if any(engine_of(group, k, m)[0] == "k_sweep_affine16"
+                                  for k, m, _, _ in group["scales"]) else 0
     if p == swg.PLANES_DECAY:
         return cells * 4 * 8
     if p == swg.PLANES_QUADRATIC:
-        return cells * 5 * 4
+        return cells * 5 * 4 + narrow
     if p == swg.PLANES_AFFINE:
-        return cells * 3 * 4
+        return cells * 3 * 4 + narrow
     b = cells * 2  # narrow 16-bit plain planes
     if any(engine_of(group, k, m)[0] == "k_sweep_cake" for k, m, _, _ in group["scales"]):
         b += cells * 4  # 32-bit plain planes for the large windows

@@ -612,7 +612,8 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const size_t smem = (size_t)threads * cpt * stage_chunks_per_record<T>() * 16;
   const unsigned grid = (unsigned)(a.nbands * a.groups);
-  const int kinds = sizeof(T) == 2 ? 1 : a.planes;  // narrow tables: plain only
+  // narrow tables: plain only, unless asked for (the 16-bit {1, x, y} planes)
+  const int kinds = a.kinds > 0 ? a.kinds : sizeof(T) == 2 ? 1 : a.planes;
   if (kinds > 1 && grid < 2u * 148u) {
     dim3 g3(grid, (unsigned)kinds);
     if (cpt == 4) {

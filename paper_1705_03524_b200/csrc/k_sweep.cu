@@ -161,6 +161,85 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
   sweep_peak(active && half == 0 ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
+// K2a16: the Manhattan sweep over NARROW (uint16) {1, x, y} planes, for
+// windows whose mass (the largest per-bin value H can take) is < 2^16: H is
+// a polynomial with integer coefficients in the box sums, so computing it
+// mod 2^16 from tables wrapped mod 2^16 gives H itself -- half the bytes of
+// the 32-bit sweep.  One lane per window, 8-byte half-record loads (4 bins;
+// a warp's corner load is 256 contiguous bytes), the half-octets' bins in
+// order, so the lane forms the ordered sums alone (no shuffles).
+template <int SIM>
+__global__ void __launch_bounds__(kAff16Threads) k_sweep_affine16(const SweepArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int tx, ty;
+  sweep_tile(a.sc_tiles, tx, ty);
+  const int u0 = tx * 32 + lane, r0 = ty * kAff16TileY + warp;
+  const bool active = u0 < a.mw && r0 < a.rows;
+  const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
+  const int v = a.row0 + r;
+  const int cx = u + a.hx, cy = v + a.hy;
+  const uint32_t centre = ((uint32_t)cy * (uint32_t)a.pitch + (uint32_t)cx) * kOct;
+  const size_t ps8 = a.plane_stride * kOct;
+  const uint32_t M = (uint32_t)(a.hx + a.hy + 1);
+  const uint32_t ucx = (uint32_t)cx, ucy = (uint32_t)(cy + a.y_off);
+  double s = 0.0;
+  const size_t widx = (size_t)r * a.mw + u;
+  if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
+  auto box = [](uint2 br, uint2 bl, uint2 tr, uint2 tl) {  // packed 16-bit fields
+    return make_uint2(__vsub2(__vadd2(br.x, tl.x), __vadd2(bl.x, tr.x)),
+                      __vsub2(__vadd2(br.y, tl.y), __vadd2(bl.y, tr.y)));
+  };
+  for (int g = 0; g < a.groups; ++g) {
+    const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint16_t*>(a.tab) +
+                                                  (size_t)g * a.planes * ps8 + centre);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      auto ld = [&](int q) { return __ldg(reinterpret_cast<const uint2*>(w + a.lat[q] + 8 * hf)); };
+      const uint2 p00 = ld(0), p10 = ld(1), p20 = ld(2), p01 = ld(3), p21 = ld(4);
+      const uint2 p02 = ld(5), p12 = ld(6), p22 = ld(7);
+      const uint2 n = box(p22, p02, p20, p00), nl = box(p12, p02, p10, p00);
+      const uint2 nt = box(p21, p01, p20, p00);
+      const uint2 q00 = ld(8), q10 = ld(9), q20 = ld(10), q02 = ld(11), q12 = ld(12), q22 = ld(13);
+      const uint2 xl = box(q12, q02, q10, q00), xa = box(q22, q02, q20, q00);
+      const uint2 w00 = ld(14), w20 = ld(15), w01 = ld(16), w21 = ld(17), w02 = ld(18), w22 = ld(19);
+      const uint2 yt = box(w21, w01, w20, w00), ya = box(w22, w02, w20, w00);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        auto f = [&](const uint2& pk) {
+          const uint32_t word = (k >> 1) ? pk.y : pk.x;
+          return (k & 1) ? word >> 16 : word & 0xFFFFu;
+        };
+        const uint32_t n_ = f(n), nl_ = f(nl), nt_ = f(nt), xl_ = f(xl), xa_ = f(xa);
+        const uint32_t yt_ = f(yt), ya_ = f(ya);
+        const uint32_t nr = n_ - nl_, nb = n_ - nt_, xr = xa_ - xl_, yb = ya_ - yt_;
+        const uint32_t raw =
+            (M * n_ + xl_ - xr + ucx * (nr - nl_) + yt_ - yb + ucy * (nb - nt_)) & 0xFFFFu;
+        if (raw != 0u) {  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
+          const double model = a.model[g * kOct + hf * 4 + k];
+          const double val = u2d(raw);
+          double term;
+          if (SIM == SWG_SIM_BHATTACHARYYA) {
+            term = __dsqrt_rn(__dmul_rn(model, val));
+          } else {
+            const double q = __ddiv_rn(val, a.mass);
+            term = (q < model) ? q : model;
+          }
+          s = __dadd_rn(s, term);
+        }
+      }
+    }
+  }
+  if (a.pout) {
+    if (active) a.pout[widx] = make_double2(s, a.mass);
+    s = -2.0;
+  } else {
+    if constexpr (SIM == SWG_SIM_BHATTACHARYYA) s = __ddiv_rn(s, __dsqrt_rn(a.mass));
+    s = clamp01(s);
+    if (active) a.scores[widx] = s;
+  }
+  sweep_peak(active ? s : -2.0, (long long)v * a.mw + u, a);
+}
+
 // K2q: declared Euclidean extension, w = A - ky*dx^2 - kx*dy^2 with
 // kx = (hx+1)^2, ky = (hy+1)^2, A = 2*kx*ky.  Over the whole window box,
 //   H = A*N - ky*Dxx - kx*Dyy,  Dxx = Sxx - 2cx*Sx + cx^2*N = sum (x-cx)^2
@@ -598,6 +677,12 @@ cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cud
     if (uniform) k_sweep_affine<1, true><<<grid, kSweepThreads, 0, s>>>(a);
     else k_sweep_affine<1, false><<<grid, kSweepThreads, 0, s>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_affine16(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+  if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_affine16<0><<<grid, kAff16Threads, 0, s>>>(a);
+  else k_sweep_affine16<1><<<grid, kAff16Threads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -285,6 +285,8 @@ struct swg_tables {
   uint16_t* t16 = nullptr;  // narrow plain planes (P = 1 tables): exact box
                             // counts for boxes of area < 2^16
   uint32_t* t32 = nullptr;  // primary for P = 3; on demand for P = 1
+  uint16_t* t16a = nullptr; // narrow {1, x, y} planes (3-plane layout) of P >= 3
+                            // tables, built on demand for windows of mass < 2^16
   uint64_t* t64 = nullptr;
   double* tdec = nullptr;    // decayed directional tables (EXP_L1), 4 planes
   double decay = 0.0;
@@ -409,6 +411,57 @@ swg_status ensure_t32(swg_tables* t) {
   }
   t->bytes += bytes;
   return run_build<uint32_t>(t, t->t32);
+}
+
+// The narrow {1, x, y} planes reuse the column sums the 32-bit build left in
+// t->lb when `fresh` is false (a rebuild runs them right after the 32-bit planes).
+swg_status build_t16a(swg_tables* t, bool fresh) {
+  swg_ctx* c = t->ctx;
+  BuildArgs a{};
+  a.fi = t->fi;
+  a.fi_pitch = t->fip;
+  a.out = t->t16a;
+  a.pitch = t->pitch;
+  a.plane_stride = t->ps;
+  a.w = t->w;
+  a.h = t->h;
+  a.bins = t->bins;
+  a.groups = t->groups;
+  a.planes = 3;  // the narrow set's own layout
+  a.kinds = 3;
+  a.band_h = t->band_h;
+  a.nbands = t->nbands;
+  a.wa = t->wa;
+  a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : 16;  // the carry layout of the column sums
+  a.agg = t->lb;
+  a.bin0 = t->bin0;
+  if (fresh && t->nbands > 1) {
+    BuildArgs ca = a;
+    ca.planes = t->planes;
+    CUDA_TRY(launch_colsum(ca, c->stream));
+    c->launches += 2;
+  }
+  int nl = 0;
+  CUDA_TRY(launch_build<uint16_t>(a, c->stream, &nl));
+  c->launches += (uint64_t)nl;
+  return SWG_OK;
+}
+
+swg_status ensure_t16a(swg_tables* t) {
+  if (t->t16a) return SWG_OK;
+  if (t->planes < 3 || t->tdec || !t->has_fi)
+    return fail(SWG_ERR, "tables: no narrow ramp planes");
+  const size_t bytes = t->ps * 3 * t->groups * kOct * 2;
+  cudaError_t e = cudaMalloc(&t->t16a, bytes);
+  if (e != cudaSuccess) {
+    t->t16a = nullptr;
+    cudaGetLastError();
+    g_required = bytes;
+    return fail(SWG_ERR_CAPACITY, "tables: 16-bit ramp planes need %zu bytes: %s", bytes,
+                cudaGetErrorString(e));
+  }
+  t->bytes += bytes;
+  return build_t16a(t, true);
 }
 
 swg_status ensure_t64(swg_tables* t) {
@@ -846,6 +899,7 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   t->carry_y0 = 0;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
+  if (t->t16a) ST_TRY(build_t16a(t, !t->t32));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   if (t->tdec) ST_TRY(run_build_decay(t));
   return SWG_OK;
@@ -865,6 +919,7 @@ swg_status swg_tables_rebuild_bins(swg_tables* t, const void* pixels, int is_dev
   t->bin0 = bin_begin;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
+  if (t->t16a) ST_TRY(build_t16a(t, !t->t32));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   if (t->tdec) ST_TRY(run_build_decay(t));
   return SWG_OK;
@@ -934,6 +989,7 @@ swg_status swg_tables_destroy(swg_tables* t) {
     cudaStreamSynchronize(t->ctx->stream);
     cudaFree(t->t16);
     cudaFree(t->t32);
+    cudaFree(t->t16a);
     cudaFree(t->t64);
     cudaFree(t->tdec);
     cudaFree(t->fflip);
@@ -1343,7 +1399,7 @@ swg_status swg_map_peak(swg_ctx* c, const double* scores, int mw, int mh, int hx
 namespace {
 
 // Sweep engine of one map request (plan_request).
-enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64 };
+enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64, kAffine16 };
 
 struct MapPlan {
   int row0 = 0, rows = 0, mw = 0;  // map rows [row0, row0 + rows) of width mw
@@ -1427,16 +1483,18 @@ swg_status validate_request(const swg_tables* t, const swg_map_request& r, bool 
 int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int hx, int hy) {
   size_t cell = 0;  // table bytes per pixel the engine reads
   if (e == kAffine32) cell = (size_t)t->groups * kOct * (k.kind == SWG_KERNEL_UNIFORM ? 1 : 3) * 4;
+  else if (e == kAffine16) cell = (size_t)t->groups * kOct * 3 * 2;
   else if (e == kQuad) cell = (size_t)t->groups * kOct * 5 * 4;
   else if (e == kExp64) cell = (size_t)t->groups * kOct * 4 * 8;
   else if (e == kCake32) cell = (size_t)t->groups * kOct * 4;
   if (!cell) return 0;
   const double budget = (double)SWG_L2_BUDGET_MB * 1048576.0;
   const double span =
-      2.0 * hy + 2 + (e == kExp64 ? kExpTileY : e == kQuad ? kQuadTileY : kSweepTileY);
+      2.0 * hy + 2 + (e == kExp64 ? kExpTileY : e == kQuad ? kQuadTileY
+                                               : e == kAffine16 ? kAff16TileY : kSweepTileY);
   if (span * (t->w + 1) * cell <= budget) return 0;
   const double sw = budget / (span * cell) - (2.0 * hx + 2);
-  const int tw = e == kExp64 ? kExpTileX : kSweepTileX;  // windows per tile
+  const int tw = e == kExp64 ? kExpTileX : e == kAffine16 ? 32 : kSweepTileX;  // windows per tile
   if (sw >= 2 * tw && (sw + 2.0 * hx + 2) / sw < 1.7) return std::max(1, (int)(sw / tw));
   return 0;
 }
@@ -1445,11 +1503,12 @@ int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int h
 dim3 sweep_grid(Engine e, int mw, int rows) {
   if (e == kBrute)
     return dim3((unsigned)((mw + kBruteThreads - 1) / kBruteThreads), (unsigned)std::max(rows, 1));
-  const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? 32 : kSweepTileX;
-  const int th = e == kExp64    ? kExpTileY
-                 : e == kCake16 ? kCakeTileY
-                 : e == kQuad   ? kQuadTileY
-                                : kSweepTileY;
+  const int tw = e == kExp64 ? kExpTileX : (e == kCake16 || e == kAffine16) ? 32 : kSweepTileX;
+  const int th = e == kExp64      ? kExpTileY
+                 : e == kCake16   ? kCakeTileY
+                 : e == kAffine16 ? kAff16TileY
+                 : e == kQuad     ? kQuadTileY
+                                  : kSweepTileY;
   return dim3((unsigned)((mw + tw - 1) / tw), (unsigned)std::max((rows + th - 1) / th, 1));
 }
 
@@ -1479,8 +1538,15 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
     e = t->t16 && (small || cake16_wide0(k, r)) ? kCake16 : kCake32;
   else if (k.kind == SWG_KERNEL_UNIFORM && t->t16 && small) e = kCake16;
   else e = kAffine32;
+  // Manhattan windows of mass < 2^16 on narrow {1, x, y} planes (k_sweep_affine16;
+  // SWG_AFFINE16=0 keeps the 32-bit sweep)
+  if (e == kAffine32 && k.kind == SWG_KERNEL_MANHATTAN && t->planes >= 3 && t->has_fi &&
+      !t->carried && affine_mass(k) < 65536) {
+    const char* env = std::getenv("SWG_AFFINE16");
+    if (!env || std::atoi(env)) e = kAffine16;
+  }
   if (r.partial_in || r.partial_out) {  // engines that can continue a bin-range chain
-    const bool closed_mass = e == kAffine32 || e == kQuad;
+    const bool closed_mass = e == kAffine32 || e == kQuad || e == kAffine16;
     if (e == kBrute || (!closed_mass && r.sim != SWG_SIM_BHATTACHARYYA))
       return fail(SWG_ERR_CONFIG,
                   "bin-range chains: Bhattacharyya, or intersection on swih Manhattan / "
@@ -1549,12 +1615,13 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
 // The kernel-independent sweep arguments of one request.
 void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r,
                      const MapPlan& p, double* scores, PeakPart* parts) {
-  a.tab = p.engine == kCake16 ? (const void*)t->t16
-          : p.engine == kExp64 ? (const void*)t->tdec
-                               : (const void*)t->t32;
+  a.tab = p.engine == kCake16     ? (const void*)t->t16
+          : p.engine == kExp64    ? (const void*)t->tdec
+          : p.engine == kAffine16 ? (const void*)t->t16a
+                                  : (const void*)t->t32;
   a.plane_stride = t->ps;
   a.pitch = t->pitch;
-  a.planes = t->planes;
+  a.planes = p.engine == kAffine16 ? 3 : t->planes;
   a.bins = t->bins;
   a.groups = t->groups;
   a.hx = k_hx(p.k);
@@ -1699,6 +1766,24 @@ swg_status run_affine(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaS
   return SWG_OK;
 }
 
+// 16-bit Manhattan: the same corner points on the narrow {1, x, y} planes
+// (16-byte records of 8 uint16 bins, 3-plane layout).
+swg_status run_affine16(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
+  a.mass = (double)affine_mass(p.k);
+  const long long p8 = (long long)t->pitch * kOct, ps8 = (long long)t->ps * kOct;
+  const long long xs[3] = {-a.hx, 1, a.hx + 1}, ys[3] = {-a.hy, 1, a.hy + 1};
+  auto off = [&](int plane, int xi, int yi) {
+    return (int)(2 * (plane * ps8 + ys[yi] * p8 + xs[xi] * kOct));
+  };
+  const int pts[20][3] = {{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, 1}, {0, 2, 1},
+                          {0, 0, 2}, {0, 1, 2}, {0, 2, 2}, {1, 0, 0}, {1, 1, 0},
+                          {1, 2, 0}, {1, 0, 2}, {1, 1, 2}, {1, 2, 2}, {2, 0, 0},
+                          {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
+  for (int q = 0; q < 20; ++q) a.lat[q] = off(pts[q][0], pts[q][1], pts[q][2]);
+  CUDA_TRY(launch_sweep_affine16(a, p.grid, st));
+  return SWG_OK;
+}
+
 // Cake (or a Uniform box as a one-ring cake): ring corner byte offsets from
 // the centre record and the ring coefficients.
 swg_status run_cake(const swg_tables* t, const swg_map_request& r, const MapPlan& p,
@@ -1838,6 +1923,8 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   // the lazily built 32-bit planes go on the main stream before the fan-out
   for (const MapPlan& p : plan)
     if (p.rows > 0 && (p.engine == kAffine32 || p.engine == kCake32)) ST_TRY(ensure_t32(t));
+  for (const MapPlan& p : plan)
+    if (p.rows > 0 && p.engine == kAffine16) ST_TRY(ensure_t16a(t));
 
   bool host_maps = false;  // maps that still need a device-to-host copy
   for (int i = 0; i < n; ++i) host_maps |= copy_map(i);
@@ -1932,6 +2019,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       fill_sweep_args(a, t, r, q, sc, pp);
       if (q.engine == kQuad) ST_TRY(run_quad(t, q, a, st));
       else if (q.engine == kAffine32) ST_TRY(run_affine(t, q, a, st));
+      else if (q.engine == kAffine16) ST_TRY(run_affine16(t, q, a, st));
       else if (q.engine == kBrute) ST_TRY(run_brute(c, t, q, a, st));
       else ST_TRY(run_cake(t, r, q, a, st));
       c->launches += 1;

@@ -64,6 +64,7 @@ struct BuildArgs {
   size_t wa;           // padded width (columns) of the carry array
   int aw;              // carry words per column: 8 (plain), 16 (ramps), 24 (quadratic)
   int bin0;            // global bin of local bin 0 (bin-range tables)
+  int kinds;           // table kinds to build (0: every plane; narrow tables: plain)
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
                        // then of all rows above the band (K1b, exclusive scan)
@@ -313,6 +314,12 @@ constexpr int kSweepTileX = 16;
 #define SWG_QUADM_MINB 8  // the multi-map launch: 64 registers (72: config 3 +2 %)
 #endif
 constexpr int kQuadTileY = SWG_QUAD_TY, kQuadThreads = 32 * kQuadTileY;
+// 16-bit affine sweep (windows of mass < 2^16): one lane per window, CTAs
+// of 32 windows x kAff16TileY map rows.
+#ifndef SWG_AFF16_TY
+#define SWG_AFF16_TY 4
+#endif
+constexpr int kAff16TileY = SWG_AFF16_TY, kAff16Threads = 32 * kAff16TileY;
 // Exponential sweep CTA tile: kExpWarpsX warps side by side on one map row
 // (32 windows each), kExpThreads / 32 / kExpWarpsX rows: 128 x 1 windows
 // (measured: 128 x 2 +3 % on config 4 and +7 % on config 5's exponential
@@ -346,6 +353,7 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s);
 template <typename T>
 cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
+cudaError_t launch_sweep_affine16(const SweepArgs& a, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);

@@ -80,7 +80,11 @@ def test_workloads_and_engines():
     assert kinds == [[swg.MANHATTAN] * 8 + [swg.EUCLID_QUAD] * 8, [swg.GAUSS_CHEB] * 8,
                      [swg.EXP_L1] * 8]
     quad = c5["groups"][0]
-    assert bench.engine_of(quad, quad["scales"][0][0], swg.SWIH) == ("k_sweep_affine", 3, 4)
+    # Manhattan windows of mass < 2^16 (17, 25, 37) on the narrow 16-bit planes
+    assert [bench.engine_of(quad, k, m)[0] for k, m, _, _ in quad["scales"][:8]] == \
+        ["k_sweep_affine16"] * 3 + ["k_sweep_affine"] * 5
+    assert bench.manhattan_mass(swg.Kernel(swg.MANHATTAN, 49, 49)) < 65536 <= \
+        bench.manhattan_mass(swg.Kernel(swg.MANHATTAN, 51, 51))
     assert bench.engine_of(quad, quad["scales"][8][0], swg.SWIH) == ("k_sweep_quad", 5, 4)
     # 257x257 Gaussian: ring 0's box exceeds 16-bit counts, but ring 1's box
     # and ring 0's frame do not -> still the 16-bit sweep (wide ring 0)
