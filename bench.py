@@ -156,15 +156,16 @@ def manhattan_mass(k):
     return k.kw * k.kh * (hx + hy + 1) - k.kh * hx * (hx + 1) - k.kw * hy * (hy + 1)
 
 
-def engine_of(group, k, method):
+def engine_of(group, k, method, windows=1 << 30):
     """(sweep kernel, planes read, bytes per entry) the library picks
-    (swg_abi.cu likelihood_maps engine choice)."""
+    (swg_abi.cu likelihood_maps engine choice) for a map of `windows`."""
     from paper_1705_03524_b200 import swg
     if group["planes"] == swg.PLANES_DECAY:
         return "k_sweep_exp", 4, 8
     if (group["planes"] in (swg.PLANES_AFFINE, swg.PLANES_QUADRATIC) and
             k.kind == swg.MANHATTAN and method in (swg.SWIH, swg.BRUTE) and
-            manhattan_mass(k) < 65536 and os.environ.get("SWG_AFFINE16", "1") != "0"):
+            manhattan_mass(k) < 65536 and windows >= 1 << 20 and
+            os.environ.get("SWG_AFFINE16", "1") != "0"):
         return "k_sweep_affine16", 3, 2  # narrow {1, x, y} planes: H < 2^16
     if group["planes"] == swg.PLANES_QUADRATIC:
         if k.kind == swg.MANHATTAN:  # planes {1, x, y} of the quadratic set
@@ -185,8 +186,9 @@ def group_build_bytes(group, w, h, nbins):
     from paper_1705_03524_b200 import swg
     cells = (w + 1) * (h + 1) * nbins
     p = group["planes"]
-    narrow = cells * 3 * 2 if any(engine_of(group, k, m)[0] == "k_sweep_affine16"
-                                  for k, m, _, _ in group["scales"]) else 0
+    narrow = cells * 3 * 2 if any(
+        engine_of(group, k, m, (w - k.kw + 1) * (h - k.kh + 1))[0] == "k_sweep_affine16"
+        for k, m, _, _ in group["scales"]) else 0
     if p == swg.PLANES_DECAY:
         return cells * 4 * 8
     if p == swg.PLANES_QUADRATIC:
@@ -205,7 +207,7 @@ def est_request_ms(group, k, method, rings, rows, w, h, nbins):
     of algorithmic bytes, the cake at ~9.4e-9 ms per window-ring at 64 bins)."""
     from paper_1705_03524_b200 import swg
     mw = w - k.kw + 1
-    kname, P, e = engine_of(group, k, method)
+    kname, P, e = engine_of(group, k, method, (w - k.kw + 1) * (h - k.kh + 1))
     tab = min(h + 1, rows + k.kh) * (w + 1) * nbins * P * e
     if kname in ("k_sweep_cake16", "k_sweep_cake"):
         return 0.05 + 9.4e-9 * rows * mw * rings * nbins / 64 * (2 if kname == "k_sweep_cake" else 1)
@@ -1098,7 +1100,7 @@ class OursArm:
             u = self.units[ui]
             g = wl["groups"][u["g"]]
             k, meth = g["scales"][u["sidx"][i]][:2]
-            kname, P, e = engine_of(g, k, meth)
+            kname, P, e = engine_of(g, k, meth, (self.tab_w - k.kw + 1) * (self.tab_h - k.kh + 1))
             bins = u.get("bins_per_launch", self.nb)
             r = u["reqs"][i]
             rows = r.rows[1] - r.rows[0] if r.rows else self.tab_h - k.kh + 1

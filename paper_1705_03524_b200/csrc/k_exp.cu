@@ -249,25 +249,40 @@ __global__ void __launch_bounds__(128) k_rescore(const SweepArgs a, const Rescor
 // with the critical path the most populous bin's pixel count instead of the
 // whole window (config 5 257^2: one candidate 240 -> ~40 us).
 constexpr int kRsWarps = 8;
+// The window's bins are first staged in shared memory (8-bit when the
+// histogram has <= 256 bins) so the two sorting passes run from shared
+// memory, and the weight of pixel (dx, dy) -- the declared exponential
+// kernel's d^(|dx|+|dy|), a function of the L1 distance n alone -- comes from
+// a shared table ltab[n] holding the host grid's own values (bit-identical).
 __global__ void __launch_bounds__(32 * kRsWarps) k_rescore_sorted(const SweepArgs a,
                                                                  const RescoreArgs r,
                                                                  const swg_peak* fast) {
   extern __shared__ __align__(16) unsigned char s_mem[];
-  const int bins = r.bins, kw = r.kw, kh = r.kh;
-  double* h = reinterpret_cast<double*>(s_mem);                     // [bins]
-  int* off = reinterpret_cast<int*>(h + bins);                       // [kRsWarps][bins]
-  uint16_t* pos = reinterpret_cast<uint16_t*>(off + kRsWarps * bins);  // [kw * kh]
+  const int bins = r.bins, kw = r.kw, kh = r.kh, hx = (kw - 1) / 2, hy = (kh - 1) / 2;
+  const int npx = kw * kh, nl = hx + hy + 1;
+  const bool narrow = bins <= 256;
+  double* h = reinterpret_cast<double*>(s_mem);                          // [bins]
+  double* ltab = h + bins;                                                // [nl]
+  int* off = reinterpret_cast<int*>(ltab + nl);                           // [kRsWarps][bins]
+  uint16_t* pos = reinterpret_cast<uint16_t*>(off + kRsWarps * bins);     // [npx]
+  unsigned char* stage = reinterpret_cast<unsigned char*>(pos + npx);     // [npx] u8 / u16
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = (kh + kRsWarps - 1) / kRsWarps;  // rows per warp's block
   const int rb0 = warp * R, rb1 = min(kh, rb0 + R);
   const int segs = (kw + 31) >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  // the distance table: row hy of the grid for n <= hx, column kw-1 beyond
+  for (int n = threadIdx.x; n < nl; n += blockDim.x)
+    ltab[n] = n <= hx ? r.grid[(size_t)hy * kw + hx + n] : r.grid[(size_t)(hy + n - hx) * kw + kw - 1];
   const int cnt = *r.count;
   const bool overflow = cnt > r.cap;
   const double lim = fast->score - r.eps;
   const long long total = overflow ? (long long)a.rows * a.mw : cnt;
   double best = -2.0;
   long long bidx = 0x7FFFFFFFFFFFFFFFLL;
+  auto bin_at = [&](int i) -> int {
+    return narrow ? (int)stage[i] : (int)reinterpret_cast<const uint16_t*>(stage)[i];
+  };
   for (long long c = blockIdx.x; c < total; c += gridDim.x) {
     long long idx;
     if (overflow) {
@@ -278,14 +293,21 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore_sorted(const SweepArg
     }
     const int u = (int)(idx % a.mw), v = (int)(idx / a.mw);
     const uint16_t* fi = r.fi + (size_t)v * r.fi_pitch + u;
+    // stage the window's bins (all loads in flight across the CTA)
+    for (int y = warp; y < kh; y += kRsWarps)
+      for (int x = lane; x < kw; x += 32) {
+        const uint16_t bv = __ldg(fi + (size_t)y * r.fi_pitch + x);
+        if (narrow) stage[y * kw + x] = (unsigned char)(bv < bins ? bv : 255);
+        else reinterpret_cast<uint16_t*>(stage)[y * kw + x] = bv;
+      }
     int* mine = off + warp * bins;
     for (int b = lane; b < bins; b += 32) mine[b] = 0;
-    __syncwarp();
+    __syncthreads();
     // count: this warp's rows, 32 pixels at a time
     for (int y = rb0; y < rb1; ++y)
       for (int sgi = 0; sgi < segs; ++sgi) {
         const int dx = sgi * 32 + lane;
-        const int bl = dx < kw ? __ldg(fi + (size_t)y * r.fi_pitch + dx) : 0xFFFF;
+        const int bl = dx < kw ? bin_at(y * kw + dx) : 0xFFFF;
         const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
         if (bl < bins && (grp & lt) == 0) mine[bl] += __popc(grp);
         __syncwarp();
@@ -293,7 +315,7 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore_sorted(const SweepArg
     __syncthreads();
     // offsets: bin-major, then row block (bin b's pixels contiguous in pixel order)
     if (threadIdx.x < 32) {
-      int run = 0;  // running total over bins (chunks of 32 bins)
+      int run = 0;
       for (int b0 = 0; b0 < bins; b0 += 32) {
         const int b = b0 + lane;
         int tot = 0;
@@ -317,44 +339,37 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore_sorted(const SweepArg
       }
     }
     __syncthreads();
-    // scatter: stable ranks within each segment, segments in pixel order
+    // scatter: stable ranks within each segment, segments in pixel order;
+    // a position code is the pixel's L1 distance from the centre (its weight)
     for (int y = rb0; y < rb1; ++y)
       for (int sgi = 0; sgi < segs; ++sgi) {
         const int dx = sgi * 32 + lane;
-        const int bl = dx < kw ? __ldg(fi + (size_t)y * r.fi_pitch + dx) : 0xFFFF;
+        const int bl = dx < kw ? bin_at(y * kw + dx) : 0xFFFF;
         const unsigned grp = __match_any_sync(0xFFFFFFFFu, bl);
         const int base = bl < bins ? mine[bl] : 0;
         __syncwarp();
         if (bl < bins) {
-          pos[base + __popc(grp & lt)] = (uint16_t)(((y - rb0) << 9) | dx);
+          pos[base + __popc(grp & lt)] = (uint16_t)(abs(dx - hx) + abs(y - hy));
           if ((grp & lt) == 0) mine[bl] = base + __popc(grp);
         }
         __syncwarp();
       }
     __syncthreads();
-    // per bin: its weights in pixel order (mine[] now holds each (block, bin)
-    // segment's END; bin b's list starts where bin b-1's last block ended)
+    // per bin: its weights in pixel order (bin b's list ends where
+    // mine[last block][b] points; it starts where bin b-1's ended)
     for (int b = threadIdx.x; b < bins; b += blockDim.x) {
       double t = 0.0;
       int k = b > 0 ? off[(kRsWarps - 1) * bins + b - 1] : 0;
-      for (int w = 0; w < kRsWarps; ++w) {
-        const int end = off[w * bins + b];
-        const double* gw = r.grid + (size_t)(w * R) * kw;
-        for (; k + 4 <= end; k += 4) {
-          double wt[4];
+      const int end = off[(kRsWarps - 1) * bins + b];
+      constexpr int kU = 8;  // weights of the next 8 pixels loaded ahead of their adds
+      for (; k + kU <= end; k += kU) {
+        double wt[kU];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int code = pos[k + q];
-            wt[q] = __ldg(gw + (code >> 9) * kw + (code & 511));
-          }
+        for (int q = 0; q < kU; ++q) wt[q] = ltab[pos[k + q]];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) t = __dadd_rn(t, wt[q]);
-        }
-        for (; k < end; ++k) {
-          const int code = pos[k];
-          t = __dadd_rn(t, __ldg(gw + (code >> 9) * kw + (code & 511)));
-        }
+        for (int q = 0; q < kU; ++q) t = __dadd_rn(t, wt[q]);
       }
+      for (; k < end; ++k) t = __dadd_rn(t, ltab[pos[k]]);
       h[b] = t;
     }
     __syncthreads();
@@ -431,11 +446,12 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
       a.scores, n, a.row0, a.mw, peak, r.eps, r.cap, r.count, r.cand);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)r.bins * 8 + (size_t)kRsWarps * r.bins * 4 +
-                      round_up((size_t)r.kw * r.kh * 2, 16);
-  const int R = (r.kh + kRsWarps - 1) / kRsWarps;
+  const size_t npx = (size_t)r.kw * r.kh;
+  const size_t smem = (size_t)r.bins * 8 + (size_t)((r.kw - 1) / 2 + (r.kh - 1) / 2 + 1) * 8 +
+                      (size_t)kRsWarps * r.bins * 4 + npx * 2 + npx * (r.bins <= 256 ? 1 : 2);
   const char* rw = std::getenv("SWG_RESCORE_WARP");  // A/B: 1 = the per-warp kernel
-  if (!(rw && std::atoi(rw)) && r.kw <= 512 && R <= 127 && smem <= (200u << 10)) {
+  // pixel codes are 16-bit L1 distances; the window's bins and codes fit in shared memory
+  if (!(rw && std::atoi(rw)) && r.kw + r.kh <= 65536 && smem <= (220u << 10)) {
     // bin-sorted re-score: one CTA per candidate, persistent over them
     cudaFuncSetAttribute(k_rescore_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);

@@ -1540,8 +1540,10 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
   else e = kAffine32;
   // Manhattan windows of mass < 2^16 on narrow {1, x, y} planes (k_sweep_affine16;
   // SWG_AFFINE16=0 keeps the 32-bit sweep)
+  // (large maps only: for a small frame the extra narrow build costs more than
+  // the sweep saves -- config 1, 50k windows: 0.033 -> 0.051 ms per step)
   if (e == kAffine32 && k.kind == SWG_KERNEL_MANHATTAN && t->planes >= 3 && t->has_fi &&
-      !t->carried && affine_mass(k) < 65536) {
+      !t->carried && affine_mass(k) < 65536 && (int64_t)p.rows * p.mw >= (int64_t(1) << 20)) {
     const char* env = std::getenv("SWG_AFFINE16");
     if (!env || std::atoi(env)) e = kAffine16;
   }

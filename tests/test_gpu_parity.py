@@ -1131,35 +1131,40 @@ def test_device_boundary_row_exchange(ctx, oracle, planes):
 
 @pytest.mark.parametrize("kw,kh", [(3, 3), (9, 7), (17, 17), (37, 37), (49, 45), (1, 11)])
 def test_affine16_manhattan_exact(ctx, oracle, kw, kh):
-    """Manhattan windows of mass < 2^16 sweep the narrow 16-bit {1, x, y}
-    planes (k_sweep_affine16): maps and peaks identical to the oracle and to
-    the 32-bit sweep (SWG_AFFINE16=0), on affine and quadratic table sets,
-    both similarities, full maps and row ranges."""
+    """Manhattan windows of mass < 2^16 on maps of >= 2^20 windows sweep the
+    narrow 16-bit {1, x, y} planes (k_sweep_affine16): maps and peaks
+    identical to the oracle and to the 32-bit sweep (SWG_AFFINE16=0), on
+    affine and quadratic table sets, both similarities, full maps and row
+    ranges, and after a rebuild."""
     import os
-    img = oracle.random_gray(173, 121, 5 + kw)
+    w, h = 1200, 1000
+    img = oracle.random_gray(w, h, 5 + kw)
+    img = ((img.astype(np.uint16) + np.roll(img, 1, 1) + np.roll(img, 1, 0)) // 3).astype(np.uint8)
     bins = 16
     fi = oracle.quantize_gray8(img, bins)
     k = K(swg.MANHATTAN, kw, kh)
     ok = O.kernel(O.MANHATTAN, kw, kh)
     mdl = oracle.target_model(fi[30:30 + kh, 40:40 + kw].copy(), bins, ok)
+    assert (w - kw + 1) * (h - kh + 1) >= 1 << 20
     for planes in (swg.PLANES_AFFINE, swg.PLANES_QUADRATIC):
         t = ctx.build(img, swg.FMT_GRAY8, bins, planes)
         for sim in (swg.BHATTACHARYYA, swg.INTERSECTION):
-            want = oracle.likelihood_map(fi, bins, mdl, ok, O.SWIH, sim)
+            want, wpk, _ = oracle.fast_map(fi, bins, mdl, ok, O.SWIH, sim)
             got, pk = t.likelihood_map(k, mdl, swg.SWIH, sim)
             assert (got == want).all()
-            assert pk == oracle.peak(want, k.hx, k.hy)
+            assert pk == wpk
             os.environ["SWG_AFFINE16"] = "0"
             try:
                 g32, p32 = t.likelihood_map(k, mdl, swg.SWIH, sim)
             finally:
                 del os.environ["SWG_AFFINE16"]
             assert (g32 == got).all() and p32 == pk
-        rows = (5, min(60, 121 - kh + 1))
+        wantb, _, _ = oracle.fast_map(fi, bins, mdl, ok, O.SWIH, O.BHATTACHARYYA)
+        rows = (5, 900)
         part, _ = t.likelihood_maps([swg.MapRequest(k, mdl, rows=rows)])
-        wantb = oracle.likelihood_map(fi, bins, mdl, ok, O.SWIH, O.BHATTACHARYYA)
         assert (part[0] == wantb[rows[0]:rows[1]]).all()
         t.rebuild(np.ascontiguousarray(img[::-1]))  # rebuild refreshes the narrow planes
-        want2 = oracle.likelihood_map(np.ascontiguousarray(fi[::-1]), bins, mdl, ok)
+        want2, _, _ = oracle.fast_map(np.ascontiguousarray(fi[::-1]), bins, mdl, ok)
         got2, _ = t.likelihood_map(k, mdl)
         assert (got2 == want2).all()
+        t.close()
