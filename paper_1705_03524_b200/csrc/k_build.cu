@@ -301,6 +301,13 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
 #pragma unroll
       for (int i = 0; i < CPT; ++i) store_zero_record<T>(plane + (size_t)(xb + 1 + i) * kOct);
     if (tid == 0) store_zero_record<T>(plane);
+    if (sizeof(T) == 4 && KIND <= 2 && g.out16) {
+      uint16_t* p16 = static_cast<uint16_t*>(g.out16) + ((size_t)grp * 3 + KIND) * g.plane_stride * kOct;
+      if (live)
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) store_zero_record<uint16_t>(p16 + (size_t)(xb + 1 + i) * kOct);
+      if (tid == 0) store_zero_record<uint16_t>(p16);
+    }
   }
 
   // ---- rows of the band (next row's bins prefetched under this row's scan)
@@ -401,6 +408,33 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
         if (wrec0 + c / NQ < g.w) dst[c] = st[swz(c)];
       }
       __syncwarp();
+      if constexpr (sizeof(T) == 4 && KIND <= 2) {
+        // the narrow {1, x, y} planes (low 16 bits, 3-plane layout) from the
+        // same values: one more staged pass of 16-byte records
+        if (g.out16) {
+          uint16_t* row16 = static_cast<uint16_t*>(g.out16) +
+                            (((size_t)grp * 3 + KIND) * g.plane_stride + (size_t)(y + 1) * g.pitch) *
+                                kOct;
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const T* v = t[i];
+            st[swz(lane * CPT + i)] =
+                make_uint4((uint32_t)(v[0] & 0xFFFFu) | (uint32_t)v[1] << 16,
+                           (uint32_t)(v[2] & 0xFFFFu) | (uint32_t)v[3] << 16,
+                           (uint32_t)(v[4] & 0xFFFFu) | (uint32_t)v[5] << 16,
+                           (uint32_t)(v[6] & 0xFFFFu) | (uint32_t)v[7] << 16);
+          }
+          __syncwarp();
+          uint4* dst16 = reinterpret_cast<uint4*>(row16) + (size_t)(wrec0 + 1);
+#pragma unroll
+          for (int m = 0; m < CPT; ++m) {
+            const int c = m * 32 + lane;
+            if (wrec0 + c < g.w) dst16[c] = st[swz(c)];
+          }
+          __syncwarp();
+          if (tid == 0) reinterpret_cast<uint4*>(row16)[0] = make_uint4(0, 0, 0, 0);
+        }
+      }
     } else {
       if (live)
 #pragma unroll

@@ -150,10 +150,10 @@ __global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nband
 // out as 512-byte warp stores.  Two block barriers per 16 rows instead of a
 // block-wide scan and barrier per row.
 #ifndef SWG_STRIP_ROWS
-#define SWG_STRIP_ROWS 16
+#define SWG_STRIP_ROWS 8  // 8-row blocks at 4 CTAs per SM: config 5 decayed set 2.82 -> 2.74 ms (16 rows at 3)
 #endif
 #ifndef SWG_STRIP_MINB
-#define SWG_STRIP_MINB 3
+#define SWG_STRIP_MINB 4
 #endif
 constexpr int kStripW = 256, kStripRows = SWG_STRIP_ROWS;
 

@@ -359,6 +359,8 @@ swg_status run_build(swg_tables* t, T* out) {
   a.aw = t->planes == SWG_PLANES_QUADRATIC ? 24 : t->planes == SWG_PLANES_PLAIN ? 8 : 16;
   a.agg = t->lb;
   a.bin0 = t->bin0;
+  // the 32-bit build writes the narrow ramp planes too (their low 16 bits)
+  if (sizeof(T) == 4 && static_cast<void*>(out) == static_cast<void*>(t->t32)) a.out16 = t->t16a;
   if (t->nbands > 1) {
     CUDA_TRY(launch_colsum(a, c->stream));
     c->launches += 2;
@@ -898,8 +900,8 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   t->carried = false;
   t->carry_y0 = 0;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
-  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
-  if (t->t16a) ST_TRY(build_t16a(t, !t->t32));
+  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));  // (+ the narrow ramp planes)
+  if (t->t16a && !t->t32) ST_TRY(build_t16a(t, true));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   if (t->tdec) ST_TRY(run_build_decay(t));
   return SWG_OK;
@@ -918,8 +920,8 @@ swg_status swg_tables_rebuild_bins(swg_tables* t, const void* pixels, int is_dev
   if (pixels) ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
   t->bin0 = bin_begin;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
-  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
-  if (t->t16a) ST_TRY(build_t16a(t, !t->t32));
+  if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));  // (+ the narrow ramp planes)
+  if (t->t16a && !t->t32) ST_TRY(build_t16a(t, true));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   if (t->tdec) ST_TRY(run_build_decay(t));
   return SWG_OK;
@@ -1947,6 +1949,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     wj = c->hjoin;
   } else {
     nwork = std::min(n, (int)swg_ctx::kWorkers);
+    if (const char* ew = std::getenv("SWG_WORKERS")) nwork = std::min(nwork, std::max(1, std::atoi(ew)));
     if (n <= swg_ctx::kHostFan) {  // a few requests: costliest first on the highest priority
       wk = c->hwork;              // (config 2: e2e 1.19 -> 1.17 ms with mapped host maps,
       wj = c->hjoin;              // device-resident 1.114 -> 1.116 ms)

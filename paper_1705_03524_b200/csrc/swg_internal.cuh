@@ -65,6 +65,8 @@ struct BuildArgs {
   int aw;              // carry words per column: 8 (plain), 16 (ramps), 24 (quadratic)
   int bin0;            // global bin of local bin 0 (bin-range tables)
   int kinds;           // table kinds to build (0: every plane; narrow tables: plain)
+  void* out16;         // 32-bit builds: also write kinds 0-2 mod 2^16 here (narrow
+                       // {1, x, y} planes, 3-plane layout), or null
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
                        // then of all rows above the band (K1b, exclusive scan)
