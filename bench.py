@@ -181,14 +181,17 @@ def engine_of(group, k, method, windows=1 << 30):
     return "k_sweep_affine", 3, 4
 
 
-def group_build_bytes(group, w, h, nbins):
-    """Plane bytes one rebuild writes (every plane set the tables hold)."""
+def group_build_bytes(group, w, h, nbins, narrow=None):
+    """Plane bytes one rebuild writes (every plane set the tables hold);
+    `narrow`: whether the tables hold the 16-bit {1, x, y} planes (None:
+    estimate from the kernels)."""
     from paper_1705_03524_b200 import swg
     cells = (w + 1) * (h + 1) * nbins
     p = group["planes"]
-    narrow = cells * 3 * 2 if any(
-        engine_of(group, k, m, (w - k.kw + 1) * (h - k.kh + 1))[0] == "k_sweep_affine16"
-        for k, m, _, _ in group["scales"]) else 0
+    if narrow is None:
+        narrow = any(engine_of(group, k, m, (w - k.kw + 1) * (h - k.kh + 1))[0] ==
+                     "k_sweep_affine16" for k, m, _, _ in group["scales"])
+    narrow = cells * 3 * 2 if narrow else 0
     if p == swg.PLANES_DECAY:
         return cells * 4 * 8
     if p == swg.PLANES_QUADRATIC:
@@ -1086,6 +1089,29 @@ class OursArm:
                     return tr
         return None
 
+    def _plan(self, u, i):
+        """swg_request_plan of request i of unit u; a bin-range walk (config 4)
+        asks about its last range and averages the bins read per range with
+        the library's rule (records of the model's nonzero bins: pairs for the
+        exponential sweep, octets for the integer stream sweeps)."""
+        chunks = u.get("chunks") or []
+        if len(chunks) <= 1:
+            return u["t"].request_plan(u["reqs"][i])
+        import numpy as np
+        from paper_1705_03524_b200 import dist as D
+        pl = dict(u["t"].request_plan(chunks[-1][1][i]))
+        grp = {"k_sweep_exp": 2, "k_stream_affine": 8, "k_stream_affine16": 8,
+               "k_stream_quad": 8}.get(pl["kernel"])
+        if grp and os.environ.get("SWG_SPARSE", "1") != "0":
+            m = np.asarray(u["reqs"][i].model)
+            per = []
+            for b0, b1 in D.bin_ranges(self.nb, len(chunks)):
+                nz = m[b0:b1] != 0
+                per.append(sum(min(grp, b1 - g) for g in range(b0, b1, grp)
+                               if nz[g - b0:g - b0 + grp].any()))
+            pl["bins_read"] = sum(per) / len(per)
+        return pl
+
     def kernel_table(self, build_ms, sweep_ms):
         """Per kernel function: launches, ms and algorithmic bytes per step
         (the table rows a launch's windows read, each once, + 8 B
@@ -1100,9 +1126,13 @@ class OursArm:
             u = self.units[ui]
             g = wl["groups"][u["g"]]
             k, meth = g["scales"][u["sidx"][i]][:2]
-            kname, P, e = engine_of(g, k, meth, (self.tab_w - k.kw + 1) * (self.tab_h - k.kh + 1))
-            bins = u.get("bins_per_launch", self.nb)
             r = u["reqs"][i]
+            # the library's own report of what it runs (swg_request_plan):
+            # kernel, planes, entry bytes and the bins whose records it reads
+            # (a model's zero bins are skipped by the closed-form-mass sweeps)
+            pl = self._plan(u, i)
+            kname, P, e = pl["kernel"], pl["planes"], pl["entry_bytes"]
+            bins = pl["bins_read"]
             rows = r.rows[1] - r.rows[0] if r.rows else self.tab_h - k.kh + 1
             mw = self.tab_w - k.kw + 1
             win = rows * mw
@@ -1120,8 +1150,10 @@ class OursArm:
         if build_ms:
             bms = sum(build_ms) / steps
             in_bytes = sum(u["h2d"] for u in self.units)
-            bb = in_bytes + sum(group_build_bytes(wl["groups"][u["g"]], self.tab_w, self.tab_h,
-                                                  self.nb) for u in self.units)
+            bb = in_bytes + sum(group_build_bytes(
+                wl["groups"][u["g"]], self.tab_w, self.tab_h, self.nb,
+                narrow=any(self._plan(u, i)["kernel"].endswith("affine16")
+                           for i in range(len(u["reqs"])))) for u in self.units)
             kt["ih_build"] = {"launches_per_step": len(build_ms) // steps, "ms_per_step": bms,
                               "bytes_per_step": int(bb), "launches": [],
                               "kernels": "k_quantize + k_colsum + k_bandscan + k_build / "

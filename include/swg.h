@@ -346,6 +346,20 @@ swg_status swg_likelihood_maps(swg_tables* t, int n,
                                double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev);
 
+/* What swg_likelihood_maps would run for one request (measurement and
+ * tests; no device work): the sweep kernel's name, the table planes it reads,
+ * bytes per table entry, and how many bins' records it reads (a model's zero
+ * bins are skipped by the sweeps whose window mass is closed-form: affine,
+ * quadratic, exponential; SWG_SPARSE=0 reads every bin), and its CTA count. */
+typedef struct swg_plan_info {
+  char kernel[32];
+  int planes;
+  int entry_bytes;
+  int bins_read;
+  int ctas;
+} swg_plan_info;
+swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_plan_info* out);
+
 /* Batch of frames of the tables' geometry (tracking sequences, config 3):
  * for each frame f, rebuild the tables from frames[f] (pitch_bytes, host or
  * device as is_device; a search-region crop is a pointer into the full frame

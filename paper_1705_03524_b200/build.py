@@ -20,7 +20,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libswg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["swg_abi.cu", "k_build.cu", "k_sweep.cu", "k_brute.cu", "k_decay.cu", "k_exp.cu"]
+SOURCES = ["swg_abi.cu", "k_build.cu", "k_sweep.cu", "k_stream.cu", "k_brute.cu", "k_decay.cu", "k_exp.cu"]
 HEADERS = ["swg_internal.cuh"]
 
 NVCC_FLAGS = [

@@ -94,7 +94,30 @@ __global__ void __launch_bounds__(kExpThreads, SWG_EXP_MINB) k_sweep_exp(const S
     s = a.pin[widx].x;
     mass = a.pin[widx].y;
   }
-  if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
+  if (e.wmass > 0.0) {  // sparse: closed-form mass, the model's bin pairs only
+    mass = e.wmass;
+#pragma unroll 1
+    for (int i = 0; i < e.npair; ++i) {
+      const int q = e.pairs[i];
+      const char* base = reinterpret_cast<const char*>(a.tab) + (size_t)q * pair_bytes;
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double k0 = e.coef[4 * k], k1 = e.coef[4 * k + 1], k2 = e.coef[4 * k + 2],
+                     k3 = e.coef[4 * k + 3];
+        const char* w = base + cen[k];
+        const double2 p0 = ldd2(w + e.off[4 * k]), p1 = ldd2(w + e.off[4 * k + 1]);
+        const double2 p2 = ldd2(w + e.off[4 * k + 2]), p3 = ldd2(w + e.off[4 * k + 3]);
+        o0 += k0 * p0.x + k1 * p1.x + k2 * p2.x + k3 * p3.x;
+        o1 += k0 * p0.y + k1 * p1.y + k2 * p2.y + k3 * p3.y;
+      }
+      const double m0 = a.model[2 * q], m1 = a.model[2 * q + 1];
+      if (o0 > e.snap && m0 != 0.0)
+        s += SIM == SWG_SIM_BHATTACHARYYA ? sqrt(m0 * o0) : fmin(m0, o0 / mass);
+      if (o1 > e.snap && m1 != 0.0)
+        s += SIM == SWG_SIM_BHATTACHARYYA ? sqrt(m1 * o1) : fmin(m1, o1 / mass);
+    }
+  } else if constexpr (SIM == SWG_SIM_BHATTACHARYYA) {
     for (int g = 0; g < a.groups; ++g) {
       double out[kOct];
       octet(g, out);

@@ -1406,6 +1406,7 @@ enum Engine { kAffine32, kCake16, kCake32, kBrute, kQuad, kExp64, kAffine16 };
 struct MapPlan {
   int row0 = 0, rows = 0, mw = 0;  // map rows [row0, row0 + rows) of width mw
   int chain_s = 0, chain_k = 0, chain_j = 0;  // chain order (0: off; SweepArgs)
+  bool stream = false;  // Manhattan: the row-streaming chain sweep (k_stream.cu)
   Engine engine = kAffine32;
   swg_kernel k{};  // the kernel the engine sweeps (Plain maps: Uniform)
   dim3 grid;
@@ -1521,6 +1522,21 @@ dim3 sweep_grid(Engine e, int mw, int rows) {
 // one-ring cake with coefficient 1.0 (exact integer weights, same scores:
 // score_counts == score_weights on integers), so on narrow tables it runs the
 // 16-bit cake sweep.
+// Octets of the tables' bins holding a nonzero model value (SweepArgs::act;
+// every octet with SWG_SPARSE=0).
+int active_octets(const swg_tables* t, const swg_map_request& r) {
+  const char* sp = std::getenv("SWG_SPARSE");
+  if ((sp && std::atoi(sp) == 0) || !r.model) return t->groups;
+  int nact = 0;
+  for (int g8 = 0; g8 < t->groups; ++g8) {
+    bool any = false;
+    for (int b = g8 * kOct; b < std::min(t->bins, (g8 + 1) * kOct) && !any; ++b)
+      any = r.model[t->bin0 + b] != 0.0;
+    nact += any;
+  }
+  return nact;
+}
+
 swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& p) {
   swg_kernel k = r.kernel;
   int method = r.method;
@@ -1545,7 +1561,11 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
   // (large maps only: for a small frame the extra narrow build costs more than
   // the sweep saves -- config 1, 50k windows: 0.033 -> 0.051 ms per step)
   if (e == kAffine32 && k.kind == SWG_KERNEL_MANHATTAN && t->planes >= 3 && t->has_fi &&
-      !t->carried && affine_mass(k) < 65536 && (int64_t)p.rows * p.mw >= (int64_t(1) << 20)) {
+      !t->carried && affine_mass(k) < 65536 && (int64_t)p.rows * p.mw >= (int64_t(1) << 20) &&
+      // the narrow planes cost a 3-plane 16-bit build per frame (config 5:
+      // 0.38 ms) against 0.05-0.2 ms saved per scale: worth it for a model
+      // that spans most octets, or once the planes exist
+      (t->t16a || 2 * active_octets(t, r) > t->groups)) {
     const char* env = std::getenv("SWG_AFFINE16");
     if (!env || std::atoi(env)) e = kAffine16;
   }
@@ -1587,6 +1607,27 @@ swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& 
       const unsigned gx = (unsigned)((p.mw + tw - 1) / tw);
       p.grid = dim3(gx * (unsigned)(p.chain_k * p.chain_j),
                     (unsigned)((p.chain_s + p.chain_k - 1) / p.chain_k));
+    }
+  }
+  // Row-streaming chain sweep for Manhattan (k_stream.cu: one table row per
+  // window instead of 20 corner records; SWG_STREAM=0 / 1 forces it off / on):
+  // it needs the chain's segments (hy + 1 chains) x column blocks to fill the
+  // GPU, so small maps keep the per-window sweeps.
+  if ((e == kAffine32 && k.kind == SWG_KERNEL_MANHATTAN) || e == kAffine16 || e == kQuad) {
+    const int hy = k_hy(k);
+    const dim3 g = e == kQuad ? stream_quad_grid(p.mw, p.rows, hy)
+                              : stream_grid(e == kAffine16, p.mw, p.rows, hy);
+    bool on = hy >= 2 && (long long)g.x * g.y >= 2 * 148;
+    // the quadratic stream sweep (10 x 256-bit loads per row, 128 registers)
+    // wins when the model leaves octets out (config 5: 9.9 -> 4.1 ms); on a
+    // dense model the per-window sweep is ~10 % faster
+    if (e == kQuad && on) on = 4 * active_octets(t, r) <= 3 * t->groups;
+    if (const char* env = std::getenv(e == kQuad ? "SWG_STREAM_QUAD" : "SWG_STREAM"))
+      on = std::atoi(env) != 0 && p.rows > 0;
+    if (on) {
+      p.stream = true;
+      p.grid = g;
+      p.chain_s = p.chain_k = p.chain_j = 0;
     }
   }
   if (e == kExp64 && kExpTileY == 1) {
@@ -1638,6 +1679,14 @@ void fill_sweep_args(SweepArgs& a, const swg_tables* t, const swg_map_request& r
   a.parts = parts;
   std::memset(a.model, 0, sizeof(a.model));
   std::memcpy(a.model, r.model + t->bin0, sizeof(double) * t->bins);
+  const char* sp = std::getenv("SWG_SPARSE");
+  const bool sparse = !sp || std::atoi(sp) != 0;
+  a.nact = 0;
+  for (int g = 0; g < t->groups; ++g) {
+    bool any = !sparse;
+    for (int k = 0; k < kOct && !any; ++k) any = a.model[g * kOct + k] != 0.0;
+    if (any) a.act[a.nact++] = (unsigned char)g;
+  }
   a.pin = static_cast<const double2*>(r.partial_in);
   a.pout = static_cast<double2*>(r.partial_out);
   a.sc_tiles = p.chain_s ? 0 : super_column_tiles(t, p.engine, p.k, a.hx, a.hy);
@@ -1680,6 +1729,20 @@ double exp_plan(const swg_tables* t, const swg_map_request& r, int hx, int hy, E
   const double dh = 8.0 * 16.0 * T * u / (1.0 - dd);
   const double hmin = pw(hx + hy);
   es.snap = 2.0 * dh;
+  // sparse mode: the closed-form window mass, the model's nonzero bin pairs
+  es.wmass = 0.0;
+  es.npair = 0;
+  const char* sp = std::getenv("SWG_SPARSE");
+  if ((!sp || std::atoi(sp) != 0) && r.model) {
+    double sx = 0.0, sy = 0.0;
+    for (int d = -hx; d <= hx; ++d) sx += pw(std::abs(d));
+    for (int d = -hy; d <= hy; ++d) sy += pw(std::abs(d));
+    es.wmass = sx * sy;
+    const double* m = r.model + t->bin0;
+    for (int q = 0; q < (t->bins + 1) / 2; ++q)
+      if (m[2 * q] != 0.0 || (2 * q + 1 < t->bins && m[2 * q + 1] != 0.0))
+        es.pairs[es.npair++] = (unsigned short)q;
+  }
   if (es.snap >= 0.5 * hmin) return 1.0;  // no separation of noise and data: re-score everything
   if (r.sim == SWG_SIM_BHATTACHARYYA)
     // |d sum sqrt(m h)| <= sqrt(bins) dh / (2 sqrt(h_min)); mass term <= bins dh / 2
@@ -1748,7 +1811,8 @@ void quad_args(const swg_tables* t, const MapPlan& p, SweepArgs& a) {
 
 swg_status run_quad(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaStream_t st) {
   quad_args(t, p, a);
-  CUDA_TRY(launch_sweep_quad(a, p.grid, st));
+  if (p.stream) CUDA_TRY(launch_stream_quad(a, p.grid, st));
+  else CUDA_TRY(launch_sweep_quad(a, p.grid, st));
   return SWG_OK;
 }
 
@@ -1766,7 +1830,8 @@ swg_status run_affine(const swg_tables* t, const MapPlan& p, SweepArgs& a, cudaS
                           {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
   for (int q = 0; q < 20; ++q)
     a.lat[q] = pts[q][0] < t->planes ? off(pts[q][0], pts[q][1], pts[q][2]) : 0;
-  CUDA_TRY(launch_sweep_affine(a, p.k.kind == SWG_KERNEL_UNIFORM, p.grid, st));
+  if (p.stream) CUDA_TRY(launch_stream_affine(a, false, p.grid, st));
+  else CUDA_TRY(launch_sweep_affine(a, p.k.kind == SWG_KERNEL_UNIFORM, p.grid, st));
   return SWG_OK;
 }
 
@@ -1784,7 +1849,8 @@ swg_status run_affine16(const swg_tables* t, const MapPlan& p, SweepArgs& a, cud
                           {1, 2, 0}, {1, 0, 2}, {1, 1, 2}, {1, 2, 2}, {2, 0, 0},
                           {2, 2, 0}, {2, 0, 1}, {2, 2, 1}, {2, 0, 2}, {2, 2, 2}};
   for (int q = 0; q < 20; ++q) a.lat[q] = off(pts[q][0], pts[q][1], pts[q][2]);
-  CUDA_TRY(launch_sweep_affine16(a, p.grid, st));
+  if (p.stream) CUDA_TRY(launch_stream_affine(a, true, p.grid, st));
+  else CUDA_TRY(launch_sweep_affine16(a, p.grid, st));
   return SWG_OK;
 }
 
@@ -1882,6 +1948,55 @@ swg_status run_brute(swg_ctx* c, const swg_tables* t, const MapPlan& p, const Sw
 
 }  // namespace
 
+swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_plan_info* out) {
+  ST_TRY(check_tables(t));
+  if (!r || !out) return fail(SWG_ERR_ARG, "NULL argument");
+  MapPlan p;
+  ST_TRY(validate_request(t, *r, false, p));
+  ST_TRY(plan_request(t, *r, p));
+  std::memset(out, 0, sizeof(*out));
+  static thread_local SweepArgs a;
+  fill_sweep_args(a, t, *r, p, nullptr, nullptr);
+  const char* name = "";
+  int planes = 1, eb = 4, bins = t->bins;
+  switch (p.engine) {
+    case kAffine32:
+      name = p.stream ? "k_stream_affine" : "k_sweep_affine";
+      planes = p.k.kind == SWG_KERNEL_UNIFORM ? 1 : 3;
+      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      break;
+    case kAffine16:
+      name = p.stream ? "k_stream_affine16" : "k_sweep_affine16";
+      planes = 3;
+      eb = 2;
+      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      break;
+    case kQuad:
+      name = p.stream ? "k_stream_quad" : "k_sweep_quad";
+      planes = 5;
+      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      break;
+    case kExp64: {
+      name = "k_sweep_exp";
+      planes = 4;
+      eb = 8;
+      static thread_local ExpSweep es;
+      exp_plan(t, *r, a.hx, a.hy, es);
+      if (es.wmass > 0.0) bins = std::min(t->bins, es.npair * kDP);
+      break;
+    }
+    case kCake16: name = "k_sweep_cake16"; eb = 2; break;
+    case kCake32: name = "k_sweep_cake"; break;
+    case kBrute: name = "k_sweep_brute"; planes = 0; eb = 0; break;
+  }
+  std::snprintf(out->kernel, sizeof(out->kernel), "%s", name);
+  out->planes = planes;
+  out->entry_bytes = eb;
+  out->bins_read = bins;
+  out->ctas = (int)(p.grid.x * p.grid.y);
+  return SWG_OK;
+}
+
 swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs,
                                double* const* scores_host, double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev) {
@@ -1916,7 +2031,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
       stot += round_up((size_t)p.rows * p.mw, 32);
     }
     p.poff = ptot;
-    ptot += (size_t)p.grid.x * (p.grid.y + 1);  // + a spare CTA row: the split last map
+    // + spare CTA rows: the split last map (a stream sweep's halves may each
+    // round up a segment row of hy + 1 chains)
+    ptot += (size_t)p.grid.x * (p.grid.y + 1 + (p.stream ? 2 * k_hy(p.k) + 1 : 0));
   }
   swg_ctx::Scratch& S = c->scr[c->slot];
   ST_TRY(S.scores.ensure(std::max<size_t>(stot, 1) * 8));
@@ -1975,7 +2092,7 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   bool fused = c->fanout_off && nwork == 0 && n >= 2 && n <= kQuadMulti && t->carry_y0 == 0;
   for (int i = 0; i < n && fused; ++i)
     fused = plan[i].engine == kQuad && plan[i].rows > 0 && !reqs[i].partial_in &&
-            !reqs[i].partial_out && !copy_map(i) && plan[i].chain_s == 0 &&
+            !reqs[i].partial_out && !copy_map(i) && plan[i].chain_s == 0 && !plan[i].stream &&
             super_column_tiles(t, kQuad, plan[i].k, k_hx(plan[i].k), k_hy(plan[i].k)) == 0;
   if (fused) ST_TRY(run_quad_multi(c, t, n, reqs, plan, out.data(), parts0, dpeaks));
   // Device-output fan-out issues the costliest sweeps first (longest-first
@@ -2047,7 +2164,9 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
         MapPlan h = p;
         h.row0 = p.row0 + done;
         h.rows = (q + 1) * p.rows / kSplit - done;
-        h.grid = sweep_grid(p.engine, p.mw, h.rows);
+        h.grid = !p.stream           ? sweep_grid(p.engine, p.mw, h.rows)
+                 : p.engine == kQuad ? stream_quad_grid(p.mw, h.rows, k_hy(p.k))
+                                     : stream_grid(p.engine == kAffine16, p.mw, h.rows, k_hy(p.k));
         ST_TRY(sweep(h, dscores + (size_t)done * p.mw, parts + np));
         np += (int)(h.grid.x * h.grid.y);
         if (q + 1 < kSplit) ST_TRY(copy_rows(n * (q + 1) + i, done, h.rows));  // own event

@@ -123,6 +123,13 @@ struct SweepArgs {
   int chain_s, chain_k, chain_j;  // 0: off
   int wide0;           // cake16: ring 0's box count may exceed 16 bits
   int y_off;           // table row 0 is image row y_off (carried band tables)
+  // Octets holding a nonzero model bin, in bin order.  A bin whose model
+  // value is 0 scores sqrt(0 * h) = +0 (Bhattacharyya) or min(0, h/mass) =
+  // +0 (intersection), and s + (+0) == s, so the sweeps whose window mass is
+  // closed-form (affine, quadratic, exponential) read and score only these
+  // octets (SWG_SPARSE=0: every octet).  Bit-identical by construction.
+  int nact;
+  unsigned char act[kMaxBins / kOct];
   double model[kMaxBins];  // zero-padded to a multiple of 8
 };
 
@@ -165,6 +172,14 @@ struct ExpSweep {
   double coef[16];
   int w, h;     // image size (flip mapping)
   double snap;  // values below this are fp32 noise of an empty bin
+  // Sparse mode (wmass > 0): every strict window holds one weight per pixel,
+  // so its mass is the closed-form kernel sum wmass, and only the bin pairs
+  // with a nonzero model value (pairs[0..npair)) are read and scored -- a
+  // zero-model bin adds +0 to the score (the map stays within the fast
+  // path's error bound; the exact peak is re-scored over every bin).
+  double wmass;
+  int npair;
+  unsigned short pairs[kMaxBins / kDP];
 };
 
 // Two-phase exact peak of a tolerance-based map.
@@ -346,6 +361,27 @@ constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kExpThreads / 32 / kExpWa
 #define SWG_CAKE_MINB 10  // <= 48 registers: 10 CTAs (40 warps) per SM; 40 registers spill (+3 %)
 #endif
 constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
+// Row-streaming chain sweeps (k_stream.cu): a CTA = kStreamWarps warps side
+// by side (32 windows each, one lane per window) on a segment of at most
+// kStreamLen windows of one chain.
+#ifndef SWG_STREAM_LEN
+#define SWG_STREAM_LEN 16
+#endif
+#ifndef SWG_STREAM_WARPS
+#define SWG_STREAM_WARPS 4
+#endif
+#ifndef SWG_STREAM_MINB
+#define SWG_STREAM_MINB 4
+#endif
+#ifndef SWG_STREAMQ_MINB
+#define SWG_STREAMQ_MINB 4
+#endif
+#ifndef SWG_STREAM16_MINB
+#define SWG_STREAM16_MINB 6
+#endif
+constexpr int kStreamLen = SWG_STREAM_LEN;
+constexpr int kStreamWarps = SWG_STREAM_WARPS, kStreamThreads = 32 * kStreamWarps;
+constexpr int kStreamCols = 32 * kStreamWarps;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
 
@@ -356,6 +392,10 @@ template <typename T>
 cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_sweep_affine(const SweepArgs& a, bool uniform, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_affine16(const SweepArgs& a, dim3 grid, cudaStream_t s);
+dim3 stream_grid(bool narrow, int mw, int rows, int hy);
+cudaError_t launch_stream_affine(const SweepArgs& a, bool narrow, dim3 grid, cudaStream_t s);
+dim3 stream_quad_grid(int mw, int rows, int hy);
+cudaError_t launch_stream_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);
 cudaError_t launch_sweep_cake(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                               cudaStream_t s);
 cudaError_t launch_sweep_quad(const SweepArgs& a, dim3 grid, cudaStream_t s);

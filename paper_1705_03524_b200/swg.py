@@ -101,6 +101,11 @@ class Peak(C.Structure):
         return (self.map_x, self.map_y, self.center_x, self.center_y, self.score)
 
 
+class _PlanInfo(C.Structure):
+    _fields_ = [("kernel", C.c_char * 32), ("planes", C.c_int), ("entry_bytes", C.c_int),
+                ("bins_read", C.c_int), ("ctas", C.c_int)]
+
+
 class _Req(C.Structure):
     _fields_ = [("kernel", Kernel), ("method", C.c_int), ("sim", C.c_int), ("rings", C.c_int),
                 ("ring_rule", C.c_int), ("row_begin", C.c_int), ("row_end", C.c_int),
@@ -179,6 +184,7 @@ def lib():
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
         "swg_likelihood_maps": [vp, C.c_int, vp, vp, vp, vp, vp],
+        "swg_request_plan": [vp, vp, vp],
         "swg_likelihood_batch": [vp, C.c_int, vp, C.c_int, C.c_size_t, C.c_int, vp, vp, vp],
         "swg_brute_windows": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
                               C.POINTER(Kernel), C.c_int, vp, vp],
@@ -520,6 +526,16 @@ class Tables:
             return maps, None
         return maps, [None if r.partial_out is not None else p.astuple()
                       for p, r in zip(peaks, reqs)]
+
+    def request_plan(self, req: "MapRequest") -> dict:
+        """What likelihood_maps runs for `req` (swg_request_plan): sweep
+        kernel, planes read, bytes per entry, bins whose records are read,
+        CTAs."""
+        creqs, _keep = self._creqs([req], self.total_bins)
+        out = _PlanInfo()
+        _check(lib().swg_request_plan(self._h, C.addressof(creqs), C.byref(out)))
+        return {"kernel": out.kernel.decode(), "planes": out.planes,
+                "entry_bytes": out.entry_bytes, "bins_read": out.bins_read, "ctas": out.ctas}
 
     @staticmethod
     def _creqs(reqs, bins):
