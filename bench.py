@@ -809,7 +809,9 @@ class OursArm:
                     ev[j].record()
                     j += 1
                 if len(u["chunks"]) == 1:
-                    u["t"].rebuild(u["src"], u["pitch"])
+                    # the frame's tables, the units its requests read (octets /
+                    # bin pairs of the models' nonzero bins; swg_tables_rebuild_for)
+                    u["t"].rebuild_for(u["src"], u["reqs"], u["pitch"])
                 else:  # bin-range walk: the new frame with the first range, then ranges
                     u["t"].rebuild_bins(b0, u["src"] if c == 0 else None, u["pitch"])
                 if ev:
@@ -1039,7 +1041,7 @@ class OursArm:
                 if walk:  # bin ranges: the frame with the first range, then ranges
                     _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
                 else:
-                    _check(lib().swg_tables_rebuild(t._h, src, 0, 0))
+                    _check(lib().swg_tables_rebuild_for(t._h, src, 0, 0, n, C.addressof(creqs)))
                 _check(lib().swg_likelihood_maps(
                     t._h, n, C.addressof(creqs),
                     C.addressof(hp) if hp is not None else None, None, C.addressof(pk), None))
@@ -1101,7 +1103,8 @@ class OursArm:
         from paper_1705_03524_b200 import dist as D
         pl = dict(u["t"].request_plan(chunks[-1][1][i]))
         grp = {"k_sweep_exp": 2, "k_stream_affine": 8, "k_stream_affine16": 8,
-               "k_stream_quad": 8}.get(pl["kernel"])
+               "k_stream_quad": 8, "k_sweep_affine": 8, "k_sweep_affine16": 8,
+               "k_sweep_quad": 8}.get(pl["kernel"])
         if grp and os.environ.get("SWG_SPARSE", "1") != "0":
             m = np.asarray(u["reqs"][i].model)
             per = []
@@ -1150,10 +1153,14 @@ class OursArm:
         if build_ms:
             bms = sum(build_ms) / steps
             in_bytes = sum(u["h2d"] for u in self.units)
-            bb = in_bytes + sum(group_build_bytes(
-                wl["groups"][u["g"]], self.tab_w, self.tab_h, self.nb,
-                narrow=any(self._plan(u, i)["kernel"].endswith("affine16")
-                           for i in range(len(u["reqs"])))) for u in self.units)
+            # plane bytes the builds wrote (the library's count: a model-driven
+            # rebuild writes only the units its requests read); a bin-range
+            # walk rebuilds every range's planes
+            bb = in_bytes + sum(
+                u["t"].built_bytes() if len(u.get("chunks") or []) <= 1 else group_build_bytes(
+                    wl["groups"][u["g"]], self.tab_w, self.tab_h, self.nb,
+                    narrow=any(self._plan(u, i)["kernel"].endswith("affine16")
+                               for i in range(len(u["reqs"])))) for u in self.units)
             kt["ih_build"] = {"launches_per_step": len(build_ms) // steps, "ms_per_step": bms,
                               "bytes_per_step": int(bb), "launches": [],
                               "kernels": "k_quantize + k_colsum + k_bandscan + k_build / "

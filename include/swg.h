@@ -346,6 +346,22 @@ swg_status swg_likelihood_maps(swg_tables* t, int n,
                                double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev);
 
+/* swg_tables_rebuild for a known set of requests: quantise the new frame,
+ * then build only the table units those requests read -- bin octets of the
+ * 32-bit planes (Manhattan / Euclidean sweeps) or bin pairs of the decay
+ * planes (exponential sweep) holding a nonzero model value; a model's zero
+ * bins contribute +0 to every score, so those sweeps never read them
+ * (SWG_SPARSE=0: every unit).  The other units are marked stale and built
+ * on first use by any later call (maps with other models, exports, window
+ * queries, device layout), so the tables' contents are never observably
+ * incomplete.  Plain-only (16-bit) tables and bin-range tables build fully.
+ * reqs are the swg_likelihood_maps requests that will follow. */
+swg_status swg_tables_rebuild_for(swg_tables* t, const void* pixels, int is_device,
+                                  size_t pitch_bytes, int n, const swg_map_request* reqs);
+/* Plane bytes written by the builds since the last rebuild began
+ * (measurement: the IH-build GB/s). */
+swg_status swg_tables_built_bytes(const swg_tables* t, size_t* bytes);
+
 /* What swg_likelihood_maps would run for one request (measurement and
  * tests; no device work): the sweep kernel's name, the table planes it reads,
  * bytes per table entry, and how many bins' records it reads (a model's zero

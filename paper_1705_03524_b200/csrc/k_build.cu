@@ -448,14 +448,17 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
 // kind gets its own register allocation.
 template <typename T, int KIND, int CPT>
 __global__ void __launch_bounds__(512) k_build(const BuildArgs g) {
-  build_body<T, KIND, CPT>(g, blockIdx.x / g.groups, blockIdx.x % g.groups);
+  const int ng = g.nsel ? g.nsel : g.groups;  // selective build: the listed octets
+  const int i = blockIdx.x % ng;
+  build_body<T, KIND, CPT>(g, blockIdx.x / ng, g.nsel ? (int)g.sel[i] : i);
 }
 
 // Small tables: all kinds in ONE launch (blockIdx.y = kind) -- fewer
 // serialized launches where a launch is latency, not bandwidth.
 template <typename T, int CPT>
 __global__ void __launch_bounds__(512) k_build_fused(const BuildArgs g) {
-  const int band = blockIdx.x / g.groups, grp = blockIdx.x % g.groups;
+  const int ng = g.nsel ? g.nsel : g.groups;
+  const int band = blockIdx.x / ng, grp = g.nsel ? (int)g.sel[blockIdx.x % ng] : blockIdx.x % ng;
   switch (blockIdx.y) {
     case 0: build_body<T, 0, CPT>(g, band, grp); break;
     case 1: build_body<T, 1, CPT>(g, band, grp); break;
@@ -645,7 +648,7 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
   const int cpt = choose_cpt(a.w);
   const int threads = (int)round_up((size_t)((a.w + cpt - 1) / cpt), 32);
   const size_t smem = (size_t)threads * cpt * stage_chunks_per_record<T>() * 16;
-  const unsigned grid = (unsigned)(a.nbands * a.groups);
+  const unsigned grid = (unsigned)(a.nbands * (a.nsel ? a.nsel : a.groups));
   // narrow tables: plain only, unless asked for (the 16-bit {1, x, y} planes)
   const int kinds = a.kinds > 0 ? a.kinds : sizeof(T) == 2 ? 1 : a.planes;
   if (kinds > 1 && grid < 2u * 148u) {

@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
     k_build_decay_strip(const BuildArgs g, real dec, int kind, int pairs) {
   extern __shared__ double2 s_tile[];  // [kStripRows][kStripW] swizzled, then carry[band_h]
   double2* carry = s_tile + kStripRows * kStripW;
-  const int band = blockIdx.x / pairs, pr = blockIdx.x % pairs;
+  const int np = g.nsel ? g.nsel : pairs;  // selective build: the listed pairs
+  const int band = blockIdx.x / np, pr = g.nsel ? (int)g.sel[blockIdx.x % np] : blockIdx.x % np;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kStripW / 32;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
@@ -331,7 +332,7 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }
-  const unsigned grid = (unsigned)(a.nbands * pairs);
+  const unsigned grid = (unsigned)(a.nbands * (a.nsel ? a.nsel : pairs));
   const size_t smem = (size_t)(kStripRows * kStripW + a.band_h) * sizeof(double2);
   if (smem > (200 << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~8500 rows
   // set on every launch: the attribute is per device (a process-wide cache

@@ -44,9 +44,6 @@ __device__ __forceinline__ double clamp01s(double v) {
 __device__ __forceinline__ double u2ds(uint32_t n) {
   return __dsub_rn(__hiloint2double(0x43300000, (int)n), 4503599627370496.0);
 }
-__device__ __forceinline__ uint4 ldq(const uint32_t* p) {
-  return __ldg(reinterpret_cast<const uint4*>(p));
-}
 __device__ __forceinline__ uint32_t cmp4(const uint4& v, int k) {
   return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
 }

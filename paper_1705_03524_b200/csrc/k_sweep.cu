@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
   double s = 0.0, mass_unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;
   if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
-  for (int g = 0; g < a.groups; ++g) {
+  for (int gi = 0; gi < a.nact; ++gi) {  // the model's octets (SweepArgs::act)
+    const int g = a.act[gi];
     const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
     uint4 hist;
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kSweepThreads, SWG_AFFINE_MINB) k_sweep_affine
       const uint32_t raw = comp(hist, k);
       const double model = a.model[g * kOct + half * 4 + k];
       val[k] = u2d(raw);
-      if (raw == 0u) {
+      if (raw == 0u || model == 0.0) {  // +0 terms either way
         term[k] = 0.0;  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
       } else if (SIM == SWG_SIM_BHATTACHARYYA) {
         term[k] = __dsqrt_rn(__dmul_rn(model, val[k]));
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(kAff16Threads) k_sweep_affine16(const SweepArg
     return make_uint2(__vsub2(__vadd2(br.x, tl.x), __vadd2(bl.x, tr.x)),
                       __vsub2(__vadd2(br.y, tl.y), __vadd2(bl.y, tr.y)));
   };
-  for (int g = 0; g < a.groups; ++g) {
+  for (int gi = 0; gi < a.nact; ++gi) {  // the model's octets (SweepArgs::act)
+    const int g = a.act[gi];
     const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint16_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
 #pragma unroll
@@ -214,8 +216,8 @@ __global__ void __launch_bounds__(kAff16Threads) k_sweep_affine16(const SweepArg
         const uint32_t nr = n_ - nl_, nb = n_ - nt_, xr = xa_ - xl_, yb = ya_ - yt_;
         const uint32_t raw =
             (M * n_ + xl_ - xr + ucx * (nr - nl_) + yt_ - yb + ucy * (nb - nt_)) & 0xFFFFu;
-        if (raw != 0u) {  // sqrt(m*0) = 0 and min(m, 0) = 0: s unchanged
-          const double model = a.model[g * kOct + hf * 4 + k];
+        const double model = a.model[g * kOct + hf * 4 + k];
+        if (raw != 0u && model != 0.0) {  // else a +0 term: s unchanged
           const double val = u2d(raw);
           double term;
           if (SIM == SWG_SIM_BHATTACHARYYA) {
@@ -270,7 +272,8 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
   double s = 0.0, unused = 0.0;
   const size_t widx = (size_t)r * a.mw + u;
   if (a.pin) s = a.pin[widx].x;  // bin-range chain: running sum of earlier bins
-  for (int g = 0; g < a.groups; ++g) {
+  for (int gi = 0; gi < a.nact; ++gi) {  // the model's octets (SweepArgs::act)
+    const int g = a.act[gi];
     const char* w = reinterpret_cast<const char*>(reinterpret_cast<const uint32_t*>(a.tab) +
                                                   (size_t)g * a.planes * ps8 + centre);
     uint4 box[5];
@@ -289,7 +292,7 @@ __device__ __forceinline__ void quad_body(const SweepArgs& a, int tx, int ty, Pe
       const uint64_t h = A * n - ky * dxx - kx * dyy;
       val[k] = (double)h;
       const double model = a.model[g * kOct + half * 4 + k];
-      if (h == 0) {
+      if (h == 0 || model == 0.0) {  // +0 terms either way
         term[k] = 0.0;
       } else if (SIM == SWG_SIM_BHATTACHARYYA) {
         term[k] = __dsqrt_rn(__dmul_rn(model, val[k]));
@@ -441,8 +444,8 @@ template <int SIM>
 __global__ void __launch_bounds__(kCakeThreads, SIM == SWG_SIM_BHATTACHARYYA ? SWG_CAKE_MINB : 1)
     k_sweep_cake16(const SweepArgs a, const CakeSweep rg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int u0 = blockIdx.x * 32 + lane;
-  const int r0 = blockIdx.y * kCakeTileY + warp;
+  const int u0 = blockIdx.x * kCakeCtaX + (lane % kCakeWX);
+  const int r0 = blockIdx.y * kCakeCtaY + warp * kCakeWY + lane / kCakeWX;
   const bool active = u0 < a.mw && r0 < a.rows;
   const int u = min(u0, a.mw - 1), r = min(r0, a.rows - 1);
   const int v = a.row0 + r;

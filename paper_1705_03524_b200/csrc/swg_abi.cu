@@ -297,6 +297,13 @@ struct swg_tables {
   int band_h = 0, nbands = 0;
   size_t wa = 0;
   size_t bytes = 0;
+  // Selective (model-driven) builds, swg_tables_rebuild_for: units of the
+  // primary set -- bin octets of the 32-bit planes (+ the narrow ramp
+  // planes), or bin pairs of the decay planes -- not yet built for the
+  // current frame.  Empty: every unit is current.  Any consumer builds the
+  // units it reads first (ensure_fresh).
+  std::vector<unsigned char> stale;
+  size_t built_bytes = 0;  // plane bytes written since the last rebuild began
 };
 
 #ifndef SWG_L2_BUDGET_MB
@@ -340,9 +347,15 @@ void choose_bands(swg_tables* t) {
 }
 
 template <typename T>
-swg_status run_build(swg_tables* t, T* out) {
+swg_status run_build(swg_tables* t, T* out, const std::vector<int>* sel = nullptr) {
   swg_ctx* c = t->ctx;
-  BuildArgs a{};
+  static thread_local BuildArgs a;
+  a = BuildArgs{};
+  if (sel) {
+    a.nsel = (int)sel->size();
+    for (int i = 0; i < a.nsel; ++i) a.sel[i] = (unsigned short)(*sel)[i];
+    if (a.nsel == 0) return SWG_OK;
+  }
   a.fi = t->fi;
   a.fi_pitch = t->fip;
   a.out = out;
@@ -368,6 +381,9 @@ swg_status run_build(swg_tables* t, T* out) {
   int nl = 0;
   CUDA_TRY(launch_build<T>(a, c->stream, &nl));
   c->launches += (uint64_t)nl;
+  const size_t units = a.nsel ? (size_t)a.nsel : (size_t)t->groups;
+  const int kinds = sizeof(T) == 2 ? 1 : t->planes;
+  t->built_bytes += units * kOct * t->ps * kinds * sizeof(T) + (a.out16 ? units * kOct * t->ps * 3 * 2 : 0);
   return SWG_OK;
 }
 
@@ -523,13 +539,19 @@ swg_status weight_grid(swg_ctx* c, const swg_kernel& k, const double** out) {
   return SWG_OK;
 }
 
-swg_status run_build_decay(swg_tables* t) {
+swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr) {
   swg_ctx* c = t->ctx;
+  if (sel && sel->empty()) return SWG_OK;
   const size_t fsz = t->fip * t->h;
   CUDA_TRY(launch_flip(t->fi, t->fip, t->w, t->h, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz,
                        c->stream));
   c->launches += 1;
-  BuildArgs a{};
+  static thread_local BuildArgs a;
+  a = BuildArgs{};
+  if (sel) {
+    a.nsel = (int)sel->size();
+    for (int i = 0; i < a.nsel; ++i) a.sel[i] = (unsigned short)(*sel)[i];
+  }
   a.fi_pitch = t->fip;
   a.out = t->tdec;
   a.pitch = t->pitch;
@@ -552,8 +574,34 @@ swg_status run_build_decay(swg_tables* t) {
     CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
     c->launches += (uint64_t)nl;
   }
+  const size_t units = a.nsel ? (size_t)a.nsel : (size_t)t->groups * (kOct / kDP);
+  t->built_bytes += units * kDP * t->ps * 4 * 8;
   return SWG_OK;
 }
+
+// ---- selective builds
+bool selective(const swg_tables* t) {
+  return t->bins == t->total_bins && t->has_fi &&
+         (t->tdec || (t->t32 && t->planes >= SWG_PLANES_AFFINE));
+}
+int sel_units(const swg_tables* t) { return t->tdec ? t->groups * (kOct / kDP) : t->groups; }
+
+// Build the stale units `need` marks (null: every stale unit).
+swg_status ensure_fresh(swg_tables* t, const std::vector<unsigned char>* need) {
+  if (t->stale.empty()) return SWG_OK;
+  std::vector<int> sel;
+  for (int u = 0; u < (int)t->stale.size(); ++u)
+    if (t->stale[u] && (!need || (*need)[u])) sel.push_back(u);
+  if (sel.empty()) return SWG_OK;
+  if (t->tdec) ST_TRY(run_build_decay(t, &sel));
+  else ST_TRY(run_build<uint32_t>(t, t->t32, &sel));
+  for (int u : sel) t->stale[u] = 0;
+  bool any = false;
+  for (unsigned char v : t->stale) any |= v != 0;
+  if (!any) t->stale.clear();
+  return SWG_OK;
+}
+swg_status fresh_all(swg_tables* t) { return ensure_fresh(t, nullptr); }
 
 // A cake whose outer box holds >= 2^16 pixels still runs on 16-bit planes
 // when ring 1's box and ring 0's frame hold fewer (k_sweep_cake16 wide0).
@@ -899,6 +947,8 @@ swg_status swg_tables_rebuild(swg_tables* t, const void* pixels, int is_device,
   ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
   t->carried = false;
   t->carry_y0 = 0;
+  t->stale.clear();
+  t->built_bytes = 0;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));  // (+ the narrow ramp planes)
   if (t->t16a && !t->t32) ST_TRY(build_t16a(t, true));
@@ -919,11 +969,20 @@ swg_status swg_tables_rebuild_bins(swg_tables* t, const void* pixels, int is_dev
   DeviceGuard g(t->ctx->device);
   if (pixels) ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
   t->bin0 = bin_begin;
+  t->stale.clear();
+  t->built_bytes = 0;
   if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
   if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));  // (+ the narrow ramp planes)
   if (t->t16a && !t->t32) ST_TRY(build_t16a(t, true));
   if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   if (t->tdec) ST_TRY(run_build_decay(t));
+  return SWG_OK;
+}
+
+swg_status swg_tables_built_bytes(const swg_tables* t, size_t* bytes) {
+  ST_TRY(check_tables(t));
+  if (!bytes) return fail(SWG_ERR_ARG, "NULL");
+  *bytes = t->built_bytes;
   return SWG_OK;
 }
 
@@ -1018,6 +1077,12 @@ swg_status swg_tables_info(const swg_tables* t, int* w, int* h, int* bins, int* 
 swg_status swg_tables_device_layout(const swg_tables* t, const void** base, size_t* ps,
                                     size_t* pitch, int* bins_per_record) {
   ST_TRY(check_tables(t));
+  if (!t->stale.empty()) {  // raw plane pointers: every unit current first
+    swg_tables* m = const_cast<swg_tables*>(t);
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    DeviceGuard g(m->ctx->device);
+    ST_TRY(fresh_all(m));
+  }
   if (base) *base = t->tdec ? (const void*)t->tdec : (const void*)t->t32;
   if (ps) *ps = t->ps;
   if (pitch) *pitch = t->pitch;
@@ -1079,6 +1144,7 @@ swg_status swg_tables_export_u32(swg_tables* t, int kind, int b0, int b1, uint32
   DeviceGuard g(t->ctx->device);
   if (kind >= 3) return fail(SWG_ERR_OUT_OF_RANGE, "quadratic planes are 64-bit only");
   ST_TRY(ensure_t32(t));
+  ST_TRY(fresh_all(t));
   return export_planes<uint32_t, uint32_t>(t, t->t32, kind, b0, b1, out);
 }
 
@@ -1088,6 +1154,7 @@ swg_status swg_tables_export_f64(swg_tables* t, int kind, int b0, int b1, double
   if (b0 == b1) return SWG_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
+  ST_TRY(fresh_all(t));
   swg_ctx* c = t->ctx;
   const size_t per_bin = (size_t)(t->w + 1) * (t->h + 1);
   const int chunk = (int)std::max<size_t>(1, (256u << 20) / (per_bin * 8));
@@ -1147,6 +1214,7 @@ swg_status swg_query_terms(swg_tables* t, int n, int tpw, const swg_term* terms,
   swg_ctx* c = t->ctx;
   if (need64) ST_TRY(ensure_t64(t));
   else ST_TRY(ensure_t32(t));
+  ST_TRY(fresh_all(t));
   const size_t tb = (size_t)n * tpw * sizeof(swg_term), ob = (size_t)n * t->bins * 8;
   ST_TRY(c->terms.ensure(tb));
   ST_TRY(c->qout.ensure(ob));
@@ -1284,6 +1352,7 @@ swg_status swg_cake_windows(swg_tables* t, int n, const int* cx, const int* cy,
   DeviceGuard g(t->ctx->device);
   swg_ctx* c = t->ctx;
   ST_TRY(ensure_t32(t));
+  ST_TRY(fresh_all(t));
   const size_t tb = terms.size() * sizeof(swg_term), cb = coeff.size() * 8;
   const size_t ob = (size_t)n * t->bins * 8;
   ST_TRY(c->terms.ensure(tb + cb));
@@ -1506,9 +1575,9 @@ int super_column_tiles(const swg_tables* t, Engine e, const swg_kernel& k, int h
 dim3 sweep_grid(Engine e, int mw, int rows) {
   if (e == kBrute)
     return dim3((unsigned)((mw + kBruteThreads - 1) / kBruteThreads), (unsigned)std::max(rows, 1));
-  const int tw = e == kExp64 ? kExpTileX : (e == kCake16 || e == kAffine16) ? 32 : kSweepTileX;
+  const int tw = e == kExp64 ? kExpTileX : e == kCake16 ? kCakeCtaX : e == kAffine16 ? 32 : kSweepTileX;
   const int th = e == kExp64      ? kExpTileY
-                 : e == kCake16   ? kCakeTileY
+                 : e == kCake16   ? kCakeCtaY
                  : e == kAffine16 ? kAff16TileY
                  : e == kQuad     ? kQuadTileY
                                   : kSweepTileY;
@@ -1535,6 +1604,37 @@ int active_octets(const swg_tables* t, const swg_map_request& r) {
     nact += any;
   }
   return nact;
+}
+
+// Units of the selective set (octets of the 32-bit planes, pairs of the
+// decay planes) that a planned request reads: the model's nonzero ones for
+// the sweeps that skip zero-model bins, all for the rest that read the set.
+void plan_needs(const swg_tables* t, const swg_map_request& r, const MapPlan& p,
+                std::vector<unsigned char>& need) {
+  const char* sp = std::getenv("SWG_SPARSE");
+  const bool sparse = !(sp && std::atoi(sp) == 0) && r.model;
+  const int U = (int)need.size();
+  auto all = [&] { std::fill(need.begin(), need.end(), (unsigned char)1); };
+  if (p.rows == 0) return;
+  switch (p.engine) {
+    case kAffine32:
+    case kAffine16:
+    case kQuad:
+      if (t->tdec || !sparse) return all();
+      for (int b = 0; b < t->bins; ++b)
+        if (r.model[t->bin0 + b] != 0.0 && b / kOct < U) need[b / kOct] = 1;
+      return;
+    case kExp64:
+      if (!t->tdec || !sparse) return all();
+      for (int b = 0; b < t->bins; ++b)
+        if (r.model[t->bin0 + b] != 0.0 && b / kDP < U) need[b / kDP] = 1;
+      return;
+    case kCake32:
+      if (!t->tdec) all();
+      return;
+    default:
+      return;  // 16-bit plain planes / the feature image
+  }
 }
 
 swg_status plan_request(const swg_tables* t, const swg_map_request& r, MapPlan& p) {
@@ -1963,18 +2063,18 @@ swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_p
     case kAffine32:
       name = p.stream ? "k_stream_affine" : "k_sweep_affine";
       planes = p.k.kind == SWG_KERNEL_UNIFORM ? 1 : 3;
-      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      bins = std::min(t->bins, a.nact * kOct);
       break;
     case kAffine16:
       name = p.stream ? "k_stream_affine16" : "k_sweep_affine16";
       planes = 3;
       eb = 2;
-      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      bins = std::min(t->bins, a.nact * kOct);
       break;
     case kQuad:
       name = p.stream ? "k_stream_quad" : "k_sweep_quad";
       planes = 5;
-      if (p.stream) bins = std::min(t->bins, a.nact * kOct);
+      bins = std::min(t->bins, a.nact * kOct);
       break;
     case kExp64: {
       name = "k_sweep_exp";
@@ -1994,6 +2094,48 @@ swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_p
   out->entry_bytes = eb;
   out->bins_read = bins;
   out->ctas = (int)(p.grid.x * p.grid.y);
+  return SWG_OK;
+}
+
+swg_status swg_tables_rebuild_for(swg_tables* t, const void* pixels, int is_device,
+                                  size_t pitch_bytes, int n, const swg_map_request* reqs) {
+  ST_TRY(check_tables(t));
+  if (!pixels) return fail(SWG_ERR_ARG, "NULL pixels");
+  if (n < 0 || (n && !reqs)) return fail(SWG_ERR_ARG, "bad request list");
+  if (!t->fi) return fail(SWG_ERR, "tables were loaded, not built: cannot rebuild");
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  DeviceGuard g(t->ctx->device);
+  ST_TRY(upload_and_quantize(t, pixels, is_device, pitch_bytes));
+  t->carried = false;
+  t->carry_y0 = 0;
+  t->stale.clear();
+  t->built_bytes = 0;
+  if (t->t16) ST_TRY(run_build<uint16_t>(t, t->t16));
+  if (selective(t)) {
+    std::vector<unsigned char> need((size_t)sel_units(t), 0);
+    for (int i = 0; i < n; ++i) {
+      MapPlan p;
+      if (validate_request(t, reqs[i], false, p) != SWG_OK || plan_request(t, reqs[i], p) != SWG_OK)
+        std::fill(need.begin(), need.end(), (unsigned char)1);  // the map call reports it
+      else
+        plan_needs(t, reqs[i], p, need);
+    }
+    std::vector<int> sel;
+    for (int u = 0; u < (int)need.size(); ++u)
+      if (need[u]) sel.push_back(u);
+    const bool full = sel.size() == need.size();
+    if (t->tdec) ST_TRY(run_build_decay(t, full ? nullptr : &sel));
+    else ST_TRY(run_build<uint32_t>(t, t->t32, full ? nullptr : &sel));
+    if (!full) {
+      t->stale.assign(need.size(), 1);
+      for (int u : sel) t->stale[u] = 0;
+    }
+  } else {
+    if (t->t32) ST_TRY(run_build<uint32_t>(t, t->t32));
+    if (t->t16a && !t->t32) ST_TRY(build_t16a(t, true));
+    if (t->tdec) ST_TRY(run_build_decay(t));
+  }
+  if (t->t64) ST_TRY(run_build<uint64_t>(t, t->t64));
   return SWG_OK;
 }
 
@@ -2041,6 +2183,12 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   ST_TRY(S.peaks.ensure((size_t)n * sizeof(swg_peak)));
   ST_TRY(S.resc.ensure(RescoreSlice::kBytes * n));
   swg_peak* dpeaks = peaks_dev ? peaks_dev : static_cast<swg_peak*>(S.peaks.p);
+  // units of a selective rebuild that these requests read but are stale
+  if (!t->stale.empty()) {
+    std::vector<unsigned char> need((size_t)sel_units(t), 0);
+    for (int i = 0; i < n; ++i) plan_needs(t, reqs[i], plan[i], need);
+    ST_TRY(ensure_fresh(t, &need));
+  }
   // the lazily built 32-bit planes go on the main stream before the fan-out
   for (const MapPlan& p : plan)
     if (p.rows > 0 && (p.engine == kAffine32 || p.engine == kCake32)) ST_TRY(ensure_t32(t));
@@ -2257,7 +2405,7 @@ swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* 
     const int k = f % K;
     c->stream = c->work[k];
     c->slot = k;
-    ST_TRY(swg_tables_rebuild(sets[k], frames[f], is_device, pitch_bytes));
+    ST_TRY(swg_tables_rebuild_for(sets[k], frames[f], is_device, pitch_bytes, n, reqs));
     ST_TRY(swg_likelihood_maps(sets[k], n, reqs, nullptr, nullptr, nullptr,
                                dst + (size_t)f * n));
   }
@@ -2296,6 +2444,7 @@ swg_status swg_decay_windows(swg_tables* t, int n, const int* cx, const int* cy,
   exp_plan(t, r, k_hx(*k), k_hy(*k), es);
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
+  ST_TRY(fresh_all(t));
   swg_ctx* c = t->ctx;
   const size_t cb = round_up((size_t)n * 4, 256), ob = (size_t)n * t->bins * 8;
   ST_TRY(c->terms.ensure(2 * cb));
@@ -2322,6 +2471,7 @@ swg_status swg_tables_last_row(swg_tables* t, void* dev_out) {
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(ensure_t32(t));
+  ST_TRY(fresh_all(t));
   const int kinds = t->planes;
   CUDA_TRY(launch_last_row(t->t32, t->ps, t->pitch, t->planes, kinds, t->w, t->h, t->groups,
                            dev_out, t->ctx->stream));
@@ -2338,6 +2488,7 @@ swg_status swg_tables_add_carry(swg_tables* t, int y0, const void* dev_carry) {
   std::lock_guard<std::mutex> lk(t->ctx->mu);
   DeviceGuard g(t->ctx->device);
   ST_TRY(ensure_t32(t));
+  ST_TRY(fresh_all(t));
   CUDA_TRY(launch_add_carry(t->t32, t->ps, t->pitch, t->planes, t->planes, t->w, t->h,
                             t->groups, y0, dev_carry, t->ctx->stream));
   t->ctx->launches += 1;

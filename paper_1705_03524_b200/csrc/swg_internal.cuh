@@ -67,6 +67,11 @@ struct BuildArgs {
   int kinds;           // table kinds to build (0: every plane; narrow tables: plain)
   void* out16;         // 32-bit builds: also write kinds 0-2 mod 2^16 here (narrow
                        // {1, x, y} planes, 3-plane layout), or null
+  // Selective build (nsel > 0): only these units -- bin octets (integral
+  // planes) or bin pairs (decay planes) -- are written, each into its own
+  // slot of the full layout; the carries (K1a/K1b) still cover every unit.
+  int nsel;
+  unsigned short sel[kMaxBins / kDP];
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
                        // then of all rows above the band (K1b, exclusive scan)
@@ -361,6 +366,15 @@ constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kExpThreads / 32 / kExpWa
 #define SWG_CAKE_MINB 10  // <= 48 registers: 10 CTAs (40 warps) per SM; 40 registers spill (+3 %)
 #endif
 constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
+// A cake16 warp covers kCakeWX x (32 / kCakeWX) windows: the lanes of a warp
+// run until the last of them has emptied its octet's boxes, so compact warps
+// (windows closer together, more similar inner bins) diverge less; a corner
+// load is still 4 x 128-byte lines.
+#ifndef SWG_CAKE_WX
+#define SWG_CAKE_WX 32
+#endif
+constexpr int kCakeWX = SWG_CAKE_WX, kCakeWY = 32 / kCakeWX;
+constexpr int kCakeCtaX = kCakeWX, kCakeCtaY = kCakeWY * kCakeTileY;
 // Row-streaming chain sweeps (k_stream.cu): a CTA = kStreamWarps warps side
 // by side (32 windows each, one lane per window) on a segment of at most
 // kStreamLen windows of one chain.

@@ -165,6 +165,8 @@ def lib():
         "swg_tables_bin_range": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "swg_tables_rebuild": [vp, vp, C.c_int, C.c_size_t],
         "swg_tables_rebuild_bins": [vp, vp, C.c_int, C.c_size_t, C.c_int],
+        "swg_tables_rebuild_for": [vp, vp, C.c_int, C.c_size_t, C.c_int, vp],
+        "swg_tables_built_bytes": [vp, C.POINTER(C.c_size_t)],
         "swg_tables_upload_i64": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)],
         "swg_tables_destroy": [vp],
         "swg_tables_info": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -394,6 +396,21 @@ class Tables:
         is_dev = 0 if isinstance(pixels, np.ndarray) else int(pixels.is_cuda)
         self._keep = pixels
         _check(lib().swg_tables_rebuild(self._h, _ptr(pixels), is_dev, pitch))
+
+    def rebuild_for(self, pixels, reqs, pitch=0):
+        """swg_tables_rebuild_for: a new frame, building only the table units
+        (octets / bin pairs) the requests' sweeps read; the rest are built on
+        first use.  Returns nothing; built_bytes() reports the plane bytes."""
+        is_dev = 0 if isinstance(pixels, np.ndarray) else int(pixels.is_cuda)
+        self._keep = pixels
+        creqs, _keep = self._creqs(reqs, self.total_bins)
+        _check(lib().swg_tables_rebuild_for(self._h, _ptr(pixels), is_dev, pitch, len(reqs),
+                                            C.addressof(creqs) if len(reqs) else None))
+
+    def built_bytes(self) -> int:
+        v = C.c_size_t(0)
+        _check(lib().swg_tables_built_bytes(self._h, C.byref(v)))
+        return int(v.value)
 
     def rebuild_bins(self, bin_begin, pixels=None, pitch=0):
         """Rebuild for bins [bin_begin, bin_begin + bins): from `pixels` (a
