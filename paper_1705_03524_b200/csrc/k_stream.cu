@@ -90,6 +90,23 @@ __device__ __forceinline__ Seg quad_seg(const SweepArgs& a) {
   return s;
 }
 
+// L2 prefetch of a row segment by the TMA engine (no registers held): the
+// stream sweeps walk their rows in a known order, so thread i < segments
+// prefetches segment i of the row kStreamPf steps ahead.
+// Measured on config 5 (A/B of 0, 1, 2, 4 steps): the quadratic sweep gains
+// at one step (4.11 -> 3.82 ms), the affine sweep loses at any distance
+// (2.87 -> 3.12 ms: its 256-bit loads already keep enough bytes in flight).
+#ifndef SWG_STREAM_PF
+#define SWG_STREAM_PF 0
+#endif
+#ifndef SWG_STREAMQ_PF
+#define SWG_STREAMQ_PF 1
+#endif
+constexpr int kStreamPf = SWG_STREAM_PF, kStreamPfQ = SWG_STREAMQ_PF;
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Block argmax epilogue shared by the stream sweeps.
 __device__ __forceinline__ void stream_peak(double s, long long idx, const SweepArgs& a) {
   cta_peak(s, idx, a.parts + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
@@ -201,6 +218,7 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAM_MINB) k_stream_affi
                ox2 = ox0 + (size_t)(2 * a.hx + 1) * kOct;
   const int hy = a.hy;
   const int ybase = a.row0 + hy + a.y_off;  // cy of local row 0 (global rows)
+  const uint32_t seg_bytes = (uint32_t)min(kStreamCols, a.mw - (int)blockIdx.x * kStreamCols) * 32u;
   stream_init(a, sg, ssum, col, u);
 
   for (int gi = 0; gi < a.nact; ++gi) {
@@ -212,6 +230,15 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAM_MINB) k_stream_affi
 #pragma unroll
     for (int k = 0; k < 8; ++k) S1[k] = S2[k] = 0u;
     for (int j = sg.kb; j < sg.ke + 2; ++j) {
+      if (kStreamPf > 0 && threadIdx.x < 8 && j + kStreamPf < sg.ke + 2) {
+        const size_t rp = (size_t)(a.row0 + chain_r(sg.c, hy, j + kStreamPf)) * p8;
+        const int q = threadIdx.x;  // segments: P, X at x0 x1 x2; Y at x0 x2
+        const uint32_t* pl = q < 3 ? pl0 : q < 6 ? pl1 : pl2;
+        const int xi = q < 6 ? q % 3 : (q == 6 ? 0 : 2);
+        const size_t ox = (size_t)(blockIdx.x * kStreamCols) * kOct +
+                          (xi == 0 ? 0 : xi == 1 ? (size_t)(a.hx + 1) * kOct : (size_t)(2 * a.hx + 1) * kOct);
+        l2_prefetch(pl + rp + ox, seg_bytes);
+      }
       const size_t ro = (size_t)(a.row0 + chain_r(sg.c, hy, j)) * p8;
       const uint32_t cyb = (uint32_t)(ybase + chain_r(sg.c, hy, j - 2));
       const uint32_t cym = (uint32_t)(ybase + chain_r(sg.c, hy, j - 1));
@@ -276,6 +303,7 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAM16_MINB) k_stream_af
                ox2 = ox0 + (size_t)(2 * a.hx + 1) * kOct;
   const int hy = a.hy;
   const int ybase = a.row0 + hy + a.y_off;
+  const uint32_t seg_bytes = (uint32_t)min(kStreamCols, a.mw - (int)blockIdx.x * kStreamCols) * 16u;
   auto ld = [](const uint16_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); };
   stream_init(a, sg, ssum, col, u);
 
@@ -289,6 +317,15 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAM16_MINB) k_stream_af
     for (int k = 0; k < 8; ++k) S1[k] = S2[k] = 0u;
 #pragma unroll 2
     for (int j = sg.kb; j < sg.ke + 2; ++j) {
+      if (kStreamPf > 0 && threadIdx.x < 8 && j + kStreamPf < sg.ke + 2) {
+        const size_t rp = (size_t)(a.row0 + chain_r(sg.c, hy, j + kStreamPf)) * p8;
+        const int q = threadIdx.x;
+        const uint16_t* pl = q < 3 ? pl0 : q < 6 ? pl1 : pl2;
+        const int xi = q < 6 ? q % 3 : (q == 6 ? 0 : 2);
+        const size_t ox = (size_t)(blockIdx.x * kStreamCols) * kOct +
+                          (xi == 0 ? 0 : xi == 1 ? (size_t)(a.hx + 1) * kOct : (size_t)(2 * a.hx + 1) * kOct);
+        l2_prefetch(pl + rp + ox, seg_bytes);
+      }
       const size_t ro = (size_t)(a.row0 + chain_r(sg.c, hy, j)) * p8;
       const uint4 p0 = ld(pl0 + ro + ox0), p1 = ld(pl0 + ro + ox1), p2 = ld(pl0 + ro + ox2);
       const uint4 x0 = ld(pl1 + ro + ox0), x1 = ld(pl1 + ro + ox1), x2 = ld(pl1 + ro + ox2);
@@ -348,6 +385,7 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAMQ_MINB) k_stream_qua
   const size_t ox0 = (size_t)u * kOct, ox2 = ox0 + (size_t)(2 * a.hx + 1) * kOct;
   const int P = 2 * a.hy + 1;
   const int ybase = a.row0 + a.hy + a.y_off + sg.c;  // cy of window 0 of this chain
+  const uint32_t seg_bytes = (uint32_t)min(kStreamCols, a.mw - (int)blockIdx.x * kStreamCols) * 32u;
   stream_init(a, sg, ssum, col, u, true);
 
   for (int gi = 0; gi < a.nact; ++gi) {
@@ -357,6 +395,13 @@ __global__ void __launch_bounds__(kStreamThreads, SWG_STREAMQ_MINB) k_stream_qua
 #pragma unroll
     for (int k = 0; k < 8; ++k) N0[k] = QX[k] = QY[k] = 0u;
     for (int j = sg.kb; j <= sg.ke; ++j) {
+      if (kStreamPfQ > 0 && threadIdx.x < 10 && j + kStreamPfQ <= sg.ke) {
+        const size_t rp = (size_t)(a.row0 + sg.c + (j + kStreamPfQ) * P) * p8;
+        const int q = threadIdx.x;  // plane q / 2 at x0 (even) or x2 (odd)
+        const size_t ox = (size_t)(blockIdx.x * kStreamCols) * kOct +
+                          ((q & 1) ? (size_t)(2 * a.hx + 1) * kOct : 0);
+        l2_prefetch(pl + (size_t)(q >> 1) * ps8 + rp + ox, seg_bytes);
+      }
       const size_t ro = (size_t)(a.row0 + sg.c + j * P) * p8;
       const uint32_t cyb = (uint32_t)(ybase + (j - 1) * P);  // window j-1 (bottom row)
       const uint32_t cyt = cyb + (uint32_t)P;                 // window j (top row)
