@@ -219,6 +219,26 @@ def est_request_ms(group, k, method, rings, rows, w, h, nbins):
     return 0.05 + tab / 3.0e9
 
 
+def model_bins_read(group, k, method, model, nbins):
+    """(bins whose records a sweep reads, the selective-build units it
+    needs) -- the library's rule (plan_needs): nonzero-model bin pairs for the
+    exponential sweep, octets for the Manhattan / Euclidean sweeps; every bin
+    (no units) for the cake and brute force."""
+    import numpy as np
+    from paper_1705_03524_b200 import swg
+    if os.environ.get("SWG_SPARSE", "1") == "0":
+        return nbins, set()
+    kname = engine_of(group, k, method)[0]
+    if kname == "k_sweep_exp":
+        grp = 2
+    elif kname in ("k_sweep_affine", "k_sweep_affine16", "k_sweep_quad") and method == swg.SWIH:
+        grp = 8
+    else:
+        return nbins, set()
+    units = {int(b) // grp for b in np.flatnonzero(np.asarray(model) != 0)}
+    return min(nbins, grp * len(units)), units
+
+
 def est_build_ms(group, w, h, nbins):
     return 0.1 + group_build_bytes(group, w, h, nbins) / 3.0e9
 
@@ -560,12 +580,21 @@ class OursArm:
         frame_dev = torch.from_numpy(data.image).cuda()
         H, W = data.image.shape[:2]
         reqs_all = []
+        build = []
         for gi, g in enumerate(groups):
+            union = set()
             for si, (k, meth, rings, _) in enumerate(g["scales"]):
                 mh = H - k.kh + 1
+                # the sweeps with a closed-form window mass read only the
+                # model's nonzero octets / bin pairs (SweepArgs::act, ExpSweep::pairs)
+                nb_read, units = model_bins_read(g, k, meth, self.models[gi][si], self.nb)
+                union |= units
                 reqs_all.append(((gi, si), gi, mh,
-                                 est_request_ms(g, k, meth, rings, mh, W, H, self.nb)))
-        build = [est_build_ms(g, W, H, self.nb) for g in groups]
+                                 est_request_ms(g, k, meth, rings, mh, W, H, nb_read)))
+            full = est_build_ms(g, W, H, self.nb)
+            # a model-driven rebuild writes only the units the requests read
+            frac = len(union) / max(1, -(-self.nb // (2 if g["planes"] == swg.PLANES_DECAY else 8)))
+            build.append(full if not union else 0.1 + (full - 0.1) * min(1.0, frac))
         self.plan = D.plan_frame(reqs_all, build, self.world, min_rows=8)
         mine = self.plan[self.rank]
         for gi, (g, ms) in enumerate(zip(groups, self.models)):
