@@ -384,11 +384,14 @@ constexpr int kCakeCtaX = kCakeWX, kCakeCtaY = kCakeWY * kCakeTileY;
 #ifndef SWG_STREAM_WARPS
 #define SWG_STREAM_WARPS 4
 #endif
+// 5 CTAs per SM (<= 102 registers): config 5 Manhattan 2.87 -> 2.42 ms (96
+// registers, no spill), Euclidean 3.82 -> 3.66 ms (96 registers, 60-76 B of
+// spills); 6 per SM spills and loses on both
 #ifndef SWG_STREAM_MINB
-#define SWG_STREAM_MINB 4
+#define SWG_STREAM_MINB 5
 #endif
 #ifndef SWG_STREAMQ_MINB
-#define SWG_STREAMQ_MINB 4
+#define SWG_STREAMQ_MINB 5
 #endif
 #ifndef SWG_STREAM16_MINB
 #define SWG_STREAM16_MINB 6
