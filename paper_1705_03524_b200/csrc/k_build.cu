@@ -389,29 +389,53 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
     constexpr int NQ = stage_chunks_per_record<T>();
     if constexpr (NQ > 0) {
       // coalesced row stores: the warp's 32*CPT records are staged in shared
-      // memory (XOR-swizzled 16-byte chunks) and written back as 512
-      // contiguous bytes per store instruction; per-thread record runs touch
-      // 32 lines per instruction and throttle the LSU (lg_throttle)
-      extern __shared__ uint4 s_stage[];
+      // memory (XOR-swizzled 16-byte chunks = the TMA SWIZZLE_128B layout)
+      // and written back by ONE cp.async.bulk.tensor store per warp and row
+      // (the TMA engine reads shared memory: no per-thread global stores
+      // through the LSU), or without a tensor map as 512 contiguous bytes
+      // per store instruction
+      extern __shared__ __align__(1024) uint4 s_stage[];
       uint4* st = s_stage + warp * 32 * CPT * NQ;
       auto swz = [](int c) { return c ^ ((c >> 3) & 7); };
+      const int wrec0 = warp * 32 * CPT;
+      const bool tma = g.tmap_ok && wrec0 < g.w;
+      if (tma && lane == 0) {  // the previous row's store has read the buffer
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
 #pragma unroll
       for (int i = 0; i < CPT; ++i)
 #pragma unroll
         for (int q = 0; q < NQ; ++q) st[swz((lane * CPT + i) * NQ + q)] = record_chunk<T>(t[i], q);
-      __syncwarp();
-      const int wrec0 = warp * 32 * CPT;
-      uint4* dst = reinterpret_cast<uint4*>(row) + (size_t)(wrec0 + 1) * NQ;
+      if (tma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int line0 = wrec0 * (int)(kOct * sizeof(T)) / 128;
+          const int plane_i = grp * g.planes + KIND;
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(st);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+              ::"l"(&g.tmap), "r"(0), "r"(line0), "r"(y + 1), "r"(plane_i), "r"(sa)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else {
+        __syncwarp();
+        uint4* dst = reinterpret_cast<uint4*>(row) + (size_t)(wrec0 + 1) * NQ;
 #pragma unroll
-      for (int m = 0; m < CPT * NQ; ++m) {
-        const int c = m * 32 + lane;
-        if (wrec0 + c / NQ < g.w) dst[c] = st[swz(c)];
+        for (int m = 0; m < CPT * NQ; ++m) {
+          const int c = m * 32 + lane;
+          if (wrec0 + c / NQ < g.w) dst[c] = st[swz(c)];
+        }
       }
       __syncwarp();
       if constexpr (sizeof(T) == 4 && KIND <= 2) {
         // the narrow {1, x, y} planes (low 16 bits, 3-plane layout) from the
         // same values: one more staged pass of 16-byte records
         if (g.out16) {
+          if (tma && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
           uint16_t* row16 = static_cast<uint16_t*>(g.out16) +
                             (((size_t)grp * 3 + KIND) * g.plane_stride + (size_t)(y + 1) * g.pitch) *
                                 kOct;
@@ -442,12 +466,15 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
     }
     if (tid == 0) store_zero_record<T>(row);
   }
+  if constexpr (stage_chunks_per_record<T>() > 0) {  // every TMA store done before exit
+    if (g.tmap_ok && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
 }
 
 // K1c: one CTA per (row band, bin octet); one launch per table kind so each
 // kind gets its own register allocation.
 template <typename T, int KIND, int CPT>
-__global__ void __launch_bounds__(512) k_build(const BuildArgs g) {
+__global__ void __launch_bounds__(512) k_build(const __grid_constant__ BuildArgs g) {
   const int ng = g.nsel ? g.nsel : g.groups;  // selective build: the listed octets
   const int i = blockIdx.x % ng;
   build_body<T, KIND, CPT>(g, blockIdx.x / ng, g.nsel ? (int)g.sel[i] : i);
@@ -456,7 +483,7 @@ __global__ void __launch_bounds__(512) k_build(const BuildArgs g) {
 // Small tables: all kinds in ONE launch (blockIdx.y = kind) -- fewer
 // serialized launches where a launch is latency, not bandwidth.
 template <typename T, int CPT>
-__global__ void __launch_bounds__(512) k_build_fused(const BuildArgs g) {
+__global__ void __launch_bounds__(512) k_build_fused(const __grid_constant__ BuildArgs g) {
   const int ng = g.nsel ? g.nsel : g.groups;
   const int band = blockIdx.x / ng, grp = g.nsel ? (int)g.sel[blockIdx.x % ng] : blockIdx.x % ng;
   switch (blockIdx.y) {

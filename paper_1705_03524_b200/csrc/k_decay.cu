@@ -160,8 +160,11 @@ constexpr int kStripW = 256, kStripRows = SWG_STRIP_ROWS;
 __device__ __forceinline__ int strip_swz(int x) { return x ^ ((x >> 3) & 7); }
 
 __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
-    k_build_decay_strip(const BuildArgs g, real dec, int kind, int pairs) {
-  extern __shared__ double2 s_tile[];  // [kStripRows][kStripW] swizzled, then carry[band_h]
+    k_build_decay_strip(const __grid_constant__ BuildArgs g, real dec, int kind, int pairs) {
+  // [kStripRows][kStripW] swizzled (= the TMA SWIZZLE_128B layout of each
+  // 4 KB row), then carry[band_h]
+  extern __shared__ __align__(1024) double2 s_tile[];
+  const bool tma = g.tmap_ok != 0;
   double2* carry = s_tile + kStripRows * kStripW;
   const int np = g.nsel ? g.nsel : pairs;  // selective build: the listed pairs
   const int band = blockIdx.x / np, pr = g.nsel ? (int)g.sel[blockIdx.x % np] : blockIdx.x % np;
@@ -214,8 +217,13 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
     int prev = 0;  // rows of the previous block still in the tile (phase C pending)
     for (int rb = 0;; rb += kStripRows) {
       const int nr = min(kStripRows, nrows - rb);
+      if (tma) {  // phase C is the TMA stores: the tile is free once they have read it
+        if (nr <= 0) break;
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+      }
       // C (previous block) + A (this block): the same thread, the same tile slots
-      if (in) {
+      if (in && !tma) {
         if (prev == kStripRows) {
 #pragma unroll
           for (int r = 0; r < kStripRows; ++r) {
@@ -284,10 +292,29 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
         const real n1 = __shfl_sync(0xFFFFFFFFu, v1[7], 31);
         if (lane == 0) carry[rb + r] = make_double2(n0, n1);  // E(x0 + kStripW - 1, y)
       }
-      __syncthreads();
+      if (tma) {
+        // C: one TMA tensor store per row (records x0+1 .. x0+256: 32 lines of
+        // 128 B; the tensor's bounds clip the strip at the image's edge)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+          const int plane_i = pr * g.planes + kind;
+          for (int r = 0; r < nr; ++r) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_tile + r * kStripW);
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                ::"l"(&g.tmap), "r"(0), "r"(x0 / 8), "r"(y0 + rb + r + 1), "r"(plane_i), "r"(sa)
+                : "memory");
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else {
+        __syncthreads();
+      }
       prev = nr;
     }
   }
+  if (tma && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Decay-table export: planes [b0, b1) of orientation `kind` -> (W+1)x(H+1) each.

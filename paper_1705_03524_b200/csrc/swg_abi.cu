@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "swg.h"
+#include <cudaTypedefs.h>
+
 #include "swg_internal.cuh"
 
 using namespace swg;
@@ -304,11 +306,45 @@ struct swg_tables {
   // units it reads first (ensure_fresh).
   std::vector<unsigned char> stale;
   size_t built_bytes = 0;  // plane bytes written since the last rebuild began
+  // TMA row tensor maps of the 32-bit / 16-bit plain planes (BuildArgs::tmap),
+  // encoded on first build: 0 not yet, 1 ok, -1 unavailable
+  CUtensorMap tm[2];
+  int tm_state[2] = {0, 0};
 };
 
 #ifndef SWG_L2_BUDGET_MB
 #define SWG_L2_BUDGET_MB 64  // share of the 126 MB L2 a sweep's corner rows may use
 #endif
+
+// TMA row tensor maps (BuildArgs::tmap): cuTensorMapEncodeTiled through the
+// runtime's driver entry point (no libcuda link).  Rank 4, uint32 elements:
+// {32 words = one 128-byte line, lines of a row (records 1..W), rows 0..H,
+// planes}, box {32, box_lines, 1, 1}, SWIZZLE_128B.
+bool swg::encode_row_tmap(CUtensorMap* m, void* record1, int rec_bytes, int w, int h, size_t pitch,
+                     size_t plane_stride, int nplanes, int box_lines) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!fn || std::getenv("SWG_NO_TMA")) return false;
+  if (reinterpret_cast<uintptr_t>(record1) % 16 || (pitch * rec_bytes) % 16 ||
+      (plane_stride * rec_bytes) % 16 || box_lines < 1 || box_lines > 256)
+    return false;
+  const cuuint64_t dims[4] = {32, (cuuint64_t)(((size_t)w * rec_bytes + 127) / 128),
+                              (cuuint64_t)h + 1, (cuuint64_t)nplanes};
+  const cuuint64_t strides[3] = {128, (cuuint64_t)(pitch * rec_bytes),
+                                 (cuuint64_t)(plane_stride * rec_bytes)};
+  const cuuint32_t box[4] = {32, (cuuint32_t)box_lines, 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, record1, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 namespace {
 
@@ -374,6 +410,22 @@ swg_status run_build(swg_tables* t, T* out, const std::vector<int>* sel = nullpt
   a.bin0 = t->bin0;
   // the 32-bit build writes the narrow ramp planes too (their low 16 bits)
   if (sizeof(T) == 4 && static_cast<void*>(out) == static_cast<void*>(t->t32)) a.out16 = t->t16a;
+  // TMA stores of the staged rows (16- and 32-bit planes)
+  const int ti = static_cast<void*>(out) == static_cast<void*>(t->t32) ? 0
+                 : static_cast<void*>(out) == static_cast<void*>(t->t16) ? 1 : -1;
+  if (ti >= 0 && sizeof(T) <= 4) {
+    if (t->tm_state[ti] == 0) {
+      const int rec = kOct * (int)sizeof(T);
+      const int box_lines = 32 * choose_cpt(t->w) * rec / 128;
+      t->tm_state[ti] = encode_row_tmap(&t->tm[ti], reinterpret_cast<char*>(out) + rec, rec, t->w,
+                                        t->h, t->pitch, t->ps, t->groups * t->planes, box_lines)
+                            ? 1 : -1;
+    }
+    if (t->tm_state[ti] == 1) {
+      a.tmap = t->tm[ti];
+      a.tmap_ok = 1;
+    }
+  }
   if (t->nbands > 1) {
     CUDA_TRY(launch_colsum(a, c->stream));
     c->launches += 2;
@@ -567,6 +619,15 @@ swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr)
   a.aw = 16;
   a.agg = t->lb;
   a.bin0 = t->bin0;
+  // TMA stores of the strip tiles' rows (16-byte pair records, 256 per row segment)
+  if (t->tm_state[0] == 0)
+    t->tm_state[0] = encode_row_tmap(&t->tm[0], reinterpret_cast<char*>(t->tdec) + 16, 16, t->w,
+                                     t->h, t->pitch, t->ps, t->groups * (kOct / kDP) * 4, 32)
+                         ? 1 : -1;
+  if (t->tm_state[0] == 1) {
+    a.tmap = t->tm[0];
+    a.tmap_ok = 1;
+  }
   const uint16_t* src[4] = {t->fi, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz};
   for (int k = 0; k < 4; ++k) {
     a.fi = src[k];

@@ -18,6 +18,7 @@
 // and plane_stride (in records).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -53,7 +54,14 @@ __host__ __device__ inline size_t elem_index(size_t ps, size_t pitch, int planes
 }
 
 // ---------------------------------------------------------------- build
-struct BuildArgs {
+struct alignas(64) BuildArgs {
+  // TMA tensor map over the output planes' rows (tmap_ok != 0): records
+  // 1..W of row y of plane k as 128-byte lines (box: one warp's staged row
+  // segment, SWIZZLE_128B = the staging's XOR layout); the build kernels
+  // then write their staged rows with cp.async.bulk.tensor stores instead
+  // of per-thread 16-byte stores.
+  CUtensorMap tmap;
+  int tmap_ok;
   const uint16_t* fi;  // quantised image, fi_pitch elements per row
   size_t fi_pitch;
   void* out;           // planes (T)
@@ -401,6 +409,12 @@ constexpr int kStreamWarps = SWG_STREAM_WARPS, kStreamThreads = 32 * kStreamWarp
 constexpr int kStreamCols = 32 * kStreamWarps;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
+
+// Encode a row tensor map for TMA stores (swg_abi.cu): planes of records of
+// rec_bytes, base = record 1 of row 0 of plane 0, box = box_lines 128-byte
+// lines x 1 row.  Returns false when the driver entry point is unavailable.
+bool encode_row_tmap(CUtensorMap* m, void* record1, int rec_bytes, int w, int h, size_t pitch,
+                     size_t plane_stride, int nplanes, int box_lines);
 
 // Kernel launchers (defined in the .cu files).
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
