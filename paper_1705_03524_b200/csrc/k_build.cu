@@ -678,7 +678,9 @@ cudaError_t launch_build(const BuildArgs& a, cudaStream_t s, int* launches) {
   const unsigned grid = (unsigned)(a.nbands * (a.nsel ? a.nsel : a.groups));
   // narrow tables: plain only, unless asked for (the 16-bit {1, x, y} planes)
   const int kinds = a.kinds > 0 ? a.kinds : sizeof(T) == 2 ? 1 : a.planes;
-  if (kinds > 1 && grid < 2u * 148u) {
+  bool fuse = kinds > 1 && grid < 2u * 148u;
+  if (const char* ef = std::getenv("SWG_BUILD_FUSED")) fuse = kinds > 1 && std::atoi(ef) != 0;  // A/B
+  if (fuse) {
     dim3 g3(grid, (unsigned)kinds);
     if (cpt == 4) {
       allow_smem(k_build_fused<T, 4>, smem);

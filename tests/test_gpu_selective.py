@@ -138,3 +138,33 @@ def test_rebuild_for_sparse_env_off(ctx, oracle, monkeypatch):
     assert t.built_bytes() == full
     assert t.request_plan(swg.MapRequest(K(swg.MANHATTAN, 9, 9), m))["bins_read"] == bins
     t.close()
+
+
+def test_tma_and_thread_stores_build_identical_tables(ctx, oracle, monkeypatch):
+    """The TMA tensor stores of the staged rows (default) and the per-thread
+    stores (SWG_NO_TMA=1, read when a table set first builds) write the same
+    planes: 16- / 32-bit integral sets at widths that do and do not fill the
+    last warp segment, and the decayed set."""
+    for w, h in ((2048, 37), (1000, 23), (257, 64)):
+        img = oracle.random_gray(w, h, w + h)
+        bins = 24
+        tm = {}
+        for env in ("0", "1"):
+            if env == "1":
+                monkeypatch.setenv("SWG_NO_TMA", "1")
+            else:
+                monkeypatch.delenv("SWG_NO_TMA", raising=False)
+            tq = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_QUADRATIC)
+            tp = ctx.build(img, swg.FMT_GRAY8, bins, swg.PLANES_PLAIN)
+            td = ctx.build_decay(img, 0.9375, swg.FMT_GRAY8, bins)
+            tm[env] = ([tq.export_u32(k) for k in range(3)], tp.export_u32(0),
+                       [td.export_f64(k) for k in range(4)])
+            for t in (tq, tp, td):
+                t.close()
+        a, b = tm["0"], tm["1"]
+        assert all((x == y).all() for x, y in zip(a[0], b[0]))
+        assert (a[1] == b[1]).all()
+        assert all((x == y).all() for x, y in zip(a[2], b[2]))
+        fi = oracle.quantize_gray8(img, bins)
+        p, _, _ = oracle.build_tables(fi, bins)
+        assert (a[1] == p.astype(np.uint32)).all()

@@ -153,7 +153,7 @@ def test_profiles_traffic_entries_resolve():
         wl = bench.workload(cfg)
         sizes = {f"{k.kw}x{k.kh}" for g in wl["groups"] for k, _, _, _ in g["scales"]}
         for e in entries if isinstance(entries, list) else [entries]:
-            assert e["kernel"].startswith("k_sweep_"), e
+            assert e["kernel"].startswith(("k_sweep_", "k_stream_")), e
             scale = re.search(r"\((\d+x\d+) scale", e["kernel"]).group(1)
             assert scale in sizes, (cfg, scale)
             src = os.path.join(root, e["source"])
