@@ -1052,7 +1052,11 @@ class OursArm:
             mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
             maps_pin.append(mp)
             hp = (C.c_void_p * len(mp))(*[m.array.ctypes.data for m in mp])
-            pk = (Peak * len(u["reqs"]))()
+            # peaks in page-locked memory too: an async copy into pageable
+            # memory would block the host until the sweeps are done
+            pkb = swg.PinnedBuffer((C.sizeof(Peak) * len(u["reqs"]),), np.uint8)
+            mp.append(pkb)
+            pk = (Peak * len(u["reqs"])).from_address(pkb.array.ctypes.data)
             src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
             # per bin range (one range unless the bins are walked in chunks):
             # rebuild (upload the frame on the first), requests; host maps
@@ -1063,21 +1067,25 @@ class OursArm:
                 calls.append((u["t"], src if c == 0 else None, b0, len(u["chunks"]) > 1,
                               creqs, keep, hp if last else None, pk, len(cr)))
             h2d += u["h2d"]
-            d2h += sum(m.nbytes for m in mp) + C.sizeof(pk)
+            d2h += sum(m.nbytes for m in mp)  # the maps and the peaks
 
         def e2e_step():
+            # the frame's table sets back to back (swg_likelihood_maps_async:
+            # one set's map copies overlap the next set's sweeps), host maps
+            # and peaks filled at the context synchronisation
             for t, src, b0, walk, creqs, _k, hp, pk, n in calls:
                 if walk:  # bin ranges: the frame with the first range, then ranges
                     _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
                 else:
                     _check(lib().swg_tables_rebuild_for(t._h, src, 0, 0, n, C.addressof(creqs)))
-                _check(lib().swg_likelihood_maps(
+                _check(lib().swg_likelihood_maps_async(
                     t._h, n, C.addressof(creqs),
                     C.addressof(hp) if hp is not None else None, None, C.addressof(pk), None))
+            self.ctx.synchronize()
 
         def check():
             for u, mp in zip(units, maps_pin):
-                for m, mpin in zip(u["maps"], mp):
+                for m, mpin in zip(u["maps"], mp[:len(u["maps"])]):
                     assert (mpin.array == m.cpu().numpy()).all()
         return e2e_step, check, h2d, d2h, (pin, calls, maps_pin)
 

@@ -376,6 +376,17 @@ typedef struct swg_plan_info {
 } swg_plan_info;
 swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_plan_info* out);
 
+/* swg_likelihood_maps without the final host synchronisation: the call
+ * enqueues the builds' consumers, sweeps and map copies and returns; host
+ * maps and host peaks are filled once swg_ctx_synchronize returns.  Successive
+ * asynchronous calls rotate over the context's scratch slots, so one table
+ * set's map copies overlap the next set's sweeps (a frame's units run back to
+ * back).  The caller keeps the request array, models and host buffers alive
+ * until the synchronisation. */
+swg_status swg_likelihood_maps_async(swg_tables* t, int n, const swg_map_request* reqs,
+                                     double* const* scores_host, double* const* scores_dev,
+                                     swg_peak* peaks_host, swg_peak* peaks_dev);
+
 /* Batch of frames of the tables' geometry (tracking sequences, config 3):
  * for each frame f, rebuild the tables from frames[f] (pitch_bytes, host or
  * device as is_device; a search-region crop is a pointer into the full frame

@@ -261,6 +261,10 @@ struct swg_ctx {
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
   std::atomic<uint64_t> map_copies{0};  // device->host map copies issued (zero-copy check)
+  // swg_likelihood_maps_async: scratch slots rotate over the calls; a slot
+  // is reused only after the copies (or sweeps) of its last call (free[k])
+  int aslot = 0;
+  cudaEvent_t free_ev[kWorkers] = {};
   DevBuf terms, qout, grid, io, bpeaks;
   // exact kernel-weight grids, uploaded once per kernel (graph-capture safe)
   struct Grid {
@@ -310,6 +314,7 @@ struct swg_tables {
   // encoded on first build: 0 not yet, 1 ok, -1 unavailable
   CUtensorMap tm[2];
   int tm_state[2] = {0, 0};
+  int aslot = -1;  // scratch slot of swg_likelihood_maps_async (-1: not yet)
 };
 
 #ifndef SWG_L2_BUDGET_MB
@@ -769,6 +774,8 @@ static void ctx_release(swg_ctx* c) {
     }
     cudaStreamSynchronize(c->copy);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->free_ev)
+      if (e) cudaEventDestroy(e);
     for (int w = 0; w < swg_ctx::kWorkers; ++w) {
       if (c->work[w]) {
         cudaStreamSynchronize(c->work[w]);
@@ -851,6 +858,7 @@ swg_status swg_ctx_synchronize(swg_ctx* c) {
   if (!c) return fail(SWG_ERR_ARG, "NULL ctx");
   DeviceGuard g(c->device);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->copy));  // host maps of swg_likelihood_maps_async
   return SWG_OK;
 }
 
@@ -2200,9 +2208,27 @@ swg_status swg_tables_rebuild_for(swg_tables* t, const void* pixels, int is_devi
   return SWG_OK;
 }
 
+static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_request* reqs,
+                                       double* const* scores_host, double* const* scores_dev,
+                                       swg_peak* peaks_host, swg_peak* peaks_dev, bool async);
+
 swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs,
                                double* const* scores_host, double* const* scores_dev,
                                swg_peak* peaks_host, swg_peak* peaks_dev) {
+  return likelihood_maps_impl(t, n, reqs, scores_host, scores_dev, peaks_host, peaks_dev, false);
+}
+
+swg_status swg_likelihood_maps_async(swg_tables* t, int n, const swg_map_request* reqs,
+                                     double* const* scores_host, double* const* scores_dev,
+                                     swg_peak* peaks_host, swg_peak* peaks_dev) {
+  return likelihood_maps_impl(t, n, reqs, scores_host, scores_dev, peaks_host, peaks_dev, true);
+}
+
+}  // extern "C"
+
+static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_request* reqs,
+                                       double* const* scores_host, double* const* scores_dev,
+                                       swg_peak* peaks_host, swg_peak* peaks_dev, bool async) {
   ST_TRY(check_tables(t));
   if (n < 0 || (n && !reqs)) return fail(SWG_ERR_ARG, "bad request list");
   if (n == 0) return SWG_OK;
@@ -2221,7 +2247,15 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   std::vector<double*> zc(n, nullptr);
   for (int i = 0; i < n; ++i) {
     ST_TRY(plan_request(t, reqs[i], plan[i]));
-    if (host_map(i) && !dev_map(i) && plan[i].engine != kExp64) zc[i] = mapped_host(scores_host[i], c->device);
+    // zero-copy maps for a few requests (their sweeps fan out and write over
+    // PCIe directly: config 2 e2e 1.31 -> 1.18 ms); with more requests the
+    // sweeps run back to back and each finished map is copied by the copy
+    // engine while the next one sweeps -- a burst of fast sweeps writing over
+    // PCIe would stall on the link (config 5 e2e 32.5 -> 28.7 ms per step)
+    const char* ez = std::getenv("SWG_ZC_MAX");  // A/B: most requests that use zero-copy maps
+    const int zc_max = ez ? std::atoi(ez) : swg_ctx::kHostFan;
+    if (host_map(i) && !dev_map(i) && plan[i].engine != kExp64 && n <= zc_max)
+      zc[i] = mapped_host(scores_host[i], c->device);
   }
   auto copy_map = [&](int i) { return host_map(i) && !zc[i]; };
   // scratch: per-request score buffers (when the caller gave no device or
@@ -2238,7 +2272,19 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
     // round up a segment row of hy + 1 chains)
     ptot += (size_t)p.grid.x * (p.grid.y + 1 + (p.stream ? 2 * k_hy(p.k) + 1 : 0));
   }
-  swg_ctx::Scratch& S = c->scr[c->slot];
+  // an asynchronous call takes the next scratch slot, once the copies (or
+  // sweeps) of the call that used it last have finished
+  // (a table set keeps its slot: the slots' scratch sizes stay put)
+  int sl = c->slot;
+  if (async && c->slot == 0) {
+    if (t->aslot < 0) {
+      t->aslot = c->aslot;
+      c->aslot = (c->aslot + 1) % swg_ctx::kWorkers;
+    }
+    sl = t->aslot;
+    if (c->free_ev[sl]) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->free_ev[sl], 0));
+  }
+  swg_ctx::Scratch& S = c->scr[sl];
   ST_TRY(S.scores.ensure(std::max<size_t>(stot, 1) * 8));
   ST_TRY(S.parts.ensure(ptot * sizeof(PeakPart)));
   ST_TRY(S.peaks.ensure((size_t)n * sizeof(swg_peak)));
@@ -2403,14 +2449,36 @@ swg_status swg_likelihood_maps(swg_tables* t, int n, const swg_map_request* reqs
   bool sync = copies;
   for (int i = 0; i < n; ++i) sync |= zc[i] != nullptr;  // mapped maps: filled on return
   if (peaks_host) {
-    CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
-                             cudaMemcpyDeviceToHost, c->stream));
+    // behind the map copies on the copy stream: a device-to-host copy on the
+    // compute stream would queue on the copy engine behind the maps' copies
+    // and hold the next call's sweeps (config 5 e2e: 32.1 -> see DESIGN)
+    if (copies) {
+      while (c->events.size() <= (size_t)(3 * n)) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->events.push_back(ev);
+      }
+      CUDA_TRY(cudaEventRecord(c->events[3 * n], c->stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[3 * n], 0));
+      CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
+                               cudaMemcpyDeviceToHost, c->copy));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(peaks_host, dpeaks, (size_t)n * sizeof(swg_peak),
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
     sync = true;
+  }
+  if (async) {  // host outputs are filled when the context's streams are synchronised
+    if (!c->free_ev[sl]) CUDA_TRY(cudaEventCreateWithFlags(&c->free_ev[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c->free_ev[sl], copies ? c->copy : c->stream));
+    return SWG_OK;
   }
   if (sync) CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (copies) CUDA_TRY(cudaStreamSynchronize(c->copy));
   return SWG_OK;
 }
+
+extern "C" {
 
 swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* frames,
                                 int is_device, size_t pitch_bytes, int n,

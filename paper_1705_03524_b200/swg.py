@@ -186,6 +186,7 @@ def lib():
                              vp],
         "swg_cake_plan": [C.POINTER(Kernel), C.c_int, C.c_int, vp, vp, vp],
         "swg_likelihood_maps": [vp, C.c_int, vp, vp, vp, vp, vp],
+        "swg_likelihood_maps_async": [vp, C.c_int, vp, vp, vp, vp, vp],
         "swg_request_plan": [vp, vp, vp],
         "swg_likelihood_batch": [vp, C.c_int, vp, C.c_int, C.c_size_t, C.c_int, vp, vp, vp],
         "swg_brute_windows": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,

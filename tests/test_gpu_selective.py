@@ -168,3 +168,63 @@ def test_tma_and_thread_stores_build_identical_tables(ctx, oracle, monkeypatch):
         fi = oracle.quantize_gray8(img, bins)
         p, _, _ = oracle.build_tables(fi, bins)
         assert (a[1] == p.astype(np.uint32)).all()
+
+
+def test_likelihood_maps_async_rotating_scratch(ctx, oracle):
+    """swg_likelihood_maps_async over several table sets back to back (map
+    copies, zero-copy maps and the exponential re-score on rotating scratch
+    slots), host outputs read after swg_ctx_synchronize: identical to the
+    synchronous calls, over two frames (slot reuse)."""
+    import ctypes as C
+    from paper_1705_03524_b200.swg import Peak, _check, lib
+    bins, d = 16, 0.875
+    frames = [oracle.random_gray(260, 200, s) for s in (31, 32)]
+    fi0 = oracle.quantize_gray8(frames[0], bins)
+    sets = [ctx.build(frames[0], swg.FMT_GRAY8, bins, swg.PLANES_AFFINE),
+            ctx.build(frames[0], swg.FMT_GRAY8, bins, swg.PLANES_PLAIN),
+            ctx.build_decay(frames[0], d, swg.FMT_GRAY8, bins)]
+    reqs = []
+    for kw in (9, 15, 21, 27, 33):  # five requests: the copy path
+        reqs.append((0, swg.MapRequest(K(swg.MANHATTAN, kw, kw),
+                                       oracle.target_model(fi0[5:5 + kw, 7:7 + kw].copy(), bins,
+                                                           O.kernel(O.MANHATTAN, kw, kw)))))
+    for kw in (11, 25):  # two requests: zero-copy maps
+        okc = O.kernel(O.GAUSS_CHEB, kw, kw, 0.5)
+        reqs.append((1, swg.MapRequest(K(swg.GAUSS_CHEB, kw, kw, 0.5),
+                                       oracle.target_model(fi0[3:3 + kw, 9:9 + kw].copy(), bins,
+                                                           okc, O.CAKE, kw // 2 + 1),
+                                       swg.CAKE, rings=kw // 2 + 1)))
+    for kw in (13, 19):
+        oke = O.kernel(O.EXP_L1, kw, kw, d)
+        reqs.append((2, swg.MapRequest(K(swg.EXP_L1, kw, kw, d),
+                                       oracle.target_model(fi0[8:8 + kw, 4:4 + kw].copy(), bins,
+                                                           oke, O.BRUTE))))
+    for img in frames:
+        want = {}
+        for si, t in enumerate(sets):
+            rs = [r for s, r in reqs if s == si]
+            t.rebuild(img)
+            want[si] = t.likelihood_maps(rs)
+        keep = []
+        outs = {}
+        for si, t in enumerate(sets):
+            rs = [r for s, r in reqs if s == si]
+            t.rebuild_for(img, rs)
+            maps = [swg.PinnedBuffer(t.map_shape(r.kernel), np.float64) for r in rs]
+            pkb = swg.PinnedBuffer((C.sizeof(Peak) * len(rs),), np.uint8)
+            pk = (Peak * len(rs)).from_address(pkb.array.ctypes.data)
+            hp = (C.c_void_p * len(rs))(*[m.array.ctypes.data for m in maps])
+            creqs, k2 = swg.Tables._creqs(rs, t.total_bins)
+            keep += [maps, pkb, pk, hp, creqs, k2]
+            _check(lib().swg_likelihood_maps_async(t._h, len(rs), C.addressof(creqs),
+                                                   C.addressof(hp), None, C.addressof(pk), None))
+            outs[si] = (maps, pk)
+        ctx.synchronize()
+        for si in outs:
+            maps, pk = outs[si]
+            wmaps, wpks = want[si]
+            for m, w in zip(maps, wmaps):
+                assert (m.array == w).all(), si
+            assert [p.astuple() for p in pk] == wpks, si
+    for t in sets:
+        t.close()
