@@ -1240,9 +1240,18 @@ class OursArm:
                 if roofline["traffic"] is not None:
                     break
         if dom.startswith("k_sweep_cake"):
+            # the ring telescope reads 4 corner records per ring, octet and
+            # window from L1 (O(rings*b) on-chip bytes per window):
+            # its roofline is the L1 data pipe, measured by ncu on one launch
+            # (profiles/onchip.json), not HBM
             roofline["onchip"] = {"note": "the wedding-cake sweep is bound by the L1 -> register "
                                           "data path (ring corners, O(rings*bins) per window), "
-                                          "not HBM: see profiles/ for its L1 utilisation"}
+                                          "not HBM"}
+            op = os.path.join(ROOT, "profiles", "onchip.json")
+            if os.path.exists(op):
+                oc = json.load(open(op)).get(self.args.config)
+                if oc:
+                    roofline["onchip"].update(oc)
         return roofline
 
     def cpu_baseline(self):
