@@ -2277,9 +2277,9 @@ static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_reque
   // (a table set keeps its slot: the slots' scratch sizes stay put)
   int sl = c->slot;
   if (async && c->slot == 0) {
-    if (t->aslot < 0) {
-      t->aslot = c->aslot;
-      c->aslot = (c->aslot + 1) % swg_ctx::kWorkers;
+    if (t->aslot < 0) {  // slots 1.. (slot 0 stays the synchronous calls')
+      t->aslot = 1 + c->aslot;
+      c->aslot = (c->aslot + 1) % (swg_ctx::kWorkers - 1);
     }
     sl = t->aslot;
     if (c->free_ev[sl]) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->free_ev[sl], 0));
@@ -2527,7 +2527,11 @@ swg_status swg_likelihood_batch(swg_tables* t, int n_frames, const void* const* 
   {
     DeviceGuard g(c->device);
     CUDA_TRY(cudaEventRecord(c->fork, orig));
-    for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(c->work[k], c->fork, 0));
+    for (int k = 0; k < K; ++k) {
+      CUDA_TRY(cudaStreamWaitEvent(c->work[k], c->fork, 0));
+      // scratch slot k may still feed an asynchronous call's map copies
+      if (c->free_ev[k]) CUDA_TRY(cudaStreamWaitEvent(c->work[k], c->free_ev[k], 0));
+    }
   }
   c->fanout_off = true;
   for (int f = 0; f < n_frames; ++f) {
