@@ -579,6 +579,7 @@ class OursArm:
         data, groups = self.data, self.wl["groups"]
         frame_dev = torch.from_numpy(data.image).cuda()
         H, W = data.image.shape[:2]
+        measured = self._measure_costs(groups, frame_dev) if self.dist else None
         reqs_all = []
         build = []
         for gi, g in enumerate(groups):
@@ -595,7 +596,15 @@ class OursArm:
             # a model-driven rebuild writes only the units the requests read
             frac = len(union) / max(1, -(-self.nb // (2 if g["planes"] == swg.PLANES_DECAY else 8)))
             build.append(full if not union else 0.1 + (full - 0.1) * min(1.0, frac))
+        if measured is not None:  # rank 0's timings, the same on every rank
+            req_ms, build_ms = measured
+            reqs_all = [(key, gi, mh, req_ms[i]) for i, (key, gi, mh, _) in enumerate(reqs_all)]
+            build = build_ms
         self.plan = D.plan_frame(reqs_all, build, self.world, min_rows=8)
+        # each rank's planned load (ms): its requests + the builds of its sets
+        self.plan_load = [round(sum(w.cost for w in p) + sum(build[g] for g in {w.group for w in p}), 3)
+                          for p in self.plan]
+        self.plan_costs = "measured (rank 0, broadcast)" if measured is not None else "estimated"
         mine = self.plan[self.rank]
         for gi, (g, ms) in enumerate(zip(groups, self.models)):
             work = [w for w in mine if w.group == gi]
@@ -614,6 +623,46 @@ class OursArm:
                                    sidx=[w.key[1] for w in work],
                                    rows=[w.rows for w in work], h2d=data.image.nbytes))
         self.tab_w, self.tab_h = W, H
+
+    def _measure_costs(self, groups, frame_dev):
+        """Multi-GPU plan costs measured, not estimated: rank 0 times every
+        request's full map and every table set's model-driven rebuild on its
+        GPU (eager, CUDA events, median of 3) and broadcasts them, so every
+        rank derives the same partition (setup only, outside the timed step).
+        Returns ([ms per request in group/scale order], [build ms per group])."""
+        torch = self.torch
+        n_req = sum(len(g["scales"]) for g in groups)
+        dev = "cpu" if self.share else "cuda"
+        costs = torch.zeros(n_req + len(groups), dtype=torch.float64, device=dev)
+        if self.rank == 0:
+            vals, builds = [], []
+
+            def timed(fn, reps=3):
+                ts = []
+                for _ in range(reps + 1):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    fn()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1))
+                return sorted(ts[1:])[len(ts[1:]) // 2]
+
+            for gi, g in enumerate(groups):
+                t = self.new_tables(g, frame_dev)
+                reqs = self._requests(g, self.models[gi])
+                maps = self._map_buffers(t, reqs)
+                peaks = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
+                builds.append(timed(lambda: t.rebuild_for(frame_dev, reqs)))
+                for i, r in enumerate(reqs):
+                    vals.append(timed(lambda: t.likelihood_maps([r], scores="none",
+                                                                 scores_dev=[maps[i]],
+                                                                 peaks_dev=peaks[i])))
+                t.close()
+            costs.copy_(torch.tensor(vals + builds, dtype=torch.float64))
+        self.dist.broadcast(costs, 0)
+        c = costs.cpu().tolist()
+        return c[:n_req], c[n_req:]
 
     def _sequence_units(self):
         """c3: this rank's frames, each a search region swept on one table set."""
@@ -1305,6 +1354,8 @@ class OursArm:
                             if wl["kind"] == "frame" else
                             f"{wl['kind']} sharded over {self.world} GPU(s), no collective"),
             "tables": {"shape": [self.tab_w, self.tab_h], "units_rank0": len(self.units)},
+            "plan": ({"load_ms_per_rank": self.plan_load, "costs": self.plan_costs}
+                     if getattr(self, "plan_load", None) else None),
             "ih_build": ({"ms": ih["ms_per_step"], "gbps": ih["gbps"], "frac": ih["hbm_frac"],
                           "bytes": ih["bytes_per_step"]} if ih else None),
             "per_scale_ms": per_scale,
