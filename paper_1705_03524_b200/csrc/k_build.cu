@@ -24,6 +24,7 @@
 #include "swg_internal.cuh"
 
 #include <cstdlib>
+#include <cstring>
 
 namespace swg {
 
@@ -135,6 +136,11 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
   const int band = blockIdx.x, grp0 = blockIdx.y * G;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
+  if (g.nsel) {  // selective build: octets no sweep reads need no carries
+    bool any = false;
+    for (int k = 0; k < G && !any; ++k) any = grp0 + k < g.groups && sel_has(g.selmask, g.nsel, grp0 + k);
+    if (!any) return;
+  }
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
   const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp0 * kOct;
   const uint32_t lim = (uint32_t)(g.bins - grp0 * kOct);  // bins of these octets in range
@@ -181,10 +187,11 @@ __global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
 // K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
 // One warp per uint4 column of the carry array: the lanes hold 32 bands at a
 // time and a shuffle scan combines them (all loads of a batch in flight).
-__global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t per_band) {
+__global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t per_band,
+                                                  const SelMask m) {
   const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (col >= per_band) return;
+  if (col >= per_band || m.skip(col)) return;
   uint4 run = make_uint4(0, 0, 0, 0);
   for (int b0 = 0; b0 < nbands; b0 += 32) {
     const int b = b0 + lane;
@@ -215,9 +222,10 @@ __global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t
 // warp-per-word shuffle scan above keeps 32 lanes busy per word, but with a
 // few dozen bands most lanes idle and the shuffles throttle the MIO pipe
 // (config 5: 53 us for 58 MB).
-__global__ void __launch_bounds__(256) k_bandscan_seq(uint4* agg, int nbands, size_t per_band) {
+__global__ void __launch_bounds__(256) k_bandscan_seq(uint4* agg, int nbands, size_t per_band,
+                                                      const SelMask m) {
   const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (col >= per_band) return;
+  if (col >= per_band || m.skip(col)) return;
   uint4 run = make_uint4(0, 0, 0, 0);
   constexpr int kB = 8;
   for (int b0 = 0; b0 < nbands; b0 += kB) {
@@ -652,13 +660,17 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t per_band = (size_t)a.groups * a.wa * a.aw / 4;
+  SelMask m{};
+  m.on = a.nsel > 0;
+  m.words_per_unit = a.wa * a.aw / 4;
+  std::memcpy(m.w, a.selmask, sizeof(m.w));
   const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
   if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
     k_bandscan<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
+        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m);
   else
     k_bandscan_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band);
+        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 namespace swg {
 
@@ -64,6 +65,11 @@ __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real de
   const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
   const int x = blockIdx.z * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
+  if (g.nsel) {  // selective build: pairs no sweep reads need no carries
+    bool any = false;
+    for (int k = 0; k < kColPairs && !any; ++k) any = pr0 + k < pairs && sel_has(g.selmask, g.nsel, pr0 + k);
+    if (!any) return;
+  }
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
   const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr0 * kDP;
   const uint32_t lim = (uint32_t)max(g.bins - pr0 * kDP, 0);  // bins of these pairs in range
@@ -88,10 +94,10 @@ __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real de
 // one warp per column word, lanes = 32 bands, affine shuffle scan.
 __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, int band_h,
                                                         int h, real dband, real dlast,
-                                                        size_t per_band) {
+                                                        size_t per_band, const SelMask m) {
   const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (col >= per_band) return;
+  if (col >= per_band || m.skip(col)) return;
   real run = 0.0;
   for (int b0 = 0; b0 < nbands; b0 += 32) {
     const int b = b0 + lane;
@@ -118,9 +124,10 @@ __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, i
 // K1b', sequential form: one thread per column word walks the bands in order
 // (loads of 8 bands in flight); see k_bandscan_seq.
 __global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nbands, real dband,
-                                                            real dlast, size_t per_band) {
+                                                            real dlast, size_t per_band,
+                                                            const SelMask m) {
   const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (col >= per_band) return;
+  if (col >= per_band || m.skip(col)) return;
   real run = 0.0;
   constexpr int kB = 8;
   for (int b0 = 0; b0 < nbands; b0 += kB) {
@@ -349,13 +356,17 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     const size_t per_band = (size_t)pairs * a.wa * kDP;
     const double dband = std::pow(dec, (double)a.band_h);
     const double dlast = std::pow(dec, (double)(a.h - (a.nbands - 1) * a.band_h));
+    SelMask m{};
+    m.on = a.nsel > 0;
+    m.words_per_unit = a.wa * kDP;
+    std::memcpy(m.w, a.selmask, sizeof(m.w));
     const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
     if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
       k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band);
+          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band, m);
     else
       k_bandscan_decay_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band);
+          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band, m);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }

@@ -394,7 +394,10 @@ swg_status run_build(swg_tables* t, T* out, const std::vector<int>* sel = nullpt
   a = BuildArgs{};
   if (sel) {
     a.nsel = (int)sel->size();
-    for (int i = 0; i < a.nsel; ++i) a.sel[i] = (unsigned short)(*sel)[i];
+    for (int i = 0; i < a.nsel; ++i) {
+      a.sel[i] = (unsigned short)(*sel)[i];
+      a.selmask[(*sel)[i] >> 5] |= 1u << ((*sel)[i] & 31);
+    }
     if (a.nsel == 0) return SWG_OK;
   }
   a.fi = t->fi;
@@ -607,7 +610,10 @@ swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr)
   a = BuildArgs{};
   if (sel) {
     a.nsel = (int)sel->size();
-    for (int i = 0; i < a.nsel; ++i) a.sel[i] = (unsigned short)(*sel)[i];
+    for (int i = 0; i < a.nsel; ++i) {
+      a.sel[i] = (unsigned short)(*sel)[i];
+      a.selmask[(*sel)[i] >> 5] |= 1u << ((*sel)[i] & 31);
+    }
   }
   a.fi_pitch = t->fip;
   a.out = t->tdec;

@@ -80,6 +80,8 @@ struct alignas(64) BuildArgs {
   // slot of the full layout; the carries (K1a/K1b) still cover every unit.
   int nsel;
   unsigned short sel[kMaxBins / kDP];
+  // the same selection as a bit mask (carry passes skip unselected units)
+  uint32_t selmask[kMaxBins / kDP / 32];
   uint32_t* agg;       // [nbands][groups][wa][aw]: per column, 8 bin counts +
                        // 8 bin y-sums (+ 8 bin y^2-sums) of the band (K1a),
                        // then of all rows above the band (K1b, exclusive scan)
@@ -409,6 +411,21 @@ constexpr int kStreamWarps = SWG_STREAM_WARPS, kStreamThreads = 32 * kStreamWarp
 constexpr int kStreamCols = 32 * kStreamWarps;
 // Brute-force sweep: one thread per window.
 constexpr int kBruteThreads = 128;
+
+// A selective build's unit mask for the band-carry scans (by value).
+struct SelMask {
+  uint32_t w[kMaxBins / kDP / 32];
+  int on;              // 0: every unit
+  size_t words_per_unit;  // carry words of one unit per band
+  __device__ __forceinline__ bool skip(size_t col) const {
+    if (!on) return false;
+    const size_t u = col / words_per_unit;
+    return !((w[u >> 5] >> (u & 31)) & 1u);
+  }
+};
+__host__ __device__ inline bool sel_has(const uint32_t* m, int nsel, int u) {
+  return nsel == 0 || ((m[u >> 5] >> (u & 31)) & 1u);
+}
 
 // Encode a row tensor map for TMA stores (swg_abi.cu): planes of records of
 // rec_bytes, base = record 1 of row 0 of plane 0, box = box_lines 128-byte
