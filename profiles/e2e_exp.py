@@ -1,12 +1,18 @@
 """End-to-end strategies for config 5 (tuning driver, not a bench line):
     python profiles/e2e_exp.py
-Times one step (pinned frame in, every map + peak out to host memory) with
-  zc      : mapped pinned host maps through swg_likelihood_maps (the bench's
-            e2e path), unit by unit
-  dev+cp  : device maps, each unit's maps copied to pinned host memory on a
-            copy stream behind the unit's sweeps, one sync per step
-for several unit orders."""
-import itertools
+Times one frame through the three table sets -- pinned frame in, every map
+and peak out to page-locked host memory -- as
+  req+cp    : one swg_likelihood_maps call per request with a device map,
+              each map copied to the host on a copy stream right behind its
+              sweep (the overlap target)
+  lib_sync  : swg_likelihood_maps per table set with host maps (copy path,
+              host synchronisation at the end of every call)
+  lib_async : swg_likelihood_maps_async per table set, one
+              swg_ctx_synchronize per frame (bench.py's e2e path)
+and prints, for the library paths, when each set's work ends on the
+compute stream (a device-to-host copy queued on the compute stream shows
+up as a set ending at its copies' end instead of its sweeps')."""
+import ctypes as C
 import os
 import sys
 import time
@@ -17,6 +23,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_1705_03524_b200 import swg  # noqa: E402
+from paper_1705_03524_b200.swg import Peak, _check, lib  # noqa: E402
 
 wl = bench.workload("c5")
 data = wl["gen"](1)
@@ -28,62 +35,29 @@ copy = torch.cuda.Stream()
 models = bench.make_models(ctx, wl, data)
 pin = swg.PinnedBuffer(data.image.shape, data.image.dtype)
 pin.array[...] = data.image
+frame = torch.from_numpy(data.image).cuda()
 units = []
 for gi, g in enumerate(wl["groups"]):
-    if g.get("decay"):
-        t = ctx.build_decay(torch.from_numpy(data.image).cuda(), g["decay"], wl["fmt"], wl["bins"])
-    else:
-        t = ctx.build(torch.from_numpy(data.image).cuda(), wl["fmt"], wl["bins"], g["planes"])
+    t = (ctx.build_decay(frame, g["decay"], wl["fmt"], wl["bins"]) if g.get("decay")
+         else ctx.build(frame, wl["fmt"], wl["bins"], g["planes"]))
     reqs = [swg.MapRequest(k, m, meth, swg.BHATTACHARYYA, rings)
             for (k, meth, rings, _), m in zip(g["scales"], models[gi])]
-    dmaps = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda") for r in reqs]
-    hmaps = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in dmaps]
-    hmaps_t = [torch.from_numpy(h.array) for h in hmaps]
-    peaks = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
-    units.append(dict(t=t, reqs=reqs, dmaps=dmaps, hmaps=hmaps, hmaps_t=hmaps_t, peaks=peaks,
-                      name=g["scales"][0][0].kind))
+    u = dict(t=t, reqs=reqs)
+    u["dmaps"] = [torch.empty(t.map_shape(r.kernel), dtype=torch.float64, device="cuda")
+                  for r in reqs]
+    u["hmaps"] = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["dmaps"]]
+    u["hmaps_t"] = [torch.from_numpy(h.array) for h in u["hmaps"]]
+    u["peaks"] = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
+    u["creqs"], u["keep"] = swg.Tables._creqs(reqs, t.total_bins)
+    u["hp"] = (C.c_void_p * len(reqs))(*[h.array.ctypes.data for h in u["hmaps"]])
+    u["pkb"] = swg.PinnedBuffer((C.sizeof(Peak) * len(reqs),), np.uint8)
+    u["pk"] = (Peak * len(reqs)).from_address(u["pkb"].array.ctypes.data)
+    units.append(u)
+marks = []
 
 
-def step_zc(order):
-    for i in order:
-        u = units[i]
-        u["t"].rebuild_for(pin.array, u["reqs"])
-        _zc(u)
-
-
-def _zc(u):
-    import ctypes as C
-    from paper_1705_03524_b200.swg import Peak, _check, lib
-    creqs, keep = swg.Tables._creqs(u["reqs"], u["t"].total_bins)
-    hp = (C.c_void_p * len(u["hmaps"]))(*[h.array.ctypes.data for h in u["hmaps"]])
-    pk = (Peak * len(u["reqs"]))()
-    _check(lib().swg_likelihood_maps(u["t"]._h, len(u["reqs"]), C.addressof(creqs),
-                                     C.addressof(hp), None, C.addressof(pk), None))
-
-
-def step_dev(order):
-    for i in order:
-        u = units[i]
-        u["t"].rebuild_for(pin.array, u["reqs"])
-        u["t"].likelihood_maps(u["reqs"], scores="none", scores_dev=u["dmaps"],
-                               peaks_dev=u["peaks"])
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        copy.wait_event(ev)
-        with torch.cuda.stream(copy):
-            for d, h in zip(u["dmaps"], u["hmaps_t"]):
-                h.copy_(d, non_blocking=True)
-    torch.cuda.synchronize()
-
-
-def step_req(order):
-    e0 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    evs = []
-    for i in order:
-        if evs is not None and i != order[0]:
-            pass
-        u = units[i]
+def step_req():
+    for u in units:
         u["t"].rebuild_for(pin.array, u["reqs"])
         for j, r in enumerate(u["reqs"]):
             u["t"].likelihood_maps([r], scores="none", scores_dev=[u["dmaps"][j]],
@@ -93,102 +67,38 @@ def step_req(order):
             copy.wait_event(ev)
             with torch.cuda.stream(copy):
                 u["hmaps_t"][j].copy_(u["dmaps"][j], non_blocking=True)
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
-        evs.append(ev)
     torch.cuda.synchronize()
-    EV.append([round(e0.elapsed_time(e), 2) for e in evs])
 
 
-import ctypes as C  # noqa: E402
-from paper_1705_03524_b200.swg import Peak, _check, lib  # noqa: E402
-for u in units:
-    u["creqs"], u["keep"] = swg.Tables._creqs(u["reqs"], u["t"].total_bins)
-    u["hp"] = (C.c_void_p * len(u["hmaps"]))(*[h.array.ctypes.data for h in u["hmaps"]])
-    u["pkb"] = swg.PinnedBuffer((C.sizeof(Peak) * len(u["reqs"]),), np.uint8)
-    u["pk"] = (Peak * len(u["reqs"])).from_address(u["pkb"].array.ctypes.data)
-
-
-HT = []
-
-
-EV = []
-
-
-def step_lib(order, fn_name):
-    t0 = time.perf_counter()
-    ht = []
+def step_lib(fn_name):
     e0 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    evs = [e0]
-    for i in order:
-        u = units[i]
+    ends = []
+    for u in units:
         u["t"].rebuild_for(pin.array, u["reqs"])
-        ht.append(time.perf_counter() - t0)
         _check(getattr(lib(), fn_name)(u["t"]._h, len(u["reqs"]), C.addressof(u["creqs"]),
                                        C.addressof(u["hp"]), None, C.addressof(u["pk"]), None))
-        ht.append(time.perf_counter() - t0)
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
-        evs.append(ev)
+        ends.append(ev)
     ctx.synchronize()
-    EV.append([round(e0.elapsed_time(e), 2) for e in evs[1:]])
-    ht.append(time.perf_counter() - t0)
-    HT.append(ht)
-
-
-def step_libdev(order):
-    for i in order:
-        u = units[i]
-        u["t"].rebuild_for(pin.array, u["reqs"])
-        u["t"].likelihood_maps(u["reqs"], scores="none", scores_dev=u["dmaps"], peaks_dev=u["peaks"])
-        for d, h in zip(u["dmaps"], u["hmaps_t"]):
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            copy.wait_event(ev)
-            with torch.cuda.stream(copy):
-                h.copy_(d, non_blocking=True)
-    torch.cuda.synchronize()
-
-
-for u in units:
-    u["creq1"] = [swg.Tables._creqs([r], u["t"].total_bins) for r in u["reqs"]]
-    u["hp1"] = [(C.c_void_p * 1)(h.array.ctypes.data) for h in u["hmaps"]]
-
-
-def step_lib1(order):
-    for i in order:
-        u = units[i]
-        u["t"].rebuild_for(pin.array, u["reqs"])
-        for j in range(len(u["reqs"])):
-            cr, _k = u["creq1"][j]
-            _check(lib().swg_likelihood_maps_async(u["t"]._h, 1, C.addressof(cr),
-                                                   C.addressof(u["hp1"][j]), None, None,
-                                                   ctypes_peak_dev(u, j)))
-    ctx.synchronize()
-
-
-def ctypes_peak_dev(u, j):
-    return C.c_void_p(u["peaks"][j].data_ptr())
+    marks.append([round(e0.elapsed_time(e), 2) for e in ends])
 
 
 for name, fn in (("req+cp", step_req),
-                 ("lib_sync", lambda o: step_lib(o, "swg_likelihood_maps")),
-                 ("lib_async", lambda o: step_lib(o, "swg_likelihood_maps_async"))):
-    for order in [(0, 1, 2)]:
-        for _ in range(3):
-            fn(order)
+                 ("lib_sync", lambda: step_lib("swg_likelihood_maps")),
+                 ("lib_async", lambda: step_lib("swg_likelihood_maps_async"))):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(8):
+        t0 = time.perf_counter()
+        fn()
         torch.cuda.synchronize()
-        ts = []
-        for _ in range(8):
-            t0 = time.perf_counter()
-            fn(order)
-            torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
-        print(f"{name:7s} order {order}: {1e3 * sorted(ts)[len(ts) // 2]:.2f} ms", flush=True)
-        if HT:
-            print("   host marks (ms):", [round(1e3 * x, 2) for x in HT[-1]])
-            HT.clear()
-        if EV:
-            print("   compute-stream unit ends (ms):", EV[-1])
-            EV.clear()
+        ts.append(time.perf_counter() - t0)
+    line = f"{name:10s} {1e3 * sorted(ts)[len(ts) // 2]:.2f} ms per frame"
+    if marks:
+        line += f"   compute-stream set ends (ms): {marks[-1]}"
+        marks.clear()
+    print(line, flush=True)
