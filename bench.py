@@ -1094,9 +1094,13 @@ class OursArm:
         swg, data, units, nb = self.swg, self.data, self.units, self.nb
         pin = swg.PinnedBuffer(data.image.shape, data.image.dtype)
         pin.array[...] = data.image
+        pin_t = self.torch.from_numpy(pin.array)
+        # the frame is uploaded ONCE per step (pinned -> device, stream
+        # ordered); every table set's rebuild reads the device copy
+        fdev = self.torch.empty(pin_t.shape, dtype=pin_t.dtype, device="cuda")
         row_bytes = data.image.strides[0]
         calls, maps_pin = [], []
-        h2d = d2h = 0
+        h2d, d2h = data.image.nbytes, 0
         for u in units:
             mp = [swg.PinnedBuffer(tuple(m.shape), np.float64) for m in u["maps"]]
             maps_pin.append(mp)
@@ -1106,7 +1110,7 @@ class OursArm:
             pkb = swg.PinnedBuffer((C.sizeof(Peak) * len(u["reqs"]),), np.uint8)
             mp.append(pkb)
             pk = (Peak * len(u["reqs"])).from_address(pkb.array.ctypes.data)
-            src = pin.array.ctypes.data + u.get("p0", 0) * row_bytes
+            src = fdev.data_ptr() + u.get("p0", 0) * row_bytes
             # per bin range (one range unless the bins are walked in chunks):
             # rebuild (upload the frame on the first), requests; host maps
             # and peaks from the last range
@@ -1115,18 +1119,18 @@ class OursArm:
                 last = c == len(u["chunks"]) - 1
                 calls.append((u["t"], src if c == 0 else None, b0, len(u["chunks"]) > 1,
                               creqs, keep, hp if last else None, pk, len(cr)))
-            h2d += u["h2d"]
             d2h += sum(m.nbytes for m in mp)  # the maps and the peaks
 
         def e2e_step():
             # the frame's table sets back to back (swg_likelihood_maps_async:
             # one set's map copies overlap the next set's sweeps), host maps
             # and peaks filled at the context synchronisation
+            fdev.copy_(pin_t, non_blocking=True)
             for t, src, b0, walk, creqs, _k, hp, pk, n in calls:
                 if walk:  # bin ranges: the frame with the first range, then ranges
-                    _check(lib().swg_tables_rebuild_bins(t._h, src, 0, 0, b0))
+                    _check(lib().swg_tables_rebuild_bins(t._h, src, 1 if src else 0, 0, b0))
                 else:
-                    _check(lib().swg_tables_rebuild_for(t._h, src, 0, 0, n, C.addressof(creqs)))
+                    _check(lib().swg_tables_rebuild_for(t._h, src, 1, 0, n, C.addressof(creqs)))
                 _check(lib().swg_likelihood_maps_async(
                     t._h, n, C.addressof(creqs),
                     C.addressof(hp) if hp is not None else None, None, C.addressof(pk), None))
@@ -1136,7 +1140,7 @@ class OursArm:
             for u, mp in zip(units, maps_pin):
                 for m, mpin in zip(u["maps"], mp[:len(u["maps"])]):
                     assert (mpin.array == m.cpu().numpy()).all()
-        return e2e_step, check, h2d, d2h, (pin, calls, maps_pin)
+        return e2e_step, check, h2d, d2h, (pin, calls, maps_pin, fdev, pin_t)
 
     def e2e(self, job_win):
         """The metric through the C-ABI with pinned host input and host outputs,
