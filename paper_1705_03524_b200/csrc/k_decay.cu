@@ -173,6 +173,9 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
   extern __shared__ __align__(1024) double2 s_tile[];
   const bool tma = g.tmap_ok != 0;
   double2* carry = s_tile + kStripRows * kStripW;
+  if (gridDim.y > 1) kind = blockIdx.y;  // all four orientations in one launch
+  const uint16_t* gfi = gridDim.y > 1 ? g.fio[kind] : g.fi;
+  const uint32_t* gagg = g.agg + (gridDim.y > 1 ? (size_t)kind * g.agg_stride : 0);
   const int np = g.nsel ? g.nsel : pairs;  // selective build: the listed pairs
   const int band = blockIdx.x / np, pr = g.nsel ? (int)g.sel[blockIdx.x % np] : blockIdx.x % np;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
     plane[(size_t)(y0 + r + 1) * g.pitch] = zero;
     carry[r] = zero;
   }
-  const double2* agg = reinterpret_cast<const double2*>(g.agg) + ((size_t)band * pairs + pr) * g.wa;
+  const double2* agg = reinterpret_cast<const double2*>(gagg) + ((size_t)band * pairs + pr) * g.wa;
   const int sw = strip_swz(tid);
   auto step = [&](uint32_t v, real& c0, real& c1) {
     c0 = fma(dec, c0, v == gb0 ? 1.0 : 0.0);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
       c1 = v.y;
     }
     // pixel column x of the band (kNoBin beyond the image) and its table column
-    const uint16_t* col = g.fi + (size_t)y0 * g.fi_pitch + (in ? x : 0);
+    const uint16_t* col = gfi + (size_t)y0 * g.fi_pitch + (in ? x : 0);
     const size_t fstep = in ? g.fi_pitch : 0;
     const uint32_t vor = in ? 0u : 0x10000u;  // beyond the image: a value no bin matches
     double2* out = plane + (size_t)(y0 + 1) * g.pitch + x + 1;
@@ -347,7 +350,7 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
                                int* launches) {
   *launches = 0;
   const int pairs = a.groups * (kOct / kDP);
-  if (a.nbands > 1) {
+  if (a.nbands > 1 && kind != -2) {
     dim3 grid((unsigned)a.nbands, (unsigned)((pairs + kColPairs - 1) / kColPairs),
               (unsigned)((a.w + 255) / 256));
     k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs);
@@ -370,7 +373,8 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }
-  const unsigned grid = (unsigned)(a.nbands * (a.nsel ? a.nsel : pairs));
+  if (kind == -1) return cudaSuccess;  // carries only
+  const dim3 grid((unsigned)(a.nbands * (a.nsel ? a.nsel : pairs)), kind == -2 ? 4u : 1u);
   const size_t smem = (size_t)(kStripRows * kStripW + a.band_h) * sizeof(double2);
   if (smem > (200 << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~8500 rows
   // set on every launch: the attribute is per device (a process-wide cache

@@ -315,6 +315,7 @@ struct swg_tables {
   CUtensorMap tm[2];
   int tm_state[2] = {0, 0};
   int aslot = -1;  // scratch slot of swg_likelihood_maps_async (-1: not yet)
+  size_t lb_bytes = 0;
 };
 
 #ifndef SWG_L2_BUDGET_MB
@@ -640,10 +641,30 @@ swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr)
     a.tmap_ok = 1;
   }
   const uint16_t* src[4] = {t->fi, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz};
+  // a selective build has few (band, pair) strips per orientation: the four
+  // orientations' strips go in one launch (each with its own carry array)
+  // so the grid fills the SMs; a full build keeps one launch per orientation
+  // (measured: its orientations' rows compete for L2)
+  const char* ef = std::getenv("SWG_DECAY_FUSE");
+  const bool fuse = ef ? std::atoi(ef) != 0 : (a.nsel > 0 && t->nbands > 1);
+  const size_t stride = t->lb_bytes / 4 / 4;  // uint32 words per orientation
   for (int k = 0; k < 4; ++k) {
     a.fi = src[k];
+    a.fio[k] = src[k];
     int nl = 0;
-    CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
+    if (fuse) {
+      a.agg = t->lb + k * stride;
+      CUDA_TRY(launch_build_decay(a, t->decay, -1, c->stream, &nl));
+    } else {
+      CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
+    }
+    c->launches += (uint64_t)nl;
+  }
+  if (fuse) {
+    a.agg = t->lb;
+    a.agg_stride = stride;
+    int nl = 0;
+    CUDA_TRY(launch_build_decay(a, t->decay, -2, c->stream, &nl));
     c->launches += (uint64_t)nl;
   }
   const size_t units = a.nsel ? (size_t)a.nsel : (size_t)t->groups * (kOct / kDP);
@@ -935,8 +956,11 @@ static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
   // demand); affine and quadratic tables uint32 planes; decay fp64
   const size_t elem = planes == SWG_PLANES_PLAIN ? 2 : planes == SWG_PLANES_DECAY ? 8 : 4;
   const size_t tab_bytes = t->ps * planes * (size_t)t->groups * kOct * elem;
+  // (decayed tables: one carry array per orientation)
   const size_t lb_bytes = (size_t)t->nbands * t->groups * t->wa * kOct *
-                          (planes == SWG_PLANES_QUADRATIC ? 12 : 8);
+                          (planes == SWG_PLANES_QUADRATIC ? 12 : 8) *
+                          (planes == SWG_PLANES_DECAY ? 4 : 1);
+  t->lb_bytes = lb_bytes;
   const size_t fb = t->fip * height * 2;
   const size_t need = tab_bytes + lb_bytes + fb * (planes == SWG_PLANES_DECAY ? 4 : 1);
   if (memory_budget && need > memory_budget) {

@@ -78,6 +78,10 @@ struct alignas(64) BuildArgs {
   // Selective build (nsel > 0): only these units -- bin octets (integral
   // planes) or bin pairs (decay planes) -- are written, each into its own
   // slot of the full layout; the carries (K1a/K1b) still cover every unit.
+  // decayed builds of all four orientations in ONE strip launch
+  // (blockIdx.y = orientation): their feature images and carry arrays
+  const uint16_t* fio[4];
+  size_t agg_stride;  // uint32 words between orientations' carry arrays
   int nsel;
   unsigned short sel[kMaxBins / kDP];
   // the same selection as a bit mask (carry passes skip unselected units)
@@ -451,6 +455,8 @@ cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s);
 cudaError_t launch_peak_reduce_multi(const PeakMulti& m, int maps, cudaStream_t s);
 cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s);
+// kind >= 0: carries + strips of one orientation; kind = -1: carries only
+// (a.fi, a.agg); kind = -2: strips of all four orientations (a.fio, agg_stride)
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
                                int* launches);
 cudaError_t launch_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
