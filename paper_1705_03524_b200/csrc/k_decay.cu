@@ -61,10 +61,16 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 #define SWG_COL_PAIRS 8  // 16 bins per thread (4 pairs: config 4 builds +0.4 ms)
 #endif
 constexpr int kColPairs = SWG_COL_PAIRS;
-__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs) {
+__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs,
+                                                      int nori) {
+  // nori = 4: the four orientations in one launch (blockIdx.z = column block
+  // * 4 + orientation, each with its image and carry array)
   const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
-  const int x = blockIdx.z * blockDim.x + threadIdx.x;
+  const int ori = nori > 1 ? (int)(blockIdx.z % nori) : 0;
+  const int x = (int)(blockIdx.z / nori) * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
+  const uint16_t* gfi = nori > 1 ? g.fio[ori] : g.fi;
+  double2* dst = reinterpret_cast<double2*>(g.agg + (nori > 1 ? (size_t)ori * g.agg_stride : 0));
   if (g.nsel) {  // selective build: pairs no sweep reads need no carries
     bool any = false;
     for (int k = 0; k < kColPairs && !any; ++k) any = pr0 + k < pairs && sel_has(g.selmask, g.nsel, pr0 + k);
@@ -76,14 +82,14 @@ __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real de
   real c[2 * kColPairs];
 #pragma unroll
   for (int j = 0; j < 2 * kColPairs; ++j) c[j] = 0.0;
-  const uint16_t* col = g.fi + x;
+  const uint16_t* col = gfi + x;
   for (int y = y0; y < y1; ++y) {
     uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
     d = d < lim ? d : 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < 2 * kColPairs; ++j) c[j] = fma(dec, c[j], d == (uint32_t)j ? 1.0 : 0.0);
   }
-  double2* dst = reinterpret_cast<double2*>(g.agg);
+  
 #pragma unroll
   for (int q = 0; q < kColPairs; ++q)
     if (pr0 + q < pairs)
@@ -94,10 +100,14 @@ __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real de
 // one warp per column word, lanes = 32 bands, affine shuffle scan.
 __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, int band_h,
                                                         int h, real dband, real dlast,
-                                                        size_t per_band, const SelMask m) {
-  const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+                                                        size_t per_band, const SelMask m,
+                                                        int nori, size_t ori_stride) {
+  const size_t cw = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (col >= per_band || m.skip(col)) return;
+  if (cw >= per_band * nori) return;
+  const size_t col = cw % per_band;
+  if (m.skip(col)) return;
+  agg += (cw / per_band) * ori_stride;
   real run = 0.0;
   for (int b0 = 0; b0 < nbands; b0 += 32) {
     const int b = b0 + lane;
@@ -125,9 +135,13 @@ __global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, i
 // (loads of 8 bands in flight); see k_bandscan_seq.
 __global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nbands, real dband,
                                                             real dlast, size_t per_band,
-                                                            const SelMask m) {
-  const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (col >= per_band || m.skip(col)) return;
+                                                            const SelMask m, int nori,
+                                                            size_t ori_stride) {
+  const size_t cw = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (cw >= per_band * nori) return;
+  const size_t col = cw % per_band;  // (orientation cw / per_band)
+  if (m.skip(col)) return;
+  agg += (cw / per_band) * ori_stride;
   real run = 0.0;
   constexpr int kB = 8;
   for (int b0 = 0; b0 < nbands; b0 += kB) {
@@ -351,9 +365,11 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
   *launches = 0;
   const int pairs = a.groups * (kOct / kDP);
   if (a.nbands > 1 && kind != -2) {
+    // kind == -1: the carries of all four orientations (a.fio, agg_stride)
+    const int nori = kind == -1 ? 4 : 1;
     dim3 grid((unsigned)a.nbands, (unsigned)((pairs + kColPairs - 1) / kColPairs),
-              (unsigned)((a.w + 255) / 256));
-    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs);
+              (unsigned)((a.w + 255) / 256 * nori));
+    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs, nori);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t per_band = (size_t)pairs * a.wa * kDP;
@@ -364,12 +380,15 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     m.words_per_unit = a.wa * kDP;
     std::memcpy(m.w, a.selmask, sizeof(m.w));
     const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
-    if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
-      k_bandscan_decay<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band, m);
+    const size_t ori_stride = a.agg_stride / 2;  // doubles
+    if (bw ? std::atoi(bw) != 0 : per_band * nori < 148u * 256u)  // few words: a warp each
+      k_bandscan_decay<<<(unsigned)((per_band * nori * 32 + 255) / 256), 256, 0, s>>>(
+          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band, m,
+          nori, ori_stride);
     else
-      k_bandscan_decay_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band, m);
+      k_bandscan_decay_seq<<<(unsigned)((per_band * nori + 255) / 256), 256, 0, s>>>(
+          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band, m, nori,
+          ori_stride);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }

@@ -648,24 +648,22 @@ swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr)
   const char* ef = std::getenv("SWG_DECAY_FUSE");
   const bool fuse = ef ? std::atoi(ef) != 0 : (a.nsel > 0 && t->nbands > 1);
   const size_t stride = t->lb_bytes / 4 / 4;  // uint32 words per orientation
-  for (int k = 0; k < 4; ++k) {
-    a.fi = src[k];
-    a.fio[k] = src[k];
-    int nl = 0;
-    if (fuse) {
-      a.agg = t->lb + k * stride;
-      CUDA_TRY(launch_build_decay(a, t->decay, -1, c->stream, &nl));
-    } else {
-      CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
-    }
-    c->launches += (uint64_t)nl;
-  }
-  if (fuse) {
+  for (int k = 0; k < 4; ++k) a.fio[k] = src[k];
+  if (fuse) {  // the four orientations' carries in one pass, then their strips
     a.agg = t->lb;
     a.agg_stride = stride;
     int nl = 0;
+    CUDA_TRY(launch_build_decay(a, t->decay, -1, c->stream, &nl));
+    c->launches += (uint64_t)nl;
     CUDA_TRY(launch_build_decay(a, t->decay, -2, c->stream, &nl));
     c->launches += (uint64_t)nl;
+  } else {
+    for (int k = 0; k < 4; ++k) {
+      a.fi = src[k];
+      int nl = 0;
+      CUDA_TRY(launch_build_decay(a, t->decay, k, c->stream, &nl));
+      c->launches += (uint64_t)nl;
+    }
   }
   const size_t units = a.nsel ? (size_t)a.nsel : (size_t)t->groups * (kOct / kDP);
   t->built_bytes += units * kDP * t->ps * 4 * 8;
