@@ -333,14 +333,16 @@ swg_status swg_map_peak(swg_ctx* ctx, const double* scores, int map_width,
  * With only device outputs the call is asynchronous on the context stream:
  * the requests fork from it onto the context's worker streams (their sweeps
  * overlap) and join back into it before the call returns, so work queued on
- * the context stream afterwards sees every output (graph-capturable).  A
- * host map in page-locked, device-mapped memory (swg_host_alloc,
- * cudaMallocHost, cudaHostRegister) is written by the sweep directly; other
- * host maps are copied (up to three requests overlap on prioritised
- * streams, each map copied as its sweep ends; more run in order, each map
- * copied while the next one sweeps).  The call returns when the host
- * outputs are filled.  Any of the per-request pointer arrays may itself be
- * NULL. */
+ * the context stream afterwards sees every output (graph-capturable).  In
+ * a call of at most three requests, a host map in page-locked,
+ * device-mapped memory (swg_host_alloc, cudaMallocHost, cudaHostRegister)
+ * is written by the sweep directly; other host maps -- and every host map
+ * of a call with more requests -- are copied (up to three requests overlap
+ * on prioritised streams, each map copied as its sweep ends; more run in
+ * order, each map copied by the copy engine while the next one sweeps).
+ * The call returns when the host outputs are filled
+ * (swg_likelihood_maps_async: when the context is synchronised).  Any of
+ * the per-request pointer arrays may itself be NULL. */
 swg_status swg_likelihood_maps(swg_tables* t, int n,
                                const swg_map_request* reqs,
                                double* const* scores_host,
