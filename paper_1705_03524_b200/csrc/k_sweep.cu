@@ -551,6 +551,222 @@ __global__ void __launch_bounds__(kCakeThreads, SIM == SWG_SIM_BHATTACHARYYA ? S
   sweep_peak(active ? s : -2.0, (long long)v * a.mw + u, a);
 }
 
+// K2c16m: the 16-bit cake sweep over S full-ring square scales at once
+// (CakeMulti).  A lane owns one window CENTRE (cx, cy) and walks the boxes of
+// half-extent e from the largest scale valid at that centre down to 0: the
+// four corner records of box e are loaded and the box counts formed once,
+// then every scale with h_s >= e adds coef_s(e) * count (separately rounded,
+// its rings in its own outer-to-inner order), so each scale's histogram is
+// bit-identical to k_sweep_cake16's while the loads and box arithmetic of
+// the shared extents are paid once (config 5's 8 Gaussian scales: 383 ring
+// extents per centre and octet in 8 launches -> 156 in 2).  Scales sorted by
+// h descending: the scales valid at a centre are a suffix s >= s0; lanes
+// also accumulate the invalid larger scales below their start extent (no
+// divergence in the scale loop) and drop them at the end.
+// Q bins of a 16-bit record per pass: 8 (the whole 16-byte record) or 4
+// (one 8-byte half: half the accumulator registers, so more warps per SM,
+// and each half leaves its box walk as soon as ITS four bins are empty).
+template <int Q>
+struct Rec16 {
+  uint32_t v[Q / 2];
+};
+template <int Q>
+__device__ __forceinline__ Rec16<Q> ldrec(const char* p) {
+  Rec16<Q> r;
+  if constexpr (Q == 8) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    r.v[0] = x.x;
+    r.v[1] = x.y;
+    r.v[2] = x.z;
+    r.v[3] = x.w;
+  } else {
+    const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+    r.v[0] = x.x;
+    r.v[1] = x.y;
+  }
+  return r;
+}
+// (br + tl) - (bl + tr) on packed 16-bit pairs
+template <int Q>
+__device__ __forceinline__ Rec16<Q> box16(const Rec16<Q>& br, const Rec16<Q>& bl,
+                                          const Rec16<Q>& tr, const Rec16<Q>& tl) {
+  Rec16<Q> c;
+#pragma unroll
+  for (int q = 0; q < Q / 2; ++q) c.v[q] = __vsub2(__vadd2(br.v[q], tl.v[q]), __vadd2(bl.v[q], tr.v[q]));
+  return c;
+}
+
+template <int S, int Q>
+__global__ void __launch_bounds__(kCakeThreads, Q == 8 ? SWG_CAKEM_MINB : SWG_CAKEM_MINB4)
+    k_sweep_cake16_multi(const CakeMulti m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hmin = m.hs[S - 1];
+  const int cw = m.w - 2 * hmin, ch = m.h - 2 * hmin;  // centre domain of the smallest scale
+  const int u0 = blockIdx.x * 32 + lane, v0 = blockIdx.y * kCakeTileY + warp;
+  const bool inb = u0 < cw && v0 < ch;
+  const int cx = min(u0, cw - 1) + hmin, cy = min(v0, ch - 1) + hmin;
+  const int dist = min(min(cx, cy), min(m.w - 1 - cx, m.h - 1 - cy));
+  int s0 = 0;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) s0 += m.hs[s] > dist;
+  int e0 = m.hs[S - 1];
+#pragma unroll
+  for (int s = S - 2; s >= 0; --s) e0 = s >= s0 ? m.hs[s] : e0;
+  const int P = (int)(m.pitch * kOct * 2);  // bytes per record row
+  const char* base = reinterpret_cast<const char*>(reinterpret_cast<const uint16_t*>(m.tab) +
+                                                   ((size_t)cy * m.pitch + cx) * kOct);
+  const size_t gstride = (size_t)m.planes * m.plane_stride * kOct * 2;
+  const int P16 = P + 16, Pm16 = P - 16;
+
+  double sc[S], mass[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) sc[s] = mass[s] = 0.0;
+  for (int pass = 0; pass < m.groups * (kOct / Q); ++pass) {
+    const int g = pass / (kOct / Q), half = pass % (kOct / Q);
+    const char* w = base + g * gstride + half * (Q * 2);
+    double out[S][Q];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int k = 0; k < Q; ++k) out[s][k] = 0.0;
+    // corner pointers of the box of half-extent e (byte offsets from the
+    // centre record TL -e(P+16), TR -eP+(e+1)16, BL (e+1)P-16e, BR (e+1)(P+16)),
+    // stepped inwards by constant deltas
+    int e = e0;
+    const char* ptl = w - (ptrdiff_t)e * P16;
+    const char* ptr = w - (ptrdiff_t)e * P + (e + 1) * 16;
+    const char* pbl = w + (ptrdiff_t)(e + 1) * P - e * 16;
+    const char* pbr = w + (ptrdiff_t)(e + 1) * P16;
+    auto step = [&] {
+      ptl += P16;
+      ptr += Pm16;
+      pbl -= Pm16;
+      pbr -= P16;
+      --e;
+    };
+    auto todouble = [&](const Rec16<Q>& c, double (&d)[Q]) {
+      // exact conversions, split between the fp64 pipe (magic number) and
+      // the conversion pipe (I2F)
+#pragma unroll
+      for (int q = 0; q < Q / 2; ++q) {
+        d[2 * q] = u2d(c.v[q] & 0xFFFFu);
+        d[2 * q + 1] = __uint2double_rn(c.v[q] >> 16);
+      }
+    };
+    if (m.wide0 && e == m.hs[0]) {
+      // the outer box may hold >= 2^16 pixels; box e-1 and the frame
+      // between them hold fewer (host-checked): c = c1 + ((c0 - c1) mod 2^16)
+      const Rec16<Q> k0 = box16<Q>(ldrec<Q>(pbr), ldrec<Q>(pbl), ldrec<Q>(ptr), ldrec<Q>(ptl));
+      const Rec16<Q> k1 = box16<Q>(ldrec<Q>(pbr - P16), ldrec<Q>(pbl - Pm16),
+                                   ldrec<Q>(ptr + Pm16), ldrec<Q>(ptl + P16));
+      uint32_t any = 0;
+      Rec16<Q> dd;
+#pragma unroll
+      for (int q = 0; q < Q / 2; ++q) {
+        dd.v[q] = __vsub2(k0.v[q], k1.v[q]);
+        any |= dd.v[q] | k1.v[q];
+      }
+      if (any == 0u) {
+        e = -1;  // every box of this pass is empty
+      } else {
+        double d[Q];
+#pragma unroll
+        for (int q = 0; q < Q / 2; ++q) {
+          d[2 * q] = u2d((k1.v[q] & 0xFFFFu) + (dd.v[q] & 0xFFFFu));
+          d[2 * q + 1] = __uint2double_rn((k1.v[q] >> 16) + (dd.v[q] >> 16));
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s)  // the scales whose outer box this is
+          if (m.hs[s] == e) {
+            const double c = m.coef[s][e];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) out[s][k] = __dadd_rn(out[s][k], __dmul_rn(c, d[k]));
+          }
+        step();
+      }
+    }
+    // box e's corners are loaded one step ahead, so their latency overlaps
+    // the previous box's fp64 work (few warps per SM at these register counts)
+    Rec16<Q> nbr, nbl, ntr, ntl;
+    if (e >= 0) {
+      nbr = ldrec<Q>(pbr);
+      nbl = ldrec<Q>(pbl);
+      ntr = ldrec<Q>(ptr);
+      ntl = ldrec<Q>(ptl);
+    }
+    // Phases by the number of scales whose boxes reach e (NA = scales with
+    // h_s >= e, a prefix: half-extents descending), so the step loop has no
+    // per-scale predicate.  Returns false once a box is empty (every inner
+    // box is then empty too).
+    auto phase = [&](auto na_c) -> bool {
+      constexpr int NA = decltype(na_c)::value;
+      const int lo = NA < S ? m.hs[NA < S ? NA : 0] : -1;
+      // box e's counts into the NA scales' sums; false when the box is empty
+      auto consume = [&](const Rec16<Q>& br, const Rec16<Q>& bl, const Rec16<Q>& tr,
+                         const Rec16<Q>& tl) -> bool {
+        const Rec16<Q> c = box16<Q>(br, bl, tr, tl);
+        uint32_t any = 0;
+#pragma unroll
+        for (int q = 0; q < Q / 2; ++q) any |= c.v[q];
+        if (any == 0u) return false;  // nested boxes: all inner counts 0
+        double d[Q];
+        todouble(c, d);
+#pragma unroll
+        for (int s = 0; s < NA; ++s) {
+          const double cf = m.coef[s][e];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) out[s][k] = __dadd_rn(out[s][k], __dmul_rn(cf, d[k]));
+        }
+        step();
+        return true;
+      };
+      // two steps per iteration over two corner buffers (no register copies);
+      // the prefetch of box -1 (after box 0) stays inside the padded table
+      while (e > lo) {
+        const Rec16<Q> bbr = ldrec<Q>(pbr - P16), bbl = ldrec<Q>(pbl - Pm16),
+                       btr = ldrec<Q>(ptr + Pm16), btl = ldrec<Q>(ptl + P16);
+        if (!consume(nbr, nbl, ntr, ntl)) return false;
+        if (e <= lo) {
+          nbr = bbr;
+          nbl = bbl;
+          ntr = btr;
+          ntl = btl;
+          return true;
+        }
+        nbr = ldrec<Q>(pbr - P16);
+        nbl = ldrec<Q>(pbl - Pm16);
+        ntr = ldrec<Q>(ptr + Pm16);
+        ntl = ldrec<Q>(ptl + P16);
+        if (!consume(bbr, bbl, btr, btl)) return false;
+      }
+      return true;
+    };
+    bool more = e >= 0;
+    if (more) more = phase(std::integral_constant<int, 1>{});
+    if constexpr (S >= 2) if (more) more = phase(std::integral_constant<int, 2>{});
+    if constexpr (S >= 3) if (more) more = phase(std::integral_constant<int, 3>{});
+    if constexpr (S >= 4) if (more) more = phase(std::integral_constant<int, 4>{});
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        mass[s] = __dadd_rn(mass[s], out[s][j]);
+        if (out[s][j] != 0.0)
+          sc[s] = __dadd_rn(sc[s], __dsqrt_rn(__dmul_rn(m.model[s][pass * Q + j], out[s][j])));
+      }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const bool valid = inb && s >= s0;
+    const int us = cx - m.hs[s], vs = cy - m.hs[s];
+    const double v = valid ? clamp01(__ddiv_rn(sc[s], __dsqrt_rn(mass[s]))) : -2.0;
+    const long long idx = valid ? (long long)vs * m.mw[s] + us : 0x7FFFFFFFFFFFFFFFLL;
+    if (valid) m.scores[s][idx] = v;
+    if (s) __syncthreads();  // cta_peak's shared slots of the previous scale
+    cta_peak(v, idx, m.parts[s] + (size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  }
+}
+
 // K3: reduce CTA candidates to the map peak (one CTA).
 __device__ __forceinline__ void peak_reduce_body(const PeakPart* parts, int n, int mw, int hx,
                                                  int hy, swg_peak* out);
@@ -721,6 +937,37 @@ cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 gri
                                 cudaStream_t s) {
   if (a.sim == SWG_SIM_BHATTACHARYYA) k_sweep_cake16<0><<<grid, kCakeThreads, 0, s>>>(a, r);
   else k_sweep_cake16<1><<<grid, kCakeThreads, 0, s>>>(a, r);
+  return cudaGetLastError();
+}
+
+dim3 cake_multi_grid(const CakeMulti& m) {
+  const int hmin = m.hs[m.n - 1];
+  return dim3((unsigned)((m.w - 2 * hmin + 31) / 32),
+              (unsigned)((m.h - 2 * hmin + kCakeTileY - 1) / kCakeTileY));
+}
+
+cudaError_t launch_sweep_cake16_multi(const CakeMulti& m, cudaStream_t s) {
+  const dim3 grid = cake_multi_grid(m);
+  static const int q = [] {
+    const char* e = std::getenv("SWG_CAKEM_Q");  // A/B: bins per pass (8 or 4)
+    return e ? (std::atoi(e) == 4 ? 4 : 8) : SWG_CAKEM_Q;
+  }();
+#define SWG_CAKEM_CASE(S)                                                       \
+  case S:                                                                       \
+    if (q == 8) k_sweep_cake16_multi<S, 8><<<grid, kCakeThreads, 0, s>>>(m);   \
+    else k_sweep_cake16_multi<S, 4><<<grid, kCakeThreads, 0, s>>>(m);          \
+    break;
+  switch (m.n) {
+    SWG_CAKEM_CASE(2)
+#if SWG_CAKE_MULTI >= 3
+    SWG_CAKEM_CASE(3)
+#endif
+#if SWG_CAKE_MULTI >= 4
+    SWG_CAKEM_CASE(4)
+#endif
+    default: return cudaErrorInvalidValue;
+  }
+#undef SWG_CAKEM_CASE
   return cudaGetLastError();
 }
 

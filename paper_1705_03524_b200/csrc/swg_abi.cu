@@ -2129,6 +2129,94 @@ swg_status run_quad_multi(swg_ctx* c, const swg_tables* t, int n, const swg_map_
   return SWG_OK;
 }
 
+// Multi-scale cake (k_sweep_cake16_multi): a full-ring square cake map of
+// the whole frame on the narrow planes, Bhattacharyya (the intersection
+// needs each scale's mass before its terms), all bins of one table.
+bool cake_multi_ok(const swg_tables* t, const swg_map_request& r, const MapPlan& p) {
+  const int h = k_hx(p.k);
+  return p.engine == kCake16 && r.method == SWG_METHOD_CAKE && p.k.kw == p.k.kh && p.k.kw % 2 == 1 &&
+         r.rings == h + 1 && h < kCakeMultiSpan && r.sim == SWG_SIM_BHATTACHARYYA &&
+         !r.partial_in && !r.partial_out && p.row0 == 0 && p.rows == t->h - p.k.kh + 1 &&
+         t->bin0 == 0 && t->bins == t->total_bins && t->groups * kOct <= kCakeMultiBins;
+}
+
+// Groups of up to kCakeMulti multi-scale cake requests (half-extents
+// descending, each group's scales adjacent so its longest walk is shared by
+// the most scales); gid[i] = the group of request i or -1.
+void cake_groups(const swg_tables* t, int n, const swg_map_request* reqs,
+                 const std::vector<MapPlan>& plan, std::vector<std::vector<int>>& groups,
+                 std::vector<int>& gid) {
+  gid.assign(n, -1);
+  groups.clear();
+  const char* ev = std::getenv("SWG_CAKE_GROUP");  // A/B: scales per launch (1 = off)
+  const int gmax = std::min(ev ? std::atoi(ev) : kCakeMulti, kCakeMulti);
+  if (gmax < 2) return;
+  std::vector<int> cand;
+  for (int i = 0; i < n; ++i)
+    if (cake_multi_ok(t, reqs[i], plan[i])) cand.push_back(i);
+  std::stable_sort(cand.begin(), cand.end(),
+                   [&](int x, int y) { return k_hx(plan[x].k) > k_hx(plan[y].k); });
+  const int nc = (int)cand.size();
+  const int ng = (nc + gmax - 1) / gmax;
+  for (int g = 0; g < ng; ++g) {  // near-equal group sizes
+    const int b = g * nc / ng, e = (g + 1) * nc / ng;
+    if (e - b < 2) continue;
+    groups.emplace_back(cand.begin() + b, cand.begin() + e);
+    for (int k = b; k < e; ++k) gid[cand[k]] = (int)groups.size() - 1;
+  }
+}
+
+dim3 cake_group_grid(const swg_tables* t, const MapPlan& smallest) {
+  CakeMulti m;
+  m.w = t->w;
+  m.h = t->h;
+  m.n = 1;
+  m.hs[0] = k_hx(smallest.k);
+  return cake_multi_grid(m);
+}
+
+// One launch for a group's maps, one for their peaks.
+swg_status run_cake_multi(swg_ctx* c, const swg_tables* t, const std::vector<int>& grp,
+                          const swg_map_request* reqs, const std::vector<MapPlan>& plan,
+                          double* const* scores, PeakPart* parts0, swg_peak* peaks,
+                          cudaStream_t st) {
+  static thread_local CakeMulti m;  // ~8 KB of kernel parameters
+  static thread_local CakeRings rg;
+  PeakMulti pm;
+  std::memset(m.model, 0, sizeof(m.model));
+  m.tab = t->t16;
+  m.plane_stride = t->ps;
+  m.pitch = t->pitch;
+  m.planes = t->planes;
+  m.groups = t->groups;
+  m.w = t->w;
+  m.h = t->h;
+  m.n = (int)grp.size();
+  const dim3 grid = cake_group_grid(t, plan[grp.back()]);
+  for (int s = 0; s < m.n; ++s) {
+    const int i = grp[s];
+    const MapPlan& p = plan[i];
+    const int h = k_hx(p.k);
+    ST_TRY(cake_plan(p.k, reqs[i].rings, reqs[i].ring_rule, rg));
+    m.hs[s] = h;
+    m.mw[s] = p.mw;
+    m.scores[s] = scores[i];
+    m.parts[s] = parts0 + p.poff;
+    for (int e = 0; e < kCakeMultiSpan; ++e) m.coef[s][e] = e <= h ? rg.coeff[h - e] : 0.0;
+    std::memcpy(m.model[s], reqs[i].model, sizeof(double) * t->bins);
+    pm.parts[s] = m.parts[s];
+    pm.n[s] = (int)(grid.x * grid.y);
+    pm.mw[s] = p.mw;
+    pm.hx[s] = pm.hy[s] = h;
+    pm.out[s] = peaks + i;
+  }
+  m.wide0 = (2LL * m.hs[0] + 1) * (2LL * m.hs[0] + 1) >= 65536;
+  CUDA_TRY(launch_sweep_cake16_multi(m, st));
+  CUDA_TRY(launch_peak_reduce_multi(pm, m.n, st));
+  c->launches += 2;
+  return SWG_OK;
+}
+
 // Direct per-pixel weighted histogram (baselines.cpp:24-69).
 swg_status run_brute(swg_ctx* c, const swg_tables* t, const MapPlan& p, const SweepArgs& a,
                      cudaStream_t st) {
@@ -2286,6 +2374,14 @@ static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_reque
       zc[i] = mapped_host(scores_host[i], c->device);
   }
   auto copy_map = [&](int i) { return host_map(i) && !zc[i]; };
+  // multi-scale cake groups: each member's CTA candidates cover the group's grid
+  std::vector<std::vector<int>> cgroups;
+  std::vector<int> cgid;
+  cake_groups(t, n, reqs, plan, cgroups, cgid);
+  for (const auto& g : cgroups) {
+    const dim3 gg = cake_group_grid(t, plan[g.back()]);
+    for (int i : g) plan[i].grid = gg;
+  }
   // scratch: per-request score buffers (when the caller gave no device or
   // mapped output), CTA peak candidates, device peaks, exact-peak slices
   size_t stot = 0, ptot = 0;
@@ -2390,6 +2486,12 @@ static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_reque
       const double rings = p.engine == kCake16 || p.engine == kCake32
                                ? (reqs[i].method == SWG_METHOD_CAKE ? reqs[i].rings : 1)
                                : 1;
+      if (cgid[i] >= 0) {  // a multi-scale cake group: its members' cost (leader only)
+        if (cgroups[cgid[i]][0] != i) return 0.0;
+        double g = 0.0;
+        for (int j : cgroups[cgid[i]]) g += (double)plan[j].rows * plan[j].mw * reqs[j].rings;
+        return 0.5 * g;
+      }
       return (double)p.rows * p.mw * rings;
     };
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
@@ -2402,6 +2504,26 @@ static swg_status likelihood_maps_impl(swg_tables* t, int n, const swg_map_reque
     const cudaStream_t st = nwork ? wk[q % nwork] : c->stream;
     double* dscores = out[i];
     PeakPart* parts = parts0 + p.poff;
+    if (cgid[i] >= 0) {  // multi-scale cake: the group's leader sweeps every member
+      const std::vector<int>& grp = cgroups[cgid[i]];
+      if (grp[0] != i) continue;
+      ST_TRY(run_cake_multi(c, t, grp, reqs, plan, out.data(), parts0, dpeaks, st));
+      for (int j : grp) {
+        if (!copy_map(j)) continue;
+        while (c->events.size() <= (size_t)j) {
+          cudaEvent_t ev;
+          CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          c->events.push_back(ev);
+        }
+        CUDA_TRY(cudaEventRecord(c->events[j], st));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy, c->events[j], 0));
+        CUDA_TRY(cudaMemcpyAsync(scores_host[j], out[j], (size_t)plan[j].rows * plan[j].mw * 8,
+                                 cudaMemcpyDeviceToHost, c->copy));
+        c->map_copies += 1;
+        copies = true;
+      }
+      continue;
+    }
     static thread_local SweepArgs a;  // 8 KB of model constants: keep off the stack
     // the copy stream takes a finished map (or row range of it) while later
     // sweeps run

@@ -160,10 +160,38 @@ struct QuadMulti {
   int n;
 };
 
+// Up to kCakeMulti full-ring square cake maps of one narrow (uint16) plain
+// table swept by one launch (k_sweep_cake16_multi): every scale's ring boxes
+// are the boxes of half-extent e = h .. 0 around the window centre, so a
+// centre's box counts are loaded and formed once for all the scales and each
+// scale accumulates its own coefficient of the box (in its own ring order:
+// outer to inner, as WeddingCakePlan::histogram_into, baselines.cpp:139-148).
+#ifndef SWG_CAKE_MULTI
+#define SWG_CAKE_MULTI 4
+#endif
+constexpr int kCakeMulti = SWG_CAKE_MULTI;
+constexpr int kCakeMultiSpan = 129;  // half-extents 0..128 (16-bit planes: kw*kh < 2^16 or wide0)
+constexpr int kCakeMultiBins = 128;
+struct CakeMulti {
+  const void* tab;      // uint16 plain planes
+  size_t plane_stride;  // records
+  size_t pitch;         // records
+  int planes, groups;
+  int w, h;             // image; centres [hmin, w-1-hmin] x [hmin, h-1-hmin]
+  int n;                // maps, half-extents descending
+  int wide0;            // hs[0]'s outer box may hold >= 2^16 pixels
+  int hs[kCakeMulti], mw[kCakeMulti];
+  double* scores[kCakeMulti];
+  PeakPart* parts[kCakeMulti];
+  double coef[kCakeMulti][kCakeMultiSpan];  // ring coefficient of the box of half-extent e
+  double model[kCakeMulti][kCakeMultiBins]; // zero-padded to a multiple of 8
+};
+
+constexpr int kPeakMulti = kQuadMulti > kCakeMulti ? kQuadMulti : kCakeMulti;
 struct PeakMulti {  // k_peak_reduce over the maps of one multi-map launch
-  const PeakPart* parts[kQuadMulti];
-  int n[kQuadMulti], mw[kQuadMulti], hx[kQuadMulti], hy[kQuadMulti];
-  swg_peak* out[kQuadMulti];
+  const PeakPart* parts[kPeakMulti];
+  int n[kPeakMulti], mw[kPeakMulti], hx[kPeakMulti], hy[kPeakMulti];
+  swg_peak* out[kPeakMulti];
 };
 
 // Host-side ring plan of a wedding-cake configuration.
@@ -380,6 +408,15 @@ constexpr int kExpTileX = 32 * kExpWarpsX, kExpTileY = kExpThreads / 32 / kExpWa
 #define SWG_CAKE_MINB 10  // <= 48 registers: 10 CTAs (40 warps) per SM; 40 registers spill (+3 %)
 #endif
 constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
+#ifndef SWG_CAKEM_MINB
+#define SWG_CAKEM_MINB 3  // the multi-scale cake, whole records: up to 168 registers
+#endif
+#ifndef SWG_CAKEM_MINB4
+#define SWG_CAKEM_MINB4 4  // half records: up to 128 registers
+#endif
+#ifndef SWG_CAKEM_Q
+#define SWG_CAKEM_Q 8  // bins per pass of the multi-scale cake (4: half records, measured slower)
+#endif
 // A cake16 warp covers kCakeWX x (32 / kCakeWX) windows: the lanes of a warp
 // run until the last of them has emptied its octet's boxes, so compact warps
 // (windows closer together, more similar inner bins) diverge less; a corner
@@ -469,6 +506,8 @@ cudaError_t launch_exact_peak(const SweepArgs& a, const RescoreArgs& r, swg_peak
                               cudaStream_t s);
 cudaError_t launch_sweep_cake16(const SweepArgs& a, const CakeSweep& r, dim3 grid,
                                 cudaStream_t s);
+dim3 cake_multi_grid(const CakeMulti& m);
+cudaError_t launch_sweep_cake16_multi(const CakeMulti& m, cudaStream_t s);
 cudaError_t launch_sweep_brute(const SweepArgs& a, const BruteArgs& b, int blocks_x,
                                cudaStream_t s);
 cudaError_t launch_peak_reduce(const PeakPart* parts, int nparts, int mw, int hx, int hy,

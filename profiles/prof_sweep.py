@@ -3,7 +3,8 @@
 group: manhattan | gauss | euclid | exp (config 5's table groups) or c2 / c4.
 Builds the group's tables once, then runs each listed scale's request
 (device outputs, as the timed step) `reps` times (default 1), one launch
-per request in order."""
+per request in order; a 5th argument "joint" sends them in one call (the
+multi-scale cake groups the library forms, as in the timed step)."""
 import os
 import sys
 
@@ -16,6 +17,7 @@ from paper_1705_03524_b200 import swg  # noqa: E402
 cfg, group = sys.argv[1], sys.argv[2]
 want = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+joint = len(sys.argv) > 5 and sys.argv[5] == "joint"
 wl = bench.workload(cfg)
 KIND = {"manhattan": swg.MANHATTAN, "gauss": swg.GAUSS_CHEB, "euclid": swg.EUCLID_QUAD,
         "exp": swg.EXP_L1}
@@ -41,6 +43,9 @@ for (k, meth, rings, _), m in zip(g["scales"], models):
     maps.append(torch.empty(t.map_shape(k), dtype=torch.float64, device="cuda"))
 peaks = torch.zeros(len(reqs), 3, dtype=torch.float64, device="cuda")
 for _ in range(reps):
+    if joint:
+        t.likelihood_maps(reqs, scores="none", scores_dev=maps, peaks_dev=peaks)
+        continue
     for i, r in enumerate(reqs):
         t.likelihood_maps([r], scores="none", scores_dev=[maps[i]], peaks_dev=peaks[i])
 ctx.synchronize()
