@@ -596,8 +596,26 @@ __device__ __forceinline__ Rec16<Q> box16(const Rec16<Q>& br, const Rec16<Q>& bl
   return c;
 }
 
-template <int S, int Q>
-__global__ void __launch_bounds__(kCakeThreads, Q == 8 ? SWG_CAKEM_MINB : SWG_CAKEM_MINB4)
+constexpr int kCakeStages = SWG_CAKEM_STAGES;
+__shared__ uint4 cake_pf[kCakeStages * 4 * kCakeThreads];  // ASYNC: per-thread corner slots
+template <int B>
+__device__ __forceinline__ void cp_async_ca(uint32_t dst, const char* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(B) : "memory");
+}
+template <int Q>
+__device__ __forceinline__ Rec16<Q> lds_rec(uint32_t a) {
+  Rec16<Q> r;
+  if constexpr (Q == 8)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]) : "r"(a) : "memory");
+  else
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.v[0]), "=r"(r.v[1]) : "r"(a) : "memory");
+  return r;
+}
+
+template <int S, int Q, bool ASYNC>
+__global__ void __launch_bounds__(kCakeThreads, ASYNC ? SWG_CAKEM_MINBA
+                                                : (Q == 8 ? SWG_CAKEM_MINB : SWG_CAKEM_MINB4))
     k_sweep_cake16_multi(const CakeMulti m) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hmin = m.hs[S - 1];
@@ -685,10 +703,36 @@ __global__ void __launch_bounds__(kCakeThreads, Q == 8 ? SWG_CAKEM_MINB : SWG_CA
         step();
       }
     }
-    // box e's corners are loaded one step ahead, so their latency overlaps
-    // the previous box's fp64 work (few warps per SM at these register counts)
+    // ASYNC: box corners stream through a per-thread ring of kCakeStages
+    // shared-memory slots (cp.async, kCakeStages - 1 boxes ahead): no
+    // registers hold loads in flight.  Otherwise: box e's corners are loaded
+    // one step ahead into registers, so their latency overlaps the previous
+    // box's fp64 work.
     Rec16<Q> nbr, nbl, ntr, ntl;
-    if (e >= 0) {
+    [[maybe_unused]] const char *qtl = ptl, *qtr = ptr, *qbl = pbl, *qbr = pbr;
+    [[maybe_unused]] int qe = e, slot_in = 0, slot_out = 0;
+    [[maybe_unused]] uint32_t sbase = 0;
+    [[maybe_unused]] auto issue = [&] {  // the next box's corners into slot_in
+      if (qe >= -1) {  // box -1 (after box 0) is the last one inside the padded table
+        const uint32_t d = sbase + slot_in * (4 * kCakeThreads * 16);
+        cp_async_ca<Q * 2>(d, qbr);
+        cp_async_ca<Q * 2>(d + kCakeThreads * 16, qbl);
+        cp_async_ca<Q * 2>(d + 2 * kCakeThreads * 16, qtr);
+        cp_async_ca<Q * 2>(d + 3 * kCakeThreads * 16, qtl);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      qtl += P16;
+      qtr += Pm16;
+      qbl -= Pm16;
+      qbr -= P16;
+      --qe;
+      slot_in = slot_in == kCakeStages - 1 ? 0 : slot_in + 1;
+    };
+    if constexpr (ASYNC) {
+      sbase = (uint32_t)__cvta_generic_to_shared(cake_pf) + threadIdx.x * 16;
+      if (e >= 0)
+        for (int j = 0; j < kCakeStages - 1; ++j) issue();
+    } else if (e >= 0) {
       nbr = ldrec<Q>(pbr);
       nbl = ldrec<Q>(pbl);
       ntr = ldrec<Q>(ptr);
@@ -720,6 +764,19 @@ __global__ void __launch_bounds__(kCakeThreads, Q == 8 ? SWG_CAKEM_MINB : SWG_CA
         step();
         return true;
       };
+      if constexpr (ASYNC) {
+        while (e > lo) {
+          issue();
+          asm volatile("cp.async.wait_group %0;" ::"n"(kCakeStages - 1) : "memory");
+          const uint32_t d = sbase + slot_out * (4 * kCakeThreads * 16);
+          slot_out = slot_out == kCakeStages - 1 ? 0 : slot_out + 1;
+          const Rec16<Q> br = lds_rec<Q>(d), bl = lds_rec<Q>(d + kCakeThreads * 16),
+                         tr = lds_rec<Q>(d + 2 * kCakeThreads * 16),
+                         tl = lds_rec<Q>(d + 3 * kCakeThreads * 16);
+          if (!consume(br, bl, tr, tl)) return false;
+        }
+        return true;
+      } else {
       // two steps per iteration over two corner buffers (no register copies);
       // the prefetch of box -1 (after box 0) stays inside the padded table
       while (e > lo) {
@@ -740,12 +797,14 @@ __global__ void __launch_bounds__(kCakeThreads, Q == 8 ? SWG_CAKEM_MINB : SWG_CA
         if (!consume(bbr, bbl, btr, btl)) return false;
       }
       return true;
+      }
     };
     bool more = e >= 0;
     if (more) more = phase(std::integral_constant<int, 1>{});
     if constexpr (S >= 2) if (more) more = phase(std::integral_constant<int, 2>{});
     if constexpr (S >= 3) if (more) more = phase(std::integral_constant<int, 3>{});
     if constexpr (S >= 4) if (more) more = phase(std::integral_constant<int, 4>{});
+    if constexpr (ASYNC) asm volatile("cp.async.wait_group 0;" ::: "memory");  // slots reused
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -952,10 +1011,15 @@ cudaError_t launch_sweep_cake16_multi(const CakeMulti& m, cudaStream_t s) {
     const char* e = std::getenv("SWG_CAKEM_Q");  // A/B: bins per pass (8 or 4)
     return e ? (std::atoi(e) == 4 ? 4 : 8) : SWG_CAKEM_Q;
   }();
-#define SWG_CAKEM_CASE(S)                                                       \
-  case S:                                                                       \
-    if (q == 8) k_sweep_cake16_multi<S, 8><<<grid, kCakeThreads, 0, s>>>(m);   \
-    else k_sweep_cake16_multi<S, 4><<<grid, kCakeThreads, 0, s>>>(m);          \
+  static const bool as = [] {
+    const char* e = std::getenv("SWG_CAKEM_ASYNC");  // A/B: cp.async corner ring
+    return e ? std::atoi(e) != 0 : SWG_CAKEM_ASYNC != 0;
+  }();
+#define SWG_CAKEM_CASE(S)                                                               \
+  case S:                                                                               \
+    if (as) k_sweep_cake16_multi<S, 8, true><<<grid, kCakeThreads, 0, s>>>(m);          \
+    else if (q == 8) k_sweep_cake16_multi<S, 8, false><<<grid, kCakeThreads, 0, s>>>(m); \
+    else k_sweep_cake16_multi<S, 4, false><<<grid, kCakeThreads, 0, s>>>(m);            \
     break;
   switch (m.n) {
     SWG_CAKEM_CASE(2)

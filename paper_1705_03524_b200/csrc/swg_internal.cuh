@@ -414,6 +414,15 @@ constexpr int kCakeTileY = SWG_CAKE_TY, kCakeThreads = 32 * kCakeTileY;
 #ifndef SWG_CAKEM_MINB4
 #define SWG_CAKEM_MINB4 4  // half records: up to 128 registers
 #endif
+#ifndef SWG_CAKEM_ASYNC
+#define SWG_CAKEM_ASYNC 1  // corners through a cp.async ring in shared memory
+#endif
+#ifndef SWG_CAKEM_STAGES
+#define SWG_CAKEM_STAGES 3
+#endif
+#ifndef SWG_CAKEM_MINBA
+#define SWG_CAKEM_MINBA 4  // the cp.async ring frees the in-flight registers: <= 128
+#endif
 #ifndef SWG_CAKEM_Q
 #define SWG_CAKEM_Q 8  // bins per pass of the multi-scale cake (4: half records, measured slower)
 #endif
