@@ -904,16 +904,42 @@ class OursArm:
                                            scores_dev=u["maps"] if last else None,
                                            peaks_dev=u["peaks"])
                     continue
-                for i, r in enumerate(creqs):
-                    if "pin" in u:
-                        self._chain_sweep(u, i, r)
+                for bt in self._batches(u, c, creqs):
+                    if len(bt) > 1:  # a multi-scale cake launch: its scales in one call
+                        u["t"].likelihood_maps([creqs[i] for i in bt], scores="none",
+                                               scores_dev=[u["maps"][i] for i in bt],
+                                               peaks_dev=u["bpeaks"])
+                    elif "pin" in u:
+                        self._chain_sweep(u, bt[0], creqs[bt[0]])
                     else:
+                        i, r = bt[0], creqs[bt[0]]
                         u["t"].likelihood_maps([r], scores="none",
                                                scores_dev=None if r.partial_out is not None
                                                else [u["maps"][i]], peaks_dev=u["peaks"][i])
                     if ev:
                         ev[j].record()
                         j += 1
+
+    def _batches(self, u, c, creqs):
+        """The per-launch timing path's calls for chunk c of unit u: one call
+        per request, except the requests the library sweeps in one
+        multi-scale cake launch (swg_request_groups), which share a call."""
+        key = ("batches", c)
+        if key not in u:
+            gid = u["t"].request_groups(creqs) if "pin" not in u else [-1] * len(creqs)
+            out, seen = [], {}
+            for i, g in enumerate(gid):
+                if g < 0:
+                    out.append([i])
+                elif g not in seen:
+                    seen[g] = len(out)
+                    out.append([i])
+                else:
+                    out[seen[g]].append(i)
+            u[key] = out
+            u["bpeaks"] = self.torch.zeros(len(creqs), 3, dtype=self.torch.float64,
+                                           device="cuda")
+        return u[key]
 
     # ------------------------------------------------------------ timing
     def barrier(self):
@@ -945,7 +971,8 @@ class OursArm:
                 graph.replay()
             torch.cuda.synchronize()
 
-        nev = sum(2 + len(cr) for u in self.units for _, cr in u["chunks"])
+        nev = sum(2 + len(self._batches(u, c, cr)) for u in self.units
+                  for c, (_, cr) in enumerate(u["chunks"]))
         events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)]
                   for _ in range(args.steps)]
         clocks = Clocks(self.local)
@@ -1004,11 +1031,12 @@ class OursArm:
         for e in events:
             j = 0
             for ui, u in enumerate(self.units):
-                for _, creqs in u["chunks"]:
+                for c, (_, creqs) in enumerate(u["chunks"]):
                     build_ms.append(e[j].elapsed_time(e[j + 1]))
                     j += 1
-                    for i in range(len(creqs)):
-                        sweep_ms.setdefault((ui, i), []).append(e[j].elapsed_time(e[j + 1]))
+                    for bt in self._batches(u, c, creqs):
+                        key = (ui, bt[0]) if len(bt) == 1 else (ui, tuple(bt))
+                        sweep_ms.setdefault(key, []).append(e[j].elapsed_time(e[j + 1]))
                         j += 1
                     j += 1
         return build_ms, sweep_ms
@@ -1218,6 +1246,28 @@ class OursArm:
         for (ui, i), ts in sweep_ms.items():
             u = self.units[ui]
             g = wl["groups"][u["g"]]
+            if isinstance(i, tuple):  # one multi-scale cake launch over these scales
+                ks = sorted((g["scales"][u["sidx"][x]][0] for x in i), key=lambda k: -k.kw)
+                hmin = min(k.kw for k in ks)
+                bins = self.nb
+                # algorithmic: the table's records once (16-bit, one plane)
+                # + 8 B per window of every scale
+                win = sum((self.tab_h - k.kh + 1) * (self.tab_w - k.kw + 1) for k in ks)
+                byts = (self.tab_h + 1) * (W + 1) * bins * 2 + 8 * win
+                ms = sum(ts) / len(ts)
+                ent = kt.setdefault("k_sweep_cake16_multi", {"launches_per_step": 0,
+                                                             "ms_per_step": 0.0,
+                                                             "bytes_per_step": 0,
+                                                             "launches": []})
+                n = len(ts) // steps
+                ent["launches_per_step"] += n
+                ent["ms_per_step"] += ms * n
+                ent["bytes_per_step"] += byts * n
+                ent["launches"].append({"window": "/".join(f"{k.kw}x{k.kh}" for k in ks),
+                                        "rows": int(self.tab_h - hmin + 1), "bins": int(bins),
+                                        "ms": ms, "bytes": int(byts),
+                                        "hbm_frac": byts / (ms / 1e3) / 1e9 / hbm})
+                continue
             k, meth = g["scales"][u["sidx"][i]][:2]
             r = u["reqs"][i]
             # the library's own report of what it runs (swg_request_plan):
@@ -1340,8 +1390,9 @@ class OursArm:
         per_scale = {}
         for (ui, i), ts in sweep_ms.items():
             u = self.units[ui]
-            sc = wl["groups"][u["g"]]["scales"][u["sidx"][i]]
-            key = f"{kinds[sc[0].kind]}{sc[0].kw}x{sc[0].kh}"
+            scs = sorted((wl["groups"][u["g"]]["scales"][u["sidx"][x]]
+                          for x in (i if isinstance(i, tuple) else (i,))), key=lambda sc: -sc[0].kw)
+            key = kinds[scs[0][0].kind] + "/".join(f"{sc[0].kw}x{sc[0].kh}" for sc in scs)
             per_scale[key] = per_scale.get(key, 0.0) + sum(ts) / args.steps
         ih = kt.get("ih_build")
         out = {

@@ -379,6 +379,18 @@ typedef struct swg_plan_info {
 } swg_plan_info;
 swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_plan_info* out);
 
+/* Which requests of one swg_likelihood_maps call share a launch (no device
+ * work): group_of[i] = the multi-scale cake launch request i joins, or -1
+ * when it runs on its own.  A call's full-ring square GaussianChebyshev /
+ * cake requests (Bhattacharyya, whole map, all bins of the table) on the
+ * 16-bit plain planes are swept together, up to SWG_CAKE_MULTI scales per
+ * launch, largest half-extents first: every scale's ring boxes are the
+ * boxes of half-extent h .. 0 around the window centre, loaded once for all
+ * of them (WeddingCakePlan::histogram_into, baselines.cpp:139-148, per
+ * scale, bit for bit). */
+swg_status swg_request_groups(const swg_tables* t, int n, const swg_map_request* reqs,
+                              int* group_of);
+
 /* swg_likelihood_maps without the final host synchronisation: the call
  * enqueues the builds' consumers, sweeps and map copies and returns; host
  * maps and host peaks are filled once swg_ctx_synchronize returns.  Successive

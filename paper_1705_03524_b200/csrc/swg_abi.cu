@@ -2233,6 +2233,22 @@ swg_status run_brute(swg_ctx* c, const swg_tables* t, const MapPlan& p, const Sw
 
 }  // namespace
 
+swg_status swg_request_groups(const swg_tables* t, int n, const swg_map_request* reqs,
+                              int* group_of) {
+  ST_TRY(check_tables(t));
+  if (n < 0 || (n && (!reqs || !group_of))) return fail(SWG_ERR_ARG, "bad request list");
+  std::vector<MapPlan> plan(n);
+  for (int i = 0; i < n; ++i) {
+    ST_TRY(validate_request(t, reqs[i], false, plan[i]));
+    ST_TRY(plan_request(t, reqs[i], plan[i]));
+  }
+  std::vector<std::vector<int>> groups;
+  std::vector<int> gid;
+  cake_groups(t, n, reqs, plan, groups, gid);
+  for (int i = 0; i < n; ++i) group_of[i] = gid[i];
+  return SWG_OK;
+}
+
 swg_status swg_request_plan(const swg_tables* t, const swg_map_request* r, swg_plan_info* out) {
   ST_TRY(check_tables(t));
   if (!r || !out) return fail(SWG_ERR_ARG, "NULL argument");

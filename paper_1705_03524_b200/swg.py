@@ -188,6 +188,7 @@ def lib():
         "swg_likelihood_maps": [vp, C.c_int, vp, vp, vp, vp, vp],
         "swg_likelihood_maps_async": [vp, C.c_int, vp, vp, vp, vp, vp],
         "swg_request_plan": [vp, vp, vp],
+        "swg_request_groups": [vp, st, vp, vp],
         "swg_likelihood_batch": [vp, C.c_int, vp, C.c_int, C.c_size_t, C.c_int, vp, vp, vp],
         "swg_brute_windows": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
                               C.POINTER(Kernel), C.c_int, vp, vp],
@@ -554,6 +555,14 @@ class Tables:
         _check(lib().swg_request_plan(self._h, C.addressof(creqs), C.byref(out)))
         return {"kernel": out.kernel.decode(), "planes": out.planes,
                 "entry_bytes": out.entry_bytes, "bins_read": out.bins_read, "ctas": out.ctas}
+
+    def request_groups(self, reqs: Sequence["MapRequest"]) -> list:
+        """swg_request_groups: per request, the multi-scale cake launch it
+        joins in one likelihood_maps call (-1: its own launch)."""
+        creqs, _keep = self._creqs(reqs, self.total_bins)
+        out = (C.c_int * len(reqs))()
+        _check(lib().swg_request_groups(self._h, len(reqs), C.addressof(creqs), out))
+        return list(out)
 
     @staticmethod
     def _creqs(reqs, bins):
