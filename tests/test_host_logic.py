@@ -154,8 +154,9 @@ def test_profiles_traffic_entries_resolve():
         sizes = {f"{k.kw}x{k.kh}" for g in wl["groups"] for k, _, _, _ in g["scales"]}
         for e in entries if isinstance(entries, list) else [entries]:
             assert e["kernel"].startswith(("k_sweep_", "k_stream_")), e
-            scale = re.search(r"\((\d+x\d+) scale", e["kernel"]).group(1)
-            assert scale in sizes, (cfg, scale)
+            # one scale, or the scales of one multi-scale cake launch
+            scales = re.search(r"\(\s*((?:\d+x\d+/?)+) scales?", e["kernel"]).group(1).split("/")
+            assert scales and all(s in sizes for s in scales), (cfg, scales)
             src = os.path.join(root, e["source"])
             assert os.path.exists(src), src
             assert "dram__bytes_read.sum" in open(src).read()
