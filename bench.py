@@ -1305,7 +1305,7 @@ class OursArm:
                               "bytes_per_step": int(bb), "launches": [],
                               "kernels": "k_quantize + k_colsum + k_bandscan + k_build / "
                                          "k_build_fused (+ decayed: k_flip, k_colsum_decay, "
-                                         "k_bandscan_decay, k_build_decay_strip)"}
+                                         "k_bandscan_decay, k_build_decay_warp)"}
         for ent in kt.values():
             ent["gbps"] = ent["bytes_per_step"] / (ent["ms_per_step"] / 1e3) / 1e9
             ent["hbm_frac"] = ent["gbps"] / hbm

@@ -13,7 +13,7 @@
 // The four orientations are the same SE table built on the feature image
 // flipped horizontally / vertically / both (k_flip), so one build pipeline
 // serves all four.  It mirrors the integer build: K1a' decayed column sums
-// per band, K1b' decayed scan over bands, K1c' per (band, bin pair) CTA in
+// per band, K1b' decayed scan over bands, K1c' one warp per (band, bin pair) in
 // column strips (column recurrence, then one warp scan per row segment).
 // Layout: BIN PAIRS, not octets -- a record is the 2 bins of one pair at one
 // cell (16 B of fp64), element (b, kind k, x, y) at
@@ -159,44 +159,49 @@ __global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nband
   }
 }
 
-// K1c': decayed SE table of one orientation, column recurrence first.  With
-//   c(x, y) = d c(x, y-1) + f(x, y)        (c(x, y0-1) = the band's carry, K1b')
-//   E(x+1, y+1) = sum_{x' <= x} d^(x-x') c(x', y)
-// one CTA per (band, bin pair) walks the row in strips of kStripW columns and
-// the band in blocks of kStripRows rows: phase A (thread per column) runs the
-// column recurrence down the block into a shared tile; phase B (warp per row,
-// lane = 8 consecutive columns) forms the decayed row prefix with one warp
-// scan per row and the carry E(x0-1, y) of the strip to the left; phase C
-// (thread per column, fused with the next block's phase A) writes the tile
-// out as 512-byte warp stores.  Two block barriers per 16 rows instead of a
-// block-wide scan and barrier per row.
-#ifndef SWG_STRIP_ROWS
-#define SWG_STRIP_ROWS 8  // 8-row blocks at 4 CTAs per SM: config 5 decayed set 2.82 -> 2.74 ms (16 rows at 3)
-#endif
-#ifndef SWG_STRIP_MINB
-#define SWG_STRIP_MINB 4
-#endif
-constexpr int kStripW = 256, kStripRows = SWG_STRIP_ROWS;
+constexpr int kStripW = 256;  // columns per strip: 8 per lane
 
 __device__ __forceinline__ int strip_swz(int x) { return x ^ ((x >> 3) & 7); }
 
-__global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
-    k_build_decay_strip(const __grid_constant__ BuildArgs g, real dec, int kind, int pairs) {
-  // [kStripRows][kStripW] swizzled (= the TMA SWIZZLE_128B layout of each
-  // 4 KB row), then carry[band_h]
+// K1c': decayed SE table of one orientation.  With
+//   c(x, y) = d c(x, y-1) + f(x, y)        (c(x, y0-1) = the band's carry, K1b')
+//   E(x+1, y+1) = sum_{x' <= x} d^(x-x') c(x', y)
+// one WARP builds one (band, bin pair, orientation) unit, with no block
+// barrier anywhere: the warp walks the row in strips of kStripW columns,
+// lane l owning columns 8l .. 8l+7 of the strip, and runs BOTH recurrences
+// for them row by row -- the column recurrence in registers (16 running
+// values) and the decayed row prefix (its 8 columns, one warp scan, and the
+// carry E(x0-1, y) of the strip to the left, kept per row in shared memory).
+// The finished 4 KB row segment goes into one of kWarpRows swizzled row
+// buffers (= the TMA SWIZZLE_128B layout) and out through one TMA tensor
+// store; the next rows are built while earlier stores drain.
+// (The first form gave a CTA one unit: threads ran the column recurrence
+// into a shared 8-row tile, warps the row prefixes, two to three block
+// barriers per 8 rows.  Each record crossed shared memory four times and
+// ncu showed barrier stalls on top of an instruction-bound loop -- 542 warp
+// instructions per 4 KB row segment against 339 here; config 5's decayed set
+// 1.03 -> 0.85 ms.  Same operation order per value: identical tables.)
+constexpr int kWarpRows = 3;  // row buffers per warp (4 KB each)
+constexpr int kWarpsPerCta = 8;  // (fewer when the bands are tall: the carries share the CTA's shared memory)
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_build_decay_warp(const __grid_constant__ BuildArgs g, real dec, int kind, int pairs,
+                       int nori) {
   extern __shared__ __align__(1024) double2 s_tile[];
-  const bool tma = g.tmap_ok != 0;
-  double2* carry = s_tile + kStripRows * kStripW;
-  if (gridDim.y > 1) kind = blockIdx.y;  // all four orientations in one launch
-  const uint16_t* gfi = gridDim.y > 1 ? g.fio[kind] : g.fi;
-  const uint32_t* gagg = g.agg + (gridDim.y > 1 ? (size_t)kind * g.agg_stride : 0);
-  const int np = g.nsel ? g.nsel : pairs;  // selective build: the listed pairs
-  const int band = blockIdx.x / np, pr = g.nsel ? (int)g.sel[blockIdx.x % np] : blockIdx.x % np;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kStripW / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;  // warps (units) per CTA
+  const int np = g.nsel ? g.nsel : pairs;
+  const long long unit = (long long)blockIdx.x * wpc + warp;
+  if (unit >= (long long)g.nbands * np * nori) return;  // (no block barriers below)
+  const int pr = g.nsel ? (int)g.sel[unit % np] : (int)(unit % np);
+  const int band = (int)((unit / np) % g.nbands);
+  if (nori > 1) kind = (int)(unit / np / g.nbands);
+  const uint16_t* gfi = nori > 1 ? g.fio[kind] : g.fi;
+  const uint32_t* gagg = g.agg + (nori > 1 ? (size_t)kind * g.agg_stride : 0);
+  double2* rowbuf = s_tile + (size_t)warp * kWarpRows * kStripW;
+  double2* carry = s_tile + (size_t)wpc * kWarpRows * kStripW + (size_t)warp * g.band_h;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
   const int nrows = y1 - y0;
-  // the pair's two global bins (~0: bin out of range, no pixel matches)
   const int nin = g.bins - pr * kDP;  // bins of this pair in range
   const uint32_t gb0 = nin > 0 ? (uint32_t)g.bin0 + (uint32_t)pr * kDP : 0xFFFFFFFFu;
   const uint32_t gb1 = nin > 1 ? gb0 + 1 : 0xFFFFFFFFu;
@@ -213,132 +218,111 @@ __global__ void __launch_bounds__(kStripW, SWG_STRIP_MINB)
                    ((size_t)pr * g.planes + kind) * g.plane_stride;
   const double2 zero = make_double2(0.0, 0.0);
   if (band == 0)
-    for (int x = tid; x <= g.w; x += kStripW) plane[x] = zero;
-  for (int r = tid; r < nrows; r += kStripW) {
+    for (int x = lane; x <= g.w; x += 32) plane[x] = zero;
+  for (int r = lane; r < nrows; r += 32) {
     plane[(size_t)(y0 + r + 1) * g.pitch] = zero;
     carry[r] = zero;
   }
+  __syncwarp();
   const double2* agg = reinterpret_cast<const double2*>(gagg) + ((size_t)band * pairs + pr) * g.wa;
-  const int sw = strip_swz(tid);
-  auto step = [&](uint32_t v, real& c0, real& c1) {
-    c0 = fma(dec, c0, v == gb0 ? 1.0 : 0.0);
-    c1 = fma(dec, c1, v == gb1 ? 1.0 : 0.0);
-  };
+  const bool tma = g.tmap_ok != 0;
+  const int plane_i = pr * g.planes + kind;
+  const uint4 nopix = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  int slot = 0;
   for (int x0 = 0; x0 < g.w; x0 += kStripW) {
-    const int x = x0 + tid;
-    const bool in = x < g.w;
-    real c0 = 0.0, c1 = 0.0;
-    if (in && band > 0) {
-      const double2 v = agg[x];
-      c0 = v.x;
-      c1 = v.y;
+    const int xl = x0 + 8 * lane;  // this lane's first column
+    const bool inp = (size_t)xl < g.fi_pitch;  // its 8 pixels lie inside the padded row
+    real c0[8], c1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      c0[i] = c1[i] = 0.0;
+      if (band > 0 && xl + i < g.w) {
+        const double2 v = agg[xl + i];
+        c0[i] = v.x;
+        c1[i] = v.y;
+      }
     }
-    // pixel column x of the band (kNoBin beyond the image) and its table column
-    const uint16_t* col = gfi + (size_t)y0 * g.fi_pitch + (in ? x : 0);
-    const size_t fstep = in ? g.fi_pitch : 0;
-    const uint32_t vor = in ? 0u : 0x10000u;  // beyond the image: a value no bin matches
-    double2* out = plane + (size_t)(y0 + 1) * g.pitch + x + 1;
-    int prev = 0;  // rows of the previous block still in the tile (phase C pending)
-    for (int rb = 0;; rb += kStripRows) {
-      const int nr = min(kStripRows, nrows - rb);
-      if (tma) {  // phase C is the TMA stores: the tile is free once they have read it
-        if (nr <= 0) break;
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncthreads();
+    const uint16_t* prow = gfi + (size_t)y0 * g.fi_pitch + (inp ? xl : 0);
+    // pixels two rows ahead of the row being built
+    uint4 pa = inp && 0 < nrows ? __ldg(reinterpret_cast<const uint4*>(prow)) : nopix;
+    uint4 pb = inp && 1 < nrows ? __ldg(reinterpret_cast<const uint4*>(prow + g.fi_pitch)) : nopix;
+    for (int r = 0; r < nrows; ++r) {
+      const uint4 px = pa;
+      pa = pb;
+      pb = inp && r + 2 < nrows
+               ? __ldg(reinterpret_cast<const uint4*>(prow + (size_t)(r + 2) * g.fi_pitch))
+               : nopix;
+      const uint32_t w4[4] = {px.x, px.y, px.z, px.w};
+      real v0[8], v1[8];
+      real run0 = 0.0, run1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // (columns >= W hold kNoBin: no bin matches)
+        const uint32_t v = (w4[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+        c0[i] = fma(dec, c0[i], v == gb0 ? 1.0 : 0.0);
+        c1[i] = fma(dec, c1[i], v == gb1 ? 1.0 : 0.0);
+        run0 = fma(dec, run0, c0[i]);
+        run1 = fma(dec, run1, c1[i]);
+        v0[i] = run0;
+        v1[i] = run1;
       }
-      // C (previous block) + A (this block): the same thread, the same tile slots
-      if (in && !tma) {
-        if (prev == kStripRows) {
+      real i0 = run0, i1 = run1;  // inclusive scan of the lanes' totals
+      real sk = d8;               // (d^8)^(2^k)
 #pragma unroll
-          for (int r = 0; r < kStripRows; ++r) {
-            *out = s_tile[r * kStripW + sw];
-            out += g.pitch;
-          }
-        } else {
-          for (int r = 0; r < prev; ++r) {
-            *out = s_tile[r * kStripW + sw];
-            out += g.pitch;
-          }
+      for (int k = 0; k < 5; ++k) {
+        const real t0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1 << k);
+        const real t1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1 << k);
+        if (lane >= (1 << k)) {
+          i0 = fma(sk, t0, i0);
+          i1 = fma(sk, t1, i1);
         }
+        sk *= sk;
       }
-      if (nr <= 0) break;
-      {  // all of the block's loads in flight at once (a partial block predicates)
-        uint32_t fv[kStripRows];
-#pragma unroll
-        for (int r = 0; r < kStripRows; ++r) fv[r] = r < nr ? col[r * fstep] : 0u;
-        col += kStripRows * fstep;
-#pragma unroll
-        for (int r = 0; r < kStripRows; ++r)
-          if (r < nr) {
-            step(fv[r] | vor, c0, c1);
-            s_tile[r * kStripW + sw] = make_double2(c0, c1);
-          }
+      real e0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1), e1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1);
+      if (lane == 0) e0 = e1 = 0.0;
+      const double2 cin = carry[r];
+      const real q0 = fma(p8l, cin.x, e0), q1 = fma(p8l, cin.y, e1);
+      double2* buf = rowbuf + slot * kStripW;
+      if (tma) {  // the store that last read this row buffer is done with it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kWarpRows - 1) : "memory");
       }
-      __syncthreads();
-      // B: decayed row prefix, one warp per row
-      for (int r = warp; r < nr; r += kWarps) {
-        double2* trow = s_tile + r * kStripW;
-        real v0[8], v1[8];
-        real run0 = 0.0, run1 = 0.0;
+      __syncwarp();
+      real pw = dec;  // d^(i+1)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const double2 q = trow[8 * lane + (i ^ (lane & 7))];
-          run0 = fma(dec, run0, q.x);
-          run1 = fma(dec, run1, q.y);
-          v0[i] = run0;
-          v1[i] = run1;
-        }
-        real i0 = run0, i1 = run1;  // inclusive scan of the lanes' totals
-        real sk = d8;               // (d^8)^(2^k)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-          const real t0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1 << k);
-          const real t1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1 << k);
-          if (lane >= (1 << k)) {
-            i0 = fma(sk, t0, i0);
-            i1 = fma(sk, t1, i1);
-          }
-          sk *= sk;
-        }
-        real e0 = __shfl_up_sync(0xFFFFFFFFu, i0, 1), e1 = __shfl_up_sync(0xFFFFFFFFu, i1, 1);
-        if (lane == 0) e0 = e1 = 0.0;
-        const double2 cin = carry[rb + r];
-        const real q0 = fma(p8l, cin.x, e0), q1 = fma(p8l, cin.y, e1);
-        real pw = dec;  // d^(i+1)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v0[i] = fma(pw, q0, v0[i]);
-          v1[i] = fma(pw, q1, v1[i]);
-          trow[8 * lane + (i ^ (lane & 7))] = make_double2(v0[i], v1[i]);
-          pw *= dec;
-        }
-        const real n0 = __shfl_sync(0xFFFFFFFFu, v0[7], 31);
-        const real n1 = __shfl_sync(0xFFFFFFFFu, v1[7], 31);
-        if (lane == 0) carry[rb + r] = make_double2(n0, n1);  // E(x0 + kStripW - 1, y)
+      for (int i = 0; i < 8; ++i) {
+        v0[i] = fma(pw, q0, v0[i]);
+        v1[i] = fma(pw, q1, v1[i]);
+        buf[8 * lane + (i ^ (lane & 7))] = make_double2(v0[i], v1[i]);
+        pw *= dec;
       }
+      const real n0 = __shfl_sync(0xFFFFFFFFu, v0[7], 31);
+      const real n1 = __shfl_sync(0xFFFFFFFFu, v1[7], 31);
+      if (lane == 0) carry[r] = make_double2(n0, n1);  // E(x0 + kStripW - 1, y)
       if (tma) {
-        // C: one TMA tensor store per row (records x0+1 .. x0+256: 32 lines of
-        // 128 B; the tensor's bounds clip the strip at the image's edge)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-          const int plane_i = pr * g.planes + kind;
-          for (int r = 0; r < nr; ++r) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_tile + r * kStripW);
-            asm volatile(
-                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
-                ::"l"(&g.tmap), "r"(0), "r"(x0 / 8), "r"(y0 + rb + r + 1), "r"(plane_i), "r"(sa)
-                : "memory");
-          }
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+              ::"l"(&g.tmap), "r"(0), "r"(x0 / 8), "r"(y0 + r + 1), "r"(plane_i), "r"(sa)
+              : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       } else {
-        __syncthreads();
+        __syncwarp();
+        double2* out = plane + (size_t)(y0 + r + 1) * g.pitch + x0 + 1;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int c = m * 32 + lane;
+          if (x0 + c < g.w) out[c] = buf[strip_swz(c)];
+        }
+        __syncwarp();
       }
-      prev = nr;
+      slot = slot + 1 == kWarpRows ? 0 : slot + 1;
     }
   }
-  if (tma && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Decay-table export: planes [b0, b1) of orientation `kind` -> (W+1)x(H+1) each.
@@ -393,14 +377,21 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     *launches += 2;
   }
   if (kind == -1) return cudaSuccess;  // carries only
-  const dim3 grid((unsigned)(a.nbands * (a.nsel ? a.nsel : pairs)), kind == -2 ? 4u : 1u);
-  const size_t smem = (size_t)(kStripRows * kStripW + a.band_h) * sizeof(double2);
-  if (smem > (200 << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~8500 rows
+  const int nori = kind == -2 ? 4 : 1;
+  const long long units = (long long)a.nbands * (a.nsel ? a.nsel : pairs) * nori;
+  // row buffers + one carry per band row for every warp of the CTA
+  auto smem_of = [&](int wpc) {
+    return ((size_t)wpc * kWarpRows * kStripW + (size_t)wpc * a.band_h) * sizeof(double2);
+  };
+  int wpc = kWarpsPerCta;
+  while (wpc > 1 && 2 * smem_of(wpc) > (200u << 10)) wpc >>= 1;  // two CTAs per SM
+  if (smem_of(wpc) > (200u << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~12000 rows
   // set on every launch: the attribute is per device (a process-wide cache
   // would skip it on a second device and race between host threads)
-  cudaFuncSetAttribute(k_build_decay_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_build_decay_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 << 10);
-  k_build_decay_strip<<<grid, kStripW, smem, s>>>(a, dec, kind, pairs);
+  k_build_decay_warp<<<(unsigned)((units + wpc - 1) / wpc), 32 * wpc, smem_of(wpc), s>>>(
+      a, dec, kind, pairs, nori);
   *launches += 1;
   return cudaGetLastError();
 }

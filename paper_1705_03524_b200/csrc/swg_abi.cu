@@ -375,6 +375,26 @@ size_t pixel_bytes(int format) {
   }
 }
 
+// Planes of 16-byte records (16-bit octets, fp64 bin pairs) start 16 bytes
+// into their allocation.  Record 0 of a row is the zero column and the
+// builds write records 1..W in long runs: with the plane at an allocation
+// boundary every run started 16 bytes into a 32-byte sector, and a pure
+// store kernel with that pattern tops out at 4.0 TB/s against 5.5 TB/s for
+// sector-aligned runs (profiles/store_bw.cu; the same for per-lane, TMA
+// tensor and bulk stores).  Pitch and plane stride are even record counts,
+// so the shift aligns every row of every plane.  (32-byte records are
+// sector-aligned as they are.)
+constexpr size_t kRec16Shift = 16;
+cudaError_t alloc_rec16(void** p, size_t bytes) {
+  void* raw = nullptr;
+  const cudaError_t e = cudaMalloc(&raw, bytes + kRec16Shift);
+  *p = e == cudaSuccess ? static_cast<char*>(raw) + kRec16Shift : nullptr;
+  return e;
+}
+void free_rec16(void* p) {
+  if (p) cudaFree(static_cast<char*>(p) - kRec16Shift);
+}
+
 void choose_bands(swg_tables* t) {
   // ~4 row-wide CTAs per SM and table kind
 #ifndef SWG_BAND_TARGET
@@ -531,7 +551,7 @@ swg_status ensure_t16a(swg_tables* t) {
   if (t->planes < 3 || t->tdec || !t->has_fi)
     return fail(SWG_ERR, "tables: no narrow ramp planes");
   const size_t bytes = t->ps * 3 * t->groups * kOct * 2;
-  cudaError_t e = cudaMalloc(&t->t16a, bytes);
+  cudaError_t e = alloc_rec16(reinterpret_cast<void**>(&t->t16a), bytes);
   if (e != cudaSuccess) {
     t->t16a = nullptr;
     cudaGetLastError();
@@ -971,7 +991,7 @@ static swg_status build_common(swg_ctx* c, const void* pixels, int is_device,
   void** tab = elem == 2   ? reinterpret_cast<void**>(&t->t16)
                : elem == 4 ? reinterpret_cast<void**>(&t->t32)
                            : reinterpret_cast<void**>(&t->tdec);
-  if ((e = cudaMalloc(tab, tab_bytes)) != cudaSuccess ||
+  if ((e = elem == 4 ? cudaMalloc(tab, tab_bytes) : alloc_rec16(tab, tab_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&t->fi, fb)) != cudaSuccess ||
       (e = cudaMalloc(&t->lb, lb_bytes)) != cudaSuccess ||
       (planes == SWG_PLANES_DECAY && (e = cudaMalloc(&t->fflip, 3 * fb)) != cudaSuccess)) {
@@ -1145,11 +1165,11 @@ swg_status swg_tables_destroy(swg_tables* t) {
   if (t->ctx) {
     DeviceGuard g(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
-    cudaFree(t->t16);
+    free_rec16(t->t16);
     cudaFree(t->t32);
-    cudaFree(t->t16a);
+    free_rec16(t->t16a);
     cudaFree(t->t64);
-    cudaFree(t->tdec);
+    free_rec16(t->tdec);
     cudaFree(t->fflip);
     cudaFree(t->fi);
     cudaFree(t->in);

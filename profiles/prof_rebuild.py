@@ -2,7 +2,7 @@
 builds): builds the three table sets in full once, then runs
 swg_tables_rebuild_for with the step's requests -- quadratic set first,
 then the decayed set, then the 16-bit plain set -- `reps` times.
-    ncu -k regex:"k_build_fused<unsigned int, 8>|k_build_decay_strip" --launch-skip 4 -c 2 \\
+    ncu -k regex:"k_build_fused<unsigned int, 8>|k_build_decay_warp" --launch-skip 4 -c 2 \\
         python profiles/prof_rebuild.py
 (skips the initial decayed build's four strip launches: the capture is the
 selective quadratic build and the first selective decayed orientation)."""
