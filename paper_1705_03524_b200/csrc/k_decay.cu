@@ -384,7 +384,8 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     return ((size_t)wpc * kWarpRows * kStripW + (size_t)wpc * a.band_h) * sizeof(double2);
   };
   int wpc = kWarpsPerCta;
-  while (wpc > 1 && 2 * smem_of(wpc) > (200u << 10)) wpc >>= 1;  // two CTAs per SM
+  // two CTAs per SM: 228 KB of shared memory, 1 KB reserved per CTA
+  while (wpc > 1 && 2 * (smem_of(wpc) + 1024) > (228u << 10)) wpc >>= 1;
   if (smem_of(wpc) > (200u << 10)) return cudaErrorInvalidConfiguration;  // band_h > ~12000 rows
   // set on every launch: the attribute is per device (a process-wide cache
   // would skip it on a second device and race between host threads)
