@@ -63,10 +63,13 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 constexpr int kColPairs = SWG_COL_PAIRS;
 __global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs,
                                                       int nori) {
-  // nori = 4: the four orientations in one launch (blockIdx.z = column block
-  // * 4 + orientation, each with its image and carry array)
+  // nori = 2: the unflipped and the v-flipped image in one launch (blockIdx.z
+  // = column block * 2 + which), into carry slots 0 and 2.  The h-flipped
+  // orientations need no pass of their own: column x of an h-flipped image
+  // is column W-1-x of the unflipped one, over the same rows, so their
+  // carries are slot 0's / slot 2's read mirrored (k_build_decay_warp).
   const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
-  const int ori = nori > 1 ? (int)(blockIdx.z % nori) : 0;
+  const int ori = nori > 1 ? 2 * (int)(blockIdx.z % nori) : 0;
   const int x = (int)(blockIdx.z / nori) * blockDim.x + threadIdx.x;
   if (x >= g.w) return;
   const uint16_t* gfi = nori > 1 ? g.fio[ori] : g.fi;
@@ -197,7 +200,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   const int band = (int)((unit / np) % g.nbands);
   if (nori > 1) kind = (int)(unit / np / g.nbands);
   const uint16_t* gfi = nori > 1 ? g.fio[kind] : g.fi;
-  const uint32_t* gagg = g.agg + (nori > 1 ? (size_t)kind * g.agg_stride : 0);
+  // carries: slot 0 (unflipped) or 2 (v-flipped); an h-flipped orientation
+  // reads its partner's columns mirrored
+  const uint32_t* gagg = g.agg + (nori > 1 ? (size_t)(kind & 2) * g.agg_stride : 0);
+  const bool mirror = (kind & 1) != 0;
   double2* rowbuf = s_tile + (size_t)warp * kWarpRows * kStripW;
   double2* carry = s_tile + (size_t)wpc * kWarpRows * kStripW + (size_t)warp * g.band_h;
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
     for (int i = 0; i < 8; ++i) {
       c0[i] = c1[i] = 0.0;
       if (band > 0 && xl + i < g.w) {
-        const double2 v = agg[xl + i];
+        const double2 v = agg[mirror ? g.w - 1 - (xl + i) : xl + i];
         c0[i] = v.x;
         c1[i] = v.y;
       }
@@ -348,9 +354,11 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
                                int* launches) {
   *launches = 0;
   const int pairs = a.groups * (kOct / kDP);
-  if (a.nbands > 1 && kind != -2) {
-    // kind == -1: the carries of all four orientations (a.fio, agg_stride)
-    const int nori = kind == -1 ? 4 : 1;
+  if (a.nbands > 1 && kind != -2 && !(kind & 1 && kind > 0)) {
+    // kind == -1: the carries of the unflipped and the v-flipped image
+    // (a.fio[0], a.fio[2] -> slots 0 and 2 of a.agg); kind 0 / 2: of a.fi.
+    // Kinds 1 and 3 (h-flipped) read the carries kind 0 / 2 left in a.agg.
+    const int nori = kind == -1 ? 2 : 1;
     dim3 grid((unsigned)a.nbands, (unsigned)((pairs + kColPairs - 1) / kColPairs),
               (unsigned)((a.w + 255) / 256 * nori));
     k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs, nori);
@@ -364,7 +372,7 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     m.words_per_unit = a.wa * kDP;
     std::memcpy(m.w, a.selmask, sizeof(m.w));
     const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
-    const size_t ori_stride = a.agg_stride / 2;  // doubles
+    const size_t ori_stride = 2 * (a.agg_stride / 2);  // doubles between slots 0 and 2
     if (bw ? std::atoi(bw) != 0 : per_band * nori < 148u * 256u)  // few words: a warp each
       k_bandscan_decay<<<(unsigned)((per_band * nori * 32 + 255) / 256), 256, 0, s>>>(
           reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band, m,

@@ -501,8 +501,11 @@ cudaError_t launch_sweep_quad_multi(const QuadMulti& m, cudaStream_t s);
 cudaError_t launch_peak_reduce_multi(const PeakMulti& m, int maps, cudaStream_t s);
 cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s);
-// kind >= 0: carries + strips of one orientation; kind = -1: carries only
-// (a.fi, a.agg); kind = -2: strips of all four orientations (a.fio, agg_stride)
+// kind 0 / 2: carries (into a.agg) + strips of the unflipped / v-flipped
+// orientation; kind 1 / 3: strips of its h-flipped partner (the carries
+// kind - 1 left in a.agg, read mirrored); kind = -1: the carries of
+// orientations 0 and 2 only (a.fio, slots 0 and 2 of a.agg); kind = -2:
+// strips of all four orientations (a.fio, agg_stride)
 cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStream_t s,
                                int* launches);
 cudaError_t launch_export_decay(const double* tab, size_t ps, size_t pitch, int w, int h,
