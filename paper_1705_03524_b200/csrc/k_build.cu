@@ -23,6 +23,7 @@
 // them; T = uint64_t reproduces the reference's int64 tables.
 #include "swg_internal.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -127,59 +128,65 @@ __device__ __forceinline__ void block_exscan(const V (&val)[N], V (&excl)[N], V*
   }
 }
 
-// K1a: column count, y-sum (and y^2-sum for quadratic planes) of each bin of
-// G octets over one row band (each pixel read once per G octets).
-// agg[band][group][column][aw]: words 0-7 counts, 8-15 y-sums (aw >= 16: ramp
-// planes), 16-23 y^2-sums (aw = 24).
-template <int G, int AW>
-__global__ void __launch_bounds__(256) k_colsum(const BuildArgs g) {
-  const int band = blockIdx.x, grp0 = blockIdx.y * G;
-  const int x = blockIdx.z * blockDim.x + threadIdx.x;
+// K1a: column count, y-sum (and y^2-sum for quadratic planes) of each bin
+// over one row band.  agg[band][group][column][aw]: words 0-7 counts, 8-15
+// y-sums (aw >= 16: ramp planes), 16-23 y^2-sums (aw = 24).
+// A thread owns one column and keeps its per-bin sums in SHARED memory
+// (sums[plane][slot bin][thread]: conflict-free, private to the thread), so a
+// pixel costs one read-modify-write per plane whatever the bin count -- the
+// first form compared every pixel against each of an octet group's bins in
+// registers (64-128 instructions per pixel, the pixels re-read per group:
+// config 5 52 + 50 us for the quadratic and plain sets).  The bins summed
+// are the octets the build will read (a selective build's, else all), in
+// chunks of as many octets as the shared memory holds (blockIdx.z).
+constexpr int kColThreads = 128;
+constexpr int kColSmem = 96 << 10;
+template <int AW>
+__global__ void __launch_bounds__(kColThreads) k_colsum(const BuildArgs g, int opc) {
+  extern __shared__ uint32_t s_sum[];  // [AW / 8][slots * 8][kColThreads]
+  __shared__ unsigned char s_slot[kMaxBins / kOct];  // octet -> slot of this chunk (0xFF: none)
+  constexpr int NP = AW / 8;
+  const int tid = threadIdx.x, band = blockIdx.x;
+  const int x = blockIdx.y * kColThreads + tid;
+  const int noct = g.nsel ? g.nsel : g.groups;
+  const int o0 = blockIdx.z * opc, slots = min(opc, noct - o0);
+  for (int i = tid; i < g.groups; i += kColThreads) s_slot[i] = 0xFF;
+  __syncthreads();
+  if (tid < slots) s_slot[g.nsel ? (int)g.sel[o0 + tid] : o0 + tid] = (unsigned char)tid;
+  const int nb = slots * kOct;  // bins of this chunk
+  for (int i = tid; i < NP * nb * kColThreads; i += kColThreads) s_sum[i] = 0;
+  __syncthreads();
   if (x >= g.w) return;
-  if (g.nsel) {  // selective build: octets no sweep reads need no carries
-    bool any = false;
-    for (int k = 0; k < G && !any; ++k) any = grp0 + k < g.groups && sel_has(g.selmask, g.nsel, grp0 + k);
-    if (!any) return;
-  }
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)grp0 * kOct;
-  const uint32_t lim = (uint32_t)(g.bins - grp0 * kOct);  // bins of these octets in range
-  uint32_t cnt[G * kOct], ys[AW >= 16 ? G * kOct : 1], y2[AW == 24 ? G * kOct : 1];
-#pragma unroll
-  for (int j = 0; j < G * kOct; ++j) {
-    cnt[j] = 0;
-    if constexpr (AW >= 16) ys[j] = 0;
-    if constexpr (AW == 24) y2[j] = 0;
-  }
   const uint16_t* col = g.fi + x;
-  for (int y = y0; y < y1; ++y) {
-    uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
-    d = d < lim ? d : 0xFFFFFFFFu;
+  uint32_t* mine = s_sum + tid;
+  constexpr int kB = 8;  // rows whose pixels are in flight at once
+  for (int yb = y0; yb < y1; yb += kB) {
+    uint32_t v[kB];
 #pragma unroll
-    for (int j = 0; j < G * kOct; ++j) {
-      const bool hit = d == (uint32_t)j;
-      cnt[j] += hit ? 1u : 0u;
-      if constexpr (AW >= 16) ys[j] += hit ? (uint32_t)y : 0u;
-      if constexpr (AW == 24) y2[j] += hit ? (uint32_t)y * (uint32_t)y : 0u;
+    for (int k = 0; k < kB; ++k) v[k] = yb + k < y1 ? (uint32_t)col[(size_t)(yb + k) * g.fi_pitch] : 0xFFFFu;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t d = v[k] - (uint32_t)g.bin0;
+      if (d >= (uint32_t)g.bins) continue;  // another range's bin, or padding
+      const uint32_t sl = s_slot[d >> 3];
+      if (sl == 0xFFu) continue;
+      uint32_t* p = mine + (sl * kOct + (d & 7u)) * kColThreads;
+      const uint32_t y = (uint32_t)(yb + k);
+      p[0] += 1u;
+      if constexpr (AW >= 16) p[nb * kColThreads] += y;
+      if constexpr (AW == 24) p[2 * nb * kColThreads] += y * y;
     }
   }
+  for (int sl = 0; sl < slots; ++sl) {
+    const int grp = g.nsel ? (int)g.sel[o0 + sl] : o0 + sl;
+    uint4* dst = reinterpret_cast<uint4*>(g.agg + (((size_t)band * g.groups + grp) * g.wa + x) * AW);
 #pragma unroll
-  for (int q = 0; q < G; ++q) {
-    if (grp0 + q >= g.groups) break;
-    uint4* dst = reinterpret_cast<uint4*>(
-        g.agg + (((size_t)band * g.groups + grp0 + q) * g.wa + x) * AW);
-    const uint32_t* c = cnt + q * kOct;
-    dst[0] = make_uint4(c[0], c[1], c[2], c[3]);
-    dst[1] = make_uint4(c[4], c[5], c[6], c[7]);
-    if constexpr (AW >= 16) {
-      const uint32_t* t = ys + q * kOct;
-      dst[2] = make_uint4(t[0], t[1], t[2], t[3]);
-      dst[3] = make_uint4(t[4], t[5], t[6], t[7]);
-    }
-    if constexpr (AW == 24) {
-      const uint32_t* t = y2 + q * kOct;
-      dst[4] = make_uint4(t[0], t[1], t[2], t[3]);
-      dst[5] = make_uint4(t[4], t[5], t[6], t[7]);
+    for (int pl = 0; pl < NP; ++pl) {
+      const uint32_t* c = mine + ((size_t)pl * nb + sl * kOct) * kColThreads;
+      dst[2 * pl] = make_uint4(c[0], c[kColThreads], c[2 * kColThreads], c[3 * kColThreads]);
+      dst[2 * pl + 1] = make_uint4(c[4 * kColThreads], c[5 * kColThreads], c[6 * kColThreads],
+                                   c[7 * kColThreads]);
     }
   }
 }
@@ -642,21 +649,29 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Opt a build kernel into the dynamic shared memory its row staging needs.
+// (static + dynamic shared memory above 48 KB needs the opt-in; the fused
+// kernel's static arrays add up over its table kinds)
+template <typename K>
+static void allow_smem(K* kernel, size_t bytes) {
+  if (bytes) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
-  // several octets per thread (up to 32 column sums in registers) while the
-  // grid keeps >= 2 CTAs per SM; small tables keep one octet per thread
-  // (config 1: 2 octets per thread +6 % per step, config 2: 4 octets -3 % build)
-  const unsigned cols = (unsigned)((a.w + 255) / 256);
-  auto ctas = [&](int gpt) { return (unsigned)a.nbands * ((a.groups + gpt - 1) / gpt) * cols; };
-  auto go = [&](auto kernel, int gpt) {
-    dim3 grid((unsigned)a.nbands, (unsigned)((a.groups + gpt - 1) / gpt), cols);
-    kernel<<<grid, 256, 0, s>>>(a);
+  // octets per chunk: as many as kColSmem holds (aw / 8 planes of 8 bins x
+  // kColThreads words each)
+  const int noct = a.nsel ? a.nsel : a.groups;
+  const int opc = std::min(noct, kColSmem / (a.aw / 8 * kOct * kColThreads * 4));
+  const size_t smem = (size_t)opc * (a.aw / 8) * kOct * kColThreads * 4;
+  dim3 grid((unsigned)a.nbands, (unsigned)((a.w + kColThreads - 1) / kColThreads),
+            (unsigned)((noct + opc - 1) / opc));
+  auto go = [&](auto kernel) {
+    allow_smem(kernel, smem);
+    kernel<<<grid, kColThreads, smem, s>>>(a, opc);
   };
-  if (a.aw == 8 && ctas(4) >= 296) go(k_colsum<4, 8>, 4);
-  else if (a.aw == 8) go(k_colsum<1, 8>, 1);
-  else if (a.aw == 16 && ctas(2) >= 296) go(k_colsum<2, 16>, 2);
-  else if (a.aw == 16) go(k_colsum<1, 16>, 1);
-  else go(k_colsum<1, 24>, 1);
+  if (a.aw == 8) go(k_colsum<8>);
+  else if (a.aw == 16) go(k_colsum<16>);
+  else go(k_colsum<24>);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t per_band = (size_t)a.groups * a.wa * a.aw / 4;
@@ -672,14 +687,6 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
     k_bandscan_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
         reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m);
   return cudaGetLastError();
-}
-
-// Opt a build kernel into the dynamic shared memory its row staging needs.
-// (static + dynamic shared memory above 48 KB needs the opt-in; the fused
-// kernel's static arrays add up over its table kinds)
-template <typename K>
-static void allow_smem(K* kernel, size_t bytes) {
-  if (bytes) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <typename T>
