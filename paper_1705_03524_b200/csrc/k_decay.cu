@@ -28,6 +28,7 @@
 
 #include <math.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -55,48 +56,83 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
 }
 
 // K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
-// agg: [nbands][pairs][wa] double2.  A thread covers kColPairs bin pairs of
-// one column, so each pixel is read once per 2 * kColPairs bins.
-#ifndef SWG_COL_PAIRS
-#define SWG_COL_PAIRS 8  // 16 bins per thread (4 pairs: config 4 builds +0.4 ms)
-#endif
-constexpr int kColPairs = SWG_COL_PAIRS;
-__global__ void __launch_bounds__(256) k_colsum_decay(const BuildArgs g, real dec, int pairs,
-                                                      int nori) {
-  // nori = 2: the unflipped and the v-flipped image in one launch (blockIdx.z
+// agg: [nbands][pairs][wa] double2.
+// A thread owns one column and keeps each bin's running sum in SHARED memory
+// with the row it was last updated at (sums[slot bin][thread], private to
+// the thread): a pixel of bin b at row r costs one update
+//   c_b <- c_b d^(r - last_b) + 1,  last_b <- r
+// with the powers from a shared table, whatever the bin count, and the sums
+// are decayed to the band's last row at the end.  (The first form ran the
+// recurrence c <- d c + [bin] for every bin of 8 pairs at every pixel in
+// registers: 16 fp64 operations per pixel and pair group, the pixels re-read
+// per group; config 5 136 us for the model's pairs of four orientations.)
+// The bins summed are the pairs the build will read (a selective build's,
+// else all), in chunks of as many pairs as the shared memory holds.
+constexpr int kDColThreads = 128;
+constexpr int kDColSmem = 96 << 10;
+__global__ void __launch_bounds__(kDColThreads) k_colsum_decay(const BuildArgs g, real dec,
+                                                               int pairs, int nori, int ppc) {
+  // nori = 2: the unflipped and the v-flipped image in one launch (blockIdx.y
   // = column block * 2 + which), into carry slots 0 and 2.  The h-flipped
   // orientations need no pass of their own: column x of an h-flipped image
   // is column W-1-x of the unflipped one, over the same rows, so their
   // carries are slot 0's / slot 2's read mirrored (k_build_decay_warp).
-  const int band = blockIdx.x, pr0 = blockIdx.y * kColPairs;
-  const int ori = nori > 1 ? 2 * (int)(blockIdx.z % nori) : 0;
-  const int x = (int)(blockIdx.z / nori) * blockDim.x + threadIdx.x;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  __shared__ unsigned char s_slot[kMaxBins / kDP];  // pair -> slot of this chunk (0xFF: none)
+  const int tid = threadIdx.x, band = blockIdx.x;
+  const int ori = nori > 1 ? 2 * (int)(blockIdx.y % nori) : 0;
+  const int x = (int)(blockIdx.y / nori) * kDColThreads + tid;
+  const int np = g.nsel ? g.nsel : pairs;
+  const int p0 = blockIdx.z * ppc, slots = min(ppc, np - p0);
+  const int nb = slots * kDP;
+  real* cs = reinterpret_cast<real*>(s_raw);              // [nb][threads]
+  real* dpow = cs + (size_t)ppc * kDP * kDColThreads;     // d^k, k = 0 .. band_h
+  uint16_t* last = reinterpret_cast<uint16_t*>(dpow + g.band_h + 1);  // [nb][threads]
+  for (int i = tid; i < pairs; i += kDColThreads) s_slot[i] = 0xFF;
+  __syncthreads();
+  if (tid < slots) s_slot[g.nsel ? (int)g.sel[p0 + tid] : p0 + tid] = (unsigned char)tid;
+  for (int i = tid; i < nb * kDColThreads; i += kDColThreads) {
+    cs[i] = 0.0;
+    last[i] = 0;
+  }
+  for (int k = tid; k <= g.band_h; k += kDColThreads) {
+    real r = 1.0, p = dec;
+    for (int e = k; e; e >>= 1) {
+      if (e & 1) r *= p;
+      p *= p;
+    }
+    dpow[k] = r;
+  }
+  __syncthreads();
   if (x >= g.w) return;
   const uint16_t* gfi = nori > 1 ? g.fio[ori] : g.fi;
   double2* dst = reinterpret_cast<double2*>(g.agg + (nori > 1 ? (size_t)ori * g.agg_stride : 0));
-  if (g.nsel) {  // selective build: pairs no sweep reads need no carries
-    bool any = false;
-    for (int k = 0; k < kColPairs && !any; ++k) any = pr0 + k < pairs && sel_has(g.selmask, g.nsel, pr0 + k);
-    if (!any) return;
-  }
   const int y0 = band * g.band_h, y1 = min(y0 + g.band_h, g.h);
-  const uint32_t gb = (uint32_t)g.bin0 + (uint32_t)pr0 * kDP;
-  const uint32_t lim = (uint32_t)max(g.bins - pr0 * kDP, 0);  // bins of these pairs in range
-  real c[2 * kColPairs];
+  const int nrows = y1 - y0;
+  const uint16_t* col = gfi + (size_t)y0 * g.fi_pitch + x;
+  constexpr int kB = 8;  // rows whose pixels are in flight at once
+  for (int rb = 0; rb < nrows; rb += kB) {
+    uint32_t v[kB];
 #pragma unroll
-  for (int j = 0; j < 2 * kColPairs; ++j) c[j] = 0.0;
-  const uint16_t* col = gfi + x;
-  for (int y = y0; y < y1; ++y) {
-    uint32_t d = (uint32_t)col[(size_t)y * g.fi_pitch] - gb;
-    d = d < lim ? d : 0xFFFFFFFFu;
+    for (int k = 0; k < kB; ++k) v[k] = rb + k < nrows ? (uint32_t)col[(size_t)(rb + k) * g.fi_pitch] : 0xFFFFu;
 #pragma unroll
-    for (int j = 0; j < 2 * kColPairs; ++j) c[j] = fma(dec, c[j], d == (uint32_t)j ? 1.0 : 0.0);
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t d = v[k] - (uint32_t)g.bin0;
+      if (d >= (uint32_t)g.bins) continue;  // another range's bin, or padding
+      const uint32_t sl = s_slot[d >> 1];
+      if (sl == 0xFFu) continue;
+      const int i = (int)(sl * kDP + (d & 1u)) * kDColThreads + tid;
+      const int r = rb + k;
+      cs[i] = fma(cs[i], dpow[r - (int)last[i]], 1.0);
+      last[i] = (uint16_t)r;
+    }
   }
-  
-#pragma unroll
-  for (int q = 0; q < kColPairs; ++q)
-    if (pr0 + q < pairs)
-      dst[((size_t)band * pairs + pr0 + q) * g.wa + x] = make_double2(c[2 * q], c[2 * q + 1]);
+  for (int sl = 0; sl < slots; ++sl) {
+    const int pr = g.nsel ? (int)g.sel[p0 + sl] : p0 + sl;
+    const int i0 = sl * kDP * kDColThreads + tid, i1 = i0 + kDColThreads;
+    dst[((size_t)band * pairs + pr) * g.wa + x] =
+        make_double2(cs[i0] * dpow[nrows - 1 - (int)last[i0]], cs[i1] * dpow[nrows - 1 - (int)last[i1]]);
+  }
 }
 
 // K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place);
@@ -359,9 +395,18 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     // (a.fio[0], a.fio[2] -> slots 0 and 2 of a.agg); kind 0 / 2: of a.fi.
     // Kinds 1 and 3 (h-flipped) read the carries kind 0 / 2 left in a.agg.
     const int nori = kind == -1 ? 2 : 1;
-    dim3 grid((unsigned)a.nbands, (unsigned)((pairs + kColPairs - 1) / kColPairs),
-              (unsigned)((a.w + 255) / 256 * nori));
-    k_colsum_decay<<<grid, 256, 0, s>>>(a, dec, pairs, nori);
+    // pairs per chunk: as many as kDColSmem holds beside the power table
+    // (10 bytes per bin and thread: the sum and its last row)
+    const int np = a.nsel ? a.nsel : pairs;
+    const size_t per_pair = (size_t)kDP * kDColThreads * (sizeof(double) + sizeof(uint16_t));
+    const size_t tab = (size_t)(a.band_h + 1) * sizeof(double);
+    if (a.band_h > 65535 || tab + per_pair > (size_t)kDColSmem) return cudaErrorInvalidConfiguration;
+    const int ppc = (int)std::min<size_t>((size_t)np, (kDColSmem - tab) / per_pair);
+    const size_t csm = (size_t)ppc * per_pair + tab;
+    dim3 grid((unsigned)a.nbands, (unsigned)((a.w + kDColThreads - 1) / kDColThreads * nori),
+              (unsigned)((np + ppc - 1) / ppc));
+    cudaFuncSetAttribute(k_colsum_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, kDColSmem);
+    k_colsum_decay<<<grid, kDColThreads, csm, s>>>(a, dec, pairs, nori, ppc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t per_band = (size_t)pairs * a.wa * kDP;
