@@ -258,7 +258,9 @@ swg_status swg_tables_feature_image(swg_tables* t, uint16_t* host_out);
  * Bins are tiled in records of 8 ("bin octets"): element (x, y) of bin b,
  * table kind k sits at
  *   base[(((b/8)*planes + k)*plane_stride + y*pitch + x)*8 + b%8]
- * with plane_stride and pitch counted in records.  Units a model-driven
+ * with plane_stride and pitch counted in records (planes of 16-byte
+ * records -- the fp64 pairs here -- start 16 bytes past an allocation
+ * boundary, so record 1 of every row is 32-byte aligned).  Units a model-driven
  * rebuild (swg_tables_rebuild_for) skipped are built before this returns. */
 swg_status swg_tables_device_layout(const swg_tables* t, const void** base,
                                     size_t* plane_stride, size_t* pitch,
