@@ -135,3 +135,36 @@ def test_decayed_selective_equals_full(ctx):
     for b in (5, 6, 33, 60, 0, 47):  # built pairs, then stale ones
         for k in range(4):
             assert (ts.export_f64(k, b, b + 1) == tf.export_f64(k, b, b + 1)).all(), (b, k)
+
+
+def test_random_shapes_against_numpy(ctx):
+    """Seeded random table shapes (ragged widths and heights from 1 pixel up,
+    1 to 130 bins, every plane set, 8- and 16-bit pixels): a few bins of every
+    kind against numpy."""
+    rng = np.random.default_rng(2024)
+    shapes = [(1, 1, 1), (2, 700, 3), (513, 9, 17), (257, 257, 64)]
+    shapes += [(int(rng.integers(1, 700)), int(rng.integers(1, 900)), int(rng.integers(1, 131)))
+               for _ in range(8)]
+    for n, (w, h, bins) in enumerate(shapes):
+        planes = (swg.PLANES_PLAIN, swg.PLANES_AFFINE, swg.PLANES_QUADRATIC)[n % 3]
+        if n % 2:
+            img, fmt = _u16_image(w, h, 100 + n), swg.FMT_GRAY16
+        else:
+            img = rng.integers(0, 256, size=(h, w), dtype=np.uint8)
+            fmt = swg.FMT_GRAY8
+        t = ctx.build(img, fmt, bins, planes)
+        fi = t.feature_image()
+        for b in sorted({0, bins - 1, int(rng.integers(0, bins))}):
+            for kind in range((1, 3, 5)[n % 3]):
+                _check_plane(t, fi, b, kind)
+        if n % 4 == 0:  # and the decayed planes of the same image
+            d = float(rng.choice([0.5, 0.9, 0.9375]))
+            td = ctx.build_decay(img, d, fmt, bins)
+            fd = td.feature_image()
+            flips = (fd, fd[:, ::-1], fd[::-1, :], fd[::-1, ::-1])
+            for b in sorted({0, bins - 1}):
+                for k, f in enumerate(flips):
+                    np.testing.assert_allclose(td.export_f64(k, b, b + 1)[0],
+                                               _decayed_plane(np.ascontiguousarray(f), b, d),
+                                               rtol=1e-12, atol=1e-13,
+                                               err_msg=f"{w}x{h} bins {bins} bin {b} orientation {k}")
