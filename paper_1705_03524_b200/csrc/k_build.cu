@@ -309,6 +309,19 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
       for (int j = 0; j < kOct; ++j) t[i][j] += ex[j];
   }
 
+  // 16-bit plain planes: the running table values stay PACKED, two bins per
+  // 32-bit word -- the record's own layout -- and a row adds its packed row
+  // prefix with one 16x2 SIMD add per word (VIADD.16x2: each half wraps mod
+  // 2^16 on its own), instead of eight extractions and adds per column
+  constexpr bool PK = sizeof(T) == 2 && KIND == 0;
+  [[maybe_unused]] uint32_t tp[PK ? CPT : 1][4];
+  if constexpr (PK) {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        tp[i][q] = (uint32_t)t[i][2 * q] | (uint32_t)t[i][2 * q + 1] << 16;
+  }
   T* plane = reinterpret_cast<T*>(g.out) +
              ((size_t)grp * g.planes + KIND) * g.plane_stride * kOct;
   if (band == 0) {  // zero row 0
@@ -393,10 +406,15 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           ex[q] += ((d[i] >> 1) == (uint32_t)q) ? (1u << ((d[i] & 1u) << 4)) : 0u;
+        if constexpr (PK) {
 #pragma unroll
-        for (int j = 0; j < kOct; ++j) {
-          const uint32_t r = (ex[j >> 1] >> ((j & 1) << 4)) & 0xFFFFu;
-          t[i][j] += KIND == 2 ? (T)y * (T)r : KIND == 4 ? (T)y * (T)y * (T)r : (T)r;
+          for (int q = 0; q < 4; ++q) tp[i][q] = __vadd2(tp[i][q], ex[q]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kOct; ++j) {
+            const uint32_t r = (ex[j >> 1] >> ((j & 1) << 4)) & 0xFFFFu;
+            t[i][j] += KIND == 2 ? (T)y * (T)r : KIND == 4 ? (T)y * (T)y * (T)r : (T)r;
+          }
         }
       }
     }
@@ -421,7 +439,10 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
 #pragma unroll
       for (int i = 0; i < CPT; ++i)
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) st[swz((lane * CPT + i) * NQ + q)] = record_chunk<T>(t[i], q);
+        for (int q = 0; q < NQ; ++q) {
+          if constexpr (PK) st[swz(lane * CPT + i)] = make_uint4(tp[i][0], tp[i][1], tp[i][2], tp[i][3]);
+          else st[swz((lane * CPT + i) * NQ + q)] = record_chunk<T>(t[i], q);
+        }
       if (tma) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -477,7 +498,13 @@ __device__ __forceinline__ void build_body(const BuildArgs& g, int band, int grp
     } else {
       if (live)
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+        for (int i = 0; i < CPT; ++i) {
+          if constexpr (PK)
+            *reinterpret_cast<uint4*>(row + (size_t)(xb + 1 + i) * kOct) =
+                make_uint4(tp[i][0], tp[i][1], tp[i][2], tp[i][3]);
+          else
+            store_record<T>(row + (size_t)(xb + 1 + i) * kOct, t[i]);
+        }
     }
     if (tid == 0) store_zero_record<T>(row);
   }
