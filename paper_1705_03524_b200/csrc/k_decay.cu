@@ -55,6 +55,29 @@ __global__ void k_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t*
   }
 }
 
+// K0', 8 pixels per thread (widths that are multiples of 8: the mirrored
+// chunk of a row is then 16-byte aligned too).
+__device__ __forceinline__ uint4 rev8(const uint4 v) {  // 8 uint16 in reverse order
+  auto sw = [](uint32_t w) { return (w >> 16) | (w << 16); };
+  return make_uint4(sw(v.w), sw(v.z), sw(v.y), sw(v.x));
+}
+__global__ void __launch_bounds__(256) k_flip_v8(const uint16_t* fi, size_t pitch, int w, int h,
+                                                 uint16_t* fh, uint16_t* fv, uint16_t* fhv) {
+  const int y = blockIdx.y;
+  const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (x0 >= (int)pitch) return;
+  const uint4 pad = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  const bool in = x0 < w;  // (w % 8 == 0: a chunk is all image or all padding)
+  const uint16_t* r0 = fi + (size_t)y * pitch;
+  const uint16_t* r1 = fi + (size_t)(h - 1 - y) * pitch;
+  const uint4 a = in ? rev8(*reinterpret_cast<const uint4*>(r0 + (w - 8 - x0))) : pad;
+  const uint4 b = *reinterpret_cast<const uint4*>(r1 + x0);
+  const uint4 c = in ? rev8(*reinterpret_cast<const uint4*>(r1 + (w - 8 - x0))) : pad;
+  *reinterpret_cast<uint4*>(fh + (size_t)y * pitch + x0) = a;
+  *reinterpret_cast<uint4*>(fv + (size_t)y * pitch + x0) = b;
+  *reinterpret_cast<uint4*>(fhv + (size_t)y * pitch + x0) = c;
+}
+
 // K1a': decayed column sums of one band: c(x) = sum_y [bin] d^(y1-1-y).
 // agg: [nbands][pairs][wa] double2.
 // A thread owns one column and keeps each bin's running sum in SHARED memory
@@ -381,6 +404,11 @@ __global__ void k_export_decay(const double* tab, size_t ps, size_t pitch, int w
 
 cudaError_t launch_flip(const uint16_t* fi, size_t pitch, int w, int h, uint16_t* fh,
                         uint16_t* fv, uint16_t* fhv, cudaStream_t s) {
+  if (w % 8 == 0) {
+    dim3 g8((unsigned)((pitch / 8 + 255) / 256), (unsigned)h);
+    k_flip_v8<<<g8, 256, 0, s>>>(fi, pitch, w, h, fh, fv, fhv);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((pitch + 255) / 256), (unsigned)h);
   k_flip<<<grid, 256, 0, s>>>(fi, pitch, w, h, fh, fv, fhv);
   return cudaGetLastError();
