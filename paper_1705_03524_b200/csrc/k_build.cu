@@ -192,59 +192,54 @@ __global__ void __launch_bounds__(kColThreads) k_colsum(const BuildArgs g, int o
 }
 
 // K1b: exclusive scan over bands, in place: agg[band] <- sum of agg[k < band].
-// One warp per uint4 column of the carry array: the lanes hold 32 bands at a
-// time and a shuffle scan combines them (all loads of a batch in flight).
+// Q lanes (a power of two <= 32, consecutive lanes of a warp) share one uint4
+// word of the carry array: each loads its kBandPT bands at once (all loads in
+// flight), sums them, the lanes' sums are scanned with Q-wide shuffles, and
+// each lane writes its bands' exclusive values.  Q (bandscan_lanes) grows
+// while the grid would leave SMs short of threads and the bands are not yet
+// covered in one round: 1-2 lanes for config 5's large carry arrays, 8 for
+// config 2's small one (a whole warp per word idles most lanes and throttles
+// on shuffles: config 5 +16 %).
+constexpr int kBandPT = 10;
 __global__ void __launch_bounds__(256) k_bandscan(uint4* agg, int nbands, size_t per_band,
-                                                  const SelMask m) {
-  const size_t col = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (col >= per_band || m.skip(col)) return;
+                                                  const SelMask m, int q) {
+  const size_t gt = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t col = gt / q;
+  const int sub = (int)(gt % q);
+  const bool act = col < per_band && !m.skip(col);  // (every lane stays for the shuffles)
   uint4 run = make_uint4(0, 0, 0, 0);
-  for (int b0 = 0; b0 < nbands; b0 += 32) {
-    const int b = b0 + lane;
-    uint4 v = b < nbands ? agg[(size_t)b * per_band + col] : make_uint4(0, 0, 0, 0);
-    uint4 inc = v;
+  for (int b0 = 0; b0 < nbands; b0 += q * kBandPT) {
+    const int bs = b0 + sub * kBandPT;
+    uint4 v[kBandPT];
+    uint4 tot = make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc.x, off);
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc.y, off);
-      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, inc.z, off);
-      const uint32_t w = __shfl_up_sync(0xFFFFFFFFu, inc.w, off);
-      if (lane >= off) {
+    for (int k = 0; k < kBandPT; ++k)
+      v[k] = act && bs + k < nbands ? agg[(size_t)(bs + k) * per_band + col] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kBandPT; ++k) {
+      tot.x += v[k].x; tot.y += v[k].y; tot.z += v[k].z; tot.w += v[k].w;
+    }
+    uint4 inc = tot;
+    for (int off = 1; off < q; off <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc.x, off, q);
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc.y, off, q);
+      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, inc.z, off, q);
+      const uint32_t w = __shfl_up_sync(0xFFFFFFFFu, inc.w, off, q);
+      if (sub >= off) {
         inc.x += x; inc.y += y; inc.z += z; inc.w += w;
       }
     }
-    if (b < nbands)
-      agg[(size_t)b * per_band + col] = make_uint4(run.x + inc.x - v.x, run.y + inc.y - v.y,
-                                                   run.z + inc.z - v.z, run.w + inc.w - v.w);
-    run.x += __shfl_sync(0xFFFFFFFFu, inc.x, 31);
-    run.y += __shfl_sync(0xFFFFFFFFu, inc.y, 31);
-    run.z += __shfl_sync(0xFFFFFFFFu, inc.z, 31);
-    run.w += __shfl_sync(0xFFFFFFFFu, inc.w, 31);
-  }
-}
-
-// K1b, sequential form: one thread per uint4 column word walks the bands in
-// order (a running sum; the loads of 8 bands in flight at a time).  The
-// warp-per-word shuffle scan above keeps 32 lanes busy per word, but with a
-// few dozen bands most lanes idle and the shuffles throttle the MIO pipe
-// (config 5: 53 us for 58 MB).
-__global__ void __launch_bounds__(256) k_bandscan_seq(uint4* agg, int nbands, size_t per_band,
-                                                      const SelMask m) {
-  const size_t col = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (col >= per_band || m.skip(col)) return;
-  uint4 run = make_uint4(0, 0, 0, 0);
-  constexpr int kB = 8;
-  for (int b0 = 0; b0 < nbands; b0 += kB) {
-    uint4 v[kB];
+    uint4 pre = make_uint4(run.x + inc.x - tot.x, run.y + inc.y - tot.y, run.z + inc.z - tot.z,
+                           run.w + inc.w - tot.w);
 #pragma unroll
-    for (int k = 0; k < kB; ++k)
-      v[k] = b0 + k < nbands ? agg[(size_t)(b0 + k) * per_band + col] : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      if (b0 + k < nbands) agg[(size_t)(b0 + k) * per_band + col] = run;
-      run.x += v[k].x; run.y += v[k].y; run.z += v[k].z; run.w += v[k].w;
+    for (int k = 0; k < kBandPT; ++k) {
+      if (act && bs + k < nbands) agg[(size_t)(bs + k) * per_band + col] = pre;
+      pre.x += v[k].x; pre.y += v[k].y; pre.z += v[k].z; pre.w += v[k].w;
     }
+    run.x += __shfl_sync(0xFFFFFFFFu, inc.x, q - 1, q);
+    run.y += __shfl_sync(0xFFFFFFFFu, inc.y, q - 1, q);
+    run.z += __shfl_sync(0xFFFFFFFFu, inc.z, q - 1, q);
+    run.w += __shfl_sync(0xFFFFFFFFu, inc.w, q - 1, q);
   }
 }
 
@@ -773,13 +768,9 @@ cudaError_t launch_colsum(const BuildArgs& a, cudaStream_t s) {
   m.on = a.nsel > 0;
   m.words_per_unit = a.wa * a.aw / 4;
   std::memcpy(m.w, a.selmask, sizeof(m.w));
-  const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
-  if (bw ? std::atoi(bw) != 0 : per_band < 148u * 256u)  // few words: a warp each
-    k_bandscan<<<(unsigned)((per_band * 32 + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m);
-  else
-    k_bandscan_seq<<<(unsigned)((per_band + 255) / 256), 256, 0, s>>>(
-        reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m);
+  const int q = bandscan_lanes(a.nbands, per_band);
+  k_bandscan<<<(unsigned)((per_band * q + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<uint4*>(a.agg), a.nbands, per_band, m, q);
   return cudaGetLastError();
 }
 

@@ -158,66 +158,57 @@ __global__ void __launch_bounds__(kDColThreads) k_colsum_decay(const BuildArgs g
   }
 }
 
-// K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place);
-// one warp per column word, lanes = 32 bands, affine shuffle scan.
-__global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, int band_h,
-                                                        int h, real dband, real dlast,
-                                                        size_t per_band, const SelMask m,
-                                                        int nori, size_t ori_stride) {
-  const size_t cw = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (cw >= per_band * nori) return;
+// K1b': C_0 = 0, C_{b+1} = d^(h_b) C_b + c_b (exclusive over bands, in place).
+// Q lanes share one column word, as in k_bandscan: each loads its 10 bands at
+// once and folds them into an affine map (A, V): C -> A C + V; the lanes'
+// maps are composed by a Q-wide shuffle scan, and each lane replays its bands
+// from the value entering it.
+constexpr int kBandPT = 10;
+__global__ void __launch_bounds__(256) k_bandscan_decay(real* agg, int nbands, real dband,
+                                                        real dlast, size_t per_band,
+                                                        const SelMask m, int nori,
+                                                        size_t ori_stride, int q) {
+  const size_t gt = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t cw = gt / q;  // (orientation cw / per_band, word cw % per_band)
+  const int sub = (int)(gt % q);
   const size_t col = cw % per_band;
-  if (m.skip(col)) return;
-  agg += (cw / per_band) * ori_stride;
+  const bool act = cw < per_band * nori && !m.skip(col);  // (every lane stays for the shuffles)
+  if (act) agg += (cw / per_band) * ori_stride;
   real run = 0.0;
-  for (int b0 = 0; b0 < nbands; b0 += 32) {
-    const int b = b0 + lane;
-    // d^(rows of band b): every band but the last has band_h rows (host powers)
-    real ia = b < nbands ? (b == nbands - 1 ? dlast : dband) : 1.0;
-    real inc = b < nbands ? agg[(size_t)b * per_band + col] : 0.0;
+  for (int b0 = 0; b0 < nbands; b0 += q * kBandPT) {
+    const int bs = b0 + sub * kBandPT;
+    real v[kBandPT];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const real pa = __shfl_up_sync(0xFFFFFFFFu, ia, off);
-      const real pv = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-      if (lane >= off) {
-        inc = fma(ia, pv, inc);
+    for (int k = 0; k < kBandPT; ++k)
+      v[k] = act && bs + k < nbands ? agg[(size_t)(bs + k) * per_band + col] : 0.0;
+    // this lane's bands as one affine map (bands past the end: the identity)
+    real A = 1.0, V = 0.0;
+#pragma unroll
+    for (int k = 0; k < kBandPT; ++k) {
+      const real f = bs + k < nbands ? (bs + k == nbands - 1 ? dlast : dband) : 1.0;
+      V = fma(f, V, v[k]);
+      A *= f;
+    }
+    real ia = A, iv = V;  // inclusive composition over the lanes of the word
+    for (int off = 1; off < q; off <<= 1) {
+      const real pa = __shfl_up_sync(0xFFFFFFFFu, ia, off, q);
+      const real pv = __shfl_up_sync(0xFFFFFFFFu, iv, off, q);
+      if (sub >= off) {
+        iv = fma(ia, pv, iv);
         ia *= pa;
       }
     }
-    const real pa = __shfl_up_sync(0xFFFFFFFFu, ia, 1);
-    const real pv = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
-    const real ent = lane > 0 ? fma(pa, run, pv) : run;
-    if (b < nbands) agg[(size_t)b * per_band + col] = ent;
-    run = fma(__shfl_sync(0xFFFFFFFFu, ia, 31), run, __shfl_sync(0xFFFFFFFFu, inc, 31));
-  }
-}
-
-// K1b', sequential form: one thread per column word walks the bands in order
-// (loads of 8 bands in flight); see k_bandscan_seq.
-__global__ void __launch_bounds__(256) k_bandscan_decay_seq(real* agg, int nbands, real dband,
-                                                            real dlast, size_t per_band,
-                                                            const SelMask m, int nori,
-                                                            size_t ori_stride) {
-  const size_t cw = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (cw >= per_band * nori) return;
-  const size_t col = cw % per_band;  // (orientation cw / per_band)
-  if (m.skip(col)) return;
-  agg += (cw / per_band) * ori_stride;
-  real run = 0.0;
-  constexpr int kB = 8;
-  for (int b0 = 0; b0 < nbands; b0 += kB) {
-    real v[kB];
+    const real ea = __shfl_up_sync(0xFFFFFFFFu, ia, 1, q);
+    const real ev = __shfl_up_sync(0xFFFFFFFFu, iv, 1, q);
+    real cur = sub > 0 ? fma(ea, run, ev) : run;  // the value entering this lane's bands
 #pragma unroll
-    for (int k = 0; k < kB; ++k) v[k] = b0 + k < nbands ? agg[(size_t)(b0 + k) * per_band + col] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      const int b = b0 + k;
-      if (b < nbands) {
-        agg[(size_t)b * per_band + col] = run;
-        run = fma(b == nbands - 1 ? dlast : dband, run, v[k]);
+    for (int k = 0; k < kBandPT; ++k) {
+      if (act && bs + k < nbands) {
+        agg[(size_t)(bs + k) * per_band + col] = cur;
+        cur = fma(bs + k == nbands - 1 ? dlast : dband, cur, v[k]);
       }
     }
+    run = fma(__shfl_sync(0xFFFFFFFFu, ia, q - 1, q), run, __shfl_sync(0xFFFFFFFFu, iv, q - 1, q));
   }
 }
 
@@ -444,16 +435,10 @@ cudaError_t launch_build_decay(const BuildArgs& a, double dec, int kind, cudaStr
     m.on = a.nsel > 0;
     m.words_per_unit = a.wa * kDP;
     std::memcpy(m.w, a.selmask, sizeof(m.w));
-    const char* bw = std::getenv("SWG_BANDSCAN_WARP");  // A/B: 1 = warp-per-word scan
     const size_t ori_stride = 2 * (a.agg_stride / 2);  // doubles between slots 0 and 2
-    if (bw ? std::atoi(bw) != 0 : per_band * nori < 148u * 256u)  // few words: a warp each
-      k_bandscan_decay<<<(unsigned)((per_band * nori * 32 + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, a.band_h, a.h, dband, dlast, per_band, m,
-          nori, ori_stride);
-    else
-      k_bandscan_decay_seq<<<(unsigned)((per_band * nori + 255) / 256), 256, 0, s>>>(
-          reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band, m, nori,
-          ori_stride);
+    const int q = bandscan_lanes(a.nbands, per_band * nori);
+    k_bandscan_decay<<<(unsigned)((per_band * nori * q + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<double*>(a.agg), a.nbands, dband, dlast, per_band, m, nori, ori_stride, q);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 2;
   }

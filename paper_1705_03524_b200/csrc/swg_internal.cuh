@@ -477,6 +477,20 @@ __host__ __device__ inline bool sel_has(const uint32_t* m, int nsel, int u) {
   return nsel == 0 || ((m[u >> 5] >> (u & 31)) & 1u);
 }
 
+// Lanes per carry word of the band scans (K1b, K1b'): enough to put ~1024
+// threads on every SM, at most what covers the bands in one round of 10
+// bands per lane (measured on config 5: 1, 2 and 4 lanes within 1 %, 8 lanes
+// +4 %, a whole warp +16 %; SWG_BANDSCAN_Q forces a count: A/B).
+inline int bandscan_lanes(int nbands, size_t words) {
+  if (const char* e = std::getenv("SWG_BANDSCAN_Q")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) return v;
+  }
+  int q = 1;
+  while (q < 32 && q * 10 < nbands && words * q < 148u * 1024u) q <<= 1;
+  return q;
+}
+
 // Encode a row tensor map for TMA stores (swg_abi.cu): planes of records of
 // rec_bytes, base = record 1 of row 0 of plane 0, box = box_lines 128-byte
 // lines x 1 row.  Returns false when the driver entry point is unavailable.
