@@ -661,12 +661,13 @@ swg_status run_build_decay(swg_tables* t, const std::vector<int>* sel = nullptr)
     a.tmap_ok = 1;
   }
   const uint16_t* src[4] = {t->fi, t->fflip, t->fflip + fsz, t->fflip + 2 * fsz};
-  // a selective build has few (band, pair) strips per orientation: the four
-  // orientations' strips go in one launch (each with its own carry array)
-  // so the grid fills the SMs; a full build keeps one launch per orientation
-  // (measured: its orientations' rows compete for L2)
-  const char* ef = std::getenv("SWG_DECAY_FUSE");
-  const bool fuse = ef ? std::atoi(ef) != 0 : (a.nsel > 0 && t->nbands > 1);
+  // the four orientations' units go in ONE launch (the carries of the
+  // unflipped and the v-flipped image in one pass before it): a warp builds
+  // a unit, so one orientation alone leaves the SMs short of warps (config 4:
+  // 1184 units per orientation, 8 warps per SM; builds 33.7 -> 26.8 ms with
+  // the orientations together, config 5's full decayed build 2.09 -> 1.70 ms)
+  const char* ef = std::getenv("SWG_DECAY_FUSE");  // A/B: 0 = a launch per orientation
+  const bool fuse = ef ? std::atoi(ef) != 0 : t->nbands > 1;
   const size_t stride = t->lb_bytes / 4 / 4;  // uint32 words per orientation
   for (int k = 0; k < 4; ++k) a.fio[k] = src[k];
   if (fuse) {  // the four orientations' carries in one pass, then their strips
